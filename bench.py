@@ -1,0 +1,366 @@
+#!/usr/bin/env python3
+"""Benchmark of the batched HyGT hot path (BASELINE.json metric: HyGT fwd+inv vectors/s and % of
+HBM roofline).
+
+One step = one pass of the hot path over one batch: class bucketing + forward + inverse of every
+row of BASELINE config 2 (N=16, C=35 classes, R=3 rounds with inter-round permutations, 2^24
+AR(1) rows per GPU; weak scaling over GPUs). Inputs are resident in HBM when the timed region
+starts (`value`); `e2e` is the same step through the public host-buffer API with H2D/D2H copies
+inside the timed region. `--impl reference` times the reference's own CPU implementation
+(oracle/_ref, the unmodified reference headers) on the host cores.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config {1,2,3,5}] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rows", type=int, default=0, help="override rows per GPU (debug only)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--verbose", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def bytes_per_row(n: int, classes: int) -> int:
+    """Algorithmic HBM bytes of one direction for one row: N fp32 in + N fp32 out + u16 class id
+    (SURVEY.md §8 d2)."""
+    return 4 * n + 4 * n + (2 if classes > 1 else 0)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+            time.sleep(0.25)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for nm, v in zip(names, r[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+def dist_setup(gpus):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ----------------------------------------------------------------------- CPU reference -----
+def host_rows(w, rows, seed=7):
+    """Numpy stand-in generator for the CPU arm (same distributions as synth.py: separable AR(1)
+    with per-class rho, sigma=16; uniform class ids) so the reference arm touches no GPU code."""
+    rng = np.random.default_rng(seed)
+    cls = rng.integers(0, w.cfg.classes, rows).astype(np.uint16)
+    bs = w.block_size()
+    rho = w.rho[cls].astype(np.float64)[:, None]
+    q = np.sqrt(1 - rho * rho)
+    z = rng.standard_normal((rows, bs, bs))
+    for r in range(1, bs):
+        z[:, r, :] = rho * z[:, r - 1, :] + q * z[:, r, :]
+    for c in range(1, bs):
+        z[:, :, c] = rho * z[:, :, c - 1] + q * z[:, :, c]
+    return (z.reshape(rows, bs * bs) * w.cfg.sigma).astype(np.float32), cls
+
+
+def run_reference_sample(w, rows, threads, data=None):
+    """Time the reference's hygt::forward + hygt::inverse (oracle/_ref shim over the unmodified
+    reference headers) on `rows` rows of the workload with `threads` host threads. Returns s."""
+    from oracle import oracle as O
+    x, cls = data if data is not None else host_rows(w, rows)
+    full, mask = None, 0
+    if w.perms is not None:
+        full = np.concatenate([w.perms, np.tile(np.arange(w.n, dtype=np.uint16), (w.cfg.classes, 1, 1))], 1)
+        mask = (1 << (w.cfg.rounds - 1)) - 1
+    t0 = time.perf_counter()
+    y = O.ref_apply_batch(w.cfg.log2_n, w.cfg.rounds, w.angles, full, mask, x, cls, False, threads, out="f32")
+    O.ref_apply_batch(w.cfg.log2_n, w.cfg.rounds, w.angles, full, mask, y, cls, True, threads, out="f32")
+    return time.perf_counter() - t0
+
+
+def cpu_sample_rows(n, threads, seconds=1.0):
+    """Rows for a bounded CPU sample: the reference does ~3e5 (N=16) / 3e4 (N=64) / 4e3 (N=256)
+    fwd+inv rows/s per core, so this is about `seconds` of work on `threads` cores."""
+    per_core = {16: 3e5, 64: 3e4, 256: 4e3}.get(n, 1e5)
+    return int(min(max(1024, per_core * threads * seconds), (1 << 31) // (4 * n)))
+
+
+def impl_reference(args):
+    rank, world, local = dist_setup(args.gpus)
+    if rank != 0:
+        return 0
+    from paper_2505_21728_b200.synth import make_workload
+    w = make_workload(args.config)
+    threads = os.cpu_count() or 1
+    rows = cpu_sample_rows(w.n, threads)
+    data = host_rows(w, rows)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t = run_reference_sample(w, rows, threads, data)
+        if i >= args.warmup:
+            times.append(t)
+    t = statistics.median(times)
+    v = rows / t
+    line = {
+        "impl": "reference", "metric": "HyGT fwd+inv vectors/s", "value": v, "unit": "vectors/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.cfg.name, "rows_sampled": rows, "N": w.n,
+                   "classes": w.cfg.classes, "rounds": w.cfg.rounds},
+        "cpu_baseline": {"value": v, "unit": "vectors/s", "cores": threads, "kind": "reference",
+                         "sample": f"{rows} rows of {w.cfg.name}, hygt::forward+hygt::inverse per row "
+                                   f"(unmodified reference headers, g++ -O2), {threads} std::threads"},
+        "e2e": {"value": v, "unit": "vectors/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- ours --------
+def impl_ours(args):
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2505_21728_b200 import HyGTPlan
+    from paper_2505_21728_b200.synth import make_workload
+    w = make_workload(args.config)
+    rows = args.rows or w.cfg.count
+    if args.config == 5 and world > 1 and not args.rows:
+        rows = w.cfg.count // world  # config 5: 2^24 rows sharded across the GPUs
+    n = w.n
+    row0 = rank * rows
+    cls = w.make_classes(rows, row0)
+    x = w.make_rows(rows, cls, row0)
+    y = torch.empty_like(x)
+    xr = torch.empty_like(x)
+    plan = HyGTPlan(w.models, w.perms)
+    ws = torch.zeros(plan.workspace_bytes(rows), dtype=torch.uint8, device=dev)
+    energy = torch.zeros(w.cfg.classes, n, dtype=torch.float64, device=dev) if w.cfg.energy else None
+    stream = torch.cuda.current_stream()
+    l2_flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        plan.bucket(cls, rows, ws)
+        if ev is not None:
+            ev[1].record(stream)
+        if energy is not None:
+            energy.zero_()
+            plan.forward_energy(x, cls, energy, out=y, workspace=ws, reuse_buckets=True)
+        else:
+            plan.forward(x, cls, out=y, workspace=ws, reuse_buckets=True)
+        if ev is not None:
+            ev[2].record(stream)
+        plan.inverse(y, cls, out=xr, workspace=ws, reuse_buckets=True)
+        if ev is not None:
+            ev[3].record(stream)
+        if energy is not None and world > 1:
+            dist.all_reduce(energy)  # the one exchange step: 35 x 256 fp64 per-class energies
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    plan.sync_status(ws)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        total_ms = 0.0
+        for k in range(args.steps):
+            l2_flush.zero_()  # inputs are > L2 already; flush anyway so no step starts L2-warm
+            start.record(stream)
+            step(evs[k])
+            stop.record(stream)
+            stop.synchronize()
+            total_ms += start.elapsed_time(stop)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = total_ms / args.steps
+    t_bucket = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
+    t_fwd = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
+    t_inv = statistics.mean(e[2].elapsed_time(e[3]) for e in evs)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    plan.sync_status(ws)
+    total_rows = rows * world
+    value = total_rows / (ms * 1e-3)
+
+    hbm, hbm_kind = peaks()
+    bpr = bytes_per_row(n, w.cfg.classes)
+    launch_ms = (t_fwd + t_inv) / 2  # the fwd and inv apply kernels (same kernel family)
+    achieved = rows * bpr / (launch_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None,
+                "kernel": "hygt_apply_kernel (forward / inverse)",
+                "bytes_per_launch": rows * bpr, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({hbm_kind})"}
+    launches_per_step = 3 + 2  # hist, scan, scatter, forward, inverse
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e(plan, w, x, cls, rows, dev, stream, args, world)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        srows = cpu_sample_rows(n, threads, seconds=5.0)
+        t = run_reference_sample(w, srows, threads)
+        cpu = {"value": srows / t, "unit": "vectors/s", "cores": threads, "kind": "reference",
+               "sample": f"{srows} rows of {w.cfg.name}: hygt::forward+hygt::inverse per row "
+                         f"(unmodified reference headers via oracle/_ref, g++ -O2), {threads} threads"}
+    if rank == 0:
+        line = {
+            "metric": "HyGT fwd+inv vectors/s", "value": value, "unit": "vectors/s",
+            "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (device-generated separable AR(1) rows, seeded)",
+            "config": {"workload": w.cfg.name, "rows_per_gpu": rows, "N": n,
+                       "classes": w.cfg.classes, "rounds": w.cfg.rounds,
+                       "inter_round_perms": w.perms is not None,
+                       "step": "class bucketing + forward + inverse",
+                       "l2": "inputs larger than L2 (>=1 GiB per array) and a 256 MiB L2 flush between steps",
+                       "parallelism": f"dp{world}", "algorithm": plan.algorithm},
+            "breakdown_ms": {"bucket": t_bucket, "forward": t_fwd, "inverse": t_inv},
+            "roofline": roofline,
+            "clocks": clocks.summary(),
+            "gpu_launches": launches_per_step * args.steps,
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def measure_e2e(plan, w, x, cls, rows, dev, stream, args, world=1):
+    """Same step through the host-buffer API: pinned host x/cls -> device -> bucket + fwd + inv ->
+    host y and reconstruction, chunked over two streams so copies overlap compute."""
+    import torch
+    from paper_2505_21728_b200.pipeline import HostPipeline
+    xh = x.cpu().pin_memory()
+    ch = cls.cpu().pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    rh = torch.empty_like(xh).pin_memory()
+    pipe = HostPipeline(plan, rows_per_chunk=min(rows, 1 << 21), device=dev)
+    for _ in range(2):
+        pipe.roundtrip(xh, ch, yh, rh)
+    torch.cuda.synchronize()
+    steps = max(2, min(args.steps, 5))
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for _ in range(steps):
+        pipe.roundtrip(xh, ch, yh, rh)
+    stop.record(stream)
+    stop.synchronize()
+    t = start.elapsed_time(stop) * 1e-3 / steps
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([t], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    n = w.n
+    h2d = rows * n * 4 + rows * 2
+    d2h = 2 * rows * n * 4
+    return {"value": rows * world / t, "unit": "vectors/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": t * 1e3,
+            "path": "HostPipeline.roundtrip (pinned host in -> H2D -> bucket+fwd+inv -> D2H coefficients and reconstruction)"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return impl_reference(args)
+    return impl_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

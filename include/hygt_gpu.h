@@ -1,0 +1,148 @@
+/*
+ * hygt_gpu.h -- C ABI of the B200-native HyGT hot path (libhygt_gpu.so).
+ *
+ * This is the drop-in boundary for the reference's batched transform path. Each entry point
+ * names the reference interface it replaces (paths relative to /root/reference/proj):
+ *
+ *   hygt_plan_create / hygt_plan_destroy
+ *       <- hygt::HyGTModel (include/hygt/model.hpp:51-96), one per class, as cached by
+ *          run_apply (tools/hygt_main.cpp:143-144; ModelBundle::dequantized, bundle.hpp:83-86).
+ *   hygt_forward_f32 / hygt_inverse_f32
+ *       <- hygt::forward / hygt::inverse (include/hygt/transform.hpp:72-96) applied per block
+ *          with class dispatch, i.e. the loop of run_apply (tools/hygt_main.cpp:145-149).
+ *   hygt_forward_energy_f32
+ *       <- forward outputs folded into per-class CorrelationAccumulator diagonals
+ *          (include/hygt/statistics.hpp:69-77) -- E[c][i] = sum_{v in c} y_v[i]^2.
+ *   hygt_fixed_plan_create, hygt_forward_i64 / hygt_inverse_i64
+ *       <- hygt::QuantizedHyGTModel + TrigTable + forward_fixed / inverse_fixed
+ *          (include/hygt/fixedpoint.hpp:35-224), per block as tools/hygt_main.cpp:150-165.
+ *   hygt_klt_plan_create, hygt_klt_forward_f32 / hygt_klt_inverse_f32
+ *       <- hygt::klt_forward (include/hygt/statistics.hpp:222-224 -> matrix.hpp:70-80) and
+ *          its transpose (matrix.hpp:82-88), per class.
+ *   hygt_last_error
+ *       <- the what() string of the exception the reference would have thrown.
+ *
+ * Conventions
+ *   - All data pointers passed to the *_f32 / *_i64 calls are DEVICE pointers owned by the
+ *     caller; the calls are asynchronous and stream-ordered on `stream` (a cudaStream_t, NULL =
+ *     legacy default stream) unless documented otherwise.
+ *   - Rows are contiguous: x[row * N + i]. Class ids are uint16 per row (dataset.hpp:32); NULL
+ *     means every row is class 0.
+ *   - Plans are immutable after creation and may be used concurrently from several host
+ *     threads on different streams with distinct workspaces.
+ *   - Status codes mirror the reference exception classes (errors.hpp:23-45, exit codes
+ *     hygt_main.cpp:275-284): 0 ok, 1 ArgumentError, 2 IoError (reserved), 3 NumericalError,
+ *     4 OverflowError (a NumericalError subclass in the reference), 5 CUDA runtime failure.
+ */
+#ifndef HYGT_GPU_H
+#define HYGT_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HYGT_OK 0
+#define HYGT_ERR_ARGUMENT 1
+#define HYGT_ERR_IO 2
+#define HYGT_ERR_NUMERICAL 3
+#define HYGT_ERR_OVERFLOW 4
+#define HYGT_ERR_CUDA 5
+
+/* hygt_plan_create flags */
+#define HYGT_PLAN_FORCE_STANDARD 0x1u /* never use the scale-folded (fast Givens) form */
+#define HYGT_PLAN_FORCE_FAST 0x2u     /* refuse (status 3) if the fast form is unsafe   */
+
+/* call flags for the *_f32 transforms */
+#define HYGT_REUSE_BUCKETS 0x1u /* workspace already holds hygt_bucket() output for d_cls */
+
+typedef struct hygt_plan hygt_plan;
+typedef struct hygt_klt_plan hygt_klt_plan;
+
+/* Copies the message of the last failing call on this host thread into buf. Returns its
+ * status. */
+int hygt_last_error(char* buf, size_t len);
+
+/* ---- float HyGT --------------------------------------------------------------------------
+ * angles : host, [class_count][rounds * log2_n * 2^(log2_n-1)] fp64, application order
+ *          (model.hpp:77-79).
+ * perms  : host, [class_count][rounds][2^log2_n] uint16 or NULL. perms[c][r] is a gather
+ *          applied after round r (out[i] = pre[perm[i]], transform.hpp:75-80) when bit r of
+ *          perm_mask is set. Bit rounds-1 is the reference's final sorting permutation;
+ *          lower bits are the inter-round permutations of the BASELINE configs. Every present
+ *          permutation must be a bijection (model.hpp:37-44).
+ * Supported on the GPU: 1 <= log2_n <= 8, rounds >= 1, 1 <= class_count <= 4096. */
+int hygt_plan_create(int log2_n, int rounds, int class_count, const double* angles,
+                     const uint16_t* perms, uint32_t perm_mask, uint32_t flags,
+                     hygt_plan** out);
+int hygt_plan_destroy(hygt_plan* plan);
+/* 0 = standard rotations, 1 = scale-folded (fast Givens) form chosen at plan time. */
+int hygt_plan_algorithm(const hygt_plan* plan);
+
+/* Device workspace for class bucketing of `count` rows. */
+size_t hygt_workspace_bytes(const hygt_plan* plan, uint64_t count);
+/* Groups rows by class (histogram + scan + scatter into the workspace). The transforms call it
+ * themselves unless HYGT_REUSE_BUCKETS is passed. Invalid class ids are recorded and reported
+ * by hygt_sync_status(). */
+int hygt_bucket(const hygt_plan* plan, const uint16_t* d_cls, uint64_t count, void* d_ws,
+                size_t ws_bytes, void* stream);
+/* y = forward(x) row-wise (in place allowed). */
+int hygt_forward_f32(const hygt_plan* plan, const float* d_x, float* d_y, const uint16_t* d_cls,
+                     uint64_t count, void* d_ws, size_t ws_bytes, uint32_t flags, void* stream);
+/* x = inverse(y) row-wise (in place allowed). */
+int hygt_inverse_f32(const hygt_plan* plan, const float* d_y, float* d_x, const uint16_t* d_cls,
+                     uint64_t count, void* d_ws, size_t ws_bytes, uint32_t flags, void* stream);
+/* Forward plus fused per-class per-coefficient energy: d_energy[c][i] += sum y[row][i]^2 over
+ * rows of class c (fp64, [class_count][N], caller zeroes it). */
+int hygt_forward_energy_f32(const hygt_plan* plan, const float* d_x, float* d_y,
+                            const uint16_t* d_cls, uint64_t count, double* d_energy, void* d_ws,
+                            size_t ws_bytes, uint32_t flags, void* stream);
+/* Synchronises `stream` and returns the first device-side error recorded by calls that used
+ * this workspace (1 = a class id >= class_count), then clears it. */
+int hygt_sync_status(const hygt_plan* plan, void* d_ws, void* stream);
+
+/* ---- fixed-point HyGT (bit-exact with forward_fixed / inverse_fixed) ----------------------
+ * codes: host [class_count][rounds * log2_n * 2^(log2_n-1)] uint16 (< 2^angle_bits).
+ * perms/perm_mask as above. The calls are synchronous: they return the status of the first
+ * failing row in row order (1 = |input| > 2^20, 4 = |intermediate| > 2^46) and write its
+ * index to *first_bad (count if none). Rows are still transformed where possible. */
+int hygt_fixed_plan_create(int log2_n, int rounds, int class_count, int angle_bits,
+                           int precision_bits, const uint16_t* codes, const uint16_t* perms,
+                           uint32_t perm_mask, hygt_plan** out);
+int hygt_forward_i64(const hygt_plan* plan, const int64_t* d_x, int64_t* d_y,
+                     const uint16_t* d_cls, uint64_t count, uint64_t* first_bad, void* stream);
+int hygt_inverse_i64(const hygt_plan* plan, const int64_t* d_y, int64_t* d_x,
+                     const uint16_t* d_cls, uint64_t count, uint64_t* first_bad, void* stream);
+
+/* ---- dense per-class KLT (comparison path) ------------------------------------------------
+ * k: host [class_count][n][n] fp64 row-major (rows = basis vectors, KLTResult::basis). */
+int hygt_klt_plan_create(int n, int class_count, const double* k, uint32_t flags,
+                         hygt_klt_plan** out);
+int hygt_klt_plan_destroy(hygt_klt_plan* plan);
+size_t hygt_klt_workspace_bytes(const hygt_klt_plan* plan, uint64_t count);
+int hygt_klt_forward_f32(const hygt_klt_plan* plan, const float* d_x, float* d_y,
+                         const uint16_t* d_cls, uint64_t count, void* d_ws, size_t ws_bytes,
+                         void* stream);
+int hygt_klt_inverse_f32(const hygt_klt_plan* plan, const float* d_y, float* d_x,
+                         const uint16_t* d_cls, uint64_t count, void* d_ws, size_t ws_bytes,
+                         void* stream);
+
+/* ---- synthetic workloads, generated on the device -------------------------
+ * Separable 2-D AR(1) rows (covariance sigma^2 * A (x) A, A_ij = rho^|i-j|, raster order,
+ * statistics.hpp:287-305) with per-class rho (rho_per_class[cls[row]]), a fraction of rows
+ * replaced by directional-edge patterns a*sign(...) + N(0, edge_noise^2). Counter-based
+ * (Philox) so any row range is reproducible independently of the launch shape. */
+int hygt_synth_rows_f32(float* d_x, uint64_t count, uint64_t row0, int block_size,
+                        const uint16_t* d_cls, const float* d_rho_per_class, int class_count,
+                        float sigma, float edge_fraction, float edge_amplitude,
+                        float edge_noise, uint64_t seed, void* stream);
+/* Uniform class ids in [0, class_count). */
+int hygt_synth_classes(uint16_t* d_cls, uint64_t count, uint64_t row0, int class_count,
+                       uint64_t seed, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HYGT_GPU_H */

@@ -1,0 +1,553 @@
+/*
+ * hygt_oracle.c -- TEST INFRASTRUCTURE ONLY (see hygt_oracle.h).
+ *
+ * A plain-C restatement of the reference's HyGT hot path. Reference paths are relative to
+ * /root/reference/proj/include/hygt/ unless stated otherwise. This file is compiled into
+ * oracle/liboracle.so by oracle/Makefile and loaded by tests through ctypes; the product
+ * library never links it.
+ */
+#include "hygt_oracle.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define PI_D 3.14159265358979323846
+
+/* ============================== RNG (rng.hpp) ============================================ */
+
+/* rng.hpp:26-31 */
+uint64_t hygt_oracle_splitmix64(uint64_t state) {
+  uint64_t z = state + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+/* rng.hpp:36-38 */
+uint64_t hygt_oracle_derive_seed(uint64_t base, uint64_t stream) {
+  return hygt_oracle_splitmix64(base ^ hygt_oracle_splitmix64(stream + 1));
+}
+
+/* The reference wraps std::mt19937_64 (rng.hpp:46, 77). Its output is fixed by the C++
+ * standard ([rand.eng.mers], [rand.predef]): w=64 n=312 m=156 r=31, a=0xB5026F5AA96619E9,
+ * u=29 d=0x5555555555555555 s=17 b=0x71D67FFFEDA60000 t=37 c=0xFFF7EEE000000000 l=43,
+ * f=6364136223846793005. Restated here from that published definition. */
+#define MT_N 312
+#define MT_M 156
+void hygt_oracle_rng_seed(hygt_oracle_rng* r, uint64_t seed) {
+  r->mt[0] = seed;
+  for (int i = 1; i < MT_N; ++i)
+    r->mt[i] = 6364136223846793005ull * (r->mt[i - 1] ^ (r->mt[i - 1] >> 62)) + (uint64_t)i;
+  r->idx = MT_N;
+  r->spare = 0.0;
+  r->have_spare = 0;
+}
+
+static void mt_twist(hygt_oracle_rng* r) {
+  const uint64_t upper = 0xFFFFFFFF80000000ull, lower = 0x7FFFFFFFull;
+  for (int i = 0; i < MT_N; ++i) {
+    uint64_t x = (r->mt[i] & upper) | (r->mt[(i + 1) % MT_N] & lower);
+    uint64_t xa = x >> 1;
+    if (x & 1ull) xa ^= 0xB5026F5AA96619E9ull;
+    r->mt[i] = r->mt[(i + MT_M) % MT_N] ^ xa;
+  }
+  r->idx = 0;
+}
+
+uint64_t hygt_oracle_rng_next(hygt_oracle_rng* r) {
+  if (r->idx >= MT_N) mt_twist(r);
+  uint64_t y = r->mt[r->idx++];
+  y ^= (y >> 29) & 0x5555555555555555ull;
+  y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+  y ^= (y << 37) & 0xFFF7EEE000000000ull;
+  y ^= y >> 43;
+  return y;
+}
+
+/* rng.hpp:49 */
+double hygt_oracle_rng_uniform01(hygt_oracle_rng* r) {
+  return (double)(hygt_oracle_rng_next(r) >> 11) * 0x1.0p-53;
+}
+
+/* rng.hpp:52 */
+double hygt_oracle_rng_uniform(hygt_oracle_rng* r, double lo, double hi) {
+  return lo + (hi - lo) * hygt_oracle_rng_uniform01(r);
+}
+
+/* rng.hpp:55-68: Box-Muller, second value cached. */
+double hygt_oracle_rng_gaussian(hygt_oracle_rng* r) {
+  if (r->have_spare) {
+    r->have_spare = 0;
+    return r->spare;
+  }
+  double u1 = hygt_oracle_rng_uniform01(r);
+  if (u1 <= 0.0) u1 = 0x1.0p-53;
+  const double u2 = hygt_oracle_rng_uniform01(r);
+  const double rr = sqrt(-2.0 * log(u1));
+  const double a = 2.0 * PI_D * u2;
+  r->spare = rr * sin(a);
+  r->have_spare = 1;
+  return rr * cos(a);
+}
+
+/* rng.hpp:71 */
+uint64_t hygt_oracle_rng_below(hygt_oracle_rng* r, uint64_t bound) {
+  return hygt_oracle_rng_next(r) % bound;
+}
+
+/* ============================== schedule / model ========================================= */
+
+/* hypercube.hpp:59-77: m_j = j + (j & -k), n_j = m_j + k, k = 2^pass. */
+int hygt_oracle_hypercube_indices(int log2_n, int pass, uint32_t* m, uint32_t* n) {
+  if (log2_n < 1 || log2_n > 16) return HYGT_ORACLE_ARGUMENT;
+  if (pass < 0 || pass >= log2_n) return HYGT_ORACLE_ARGUMENT;
+  const uint32_t half = 1u << (log2_n - 1), k = 1u << pass;
+  for (uint32_t j = 0; j < half; ++j) {
+    m[j] = j + (j & (0u - k));
+    n[j] = m[j] + k;
+  }
+  return HYGT_ORACLE_OK;
+}
+
+/* model.hpp:29-34 */
+size_t hygt_oracle_num_parameters(int log2_n, int rounds) {
+  if (log2_n < 1 || rounds < 1) return 0;
+  return (size_t)rounds * ((size_t)1 << log2_n) * (size_t)log2_n / 2;
+}
+
+/* ============================== float transform ========================================== */
+
+/* transform.hpp:45-66. dir > 0 forward (rounds 0..R-1, passes 0..n-1, +theta); otherwise the
+ * exact reverse order with -theta. cos/sin are recomputed per butterfly as the reference does. */
+void hygt_oracle_run_passes(int log2_n, int rounds, const double* angles, double* x, int dir) {
+  const size_t half = (size_t)1 << (log2_n - 1);
+  const int fwd = dir > 0;
+  for (int step = 0; step < rounds * log2_n; ++step) {
+    const int r = fwd ? step / log2_n : rounds - 1 - step / log2_n;
+    const int p = fwd ? step % log2_n : log2_n - 1 - step % log2_n;
+    const uint32_t k = 1u << p;
+    const size_t base = ((size_t)r * log2_n + p) * half; /* model.hpp:77-79 */
+    for (uint32_t j = 0; j < half; ++j) {
+      const uint32_t m = j + (j & (0u - k));
+      const uint32_t n = m + k;
+      const double t = fwd ? angles[base + j] : -angles[base + j];
+      const double c = cos(t), s = sin(t);
+      const double a = x[m], b = x[n];
+      x[m] = c * a + s * b;
+      x[n] = c * b - s * a;
+    }
+  }
+}
+
+/* transform.hpp:72-82: passes, then gather out[i] = pre[perm[i]]. */
+void hygt_oracle_forward(int log2_n, int rounds, const double* angles, const uint16_t* perm,
+                         double* x) {
+  hygt_oracle_run_passes(log2_n, rounds, angles, x, +1);
+  if (perm) {
+    const size_t n = (size_t)1 << log2_n;
+    double local[256];
+    double* heap = n <= 256 ? NULL : (double*)malloc(n * sizeof(double));
+    double* buf = heap ? heap : local;
+    memcpy(buf, x, n * sizeof(double));
+    for (size_t i = 0; i < n; ++i) x[i] = buf[perm[i]];
+    free(heap);
+  }
+}
+
+/* transform.hpp:86-96: scatter x[perm[i]] = y[i], then reverse passes with -theta. */
+void hygt_oracle_inverse(int log2_n, int rounds, const double* angles, const uint16_t* perm,
+                         double* x) {
+  if (perm) {
+    const size_t n = (size_t)1 << log2_n;
+    double local[256];
+    double* heap = n <= 256 ? NULL : (double*)malloc(n * sizeof(double));
+    double* buf = heap ? heap : local;
+    memcpy(buf, x, n * sizeof(double));
+    for (size_t i = 0; i < n; ++i) x[perm[i]] = buf[i];
+    free(heap);
+  }
+  hygt_oracle_run_passes(log2_n, rounds, angles, x, -1);
+}
+
+/* forward = forward(M_{R-1}, ... forward(M_0, x)), M_r single-round models over
+ * the contiguous angle slice of round r (round-major layout, model.hpp:77-79). */
+void hygt_oracle_forward_chain(int log2_n, int rounds, const double* angles,
+                               const uint16_t* perms, uint32_t perm_mask, double* x) {
+  const size_t n = (size_t)1 << log2_n;
+  const size_t a1 = n / 2 * (size_t)log2_n;
+  for (int r = 0; r < rounds; ++r) {
+    const uint16_t* p = (perms && ((perm_mask >> r) & 1u)) ? perms + (size_t)r * n : NULL;
+    hygt_oracle_forward(log2_n, 1, angles + (size_t)r * a1, p, x);
+  }
+}
+
+/* inverse = inverse(M_0, ... inverse(M_{R-1}, y)). */
+void hygt_oracle_inverse_chain(int log2_n, int rounds, const double* angles,
+                               const uint16_t* perms, uint32_t perm_mask, double* x) {
+  const size_t n = (size_t)1 << log2_n;
+  const size_t a1 = n / 2 * (size_t)log2_n;
+  for (int r = rounds - 1; r >= 0; --r) {
+    const uint16_t* p = (perms && ((perm_mask >> r) & 1u)) ? perms + (size_t)r * n : NULL;
+    hygt_oracle_inverse(log2_n, 1, angles + (size_t)r * a1, p, x);
+  }
+}
+
+/* transform.hpp:100-117 (column j = forward(e_j)). */
+void hygt_oracle_to_matrix(int log2_n, int rounds, const double* angles, const uint16_t* perms,
+                           uint32_t perm_mask, double* t) {
+  const size_t n = (size_t)1 << log2_n;
+  double* e = (double*)malloc(n * sizeof(double));
+  for (size_t j = 0; j < n; ++j) {
+    memset(e, 0, n * sizeof(double));
+    e[j] = 1.0;
+    hygt_oracle_forward_chain(log2_n, rounds, angles, perms, perm_mask, e);
+    for (size_t i = 0; i < n; ++i) t[i * n + j] = e[i];
+  }
+  free(e);
+}
+
+/* ============================== batched drivers ========================================== */
+
+typedef struct {
+  int log2_n, rounds, classes;
+  const double* angles;
+  const uint16_t* perms;
+  uint32_t perm_mask;
+  const float* x;
+  const uint16_t* cls;
+  uint64_t begin, end;
+  int inverse;
+  double* y;        /* apply: [count][N]; NULL for energy */
+  double* energy;   /* energy: private [classes][N] accumulator */
+  int bad;
+} batch_job;
+
+static void* batch_worker(void* arg) {
+  batch_job* j = (batch_job*)arg;
+  const size_t n = (size_t)1 << j->log2_n;
+  const size_t a = hygt_oracle_num_parameters(j->log2_n, j->rounds);
+  double* v = (double*)malloc(n * sizeof(double));
+  for (uint64_t row = j->begin; row < j->end; ++row) {
+    const unsigned c = j->cls ? j->cls[row] : 0u;
+    if ((int)c >= j->classes) {
+      j->bad = 1;
+      continue;
+    }
+    for (size_t i = 0; i < n; ++i) v[i] = (double)j->x[row * n + i]; /* dataset.hpp:106 */
+    const double* ang = j->angles + (size_t)c * a;
+    const uint16_t* pp = j->perms ? j->perms + (size_t)c * (size_t)j->rounds * n : NULL;
+    if (j->inverse)
+      hygt_oracle_inverse_chain(j->log2_n, j->rounds, ang, pp, j->perm_mask, v);
+    else
+      hygt_oracle_forward_chain(j->log2_n, j->rounds, ang, pp, j->perm_mask, v);
+    if (j->y) memcpy(j->y + row * n, v, n * sizeof(double));
+    if (j->energy)
+      for (size_t i = 0; i < n; ++i) j->energy[c * n + i] += v[i] * v[i]; /* statistics.hpp:74 */
+  }
+  free(v);
+  return NULL;
+}
+
+static int run_jobs(batch_job* proto, uint64_t count, int threads, int energy) {
+  if (threads <= 0) threads = 1;
+  if ((uint64_t)threads > count && count > 0) threads = (int)count;
+  if (threads < 1) threads = 1;
+  const size_t n = (size_t)1 << proto->log2_n;
+  batch_job* jobs = (batch_job*)calloc((size_t)threads, sizeof(batch_job));
+  pthread_t* tid = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
+  for (int t = 0; t < threads; ++t) {
+    jobs[t] = *proto;
+    jobs[t].begin = count * (uint64_t)t / (uint64_t)threads;
+    jobs[t].end = count * (uint64_t)(t + 1) / (uint64_t)threads;
+    jobs[t].bad = 0;
+    if (energy) jobs[t].energy = (double*)calloc((size_t)proto->classes * n, sizeof(double));
+    pthread_create(&tid[t], NULL, batch_worker, &jobs[t]);
+  }
+  int bad = 0;
+  for (int t = 0; t < threads; ++t) {
+    pthread_join(tid[t], NULL);
+    bad |= jobs[t].bad;
+    if (energy) { /* shards merge by addition (statistics.hpp:110-120 for the sum form) */
+      for (size_t i = 0; i < (size_t)proto->classes * n; ++i) proto->energy[i] += jobs[t].energy[i];
+      free(jobs[t].energy);
+    }
+  }
+  free(jobs);
+  free(tid);
+  return bad ? HYGT_ORACLE_ARGUMENT : HYGT_ORACLE_OK;
+}
+
+int hygt_oracle_apply_batch(int log2_n, int rounds, int classes, const double* angles,
+                            const uint16_t* perms, uint32_t perm_mask, const float* x,
+                            const uint16_t* cls, uint64_t count, int inverse, double* y,
+                            int threads) {
+  batch_job p = {log2_n, rounds, classes, angles, perms, perm_mask, x, cls, 0, count,
+                 inverse, y, NULL, 0};
+  return run_jobs(&p, count, threads, 0);
+}
+
+int hygt_oracle_class_energy(int log2_n, int rounds, int classes, const double* angles,
+                             const uint16_t* perms, uint32_t perm_mask, const float* x,
+                             const uint16_t* cls, uint64_t count, double* energy, int threads) {
+  const size_t n = (size_t)1 << log2_n;
+  memset(energy, 0, (size_t)classes * n * sizeof(double));
+  batch_job p = {log2_n, rounds, classes, angles, perms, perm_mask, x, cls, 0, count,
+                 0, NULL, energy, 0};
+  return run_jobs(&p, count, threads, 1);
+}
+
+/* ============================== fixed point ============================================== */
+
+/* fixedpoint.hpp:37-52: entries lround(cos/sin(2*pi*q/2^b) * 2^p). */
+int hygt_oracle_trig_table(int angle_bits, int precision_bits, int32_t* cos_tab,
+                           int32_t* sin_tab) {
+  if (angle_bits < 1 || angle_bits > 12) return HYGT_ORACLE_ARGUMENT;
+  if (precision_bits < 4 || precision_bits > 15) return HYGT_ORACLE_ARGUMENT;
+  const size_t size = (size_t)1 << angle_bits;
+  const double scale = (double)((int64_t)1 << precision_bits);
+  for (size_t q = 0; q < size; ++q) {
+    const double a = 2.0 * PI_D * (double)q / (double)size;
+    cos_tab[q] = (int32_t)lround(cos(a) * scale);
+    sin_tab[q] = (int32_t)lround(sin(a) * scale);
+  }
+  return HYGT_ORACLE_OK;
+}
+
+/* fixedpoint.hpp:115-128: code = llround(theta / 2pi * 2^b) mod 2^b, wrapped non-negative. */
+int hygt_oracle_quantize(const double* angles, size_t count, int angle_bits, uint16_t* codes) {
+  if (angle_bits < 1 || angle_bits > 12) return HYGT_ORACLE_ARGUMENT;
+  const int64_t size = (int64_t)1 << angle_bits;
+  for (size_t i = 0; i < count; ++i) {
+    const double scaled = angles[i] / (2.0 * PI_D) * (double)size;
+    int64_t q = llround(scaled) % size;
+    if (q < 0) q += size;
+    codes[i] = (uint16_t)q;
+  }
+  return HYGT_ORACLE_OK;
+}
+
+/* fixedpoint.hpp:131-137 */
+void hygt_oracle_dequantize(const uint16_t* codes, size_t count, int angle_bits,
+                            double* angles) {
+  const double step = 2.0 * PI_D / (double)((int64_t)1 << angle_bits);
+  for (size_t i = 0; i < count; ++i) angles[i] = step * (double)codes[i];
+}
+
+#define FIXED_INPUT_LIMIT ((int64_t)1 << 20) /* fixedpoint.hpp:142 */
+#define FIXED_VALUE_LIMIT ((int64_t)1 << 46) /* fixedpoint.hpp:143 */
+
+/* fixedpoint.hpp:154-182, one round r (all passes of that round) in the given direction. */
+static int fixed_round(int log2_n, int r, int angle_bits, int p, const int32_t* ct,
+                       const int32_t* st, const uint16_t* codes, int64_t* x, int fwd) {
+  const size_t half = (size_t)1 << (log2_n - 1);
+  const uint32_t mask = (1u << angle_bits) - 1u;
+  const int64_t rnd = (int64_t)1 << (p - 1);
+  for (int s = 0; s < log2_n; ++s) {
+    const int d = fwd ? s : log2_n - 1 - s;
+    const uint32_t k = 1u << d;
+    const size_t base = ((size_t)r * log2_n + d) * half;
+    for (uint32_t j = 0; j < half; ++j) {
+      const uint32_t m = j + (j & (0u - k));
+      const uint32_t n = m + k;
+      uint32_t code = codes[base + j];
+      if (!fwd) code = (0u - code) & mask; /* :170 */
+      const int64_t c = ct[code], sn = st[code];
+      const int64_t a = x[m], b = x[n];
+      /* :175-176, arithmetic right shift of a signed int64 (as the reference relies on). */
+      x[m] = (c * a + sn * b + rnd) >> p;
+      x[n] = (c * b - sn * a + rnd) >> p;
+      if (x[m] > FIXED_VALUE_LIMIT || x[m] < -FIXED_VALUE_LIMIT || x[n] > FIXED_VALUE_LIMIT ||
+          x[n] < -FIXED_VALUE_LIMIT)
+        return HYGT_ORACLE_OVERFLOW; /* :177-179 */
+    }
+  }
+  return HYGT_ORACLE_OK;
+}
+
+static int fixed_check_input(const int64_t* x, size_t n) { /* fixedpoint.hpp:145-150 */
+  for (size_t i = 0; i < n; ++i)
+    if (x[i] > FIXED_INPUT_LIMIT || x[i] < -FIXED_INPUT_LIMIT) return HYGT_ORACLE_ARGUMENT;
+  return HYGT_ORACLE_OK;
+}
+
+static int fixed_args_ok(int log2_n, int rounds, int angle_bits, int precision_bits) {
+  return log2_n >= 1 && log2_n <= 16 && rounds >= 1 && angle_bits >= 1 && angle_bits <= 12 &&
+         precision_bits >= 4 && precision_bits <= 15;
+}
+
+/* fixedpoint.hpp:191-205 generalised with inter-round gathers (same semantics as the float
+ * chain; without inter-round permutations it is exactly forward_fixed). */
+int hygt_oracle_forward_fixed(int log2_n, int rounds, int angle_bits, int precision_bits,
+                              const uint16_t* codes, const uint16_t* perms, uint32_t perm_mask,
+                              int64_t* x) {
+  if (!fixed_args_ok(log2_n, rounds, angle_bits, precision_bits)) return HYGT_ORACLE_ARGUMENT;
+  const size_t n = (size_t)1 << log2_n;
+  int st = fixed_check_input(x, n);
+  if (st) return st;
+  int32_t ct[4096], sn[4096];
+  hygt_oracle_trig_table(angle_bits, precision_bits, ct, sn);
+  int64_t* tmp = (int64_t*)malloc(n * sizeof(int64_t));
+  for (int r = 0; r < rounds && !st; ++r) {
+    st = fixed_round(log2_n, r, angle_bits, precision_bits, ct, sn, codes, x, 1);
+    if (!st && perms && ((perm_mask >> r) & 1u)) {
+      const uint16_t* p = perms + (size_t)r * n;
+      memcpy(tmp, x, n * sizeof(int64_t));
+      for (size_t i = 0; i < n; ++i) x[i] = tmp[p[i]];
+    }
+  }
+  free(tmp);
+  return st;
+}
+
+/* fixedpoint.hpp:210-224: input check on the call's input (y), scatter, reverse passes. */
+int hygt_oracle_inverse_fixed(int log2_n, int rounds, int angle_bits, int precision_bits,
+                              const uint16_t* codes, const uint16_t* perms, uint32_t perm_mask,
+                              int64_t* x) {
+  if (!fixed_args_ok(log2_n, rounds, angle_bits, precision_bits)) return HYGT_ORACLE_ARGUMENT;
+  const size_t n = (size_t)1 << log2_n;
+  int st = fixed_check_input(x, n);
+  if (st) return st;
+  int32_t ct[4096], sn[4096];
+  hygt_oracle_trig_table(angle_bits, precision_bits, ct, sn);
+  int64_t* tmp = (int64_t*)malloc(n * sizeof(int64_t));
+  for (int r = rounds - 1; r >= 0 && !st; --r) {
+    if (perms && ((perm_mask >> r) & 1u)) {
+      const uint16_t* p = perms + (size_t)r * n;
+      memcpy(tmp, x, n * sizeof(int64_t));
+      for (size_t i = 0; i < n; ++i) x[p[i]] = tmp[i];
+    }
+    st = fixed_round(log2_n, r, angle_bits, precision_bits, ct, sn, codes, x, 0);
+  }
+  free(tmp);
+  return st;
+}
+
+int hygt_oracle_apply_batch_fixed(int log2_n, int rounds, int classes, int angle_bits,
+                                  int precision_bits, const uint16_t* codes,
+                                  const uint16_t* perms, uint32_t perm_mask, const int64_t* x,
+                                  const uint16_t* cls, uint64_t count, int inverse, int64_t* y,
+                                  uint64_t* first_bad, int threads) {
+  (void)threads;
+  const size_t n = (size_t)1 << log2_n;
+  const size_t a = hygt_oracle_num_parameters(log2_n, rounds);
+  int first = HYGT_ORACLE_OK;
+  *first_bad = count;
+  for (uint64_t row = 0; row < count; ++row) {
+    const unsigned c = cls ? cls[row] : 0u;
+    int64_t* v = y + row * n;
+    memcpy(v, x + row * n, n * sizeof(int64_t));
+    int st;
+    if ((int)c >= classes) {
+      st = HYGT_ORACLE_ARGUMENT;
+    } else {
+      const uint16_t* pp = perms ? perms + (size_t)c * (size_t)rounds * n : NULL;
+      st = inverse ? hygt_oracle_inverse_fixed(log2_n, rounds, angle_bits, precision_bits,
+                                               codes + (size_t)c * a, pp, perm_mask, v)
+                   : hygt_oracle_forward_fixed(log2_n, rounds, angle_bits, precision_bits,
+                                               codes + (size_t)c * a, pp, perm_mask, v);
+    }
+    if (st && first == HYGT_ORACLE_OK) {
+      first = st;
+      *first_bad = row;
+    }
+  }
+  return first;
+}
+
+/* fixedpoint.hpp:231-238 */
+size_t hygt_oracle_memory_footprint(int klt, int log2_n, int rounds, int num_transforms) {
+  if (log2_n < 1 || rounds < 1 || num_transforms < 1) return 0;
+  const size_t n = (size_t)1 << log2_n;
+  if (klt) return (size_t)num_transforms * n * n;
+  return (size_t)num_transforms * hygt_oracle_num_parameters(log2_n, rounds);
+}
+
+/* ============================== KLT ======================================================= */
+
+/* statistics.hpp:222-224 -> matrix.hpp:70-80 (y_i = sum_j K_ij x_j); inverse uses K^T
+ * (matrix.hpp:82-88). */
+int hygt_oracle_klt_apply(int n, int classes, const double* k, const float* x,
+                          const uint16_t* cls, uint64_t count, int inverse, double* y,
+                          int threads) {
+  (void)threads;
+  for (uint64_t row = 0; row < count; ++row) {
+    const unsigned c = cls ? cls[row] : 0u;
+    if ((int)c >= classes) return HYGT_ORACLE_ARGUMENT;
+    const double* kc = k + (size_t)c * n * n;
+    const float* xv = x + row * (size_t)n;
+    double* yv = y + row * (size_t)n;
+    for (int i = 0; i < n; ++i) {
+      double s = 0.0;
+      for (int j = 0; j < n; ++j)
+        s += (inverse ? kc[(size_t)j * n + i] : kc[(size_t)i * n + j]) * (double)xv[j];
+      yv[i] = s;
+    }
+  }
+  return HYGT_ORACLE_OK;
+}
+
+/* ============================== fixtures ================================================= */
+
+/* tests/oracles.hpp:94-100 */
+void hygt_oracle_fisher_yates(hygt_oracle_rng* r, uint16_t* perm, int n) {
+  for (int i = 0; i < n; ++i) perm[i] = (uint16_t)i;
+  for (int i = n; i > 1; --i) {
+    const int j = (int)hygt_oracle_rng_below(r, (uint64_t)i);
+    const uint16_t t = perm[i - 1];
+    perm[i - 1] = perm[j];
+    perm[j] = t;
+  }
+}
+
+/* Config 4 generator: Q of the Householder QR of a seeded Gaussian matrix,
+ * signs fixed so diag(R) > 0. The reference has no QR; this is the textbook algorithm. */
+void hygt_oracle_random_orthogonal(uint64_t seed, int n, double* q) {
+  hygt_oracle_rng r;
+  hygt_oracle_rng_seed(&r, seed);
+  double* a = (double*)malloc((size_t)n * n * sizeof(double));
+  double* v = (double*)malloc((size_t)n * sizeof(double));
+  double* d = (double*)malloc((size_t)n * sizeof(double));
+  for (int i = 0; i < n * n; ++i) a[i] = hygt_oracle_rng_gaussian(&r);
+  /* q starts as identity; accumulate Q = H_0 H_1 ... H_{n-1}. */
+  for (int i = 0; i < n * n; ++i) q[i] = 0.0;
+  for (int i = 0; i < n; ++i) q[i * n + i] = 1.0;
+  for (int k = 0; k < n; ++k) {
+    double norm = 0.0;
+    for (int i = k; i < n; ++i) norm += a[i * n + k] * a[i * n + k];
+    norm = sqrt(norm);
+    const double alpha = a[k * n + k] > 0 ? -norm : norm;
+    for (int i = 0; i < n; ++i) v[i] = 0.0;
+    for (int i = k; i < n; ++i) v[i] = a[i * n + k];
+    v[k] -= alpha;
+    double vn = 0.0;
+    for (int i = k; i < n; ++i) vn += v[i] * v[i];
+    if (vn == 0.0) {
+      d[k] = alpha;
+      continue;
+    }
+    /* A <- H A, H = I - 2 v v^T / (v^T v) */
+    for (int j = 0; j < n; ++j) {
+      double s = 0.0;
+      for (int i = k; i < n; ++i) s += v[i] * a[i * n + j];
+      s = 2.0 * s / vn;
+      for (int i = k; i < n; ++i) a[i * n + j] -= s * v[i];
+    }
+    /* Q <- Q H */
+    for (int i = 0; i < n; ++i) {
+      double s = 0.0;
+      for (int j = k; j < n; ++j) s += q[i * n + j] * v[j];
+      s = 2.0 * s / vn;
+      for (int j = k; j < n; ++j) q[i * n + j] -= s * v[j];
+    }
+    d[k] = a[k * n + k];
+  }
+  /* make diag(R) > 0: flip column k of Q where R_kk < 0 */
+  for (int k = 0; k < n; ++k)
+    if (d[k] < 0)
+      for (int i = 0; i < n; ++i) q[i * n + k] = -q[i * n + k];
+  free(a);
+  free(v);
+  free(d);
+}

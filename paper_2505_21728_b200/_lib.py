@@ -1,0 +1,71 @@
+"""ctypes binding of libhygt_gpu.so (include/hygt_gpu.h).
+
+The product path has no CPU fallback: if the CUDA library is missing or fails to load, every
+entry point raises. Build it with ``python -c "import __graft_entry__ as g; g.build()"``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libhygt_gpu.so")
+
+_p = C.c_void_p
+_i = C.c_int
+_u32 = C.c_uint32
+_u64 = C.c_uint64
+_sz = C.c_size_t
+_f = C.c_float
+
+# Every symbol include/hygt_gpu.h declares, with its ctypes signature (restype, argtypes).
+SIGNATURES = {
+    "hygt_last_error": (_i, [C.c_char_p, _sz]),
+    "hygt_plan_create": (_i, [_i, _i, _i, _p, _p, _u32, _u32, C.POINTER(_p)]),
+    "hygt_plan_destroy": (_i, [_p]),
+    "hygt_plan_algorithm": (_i, [_p]),
+    "hygt_workspace_bytes": (_sz, [_p, _u64]),
+    "hygt_bucket": (_i, [_p, _p, _u64, _p, _sz, _p]),
+    "hygt_forward_f32": (_i, [_p, _p, _p, _p, _u64, _p, _sz, _u32, _p]),
+    "hygt_inverse_f32": (_i, [_p, _p, _p, _p, _u64, _p, _sz, _u32, _p]),
+    "hygt_forward_energy_f32": (_i, [_p, _p, _p, _p, _u64, _p, _p, _sz, _u32, _p]),
+    "hygt_sync_status": (_i, [_p, _p, _p]),
+    "hygt_fixed_plan_create": (_i, [_i, _i, _i, _i, _i, _p, _p, _u32, C.POINTER(_p)]),
+    "hygt_forward_i64": (_i, [_p, _p, _p, _p, _u64, C.POINTER(_u64), _p]),
+    "hygt_inverse_i64": (_i, [_p, _p, _p, _p, _u64, C.POINTER(_u64), _p]),
+    "hygt_klt_plan_create": (_i, [_i, _i, _p, _u32, C.POINTER(_p)]),
+    "hygt_klt_plan_destroy": (_i, [_p]),
+    "hygt_klt_workspace_bytes": (_sz, [_p, _u64]),
+    "hygt_klt_forward_f32": (_i, [_p, _p, _p, _p, _u64, _p, _sz, _p]),
+    "hygt_klt_inverse_f32": (_i, [_p, _p, _p, _p, _u64, _p, _sz, _p]),
+    "hygt_synth_rows_f32": (_i, [_p, _u64, _u64, _i, _p, _p, _i, _f, _f, _f, _f, _u64, _p]),
+    "hygt_synth_classes": (_i, [_p, _u64, _u64, _i, _u64, _p]),
+}
+
+_LIB = None
+
+
+class LibraryMissing(RuntimeError):
+    pass
+
+
+def lib():
+    """Load (once) and return the CUDA library; raises if it is not built."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise LibraryMissing(
+                f"{LIB_PATH} is not built; run __graft_entry__.build() (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _LIB = L
+    return _LIB
+
+
+def last_error() -> str:
+    buf = C.create_string_buffer(512)
+    lib().hygt_last_error(buf, 512)
+    return buf.value.decode(errors="replace")

@@ -1,0 +1,831 @@
+// hygt_capi.cu -- libhygt_gpu.so: the extern "C" boundary (include/hygt_gpu.h), class
+// bucketing, kernel dispatch, the fixed-point and KLT paths and the device-side synthetic
+// workload generators. Built for sm_100a only (see __graft_entry__.build()).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include <cub/block/block_scan.cuh>
+
+#include "../../include/hygt_gpu.h"
+#include "hygt_kernels.cuh"
+#include "hygt_plan.h"
+
+using namespace hygt_gpu;
+
+// ============================================================================ errors =====
+namespace {
+thread_local std::string g_err_msg;
+thread_local int g_err_status = 0;
+
+int fail(int status, const std::string& msg) {
+  g_err_status = status;
+  g_err_msg = msg;
+  return status;
+}
+int ok() {
+  g_err_status = 0;
+  g_err_msg.clear();
+  return HYGT_OK;
+}
+#define CU(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(HYGT_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+}  // namespace
+
+int hygt_set_error(int status, const char* msg) { return fail(status, msg ? msg : ""); }
+
+extern "C" int hygt_last_error(char* buf, size_t len) {
+  if (buf && len) {
+    std::strncpy(buf, g_err_msg.c_str(), len - 1);
+    buf[len - 1] = 0;
+  }
+  return g_err_status;
+}
+
+// ============================================================================ plan =======
+struct hygt_plan {
+  int kind = 0;  // 0 float, 1 fixed
+  int log2n = 0, rounds = 0, classes = 0, lanes_log2 = 0;
+  int algo = 0;  // 0 standard, 1 scale-folded
+  uint32_t perm_mask = 0;
+  int num_sms = 148;
+  uint64_t chunk_rows = 0;  // bucketing locality window (rows); 0 = global
+  // float tables per direction (0 = forward, 1 = inverse)
+  float2* d_coef[2] = {nullptr, nullptr};
+  uint32_t stream_len[2] = {0, 0};
+  uint16_t* d_gidx[2] = {nullptr, nullptr};
+  uint64_t gmask[2] = {0, 0};
+  // fixed point
+  int angle_bits = 0, precision_bits = 0;
+  uint16_t* d_codes = nullptr;
+  int32_t* d_cos = nullptr;
+  int32_t* d_sin = nullptr;
+  uint16_t* d_fgather[2] = {nullptr, nullptr};  // [C][R+1][N]
+  unsigned long long* d_fixed_err = nullptr;
+  std::mutex* fixed_mu = nullptr;
+};
+
+namespace {
+
+template <class T>
+int upload(T** dst, const T* src, size_t n) {
+  if (n == 0) {
+    *dst = nullptr;
+    return HYGT_OK;
+  }
+  CU(cudaMalloc(reinterpret_cast<void**>(dst), n * sizeof(T)));
+  CU(cudaMemcpy(*dst, src, n * sizeof(T), cudaMemcpyHostToDevice));
+  return HYGT_OK;
+}
+
+void free_plan(hygt_plan* p) {
+  if (!p) return;
+  for (int d = 0; d < 2; ++d) {
+    cudaFree(p->d_coef[d]);
+    cudaFree(p->d_gidx[d]);
+    cudaFree(p->d_fgather[d]);
+  }
+  cudaFree(p->d_codes);
+  cudaFree(p->d_cos);
+  cudaFree(p->d_sin);
+  cudaFree(p->d_fixed_err);
+  delete p->fixed_mu;
+  delete p;
+}
+
+int check_perms(int log2n, int rounds, int classes, const uint16_t* perms, uint32_t mask) {
+  if (!perms) return HYGT_OK;
+  if (rounds > 32) return fail(HYGT_ERR_ARGUMENT, "hygt_plan_create: permutations need rounds <= 32");
+  const int n = 1 << log2n;
+  std::vector<char> seen(n);
+  for (int c = 0; c < classes; ++c)
+    for (int r = 0; r < rounds; ++r) {
+      if (!((mask >> r) & 1u)) continue;
+      std::fill(seen.begin(), seen.end(), 0);
+      const uint16_t* p = perms + ((size_t)c * rounds + r) * n;
+      for (int i = 0; i < n; ++i) {  // model.hpp:37-44
+        if (p[i] >= n || seen[p[i]]) return fail(HYGT_ERR_ARGUMENT, "permutation: not a bijection");
+        seen[p[i]] = 1;
+      }
+    }
+  return HYGT_OK;
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+
+}  // namespace
+
+// ======================================================================= bucketing =======
+namespace {
+
+constexpr int BK_THREADS = 1024;
+constexpr int BK_PER = 16;
+constexpr uint64_t BK_TILE = (uint64_t)BK_THREADS * BK_PER;  // rows per histogram tile
+
+struct WsLayout {
+  size_t err = 0, idx = 0, counts = 0, base = 0, seg = 0, total = 0;
+  uint64_t tiles = 0, chunks = 0, tiles_per_chunk = 0;
+};
+
+WsLayout ws_layout(int classes, uint64_t chunk_rows, uint64_t count) {
+  WsLayout w;
+  auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
+  w.tiles = (count + BK_TILE - 1) / BK_TILE;
+  if (w.tiles == 0) w.tiles = 1;
+  w.tiles_per_chunk = chunk_rows ? std::max<uint64_t>(1, chunk_rows / BK_TILE) : w.tiles;
+  w.chunks = (w.tiles + w.tiles_per_chunk - 1) / w.tiles_per_chunk;
+  const size_t cp1 = (size_t)classes + 1;
+  w.err = 0;
+  w.idx = 256;
+  w.counts = al(w.idx + count * sizeof(uint32_t));
+  w.base = al(w.counts + w.tiles * cp1 * sizeof(uint32_t));
+  w.seg = al(w.base + w.tiles * cp1 * sizeof(uint32_t));
+  w.total = al(w.seg + w.chunks * cp1 * sizeof(uint32_t));
+  return w;
+}
+
+__host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned r;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+  return r;
+}
+
+__global__ void __launch_bounds__(BK_THREADS) bucket_hist_kernel(const uint16_t* __restrict__ cls,
+                                                                 uint64_t count, int classes,
+                                                                 uint32_t* tile_counts,
+                                                                 uint32_t* err) {
+  extern __shared__ uint32_t cnt[];
+  for (int i = threadIdx.x; i <= classes; i += blockDim.x) cnt[i] = 0;
+  __syncthreads();
+  const uint64_t base = (uint64_t)blockIdx.x * BK_TILE;
+  bool bad = false;
+  for (int k = 0; k < BK_PER; ++k) {
+    const uint64_t row = base + (uint64_t)k * BK_THREADS + threadIdx.x;
+    if (row < count) {
+      int c = cls[row];
+      if (c >= classes) {
+        c = classes;
+        bad = true;
+      }
+      const unsigned peers = __match_any_sync(__activemask(), c);
+      if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&cnt[c], __popc(peers));
+    }
+  }
+  if (bad) atomicOr(err, 1u);
+  __syncthreads();
+  for (int i = threadIdx.x; i <= classes; i += blockDim.x)
+    tile_counts[(size_t)blockIdx.x * (classes + 1) + i] = cnt[i];
+}
+
+// One CTA per chunk: exclusive scan of the chunk's (class, tile) counts in class-major order.
+__global__ void __launch_bounds__(BK_THREADS) bucket_scan_kernel(const uint32_t* tile_counts,
+                                                                 uint32_t* tile_base,
+                                                                 uint32_t* seg_end,
+                                                                 uint64_t tiles,
+                                                                 uint64_t tiles_per_chunk,
+                                                                 int classes, uint64_t count) {
+  using Scan = cub::BlockScan<uint32_t, BK_THREADS>;
+  __shared__ typename Scan::TempStorage tmp;
+  const uint64_t t0 = (uint64_t)blockIdx.x * tiles_per_chunk;
+  const uint64_t tn = umin64(tiles_per_chunk, tiles - t0);
+  const uint64_t cp1 = (uint64_t)classes + 1;
+  const uint64_t entries = tn * cp1;
+  const uint64_t per = (entries + BK_THREADS - 1) / BK_THREADS;
+  const uint64_t e0 = umin64(entries, per * threadIdx.x);
+  const uint64_t e1 = umin64(entries, e0 + per);
+  auto at = [&](uint64_t e) {  // class-major entry e = c * tn + tl
+    const uint64_t c = e / tn, tl = e % tn;
+    return (t0 + tl) * cp1 + c;
+  };
+  uint32_t local = 0;
+  for (uint64_t e = e0; e < e1; ++e) local += tile_counts[at(e)];
+  uint32_t excl;
+  Scan(tmp).ExclusiveSum(local, excl);
+  const uint32_t row0 = (uint32_t)umin64(count, t0 * BK_TILE);
+  uint32_t run = row0 + excl;
+  for (uint64_t e = e0; e < e1; ++e) {
+    const uint32_t v = tile_counts[at(e)];
+    tile_base[at(e)] = run;
+    run += v;
+    if (e % tn == tn - 1) seg_end[(uint64_t)blockIdx.x * cp1 + e / tn] = run;
+  }
+}
+
+__global__ void __launch_bounds__(BK_THREADS) bucket_scatter_kernel(
+    const uint16_t* __restrict__ cls, uint64_t count, int classes, const uint32_t* tile_base,
+    uint32_t* idx) {
+  extern __shared__ uint32_t cur[];
+  for (int i = threadIdx.x; i <= classes; i += blockDim.x)
+    cur[i] = tile_base[(size_t)blockIdx.x * (classes + 1) + i];
+  __syncthreads();
+  const uint64_t base = (uint64_t)blockIdx.x * BK_TILE;
+  const int lane = threadIdx.x & 31;
+  for (int k = 0; k < BK_PER; ++k) {
+    const uint64_t row = base + (uint64_t)k * BK_THREADS + threadIdx.x;
+    if (row < count) {
+      int c = cls[row];
+      if (c >= classes) c = classes;
+      const unsigned peers = __match_any_sync(__activemask(), c);
+      const int leader = __ffs(peers) - 1;
+      uint32_t b = 0;
+      if (lane == leader) b = atomicAdd(&cur[c], __popc(peers));
+      b = __shfl_sync(peers, b, leader);
+      idx[b + __popc(peers & lanemask_lt())] = (uint32_t)row;
+    }
+  }
+}
+
+__global__ void validate_classes_kernel(const uint16_t* cls, uint64_t count, int classes,
+                                        uint32_t* err) {
+  bool bad = false;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    bad |= cls[i] >= classes;
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, 1u);
+}
+
+int run_bucket(const hygt_plan* p, int classes, uint64_t chunk_rows, const uint16_t* d_cls,
+               uint64_t count, void* d_ws, size_t ws_bytes, cudaStream_t st) {
+  const WsLayout w = ws_layout(classes, chunk_rows, count);
+  if (!d_ws || ws_bytes < w.total) return fail(HYGT_ERR_ARGUMENT, "hygt_bucket: workspace too small");
+  char* ws = static_cast<char*>(d_ws);
+  uint32_t* err = reinterpret_cast<uint32_t*>(ws + w.err);
+  if (count == 0) return ok();
+  if (!d_cls) return ok();
+  if (classes == 1) {
+    validate_classes_kernel<<<std::min<uint64_t>((count + 255) / 256, (uint64_t)p->num_sms * 8),
+                              256, 0, st>>>(d_cls, count, classes, err);
+    CU(cudaGetLastError());
+    return ok();
+  }
+  const size_t smem = ((size_t)classes + 1) * sizeof(uint32_t);
+  uint32_t* idx = reinterpret_cast<uint32_t*>(ws + w.idx);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(ws + w.counts);
+  uint32_t* base = reinterpret_cast<uint32_t*>(ws + w.base);
+  uint32_t* seg = reinterpret_cast<uint32_t*>(ws + w.seg);
+  bucket_hist_kernel<<<w.tiles, BK_THREADS, smem, st>>>(d_cls, count, classes, cnt, err);
+  CU(cudaGetLastError());
+  bucket_scan_kernel<<<w.chunks, BK_THREADS, 0, st>>>(cnt, base, seg, w.tiles,
+                                                      w.tiles_per_chunk, classes, count);
+  CU(cudaGetLastError());
+  bucket_scatter_kernel<<<w.tiles, BK_THREADS, smem, st>>>(d_cls, count, classes, base, idx);
+  CU(cudaGetLastError());
+  return ok();
+}
+
+}  // namespace
+
+// ======================================================================= dispatch ========
+namespace {
+
+using ApplyFn = void (*)(ApplyParams);
+
+template <int LOG2N, int L>
+ApplyFn pick_apply(bool standard, bool fwd, bool energy) {
+  if (standard) {
+    if (!fwd) return hygt_apply_kernel<LOG2N, L, true, false, false>;
+    return energy ? hygt_apply_kernel<LOG2N, L, true, true, true>
+                  : hygt_apply_kernel<LOG2N, L, true, true, false>;
+  }
+  if (!fwd) return hygt_apply_kernel<LOG2N, L, false, false, false>;
+  return energy ? hygt_apply_kernel<LOG2N, L, false, true, true>
+                : hygt_apply_kernel<LOG2N, L, false, true, false>;
+}
+
+// Instantiated (log2 N, log2 TPV) layouts.
+ApplyFn select_apply(int log2n, int l, bool standard, bool fwd, bool energy) {
+  switch (log2n * 16 + l) {
+    case 1 * 16 + 0: return pick_apply<1, 0>(standard, fwd, energy);
+    case 2 * 16 + 0: return pick_apply<2, 0>(standard, fwd, energy);
+    case 3 * 16 + 0: return pick_apply<3, 0>(standard, fwd, energy);
+    case 4 * 16 + 0: return pick_apply<4, 0>(standard, fwd, energy);
+    case 4 * 16 + 2: return pick_apply<4, 2>(standard, fwd, energy);
+    case 5 * 16 + 0: return pick_apply<5, 0>(standard, fwd, energy);
+    case 6 * 16 + 0: return pick_apply<6, 0>(standard, fwd, energy);
+    case 6 * 16 + 1: return pick_apply<6, 1>(standard, fwd, energy);
+    case 6 * 16 + 2: return pick_apply<6, 2>(standard, fwd, energy);
+    case 7 * 16 + 2: return pick_apply<7, 2>(standard, fwd, energy);
+    case 8 * 16 + 1: return pick_apply<8, 1>(standard, fwd, energy);
+    case 8 * 16 + 2: return pick_apply<8, 2>(standard, fwd, energy);
+    default: return nullptr;
+  }
+}
+
+constexpr int APPLY_THREADS = 256;
+
+size_t apply_smem(const hygt_plan* p, int dir) {
+  if (!p->gmask[dir]) return 0;
+  return (size_t)(APPLY_THREADS / 32) * 32 * (1u << p->log2n) / (1u << p->lanes_log2) * sizeof(float);
+}
+
+int run_apply(const hygt_plan* p, int dir, const float* x, float* y, const uint16_t* d_cls,
+              uint64_t count, double* energy, void* d_ws, size_t ws_bytes, uint32_t flags,
+              cudaStream_t st) {
+  if (!p || p->kind != 0) return fail(HYGT_ERR_ARGUMENT, "hygt: not a float plan");
+  if (count == 0) return ok();
+  if (!x || !y) return fail(HYGT_ERR_ARGUMENT, "hygt: null data pointer");
+  if (count > 0xFFFFFFFFull) return fail(HYGT_ERR_ARGUMENT, "hygt: at most 2^32-1 rows per call");
+  const bool bucketed = d_cls && p->classes > 1;
+  const WsLayout w = ws_layout(p->classes, p->chunk_rows, count);
+  if (d_cls) {
+    if (!d_ws || ws_bytes < w.total) return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
+    if (!(flags & HYGT_REUSE_BUCKETS)) {
+      const int s = run_bucket(p, p->classes, p->chunk_rows, d_cls, count, d_ws, ws_bytes, st);
+      if (s) return s;
+    }
+  }
+  ApplyParams P{};
+  P.x = x;
+  P.y = y;
+  char* ws = static_cast<char*>(d_ws);
+  P.idx = bucketed ? reinterpret_cast<const uint32_t*>(ws + w.idx) : nullptr;
+  P.seg_end = bucketed ? reinterpret_cast<const uint32_t*>(ws + w.seg) : nullptr;
+  P.nseg = bucketed ? (uint32_t)(w.chunks * (p->classes + 1)) : 0;
+  P.classes = p->classes;
+  P.count = count;
+  P.coef = p->d_coef[dir];
+  P.stream_len = p->stream_len[dir];
+  P.gidx = p->d_gidx[dir];
+  P.gmask = p->gmask[dir];
+  P.rounds = p->rounds;
+  P.energy = energy;
+  ApplyFn fn = select_apply(p->log2n, p->lanes_log2, p->algo == 0, dir == 0, energy != nullptr);
+  if (!fn) return fail(HYGT_ERR_ARGUMENT, "hygt: no kernel for this dimension/layout");
+  const size_t smem = apply_smem(p, dir);
+  int occ = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, APPLY_THREADS, smem));
+  if (occ < 1) occ = 1;
+  const uint64_t rows_per_warp_step = 32u >> p->lanes_log2;
+  const uint64_t warps_per_cta = APPLY_THREADS / 32;
+  const uint64_t max_ctas = (uint64_t)p->num_sms * occ;
+  uint64_t ctas = (count + rows_per_warp_step * warps_per_cta - 1) / (rows_per_warp_step * warps_per_cta);
+  ctas = std::min(ctas, max_ctas);
+  const uint64_t warps = ctas * warps_per_cta;
+  uint64_t span = (count + warps - 1) / warps;
+  span = (span + rows_per_warp_step - 1) / rows_per_warp_step * rows_per_warp_step;
+  P.warp_span = span;
+  fn<<<(unsigned)ctas, APPLY_THREADS, smem, st>>>(P);
+  CU(cudaGetLastError());
+  return ok();
+}
+
+}  // namespace
+
+// ======================================================================= float API =======
+extern "C" int hygt_plan_create(int log2_n, int rounds, int class_count, const double* angles,
+                                const uint16_t* perms, uint32_t perm_mask, uint32_t flags,
+                                hygt_plan** out) {
+  if (!out) return fail(HYGT_ERR_ARGUMENT, "hygt_plan_create: null out");
+  *out = nullptr;
+  if (log2_n < 1 || log2_n > 16) return fail(HYGT_ERR_ARGUMENT, "HyGTModel: log2_n out of range [1, 16]");
+  if (log2_n > 8) return fail(HYGT_ERR_ARGUMENT, "hygt_plan_create: GPU path supports log2_n <= 8");
+  if (rounds < 1) return fail(HYGT_ERR_ARGUMENT, "num_parameters: log2_n and rounds must be >= 1");
+  if (class_count < 1 || class_count > 4096)
+    return fail(HYGT_ERR_ARGUMENT, "hygt_plan_create: class_count must be in [1, 4096]");
+  if (!angles) return fail(HYGT_ERR_ARGUMENT, "hygt_plan_create: null angles");
+  if (perms && perm_mask == 0) perms = nullptr;
+  if (int s = check_perms(log2_n, rounds, class_count, perms, perm_mask)) return s;
+  for (size_t i = 0, n = (size_t)class_count * rounds * log2_n * ((size_t)1 << (log2_n - 1)); i < n; ++i)
+    if (!std::isfinite(angles[i])) return fail(HYGT_ERR_ARGUMENT, "hygt_plan_create: non-finite angle");
+
+  hygt_plan* p = new (std::nothrow) hygt_plan();
+  if (!p) return fail(HYGT_ERR_CUDA, "out of host memory");
+  p->kind = 0;
+  p->log2n = log2_n;
+  p->rounds = rounds;
+  p->classes = class_count;
+  p->perm_mask = perms ? perm_mask : 0;
+  int l = env_int("HYGT_LANES_LOG2", -1);
+  if (l < 0 || !select_apply(log2_n, l, false, true, false)) l = default_lane_log2(log2_n);
+  p->lanes_log2 = l;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  if (p->num_sms <= 0) p->num_sms = 148;
+  // Locality window of the class bucketing: short rows (<= 128 B) are bucketed inside one
+  // histogram tile so a warp's gathered rows stay within ~1 MB of HBM; longer rows bucket globally.
+  const long long chunk_env = env_int("HYGT_CHUNK_ROWS", -1);
+  p->chunk_rows = chunk_env >= 0 ? (uint64_t)chunk_env : (log2_n <= 5 ? BK_TILE : 0);
+
+  const Layout ly{log2_n, l};
+  bool standard = (flags & HYGT_PLAN_FORCE_STANDARD) != 0;
+  DirTables t[2];
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    bool good = true;
+    for (int d = 0; d < 2 && good; ++d)
+      good = build_direction(ly, rounds, class_count, angles, perms, p->perm_mask, d == 0,
+                             standard, t[d]);
+    if (good) break;
+    if (flags & HYGT_PLAN_FORCE_FAST) {
+      free_plan(p);
+      return fail(HYGT_ERR_NUMERICAL, "hygt_plan_create: scale-folded form unsafe for these angles");
+    }
+    standard = true;
+  }
+  p->algo = standard ? 0 : 1;
+  for (int d = 0; d < 2; ++d) {
+    int s = upload(&p->d_coef[d], reinterpret_cast<const float2*>(t[d].coef.data()), t[d].coef.size());
+    if (!s) s = upload(&p->d_gidx[d], t[d].gidx.data(), t[d].gmask ? t[d].gidx.size() : 0);
+    if (s) {
+      free_plan(p);
+      return s;
+    }
+    p->stream_len[d] = t[d].stream_len;
+    p->gmask[d] = t[d].gmask;
+    ApplyFn fns[2] = {select_apply(log2_n, l, standard, d == 0, false),
+                      select_apply(log2_n, l, standard, d == 0, d == 0)};
+    for (ApplyFn fn : fns)
+      if (fn && apply_smem(p, d) > 48 * 1024)
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)apply_smem(p, d));
+  }
+  *out = p;
+  return ok();
+}
+
+extern "C" int hygt_plan_destroy(hygt_plan* plan) {
+  free_plan(plan);
+  return ok();
+}
+
+extern "C" int hygt_plan_algorithm(const hygt_plan* plan) { return plan ? plan->algo : -1; }
+
+extern "C" size_t hygt_workspace_bytes(const hygt_plan* plan, uint64_t count) {
+  if (!plan) return 0;
+  return ws_layout(plan->classes, plan->chunk_rows, count).total;
+}
+
+extern "C" int hygt_bucket(const hygt_plan* plan, const uint16_t* d_cls, uint64_t count,
+                           void* d_ws, size_t ws_bytes, void* stream) {
+  if (!plan) return fail(HYGT_ERR_ARGUMENT, "hygt_bucket: null plan");
+  return run_bucket(plan, plan->classes, plan->chunk_rows, d_cls, count, d_ws, ws_bytes,
+                    as_stream(stream));
+}
+
+extern "C" int hygt_forward_f32(const hygt_plan* plan, const float* d_x, float* d_y,
+                                const uint16_t* d_cls, uint64_t count, void* d_ws,
+                                size_t ws_bytes, uint32_t flags, void* stream) {
+  return run_apply(plan, 0, d_x, d_y, d_cls, count, nullptr, d_ws, ws_bytes, flags,
+                   as_stream(stream));
+}
+
+extern "C" int hygt_inverse_f32(const hygt_plan* plan, const float* d_y, float* d_x,
+                                const uint16_t* d_cls, uint64_t count, void* d_ws,
+                                size_t ws_bytes, uint32_t flags, void* stream) {
+  return run_apply(plan, 1, d_y, d_x, d_cls, count, nullptr, d_ws, ws_bytes, flags,
+                   as_stream(stream));
+}
+
+extern "C" int hygt_forward_energy_f32(const hygt_plan* plan, const float* d_x, float* d_y,
+                                       const uint16_t* d_cls, uint64_t count, double* d_energy,
+                                       void* d_ws, size_t ws_bytes, uint32_t flags,
+                                       void* stream) {
+  if (!d_energy) return fail(HYGT_ERR_ARGUMENT, "hygt_forward_energy_f32: null energy");
+  return run_apply(plan, 0, d_x, d_y, d_cls, count, d_energy, d_ws, ws_bytes, flags,
+                   as_stream(stream));
+}
+
+extern "C" int hygt_sync_status(const hygt_plan* plan, void* d_ws, void* stream) {
+  (void)plan;
+  CU(cudaStreamSynchronize(as_stream(stream)));
+  if (!d_ws) return ok();
+  uint32_t err = 0;
+  CU(cudaMemcpy(&err, d_ws, sizeof(err), cudaMemcpyDeviceToHost));
+  if (err) {
+    CU(cudaMemset(d_ws, 0, sizeof(uint32_t)));
+    return fail(HYGT_ERR_ARGUMENT, "ResidualDataset: class id out of range");
+  }
+  return ok();
+}
+
+// ===================================================================== fixed point =======
+namespace {
+
+constexpr int FX_THREADS = 256;
+
+struct FixedParams {
+  const int64_t* x;
+  int64_t* y;
+  const uint16_t* cls;
+  uint64_t count;
+  int classes, log2n, rounds, angle_bits, precision_bits;
+  const uint16_t* codes;  // [C][A]
+  const int32_t* cos_tab;
+  const int32_t* sin_tab;
+  const uint16_t* gather;  // [C][R+1][N]
+  uint64_t gmask;
+  unsigned long long* err;  // min over (row << 3 | status)
+};
+
+// One warp per row; the row lives in shared memory as int64 (fixedpoint.hpp:154-182: int64
+// products, rounding shift, |value| > 2^46 -> OverflowError).
+template <bool FWD>
+__global__ void __launch_bounds__(FX_THREADS) fixed_kernel(const FixedParams P) {
+  extern __shared__ int64_t fx_smem[];
+  const int n = 1 << P.log2n, half = n / 2;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t* buf = fx_smem + (size_t)warp * 2 * n;
+  int64_t* tmp = buf + n;
+  const uint64_t warps = (uint64_t)gridDim.x * (FX_THREADS / 32);
+  const uint32_t mask = (1u << P.angle_bits) - 1u;
+  const int prec = P.precision_bits;
+  const int64_t rnd = (int64_t)1 << (prec - 1);
+  const int64_t in_lim = (int64_t)1 << 20, val_lim = (int64_t)1 << 46;  // fixedpoint.hpp:142-143
+  const size_t a_count = (size_t)P.rounds * P.log2n * half;
+  for (uint64_t row = (uint64_t)blockIdx.x * (FX_THREADS / 32) + warp; row < P.count; row += warps) {
+    const int64_t* xr = P.x + row * n;
+    bool bad_in = false;
+    for (int i = lane; i < n; i += 32) {
+      const int64_t v = xr[i];
+      buf[i] = v;
+      bad_in |= v > in_lim || v < -in_lim;  // fixedpoint.hpp:145-150
+    }
+    int status = __any_sync(0xffffffffu, bad_in) ? 1 : 0;
+    const int c = P.cls ? (int)P.cls[row] : 0;
+    if (c >= P.classes) status = 1;  // dataset.hpp:47
+    __syncwarp();
+    if (!status) {
+      const uint16_t* codes = P.codes + (size_t)c * a_count;
+      const uint16_t* gsrc = P.gather + (size_t)c * (P.rounds + 1) * n;
+      auto gather = [&](int step) {
+        const uint16_t* gs = gsrc + (size_t)step * n;
+        for (int i = lane; i < n; i += 32) tmp[i] = buf[gs[i]];
+        __syncwarp();
+        for (int i = lane; i < n; i += 32) buf[i] = tmp[i];
+        __syncwarp();
+      };
+      if (P.gmask & 1ull) gather(0);
+      for (int k = 0; k < P.rounds && !status; ++k) {
+        const int r = FWD ? k : P.rounds - 1 - k;
+        for (int pp = 0; pp < P.log2n && !status; ++pp) {
+          const int d = FWD ? pp : P.log2n - 1 - pp;
+          const uint32_t kk = 1u << d;
+          const size_t base = ((size_t)r * P.log2n + d) * half;
+          bool over = false;
+          for (int j = lane; j < half; j += 32) {
+            const uint32_t m = j + (j & (0u - kk)), nn = m + kk;
+            uint32_t code = codes[base + j];
+            if (!FWD) code = (0u - code) & mask;  // fixedpoint.hpp:170
+            const int64_t cs = P.cos_tab[code], sn = P.sin_tab[code];
+            const int64_t a = buf[m], b = buf[nn];
+            const int64_t ym = (cs * a + sn * b + rnd) >> prec;  // arithmetic shift
+            const int64_t yn = (cs * b - sn * a + rnd) >> prec;
+            buf[m] = ym;
+            buf[nn] = yn;
+            over |= ym > val_lim || ym < -val_lim || yn > val_lim || yn < -val_lim;
+          }
+          if (__any_sync(0xffffffffu, over)) status = 4;  // fixedpoint.hpp:177-179
+          __syncwarp();
+        }
+        if (!status && ((P.gmask >> (k + 1)) & 1ull)) gather(k + 1);
+      }
+    }
+    int64_t* yr = P.y + row * n;
+    for (int i = lane; i < n; i += 32) yr[i] = buf[i];
+    if (status && lane == 0) atomicMin(P.err, (unsigned long long)((row << 3) | (uint64_t)status));
+    __syncwarp();
+  }
+}
+
+int run_fixed(const hygt_plan* p, int dir, const int64_t* x, int64_t* y, const uint16_t* cls,
+              uint64_t count, uint64_t* first_bad, cudaStream_t st) {
+  if (!p || p->kind != 1) return fail(HYGT_ERR_ARGUMENT, "hygt: not a fixed-point plan");
+  if (first_bad) *first_bad = count;
+  if (count == 0) return ok();
+  if (!x || !y) return fail(HYGT_ERR_ARGUMENT, "hygt: null data pointer");
+  std::lock_guard<std::mutex> lock(*p->fixed_mu);
+  const unsigned long long init = ~0ull;
+  CU(cudaMemcpyAsync(p->d_fixed_err, &init, sizeof(init), cudaMemcpyHostToDevice, st));
+  FixedParams P{x, y, cls, count, p->classes, p->log2n, p->rounds, p->angle_bits,
+                p->precision_bits, p->d_codes, p->d_cos, p->d_sin, p->d_fgather[dir],
+                p->gmask[dir], p->d_fixed_err};
+  const size_t smem = (size_t)(FX_THREADS / 32) * 2 * (1u << p->log2n) * sizeof(int64_t);
+  const uint64_t ctas = std::min<uint64_t>((count + 7) / 8, (uint64_t)p->num_sms * 8);
+  if (dir == 0) fixed_kernel<true><<<(unsigned)ctas, FX_THREADS, smem, st>>>(P);
+  else fixed_kernel<false><<<(unsigned)ctas, FX_THREADS, smem, st>>>(P);
+  CU(cudaGetLastError());
+  unsigned long long key = 0;
+  CU(cudaMemcpyAsync(&key, p->d_fixed_err, sizeof(key), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (key == ~0ull) return ok();
+  const uint64_t row = key >> 3;
+  const int status = (int)(key & 7);
+  if (first_bad) *first_bad = row;
+  if (status == 4) return fail(HYGT_ERR_OVERFLOW, "fixed transform: intermediate exceeds 2^46");
+  if (cls) {
+    uint16_t c = 0;
+    CU(cudaMemcpy(&c, cls + row, sizeof(c), cudaMemcpyDeviceToHost));
+    if (c >= p->classes) return fail(HYGT_ERR_ARGUMENT, "ResidualDataset: class id out of range");
+  }
+  return fail(HYGT_ERR_ARGUMENT, "fixed transform: input magnitude exceeds 2^20");
+}
+
+}  // namespace
+
+extern "C" int hygt_fixed_plan_create(int log2_n, int rounds, int class_count, int angle_bits,
+                                      int precision_bits, const uint16_t* codes,
+                                      const uint16_t* perms, uint32_t perm_mask,
+                                      hygt_plan** out) {
+  if (!out) return fail(HYGT_ERR_ARGUMENT, "hygt_fixed_plan_create: null out");
+  *out = nullptr;
+  if (log2_n < 1 || log2_n > 16) return fail(HYGT_ERR_ARGUMENT, "QuantizedHyGTModel: log2_n out of range [1, 16]");
+  if (log2_n > 8) return fail(HYGT_ERR_ARGUMENT, "hygt_fixed_plan_create: GPU path supports log2_n <= 8");
+  if (angle_bits < 1 || angle_bits > 12)
+    return fail(HYGT_ERR_ARGUMENT, "QuantizedHyGTModel: angle_bits out of range [1, 12]");
+  if (precision_bits < 4 || precision_bits > 15)
+    return fail(HYGT_ERR_ARGUMENT, "TrigTable: precision_bits out of range [4, 15]");
+  if (rounds < 1) return fail(HYGT_ERR_ARGUMENT, "num_parameters: log2_n and rounds must be >= 1");
+  if (class_count < 1 || class_count > 65535) return fail(HYGT_ERR_ARGUMENT, "hygt_fixed_plan_create: class_count");
+  if (!codes) return fail(HYGT_ERR_ARGUMENT, "hygt_fixed_plan_create: null codes");
+  const size_t n = (size_t)1 << log2_n;
+  const size_t a = (size_t)rounds * log2_n * n / 2;
+  for (size_t i = 0; i < a * class_count; ++i)
+    if (codes[i] > (1u << angle_bits) - 1u)
+      return fail(HYGT_ERR_ARGUMENT, "QuantizedHyGTModel: code exceeds 2^angle_bits");
+  if (perms && perm_mask == 0) perms = nullptr;
+  if (int s = check_perms(log2_n, rounds, class_count, perms, perm_mask)) return s;
+
+  hygt_plan* p = new (std::nothrow) hygt_plan();
+  if (!p) return fail(HYGT_ERR_CUDA, "out of host memory");
+  p->kind = 1;
+  p->log2n = log2_n;
+  p->rounds = rounds;
+  p->classes = class_count;
+  p->angle_bits = angle_bits;
+  p->precision_bits = precision_bits;
+  p->perm_mask = perms ? perm_mask : 0;
+  p->fixed_mu = new std::mutex();
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  // TrigTable (fixedpoint.hpp:37-52), evaluated on the host exactly as the reference does.
+  const size_t size = (size_t)1 << angle_bits;
+  std::vector<int32_t> ct(size), sn(size);
+  const double scale = (double)((int64_t)1 << precision_bits);
+  for (size_t q = 0; q < size; ++q) {
+    const double ang = 2.0 * 3.14159265358979323846 * (double)q / (double)size;
+    ct[q] = (int32_t)std::lround(std::cos(ang) * scale);
+    sn[q] = (int32_t)std::lround(std::sin(ang) * scale);
+  }
+  int s = upload(&p->d_cos, ct.data(), size);
+  if (!s) s = upload(&p->d_sin, sn.data(), size);
+  if (!s) s = upload(&p->d_codes, codes, a * class_count);
+  if (!s) {
+    unsigned long long* e = nullptr;
+    if (cudaMalloc(&e, sizeof(*e)) != cudaSuccess) s = fail(HYGT_ERR_CUDA, "cudaMalloc");
+    p->d_fixed_err = e;
+  }
+  for (int d = 0; d < 2 && !s; ++d) {
+    std::vector<uint16_t> g((size_t)class_count * (rounds + 1) * n, 0);
+    for (int c = 0; c < class_count; ++c) {
+      uint64_t gm = 0;
+      const auto gs = exec_gathers(log2_n, rounds, perms ? perms + (size_t)c * rounds * n : nullptr,
+                                   p->perm_mask, d == 0, &gm);
+      p->gmask[d] = gm;
+      for (int k = 0; k <= rounds; ++k)
+        for (size_t i = 0; i < n && !gs[k].empty(); ++i)
+          g[((size_t)c * (rounds + 1) + k) * n + i] = (uint16_t)gs[k][i];
+    }
+    s = upload(&p->d_fgather[d], g.data(), g.size());
+  }
+  if (s) {
+    free_plan(p);
+    return s;
+  }
+  *out = p;
+  return ok();
+}
+
+extern "C" int hygt_forward_i64(const hygt_plan* plan, const int64_t* d_x, int64_t* d_y,
+                                const uint16_t* d_cls, uint64_t count, uint64_t* first_bad,
+                                void* stream) {
+  return run_fixed(plan, 0, d_x, d_y, d_cls, count, first_bad, as_stream(stream));
+}
+
+extern "C" int hygt_inverse_i64(const hygt_plan* plan, const int64_t* d_y, int64_t* d_x,
+                                const uint16_t* d_cls, uint64_t count, uint64_t* first_bad,
+                                void* stream) {
+  return run_fixed(plan, 1, d_y, d_x, d_cls, count, first_bad, as_stream(stream));
+}
+
+// ======================================================================= synthetic =======
+namespace {
+
+__device__ __forceinline__ uint64_t smix(uint64_t z) {  // SplitMix64 finaliser
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ double u01(uint64_t h) { return (double)(h >> 11) * 0x1.0p-53; }
+__device__ __forceinline__ float gauss(uint64_t seed, uint64_t row, uint32_t k) {
+  const uint64_t h = smix(seed ^ smix(row * 0x100000001B3ull + (k >> 1)));
+  double a = u01(h), b = u01(smix(h));
+  if (a <= 0.0) a = 0x1.0p-53;
+  const double r = sqrt(-2.0 * log(a));
+  return (float)((k & 1) ? r * sin(6.283185307179586 * b) : r * cos(6.283185307179586 * b));
+}
+
+__global__ void synth_classes_kernel(uint16_t* cls, uint64_t count, uint64_t row0, int classes,
+                                     uint64_t seed) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    cls[i] = (uint16_t)(smix(seed ^ smix(row0 + i)) % (uint64_t)classes);
+}
+
+// One warp per row; the bs x bs block sits in shared memory. Separable AR(1) recursion
+// (u_0 = z_0, u_k = rho u_{k-1} + sqrt(1-rho^2) z_k) along columns then rows gives covariance
+// A (x) A with A_ij = rho^|i-j| (ar1_covariance_2d, statistics.hpp:287-305).
+__global__ void synth_rows_kernel(float* x, uint64_t count, uint64_t row0, int bs,
+                                  const uint16_t* cls, const float* rho_c, float sigma,
+                                  float edge_frac, float edge_amp, float edge_noise,
+                                  uint64_t seed) {
+  __shared__ float tile[8][256];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* t = tile[warp];
+  const int n = bs * bs;
+  for (uint64_t i = (uint64_t)blockIdx.x * 8 + warp; i < count; i += (uint64_t)gridDim.x * 8) {
+    const uint64_t row = row0 + i;
+    const float rho = rho_c ? rho_c[cls ? cls[i] : 0] : 0.9f;
+    const float q = sqrtf(1.f - rho * rho);
+    const bool edge = u01(smix(seed ^ 0xED6Eull ^ smix(row))) < (double)edge_frac;
+    if (!edge) {
+      if (lane < bs) {  // column recursion
+        float prev = 0.f;
+        for (int r = 0; r < bs; ++r) {
+          const float z = gauss(seed, row, r * bs + lane);
+          prev = r == 0 ? z : rho * prev + q * z;
+          t[r * bs + lane] = prev;
+        }
+      }
+      __syncwarp();
+      if (lane < bs) {  // row recursion
+        float prev = 0.f;
+        for (int c = 0; c < bs; ++c) {
+          const float u = t[lane * bs + c];
+          prev = c == 0 ? u : rho * prev + q * u;
+          t[lane * bs + c] = prev;
+        }
+      }
+      __syncwarp();
+      for (int k = lane; k < n; k += 32) x[i * n + k] = sigma * t[k];
+    } else {
+      const uint64_t h = smix(seed ^ 0x5EDull ^ smix(row));
+      const double phi = 3.141592653589793 * u01(h);
+      const double delta = (u01(smix(h)) - 0.5) * 0.5 * bs;
+      const double cph = cos(phi), sph = sin(phi), mid = 0.5 * (bs - 1);
+      for (int k = lane; k < n; k += 32) {
+        const int r = k / bs, c = k % bs;
+        const double d = (c - mid) * cph + (r - mid) * sph - delta;
+        x[i * n + k] = (float)(edge_amp * (d >= 0 ? 1.0 : -1.0)) + edge_noise * gauss(seed ^ 0xE, row, k);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace
+
+extern "C" int hygt_synth_classes(uint16_t* d_cls, uint64_t count, uint64_t row0,
+                                  int class_count, uint64_t seed, void* stream) {
+  if (!d_cls || class_count < 1) return fail(HYGT_ERR_ARGUMENT, "hygt_synth_classes: bad args");
+  if (!count) return ok();
+  synth_classes_kernel<<<(unsigned)std::min<uint64_t>((count + 255) / 256, 148 * 16), 256, 0,
+                         as_stream(stream)>>>(d_cls, count, row0, class_count, seed);
+  CU(cudaGetLastError());
+  return ok();
+}
+
+extern "C" int hygt_synth_rows_f32(float* d_x, uint64_t count, uint64_t row0, int block_size,
+                                   const uint16_t* d_cls, const float* d_rho_per_class,
+                                   int class_count, float sigma, float edge_fraction,
+                                   float edge_amplitude, float edge_noise, uint64_t seed,
+                                   void* stream) {
+  (void)class_count;
+  if (!d_x || block_size < 1 || block_size > 16)
+    return fail(HYGT_ERR_ARGUMENT, "hygt_synth_rows_f32: block_size in [1, 16]");
+  if (!count) return ok();
+  synth_rows_kernel<<<(unsigned)std::min<uint64_t>((count + 7) / 8, 148 * 32), 256, 0,
+                      as_stream(stream)>>>(d_x, count, row0, block_size, d_cls, d_rho_per_class,
+                                           sigma, edge_fraction, edge_amplitude, edge_noise, seed);
+  CU(cudaGetLastError());
+  return ok();
+}

@@ -1,0 +1,38 @@
+// hygt_plan.h -- host plan builder interface (see hygt_plan.cpp).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <vector>
+
+#include "layout.h"
+
+namespace hygt_gpu {
+
+struct Float2 {
+  float x, y;
+};
+
+// One direction's device tables before upload.
+struct DirTables {
+  std::vector<Float2> coef;    // [C][TPV][stream_len]
+  std::vector<uint16_t> gidx;  // [C][R+1][TPV][E] gather sources (element indices)
+  uint64_t gmask = 0;          // bit k: gather step k present
+  uint32_t stream_len = 0;     // float2 words per lane stream
+};
+
+// Lane-group width (log2 TPV) used for a dimension unless overridden.
+int default_lane_log2(int log2n);
+
+// Execution-order gathers of one class: step 0 runs before round slot 0, step k+1 after slot k.
+// Forward: step r+1 = P_r. Inverse: step 0 = P_{R-1}^{-1}, step k+1 = P_{R-2-k}^{-1}.
+std::vector<std::vector<int>> exec_gathers(int log2n, int rounds, const uint16_t* perms_c,
+                                           uint32_t mask, bool fwd, uint64_t* gmask);
+
+// Builds the coefficient/gather streams of one direction. Returns false when the scale-folded
+// form was requested but is numerically unsafe for these angles.
+bool build_direction(const Layout& ly, int rounds, int classes, const double* angles,
+                     const uint16_t* perms, uint32_t mask, bool fwd, bool standard,
+                     DirTables& out);
+
+}  // namespace hygt_gpu

@@ -1,0 +1,337 @@
+"""GPU plans: the batched drop-in for the reference's per-block transform loop.
+
+``HyGTPlan`` replaces the per-class ``HyGTModel`` cache plus the ``hygt::forward`` /
+``hygt::inverse`` loop of ``run_apply`` (tools/hygt_main.cpp:143-149); ``FixedPlan`` replaces
+``forward_fixed`` / ``inverse_fixed`` (fixedpoint.hpp:191-224, hygt_main.cpp:150-165);
+``KLTPlan`` replaces ``klt_forward`` (statistics.hpp:222-224). Device buffers are torch CUDA
+tensors (plumbing only); all arithmetic runs in libhygt_gpu.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence, Union
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ArgumentError, raise_for
+from .model import HyGTModel, ModelBundle, QuantizedHyGTModel, TrigTable
+
+HYGT_PLAN_FORCE_STANDARD = 0x1
+HYGT_PLAN_FORCE_FAST = 0x2
+HYGT_REUSE_BUCKETS = 0x1
+
+
+def _check(status: int) -> None:
+    if status:
+        raise_for(status, _lib.last_error())
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+def _dev_ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _np_ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _models_of(models) -> list:
+    if isinstance(models, ModelBundle):
+        return [models.dequantized(c) for c in range(models.class_count())]
+    if isinstance(models, HyGTModel):
+        return [models]
+    return list(models)
+
+
+def _perm_table(models, rounds: int, n: int, inter_round_perms):
+    """[C][R][N] gathers + mask: bits 0..R-2 inter-round (BASELINE extension), bit R-1 the
+    reference's final sorting permutation (transform.hpp:75-80)."""
+    classes = len(models)
+    perms = np.tile(np.arange(n, dtype=np.uint16), (classes, rounds, 1))
+    mask = 0
+    if inter_round_perms is not None:
+        ip = np.asarray(inter_round_perms, dtype=np.int64)
+        if ip.shape != (classes, rounds - 1, n):
+            raise ArgumentError(f"inter_round_perms must have shape {(classes, rounds - 1, n)}")
+        perms[:, : rounds - 1, :] = ip
+        mask |= (1 << (rounds - 1)) - 1
+    if any(m.permutation is not None for m in models):
+        for c, m in enumerate(models):
+            if m.permutation is not None:
+                perms[c, rounds - 1] = m.permutation
+        mask |= 1 << (rounds - 1)
+    return (np.ascontiguousarray(perms) if mask else None), mask
+
+
+class _Workspace:
+    def __init__(self):
+        self.buf = None
+
+    def get(self, nbytes: int, device) -> torch.Tensor:
+        if self.buf is None or self.buf.numel() < nbytes or self.buf.device != device:
+            self.buf = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
+        return self.buf
+
+
+class HyGTPlan:
+    """Batched float HyGT over per-class models.
+
+    models            : HyGTModel, list of HyGTModel (one per class) or ModelBundle
+    inter_round_perms : optional [C][R-1][N] gathers applied after rounds 0..R-2
+    """
+
+    def __init__(self, models, inter_round_perms=None, flags: int = 0):
+        models = _models_of(models)
+        if not models:
+            raise ArgumentError("HyGTPlan: need at least one class")
+        log2_n, rounds = models[0].log2_n, models[0].rounds
+        for m in models:
+            if m.log2_n != log2_n or m.rounds != rounds:
+                raise ArgumentError("HyGTPlan: all classes must share log2_n and rounds")
+        self.log2_n, self.rounds, self.classes = log2_n, rounds, len(models)
+        self.n = 1 << log2_n
+        angles = np.ascontiguousarray(np.stack([m.angles for m in models]), dtype=np.float64)
+        perms, mask = _perm_table(models, rounds, self.n, inter_round_perms)
+        self.perm_mask = mask
+        h = C.c_void_p()
+        _check(_lib.lib().hygt_plan_create(log2_n, rounds, self.classes, _np_ptr(angles),
+                                           _np_ptr(perms), mask, flags, C.byref(h)))
+        self._h = h
+        self._ws = _Workspace()
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and h.value:
+            try:
+                _lib.lib().hygt_plan_destroy(h)
+            except Exception:
+                pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def algorithm(self) -> str:
+        return "scale-folded" if _lib.lib().hygt_plan_algorithm(self._h) == 1 else "standard"
+
+    def workspace_bytes(self, count: int) -> int:
+        return _lib.lib().hygt_workspace_bytes(self._h, count)
+
+    def _prep(self, x: torch.Tensor, cls: Optional[torch.Tensor], out: Optional[torch.Tensor]):
+        if not isinstance(x, torch.Tensor) or not x.is_cuda:
+            raise ArgumentError("HyGTPlan: x must be a CUDA tensor (use apply() for host data)")
+        if x.dtype != torch.float32 or x.shape[-1] != self.n or not x.is_contiguous():
+            raise ArgumentError("forward: dimension mismatch")
+        count = x.numel() // self.n
+        if cls is not None:
+            if cls.dtype not in (torch.uint16, torch.int16) or cls.numel() != count or not cls.is_cuda:
+                raise ArgumentError("HyGTPlan: cls must be a CUDA uint16 tensor with one id per row")
+        if out is None:
+            out = torch.empty_like(x)
+        elif out.shape != x.shape or out.dtype != torch.float32 or not out.is_contiguous():
+            raise ArgumentError("HyGTPlan: bad output tensor")
+        return count, out
+
+    def _run(self, fn, x, cls, out, stream, workspace, reuse_buckets, energy=None):
+        count, out = self._prep(x, cls, out)
+        nbytes = self.workspace_bytes(count)
+        ws = workspace if workspace is not None else self._ws.get(nbytes, x.device)
+        flags = HYGT_REUSE_BUCKETS if reuse_buckets else 0
+        args = [self._h, x.data_ptr(), out.data_ptr(), _dev_ptr(cls), count]
+        if energy is not None:
+            args.append(energy.data_ptr())
+        args += [ws.data_ptr(), ws.numel(), flags, _stream_ptr(stream)]
+        _check(fn(*args))
+        return out
+
+    def forward(self, x, cls=None, out=None, stream=None, workspace=None, reuse_buckets=False):
+        """Rows y = forward(x) on the device (asynchronous)."""
+        return self._run(_lib.lib().hygt_forward_f32, x, cls, out, stream, workspace, reuse_buckets)
+
+    def inverse(self, y, cls=None, out=None, stream=None, workspace=None, reuse_buckets=False):
+        """Rows x = inverse(y) on the device (asynchronous)."""
+        return self._run(_lib.lib().hygt_inverse_f32, y, cls, out, stream, workspace, reuse_buckets)
+
+    def forward_energy(self, x, cls, energy, out=None, stream=None, workspace=None,
+                       reuse_buckets=False):
+        """Forward plus energy[c][i] += sum of y[row][i]^2 over rows of class c (fp64)."""
+        if energy.dtype != torch.float64 or energy.shape != (self.classes, self.n):
+            raise ArgumentError("forward_energy: energy must be float64 [classes][N]")
+        return self._run(_lib.lib().hygt_forward_energy_f32, x, cls, out, stream, workspace,
+                         reuse_buckets, energy=energy)
+
+    def bucket(self, cls, count, workspace, stream=None):
+        _check(_lib.lib().hygt_bucket(self._h, _dev_ptr(cls), count, workspace.data_ptr(),
+                                      workspace.numel(), _stream_ptr(stream)))
+
+    def sync_status(self, workspace=None, stream=None):
+        """Synchronise and raise the device-recorded error (invalid class ids) if any."""
+        ws = workspace if workspace is not None else self._ws.buf
+        _check(_lib.lib().hygt_sync_status(self._h, _dev_ptr(ws), _stream_ptr(stream)))
+
+    # ---- end-to-end on host buffers (the run_apply call a user makes) ----------------------
+    def apply(self, x_host: np.ndarray, cls_host: Optional[np.ndarray] = None,
+              inverse: bool = False) -> np.ndarray:
+        """Host fp32 rows in, host fp32 rows out (H2D, transform, D2H, status check)."""
+        x = torch.from_numpy(np.ascontiguousarray(x_host, dtype=np.float32)).cuda()
+        c = None
+        if cls_host is not None:
+            c = torch.from_numpy(np.ascontiguousarray(cls_host, dtype=np.uint16).view(np.int16)).cuda()
+            c = c.view(torch.uint16)
+        y = (self.inverse if inverse else self.forward)(x, c)
+        self.sync_status()
+        return y.cpu().numpy()
+
+
+class FixedPlan:
+    """Bit-exact integer HyGT (forward_fixed / inverse_fixed) over per-class quantized models."""
+
+    def __init__(self, models, table: TrigTable, inter_round_perms=None):
+        if isinstance(models, ModelBundle):
+            models = [models.quantized_model(c) for c in range(models.class_count())]
+        elif isinstance(models, QuantizedHyGTModel):
+            models = [models]
+        models = list(models)
+        for m in models:
+            if m.angle_bits != table.angle_bits:
+                raise ArgumentError("forward_fixed: table/model angle_bits mismatch")
+            if m.log2_n != models[0].log2_n or m.rounds != models[0].rounds:
+                raise ArgumentError("FixedPlan: all classes must share log2_n and rounds")
+        self.log2_n, self.rounds, self.classes = models[0].log2_n, models[0].rounds, len(models)
+        self.n = 1 << self.log2_n
+        codes = np.ascontiguousarray(np.stack([m.codes for m in models]), dtype=np.uint16)
+        perms, mask = _perm_table(models, self.rounds, self.n, inter_round_perms)
+        h = C.c_void_p()
+        _check(_lib.lib().hygt_fixed_plan_create(self.log2_n, self.rounds, self.classes,
+                                                 table.angle_bits, table.precision_bits,
+                                                 _np_ptr(codes), _np_ptr(perms), mask, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and h.value:
+            try:
+                _lib.lib().hygt_plan_destroy(h)
+            except Exception:
+                pass
+
+    def _run(self, fn, x, cls, out, stream):
+        if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dtype != torch.int64:
+            raise ArgumentError("FixedPlan: x must be a CUDA int64 tensor")
+        if x.shape[-1] != self.n or not x.is_contiguous():
+            raise ArgumentError("fixed transform: dimension mismatch")
+        count = x.numel() // self.n
+        out = torch.empty_like(x) if out is None else out
+        bad = C.c_uint64(0)
+        st = fn(self._h, x.data_ptr(), out.data_ptr(), _dev_ptr(cls), count, C.byref(bad),
+                _stream_ptr(stream))
+        self.first_bad = int(bad.value)
+        _check(st)
+        return out
+
+    def forward(self, x, cls=None, out=None, stream=None):
+        return self._run(_lib.lib().hygt_forward_i64, x, cls, out, stream)
+
+    def inverse(self, y, cls=None, out=None, stream=None):
+        return self._run(_lib.lib().hygt_inverse_i64, y, cls, out, stream)
+
+
+class KLTPlan:
+    """Per-class dense KLT: y = K_c x, x = K_c^T y (statistics.hpp:222-224, matrix.hpp:70-88)."""
+
+    def __init__(self, bases):
+        k = np.ascontiguousarray(bases, dtype=np.float64)
+        if k.ndim == 2:
+            k = k[None]
+        self.classes, self.n = k.shape[0], k.shape[1]
+        h = C.c_void_p()
+        _check(_lib.lib().hygt_klt_plan_create(self.n, self.classes, _np_ptr(k), 0, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and h.value:
+            try:
+                _lib.lib().hygt_klt_plan_destroy(h)
+            except Exception:
+                pass
+
+    def _run(self, fn, x, cls, out, stream):
+        count = x.numel() // self.n
+        out = torch.empty_like(x) if out is None else out
+        _check(fn(self._h, x.data_ptr(), out.data_ptr(), _dev_ptr(cls), count, None, 0,
+                  _stream_ptr(stream)))
+        return out
+
+    def forward(self, x, cls=None, out=None, stream=None):
+        return self._run(_lib.lib().hygt_klt_forward_f32, x, cls, out, stream)
+
+    def inverse(self, y, cls=None, out=None, stream=None):
+        return self._run(_lib.lib().hygt_klt_inverse_f32, y, cls, out, stream)
+
+
+# ------------------------------------------------ single-vector drop-ins (transform.hpp) ----
+_PLAN_CACHE: dict = {}
+
+
+def _cached(key, make):
+    p = _PLAN_CACHE.get(key)
+    if p is None:
+        p = make()
+        if len(_PLAN_CACHE) > 64:
+            _PLAN_CACHE.clear()
+        _PLAN_CACHE[key] = p
+    return p
+
+
+def _model_key(m):
+    return (id(m), m.log2_n, m.rounds)
+
+
+def forward(model: HyGTModel, x) -> np.ndarray:
+    """hygt::forward (transform.hpp:72-82) for one vector, computed on the GPU in fp32."""
+    v = np.asarray(x, dtype=np.float64).reshape(-1)
+    if v.size != model.dimension():
+        raise ArgumentError("forward: dimension mismatch")
+    plan = _cached(_model_key(model), lambda: HyGTPlan(model))
+    return plan.apply(v[None].astype(np.float32))[0].astype(np.float64)
+
+
+def inverse(model: HyGTModel, y) -> np.ndarray:
+    """hygt::inverse (transform.hpp:86-96) for one vector, computed on the GPU in fp32."""
+    v = np.asarray(y, dtype=np.float64).reshape(-1)
+    if v.size != model.dimension():
+        raise ArgumentError("inverse: dimension mismatch")
+    plan = _cached(_model_key(model), lambda: HyGTPlan(model))
+    return plan.apply(v[None].astype(np.float32), inverse=True)[0].astype(np.float64)
+
+
+def _fixed(model: QuantizedHyGTModel, table: TrigTable, x, inverse_: bool) -> np.ndarray:
+    name = "inverse_fixed" if inverse_ else "forward_fixed"
+    if table.angle_bits != model.angle_bits:
+        raise ArgumentError(f"{name}: table/model angle_bits mismatch")
+    v = np.asarray(x, dtype=np.int64).reshape(-1)
+    if v.size != model.dimension():
+        raise ArgumentError("fixed transform: dimension mismatch")
+    plan = _cached((id(model), id(table), "fx"), lambda: FixedPlan(model, table))
+    t = torch.from_numpy(v[None].copy()).cuda()
+    out = plan.inverse(t) if inverse_ else plan.forward(t)
+    return out.cpu().numpy()[0]
+
+
+def forward_fixed(model: QuantizedHyGTModel, table: TrigTable, x) -> np.ndarray:
+    """hygt::forward_fixed (fixedpoint.hpp:191-205), bit-exact, on the GPU."""
+    return _fixed(model, table, x, False)
+
+
+def inverse_fixed(model: QuantizedHyGTModel, table: TrigTable, y) -> np.ndarray:
+    """hygt::inverse_fixed (fixedpoint.hpp:210-224), bit-exact, on the GPU."""
+    return _fixed(model, table, y, True)

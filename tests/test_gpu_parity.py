@@ -1,0 +1,274 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle / golden vectors.
+
+Tolerances (fp32 GPU vs fp64 reference, SURVEY.md §8 c4 / BASELINE.md):
+    relative L2 over the batch <= 1e-6, max-abs <= 1e-5 * max|x|; energy sums rel <= 1e-5;
+    fixed point: bit-exact, identical error outcomes.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+REL_L2 = 1e-6
+MAX_ABS = 1e-5
+
+
+def check_close(y, ref, x, what=""):
+    y = np.asarray(y, np.float64)
+    ref = np.asarray(ref, np.float64)
+    scale = max(float(np.abs(x).max()), 1e-30)
+    err = y - ref
+    rel = np.linalg.norm(err) / max(np.linalg.norm(ref), 1e-300)
+    mab = float(np.abs(err).max()) if err.size else 0.0
+    assert rel <= REL_L2, f"{what}: rel L2 {rel:.3e}"
+    assert mab <= MAX_ABS * scale, f"{what}: max abs {mab:.3e} vs {MAX_ABS * scale:.3e}"
+    return rel, mab
+
+
+def _plan(models, perms_inter=None, standard=False):
+    from paper_2505_21728_b200 import HyGTPlan
+    from paper_2505_21728_b200.plan import HYGT_PLAN_FORCE_STANDARD
+    return HyGTPlan(models, perms_inter, flags=HYGT_PLAN_FORCE_STANDARD if standard else 0)
+
+
+def _models(log2n, rounds, angles, perms=None, mask=0):
+    from paper_2505_21728_b200 import HyGTModel
+    final = perms is not None and (mask >> (rounds - 1)) & 1
+    return [HyGTModel(log2n, rounds, angles[c], perms[c, rounds - 1] if final else None)
+            for c in range(angles.shape[0])]
+
+
+def _inter(perms, mask, rounds):
+    if perms is None or not (mask & ((1 << (rounds - 1)) - 1)):
+        return None
+    ip = perms[:, : rounds - 1].copy()
+    for r in range(rounds - 1):
+        if not (mask >> r) & 1:
+            ip[:, r] = np.arange(ip.shape[-1])
+    return ip
+
+
+LAYOUTS = {1: [0], 2: [0], 3: [0], 4: [0, 2], 5: [0], 6: [0, 1, 2], 7: [2], 8: [1, 2]}
+
+
+@pytest.mark.parametrize("standard", [False, True])
+@pytest.mark.parametrize("k", range(10))
+def test_golden_float_all_layouts(cuda, golden, k, standard, monkeypatch):
+    log2n, rounds, classes, mask = (int(v) for v in golden[f"f{k}_meta"])
+    angles, perms = golden[f"f{k}_angles"], golden[f"f{k}_perms"]
+    x, cls = golden[f"f{k}_x"], golden[f"f{k}_cls"]
+    xd = torch.from_numpy(x).to(cuda)
+    cd = torch.from_numpy(cls).to(cuda)
+    for lanes in LAYOUTS[log2n]:
+        monkeypatch.setenv("HYGT_LANES_LOG2", str(lanes))
+        plan = _plan(_models(log2n, rounds, angles, perms, mask), _inter(perms, mask, rounds), standard)
+        y = plan.forward(xd, cd)
+        plan.sync_status()
+        check_close(y.cpu().numpy(), golden[f"f{k}_fwd"], x, f"fwd k={k} L={lanes} {plan.algorithm}")
+        z = plan.inverse(xd, cd)
+        plan.sync_status()
+        check_close(z.cpu().numpy(), golden[f"f{k}_inv"], x, f"inv k={k} L={lanes}")
+        back = plan.inverse(y, cd)
+        check_close(back.cpu().numpy(), x, x, f"roundtrip k={k} L={lanes}")
+
+
+@pytest.mark.parametrize("config", [1, 2, 3, 5])
+def test_config_shapes_vs_oracle(cuda, oracle_mod, config):
+    from paper_2505_21728_b200.synth import make_workload
+    w = make_workload(config)
+    rows = 8192 if config != 5 else 2048
+    cls = w.make_classes(rows)
+    x = w.make_rows(rows, cls)
+    plan = _plan(w.models, w.perms)
+    inter_mask = ((1 << (w.cfg.rounds - 1)) - 1) if w.perms is not None else 0
+    full = None
+    if w.perms is not None:
+        full = np.concatenate([w.perms, np.tile(np.arange(w.n, dtype=np.uint16), (w.cfg.classes, 1, 1))], 1)
+    xh, ch = x.cpu().numpy(), cls.cpu().numpy()
+    ref_f = oracle_mod.apply_batch(w.cfg.log2_n, w.cfg.rounds, w.angles, full, inter_mask, xh, ch)
+    y = plan.forward(x, cls)
+    plan.sync_status()
+    check_close(y.cpu().numpy(), ref_f, xh, f"cfg{config} fwd ({plan.algorithm})")
+    ref_i = oracle_mod.apply_batch(w.cfg.log2_n, w.cfg.rounds, w.angles, full, inter_mask, xh, ch, inverse=True)
+    z = plan.inverse(x, cls)
+    check_close(z.cpu().numpy(), ref_i, xh, f"cfg{config} inv")
+    back = plan.inverse(y, cls)
+    check_close(back.cpu().numpy(), xh, xh, f"cfg{config} roundtrip")
+
+
+def test_edge_counts_inplace_and_identity(cuda):
+    from paper_2505_21728_b200 import HyGTModel, HyGTPlan
+    rng = np.random.default_rng(5)
+    m = HyGTModel(4, 2, rng.uniform(-np.pi, np.pi, 64))
+    plan = HyGTPlan(m)
+    for count in [0, 1, 31, 33, 1000]:
+        x = torch.from_numpy((rng.standard_normal((count, 16)) * 16).astype(np.float32)).to(cuda)
+        y = plan.forward(x)
+        if count:
+            xi = x.clone()
+            plan.forward(xi, out=xi)  # in place
+            assert torch.equal(xi, y)
+            back = plan.inverse(y)
+            check_close(back.cpu().numpy(), x.cpu().numpy(), x.cpu().numpy(), f"count={count}")
+    # zero-angle model is the identity, bit for bit (test_transform.cpp:118-124)
+    for standard in (False, True):
+        z = _plan([HyGTModel.zeros(6, 3)], standard=standard)
+        x = torch.randn(777, 64, device=cuda)
+        assert torch.equal(z.forward(x), x)
+        assert torch.equal(z.inverse(x), x)
+
+
+def test_quarter_turn_kats(cuda):
+    import math
+    from paper_2505_21728_b200 import forward, inverse, HyGTModel
+    y = forward(HyGTModel(1, 1, [math.pi / 2]), [1.0, 0.0])
+    assert abs(y[0]) < 1e-7 and abs(y[1] + 1) < 1e-7
+    y = forward(HyGTModel(2, 1, [math.pi / 2, math.pi / 2, 0, 0]), [1, 2, 3, 4])
+    np.testing.assert_allclose(y, [2, -1, 4, -3], atol=1e-6)
+    m = HyGTModel(1, 1, [0.0], [1, 0])  # permutation gathers by index (test_transform.cpp:196-202)
+    assert list(forward(m, [3.0, 4.0])) == [4.0, 3.0]
+    assert list(inverse(m, [4.0, 3.0])) == [3.0, 4.0]
+    with pytest.raises(Exception):
+        forward(HyGTModel.zeros(2, 1), [1.0, 2.0])
+
+
+def test_invalid_class_ids_raise(cuda):
+    from paper_2505_21728_b200 import ArgumentError, HyGTModel, HyGTPlan
+    rng = np.random.default_rng(9)
+    models = [HyGTModel(4, 2, rng.uniform(-3, 3, 64)) for _ in range(3)]
+    plan = HyGTPlan(models)
+    x = torch.randn(100, 16, device=cuda)
+    cls = torch.from_numpy(rng.integers(0, 3, 100).astype(np.uint16)).to(cuda)
+    plan.forward(x, cls)
+    plan.sync_status()
+    cls[17] = 3
+    plan.forward(x, cls)
+    with pytest.raises(ArgumentError):
+        plan.sync_status()
+    one = HyGTPlan(models[:1])
+    one.forward(x, cls)
+    with pytest.raises(ArgumentError):
+        one.sync_status()
+
+
+def test_bucketing_large_batch_roundtrip(cuda):
+    """Full config-2 size (2^24 rows, 1 GiB): size-independent properties -- round trip and
+    norm preservation -- through the multi-tile bucketing path."""
+    from paper_2505_21728_b200.synth import make_workload
+    w = make_workload(2)
+    cls = w.make_classes(w.cfg.count)
+    x = w.make_rows(w.cfg.count, cls)
+    plan = _plan(w.models, w.perms)
+    ws = torch.zeros(plan.workspace_bytes(w.cfg.count), dtype=torch.uint8, device=cuda)
+    y = plan.forward(x, cls, workspace=ws)
+    back = plan.inverse(y, cls, workspace=ws, reuse_buckets=True)
+    plan.sync_status(ws)
+    err = (back - x).abs().max().item()
+    assert err <= MAX_ABS * x.abs().max().item()
+    nx = x.double().pow(2).sum(1)
+    ny = y.double().pow(2).sum(1)
+    assert ((ny - nx).abs() / nx).max().item() < 1e-5
+    # a random sample of rows against the oracle
+    from oracle import oracle as O
+    idx = torch.randint(0, w.cfg.count, (4096,), device=cuda)
+    full = np.concatenate([w.perms, np.tile(np.arange(16, dtype=np.uint16), (35, 1, 1))], 1)
+    ref = O.apply_batch(4, 3, w.angles, full, 3, x[idx].cpu().numpy(), cls[idx].cpu().numpy())
+    check_close(y[idx].cpu().numpy(), ref, x[idx].cpu().numpy(), "cfg2 full-size sample")
+
+
+def test_energy_vs_oracle_and_full_size(cuda, oracle_mod, golden):
+    from paper_2505_21728_b200 import HyGTModel, HyGTPlan
+    log2n, rounds, classes = (int(v) for v in golden["en_meta"])
+    angles = golden["en_angles"]
+    plan = HyGTPlan([HyGTModel(log2n, rounds, angles[c]) for c in range(classes)])
+    x = torch.from_numpy(golden["en_x"]).to(cuda)
+    cls = torch.from_numpy(golden["en_cls"]).to(cuda)
+    e = torch.zeros(classes, 1 << log2n, dtype=torch.float64, device=cuda)
+    plan.forward_energy(x, cls, e)
+    np.testing.assert_allclose(e.cpu().numpy(), golden["en_energy"], rtol=1e-5, atol=1e-3)
+    # config 5 shape on a subset vs the oracle
+    from paper_2505_21728_b200.synth import make_workload
+    w = make_workload(5)
+    rows = 1 << 14
+    cls = w.make_classes(rows)
+    x = w.make_rows(rows, cls)
+    plan = HyGTPlan(w.models)
+    e = torch.zeros(35, 256, dtype=torch.float64, device=cuda)
+    plan.forward_energy(x, cls, e)
+    ref = oracle_mod.class_energy(8, 4, w.angles, None, 0, x.cpu().numpy(), cls.cpu().numpy())
+    np.testing.assert_allclose(e.cpu().numpy(), ref, rtol=1e-5)
+
+
+@pytest.mark.parametrize("k", range(7))
+def test_fixed_golden_bit_exact(cuda, golden, k):
+    from paper_2505_21728_b200 import ArgumentError, FixedPlan, QuantizedHyGTModel, TrigTable
+    log2n, rounds, b, p, with_perm = (int(v) for v in golden[f"x{k}_meta"])
+    perm = golden[f"x{k}_perm"] if with_perm else None
+    m = QuantizedHyGTModel(log2n, rounds, b, golden[f"x{k}_codes"], perm)
+    plan = FixedPlan(m, TrigTable(b, p))
+    x = golden[f"x{k}_x"]
+    st = golden[f"x{k}_fwd_status"]
+    xd = torch.from_numpy(x).to(cuda)
+    first = int(np.argmax(st != 0)) if (st != 0).any() else x.shape[0]
+    if first < x.shape[0]:
+        with pytest.raises(ArgumentError):
+            plan.forward(xd)
+        assert plan.first_bad == first
+    ok = np.nonzero(st == 0)[0]
+    y = plan.forward(torch.from_numpy(x[ok]).to(cuda)).cpu().numpy()
+    assert np.array_equal(y, golden[f"x{k}_fwd"][ok])
+    ist = golden[f"x{k}_inv_status"]
+    ok2 = np.nonzero((st == 0) & (ist == 0))[0]
+    z = plan.inverse(torch.from_numpy(golden[f"x{k}_fwd"][ok2]).to(cuda)).cpu().numpy()
+    assert np.array_equal(z, golden[f"x{k}_inv"][ok2])
+
+
+def test_fixed_random_multiclass_vs_oracle(cuda, oracle_mod):
+    from paper_2505_21728_b200 import FixedPlan, QuantizedHyGTModel, TrigTable
+    rng = np.random.default_rng(11)
+    for log2n, rounds, classes in [(4, 3, 35), (6, 4, 5), (8, 2, 3)]:
+        n = 1 << log2n
+        a = rounds * n * log2n // 2
+        codes = rng.integers(0, 256, (classes, a)).astype(np.uint16)
+        inter = np.stack([np.stack([rng.permutation(n) for _ in range(rounds - 1)]) for _ in range(classes)]).astype(np.uint16)
+        full = np.concatenate([inter, np.tile(np.arange(n, dtype=np.uint16), (classes, 1, 1))], 1)
+        x = rng.integers(-(1 << 20), (1 << 20) + 1, (3000, n)).astype(np.int64)
+        cls = rng.integers(0, classes, 3000).astype(np.uint16)
+        plan = FixedPlan([QuantizedHyGTModel(log2n, rounds, 8, codes[c]) for c in range(classes)],
+                         TrigTable(8, 10), inter)
+        y = plan.forward(torch.from_numpy(x).cuda(), torch.from_numpy(cls).cuda()).cpu().numpy()
+        st, bad, ref = oracle_mod.apply_batch_fixed(log2n, rounds, 8, 10, codes, full, (1 << (rounds - 1)) - 1, x, cls)
+        assert st == 0
+        assert np.array_equal(y, ref)
+        # inverse on legal inputs (forward outputs can exceed 2^20 at large N: compare status too)
+        st2, bad2, ref2 = oracle_mod.apply_batch_fixed(log2n, rounds, 8, 10, codes, full, (1 << (rounds - 1)) - 1, x, cls, inverse=True)
+        z = plan.inverse(torch.from_numpy(x).cuda(), torch.from_numpy(cls).cuda()).cpu().numpy()
+        assert np.array_equal(z, ref2)
+
+
+def test_klt_golden(cuda, golden):
+    from paper_2505_21728_b200 import KLTPlan
+    plan = KLTPlan(golden["klt_k"])
+    x = golden["klt_x"]
+    xd = torch.from_numpy(x).to(cuda)
+    cd = torch.from_numpy(golden["klt_cls"]).to(cuda)
+    check_close(plan.forward(xd, cd).cpu().numpy(), golden["klt_fwd"], x, "klt fwd")
+    check_close(plan.inverse(xd, cd).cpu().numpy(), golden["klt_inv"], x, "klt inv")
+
+
+def test_klt_config4_vs_oracle(cuda, oracle_mod):
+    from paper_2505_21728_b200 import KLTPlan
+    from paper_2505_21728_b200.synth import make_workload
+    w = make_workload(4)
+    k = w.klt_bases()
+    plan = KLTPlan(k)
+    cls = w.make_classes(8192)
+    x = w.make_rows(8192, cls)
+    y = plan.forward(x, cls)
+    ref = oracle_mod.klt_apply(k, x.cpu().numpy(), cls.cpu().numpy())
+    check_close(y.cpu().numpy(), ref, x.cpu().numpy(), "cfg4 klt fwd")
+    back = plan.inverse(y, cls)
+    check_close(back.cpu().numpy(), x.cpu().numpy(), x.cpu().numpy(), "cfg4 klt roundtrip")
