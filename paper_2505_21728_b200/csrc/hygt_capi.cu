@@ -17,6 +17,7 @@
 
 #include "../../include/hygt_gpu.h"
 #include "hygt_kernels.cuh"
+#include "hygt_tile.cuh"
 #include "hygt_plan.h"
 
 using namespace hygt_gpu;
@@ -75,6 +76,14 @@ struct hygt_plan {
   int32_t* d_cos = nullptr;
   int32_t* d_sin = nullptr;
   uint16_t* d_fgather[2] = {nullptr, nullptr};  // [C][R+1][N]
+  // tile path (N <= 32): lane-interleaved tables staged into shared memory by each CTA
+  bool tile = false;
+  int tile_l = 0, tile_vpt = 1;
+  uint32_t tile_rows = 8192;
+  float4* d_tcoef[2] = {nullptr, nullptr};
+  uint32_t tunits[2] = {0, 0};
+  uint4* d_tgidx[2] = {nullptr, nullptr};
+  size_t tile_smem[2] = {0, 0};
   unsigned long long* d_fixed_err = nullptr;
   std::mutex* fixed_mu = nullptr;
 };
@@ -98,6 +107,8 @@ void free_plan(hygt_plan* p) {
     cudaFree(p->d_coef[d]);
     cudaFree(p->d_gidx[d]);
     cudaFree(p->d_fgather[d]);
+    cudaFree(p->d_tcoef[d]);
+    cudaFree(p->d_tgidx[d]);
   }
   cudaFree(p->d_codes);
   cudaFree(p->d_cos);
@@ -337,6 +348,145 @@ size_t apply_smem(const hygt_plan* p, int dir) {
   return (size_t)(APPLY_THREADS / 32) * 32 * (1u << p->log2n) / (1u << p->lanes_log2) * sizeof(float);
 }
 
+
+// ---- tile path --------------------------------------------------------------------------
+using TileFn = void (*)(TileParams);
+
+template <int LOG2N, int L, int VPT>
+TileFn pick_tile(bool standard, bool fwd, bool energy) {
+  if (standard) {
+    if (!fwd) return hygt_tile_kernel<LOG2N, L, VPT, true, false, false>;
+    return energy ? hygt_tile_kernel<LOG2N, L, VPT, true, true, true>
+                  : hygt_tile_kernel<LOG2N, L, VPT, true, true, false>;
+  }
+  if (!fwd) return hygt_tile_kernel<LOG2N, L, VPT, false, false, false>;
+  return energy ? hygt_tile_kernel<LOG2N, L, VPT, false, true, true>
+                : hygt_tile_kernel<LOG2N, L, VPT, false, true, false>;
+}
+
+// Instantiated (log2 N, log2 TPV, rows per lane group) tile layouts; the first of each N is the
+// default. All have E = N / TPV >= 4.
+TileFn select_tile(int log2n, int l, int vpt, bool standard, bool fwd, bool energy) {
+  switch (log2n * 256 + l * 16 + vpt) {
+    case 2 * 256 + 0 * 16 + 4: return pick_tile<2, 0, 4>(standard, fwd, energy);
+    case 3 * 256 + 1 * 16 + 4: return pick_tile<3, 1, 4>(standard, fwd, energy);
+    case 3 * 256 + 0 * 16 + 2: return pick_tile<3, 0, 2>(standard, fwd, energy);
+    case 4 * 256 + 2 * 16 + 4: return pick_tile<4, 2, 4>(standard, fwd, energy);
+    case 4 * 256 + 2 * 16 + 2: return pick_tile<4, 2, 2>(standard, fwd, energy);
+    case 4 * 256 + 1 * 16 + 2: return pick_tile<4, 1, 2>(standard, fwd, energy);
+    case 4 * 256 + 0 * 16 + 1: return pick_tile<4, 0, 1>(standard, fwd, energy);
+    case 5 * 256 + 2 * 16 + 2: return pick_tile<5, 2, 2>(standard, fwd, energy);
+    case 5 * 256 + 3 * 16 + 4: return pick_tile<5, 3, 4>(standard, fwd, energy);
+    default: return nullptr;
+  }
+}
+
+void default_tile_layout(int log2n, int* l, int* vpt) {
+  switch (log2n) {
+    case 2: *l = 0; *vpt = 4; break;
+    case 3: *l = 1; *vpt = 4; break;
+    case 4: *l = 2; *vpt = 4; break;
+    case 5: *l = 2; *vpt = 2; break;
+    default: *l = -1; *vpt = 0;
+  }
+}
+
+int tile_scratch_floats(int log2n, int l, int vpt) {
+  const int n = 1 << log2n, tpv = 1 << l, v = 32 / tpv, rows = v * vpt;
+  const int want = (v / 4) % 8;
+  return n * (rows + ((want - rows % 8) % 8 + 8) % 8);
+}
+
+int run_tile(const hygt_plan* p, int dir, const float* x, float* y, const uint16_t* d_cls,
+             uint64_t count, double* energy, uint32_t* err, cudaStream_t st) {
+  TileFn fn = select_tile(p->log2n, p->tile_l, p->tile_vpt, p->algo == 0, dir == 0, energy != nullptr);
+  if (!fn) return fail(HYGT_ERR_ARGUMENT, "hygt: no tile kernel for this layout");
+  TileParams P{};
+  P.x = x;
+  P.y = y;
+  P.cls = d_cls;
+  P.count = count;
+  P.classes = p->classes;
+  P.rounds = p->rounds;
+  P.coef = p->d_tcoef[dir];
+  P.units = p->tunits[dir];
+  P.gidx = p->d_tgidx[dir];
+  P.gmask = p->gmask[dir];
+  P.tile_rows = p->tile_rows;
+  P.energy = energy;
+  P.err = err;
+  int occ = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, p->tile_smem[dir]));
+  if (occ < 1) return fail(HYGT_ERR_CUDA, "hygt: tile kernel does not fit on an SM");
+  const uint64_t tiles = (count + p->tile_rows - 1) / p->tile_rows;
+  const uint64_t ctas = std::min<uint64_t>(tiles, (uint64_t)p->num_sms * occ);
+  fn<<<(unsigned)ctas, 256, p->tile_smem[dir], st>>>(P);
+  CU(cudaGetLastError());
+  return ok();
+}
+
+int setup_tile(hygt_plan* p, const double* angles, const uint16_t* perms) {
+  int l = -1, vpt = 0;
+  default_tile_layout(p->log2n, &l, &vpt);
+  const int el = env_int("HYGT_TILE_L", -1), ev = env_int("HYGT_TILE_VPT", -1);
+  if (el >= 0 && ev > 0 && select_tile(p->log2n, el, ev, false, true, false)) {
+    l = el;
+    vpt = ev;
+  }
+  if (l < 0 || env_int("HYGT_TILE", 1) == 0) return HYGT_OK;
+  const Layout ly{p->log2n, l};
+  const int tpv = ly.tpv(), e = ly.e();
+  const int rows = env_int("HYGT_TILE_ROWS", 8192);
+  size_t smem_max = 0;
+  for (int d = 0; d < 2; ++d) {
+    DirTables t;
+    if (!build_direction(ly, p->rounds, p->classes, angles, perms, p->perm_mask, d == 0, p->algo == 0, t))
+      return HYGT_OK;  // (cannot happen: algo already chosen) -- stay on the generic path
+    const uint32_t units = t.stream_len / 2;
+    std::vector<float4> il((size_t)p->classes * units * tpv);
+    for (int c = 0; c < p->classes; ++c)
+      for (int lt = 0; lt < tpv; ++lt)
+        for (uint32_t u = 0; u < units; ++u) {
+          const Float2* w = &t.coef[((size_t)c * tpv + lt) * t.stream_len + 2 * u];
+          il[((size_t)c * units + u) * tpv + lt] = make_float4(w[0].x, w[0].y, w[1].x, w[1].y);
+        }
+    const int words = (e + 7) / 8;
+    std::vector<uint4> gi;
+    if (t.gmask) {
+      gi.assign((size_t)p->classes * (p->rounds + 1) * words * tpv, make_uint4(0, 0, 0, 0));
+      for (int c = 0; c < p->classes; ++c)
+        for (int k = 0; k <= p->rounds; ++k)
+          for (int lt = 0; lt < tpv; ++lt) {
+            const uint16_t* src = &t.gidx[(((size_t)c * (p->rounds + 1) + k) * tpv + lt) * e];
+            for (int w = 0; w < words; ++w) {
+              uint32_t q[4] = {0, 0, 0, 0};
+              for (int h = 0; h < 8 && 8 * w + h < e; ++h)
+                q[h / 2] |= (uint32_t)src[8 * w + h] << (16 * (h & 1));
+              gi[(((size_t)c * (p->rounds + 1) + k) * words + w) * tpv + lt] = make_uint4(q[0], q[1], q[2], q[3]);
+            }
+          }
+    }
+    int s = upload(&p->d_tcoef[d], il.data(), il.size());
+    if (!s && !gi.empty()) s = upload(&p->d_tgidx[d], gi.data(), gi.size());
+    if (s) return s;
+    p->tunits[d] = units;
+    p->tile_smem[d] = tile_smem_bytes(il.size() * sizeof(float4), gi.size() * sizeof(uint4),
+                                      p->classes, rows, 8, tile_scratch_floats(p->log2n, l, vpt));
+    smem_max = std::max(smem_max, p->tile_smem[d]);
+  }
+  if (smem_max > 200 * 1024) return HYGT_OK;  // tables too large: generic path
+  for (int d = 0; d < 2; ++d)
+    for (int en = 0; en < 2; ++en) {
+      TileFn fn = select_tile(p->log2n, l, vpt, p->algo == 0, d == 0, en == 1);
+      if (fn) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->tile_smem[d]);
+    }
+  p->tile = true;
+  p->tile_l = l;
+  p->tile_vpt = vpt;
+  p->tile_rows = (uint32_t)rows;
+  return HYGT_OK;
+}
+
 int run_apply(const hygt_plan* p, int dir, const float* x, float* y, const uint16_t* d_cls,
               uint64_t count, double* energy, void* d_ws, size_t ws_bytes, uint32_t flags,
               cudaStream_t st) {
@@ -344,8 +494,13 @@ int run_apply(const hygt_plan* p, int dir, const float* x, float* y, const uint1
   if (count == 0) return ok();
   if (!x || !y) return fail(HYGT_ERR_ARGUMENT, "hygt: null data pointer");
   if (count > 0xFFFFFFFFull) return fail(HYGT_ERR_ARGUMENT, "hygt: at most 2^32-1 rows per call");
-  const bool bucketed = d_cls && p->classes > 1;
   const WsLayout w = ws_layout(p->classes, p->chunk_rows, count);
+  if (p->tile) {
+    if (d_cls && (!d_ws || ws_bytes < 256)) return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
+    return run_tile(p, dir, x, y, d_cls, count, energy,
+                    d_cls ? reinterpret_cast<uint32_t*>(static_cast<char*>(d_ws) + w.err) : nullptr, st);
+  }
+  const bool bucketed = d_cls && p->classes > 1;
   if (d_cls) {
     if (!d_ws || ws_bytes < w.total) return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
     if (!(flags & HYGT_REUSE_BUCKETS)) {
@@ -457,6 +612,10 @@ extern "C" int hygt_plan_create(int log2_n, int rounds, int class_count, const d
       if (fn && apply_smem(p, d) > 48 * 1024)
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)apply_smem(p, d));
   }
+  if (int s = setup_tile(p, angles, perms)) {
+    free_plan(p);
+    return s;
+  }
   *out = p;
   return ok();
 }
@@ -470,12 +629,14 @@ extern "C" int hygt_plan_algorithm(const hygt_plan* plan) { return plan ? plan->
 
 extern "C" size_t hygt_workspace_bytes(const hygt_plan* plan, uint64_t count) {
   if (!plan) return 0;
+  if (plan->tile) return 256;
   return ws_layout(plan->classes, plan->chunk_rows, count).total;
 }
 
 extern "C" int hygt_bucket(const hygt_plan* plan, const uint16_t* d_cls, uint64_t count,
                            void* d_ws, size_t ws_bytes, void* stream) {
   if (!plan) return fail(HYGT_ERR_ARGUMENT, "hygt_bucket: null plan");
+  if (plan->tile) return ok();  // tile plans sort each tile in shared memory
   return run_bucket(plan, plan->classes, plan->chunk_rows, d_cls, count, d_ws, ws_bytes,
                     as_stream(stream));
 }

@@ -1,0 +1,396 @@
+// hygt_tile.cuh -- the "tile" HyGT kernel for short rows (N <= 32, all class tables fit in shared
+// memory): the production path of BASELINE configs 1 and 2.
+//
+// Per CTA (persistent, grid-stride over tiles of T rows):
+//   1. the direction's coefficient / scale / gather tables of ALL classes are staged once into
+//      shared memory (lane-interleaved so the TPV lanes of a row read one contiguous 16*TPV-byte
+//      run: one shared-memory wavefront per warp load when the warp is class-uniform);
+//   2. each tile's class ids are counting-sorted in shared memory (warp-aggregated atomics) --
+//      the batched equivalent of run_apply's cache[b.class_id] dispatch (hygt_main.cpp:143-149)
+//      without any index array in HBM;
+//   3. warps walk the sorted positions, VPT rows per lane-group, gathering rows from HBM with
+//      128-bit loads (a row is TPV consecutive lanes: coalesced), running all rounds in registers
+//      (packed FFMA2 butterflies, __shfl_xor_sync for the lane bits, bank-swizzled scratch for
+//      the permutations) and streaming the rows back.
+// The VPT rows of a lane group share every coefficient load when they have the same class
+// (always, except at class-run boundaries where a per-row fallback runs).
+#pragma once
+
+#include "hygt_kernels.cuh"
+
+namespace hygt_gpu {
+
+struct TileParams {
+  const float* x;
+  float* y;
+  const uint16_t* cls;      // nullptr: single class
+  uint64_t count;
+  int classes;
+  int rounds;
+  const float4* coef;       // [C][units][TPV] float4, units = stream_len / 2
+  uint32_t units;           // float4 units per lane stream
+  const uint4* gidx;        // [C][R+1][E/8][TPV] uint4 (8 u16 gather sources per uint4)
+  uint64_t gmask;
+  uint32_t tile_rows;       // T
+  double* energy;           // [C][N] (forward + energy)
+  uint32_t* err;            // class id out of range flag
+};
+
+template <int LOG2N, int L>
+struct TileGeom {
+  static constexpr Layout LY{LOG2N, L};
+  static constexpr int N = LY.n(), TPV = LY.tpv(), E = LY.e(), CH = LY.ch(), NP = E / 2;
+  static constexpr int V = 32 / TPV;  // rows per warp per VPT slot
+  // Scratch row stride (floats) for VPT rows per lane group: ROWS = V * VPT row slots, padded so
+  // that S * 4 == V (mod 32) -- the 32 lanes' stores of one register slot then land in 32
+  // distinct banks (lane bits of the element index times S*4 fill the banks V apart).
+  template <int VPT>
+  HYGT_HD static constexpr int stride() {
+    constexpr int rows = V * VPT;
+    constexpr int want = (V / 4) % 8;
+    return rows + ((want - rows % 8) % 8 + 8) % 8 + (TPV == 1 ? 0 : 0);
+  }
+};
+
+// One pass on VPT rows. SHARED: all VPT rows share the coefficient stream cp[0].
+template <int LOG2N, int L, bool STD, int P, int VPT, bool SHARED>
+__device__ __forceinline__ void tile_pass(float2 (&v)[VPT][TileGeom<LOG2N, L>::NP],
+                                          const float4* (&cp)[VPT]) {
+  using G = TileGeom<LOG2N, L>;
+  constexpr Layout LY = G::LY;
+  constexpr int NP = G::NP, TPV = G::TPV;
+  auto ld = [&](int r, int u) -> float4 { return cp[SHARED ? 0 : r][u * TPV]; };
+  if constexpr (LY.cross(P)) {
+    constexpr int LM = LY.lane_mask(P);
+    if constexpr (!STD) {
+#pragma unroll
+      for (int k = 0; k < NP; k += 2) {
+        float4 q = ld(0, k / 2);
+#pragma unroll
+        for (int r = 0; r < VPT; ++r) {
+          if (!SHARED && r) q = ld(r, k / 2);
+          const float2 w0 = make_float2(__shfl_xor_sync(0xffffffffu, v[r][k].x, LM),
+                                        __shfl_xor_sync(0xffffffffu, v[r][k].y, LM));
+          const float2 w1 = make_float2(__shfl_xor_sync(0xffffffffu, v[r][k + 1].x, LM),
+                                        __shfl_xor_sync(0xffffffffu, v[r][k + 1].y, LM));
+          v[r][k] = ffma2(make_float2(q.x, q.y), w0, v[r][k]);
+          v[r][k + 1] = ffma2(make_float2(q.z, q.w), w1, v[r][k + 1]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < VPT; ++r) cp[r] += (NP / 2) * TPV;
+    } else {
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        float4 q = ld(0, k);
+#pragma unroll
+        for (int r = 0; r < VPT; ++r) {
+          if (!SHARED && r) q = ld(r, k);
+          const float2 w0 = make_float2(__shfl_xor_sync(0xffffffffu, v[r][k].x, LM),
+                                        __shfl_xor_sync(0xffffffffu, v[r][k].y, LM));
+          v[r][k] = ffma2(make_float2(q.x, q.y), v[r][k], fmul2(make_float2(q.z, q.w), w0));
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < VPT; ++r) cp[r] += NP * TPV;
+    }
+  } else if constexpr (P == 0) {
+#pragma unroll
+    for (int k = 0; k < NP; k += 2) {
+      float4 q = ld(0, k / 2);
+#pragma unroll
+      for (int r = 0; r < VPT; ++r) {
+        if (!SHARED && r) q = ld(r, k / 2);
+        if constexpr (!STD) {
+          v[r][k] = ffma2(make_float2(q.x, q.y), swap2(v[r][k]), v[r][k]);
+          v[r][k + 1] = ffma2(make_float2(q.z, q.w), swap2(v[r][k + 1]), v[r][k + 1]);
+        } else {
+          v[r][k] = ffma2(make_float2(q.x, q.x), v[r][k], fmul2(make_float2(q.y, -q.y), swap2(v[r][k])));
+          v[r][k + 1] = ffma2(make_float2(q.z, q.z), v[r][k + 1],
+                              fmul2(make_float2(q.w, -q.w), swap2(v[r][k + 1])));
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < VPT; ++r) cp[r] += (NP / 2) * TPV;
+  } else {
+    constexpr int SO = LY.slot_stride(P) / 2;
+    int u = 0;
+#pragma unroll
+    for (int a = 0; a < NP; ++a) {
+      if ((a & SO) == 0) {
+        float4 q = ld(0, u);
+#pragma unroll
+        for (int r = 0; r < VPT; ++r) {
+          if (!SHARED && r) q = ld(r, u);
+          const float2 xa = v[r][a], xb = v[r][a + SO];
+          if constexpr (!STD) {
+            v[r][a] = ffma2(make_float2(q.x, q.y), xb, xa);
+            v[r][a + SO] = ffma2(make_float2(q.z, q.w), xa, xb);
+          } else {
+            const float2 c = make_float2(q.x, q.y), s = make_float2(q.z, q.w);
+            v[r][a] = ffma2(c, xa, fmul2(s, xb));
+            v[r][a + SO] = ffma2(c, xb, fmul2(neg2(s), xa));
+          }
+        }
+        ++u;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < VPT; ++r) cp[r] += (NP / 2) * TPV;
+  }
+}
+
+template <int LOG2N, int L, bool STD, bool FWD, int VPT, bool SHARED, int PP>
+__device__ __forceinline__ void tile_round(float2 (&v)[VPT][TileGeom<LOG2N, L>::NP],
+                                          const float4* (&cp)[VPT]) {
+  if constexpr (PP < LOG2N) {
+    constexpr int P = FWD ? PP : LOG2N - 1 - PP;
+    tile_pass<LOG2N, L, STD, P, VPT, SHARED>(v, cp);
+    tile_round<LOG2N, L, STD, FWD, VPT, SHARED, PP + 1>(v, cp);
+  }
+}
+
+// Gather v[r][s] <- pre[G[elem(t, s)]] through per-row scratch rows. Scratch is laid out
+// [element][row slot] with a per-lane-group xor so one slot's stores of the 32 lanes hit
+// distinct banks; gp[r] points at the lane's interleaved uint4 gather words.
+template <int LOG2N, int L, int VPT>
+__device__ __forceinline__ void tile_gather(float2 (&v)[VPT][TileGeom<LOG2N, L>::NP],
+                                            float* scratch, int g, int t,
+                                            const uint4* (&gp)[VPT]) {
+  using G = TileGeom<LOG2N, L>;
+  constexpr Layout LY = G::LY;
+  constexpr int E = G::E, TPV = G::TPV, V = G::V;
+  constexpr int ROWS = G::template stride<VPT>();
+  // element i of row slot (r, g) lives at scratch[i * ROWS + (r * V + g)] (see stride()).
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < VPT; ++r)
+#pragma unroll
+    for (int s = 0; s < E; s += 2) {
+      scratch[LY.elem(t, s) * ROWS + r * V + g] = v[r][s / 2].x;
+      scratch[LY.elem(t, s + 1) * ROWS + r * V + g] = v[r][s / 2].y;
+    }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < VPT; ++r) {
+    if constexpr (E % 8 == 0) {
+#pragma unroll
+      for (int s = 0; s < E; s += 8) {
+        const uint4 q = gp[r][(s / 8) * TPV];
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          v[r][s / 2 + h].x = scratch[(w[h] & 0xffffu) * ROWS + r * V + g];
+          v[r][s / 2 + h].y = scratch[(w[h] >> 16) * ROWS + r * V + g];
+        }
+      }
+    } else {
+      // E == 4: one uint2 worth of indices, stored in the .x/.y of the uint4 word
+      const uint4 q = gp[r][0];
+      v[r][0].x = scratch[(q.x & 0xffffu) * ROWS + r * V + g];
+      v[r][0].y = scratch[(q.x >> 16) * ROWS + r * V + g];
+      v[r][1].x = scratch[(q.y & 0xffffu) * ROWS + r * V + g];
+      v[r][1].y = scratch[(q.y >> 16) * ROWS + r * V + g];
+    }
+  }
+}
+
+template <int LOG2N, int L, bool STD, bool FWD, int VPT, bool SHARED>
+__device__ __forceinline__ void tile_rows(float2 (&v)[VPT][TileGeom<LOG2N, L>::NP],
+                                          const float4* (&cp)[VPT], const uint4* (&g0)[VPT],
+                                          uint32_t gstep_words, float* scratch, int g, int t,
+                                          const TileParams& P) {
+  const uint4* gp[VPT];
+#pragma unroll
+  for (int r = 0; r < VPT; ++r) gp[r] = g0[r];
+  if (P.gmask & 1ull) tile_gather<LOG2N, L, VPT>(v, scratch, g, t, gp);
+  for (int rr = 0; rr < P.rounds; ++rr) {
+    tile_round<LOG2N, L, STD, FWD, VPT, SHARED, 0>(v, cp);
+    if ((P.gmask >> (rr + 1)) & 1ull) {
+#pragma unroll
+      for (int r = 0; r < VPT; ++r) gp[r] = g0[r] + (size_t)(rr + 1) * gstep_words;
+      tile_gather<LOG2N, L, VPT>(v, scratch, g, t, gp);
+    }
+  }
+  if constexpr (!STD) {
+    using G = TileGeom<LOG2N, L>;
+#pragma unroll
+    for (int k = 0; k < G::NP; k += 2) {
+      float4 q = cp[0][(k / 2) * G::TPV];
+#pragma unroll
+      for (int r = 0; r < VPT; ++r) {
+        if (!SHARED && r) q = cp[r][(k / 2) * G::TPV];
+        v[r][k] = fmul2(v[r][k], make_float2(q.x, q.y));
+        v[r][k + 1] = fmul2(v[r][k + 1], make_float2(q.z, q.w));
+      }
+    }
+  }
+}
+
+// Shared-memory footprint of one CTA (bytes), given the table sizes.
+HYGT_HD constexpr size_t tile_smem_bytes(size_t coef_bytes, size_t gidx_bytes, int classes,
+                                         int tile_rows, int warps, int scratch_floats_per_warp) {
+  return ((coef_bytes + 15) & ~size_t(15)) + ((gidx_bytes + 15) & ~size_t(15)) +
+         ((size_t)(classes + 2) * 4 + 15) / 16 * 16 +     // run offsets
+         ((size_t)tile_rows * 2 + 15) / 16 * 16 +          // sorted local row index (u16)
+         ((size_t)tile_rows * 2 + 15) / 16 * 16 +          // class of each sorted position (u16)
+         (size_t)warps * scratch_floats_per_warp * 4;
+}
+
+template <int LOG2N, int L, int VPT, bool STD, bool FWD, bool ENERGY>
+__global__ void __launch_bounds__(256) hygt_tile_kernel(const TileParams P) {
+  using G = TileGeom<LOG2N, L>;
+  constexpr Layout LY = G::LY;
+  constexpr int N = G::N, TPV = G::TPV, E = G::E, CH = G::CH, NP = G::NP, V = G::V;
+  constexpr int ROWS = V * VPT;  // rows per warp step
+  constexpr int WARPS = 8;
+  constexpr int SCR = N * G::template stride<VPT>();  // scratch floats per warp
+  extern __shared__ __align__(16) unsigned char tile_smem[];
+  const int C = P.classes;
+  const int T = (int)P.tile_rows;
+  const size_t coef_words = (size_t)C * P.units * TPV;  // float4
+  const size_t gidx_words = P.gmask ? (size_t)C * (P.rounds + 1) * ((E + 7) / 8) * TPV : 0;
+  float4* s_coef = reinterpret_cast<float4*>(tile_smem);
+  uint4* s_gidx = reinterpret_cast<uint4*>(s_coef + coef_words);
+  uint32_t* s_off = reinterpret_cast<uint32_t*>(s_gidx + gidx_words);  // [C+2]
+  uint16_t* s_order = reinterpret_cast<uint16_t*>(s_off + ((C + 2 + 3) & ~3));
+  uint16_t* s_pcls = s_order + ((T + 7) & ~7);
+  float* s_scratch = reinterpret_cast<float*>(s_pcls + ((T + 7) & ~7));
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> L, t = lane & (TPV - 1);
+  float* scratch = s_scratch + (size_t)warp * SCR;
+
+  // ---- stage the direction's tables (once per CTA)
+  for (size_t i = tid; i < coef_words; i += blockDim.x) s_coef[i] = __ldg(P.coef + i);
+  for (size_t i = tid; i < gidx_words; i += blockDim.x) s_gidx[i] = __ldg(P.gidx + i);
+  const uint32_t gstep_words = ((E + 7) / 8) * TPV;  // uint4 words per gather step
+  const uint64_t tiles = (P.count + T - 1) / T;
+
+  for (uint64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const uint64_t row0 = tile * T;
+    const int rows = (int)((P.count - row0) < (uint64_t)T ? (P.count - row0) : (uint64_t)T);
+    __syncthreads();  // previous tile fully consumed (and tables staged on the first pass)
+    // ---- counting sort of the tile by class (bin C = invalid id)
+    if (P.cls && C > 1) {
+      for (int i = tid; i < C + 2; i += blockDim.x) s_off[i] = 0;
+      __syncthreads();
+      for (int i = tid; i < rows; i += blockDim.x) {
+        int c = P.cls[row0 + i];
+        if (c >= C) c = C;
+        const unsigned peers = __match_any_sync(__activemask(), c);
+        if (lane == __ffs(peers) - 1) atomicAdd(&s_off[c + 1], __popc(peers));
+      }
+      __syncthreads();
+      if (warp == 0) {  // exclusive scan of C+1 counts (in place, s_off[0] = 0)
+        uint32_t carry = 0;
+        for (int base = 1; base < C + 2; base += 32) {
+          const int i = base + lane;
+          uint32_t v0 = i < C + 2 ? s_off[i] : 0;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t n = __shfl_up_sync(0xffffffffu, v0, o);
+            if (lane >= o) v0 += n;
+          }
+          if (i < C + 2) s_off[i] = v0 + carry;
+          carry += __shfl_sync(0xffffffffu, v0, 31);
+        }
+      }
+      __syncthreads();
+      for (int i = tid; i < rows; i += blockDim.x) {
+        int c = P.cls[row0 + i];
+        if (c >= C) {
+          c = C;
+          atomicOr(P.err, 1u);
+        }
+        const unsigned peers = __match_any_sync(__activemask(), c);
+        const int leader = __ffs(peers) - 1;
+        uint32_t b = 0;
+        if (lane == leader) b = atomicAdd(&s_off[c], __popc(peers));
+        b = __shfl_sync(peers, b, leader) + __popc(peers & ((1u << lane) - 1u));
+        s_order[b] = (uint16_t)i;
+        s_pcls[b] = (uint16_t)c;
+      }
+      __syncthreads();
+    }
+
+    // ---- process sorted positions: each warp takes ROWS consecutive positions per step
+    for (int p0 = warp * ROWS; p0 < rows; p0 += WARPS * ROWS) {
+      int cl[VPT];
+      uint32_t lr[VPT];
+      bool act[VPT];
+#pragma unroll
+      for (int r = 0; r < VPT; ++r) {
+        const int p = p0 + r * V + g;
+        act[r] = p < rows;
+        const bool sorted = P.cls && C > 1;
+        lr[r] = act[r] ? (sorted ? s_order[p] : (uint32_t)p) : 0u;
+        cl[r] = act[r] ? (sorted ? (int)s_pcls[p] : (P.cls ? (int)P.cls[row0 + p] : 0)) : 0;
+        if (!sorted && cl[r] >= C) {
+          cl[r] = C;
+          atomicOr(P.err, 1u);
+        }
+      }
+      float2 v[VPT][NP];
+#pragma unroll
+      for (int r = 0; r < VPT; ++r) {
+        const float* xr = P.x + (row0 + lr[r]) * N;
+#pragma unroll
+        for (int u = 0; u < E / CH; ++u) {
+          const int q = t + TPV * u;
+          if (act[r]) {
+            const float4 a = __ldcs(reinterpret_cast<const float4*>(xr) + q);
+            v[r][2 * u] = make_float2(a.x, a.y);
+            v[r][2 * u + 1] = make_float2(a.z, a.w);
+          } else {
+            v[r][2 * u] = v[r][2 * u + 1] = make_float2(0.f, 0.f);
+          }
+        }
+      }
+      const float4* cp[VPT];
+      const uint4* gp[VPT];
+      bool same = true;
+#pragma unroll
+      for (int r = 0; r < VPT; ++r) {
+        const int c = cl[r] < C ? cl[r] : 0;
+        cp[r] = s_coef + (size_t)c * P.units * TPV + t;
+        gp[r] = s_gidx + (size_t)c * (P.rounds + 1) * gstep_words + t;
+        same &= (c == (cl[0] < C ? cl[0] : 0));
+      }
+      if (__all_sync(0xffffffffu, same))
+        tile_rows<LOG2N, L, STD, FWD, VPT, true>(v, cp, gp, gstep_words, scratch, g, t, P);
+      else
+        tile_rows<LOG2N, L, STD, FWD, VPT, false>(v, cp, gp, gstep_words, scratch, g, t, P);
+
+#pragma unroll
+      for (int r = 0; r < VPT; ++r) {
+        if (!act[r]) continue;
+        const size_t row = row0 + lr[r];
+        float* yr = P.y + row * N;
+        const float* xr = P.x + row * N;
+#pragma unroll
+        for (int u = 0; u < E / CH; ++u) {
+          const int q = t + TPV * u;
+          if (cl[r] >= C)  // invalid class id: pass the row through (error flagged)
+            reinterpret_cast<float4*>(yr)[q] = reinterpret_cast<const float4*>(xr)[q];
+          else
+            __stcs(reinterpret_cast<float4*>(yr) + q,
+                   make_float4(v[r][2 * u].x, v[r][2 * u].y, v[r][2 * u + 1].x, v[r][2 * u + 1].y));
+        }
+        if constexpr (ENERGY) {
+          if (cl[r] < C) {
+            double* e = P.energy + (size_t)cl[r] * N;
+#pragma unroll
+            for (int k = 0; k < NP; ++k) {
+              atomicAdd(e + LY.elem(t, 2 * k), (double)(v[r][k].x * v[r][k].x));
+              atomicAdd(e + LY.elem(t, 2 * k + 1), (double)(v[r][k].y * v[r][k].y));
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+}  // namespace hygt_gpu

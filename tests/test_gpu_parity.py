@@ -52,6 +52,18 @@ def _inter(perms, mask, rounds):
 
 
 LAYOUTS = {1: [0], 2: [0], 3: [0], 4: [0, 2], 5: [0], 6: [0, 1, 2], 7: [2], 8: [1, 2]}
+# tile-path layouts (log2 TPV, rows per lane group) for N <= 32; the generic kernel runs with
+# HYGT_TILE=0.
+TILE_LAYOUTS = {2: [(0, 4)], 3: [(1, 4), (0, 2)], 4: [(2, 4), (2, 2), (1, 2), (0, 1)],
+                5: [(2, 2), (3, 4)]}
+
+
+def _variants(log2n):
+    out = [{"HYGT_TILE": "0", "HYGT_LANES_LOG2": str(l)} for l in LAYOUTS[log2n]]
+    for l, v in TILE_LAYOUTS.get(log2n, []):
+        out.append({"HYGT_TILE": "1", "HYGT_TILE_L": str(l), "HYGT_TILE_VPT": str(v),
+                    "HYGT_TILE_ROWS": "64"})  # tiny tiles: many tiles, sort + tails exercised
+    return out
 
 
 @pytest.mark.parametrize("standard", [False, True])
@@ -62,8 +74,10 @@ def test_golden_float_all_layouts(cuda, golden, k, standard, monkeypatch):
     x, cls = golden[f"f{k}_x"], golden[f"f{k}_cls"]
     xd = torch.from_numpy(x).to(cuda)
     cd = torch.from_numpy(cls).to(cuda)
-    for lanes in LAYOUTS[log2n]:
-        monkeypatch.setenv("HYGT_LANES_LOG2", str(lanes))
+    for env in _variants(log2n):
+        for k_, v_ in env.items():
+            monkeypatch.setenv(k_, v_)
+        lanes = env
         plan = _plan(_models(log2n, rounds, angles, perms, mask), _inter(perms, mask, rounds), standard)
         y = plan.forward(xd, cd)
         plan.sync_status()
@@ -175,7 +189,7 @@ def test_bucketing_large_batch_roundtrip(cuda):
     from oracle import oracle as O
     idx = torch.randint(0, w.cfg.count, (4096,), device=cuda)
     full = np.concatenate([w.perms, np.tile(np.arange(16, dtype=np.uint16), (35, 1, 1))], 1)
-    ref = O.apply_batch(4, 3, w.angles, full, 3, x[idx].cpu().numpy(), cls[idx].cpu().numpy())
+    ref = O.apply_batch(4, 3, w.angles, full, 3, x[idx].cpu().numpy(), cls.to(torch.int32)[idx].cpu().numpy().astype(np.uint16))
     check_close(y[idx].cpu().numpy(), ref, x[idx].cpu().numpy(), "cfg2 full-size sample")
 
 
