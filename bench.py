@@ -279,9 +279,9 @@ def impl_ours(args):
     achieved = rows * bpr / (launch_ms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": None,
-                "kernel": "hygt_apply_kernel (forward / inverse)",
+                "kernel": f"{plan.path} kernel (forward / inverse), class bucketing included",
                 "bytes_per_launch": rows * bpr, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({hbm_kind})"}
-    launches_per_step = 3 + 2  # hist, scan, scatter, forward, inverse
+    launches_per_step = plan.launches_per_step()
 
     e2e = None
     if not args.no_e2e:
@@ -305,7 +305,8 @@ def impl_ours(args):
                        "inter_round_perms": w.perms is not None,
                        "step": "class bucketing + forward + inverse",
                        "l2": "inputs larger than L2 (>=1 GiB per array) and a 256 MiB L2 flush between steps",
-                       "parallelism": f"dp{world}", "algorithm": plan.algorithm},
+                       "parallelism": f"dp{world}", "algorithm": plan.algorithm,
+                       "kernel_path": plan.path},
             "breakdown_ms": {"bucket": t_bucket, "forward": t_fwd, "inverse": t_inv},
             "roofline": roofline,
             "clocks": clocks.summary(),

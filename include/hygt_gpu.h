@@ -80,6 +80,10 @@ int hygt_plan_create(int log2_n, int rounds, int class_count, const double* angl
 int hygt_plan_destroy(hygt_plan* plan);
 /* 0 = standard rotations, 1 = scale-folded (fast Givens) form chosen at plan time. */
 int hygt_plan_algorithm(const hygt_plan* plan);
+/* Kernel family serving the plan: 0 = bucketed apply kernel (hygt_bucket + per-row gather),
+ * 1 = tile kernel (class sort inside each CTA, no bucketing pass; N <= 32),
+ * 2 = class-segment kernel (global class buckets, one class table staged per CTA segment). */
+int hygt_plan_path(const hygt_plan* plan);
 
 /* Device workspace for class bucketing of `count` rows. */
 size_t hygt_workspace_bytes(const hygt_plan* plan, uint64_t count);

@@ -352,40 +352,43 @@ size_t apply_smem(const hygt_plan* p, int dir) {
 // ---- tile path --------------------------------------------------------------------------
 using TileFn = void (*)(TileParams);
 
+constexpr int TILE_THREADS = 512;
+
 template <int LOG2N, int L, int VPT>
 TileFn pick_tile(bool standard, bool fwd, bool energy) {
+  constexpr int TT = TILE_THREADS;
   if (standard) {
-    if (!fwd) return hygt_tile_kernel<LOG2N, L, VPT, true, false, false>;
-    return energy ? hygt_tile_kernel<LOG2N, L, VPT, true, true, true>
-                  : hygt_tile_kernel<LOG2N, L, VPT, true, true, false>;
+    if (!fwd) return hygt_tile_kernel<LOG2N, L, VPT, true, false, false, TT>;
+    return energy ? hygt_tile_kernel<LOG2N, L, VPT, true, true, true, TT>
+                  : hygt_tile_kernel<LOG2N, L, VPT, true, true, false, TT>;
   }
-  if (!fwd) return hygt_tile_kernel<LOG2N, L, VPT, false, false, false>;
-  return energy ? hygt_tile_kernel<LOG2N, L, VPT, false, true, true>
-                : hygt_tile_kernel<LOG2N, L, VPT, false, true, false>;
+  if (!fwd) return hygt_tile_kernel<LOG2N, L, VPT, false, false, false, TT>;
+  return energy ? hygt_tile_kernel<LOG2N, L, VPT, false, true, true, TT>
+                : hygt_tile_kernel<LOG2N, L, VPT, false, true, false, TT>;
 }
 
 // Instantiated (log2 N, log2 TPV, rows per lane group) tile layouts; the first of each N is the
 // default. All have E = N / TPV >= 4.
 TileFn select_tile(int log2n, int l, int vpt, bool standard, bool fwd, bool energy) {
   switch (log2n * 256 + l * 16 + vpt) {
-    case 2 * 256 + 0 * 16 + 4: return pick_tile<2, 0, 4>(standard, fwd, energy);
-    case 3 * 256 + 1 * 16 + 4: return pick_tile<3, 1, 4>(standard, fwd, energy);
+    case 2 * 256 + 0 * 16 + 2: return pick_tile<2, 0, 2>(standard, fwd, energy);
+    case 3 * 256 + 1 * 16 + 2: return pick_tile<3, 1, 2>(standard, fwd, energy);
     case 3 * 256 + 0 * 16 + 2: return pick_tile<3, 0, 2>(standard, fwd, energy);
-    case 4 * 256 + 2 * 16 + 4: return pick_tile<4, 2, 4>(standard, fwd, energy);
+    
     case 4 * 256 + 2 * 16 + 2: return pick_tile<4, 2, 2>(standard, fwd, energy);
     case 4 * 256 + 1 * 16 + 2: return pick_tile<4, 1, 2>(standard, fwd, energy);
     case 4 * 256 + 0 * 16 + 1: return pick_tile<4, 0, 1>(standard, fwd, energy);
     case 5 * 256 + 2 * 16 + 2: return pick_tile<5, 2, 2>(standard, fwd, energy);
-    case 5 * 256 + 3 * 16 + 4: return pick_tile<5, 3, 4>(standard, fwd, energy);
+    case 5 * 256 + 3 * 16 + 2: return pick_tile<5, 3, 2>(standard, fwd, energy);
     default: return nullptr;
   }
 }
 
 void default_tile_layout(int log2n, int* l, int* vpt) {
   switch (log2n) {
-    case 2: *l = 0; *vpt = 4; break;
-    case 3: *l = 1; *vpt = 4; break;
-    case 4: *l = 2; *vpt = 4; break;
+    case 2: *l = 0; *vpt = 2; break;
+    case 3: *l = 1; *vpt = 2; break;
+    case 4: *l = 1; *vpt = 2; break;
     case 5: *l = 2; *vpt = 2; break;
     default: *l = -1; *vpt = 0;
   }
@@ -415,12 +418,13 @@ int run_tile(const hygt_plan* p, int dir, const float* x, float* y, const uint16
   P.tile_rows = p->tile_rows;
   P.energy = energy;
   P.err = err;
+  P.load_policy = env_int("HYGT_LOAD_POLICY", 0);
   int occ = 0;
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, p->tile_smem[dir]));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, TILE_THREADS, p->tile_smem[dir]));
   if (occ < 1) return fail(HYGT_ERR_CUDA, "hygt: tile kernel does not fit on an SM");
   const uint64_t tiles = (count + p->tile_rows - 1) / p->tile_rows;
   const uint64_t ctas = std::min<uint64_t>(tiles, (uint64_t)p->num_sms * occ);
-  fn<<<(unsigned)ctas, 256, p->tile_smem[dir], st>>>(P);
+  fn<<<(unsigned)ctas, TILE_THREADS, p->tile_smem[dir], st>>>(P);
   CU(cudaGetLastError());
   return ok();
 }
@@ -436,7 +440,7 @@ int setup_tile(hygt_plan* p, const double* angles, const uint16_t* perms) {
   if (l < 0 || env_int("HYGT_TILE", 1) == 0) return HYGT_OK;
   const Layout ly{p->log2n, l};
   const int tpv = ly.tpv(), e = ly.e();
-  const int rows = env_int("HYGT_TILE_ROWS", 8192);
+  const int rows = env_int("HYGT_TILE_ROWS", 4096);
   size_t smem_max = 0;
   for (int d = 0; d < 2; ++d) {
     DirTables t;
@@ -451,6 +455,7 @@ int setup_tile(hygt_plan* p, const double* angles, const uint16_t* perms) {
           il[((size_t)c * units + u) * tpv + lt] = make_float4(w[0].x, w[0].y, w[1].x, w[1].y);
         }
     const int words = (e + 7) / 8;
+    const uint32_t stride_bytes = 4u * (uint32_t)(tile_scratch_floats(p->log2n, l, vpt) >> p->log2n);
     std::vector<uint4> gi;
     if (t.gmask) {
       gi.assign((size_t)p->classes * (p->rounds + 1) * words * tpv, make_uint4(0, 0, 0, 0));
@@ -460,8 +465,8 @@ int setup_tile(hygt_plan* p, const double* angles, const uint16_t* perms) {
             const uint16_t* src = &t.gidx[(((size_t)c * (p->rounds + 1) + k) * tpv + lt) * e];
             for (int w = 0; w < words; ++w) {
               uint32_t q[4] = {0, 0, 0, 0};
-              for (int h = 0; h < 8 && 8 * w + h < e; ++h)
-                q[h / 2] |= (uint32_t)src[8 * w + h] << (16 * (h & 1));
+              for (int h = 0; h < 8 && 8 * w + h < e; ++h)  // byte offsets into the scratch
+                q[h / 2] |= (uint32_t)(src[8 * w + h] * stride_bytes) << (16 * (h & 1));
               gi[(((size_t)c * (p->rounds + 1) + k) * words + w) * tpv + lt] = make_uint4(q[0], q[1], q[2], q[3]);
             }
           }
@@ -471,7 +476,8 @@ int setup_tile(hygt_plan* p, const double* angles, const uint16_t* perms) {
     if (s) return s;
     p->tunits[d] = units;
     p->tile_smem[d] = tile_smem_bytes(il.size() * sizeof(float4), gi.size() * sizeof(uint4),
-                                      p->classes, rows, 8, tile_scratch_floats(p->log2n, l, vpt));
+                                      p->classes, rows, TILE_THREADS / 32,
+                                      tile_scratch_floats(p->log2n, l, vpt));
     smem_max = std::max(smem_max, p->tile_smem[d]);
   }
   if (smem_max > 200 * 1024) return HYGT_OK;  // tables too large: generic path
@@ -626,6 +632,8 @@ extern "C" int hygt_plan_destroy(hygt_plan* plan) {
 }
 
 extern "C" int hygt_plan_algorithm(const hygt_plan* plan) { return plan ? plan->algo : -1; }
+
+extern "C" int hygt_plan_path(const hygt_plan* plan) { return plan ? (plan->tile ? 1 : 0) : -1; }
 
 extern "C" size_t hygt_workspace_bytes(const hygt_plan* plan, uint64_t count) {
   if (!plan) return 0;

@@ -34,7 +34,24 @@ struct TileParams {
   uint32_t tile_rows;       // T
   double* energy;           // [C][N] (forward + energy)
   uint32_t* err;            // class id out of range flag
+  int load_policy;          // 0 ld.global.cs, 1 ld.global.nc, 2 nc + L2::128B prefetch, 3 nc + evict_last
 };
+
+__device__ __forceinline__ float4 ld_row(const float4* p, int policy) {
+  float4 r;
+  switch (policy) {
+    case 0: return __ldcs(p);
+    case 1: return __ldg(p);
+    case 2:
+      asm volatile("ld.global.nc.L1::no_allocate.L2::128B.v4.f32 {%0,%1,%2,%3}, [%4];"
+                   : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+      return r;
+    default:
+      asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+                   : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+      return r;
+  }
+}
 
 template <int LOG2N, int L>
 struct TileGeom {
@@ -151,29 +168,34 @@ __device__ __forceinline__ void tile_round(float2 (&v)[VPT][TileGeom<LOG2N, L>::
   }
 }
 
-// Gather v[r][s] <- pre[G[elem(t, s)]] through per-row scratch rows. Scratch is laid out
-// [element][row slot] with a per-lane-group xor so one slot's stores of the 32 lanes hit
-// distinct banks; gp[r] points at the lane's interleaved uint4 gather words.
+// Gather v[r][s] <- pre[G[elem(t, s)]] through the warp's scratch. Element i of the row in slot
+// (r, g) lives at scratch[i * S + r * V + g] (S = stride<VPT>(): the 32 lanes' stores of one
+// register slot land in 32 distinct banks). `wbase` is this lane's store base
+// (scratch + g + (t << chl) * S, so every store is [reg + imm]); `rbase` = scratch + g. The
+// gather words hold the source elements pre-multiplied by 4*S (byte offsets, host-computed),
+// so every load is one IADD + LDS [reg + imm].
 template <int LOG2N, int L, int VPT>
 __device__ __forceinline__ void tile_gather(float2 (&v)[VPT][TileGeom<LOG2N, L>::NP],
-                                            float* scratch, int g, int t,
+                                            float* wbase, const char* rbase,
                                             const uint4* (&gp)[VPT]) {
   using G = TileGeom<LOG2N, L>;
   constexpr Layout LY = G::LY;
   constexpr int E = G::E, TPV = G::TPV, V = G::V;
-  constexpr int ROWS = G::template stride<VPT>();
-  // element i of row slot (r, g) lives at scratch[i * ROWS + (r * V + g)] (see stride()).
+  constexpr int S = G::template stride<VPT>();
   __syncwarp();
 #pragma unroll
   for (int r = 0; r < VPT; ++r)
 #pragma unroll
     for (int s = 0; s < E; s += 2) {
-      scratch[LY.elem(t, s) * ROWS + r * V + g] = v[r][s / 2].x;
-      scratch[LY.elem(t, s + 1) * ROWS + r * V + g] = v[r][s / 2].y;
+      // elem(t, s) = (t << chl) + elem(0, s): the lane part is folded into wbase
+      wbase[(LY.elem(0, s)) * S + r * V] = v[r][s / 2].x;
+      wbase[(LY.elem(0, s + 1)) * S + r * V] = v[r][s / 2].y;
     }
   __syncwarp();
 #pragma unroll
   for (int r = 0; r < VPT; ++r) {
+    const char* rb = rbase + r * V * 4;
+    auto at = [&](uint32_t off) { return *reinterpret_cast<const float*>(rb + off); };
     if constexpr (E % 8 == 0) {
 #pragma unroll
       for (int s = 0; s < E; s += 8) {
@@ -181,17 +203,16 @@ __device__ __forceinline__ void tile_gather(float2 (&v)[VPT][TileGeom<LOG2N, L>:
         const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
-          v[r][s / 2 + h].x = scratch[(w[h] & 0xffffu) * ROWS + r * V + g];
-          v[r][s / 2 + h].y = scratch[(w[h] >> 16) * ROWS + r * V + g];
+          v[r][s / 2 + h].x = at(w[h] & 0xffffu);
+          v[r][s / 2 + h].y = at(w[h] >> 16);
         }
       }
     } else {
-      // E == 4: one uint2 worth of indices, stored in the .x/.y of the uint4 word
       const uint4 q = gp[r][0];
-      v[r][0].x = scratch[(q.x & 0xffffu) * ROWS + r * V + g];
-      v[r][0].y = scratch[(q.x >> 16) * ROWS + r * V + g];
-      v[r][1].x = scratch[(q.y & 0xffffu) * ROWS + r * V + g];
-      v[r][1].y = scratch[(q.y >> 16) * ROWS + r * V + g];
+      v[r][0].x = at(q.x & 0xffffu);
+      v[r][0].y = at(q.x >> 16);
+      v[r][1].x = at(q.y & 0xffffu);
+      v[r][1].y = at(q.y >> 16);
     }
   }
 }
@@ -199,18 +220,18 @@ __device__ __forceinline__ void tile_gather(float2 (&v)[VPT][TileGeom<LOG2N, L>:
 template <int LOG2N, int L, bool STD, bool FWD, int VPT, bool SHARED>
 __device__ __forceinline__ void tile_rows(float2 (&v)[VPT][TileGeom<LOG2N, L>::NP],
                                           const float4* (&cp)[VPT], const uint4* (&g0)[VPT],
-                                          uint32_t gstep_words, float* scratch, int g, int t,
+                                          uint32_t gstep_words, float* wbase, const char* rbase,
                                           const TileParams& P) {
   const uint4* gp[VPT];
 #pragma unroll
   for (int r = 0; r < VPT; ++r) gp[r] = g0[r];
-  if (P.gmask & 1ull) tile_gather<LOG2N, L, VPT>(v, scratch, g, t, gp);
+  if (P.gmask & 1ull) tile_gather<LOG2N, L, VPT>(v, wbase, rbase, gp);
   for (int rr = 0; rr < P.rounds; ++rr) {
     tile_round<LOG2N, L, STD, FWD, VPT, SHARED, 0>(v, cp);
     if ((P.gmask >> (rr + 1)) & 1ull) {
 #pragma unroll
       for (int r = 0; r < VPT; ++r) gp[r] = g0[r] + (size_t)(rr + 1) * gstep_words;
-      tile_gather<LOG2N, L, VPT>(v, scratch, g, t, gp);
+      tile_gather<LOG2N, L, VPT>(v, wbase, rbase, gp);
     }
   }
   if constexpr (!STD) {
@@ -232,20 +253,20 @@ __device__ __forceinline__ void tile_rows(float2 (&v)[VPT][TileGeom<LOG2N, L>::N
 HYGT_HD constexpr size_t tile_smem_bytes(size_t coef_bytes, size_t gidx_bytes, int classes,
                                          int tile_rows, int warps, int scratch_floats_per_warp) {
   return ((coef_bytes + 15) & ~size_t(15)) + ((gidx_bytes + 15) & ~size_t(15)) +
-         ((size_t)(classes + 2) * 4 + 15) / 16 * 16 +     // run offsets
-         ((size_t)tile_rows * 2 + 15) / 16 * 16 +          // sorted local row index (u16)
-         ((size_t)tile_rows * 2 + 15) / 16 * 16 +          // class of each sorted position (u16)
+         ((size_t)(classes + 2 + 3) / 4 * 4) * 4 +         // run offsets
+         ((size_t)(tile_rows + 3) / 4 * 4) * 4 +            // sorted entries (class << 16 | row)
          (size_t)warps * scratch_floats_per_warp * 4;
 }
 
-template <int LOG2N, int L, int VPT, bool STD, bool FWD, bool ENERGY>
-__global__ void __launch_bounds__(256) hygt_tile_kernel(const TileParams P) {
+template <int LOG2N, int L, int VPT, bool STD, bool FWD, bool ENERGY, int THREADS>
+__global__ void __launch_bounds__(THREADS, 2) hygt_tile_kernel(const TileParams P) {
   using G = TileGeom<LOG2N, L>;
   constexpr Layout LY = G::LY;
   constexpr int N = G::N, TPV = G::TPV, E = G::E, CH = G::CH, NP = G::NP, V = G::V;
   constexpr int ROWS = V * VPT;  // rows per warp step
-  constexpr int WARPS = 8;
-  constexpr int SCR = N * G::template stride<VPT>();  // scratch floats per warp
+  constexpr int WARPS = THREADS / 32;
+  constexpr int S = G::template stride<VPT>();
+  constexpr int SCR = N * S;  // scratch floats per warp
   extern __shared__ __align__(16) unsigned char tile_smem[];
   const int C = P.classes;
   const int T = (int)P.tile_rows;
@@ -254,36 +275,37 @@ __global__ void __launch_bounds__(256) hygt_tile_kernel(const TileParams P) {
   float4* s_coef = reinterpret_cast<float4*>(tile_smem);
   uint4* s_gidx = reinterpret_cast<uint4*>(s_coef + coef_words);
   uint32_t* s_off = reinterpret_cast<uint32_t*>(s_gidx + gidx_words);  // [C+2]
-  uint16_t* s_order = reinterpret_cast<uint16_t*>(s_off + ((C + 2 + 3) & ~3));
-  uint16_t* s_pcls = s_order + ((T + 7) & ~7);
-  float* s_scratch = reinterpret_cast<float*>(s_pcls + ((T + 7) & ~7));
+  uint32_t* s_ent = s_off + ((C + 2 + 3) & ~3);                         // [T] (class << 16 | row)
+  float* s_scratch = reinterpret_cast<float*>(s_ent + ((T + 3) & ~3));
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> L, t = lane & (TPV - 1);
-  float* scratch = s_scratch + (size_t)warp * SCR;
+  float* wscr = s_scratch + (size_t)warp * SCR;
+  float* wbase = wscr + g + ((t << LY.chl()) * S);
+  const char* rbase = reinterpret_cast<const char*>(wscr + g);
+  const bool sorted = P.cls && C > 1;
 
-  // ---- stage the direction's tables (once per CTA)
-  for (size_t i = tid; i < coef_words; i += blockDim.x) s_coef[i] = __ldg(P.coef + i);
-  for (size_t i = tid; i < gidx_words; i += blockDim.x) s_gidx[i] = __ldg(P.gidx + i);
-  const uint32_t gstep_words = ((E + 7) / 8) * TPV;  // uint4 words per gather step
+  for (size_t i = tid; i < coef_words; i += THREADS) s_coef[i] = __ldg(P.coef + i);
+  for (size_t i = tid; i < gidx_words; i += THREADS) s_gidx[i] = __ldg(P.gidx + i);
+  const uint32_t gstep_words = ((E + 7) / 8) * TPV;
   const uint64_t tiles = (P.count + T - 1) / T;
 
   for (uint64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const uint64_t row0 = tile * T;
     const int rows = (int)((P.count - row0) < (uint64_t)T ? (P.count - row0) : (uint64_t)T);
-    __syncthreads();  // previous tile fully consumed (and tables staged on the first pass)
-    // ---- counting sort of the tile by class (bin C = invalid id)
-    if (P.cls && C > 1) {
-      for (int i = tid; i < C + 2; i += blockDim.x) s_off[i] = 0;
+    const float* xt = P.x + row0 * N;
+    float* yt = P.y + row0 * N;
+    __syncthreads();
+    if (sorted) {  // counting sort of the tile by class (bin C = invalid id)
+      for (int i = tid; i < C + 2; i += THREADS) s_off[i] = 0;
       __syncthreads();
-      for (int i = tid; i < rows; i += blockDim.x) {
+      for (int i = tid; i < rows; i += THREADS) {
         int c = P.cls[row0 + i];
-        if (c >= C) c = C;
-        const unsigned peers = __match_any_sync(__activemask(), c);
-        if (lane == __ffs(peers) - 1) atomicAdd(&s_off[c + 1], __popc(peers));
+        c = c < C ? c : C;
+        atomicAdd(&s_off[c + 1], 1u);  // same-address lanes serialise inside the ATOMS unit
       }
       __syncthreads();
-      if (warp == 0) {  // exclusive scan of C+1 counts (in place, s_off[0] = 0)
+      if (warp == 0) {
         uint32_t carry = 0;
         for (int base = 1; base < C + 2; base += 32) {
           const int i = base + lane;
@@ -298,95 +320,103 @@ __global__ void __launch_bounds__(256) hygt_tile_kernel(const TileParams P) {
         }
       }
       __syncthreads();
-      for (int i = tid; i < rows; i += blockDim.x) {
+      for (int i = tid; i < rows; i += THREADS) {
         int c = P.cls[row0 + i];
         if (c >= C) {
           c = C;
           atomicOr(P.err, 1u);
         }
-        const unsigned peers = __match_any_sync(__activemask(), c);
-        const int leader = __ffs(peers) - 1;
-        uint32_t b = 0;
-        if (lane == leader) b = atomicAdd(&s_off[c], __popc(peers));
-        b = __shfl_sync(peers, b, leader) + __popc(peers & ((1u << lane) - 1u));
-        s_order[b] = (uint16_t)i;
-        s_pcls[b] = (uint16_t)c;
+        // unstable within a class: the order only affects which warp handles a row
+        const uint32_t b = atomicAdd(&s_off[c], 1u);
+        s_ent[b] = ((uint32_t)c << 16) | (uint32_t)i;
       }
       __syncthreads();
     }
 
-    // ---- process sorted positions: each warp takes ROWS consecutive positions per step
-    for (int p0 = warp * ROWS; p0 < rows; p0 += WARPS * ROWS) {
-      int cl[VPT];
-      uint32_t lr[VPT];
-      bool act[VPT];
+    // entry of sorted position p: (class << 16) | local row; inactive positions map to row 0
+    auto entry = [&](int p) -> uint32_t {
+      if (p >= rows) return 0u;
+      if (sorted) return s_ent[p];
+      uint32_t c = P.cls ? (uint32_t)P.cls[row0 + p] : 0u;
+      if (c >= (uint32_t)C) {
+        atomicOr(P.err, 1u);
+        c = (uint32_t)C;
+      }
+      return (c << 16) | (uint32_t)p;
+    };
+    auto load = [&](const uint32_t (&en)[VPT], float2 (&dst)[VPT][NP]) {
 #pragma unroll
       for (int r = 0; r < VPT; ++r) {
-        const int p = p0 + r * V + g;
-        act[r] = p < rows;
-        const bool sorted = P.cls && C > 1;
-        lr[r] = act[r] ? (sorted ? s_order[p] : (uint32_t)p) : 0u;
-        cl[r] = act[r] ? (sorted ? (int)s_pcls[p] : (P.cls ? (int)P.cls[row0 + p] : 0)) : 0;
-        if (!sorted && cl[r] >= C) {
-          cl[r] = C;
-          atomicOr(P.err, 1u);
+        const float4* xr = reinterpret_cast<const float4*>(xt + (size_t)(en[r] & 0xffffu) * N);
+#pragma unroll
+        for (int u = 0; u < E / CH; ++u) {
+          const float4 a = ld_row(xr + t + TPV * u, P.load_policy);
+          dst[r][2 * u] = make_float2(a.x, a.y);
+          dst[r][2 * u + 1] = make_float2(a.z, a.w);
         }
       }
+    };
+
+    int p0 = warp * ROWS;
+    uint32_t en_n[VPT];
+    float2 vn[VPT][NP];
+#pragma unroll
+    for (int r = 0; r < VPT; ++r) en_n[r] = entry(p0 + r * V + g);
+    if (p0 < rows) load(en_n, vn);
+    for (; p0 < rows; p0 += WARPS * ROWS) {
+      uint32_t en[VPT];
       float2 v[VPT][NP];
 #pragma unroll
       for (int r = 0; r < VPT; ++r) {
-        const float* xr = P.x + (row0 + lr[r]) * N;
+        en[r] = en_n[r];
 #pragma unroll
-        for (int u = 0; u < E / CH; ++u) {
-          const int q = t + TPV * u;
-          if (act[r]) {
-            const float4 a = __ldcs(reinterpret_cast<const float4*>(xr) + q);
-            v[r][2 * u] = make_float2(a.x, a.y);
-            v[r][2 * u + 1] = make_float2(a.z, a.w);
-          } else {
-            v[r][2 * u] = v[r][2 * u + 1] = make_float2(0.f, 0.f);
-          }
-        }
+        for (int k = 0; k < NP; ++k) v[r][k] = vn[r][k];
+      }
+      const int pn = p0 + WARPS * ROWS;  // prefetch the next step's rows
+      if (pn < rows) {
+#pragma unroll
+        for (int r = 0; r < VPT; ++r) en_n[r] = entry(pn + r * V + g);
+        load(en_n, vn);
       }
       const float4* cp[VPT];
       const uint4* gp[VPT];
       bool same = true;
 #pragma unroll
       for (int r = 0; r < VPT; ++r) {
-        const int c = cl[r] < C ? cl[r] : 0;
+        uint32_t c = en[r] >> 16;
+        c = c < (uint32_t)C ? c : 0u;
         cp[r] = s_coef + (size_t)c * P.units * TPV + t;
         gp[r] = s_gidx + (size_t)c * (P.rounds + 1) * gstep_words + t;
-        same &= (c == (cl[0] < C ? cl[0] : 0));
+        same &= (en[r] >> 16) == (en[0] >> 16);
       }
       if (__all_sync(0xffffffffu, same))
-        tile_rows<LOG2N, L, STD, FWD, VPT, true>(v, cp, gp, gstep_words, scratch, g, t, P);
+        tile_rows<LOG2N, L, STD, FWD, VPT, true>(v, cp, gp, gstep_words, wbase, rbase, P);
       else
-        tile_rows<LOG2N, L, STD, FWD, VPT, false>(v, cp, gp, gstep_words, scratch, g, t, P);
+        tile_rows<LOG2N, L, STD, FWD, VPT, false>(v, cp, gp, gstep_words, wbase, rbase, P);
 
 #pragma unroll
       for (int r = 0; r < VPT; ++r) {
-        if (!act[r]) continue;
-        const size_t row = row0 + lr[r];
-        float* yr = P.y + row * N;
-        const float* xr = P.x + row * N;
+        const int p = p0 + r * V + g;
+        const uint32_t c = en[r] >> 16;
+        const size_t lr = en[r] & 0xffffu;
+        float4* yr = reinterpret_cast<float4*>(yt + lr * N);
+        if (p < rows && c < (uint32_t)C) {
 #pragma unroll
-        for (int u = 0; u < E / CH; ++u) {
-          const int q = t + TPV * u;
-          if (cl[r] >= C)  // invalid class id: pass the row through (error flagged)
-            reinterpret_cast<float4*>(yr)[q] = reinterpret_cast<const float4*>(xr)[q];
-          else
-            __stcs(reinterpret_cast<float4*>(yr) + q,
+          for (int u = 0; u < E / CH; ++u)
+            __stcs(yr + t + TPV * u,
                    make_float4(v[r][2 * u].x, v[r][2 * u].y, v[r][2 * u + 1].x, v[r][2 * u + 1].y));
-        }
-        if constexpr (ENERGY) {
-          if (cl[r] < C) {
-            double* e = P.energy + (size_t)cl[r] * N;
+          if constexpr (ENERGY) {
+            double* e = P.energy + (size_t)c * N;
 #pragma unroll
             for (int k = 0; k < NP; ++k) {
               atomicAdd(e + LY.elem(t, 2 * k), (double)(v[r][k].x * v[r][k].x));
               atomicAdd(e + LY.elem(t, 2 * k + 1), (double)(v[r][k].y * v[r][k].y));
             }
           }
+        } else if (p < rows) {  // invalid class id: pass the row through (error flagged)
+          const float4* xr = reinterpret_cast<const float4*>(xt + lr * N);
+#pragma unroll
+          for (int u = 0; u < E / CH; ++u) yr[t + TPV * u] = xr[t + TPV * u];
         }
       }
     }

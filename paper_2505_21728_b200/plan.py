@@ -122,6 +122,15 @@ class HyGTPlan:
     def algorithm(self) -> str:
         return "scale-folded" if _lib.lib().hygt_plan_algorithm(self._h) == 1 else "standard"
 
+    @property
+    def path(self) -> str:
+        """Kernel family serving this plan (include/hygt_gpu.h, hygt_plan_path)."""
+        return {0: "bucketed", 1: "tile", 2: "segment"}[_lib.lib().hygt_plan_path(self._h)]
+
+    def launches_per_step(self) -> int:
+        """Kernels launched by bucket + forward + inverse on this plan."""
+        return 2 if self.path == "tile" else 5
+
     def workspace_bytes(self, count: int) -> int:
         return _lib.lib().hygt_workspace_bytes(self._h, count)
 
@@ -282,13 +291,16 @@ class KLTPlan:
 _PLAN_CACHE: dict = {}
 
 
-def _cached(key, make):
-    p = _PLAN_CACHE.get(key)
-    if p is None:
-        p = make()
-        if len(_PLAN_CACHE) > 64:
-            _PLAN_CACHE.clear()
-        _PLAN_CACHE[key] = p
+def _cached(key, make, owners):
+    """Plan cache keyed by object identity; the entry keeps the owning objects alive so an id
+    can never be reused by a different model while its plan is cached."""
+    hit = _PLAN_CACHE.get(key)
+    if hit is not None and all(a is b for a, b in zip(hit[0], owners)):
+        return hit[1]
+    p = make()
+    if len(_PLAN_CACHE) > 64:
+        _PLAN_CACHE.clear()
+    _PLAN_CACHE[key] = (tuple(owners), p)
     return p
 
 
@@ -301,7 +313,7 @@ def forward(model: HyGTModel, x) -> np.ndarray:
     v = np.asarray(x, dtype=np.float64).reshape(-1)
     if v.size != model.dimension():
         raise ArgumentError("forward: dimension mismatch")
-    plan = _cached(_model_key(model), lambda: HyGTPlan(model))
+    plan = _cached(_model_key(model), lambda: HyGTPlan(model), (model,))
     return plan.apply(v[None].astype(np.float32))[0].astype(np.float64)
 
 
@@ -310,7 +322,7 @@ def inverse(model: HyGTModel, y) -> np.ndarray:
     v = np.asarray(y, dtype=np.float64).reshape(-1)
     if v.size != model.dimension():
         raise ArgumentError("inverse: dimension mismatch")
-    plan = _cached(_model_key(model), lambda: HyGTPlan(model))
+    plan = _cached(_model_key(model), lambda: HyGTPlan(model), (model,))
     return plan.apply(v[None].astype(np.float32), inverse=True)[0].astype(np.float64)
 
 
@@ -321,7 +333,7 @@ def _fixed(model: QuantizedHyGTModel, table: TrigTable, x, inverse_: bool) -> np
     v = np.asarray(x, dtype=np.int64).reshape(-1)
     if v.size != model.dimension():
         raise ArgumentError("fixed transform: dimension mismatch")
-    plan = _cached((id(model), id(table), "fx"), lambda: FixedPlan(model, table))
+    plan = _cached((id(model), id(table), "fx"), lambda: FixedPlan(model, table), (model, table))
     t = torch.from_numpy(v[None].copy()).cuda()
     out = plan.inverse(t) if inverse_ else plan.forward(t)
     return out.cpu().numpy()[0]

@@ -54,8 +54,8 @@ def _inter(perms, mask, rounds):
 LAYOUTS = {1: [0], 2: [0], 3: [0], 4: [0, 2], 5: [0], 6: [0, 1, 2], 7: [2], 8: [1, 2]}
 # tile-path layouts (log2 TPV, rows per lane group) for N <= 32; the generic kernel runs with
 # HYGT_TILE=0.
-TILE_LAYOUTS = {2: [(0, 4)], 3: [(1, 4), (0, 2)], 4: [(2, 4), (2, 2), (1, 2), (0, 1)],
-                5: [(2, 2), (3, 4)]}
+TILE_LAYOUTS = {2: [(0, 2)], 3: [(1, 2), (0, 2)], 4: [(1, 2), (2, 2), (0, 1)],
+                5: [(2, 2), (3, 2)]}
 
 
 def _variants(log2n):
