@@ -18,6 +18,7 @@
 #include "../../include/hygt_gpu.h"
 #include "hygt_kernels.cuh"
 #include "hygt_tile.cuh"
+#include "hygt_segment.cuh"
 #include "hygt_plan.h"
 
 using namespace hygt_gpu;
@@ -84,6 +85,10 @@ struct hygt_plan {
   uint32_t tunits[2] = {0, 0};
   uint4* d_tgidx[2] = {nullptr, nullptr};
   size_t tile_smem[2] = {0, 0};
+  // segment path (N >= 64): same interleaved tables, one class staged per CTA segment
+  bool seg = false;
+  int seg_variant = 0;
+  size_t seg_smem[2] = {0, 0};
   unsigned long long* d_fixed_err = nullptr;
   std::mutex* fixed_mu = nullptr;
 };
@@ -429,23 +434,17 @@ int run_tile(const hygt_plan* p, int dir, const float* x, float* y, const uint16
   return ok();
 }
 
-int setup_tile(hygt_plan* p, const double* angles, const uint16_t* perms) {
-  int l = -1, vpt = 0;
-  default_tile_layout(p->log2n, &l, &vpt);
-  const int el = env_int("HYGT_TILE_L", -1), ev = env_int("HYGT_TILE_VPT", -1);
-  if (el >= 0 && ev > 0 && select_tile(p->log2n, el, ev, false, true, false)) {
-    l = el;
-    vpt = ev;
-  }
-  if (l < 0 || env_int("HYGT_TILE", 1) == 0) return HYGT_OK;
+// Lane-interleaved tables of layout (l, vpt) for both directions: coefficient float4 units
+// [C][units][TPV] and gather words [C][R+1][words][TPV] holding byte offsets into the
+// permutation scratch (stride from the layout). Returns the per-class table bytes.
+int build_interleaved(hygt_plan* p, const double* angles, const uint16_t* perms, int l, int vpt,
+                      size_t* coef_bytes_per_class, size_t* gidx_bytes_per_class) {
   const Layout ly{p->log2n, l};
   const int tpv = ly.tpv(), e = ly.e();
-  const int rows = env_int("HYGT_TILE_ROWS", 4096);
-  size_t smem_max = 0;
   for (int d = 0; d < 2; ++d) {
     DirTables t;
     if (!build_direction(ly, p->rounds, p->classes, angles, perms, p->perm_mask, d == 0, p->algo == 0, t))
-      return HYGT_OK;  // (cannot happen: algo already chosen) -- stay on the generic path
+      return fail(HYGT_ERR_NUMERICAL, "hygt: table build failed");
     const uint32_t units = t.stream_len / 2;
     std::vector<float4> il((size_t)p->classes * units * tpv);
     for (int c = 0; c < p->classes; ++c)
@@ -471,16 +470,37 @@ int setup_tile(hygt_plan* p, const double* angles, const uint16_t* perms) {
             }
           }
     }
+    if ((size_t)tile_scratch_floats(p->log2n, l, vpt) * 4 > 65535)
+      return fail(HYGT_ERR_ARGUMENT, "hygt: permutation scratch exceeds 16-bit offsets");
     int s = upload(&p->d_tcoef[d], il.data(), il.size());
     if (!s && !gi.empty()) s = upload(&p->d_tgidx[d], gi.data(), gi.size());
     if (s) return s;
     p->tunits[d] = units;
-    p->tile_smem[d] = tile_smem_bytes(il.size() * sizeof(float4), gi.size() * sizeof(uint4),
-                                      p->classes, rows, TILE_THREADS / 32,
-                                      tile_scratch_floats(p->log2n, l, vpt));
+    coef_bytes_per_class[d] = (size_t)units * tpv * sizeof(float4);
+    gidx_bytes_per_class[d] = gi.empty() ? 0 : (size_t)(p->rounds + 1) * words * tpv * sizeof(uint4);
+  }
+  return HYGT_OK;
+}
+
+int setup_tile(hygt_plan* p, const double* angles, const uint16_t* perms) {
+  int l = -1, vpt = 0;
+  default_tile_layout(p->log2n, &l, &vpt);
+  const int el = env_int("HYGT_TILE_L", -1), ev = env_int("HYGT_TILE_VPT", -1);
+  if (el >= 0 && ev > 0 && select_tile(p->log2n, el, ev, false, true, false)) {
+    l = el;
+    vpt = ev;
+  }
+  if (l < 0 || env_int("HYGT_TILE", 1) == 0) return HYGT_OK;
+  const int rows = env_int("HYGT_TILE_ROWS", 4096);
+  size_t cb[2], gb[2];
+  if (int s = build_interleaved(p, angles, perms, l, vpt, cb, gb)) return s;
+  size_t smem_max = 0;
+  for (int d = 0; d < 2; ++d) {
+    p->tile_smem[d] = tile_smem_bytes(cb[d] * p->classes, gb[d] * p->classes, p->classes, rows,
+                                      TILE_THREADS / 32, tile_scratch_floats(p->log2n, l, vpt));
     smem_max = std::max(smem_max, p->tile_smem[d]);
   }
-  if (smem_max > 200 * 1024) return HYGT_OK;  // tables too large: generic path
+  if (smem_max > 200 * 1024) return HYGT_OK;  // tables too large: stay on another path
   for (int d = 0; d < 2; ++d)
     for (int en = 0; en < 2; ++en) {
       TileFn fn = select_tile(p->log2n, l, vpt, p->algo == 0, d == 0, en == 1);
@@ -491,6 +511,109 @@ int setup_tile(hygt_plan* p, const double* angles, const uint16_t* perms) {
   p->tile_vpt = vpt;
   p->tile_rows = (uint32_t)rows;
   return HYGT_OK;
+}
+
+// ---- segment path -----------------------------------------------------------------------
+using SegFn = void (*)(SegParams);
+constexpr int SEG_THREADS = 256;
+
+struct SegVariant {
+  int log2n, l, vpt;
+  bool prefetch;
+};
+// Instantiated segment layouts; the first of each N is the default.
+constexpr SegVariant kSegVariants[] = {
+    {6, 1, 1, true}, {6, 1, 2, false}, {6, 2, 2, true}, {6, 0, 1, false},
+    {7, 2, 1, true}, {7, 2, 2, false},
+    {8, 2, 1, false}, {8, 2, 1, true}, {8, 1, 1, false}, {8, 3, 2, false},
+};
+// default variant per log2 N (measured on B200): N=64 -> (L=1, VPT=2),
+// N=128 -> (L=2, VPT=1, prefetch), N=256 -> (L=1, VPT=1)
+int default_seg_variant(int log2n) { return log2n == 6 ? 1 : log2n == 7 ? 4 : log2n == 8 ? 8 : -1; }
+
+template <int LOG2N, int L, int VPT, bool PF>
+SegFn pick_seg(bool standard, bool fwd, bool energy) {
+  constexpr int TT = SEG_THREADS;
+  if (standard) {
+    if (!fwd) return hygt_segment_kernel<LOG2N, L, VPT, true, false, false, PF, TT>;
+    return energy ? hygt_segment_kernel<LOG2N, L, VPT, true, true, true, PF, TT>
+                  : hygt_segment_kernel<LOG2N, L, VPT, true, true, false, PF, TT>;
+  }
+  if (!fwd) return hygt_segment_kernel<LOG2N, L, VPT, false, false, false, PF, TT>;
+  return energy ? hygt_segment_kernel<LOG2N, L, VPT, false, true, true, PF, TT>
+                : hygt_segment_kernel<LOG2N, L, VPT, false, true, false, PF, TT>;
+}
+
+SegFn select_seg(int variant, bool standard, bool fwd, bool energy) {
+  switch (variant) {
+    case 0: return pick_seg<6, 1, 1, true>(standard, fwd, energy);
+    case 1: return pick_seg<6, 1, 2, false>(standard, fwd, energy);
+    case 2: return pick_seg<6, 2, 2, true>(standard, fwd, energy);
+    case 3: return pick_seg<6, 0, 1, false>(standard, fwd, energy);
+    case 4: return pick_seg<7, 2, 1, true>(standard, fwd, energy);
+    case 5: return pick_seg<7, 2, 2, false>(standard, fwd, energy);
+    case 6: return pick_seg<8, 2, 1, false>(standard, fwd, energy);
+    case 7: return pick_seg<8, 2, 1, true>(standard, fwd, energy);
+    case 8: return pick_seg<8, 1, 1, false>(standard, fwd, energy);
+    case 9: return pick_seg<8, 3, 2, false>(standard, fwd, energy);
+    default: return nullptr;
+  }
+}
+
+int setup_segment(hygt_plan* p, const double* angles, const uint16_t* perms) {
+  if (p->tile || env_int("HYGT_SEGMENT", 1) == 0) return HYGT_OK;
+  int variant = default_seg_variant(p->log2n);
+  const int want = env_int("HYGT_SEG_VARIANT", -1);
+  if (want >= 0 && want < (int)(sizeof(kSegVariants) / sizeof(kSegVariants[0])) &&
+      kSegVariants[want].log2n == p->log2n)
+    variant = want;
+  if (variant < 0) return HYGT_OK;
+  const SegVariant sv = kSegVariants[variant];
+  size_t cb[2], gb[2];
+  if (int s = build_interleaved(p, angles, perms, sv.l, sv.vpt, cb, gb)) return s;
+  for (int d = 0; d < 2; ++d) {
+    p->seg_smem[d] = cb[d] + gb[d] +
+                     (size_t)(SEG_THREADS / 32) * tile_scratch_floats(p->log2n, sv.l, sv.vpt) * 4;
+    if (p->seg_smem[d] > 220 * 1024) return HYGT_OK;
+    for (int en = 0; en < 2; ++en) {
+      SegFn fn = select_seg(variant, p->algo == 0, d == 0, en == 1);
+      if (fn) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->seg_smem[d]);
+    }
+  }
+  p->seg = true;
+  p->seg_variant = variant;
+  p->chunk_rows = 0;  // global class buckets
+  return HYGT_OK;
+}
+
+int run_segment(const hygt_plan* p, int dir, const float* x, float* y, uint64_t count,
+                double* energy, const WsLayout& w, char* ws, bool bucketed, cudaStream_t st) {
+  SegFn fn = select_seg(p->seg_variant, p->algo == 0, dir == 0, energy != nullptr);
+  SegParams P{};
+  P.x = x;
+  P.y = y;
+  P.idx = reinterpret_cast<const uint32_t*>(ws + w.idx);
+  P.seg_end = reinterpret_cast<const uint32_t*>(ws + w.seg);
+  P.classes = p->classes;
+  P.rounds = p->rounds;
+  P.count = count;
+  P.coef = p->d_tcoef[dir];
+  P.units = p->tunits[dir];
+  P.gidx = p->d_tgidx[dir];
+  P.gmask = p->gmask[dir];
+  P.energy = energy;
+  (void)bucketed;
+  int occ = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, SEG_THREADS, p->seg_smem[dir]));
+  if (occ < 1) return fail(HYGT_ERR_CUDA, "hygt: segment kernel does not fit on an SM");
+  const uint64_t ctas_max = (uint64_t)p->num_sms * occ;
+  const uint64_t min_span = 2048;
+  uint64_t ctas = std::min<uint64_t>(ctas_max, (count + min_span - 1) / min_span);
+  if (ctas < 1) ctas = 1;
+  P.cta_span = (count + ctas - 1) / ctas;
+  fn<<<(unsigned)ctas, SEG_THREADS, p->seg_smem[dir], st>>>(P);
+  CU(cudaGetLastError());
+  return ok();
 }
 
 int run_apply(const hygt_plan* p, int dir, const float* x, float* y, const uint16_t* d_cls,
@@ -507,6 +630,14 @@ int run_apply(const hygt_plan* p, int dir, const float* x, float* y, const uint1
                     d_cls ? reinterpret_cast<uint32_t*>(static_cast<char*>(d_ws) + w.err) : nullptr, st);
   }
   const bool bucketed = d_cls && p->classes > 1;
+  if (p->seg && bucketed) {
+    if (!d_ws || ws_bytes < w.total) return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
+    if (!(flags & HYGT_REUSE_BUCKETS)) {
+      const int s = run_bucket(p, p->classes, 0, d_cls, count, d_ws, ws_bytes, st);
+      if (s) return s;
+    }
+    return run_segment(p, dir, x, y, count, energy, w, static_cast<char*>(d_ws), true, st);
+  }
   if (d_cls) {
     if (!d_ws || ws_bytes < w.total) return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
     if (!(flags & HYGT_REUSE_BUCKETS)) {
@@ -622,6 +753,10 @@ extern "C" int hygt_plan_create(int log2_n, int rounds, int class_count, const d
     free_plan(p);
     return s;
   }
+  if (int s = setup_segment(p, angles, perms)) {
+    free_plan(p);
+    return s;
+  }
   *out = p;
   return ok();
 }
@@ -633,7 +768,9 @@ extern "C" int hygt_plan_destroy(hygt_plan* plan) {
 
 extern "C" int hygt_plan_algorithm(const hygt_plan* plan) { return plan ? plan->algo : -1; }
 
-extern "C" int hygt_plan_path(const hygt_plan* plan) { return plan ? (plan->tile ? 1 : 0) : -1; }
+extern "C" int hygt_plan_path(const hygt_plan* plan) {
+  return plan ? (plan->tile ? 1 : plan->seg ? 2 : 0) : -1;
+}
 
 extern "C" size_t hygt_workspace_bytes(const hygt_plan* plan, uint64_t count) {
   if (!plan) return 0;

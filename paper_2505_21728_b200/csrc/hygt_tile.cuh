@@ -221,14 +221,14 @@ template <int LOG2N, int L, bool STD, bool FWD, int VPT, bool SHARED>
 __device__ __forceinline__ void tile_rows(float2 (&v)[VPT][TileGeom<LOG2N, L>::NP],
                                           const float4* (&cp)[VPT], const uint4* (&g0)[VPT],
                                           uint32_t gstep_words, float* wbase, const char* rbase,
-                                          const TileParams& P) {
+                                          const int rounds, const uint64_t gmask) {
   const uint4* gp[VPT];
 #pragma unroll
   for (int r = 0; r < VPT; ++r) gp[r] = g0[r];
-  if (P.gmask & 1ull) tile_gather<LOG2N, L, VPT>(v, wbase, rbase, gp);
-  for (int rr = 0; rr < P.rounds; ++rr) {
+  if (gmask & 1ull) tile_gather<LOG2N, L, VPT>(v, wbase, rbase, gp);
+  for (int rr = 0; rr < rounds; ++rr) {
     tile_round<LOG2N, L, STD, FWD, VPT, SHARED, 0>(v, cp);
-    if ((P.gmask >> (rr + 1)) & 1ull) {
+    if ((gmask >> (rr + 1)) & 1ull) {
 #pragma unroll
       for (int r = 0; r < VPT; ++r) gp[r] = g0[r] + (size_t)(rr + 1) * gstep_words;
       tile_gather<LOG2N, L, VPT>(v, wbase, rbase, gp);
@@ -390,9 +390,9 @@ __global__ void __launch_bounds__(THREADS, 2) hygt_tile_kernel(const TileParams 
         same &= (en[r] >> 16) == (en[0] >> 16);
       }
       if (__all_sync(0xffffffffu, same))
-        tile_rows<LOG2N, L, STD, FWD, VPT, true>(v, cp, gp, gstep_words, wbase, rbase, P);
+        tile_rows<LOG2N, L, STD, FWD, VPT, true>(v, cp, gp, gstep_words, wbase, rbase, P.rounds, P.gmask);
       else
-        tile_rows<LOG2N, L, STD, FWD, VPT, false>(v, cp, gp, gstep_words, wbase, rbase, P);
+        tile_rows<LOG2N, L, STD, FWD, VPT, false>(v, cp, gp, gstep_words, wbase, rbase, P.rounds, P.gmask);
 
 #pragma unroll
       for (int r = 0; r < VPT; ++r) {

@@ -58,8 +58,13 @@ TILE_LAYOUTS = {2: [(0, 2)], 3: [(1, 2), (0, 2)], 4: [(1, 2), (2, 2), (0, 1)],
                 5: [(2, 2), (3, 2)]}
 
 
+SEG_VARIANTS = {6: [0, 1, 2, 3], 7: [4, 5], 8: [6, 7, 8, 9]}
+
+
 def _variants(log2n):
-    out = [{"HYGT_TILE": "0", "HYGT_LANES_LOG2": str(l)} for l in LAYOUTS[log2n]]
+    out = [{"HYGT_TILE": "0", "HYGT_SEGMENT": "0", "HYGT_LANES_LOG2": str(l)} for l in LAYOUTS[log2n]]
+    for v in SEG_VARIANTS.get(log2n, []):
+        out.append({"HYGT_SEGMENT": "1", "HYGT_SEG_VARIANT": str(v)})
     for l, v in TILE_LAYOUTS.get(log2n, []):
         out.append({"HYGT_TILE": "1", "HYGT_TILE_L": str(l), "HYGT_TILE_VPT": str(v),
                     "HYGT_TILE_ROWS": "64"})  # tiny tiles: many tiles, sort + tails exercised
