@@ -1,0 +1,252 @@
+// hygt_gpu_adapter.hpp -- header-only C++ adapter from the reference's types to the C ABI.
+//
+// Include it next to the reference headers (/root/reference/proj/include) and link
+// libhygt_gpu.so + cudart. It replaces, for batches:
+//   * the per-class model cache + per-block loop of run_apply (tools/hygt_main.cpp:143-149)
+//     -> hygt::gpu::Plan(std::vector<HyGTModel>) + Plan::forward/inverse on device buffers;
+//   * hygt::forward / hygt::inverse (transform.hpp:72-96) on one vector -> hygt::gpu::forward /
+//     hygt::gpu::inverse (same signatures, fp32 device arithmetic);
+//   * forward_fixed / inverse_fixed (fixedpoint.hpp:191-224) -> hygt::gpu::FixedPlan;
+//   * the whole `hygt apply` data path on a ResidualDataset (hygt_main.cpp:130-172)
+//     -> hygt::gpu::apply(bundle, dataset, forward, fixed).
+// Non-zero C-ABI statuses are rethrown as the reference's exception classes (errors.hpp:23-45).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "hygt/bundle.hpp"
+#include "hygt/dataset.hpp"
+#include "hygt/errors.hpp"
+#include "hygt/fixedpoint.hpp"
+#include "hygt/model.hpp"
+#include "hygt_gpu.h"
+
+namespace hygt::gpu {
+
+inline void check(int status) {
+  if (status == HYGT_OK) return;
+  char msg[512];
+  hygt_last_error(msg, sizeof msg);
+  switch (status) {
+    case HYGT_ERR_ARGUMENT: throw ArgumentError(msg);
+    case HYGT_ERR_IO: throw IoError(msg);
+    case HYGT_ERR_OVERFLOW: throw OverflowError(msg);
+    case HYGT_ERR_NUMERICAL: throw NumericalError(msg);
+    default: throw std::runtime_error(std::string("hygt_gpu: ") + msg);
+  }
+}
+
+inline void cuda_check(cudaError_t e) {
+  if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+}
+
+// Device buffer (RAII).
+template <class T>
+struct DeviceBuffer {
+  T* p = nullptr;
+  std::size_t n = 0;
+  explicit DeviceBuffer(std::size_t count = 0) { resize(count); }
+  ~DeviceBuffer() { cudaFree(p); }
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  void resize(std::size_t count) {
+    if (count <= n) return;
+    cudaFree(p);
+    p = nullptr;
+    n = 0;
+    if (count) cuda_check(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)));
+    n = count;
+  }
+};
+
+// Per-class float plan. inter_round_perms (optional, BASELINE extension): [C][R-1] gathers
+// applied after rounds 0..R-2; each model's own permutation is the final sorting gather.
+class Plan {
+ public:
+  explicit Plan(const std::vector<HyGTModel>& models,
+                const std::vector<std::vector<std::vector<std::uint16_t>>>* inter_round_perms = nullptr,
+                std::uint32_t flags = 0) {
+    if (models.empty()) throw ArgumentError("gpu::Plan: need at least one class");
+    const int log2n = models.front().log2_n(), rounds = models.front().rounds();
+    const std::size_t n = models.front().dimension();
+    std::vector<double> angles;
+    std::vector<std::uint16_t> perms(models.size() * rounds * n);
+    std::uint32_t mask = 0;
+    for (std::size_t c = 0; c < models.size(); ++c) {
+      const auto& m = models[c];
+      if (m.log2_n() != log2n || m.rounds() != rounds)
+        throw ArgumentError("gpu::Plan: all classes must share log2_n and rounds");
+      angles.insert(angles.end(), m.angles().begin(), m.angles().end());
+      for (int r = 0; r < rounds; ++r)
+        for (std::size_t i = 0; i < n; ++i) perms[(c * rounds + r) * n + i] = static_cast<std::uint16_t>(i);
+      if (m.permutation()) {
+        mask |= 1u << (rounds - 1);
+        for (std::size_t i = 0; i < n; ++i) perms[(c * rounds + rounds - 1) * n + i] = (*m.permutation())[i];
+      }
+      if (inter_round_perms) {
+        mask |= (1u << (rounds - 1)) - 1u;
+        for (int r = 0; r + 1 < rounds; ++r)
+          for (std::size_t i = 0; i < n; ++i) perms[(c * rounds + r) * n + i] = (*inter_round_perms)[c][r][i];
+      }
+    }
+    check(hygt_plan_create(log2n, rounds, static_cast<int>(models.size()), angles.data(),
+                           mask ? perms.data() : nullptr, mask, flags, &plan_));
+    n_ = n;
+  }
+  explicit Plan(const ModelBundle& bundle) : Plan(dequantized_models(bundle)) {}
+  ~Plan() { hygt_plan_destroy(plan_); }
+  Plan(const Plan&) = delete;
+  Plan& operator=(const Plan&) = delete;
+
+  std::size_t dimension() const { return n_; }
+  const hygt_plan* handle() const { return plan_; }
+
+  // Device rows in/out (stream-ordered, asynchronous). d_cls may be null (all class 0).
+  void forward(const float* d_x, float* d_y, const std::uint16_t* d_cls, std::size_t count,
+               cudaStream_t stream = nullptr) {
+    run(true, d_x, d_y, d_cls, count, stream);
+  }
+  void inverse(const float* d_y, float* d_x, const std::uint16_t* d_cls, std::size_t count,
+               cudaStream_t stream = nullptr) {
+    run(false, d_y, d_x, d_cls, count, stream);
+  }
+  // Throws ArgumentError if a previous call saw a class id >= class_count.
+  void sync(cudaStream_t stream = nullptr) { check(hygt_sync_status(plan_, ws_.p, stream)); }
+
+ private:
+  static std::vector<HyGTModel> dequantized_models(const ModelBundle& b) {
+    std::vector<HyGTModel> out;
+    for (std::size_t c = 0; c < b.class_count(); ++c) out.push_back(b.dequantized(c));
+    return out;
+  }
+  void run(bool fwd, const float* in, float* out, const std::uint16_t* cls, std::size_t count,
+           cudaStream_t stream) {
+    ws_.resize(hygt_workspace_bytes(plan_, count));
+    check((fwd ? hygt_forward_f32 : hygt_inverse_f32)(plan_, in, out, cls, count, ws_.p, ws_.n, 0, stream));
+  }
+  hygt_plan* plan_ = nullptr;
+  std::size_t n_ = 0;
+  DeviceBuffer<unsigned char> ws_{256};
+};
+
+// Integer plan over quantized per-class models (bit-exact with forward_fixed/inverse_fixed).
+class FixedPlan {
+ public:
+  FixedPlan(const std::vector<QuantizedHyGTModel>& models, const TrigTable& table) {
+    if (models.empty()) throw ArgumentError("gpu::FixedPlan: need at least one class");
+    const auto& m0 = models.front();
+    const std::size_t n = m0.dimension();
+    std::vector<std::uint16_t> codes, perms(models.size() * m0.rounds() * n);
+    std::uint32_t mask = 0;
+    for (std::size_t c = 0; c < models.size(); ++c) {
+      const auto& m = models[c];
+      if (m.angle_bits() != table.angle_bits())
+        throw ArgumentError("forward_fixed: table/model angle_bits mismatch");
+      codes.insert(codes.end(), m.codes().begin(), m.codes().end());
+      for (int r = 0; r < m0.rounds(); ++r)
+        for (std::size_t i = 0; i < n; ++i) perms[(c * m0.rounds() + r) * n + i] = static_cast<std::uint16_t>(i);
+      if (m.permutation()) {
+        mask |= 1u << (m0.rounds() - 1);
+        for (std::size_t i = 0; i < n; ++i) perms[(c * m0.rounds() + m0.rounds() - 1) * n + i] = (*m.permutation())[i];
+      }
+    }
+    check(hygt_fixed_plan_create(m0.log2_n(), m0.rounds(), static_cast<int>(models.size()),
+                                 table.angle_bits(), table.precision_bits(), codes.data(),
+                                 mask ? perms.data() : nullptr, mask, &plan_));
+  }
+  ~FixedPlan() { hygt_plan_destroy(plan_); }
+  FixedPlan(const FixedPlan&) = delete;
+  FixedPlan& operator=(const FixedPlan&) = delete;
+  // Synchronous; throws like the reference for the first failing row (in row order).
+  std::uint64_t forward(const std::int64_t* d_x, std::int64_t* d_y, const std::uint16_t* d_cls,
+                        std::size_t count, cudaStream_t stream = nullptr) {
+    std::uint64_t bad = 0;
+    check(hygt_forward_i64(plan_, d_x, d_y, d_cls, count, &bad, stream));
+    return bad;
+  }
+  std::uint64_t inverse(const std::int64_t* d_y, std::int64_t* d_x, const std::uint16_t* d_cls,
+                        std::size_t count, cudaStream_t stream = nullptr) {
+    std::uint64_t bad = 0;
+    check(hygt_inverse_i64(plan_, d_y, d_x, d_cls, count, &bad, stream));
+    return bad;
+  }
+
+ private:
+  hygt_plan* plan_ = nullptr;
+};
+
+// One-vector drop-ins with the signatures of hygt::forward / hygt::inverse (transform.hpp:72,86).
+inline std::vector<double> forward(const HyGTModel& model, std::vector<double> x) {
+  if (x.size() != model.dimension()) throw ArgumentError("forward: dimension mismatch");
+  Plan plan({model});
+  std::vector<float> h(x.begin(), x.end());
+  DeviceBuffer<float> d(h.size());
+  cuda_check(cudaMemcpy(d.p, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+  plan.forward(d.p, d.p, nullptr, 1);
+  cuda_check(cudaMemcpy(h.data(), d.p, h.size() * 4, cudaMemcpyDeviceToHost));
+  return std::vector<double>(h.begin(), h.end());
+}
+inline std::vector<double> inverse(const HyGTModel& model, std::vector<double> y) {
+  if (y.size() != model.dimension()) throw ArgumentError("inverse: dimension mismatch");
+  Plan plan({model});
+  std::vector<float> h(y.begin(), y.end());
+  DeviceBuffer<float> d(h.size());
+  cuda_check(cudaMemcpy(d.p, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+  plan.inverse(d.p, d.p, nullptr, 1);
+  cuda_check(cudaMemcpy(h.data(), d.p, h.size() * 4, cudaMemcpyDeviceToHost));
+  return std::vector<double>(h.begin(), h.end());
+}
+
+// The data path of `hygt apply` (hygt_main.cpp:130-172) on an in-memory dataset: float
+// arithmetic through Plan, or fixed arithmetic (llround inputs, :157) through FixedPlan.
+inline ResidualDataset apply(const ModelBundle& bundle, const ResidualDataset& ds, bool fwd,
+                             bool fixed) {
+  if (ds.log2_n() != bundle.log2_n()) throw ArgumentError("apply: model/data dimension mismatch");
+  if (ds.class_count() != bundle.class_count())
+    throw ArgumentError("apply: model/data class count mismatch");
+  const std::size_t n = ds.dimension(), rows = ds.blocks().size();
+  std::vector<std::uint16_t> cls(rows);
+  for (std::size_t r = 0; r < rows; ++r) cls[r] = ds.blocks()[r].class_id;
+  DeviceBuffer<std::uint16_t> dc(rows);
+  if (rows) cuda_check(cudaMemcpy(dc.p, cls.data(), rows * 2, cudaMemcpyHostToDevice));
+  std::vector<ResidualBlock> out(rows);
+  if (!fixed) {
+    std::vector<float> x(rows * n);
+    for (std::size_t r = 0; r < rows; ++r)
+      for (std::size_t i = 0; i < n; ++i) x[r * n + i] = static_cast<float>(ds.blocks()[r].values[i]);
+    DeviceBuffer<float> d(rows * n);
+    if (rows) cuda_check(cudaMemcpy(d.p, x.data(), x.size() * 4, cudaMemcpyHostToDevice));
+    Plan plan(bundle);
+    if (fwd) plan.forward(d.p, d.p, dc.p, rows);
+    else plan.inverse(d.p, d.p, dc.p, rows);
+    plan.sync();
+    if (rows) cuda_check(cudaMemcpy(x.data(), d.p, x.size() * 4, cudaMemcpyDeviceToHost));
+    for (std::size_t r = 0; r < rows; ++r)
+      out[r] = {cls[r], std::vector<double>(x.begin() + r * n, x.begin() + (r + 1) * n)};
+  } else {
+    if (!bundle.quantized())
+      throw ArgumentError("apply: fixed arithmetic needs a quantized bundle (train with --angle-bits 8)");
+    std::vector<std::int64_t> x(rows * n);
+    for (std::size_t r = 0; r < rows; ++r)
+      for (std::size_t i = 0; i < n; ++i) x[r * n + i] = std::llround(ds.blocks()[r].values[i]);
+    DeviceBuffer<std::int64_t> d(rows * n);
+    if (rows) cuda_check(cudaMemcpy(d.p, x.data(), x.size() * 8, cudaMemcpyHostToDevice));
+    std::vector<QuantizedHyGTModel> qm;
+    for (std::size_t c = 0; c < bundle.class_count(); ++c) qm.push_back(bundle.quantized_model(c));
+    FixedPlan plan(qm, TrigTable(bundle.angle_bits(), bundle.precision_bits()));
+    if (fwd) plan.forward(d.p, d.p, dc.p, rows);
+    else plan.inverse(d.p, d.p, dc.p, rows);
+    if (rows) cuda_check(cudaMemcpy(x.data(), d.p, x.size() * 8, cudaMemcpyDeviceToHost));
+    for (std::size_t r = 0; r < rows; ++r)
+      out[r] = {cls[r], std::vector<double>(x.begin() + r * n, x.begin() + (r + 1) * n)};
+  }
+  return ResidualDataset(ds.log2_n(), ds.class_count(), std::move(out));
+}
+
+}  // namespace hygt::gpu

@@ -1,0 +1,99 @@
+// adapter_check.cpp -- TEST PROGRAM: drives include/hygt_gpu_adapter.hpp with the reference's
+// own types (built against the unmodified /root/reference headers by oracle/Makefile into
+// oracle/_ref/adapter_check) and compares every result with the reference's own functions.
+// Run on a GPU box by tests/test_gpu_parity.py::test_reference_adapter. Exit 0 = all checks ok.
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+#include "hygt/bundle.hpp"
+#include "hygt/dataset.hpp"
+#include "hygt/fixedpoint.hpp"
+#include "hygt/rng.hpp"
+#include "hygt/transform.hpp"
+#include "hygt_gpu_adapter.hpp"
+
+static int failures = 0;
+#define EXPECT(cond, ...)             \
+  do {                                \
+    if (!(cond)) {                    \
+      std::printf("FAIL: " __VA_ARGS__); \
+      std::printf("\n");              \
+      ++failures;                     \
+    }                                 \
+  } while (0)
+
+int main() {
+  hygt::Rng rng(2505);
+  // --- one-vector drop-ins vs hygt::forward / hygt::inverse (transform.hpp:72-96)
+  for (int log2n : {1, 2, 4, 6, 8}) {
+    const std::size_t n = std::size_t{1} << log2n;
+    std::vector<double> ang(hygt::num_parameters(log2n, 3));
+    for (double& a : ang) a = rng.uniform(-3.14159, 3.14159);
+    std::vector<std::uint16_t> perm(n);  // a reversal as the final sorting permutation
+    for (std::size_t i = 0; i < n; ++i) perm[i] = static_cast<std::uint16_t>(n - 1 - i);
+    const hygt::HyGTModel m(log2n, 3, ang, perm);
+    std::vector<double> x(n);
+    for (double& v : x) v = 16 * rng.gaussian();
+    for (auto& v : x) v = static_cast<float>(v);
+    const auto yr = hygt::forward(m, x), yg = hygt::gpu::forward(m, x);
+    const auto xr = hygt::inverse(m, x), xg = hygt::gpu::inverse(m, x);
+    double e1 = 0, e2 = 0, s = 0;
+    for (std::size_t i = 0; i < n; ++i) {
+      e1 = std::max(e1, std::abs(yr[i] - yg[i]));
+      e2 = std::max(e2, std::abs(xr[i] - xg[i]));
+      s = std::max(s, std::abs(x[i]));
+    }
+    EXPECT(e1 <= 1e-5 * s && e2 <= 1e-5 * s, "gpu::forward/inverse log2n=%d err %.3g %.3g", log2n, e1, e2);
+  }
+  // --- errors rethrown as the reference's classes
+  bool threw = false;
+  try {
+    hygt::gpu::forward(hygt::HyGTModel::zeros(2, 1), {1.0, 2.0});
+  } catch (const hygt::ArgumentError&) {
+    threw = true;
+  }
+  EXPECT(threw, "dimension mismatch did not throw ArgumentError");
+  // --- the `hygt apply` data path on a ResidualDataset (hygt_main.cpp:130-172), float and fixed
+  for (int log2n : {4, 6}) {
+    const std::size_t n = std::size_t{1} << log2n;
+    const int classes = 5, rounds = 2;
+    std::vector<hygt::HyGTModel> models;
+    std::vector<hygt::QuantizedHyGTModel> qmodels;
+    for (int c = 0; c < classes; ++c) {
+      std::vector<double> ang(hygt::num_parameters(log2n, rounds));
+      for (double& a : ang) a = rng.uniform(0, 6.28318);
+      models.emplace_back(log2n, rounds, ang);
+      qmodels.push_back(hygt::quantize_model(models.back(), 8));
+    }
+    std::vector<hygt::ResidualBlock> blocks(3000);
+    for (auto& b : blocks) {
+      b.class_id = static_cast<std::uint16_t>(rng.below(classes));
+      b.values.resize(n);
+      for (double& v : b.values) v = std::round(64 * rng.gaussian());
+    }
+    const hygt::ResidualDataset ds(log2n, classes, blocks);
+    const hygt::ModelBundle fb(models), qb(qmodels);
+    const auto yf = hygt::gpu::apply(fb, ds, true, false);
+    const auto yq = hygt::gpu::apply(qb, ds, true, true);
+    const hygt::TrigTable table(8, 10);
+    double ef = 0, sc = 0;
+    long long mism = 0;
+    for (std::size_t r = 0; r < blocks.size(); ++r) {
+      const auto& b = blocks[r];
+      const auto ref = hygt::forward(models[b.class_id], b.values);
+      std::vector<std::int64_t> xi(b.values.begin(), b.values.end());
+      const auto refi = hygt::forward_fixed(qmodels[b.class_id], table, xi);
+      for (std::size_t i = 0; i < n; ++i) {
+        ef = std::max(ef, std::abs(ref[i] - yf.blocks()[r].values[i]));
+        sc = std::max(sc, std::abs(b.values[i]));
+        mism += static_cast<double>(refi[i]) != yq.blocks()[r].values[i];
+      }
+      EXPECT(yf.blocks()[r].class_id == b.class_id, "class id not carried");
+    }
+    EXPECT(ef <= 1e-5 * sc, "gpu::apply float log2n=%d max err %.3g", log2n, ef);
+    EXPECT(mism == 0, "gpu::apply fixed log2n=%d: %lld mismatches (must be bit-exact)", log2n, mism);
+  }
+  std::printf("adapter_check: %s (%d failures)\n", failures ? "FAILED" : "ok", failures);
+  return failures ? 1 : 0;
+}

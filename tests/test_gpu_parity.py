@@ -291,3 +291,16 @@ def test_klt_config4_vs_oracle(cuda, oracle_mod):
     check_close(y.cpu().numpy(), ref, x.cpu().numpy(), "cfg4 klt fwd")
     back = plan.inverse(y, cls)
     check_close(back.cpu().numpy(), x.cpu().numpy(), x.cpu().numpy(), "cfg4 klt roundtrip")
+
+
+def test_reference_adapter(cuda):
+    """include/hygt_gpu_adapter.hpp driven with the reference's own C++ types (HyGTModel,
+    ModelBundle, ResidualDataset, QuantizedHyGTModel, TrigTable) against the reference's own
+    hygt::forward / forward_fixed, built here from the unmodified headers (oracle/_ref)."""
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref",
+                       "adapter_check")
+    assert os.path.exists(exe), "oracle/_ref/adapter_check was not built (make -C oracle)"
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "adapter_check: ok" in r.stdout
