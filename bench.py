@@ -51,6 +51,21 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def measured_traffic(workload: str):
+    """DRAM bytes (read + write) of one forward launch of this workload's kernel from the latest
+    committed ncu --set full capture (profiles/*/traffic.json), or None."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "traffic.json")), reverse=True):
+        try:
+            with open(path) as f:
+                t = json.load(f).get(workload)
+            if t:
+                return t["traffic_bytes_per_launch"], os.path.relpath(path, ROOT)
+        except Exception:
+            pass
+    return None, None
+
+
 def bytes_per_row(n: int, classes: int) -> int:
     """Algorithmic HBM bytes of one direction for one row: N fp32 in + N fp32 out + u16 class id
     (SURVEY.md §8 d2)."""
@@ -277,8 +292,9 @@ def impl_ours(args):
     bpr = bytes_per_row(n, w.cfg.classes)
     launch_ms = (t_fwd + t_inv) / 2  # the fwd and inv apply kernels (same kernel family)
     achieved = rows * bpr / (launch_ms * 1e-3) / 1e9
+    traffic, traffic_src = measured_traffic(w.cfg.name) if rows == w.cfg.count else (None, None)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None,
+                "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
                 "kernel": f"{plan.path} kernel (forward / inverse), class bucketing included",
                 "bytes_per_launch": rows * bpr, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({hbm_kind})"}
     launches_per_step = plan.launches_per_step()
