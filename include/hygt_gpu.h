@@ -82,7 +82,9 @@ int hygt_plan_destroy(hygt_plan* plan);
 int hygt_plan_algorithm(const hygt_plan* plan);
 /* Kernel family serving the plan: 0 = bucketed apply kernel (hygt_bucket + per-row gather),
  * 1 = tile kernel (class sort inside each CTA, no bucketing pass; N <= 32),
- * 2 = class-segment kernel (global class buckets, one class table staged per CTA segment). */
+ * 2 = class-segment kernel (global class buckets, one class table staged per CTA segment),
+ * 3 = plan-specialised kernel compiled at plan creation (NVRTC, sm_100a; N <= 64): coefficients
+ *     are instruction immediates and permutations register renames. */
 int hygt_plan_path(const hygt_plan* plan);
 
 /* Device workspace for class bucketing of `count` rows. */

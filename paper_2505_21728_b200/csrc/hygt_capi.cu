@@ -20,6 +20,7 @@
 #include "hygt_tile.cuh"
 #include "hygt_segment.cuh"
 #include "hygt_plan.h"
+#include "hygt_jit.h"
 
 using namespace hygt_gpu;
 
@@ -85,6 +86,8 @@ struct hygt_plan {
   uint32_t tunits[2] = {0, 0};
   uint4* d_tgidx[2] = {nullptr, nullptr};
   size_t tile_smem[2] = {0, 0};
+  // JIT path (N <= 64): NVRTC-specialised kernels, coefficients as immediates
+  JitKernels jit;
   // segment path (N >= 64): same interleaved tables, one class staged per CTA segment
   bool seg = false;
   int seg_variant = 0;
@@ -119,6 +122,7 @@ void free_plan(hygt_plan* p) {
   cudaFree(p->d_cos);
   cudaFree(p->d_sin);
   cudaFree(p->d_fixed_err);
+  jit_release(p->jit);
   delete p->fixed_mu;
   delete p;
 }
@@ -185,36 +189,54 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return r;
 }
 
+// Class ids of BK_PER consecutive rows per thread (128-bit loads when aligned).
+__device__ __forceinline__ void load_ids16(const uint16_t* __restrict__ cls, uint64_t r0,
+                                           uint64_t count, uint32_t (&q)[BK_PER / 2]) {
+  if (r0 + BK_PER <= count && (reinterpret_cast<uintptr_t>(cls + r0) & 15) == 0) {
+#pragma unroll
+    for (int w = 0; w < BK_PER / 8; ++w) {
+      const uint4 v = __ldcs(reinterpret_cast<const uint4*>(cls + r0) + w);
+      q[4 * w] = v.x; q[4 * w + 1] = v.y; q[4 * w + 2] = v.z; q[4 * w + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int w = 0; w < BK_PER / 2; ++w) q[w] = 0;
+    for (int h = 0; h < BK_PER; ++h)
+      if (r0 + h < count) q[h >> 1] |= (uint32_t)cls[r0 + h] << (16 * (h & 1));
+  }
+}
+
+// Per-tile class histogram, written class-major: counts[c * tiles + tile].
 __global__ void __launch_bounds__(BK_THREADS) bucket_hist_kernel(const uint16_t* __restrict__ cls,
                                                                  uint64_t count, int classes,
-                                                                 uint32_t* tile_counts,
+                                                                 uint32_t* counts, uint64_t tiles,
                                                                  uint32_t* err) {
   extern __shared__ uint32_t cnt[];
   for (int i = threadIdx.x; i <= classes; i += blockDim.x) cnt[i] = 0;
   __syncthreads();
-  const uint64_t base = (uint64_t)blockIdx.x * BK_TILE;
+  const uint64_t r0 = (uint64_t)blockIdx.x * BK_TILE + (uint64_t)threadIdx.x * BK_PER;
+  uint32_t q[BK_PER / 2];
+  load_ids16(cls, r0, count, q);
   bool bad = false;
-  for (int k = 0; k < BK_PER; ++k) {
-    const uint64_t row = base + (uint64_t)k * BK_THREADS + threadIdx.x;
-    if (row < count) {
-      int c = cls[row];
-      if (c >= classes) {
-        c = classes;
-        bad = true;
-      }
-      const unsigned peers = __match_any_sync(__activemask(), c);
-      if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&cnt[c], __popc(peers));
+#pragma unroll
+  for (int h = 0; h < BK_PER; ++h) {
+    int c = (q[h >> 1] >> (16 * (h & 1))) & 0xffff;
+    if (c >= classes) {
+      c = classes;
+      bad |= r0 + h < count;
     }
+    if (r0 + h < count) atomicAdd(&cnt[c], 1u);
   }
   if (bad) atomicOr(err, 1u);
   __syncthreads();
-  for (int i = threadIdx.x; i <= classes; i += blockDim.x)
-    tile_counts[(size_t)blockIdx.x * (classes + 1) + i] = cnt[i];
+  for (int i = threadIdx.x; i <= classes; i += blockDim.x) counts[(size_t)i * tiles + blockIdx.x] = cnt[i];
 }
 
-// One CTA per chunk: exclusive scan of the chunk's (class, tile) counts in class-major order.
-__global__ void __launch_bounds__(BK_THREADS) bucket_scan_kernel(const uint32_t* tile_counts,
-                                                                 uint32_t* tile_base,
+// One CTA per chunk: exclusive scan of the chunk's (class, tile) counts in class-major order
+// (contiguous in the class-major count layout). Writes per-tile class bases (class-major) and
+// the chunk's class run ends.
+__global__ void __launch_bounds__(BK_THREADS) bucket_scan_kernel(const uint32_t* counts,
+                                                                 uint32_t* base,
                                                                  uint32_t* seg_end,
                                                                  uint64_t tiles,
                                                                  uint64_t tiles_per_chunk,
@@ -228,45 +250,76 @@ __global__ void __launch_bounds__(BK_THREADS) bucket_scan_kernel(const uint32_t*
   const uint64_t per = (entries + BK_THREADS - 1) / BK_THREADS;
   const uint64_t e0 = umin64(entries, per * threadIdx.x);
   const uint64_t e1 = umin64(entries, e0 + per);
-  auto at = [&](uint64_t e) {  // class-major entry e = c * tn + tl
-    const uint64_t c = e / tn, tl = e % tn;
-    return (t0 + tl) * cp1 + c;
-  };
+  auto at = [&](uint64_t e) { return (e / tn) * tiles + t0 + (e % tn); };
   uint32_t local = 0;
-  for (uint64_t e = e0; e < e1; ++e) local += tile_counts[at(e)];
+  for (uint64_t e = e0; e < e1; ++e) local += counts[at(e)];
   uint32_t excl;
   Scan(tmp).ExclusiveSum(local, excl);
-  const uint32_t row0 = (uint32_t)umin64(count, t0 * BK_TILE);
-  uint32_t run = row0 + excl;
+  uint32_t run = (uint32_t)umin64(count, t0 * BK_TILE) + excl;
   for (uint64_t e = e0; e < e1; ++e) {
-    const uint32_t v = tile_counts[at(e)];
-    tile_base[at(e)] = run;
+    const uint32_t v = counts[at(e)];
+    base[at(e)] = run;
     run += v;
     if (e % tn == tn - 1) seg_end[(uint64_t)blockIdx.x * cp1 + e / tn] = run;
   }
 }
 
+// Per tile: local counting sort in shared memory, then each class run of the tile is written
+// contiguously to its place in the bucketed index list (coalesced stores).
 __global__ void __launch_bounds__(BK_THREADS) bucket_scatter_kernel(
-    const uint16_t* __restrict__ cls, uint64_t count, int classes, const uint32_t* tile_base,
-    uint32_t* idx) {
-  extern __shared__ uint32_t cur[];
-  for (int i = threadIdx.x; i <= classes; i += blockDim.x)
-    cur[i] = tile_base[(size_t)blockIdx.x * (classes + 1) + i];
+    const uint16_t* __restrict__ cls, uint64_t count, int classes, const uint32_t* base,
+    uint64_t tiles, uint32_t* idx) {
+  extern __shared__ uint32_t sm_sc[];
+  uint32_t* lcnt = sm_sc;                                   // [C+2] local run starts / cursors
+  uint32_t* gbase = lcnt + ((classes + 2 + 3) & ~3);        // [C+1] global bases of this tile
+  uint32_t* ent = gbase + ((classes + 1 + 3) & ~3);         // [BK_TILE] (class << 16 | row)
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int i = tid; i < classes + 2; i += blockDim.x) lcnt[i] = 0;
+  for (int i = tid; i <= classes; i += blockDim.x) gbase[i] = base[(size_t)i * tiles + blockIdx.x];
   __syncthreads();
-  const uint64_t base = (uint64_t)blockIdx.x * BK_TILE;
-  const int lane = threadIdx.x & 31;
-  for (int k = 0; k < BK_PER; ++k) {
-    const uint64_t row = base + (uint64_t)k * BK_THREADS + threadIdx.x;
-    if (row < count) {
-      int c = cls[row];
-      if (c >= classes) c = classes;
-      const unsigned peers = __match_any_sync(__activemask(), c);
-      const int leader = __ffs(peers) - 1;
-      uint32_t b = 0;
-      if (lane == leader) b = atomicAdd(&cur[c], __popc(peers));
-      b = __shfl_sync(peers, b, leader);
-      idx[b + __popc(peers & lanemask_lt())] = (uint32_t)row;
+  const uint64_t row0 = (uint64_t)blockIdx.x * BK_TILE;
+  const uint64_t r0 = row0 + (uint64_t)tid * BK_PER;
+  const int rows = (int)umin64(BK_TILE, count - row0);
+  uint32_t q[BK_PER / 2];
+  load_ids16(cls, r0, count, q);
+#pragma unroll
+  for (int h = 0; h < BK_PER; ++h) {
+    int c = (q[h >> 1] >> (16 * (h & 1))) & 0xffff;
+    c = c < classes ? c : classes;
+    if (r0 + h < count) atomicAdd(&lcnt[c + 1], 1u);
+  }
+  __syncthreads();
+  if (tid < 32) {  // exclusive scan of the local counts
+    uint32_t carry = 0;
+    for (int b = 1; b < classes + 2; b += 32) {
+      const int i = b + lane;
+      uint32_t v0 = i < classes + 2 ? lcnt[i] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t n = __shfl_up_sync(0xffffffffu, v0, o);
+        if (lane >= o) v0 += n;
+      }
+      if (i < classes + 2) lcnt[i] = v0 + carry;
+      carry += __shfl_sync(0xffffffffu, v0, 31);
     }
+  }
+  __syncthreads();
+  // gbase[c] - lcnt[c] turns a local sorted position into the global one
+  for (int i = tid; i <= classes; i += blockDim.x) gbase[i] -= lcnt[i];
+  __syncthreads();
+#pragma unroll
+  for (int h = 0; h < BK_PER; ++h) {
+    int c = (q[h >> 1] >> (16 * (h & 1))) & 0xffff;
+    c = c < classes ? c : classes;
+    if (r0 + h < count) {
+      const uint32_t lp = atomicAdd(&lcnt[c], 1u);
+      ent[lp] = ((uint32_t)c << 16) | (uint32_t)(tid * BK_PER + h);
+    }
+  }
+  __syncthreads();
+  for (int j = tid; j < rows; j += blockDim.x) {
+    const uint32_t e = ent[j];
+    idx[gbase[e >> 16] + j] = (uint32_t)row0 + (e & 0xffffu);
   }
 }
 
@@ -298,12 +351,18 @@ int run_bucket(const hygt_plan* p, int classes, uint64_t chunk_rows, const uint1
   uint32_t* cnt = reinterpret_cast<uint32_t*>(ws + w.counts);
   uint32_t* base = reinterpret_cast<uint32_t*>(ws + w.base);
   uint32_t* seg = reinterpret_cast<uint32_t*>(ws + w.seg);
-  bucket_hist_kernel<<<w.tiles, BK_THREADS, smem, st>>>(d_cls, count, classes, cnt, err);
+  bucket_hist_kernel<<<w.tiles, BK_THREADS, smem, st>>>(d_cls, count, classes, cnt, w.tiles, err);
   CU(cudaGetLastError());
   bucket_scan_kernel<<<w.chunks, BK_THREADS, 0, st>>>(cnt, base, seg, w.tiles,
                                                       w.tiles_per_chunk, classes, count);
   CU(cudaGetLastError());
-  bucket_scatter_kernel<<<w.tiles, BK_THREADS, smem, st>>>(d_cls, count, classes, base, idx);
+  const size_t smem_sc = (size_t)(((classes + 2 + 3) & ~3) + ((classes + 1 + 3) & ~3)) * 4 + BK_TILE * 4;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(bucket_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+    attr_set = true;
+  }
+  bucket_scatter_kernel<<<w.tiles, BK_THREADS, smem_sc, st>>>(d_cls, count, classes, base, w.tiles, idx);
   CU(cudaGetLastError());
   return ok();
 }
@@ -423,7 +482,7 @@ int run_tile(const hygt_plan* p, int dir, const float* x, float* y, const uint16
   P.tile_rows = p->tile_rows;
   P.energy = energy;
   P.err = err;
-  P.load_policy = env_int("HYGT_LOAD_POLICY", 0);
+  P.load_policy = env_int("HYGT_LOAD_POLICY", 1);
   int occ = 0;
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, TILE_THREADS, p->tile_smem[dir]));
   if (occ < 1) return fail(HYGT_ERR_CUDA, "hygt: tile kernel does not fit on an SM");
@@ -491,7 +550,7 @@ int setup_tile(hygt_plan* p, const double* angles, const uint16_t* perms) {
     vpt = ev;
   }
   if (l < 0 || env_int("HYGT_TILE", 1) == 0) return HYGT_OK;
-  const int rows = env_int("HYGT_TILE_ROWS", 4096);
+  const int rows = 8 * TILE_THREADS;  // the tile sort loads 8 class ids per thread
   size_t cb[2], gb[2];
   if (int s = build_interleaved(p, angles, perms, l, vpt, cb, gb)) return s;
   size_t smem_max = 0;
@@ -624,6 +683,23 @@ int run_apply(const hygt_plan* p, int dir, const float* x, float* y, const uint1
   if (!x || !y) return fail(HYGT_ERR_ARGUMENT, "hygt: null data pointer");
   if (count > 0xFFFFFFFFull) return fail(HYGT_ERR_ARGUMENT, "hygt: at most 2^32-1 rows per call");
   const WsLayout w = ws_layout(p->classes, p->chunk_rows, count);
+  if (p->jit.ok && !energy) {
+    const bool bk = d_cls && p->classes > 1;
+    if (d_cls) {
+      if (!d_ws || ws_bytes < w.total) return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
+      if (!(flags & HYGT_REUSE_BUCKETS)) {
+        const int s = run_bucket(p, p->classes, p->chunk_rows, d_cls, count, d_ws, ws_bytes, st);
+        if (s) return s;
+      }
+    }
+    char* ws = static_cast<char*>(d_ws);
+    if (jit_launch(p->jit, dir, x, y, bk ? reinterpret_cast<const uint32_t*>(ws + w.idx) : nullptr,
+                   bk ? reinterpret_cast<const uint32_t*>(ws + w.seg) : nullptr,
+                   bk ? (uint32_t)(w.chunks * (p->classes + 1)) : 0u, count, p->classes,
+                   p->num_sms, st))
+      return fail(HYGT_ERR_CUDA, std::string("hygt: jit launch failed: ") + cudaGetErrorString(cudaGetLastError()));
+    return ok();
+  }
   if (p->tile) {
     if (d_cls && (!d_ws || ws_bytes < 256)) return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
     return run_tile(p, dir, x, y, d_cls, count, energy,
@@ -749,6 +825,18 @@ extern "C" int hygt_plan_create(int log2_n, int rounds, int class_count, const d
       if (fn && apply_smem(p, d) > 48 * 1024)
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)apply_smem(p, d));
   }
+  if (jit_supported(log2_n, class_count, rounds) && env_int("HYGT_JIT", 1) != 0) {
+    std::string err;
+    if (jit_build(log2_n, rounds, class_count, angles, perms, p->perm_mask, p->algo == 0, p->jit, err)) {
+      jit_release(p->jit);  // stay on the precompiled kernels
+      if (env_int("HYGT_JIT_REQUIRED", 0)) {
+        free_plan(p);
+        return fail(HYGT_ERR_CUDA, err);
+      }
+    }
+    // class runs long enough that a CTA range stays inside one or two class bodies
+    if (p->jit.ok) p->chunk_rows = chunk_env >= 0 ? (uint64_t)chunk_env : ((uint64_t)1 << 18);
+  }
   if (int s = setup_tile(p, angles, perms)) {
     free_plan(p);
     return s;
@@ -769,19 +857,19 @@ extern "C" int hygt_plan_destroy(hygt_plan* plan) {
 extern "C" int hygt_plan_algorithm(const hygt_plan* plan) { return plan ? plan->algo : -1; }
 
 extern "C" int hygt_plan_path(const hygt_plan* plan) {
-  return plan ? (plan->tile ? 1 : plan->seg ? 2 : 0) : -1;
+  return plan ? (plan->jit.ok ? 3 : plan->tile ? 1 : plan->seg ? 2 : 0) : -1;
 }
 
 extern "C" size_t hygt_workspace_bytes(const hygt_plan* plan, uint64_t count) {
   if (!plan) return 0;
-  if (plan->tile) return 256;
+  if (plan->tile && !plan->jit.ok) return 256;
   return ws_layout(plan->classes, plan->chunk_rows, count).total;
 }
 
 extern "C" int hygt_bucket(const hygt_plan* plan, const uint16_t* d_cls, uint64_t count,
                            void* d_ws, size_t ws_bytes, void* stream) {
   if (!plan) return fail(HYGT_ERR_ARGUMENT, "hygt_bucket: null plan");
-  if (plan->tile) return ok();  // tile plans sort each tile in shared memory
+  if (plan->tile && !plan->jit.ok) return ok();  // tile plans sort each tile in shared memory
   return run_bucket(plan, plan->classes, plan->chunk_rows, d_cls, count, d_ws, ws_bytes,
                     as_stream(stream));
 }

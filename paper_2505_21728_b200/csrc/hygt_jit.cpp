@@ -1,0 +1,356 @@
+// hygt_jit.cpp -- plan-specialised HyGT kernels for short rows (N <= 64), compiled at plan
+// creation with NVRTC for sm_100a.
+//
+// The transform of each class is emitted as straight-line CUDA: every butterfly is two FFMAs
+// whose coefficients are immediates (no coefficient loads at all), every permutation is a
+// compile-time register renaming (no shared-memory round trip), and the final scales are
+// immediate multiplies. One kernel per direction holds all classes behind a switch on the row's
+// class; rows are class-sorted per tile in shared memory (as in hygt_tile.cuh) so warps are
+// class-uniform and only one case body is live per warp. A row is owned by one lane; HBM traffic
+// stays coalesced through a bank-swizzled per-warp transpose buffer (cooperative 128-bit loads of
+// the warp's 32 rows, then each lane reads its own row).
+//
+// Reference arithmetic: butterflies and order as transform.hpp:45-66 / model.hpp:77-79, gathers
+// as transform.hpp:75-80 (inverse: scatter first, :88-93); coefficients from hygt_plan.cpp.
+#include "hygt_jit.h"
+
+#include <nvrtc.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <sstream>
+#include <thread>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+namespace hygt_gpu {
+
+namespace {
+
+std::string lit(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  char b[40];
+  std::snprintf(b, sizeof b, "__int_as_float(0x%08x)", u);
+  return b;
+}
+
+// Chunk swizzle of the transpose buffer: row r, 16-byte chunk q -> q ^ swz(r).
+const char* kSwizzle[] = {
+    /*log2n=2*/ "0", /*3*/ "((r >> 2) & 1)", /*4*/ "((r >> 1) & 3)", /*5*/ "(r & 7)", /*6*/ "(r & 7)"};
+
+const char* kPrologue = R"CUDA(
+typedef unsigned int u32;
+typedef unsigned long long u64;
+typedef unsigned short u16;
+#define FULL 0xffffffffu
+// Rows are visited in class-bucketed order (idx: position -> row; seg_end: [chunks][C+1] run
+// ends, bin C = invalid ids). Each CTA streams a contiguous range of positions, so all its warps
+// sit in the same class run -- one class body hot in the instruction cache. idx == 0: identity
+// order, single class.
+extern "C" __global__ void __launch_bounds__(WARPS * 32, MINB)
+hygt_jit_kernel(const float* __restrict__ x, float* __restrict__ y, const u32* __restrict__ idx,
+                const u32* __restrict__ seg_end, u32 nseg, u64 count, int C, u64 span) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float4* wb = (float4*)sm + (size_t)warp * 32 * NQ;
+  const u64 beg = (u64)blockIdx.x * span;
+  if (beg >= count) return;
+  const u64 end = beg + span < count ? beg + span : count;
+  const float4* x4 = (const float4*)x;
+  float4* y4 = (float4*)y;
+  // per-lane walk over the run ends (positions only increase)
+  u32 f = 0;
+  if (idx) {
+    u32 lo = 0, hi = nseg;
+    const u64 p = beg + (u64)warp * 32 + lane;
+    while (lo < hi) {
+      const u32 mid = (lo + hi) >> 1;
+      if ((u64)__ldg(seg_end + mid) <= p) lo = mid + 1; else hi = mid;
+    }
+    f = lo;
+  }
+  auto meta = [&](u64 p, u32& row, u32& c) {
+    if (p >= end) { row = 0; c = 0; return; }
+    if (!idx) { row = (u32)p; c = 0; return; }
+    while (f < nseg && (u64)__ldg(seg_end + f) <= p) ++f;
+    c = f % (u32)(C + 1);
+    row = __ldg(idx + p);
+  };
+  float4 pre[NQ];
+  u32 row_n, c_n;
+  auto issue = [&](u64 p0n, u32 rown) {
+    const int nr = end - p0n < 32 ? (int)(end - p0n) : 32;
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) {
+      const int cc = lane + 32 * k, r = cc / NQ, q = cc % NQ;
+      const u32 rr = __shfl_sync(FULL, rown, r);
+      if (r < nr) pre[k] = LOADX(x4 + (size_t)rr * NQ + q);
+    }
+  };
+  u64 p0 = beg + (u64)warp * 32;
+  meta(p0 + lane, row_n, c_n);
+  if (p0 < end) issue(p0, row_n);
+  for (; p0 < end; p0 += WARPS * 32) {
+    const u32 row = row_n, c = c_n;
+    const int nrows = end - p0 < 32 ? (int)(end - p0) : 32;
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) {
+      const int cc = lane + 32 * k, r = cc / NQ, q = cc % NQ;
+      if (r < nrows) wb[r * NQ + (q ^ SWZ)] = pre[k];
+    }
+    const u64 p1 = p0 + WARPS * 32;
+    if (p1 < end) {
+      meta(p1 + lane, row_n, c_n);
+      issue(p1, row_n);
+    }
+    __syncwarp();
+    float v[N];
+    {
+      const int r = lane;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const float4 a = wb[r * NQ + (q ^ SWZ)];
+        v[4 * q] = a.x; v[4 * q + 1] = a.y; v[4 * q + 2] = a.z; v[4 * q + 3] = a.w;
+      }
+    }
+    switch (c) {
+)CUDA";
+
+const char* kEpilogue = R"CUDA(
+      default: break;  // invalid class id: the row passes through unchanged (error flagged)
+    }
+    {
+      const int r = lane;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) wb[r * NQ + (q ^ SWZ)] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) {
+      const int cc = lane + 32 * k, r = cc / NQ, q = cc % NQ;
+      const u32 rr = __shfl_sync(FULL, row, r);
+      if (r < nrows) __stcs(y4 + (size_t)rr * NQ + q, wb[r * NQ + (q ^ SWZ)]);
+    }
+    __syncwarp();
+  }
+}
+)CUDA";
+
+std::string generate(int log2n, int classes, int warps, int minb, bool standard,
+                     const std::vector<ClassProgram>& progs) {
+  const int n = 1 << log2n;
+  std::ostringstream o;
+  const char* ld = std::getenv("HYGT_JIT_LOAD");
+  o << "#define LOADX " << (ld ? ld : "__ldg") << "\n";
+  o << "#define N " << n << "\n#define NQ " << n / 4 << "\n#define WARPS " << warps
+    << "\n#define MINB " << minb << "\n#define SWZ " << kSwizzle[log2n - 2] << "\n";
+  o << kPrologue;
+  // Each class body is emitted in SSA form: every butterfly defines two new values, gathers only
+  // rename (the generator tracks which value holds logical sample i), so the front end sees
+  // straight-line scalar code with no arrays to promote.
+  for (int c = 0; c < classes; ++c) {
+    o << "      case " << c << ": {\n";
+    const ClassProgram& pr = progs[c];
+    std::vector<std::string> cur(n);
+    for (int i = 0; i < n; ++i) cur[i] = "v[" + std::to_string(i) + "]";
+    int k = 0;
+    auto fresh = [&]() { return "t" + std::to_string(k++); };
+    for (const ProgOp& op : pr.ops) {
+      if (op.kind == 0) {
+        const std::string a = cur[op.m], b = cur[op.n], ym = fresh(), yn = fresh();
+        if (!standard)  // a' = a + t1 b ; b' = b - t2 a   (op.b = -t2)
+          o << "const float " << ym << "=fmaf(" << b << "," << lit(op.a) << "," << a << ");const float "
+            << yn << "=fmaf(" << a << "," << lit(op.b) << "," << b << ");\n";
+        else  // y_m = c a + s b ; y_n = c b - s a   (givens.hpp:44-47)
+          o << "const float " << ym << "=fmaf(" << a << "," << lit(op.a) << "," << b << "*" << lit(op.b)
+            << ");const float " << yn << "=fmaf(" << b << "," << lit(op.a) << ",-(" << a << "*"
+            << lit(op.b) << "));\n";
+        cur[op.m] = ym;
+        cur[op.n] = yn;
+      } else if (op.kind == 1) {
+        const auto& g = pr.gathers[op.arg];
+        std::vector<std::string> nxt(n);
+        for (int i = 0; i < n; ++i) nxt[i] = cur[g[i]];
+        cur.swap(nxt);
+      } else {
+        for (int i = 0; i < n; ++i) {
+          const std::string t = fresh();
+          o << "const float " << t << "=" << cur[i] << "*" << lit(pr.scales[i]) << ";";
+          cur[i] = t;
+        }
+        o << "\n";
+      }
+    }
+    // all samples were rewritten by the first pass, so these assignments never read an
+    // already-overwritten input
+    for (int i = 0; i < n; ++i) o << "v[" << i << "]=" << cur[i] << ";";
+    o << "\n      } break;\n";
+  }
+  o << kEpilogue;
+  return o.str();
+}
+
+std::mutex g_cache_mu;
+std::unordered_map<std::string, std::vector<char>> g_cubin_cache;  // source -> cubin
+
+int compile(const std::string& src, std::vector<char>& cubin, std::string& log) {
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_cubin_cache.find(src);
+    if (it != g_cubin_cache.end()) {
+      cubin = it->second;
+      return 0;
+    }
+  }
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, src.c_str(), "hygt_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
+    return 1;
+  std::vector<const char*> opts = {(std::getenv("HYGT_JIT_ARCH") ? std::getenv("HYGT_JIT_ARCH") : "--gpu-architecture=sm_100a"), "-default-device", "-lineinfo",
+                                   "--std=c++17", "-DNDEBUG"};
+  if (const char* e = std::getenv("HYGT_JIT_OPTS")) opts.push_back(e);
+  const nvrtcResult r = nvrtcCompileProgram(prog, (int)opts.size(), opts.data());
+  size_t ls = 0;
+  nvrtcGetProgramLogSize(prog, &ls);
+  log.resize(ls);
+  if (ls) nvrtcGetProgramLog(prog, &log[0]);
+  if (r != NVRTC_SUCCESS) {
+    nvrtcDestroyProgram(&prog);
+    return 1;
+  }
+  size_t cs = 0;
+  if (std::getenv("HYGT_JIT_ARCH")) nvrtcGetPTXSize(prog, &cs); else
+  nvrtcGetCUBINSize(prog, &cs);
+  cubin.resize(cs);
+  nvrtcGetCUBIN(prog, cubin.data());
+  nvrtcDestroyProgram(&prog);
+  if (const char* dump = std::getenv("HYGT_JIT_DUMP")) {  // development aid: keep the cubin
+    static int seq = 0;
+    const std::string path = std::string(dump) + "." + std::to_string(seq++) + ".cubin";
+    if (FILE* f = std::fopen(path.c_str(), "wb")) {
+      std::fwrite(cubin.data(), 1, cubin.size(), f);
+      std::fclose(f);
+    }
+  }
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_cubin_cache.emplace(src, cubin);
+  return 0;
+}
+
+}  // namespace
+
+int jit_compile_only(int log2n, int rounds, int classes, const double* angles,
+                     const uint16_t* perms, uint32_t mask, bool standard, size_t* cubin_bytes,
+                     std::string& err) {
+  const int warps = log2n >= 6 ? 8 : 16, minb = log2n >= 6 ? 1 : 2;
+  *cubin_bytes = 0;
+  for (int d = 0; d < 2; ++d) {
+    std::vector<ClassProgram> progs;
+    if (!build_programs(log2n, rounds, classes, angles, perms, mask, d == 0, standard, progs)) {
+      err = "unsafe";
+      return 3;
+    }
+    std::vector<char> cubin;
+    std::string log;
+    if (compile(generate(log2n, classes, warps, minb, standard, progs), cubin, log)) {
+      err = log;
+      return 5;
+    }
+    err += log;
+    *cubin_bytes += cubin.size();
+  }
+  return 0;
+}
+
+size_t jit_smem_bytes(int log2n, int classes, int warps, int tile_rows) {
+  (void)classes;
+  (void)tile_rows;
+  return (size_t)warps * 32 * (1u << log2n) * 4;  // per-warp transpose buffers
+}
+
+bool jit_supported(int log2n, int classes, int rounds) {
+  if (log2n < 2 || log2n > 5) return false;
+  // Measured: with many classes the class-bucketed 64-128 B row gathers this path
+  // needs cost more than its immediates save; the tile kernel serves those plans.
+  if (classes > 4) return false;
+  // NVRTC time grows superlinearly with the kernel body: ~16 s for N=16 x 35 classes x 3
+  // rounds (both directions), minutes for N=32 x 35 x 3. Bound the total butterflies per kernel.
+  const size_t butterflies = (size_t)classes * rounds * log2n * (1u << (log2n - 1));
+  return butterflies <= (size_t)35 * 3 * 4 * 8;
+}
+
+int jit_build(int log2n, int rounds, int classes, const double* angles, const uint16_t* perms,
+              uint32_t mask, bool standard, JitKernels& out, std::string& err) {
+  const int warps = log2n >= 6 ? 8 : 16, minb = log2n >= 6 ? 1 : 2;
+  out.warps = warps;
+  out.tile_rows = 0;
+  // generate + compile both directions concurrently (NVRTC is thread safe per program)
+  std::vector<char> cubins[2];
+  std::string logs[2];
+  int status[2] = {0, 0};
+  auto work = [&](int d) {
+    std::vector<ClassProgram> progs;
+    if (!build_programs(log2n, rounds, classes, angles, perms, mask, d == 0, standard, progs)) {
+      status[d] = 3;
+      logs[d] = "jit: scale-folded program unsafe";
+      return;
+    }
+    if (compile(generate(log2n, classes, warps, minb, standard, progs), cubins[d], logs[d])) {
+      status[d] = 5;
+      logs[d] = "jit: NVRTC compilation failed: " + logs[d].substr(0, 2000);
+    }
+  };
+  std::thread th(work, 1);
+  work(0);
+  th.join();
+  for (int d = 0; d < 2; ++d) {
+    if (status[d]) {
+      err = logs[d];
+      return status[d];
+    }
+    const std::vector<char>& cubin = cubins[d];
+    if (cudaLibraryLoadData(&out.lib[d], cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess ||
+        cudaLibraryGetKernel(&out.fn[d], out.lib[d], "hygt_jit_kernel") != cudaSuccess) {
+      err = "jit: cannot load the compiled module";
+      return 5;
+    }
+    out.smem = jit_smem_bytes(log2n, classes, warps, out.tile_rows);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaKernelSetAttributeForDevice(out.fn[d], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)out.smem, dev) != cudaSuccess) {
+      err = "jit: cannot set shared memory size";
+      return 5;
+    }
+  }
+  out.ok = true;
+  return 0;
+}
+
+void jit_release(JitKernels& k) {
+  for (int d = 0; d < 2; ++d)
+    if (k.lib[d]) cudaLibraryUnload(k.lib[d]);
+  k = JitKernels{};
+}
+
+int jit_launch(const JitKernels& k, int dir, const float* x, float* y, const uint32_t* idx,
+               const uint32_t* seg_end, uint32_t nseg, uint64_t count, int classes, int num_sms,
+               cudaStream_t st) {
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k.fn[dir], k.warps * 32, k.smem) != cudaSuccess || occ < 1)
+    occ = 1;
+  cudaGetLastError();
+  const uint64_t step = (uint64_t)k.warps * 32;
+  uint64_t grid = std::min<uint64_t>((uint64_t)num_sms * occ, (count + step - 1) / step);
+  if (grid < 1) grid = 1;
+  uint64_t span = (count + grid - 1) / grid;
+  span = (span + step - 1) / step * step;
+  void* args[] = {(void*)&x, (void*)&y, (void*)&idx, (void*)&seg_end, (void*)&nseg, (void*)&count,
+                  (void*)&classes, (void*)&span};
+  return cudaLaunchKernel((const void*)k.fn[dir], dim3((unsigned)grid), dim3(k.warps * 32), args, k.smem, st) == cudaSuccess ? 0 : 5;
+}
+
+}  // namespace hygt_gpu

@@ -1,0 +1,37 @@
+// hygt_jit.h -- NVRTC-specialised kernels for N <= 64 (see hygt_jit.cpp).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <string>
+
+#include "hygt_plan.h"
+
+namespace hygt_gpu {
+
+struct JitKernels {
+  bool ok = false;
+  cudaLibrary_t lib[2] = {nullptr, nullptr};
+  cudaKernel_t fn[2] = {nullptr, nullptr};
+  int warps = 16;
+  uint32_t tile_rows = 4096;
+  size_t smem = 0;
+};
+
+bool jit_supported(int log2n, int classes, int rounds);
+size_t jit_smem_bytes(int log2n, int classes, int warps, int tile_rows);
+// Returns 0, or a C-ABI status with `err` set.
+int jit_build(int log2n, int rounds, int classes, const double* angles, const uint16_t* perms,
+              uint32_t mask, bool standard, JitKernels& out, std::string& err);
+void jit_release(JitKernels& k);
+// Code generation + NVRTC only (no device needed): total cubin bytes of both directions.
+int jit_compile_only(int log2n, int rounds, int classes, const double* angles,
+                     const uint16_t* perms, uint32_t mask, bool standard, size_t* cubin_bytes,
+                     std::string& err);
+int jit_launch(const JitKernels& k, int dir, const float* x, float* y, const uint32_t* idx,
+               const uint32_t* seg_end, uint32_t nseg, uint64_t count, int classes, int num_sms,
+               cudaStream_t st);
+
+}  // namespace hygt_gpu

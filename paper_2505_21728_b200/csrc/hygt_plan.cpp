@@ -184,4 +184,62 @@ bool build_direction(const Layout& ly, int rounds, int classes, const double* an
   return true;
 }
 
+bool build_programs(int log2n, int rounds, int classes, const double* angles,
+                    const uint16_t* perms, uint32_t mask, bool fwd, bool standard,
+                    std::vector<ClassProgram>& out) {
+  const int n = 1 << log2n, half = n / 2;
+  const size_t a_count = (size_t)rounds * log2n * half;
+  out.assign(classes, ClassProgram{});
+  std::vector<double> sig(n);
+  for (int c = 0; c < classes; ++c) {
+    ClassProgram& pr = out[c];
+    const double* ang = angles + (size_t)c * a_count;
+    const uint16_t* pc = perms ? perms + (size_t)c * rounds * n : nullptr;
+    uint64_t gm = 0;
+    const auto gathers = exec_gathers(log2n, rounds, pc, mask, fwd, &gm);
+    for (int i = 0; i < n; ++i) sig[i] = 1.0;
+    auto gather = [&](int step) {
+      if (gathers[step].empty()) return;
+      std::vector<double> s2(n);
+      for (int i = 0; i < n; ++i) s2[i] = sig[gathers[step][i]];
+      sig.swap(s2);
+      pr.ops.push_back(ProgOp{1, 0, 0, 0.f, 0.f, (uint32_t)pr.gathers.size()});
+      pr.gathers.push_back(gathers[step]);
+    };
+    gather(0);
+    for (int k = 0; k < rounds; ++k) {
+      const int r = fwd ? k : rounds - 1 - k;
+      for (int pp = 0; pp < log2n; ++pp) {
+        const int p = fwd ? pp : log2n - 1 - pp;
+        const uint32_t kk = 1u << p;
+        const size_t base = ((size_t)r * log2n + p) * half;  // model.hpp:77-79
+        for (uint32_t j = 0; j < (uint32_t)half; ++j) {
+          const uint32_t m = j + (j & (0u - kk)), nn = m + kk;  // hypercube.hpp:73-74
+          const double th = fwd ? ang[base + j] : -ang[base + j];  // transform.hpp:57
+          const double cs = std::cos(th), sn = std::sin(th);       // transform.hpp:58-59
+          if (standard) {
+            pr.ops.push_back(ProgOp{0, (uint16_t)m, (uint16_t)nn, (float)cs, (float)sn, 0});
+          } else {
+            if (cs == 0.0) return false;
+            const double k1 = sn * sig[nn] / (cs * sig[m]);
+            const double k2 = sn * sig[m] / (cs * sig[nn]);
+            sig[m] *= cs;
+            sig[nn] *= cs;
+            if (!(std::fabs(k1) <= 0x1p100) || !(std::fabs(k2) <= 0x1p100)) return false;
+            if (!(std::fabs(sig[m]) >= 0x1p-96) || !(std::fabs(sig[nn]) >= 0x1p-96)) return false;
+            pr.ops.push_back(ProgOp{0, (uint16_t)m, (uint16_t)nn, (float)k1, (float)-k2, 0});
+          }
+        }
+      }
+      gather(k + 1);
+    }
+    if (!standard) {
+      pr.scales.resize(n);
+      for (int i = 0; i < n; ++i) pr.scales[i] = (float)sig[i];
+      pr.ops.push_back(ProgOp{2, 0, 0, 0.f, 0.f, 0});
+    }
+  }
+  return true;
+}
+
 }  // namespace hygt_gpu

@@ -21,6 +21,25 @@ struct DirTables {
   uint32_t stream_len = 0;     // float2 words per lane stream
 };
 
+// One class's transform as straight-line operations in execution order (for code generation):
+//   kind 0: butterfly on (m, n) with coefficients (a, b): scale-folded (t1, -t2) or standard (c, s)
+//   kind 1: gather new[i] = old[src[i]] (src in ClassProgram::gathers[arg])
+//   kind 2: final per-sample scales (ClassProgram::scales)
+struct ProgOp {
+  uint8_t kind;
+  uint16_t m, n;
+  float a, b;
+  uint32_t arg;
+};
+struct ClassProgram {
+  std::vector<ProgOp> ops;
+  std::vector<std::vector<int>> gathers;
+  std::vector<float> scales;
+};
+bool build_programs(int log2n, int rounds, int classes, const double* angles,
+                    const uint16_t* perms, uint32_t mask, bool fwd, bool standard,
+                    std::vector<ClassProgram>& out);
+
 // Lane-group width (log2 TPV) used for a dimension unless overridden.
 int default_lane_log2(int log2n);
 

@@ -290,6 +290,22 @@ __global__ void __launch_bounds__(THREADS, 2) hygt_tile_kernel(const TileParams 
   const uint32_t gstep_words = ((E + 7) / 8) * TPV;
   const uint64_t tiles = (P.count + T - 1) / T;
 
+  // class ids of a tile: 8 consecutive rows per thread (T == 8 * THREADS), one 128-bit load,
+  // prefetched one tile ahead so the sort never waits on HBM
+  auto load_ids = [&](uint64_t tl, uint32_t (&q)[4]) {
+    q[0] = q[1] = q[2] = q[3] = 0;
+    if (!sorted || tl >= tiles) return;
+    const uint64_t r0 = tl * T + (uint64_t)tid * 8;
+    if (r0 + 8 <= P.count && ((reinterpret_cast<uintptr_t>(P.cls + r0) & 15) == 0)) {
+      const uint4 v = __ldcs(reinterpret_cast<const uint4*>(P.cls + r0));
+      q[0] = v.x; q[1] = v.y; q[2] = v.z; q[3] = v.w;
+    } else {
+      for (int h = 0; h < 8; ++h)
+        if (r0 + h < P.count) q[h >> 1] |= (uint32_t)P.cls[r0 + h] << (16 * (h & 1));
+    }
+  };
+  uint32_t ids[4], ids_next[4];
+  load_ids(blockIdx.x, ids);
   for (uint64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const uint64_t row0 = tile * T;
     const int rows = (int)((P.count - row0) < (uint64_t)T ? (P.count - row0) : (uint64_t)T);
@@ -299,10 +315,11 @@ __global__ void __launch_bounds__(THREADS, 2) hygt_tile_kernel(const TileParams 
     if (sorted) {  // counting sort of the tile by class (bin C = invalid id)
       for (int i = tid; i < C + 2; i += THREADS) s_off[i] = 0;
       __syncthreads();
-      for (int i = tid; i < rows; i += THREADS) {
-        int c = P.cls[row0 + i];
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        int c = (ids[h >> 1] >> (16 * (h & 1))) & 0xffff;
         c = c < C ? c : C;
-        atomicAdd(&s_off[c + 1], 1u);  // same-address lanes serialise inside the ATOMS unit
+        if (tid * 8 + h < rows) atomicAdd(&s_off[c + 1], 1u);  // lanes serialise in the ATOMS unit
       }
       __syncthreads();
       if (warp == 0) {
@@ -320,17 +337,24 @@ __global__ void __launch_bounds__(THREADS, 2) hygt_tile_kernel(const TileParams 
         }
       }
       __syncthreads();
-      for (int i = tid; i < rows; i += THREADS) {
-        int c = P.cls[row0 + i];
-        if (c >= C) {
-          c = C;
-          atomicOr(P.err, 1u);
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        const int i = tid * 8 + h;
+        int c = (ids[h >> 1] >> (16 * (h & 1))) & 0xffff;
+        if (i < rows) {
+          if (c >= C) {
+            c = C;
+            atomicOr(P.err, 1u);
+          }
+          // unstable within a class: the order only affects which warp handles a row
+          const uint32_t b = atomicAdd(&s_off[c], 1u);
+          s_ent[b] = ((uint32_t)c << 16) | (uint32_t)i;
         }
-        // unstable within a class: the order only affects which warp handles a row
-        const uint32_t b = atomicAdd(&s_off[c], 1u);
-        s_ent[b] = ((uint32_t)c << 16) | (uint32_t)i;
       }
+      load_ids(tile + gridDim.x, ids_next);
       __syncthreads();
+#pragma unroll
+      for (int h = 0; h < 4; ++h) ids[h] = ids_next[h];
     }
 
     // entry of sorted position p: (class << 16) | local row; inactive positions map to row 0

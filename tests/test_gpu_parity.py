@@ -62,12 +62,14 @@ SEG_VARIANTS = {6: [0, 1, 2, 3], 7: [4, 5], 8: [6, 7, 8, 9]}
 
 
 def _variants(log2n):
-    out = [{"HYGT_TILE": "0", "HYGT_SEGMENT": "0", "HYGT_LANES_LOG2": str(l)} for l in LAYOUTS[log2n]]
+    out = [{"HYGT_JIT": "0", "HYGT_TILE": "0", "HYGT_SEGMENT": "0", "HYGT_LANES_LOG2": str(l)}
+           for l in LAYOUTS[log2n]]
     for v in SEG_VARIANTS.get(log2n, []):
         out.append({"HYGT_SEGMENT": "1", "HYGT_SEG_VARIANT": str(v)})
     for l, v in TILE_LAYOUTS.get(log2n, []):
-        out.append({"HYGT_TILE": "1", "HYGT_TILE_L": str(l), "HYGT_TILE_VPT": str(v),
-                    "HYGT_TILE_ROWS": "64"})  # tiny tiles: many tiles, sort + tails exercised
+        out.append({"HYGT_JIT": "0", "HYGT_TILE": "1", "HYGT_TILE_L": str(l), "HYGT_TILE_VPT": str(v)})
+    if log2n <= 5:  # plan-specialised NVRTC kernel (served for plans with <= 4 classes)
+        out.append({"HYGT_JIT": "1"})
     return out
 
 
@@ -304,3 +306,36 @@ def test_reference_adapter(cuda):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "adapter_check: ok" in r.stdout
+
+
+def test_jit_plan_matches_oracle(cuda, oracle_mod):
+    """The NVRTC plan-specialised path (coefficients as immediates, permutations as register
+    renames) on config-1 style plans: 1-4 classes, inter-round and final permutations, both
+    arithmetic forms, tails, invalid class ids."""
+    from paper_2505_21728_b200 import ArgumentError, HyGTModel
+    rng = np.random.default_rng(21)
+    for log2n, rounds, classes in [(2, 2, 1), (3, 3, 2), (4, 2, 1), (4, 3, 4), (5, 2, 3)]:
+        n = 1 << log2n
+        ang = rng.uniform(-np.pi, np.pi, (classes, rounds * n * log2n // 2))
+        inter = np.stack([np.stack([rng.permutation(n) for _ in range(rounds - 1)]) for _ in range(classes)]).astype(np.uint16)
+        fin = np.stack([rng.permutation(n) for _ in range(classes)]).astype(np.uint16)
+        models = [HyGTModel(log2n, rounds, ang[c], fin[c]) for c in range(classes)]
+        full = np.concatenate([inter, fin[:, None, :]], 1)
+        rows = 5000 + 17
+        x = (rng.standard_normal((rows, n)) * 16).astype(np.float32)
+        cls = rng.integers(0, classes, rows).astype(np.uint16)
+        for standard in (False, True):
+            plan = _plan(models, inter, standard)
+            assert plan.path == "jit", plan.path
+            xd, cd = torch.from_numpy(x).to(cuda), torch.from_numpy(cls).to(cuda)
+            y = plan.forward(xd, cd)
+            plan.sync_status()
+            ref = oracle_mod.apply_batch(log2n, rounds, ang, full, (1 << rounds) - 1, x, cls)
+            check_close(y.cpu().numpy(), ref, x, f"jit fwd N={n} C={classes} std={standard}")
+            back = plan.inverse(y, cd)
+            check_close(back.cpu().numpy(), x, x, f"jit roundtrip N={n}")
+            if classes > 1:
+                cd[5] = classes
+                plan.forward(xd, cd)
+                with pytest.raises(ArgumentError):
+                    plan.sync_status()

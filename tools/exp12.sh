@@ -1,0 +1,5 @@
+K="timeout 300 python tools/kbench.py"
+$K 4:3:35:perm 4:3:1:perm
+HYGT_JIT=0 $K 4:3:35:perm
+timeout 300 python bench.py --no-cpu --no-e2e > gpurun_out/bench.log 2>&1; head -c 1500 gpurun_out/bench.log; echo
+timeout 1200 python -m pytest tests -m gpu -q -x --timeout 900 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; tail -15 gpurun_out/pytest_gpu.log
