@@ -207,6 +207,65 @@ def impl_reference(args):
 
 
 # ----------------------------------------------------------------------------- ours --------
+def impl_klt(args, rank, world, local, dev):
+    """Config 4: the dense per-class KLT comparison (tcgen05 3xTF32 grouped GEMM) on config 3's
+    rows; reports vectors/s, GB/s, TFLOP/s and the KLT/HyGT memory-footprint ratio."""
+    import torch
+    from paper_2505_21728_b200 import KLTPlan, TransformKind, memory_footprint
+    from paper_2505_21728_b200.synth import make_workload
+    w = make_workload(4)
+    rows = args.rows or w.cfg.count
+    cls = w.make_classes(rows, rank * rows)
+    x = w.make_rows(rows, cls, rank * rows)
+    y = torch.empty_like(x)
+    xr = torch.empty_like(x)
+    plan = KLTPlan(w.klt_bases())
+    ws = torch.empty(max(256, plan.workspace_bytes(rows)), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    for _ in range(max(args.warmup, 3)):
+        plan.forward(x, cls, out=y, workspace=ws)
+        plan.inverse(y, cls, out=xr, workspace=ws)
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    fw = inv = 0.0
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            ev[0].record(stream)
+            plan.forward(x, cls, out=y, workspace=ws)
+            ev[1].record(stream)
+            plan.inverse(y, cls, out=xr, workspace=ws)
+            ev[2].record(stream)
+            ev[2].synchronize()
+            fw += ev[0].elapsed_time(ev[1])
+            inv += ev[1].elapsed_time(ev[2])
+    ms = (fw + inv) / args.steps
+    n = w.n
+    hbm, hbm_kind = peaks()
+    bpr = bytes_per_row(n, w.cfg.classes)
+    launch_ms = (fw + inv) / (2 * args.steps)
+    achieved = rows * bpr / (launch_ms * 1e-3) / 1e9
+    flops = 2.0 * n * n  # algorithmic per row and direction (3xTF32 issues 3x this on the tensor cores)
+    err = (xr - x).abs().max().item() / x.abs().max().item()
+    if rank == 0:
+        print(json.dumps({
+            "metric": "KLT fwd+inv vectors/s (config 4 comparison path)", "value": rows / (ms * 1e-3),
+            "unit": "vectors/s", "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32 (3xTF32 tensor cores)", "data": "synthetic (config-3 rows)",
+            "config": {"workload": w.cfg.name, "rows_per_gpu": rows, "N": n, "classes": w.cfg.classes,
+                       "kernel": "klt_tc_kernel<64> tcgen05.mma kind::tf32 M=128 N=64, 3xTF32"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": None},
+            "tflops_algorithmic": rows * flops / (launch_ms * 1e-3) / 1e12,
+            "tflops_tensor_issued": 3 * rows * flops / (launch_ms * 1e-3) / 1e12,
+            "memory_ratio_units": memory_footprint(TransformKind.klt, 6, 1, 35) /
+                                  memory_footprint(TransformKind.hygt, 6, 4, 35),
+            "memory_ratio_fp32_bytes_vs_fp32_cs_tables": (35 * 64 * 64 * 4) / (35 * 768 * 8),
+            "roundtrip_max_rel": err, "clocks": clocks.summary(), "gpu_launches": 8 * args.steps,
+        }), flush=True)
+    return 0
+
+
 def impl_ours(args):
     import torch
     import torch.distributed as dist
@@ -215,6 +274,8 @@ def impl_ours(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    if args.config == 4:
+        return impl_klt(args, rank, world, local, dev)
     from paper_2505_21728_b200 import HyGTPlan
     from paper_2505_21728_b200.synth import make_workload
     w = make_workload(args.config)

@@ -369,6 +369,31 @@ int run_bucket(const hygt_plan* p, int classes, uint64_t chunk_rows, const uint1
 
 }  // namespace
 
+namespace hygt_gpu {
+// Class bucketing for other translation units (the KLT path): workspace size and offsets.
+size_t bucket_ws_bytes(int classes, uint64_t chunk_rows, uint64_t count) {
+  return ws_layout(classes, chunk_rows, count).total;
+}
+int bucket_rows(int classes, uint64_t chunk_rows, const uint16_t* d_cls, uint64_t count,
+                void* d_ws, size_t ws_bytes, bool run, cudaStream_t st, const uint32_t** idx,
+                const uint32_t** seg_end, uint32_t* nseg) {
+  const WsLayout w = ws_layout(classes, chunk_rows, count);
+  hygt_plan tmp;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&tmp.num_sms, cudaDevAttrMultiProcessorCount, dev);
+  if (run) {
+    const int s = run_bucket(&tmp, classes, chunk_rows, d_cls, count, d_ws, ws_bytes, st);
+    if (s) return s;
+  }
+  char* ws = static_cast<char*>(d_ws);
+  *idx = reinterpret_cast<const uint32_t*>(ws + w.idx);
+  *seg_end = reinterpret_cast<const uint32_t*>(ws + w.seg);
+  *nseg = (uint32_t)(w.chunks * (classes + 1));
+  return HYGT_OK;
+}
+}  // namespace hygt_gpu
+
 // ======================================================================= dispatch ========
 namespace {
 

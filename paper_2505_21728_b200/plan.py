@@ -273,18 +273,30 @@ class KLTPlan:
             except Exception:
                 pass
 
-    def _run(self, fn, x, cls, out, stream):
+    def workspace_bytes(self, count: int) -> int:
+        return _lib.lib().hygt_klt_workspace_bytes(self._h, count)
+
+    def _run(self, fn, x, cls, out, stream, workspace=None):
+        if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dtype != torch.float32:
+            raise ArgumentError("KLTPlan: x must be a CUDA float32 tensor")
+        if x.shape[-1] != self.n or not x.is_contiguous():
+            raise ArgumentError("matrix/vector dimension mismatch")
         count = x.numel() // self.n
         out = torch.empty_like(x) if out is None else out
-        _check(fn(self._h, x.data_ptr(), out.data_ptr(), _dev_ptr(cls), count, None, 0,
-                  _stream_ptr(stream)))
+        ws = workspace
+        if ws is None:
+            ws = torch.empty(max(256, self.workspace_bytes(count)), dtype=torch.uint8, device=x.device)
+        _check(fn(self._h, x.data_ptr(), out.data_ptr(), _dev_ptr(cls), count, ws.data_ptr(),
+                  ws.numel(), _stream_ptr(stream)))
         return out
 
-    def forward(self, x, cls=None, out=None, stream=None):
-        return self._run(_lib.lib().hygt_klt_forward_f32, x, cls, out, stream)
+    def forward(self, x, cls=None, out=None, stream=None, workspace=None):
+        """y = K_c x per row on the tensor cores (3xTF32), rows of class c = cls[row]."""
+        return self._run(_lib.lib().hygt_klt_forward_f32, x, cls, out, stream, workspace)
 
-    def inverse(self, y, cls=None, out=None, stream=None):
-        return self._run(_lib.lib().hygt_klt_inverse_f32, y, cls, out, stream)
+    def inverse(self, y, cls=None, out=None, stream=None, workspace=None):
+        """x = K_c^T y per row."""
+        return self._run(_lib.lib().hygt_klt_inverse_f32, y, cls, out, stream, workspace)
 
 
 # ------------------------------------------------ single-vector drop-ins (transform.hpp) ----

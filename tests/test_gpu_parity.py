@@ -272,7 +272,7 @@ def test_fixed_random_multiclass_vs_oracle(cuda, oracle_mod):
 
 def test_klt_golden(cuda, golden):
     from paper_2505_21728_b200 import KLTPlan
-    plan = KLTPlan(golden["klt_k"])
+    plan = KLTPlan(golden["klt_k"])  # n = 16: tcgen05 3xTF32 path
     x = golden["klt_x"]
     xd = torch.from_numpy(x).to(cuda)
     cd = torch.from_numpy(golden["klt_cls"]).to(cuda)
@@ -293,6 +293,12 @@ def test_klt_config4_vs_oracle(cuda, oracle_mod):
     check_close(y.cpu().numpy(), ref, x.cpu().numpy(), "cfg4 klt fwd")
     back = plan.inverse(y, cls)
     check_close(back.cpu().numpy(), x.cpu().numpy(), x.cpu().numpy(), "cfg4 klt roundtrip")
+    # tails and a single class
+    one = KLTPlan(k[:1])
+    xs = x[:1000]
+    ys = one.forward(xs)
+    ref1 = oracle_mod.klt_apply(k[:1], xs.cpu().numpy())
+    check_close(ys.cpu().numpy(), ref1, xs.cpu().numpy(), "klt single class")
 
 
 def test_reference_adapter(cuda):
