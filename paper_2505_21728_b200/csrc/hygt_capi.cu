@@ -23,6 +23,7 @@
 #include "hygt_jit.h"
 
 using namespace hygt_gpu;
+#include "hygt_dispatch.h"
 
 // ============================================================================ errors =====
 namespace {
@@ -92,6 +93,7 @@ struct hygt_plan {
   bool seg = false;
   int seg_variant = 0;
   size_t seg_smem[2] = {0, 0};
+  size_t seg_energy_smem = 0;
   unsigned long long* d_fixed_err = nullptr;
   std::mutex* fixed_mu = nullptr;
 };
@@ -397,39 +399,6 @@ int bucket_rows(int classes, uint64_t chunk_rows, const uint16_t* d_cls, uint64_
 // ======================================================================= dispatch ========
 namespace {
 
-using ApplyFn = void (*)(ApplyParams);
-
-template <int LOG2N, int L>
-ApplyFn pick_apply(bool standard, bool fwd, bool energy) {
-  if (standard) {
-    if (!fwd) return hygt_apply_kernel<LOG2N, L, true, false, false>;
-    return energy ? hygt_apply_kernel<LOG2N, L, true, true, true>
-                  : hygt_apply_kernel<LOG2N, L, true, true, false>;
-  }
-  if (!fwd) return hygt_apply_kernel<LOG2N, L, false, false, false>;
-  return energy ? hygt_apply_kernel<LOG2N, L, false, true, true>
-                : hygt_apply_kernel<LOG2N, L, false, true, false>;
-}
-
-// Instantiated (log2 N, log2 TPV) layouts.
-ApplyFn select_apply(int log2n, int l, bool standard, bool fwd, bool energy) {
-  switch (log2n * 16 + l) {
-    case 1 * 16 + 0: return pick_apply<1, 0>(standard, fwd, energy);
-    case 2 * 16 + 0: return pick_apply<2, 0>(standard, fwd, energy);
-    case 3 * 16 + 0: return pick_apply<3, 0>(standard, fwd, energy);
-    case 4 * 16 + 0: return pick_apply<4, 0>(standard, fwd, energy);
-    case 4 * 16 + 2: return pick_apply<4, 2>(standard, fwd, energy);
-    case 5 * 16 + 0: return pick_apply<5, 0>(standard, fwd, energy);
-    case 6 * 16 + 0: return pick_apply<6, 0>(standard, fwd, energy);
-    case 6 * 16 + 1: return pick_apply<6, 1>(standard, fwd, energy);
-    case 6 * 16 + 2: return pick_apply<6, 2>(standard, fwd, energy);
-    case 7 * 16 + 2: return pick_apply<7, 2>(standard, fwd, energy);
-    case 8 * 16 + 1: return pick_apply<8, 1>(standard, fwd, energy);
-    case 8 * 16 + 2: return pick_apply<8, 2>(standard, fwd, energy);
-    default: return nullptr;
-  }
-}
-
 constexpr int APPLY_THREADS = 256;
 
 size_t apply_smem(const hygt_plan* p, int dir) {
@@ -439,40 +408,6 @@ size_t apply_smem(const hygt_plan* p, int dir) {
 
 
 // ---- tile path --------------------------------------------------------------------------
-using TileFn = void (*)(TileParams);
-
-constexpr int TILE_THREADS = 512;
-
-template <int LOG2N, int L, int VPT>
-TileFn pick_tile(bool standard, bool fwd, bool energy) {
-  constexpr int TT = TILE_THREADS;
-  if (standard) {
-    if (!fwd) return hygt_tile_kernel<LOG2N, L, VPT, true, false, false, TT>;
-    return energy ? hygt_tile_kernel<LOG2N, L, VPT, true, true, true, TT>
-                  : hygt_tile_kernel<LOG2N, L, VPT, true, true, false, TT>;
-  }
-  if (!fwd) return hygt_tile_kernel<LOG2N, L, VPT, false, false, false, TT>;
-  return energy ? hygt_tile_kernel<LOG2N, L, VPT, false, true, true, TT>
-                : hygt_tile_kernel<LOG2N, L, VPT, false, true, false, TT>;
-}
-
-// Instantiated (log2 N, log2 TPV, rows per lane group) tile layouts; the first of each N is the
-// default. All have E = N / TPV >= 4.
-TileFn select_tile(int log2n, int l, int vpt, bool standard, bool fwd, bool energy) {
-  switch (log2n * 256 + l * 16 + vpt) {
-    case 2 * 256 + 0 * 16 + 2: return pick_tile<2, 0, 2>(standard, fwd, energy);
-    case 3 * 256 + 1 * 16 + 2: return pick_tile<3, 1, 2>(standard, fwd, energy);
-    case 3 * 256 + 0 * 16 + 2: return pick_tile<3, 0, 2>(standard, fwd, energy);
-    
-    case 4 * 256 + 2 * 16 + 2: return pick_tile<4, 2, 2>(standard, fwd, energy);
-    case 4 * 256 + 1 * 16 + 2: return pick_tile<4, 1, 2>(standard, fwd, energy);
-    case 4 * 256 + 0 * 16 + 1: return pick_tile<4, 0, 1>(standard, fwd, energy);
-    case 5 * 256 + 2 * 16 + 2: return pick_tile<5, 2, 2>(standard, fwd, energy);
-    case 5 * 256 + 3 * 16 + 2: return pick_tile<5, 3, 2>(standard, fwd, energy);
-    default: return nullptr;
-  }
-}
-
 void default_tile_layout(int log2n, int* l, int* vpt) {
   switch (log2n) {
     case 2: *l = 0; *vpt = 2; break;
@@ -598,8 +533,6 @@ int setup_tile(hygt_plan* p, const double* angles, const uint16_t* perms) {
 }
 
 // ---- segment path -----------------------------------------------------------------------
-using SegFn = void (*)(SegParams);
-constexpr int SEG_THREADS = 256;
 
 struct SegVariant {
   int log2n, l, vpt;
@@ -615,35 +548,6 @@ constexpr SegVariant kSegVariants[] = {
 // N=128 -> (L=2, VPT=1, prefetch), N=256 -> (L=1, VPT=1)
 int default_seg_variant(int log2n) { return log2n == 6 ? 1 : log2n == 7 ? 4 : log2n == 8 ? 8 : -1; }
 
-template <int LOG2N, int L, int VPT, bool PF>
-SegFn pick_seg(bool standard, bool fwd, bool energy) {
-  constexpr int TT = SEG_THREADS;
-  if (standard) {
-    if (!fwd) return hygt_segment_kernel<LOG2N, L, VPT, true, false, false, PF, TT>;
-    return energy ? hygt_segment_kernel<LOG2N, L, VPT, true, true, true, PF, TT>
-                  : hygt_segment_kernel<LOG2N, L, VPT, true, true, false, PF, TT>;
-  }
-  if (!fwd) return hygt_segment_kernel<LOG2N, L, VPT, false, false, false, PF, TT>;
-  return energy ? hygt_segment_kernel<LOG2N, L, VPT, false, true, true, PF, TT>
-                : hygt_segment_kernel<LOG2N, L, VPT, false, true, false, PF, TT>;
-}
-
-SegFn select_seg(int variant, bool standard, bool fwd, bool energy) {
-  switch (variant) {
-    case 0: return pick_seg<6, 1, 1, true>(standard, fwd, energy);
-    case 1: return pick_seg<6, 1, 2, false>(standard, fwd, energy);
-    case 2: return pick_seg<6, 2, 2, true>(standard, fwd, energy);
-    case 3: return pick_seg<6, 0, 1, false>(standard, fwd, energy);
-    case 4: return pick_seg<7, 2, 1, true>(standard, fwd, energy);
-    case 5: return pick_seg<7, 2, 2, false>(standard, fwd, energy);
-    case 6: return pick_seg<8, 2, 1, false>(standard, fwd, energy);
-    case 7: return pick_seg<8, 2, 1, true>(standard, fwd, energy);
-    case 8: return pick_seg<8, 1, 1, false>(standard, fwd, energy);
-    case 9: return pick_seg<8, 3, 2, false>(standard, fwd, energy);
-    default: return nullptr;
-  }
-}
-
 int setup_segment(hygt_plan* p, const double* angles, const uint16_t* perms) {
   if (p->tile || env_int("HYGT_SEGMENT", 1) == 0) return HYGT_OK;
   int variant = default_seg_variant(p->log2n);
@@ -656,12 +560,16 @@ int setup_segment(hygt_plan* p, const double* angles, const uint16_t* perms) {
   size_t cb[2], gb[2];
   if (int s = build_interleaved(p, angles, perms, sv.l, sv.vpt, cb, gb)) return s;
   for (int d = 0; d < 2; ++d) {
+    // the permutation scratch exists only when the plan has permutations
     p->seg_smem[d] = cb[d] + gb[d] +
-                     (size_t)(SEG_THREADS / 32) * tile_scratch_floats(p->log2n, sv.l, sv.vpt) * 4;
+                     (p->gmask[d] ? (size_t)(SEG_THREADS / 32) * tile_scratch_floats(p->log2n, sv.l, sv.vpt) * 4 : 0);
+    if (d == 0)  // fused energy: per-warp fp32 partial sums [E][32] (seg_energy_smem)
+      p->seg_energy_smem = p->seg_smem[0] + (size_t)(SEG_THREADS / 32) * ((1u << p->log2n) >> sv.l) * 32 * 4;
     if (p->seg_smem[d] > 220 * 1024) return HYGT_OK;
     for (int en = 0; en < 2; ++en) {
       SegFn fn = select_seg(variant, p->algo == 0, d == 0, en == 1);
-      if (fn) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->seg_smem[d]);
+      if (fn) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(en ? p->seg_energy_smem : p->seg_smem[d]));
     }
   }
   p->seg = true;
@@ -687,15 +595,16 @@ int run_segment(const hygt_plan* p, int dir, const float* x, float* y, uint64_t 
   P.gmask = p->gmask[dir];
   P.energy = energy;
   (void)bucketed;
+  const size_t smem = energy ? p->seg_energy_smem : p->seg_smem[dir];
   int occ = 0;
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, SEG_THREADS, p->seg_smem[dir]));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, SEG_THREADS, smem));
   if (occ < 1) return fail(HYGT_ERR_CUDA, "hygt: segment kernel does not fit on an SM");
   const uint64_t ctas_max = (uint64_t)p->num_sms * occ;
   const uint64_t min_span = 2048;
   uint64_t ctas = std::min<uint64_t>(ctas_max, (count + min_span - 1) / min_span);
   if (ctas < 1) ctas = 1;
   P.cta_span = (count + ctas - 1) / ctas;
-  fn<<<(unsigned)ctas, SEG_THREADS, p->seg_smem[dir], st>>>(P);
+  fn<<<(unsigned)ctas, SEG_THREADS, smem, st>>>(P);
   CU(cudaGetLastError());
   return ok();
 }

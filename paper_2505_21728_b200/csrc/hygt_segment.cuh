@@ -7,7 +7,7 @@
 // segments inside it: for each segment it stages that class's coefficient / scale / gather
 // tables into shared memory once, then every warp processes VPT rows per lane group with all
 // coefficient loads shared by the group's rows and broadcast across the warp. The fused energy
-// epilogue (statistics.hpp:69-77 diagonal) accumulates y^2 per lane in fp32 for at most 32 rows,
+// epilogue (statistics.hpp:69-77 diagonal) accumulates y^2 per lane in fp32 for at most 128 rows,
 // then reduces across the warp's lane groups in fp64 and adds into the [C][N] fp64 sums.
 #pragma once
 
@@ -62,6 +62,10 @@ __global__ void __launch_bounds__(THREADS, (LOG2N >= 8 ? 1 : 2)) hygt_segment_ke
   float4* s_coef = reinterpret_cast<float4*>(seg_smem);
   uint4* s_gidx = reinterpret_cast<uint4*>(s_coef + cw);
   float* s_scratch = reinterpret_cast<float*>(s_gidx + gw);
+  // fused energy: per-lane fp32 partial sums in shared memory, [E][32] per warp (keeps the
+  // accumulators out of the register file, which the E samples of a long row already fill)
+  float* s_acc = s_scratch + (P.gmask ? (size_t)WARPS * N * S : 0) + (size_t)(threadIdx.x >> 5) * E * 32 +
+                 (threadIdx.x & 31);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> L, t = lane & (TPV - 1);
   float* wscr = s_scratch + (size_t)warp * N * S;
@@ -81,7 +85,6 @@ __global__ void __launch_bounds__(THREADS, (LOG2N >= 8 ? 1 : 2)) hygt_segment_ke
     }
     f = lo;
   }
-  float acc[ENERGY ? E : 1];
   for (uint64_t pos = beg; pos < end; ++f) {
     const uint64_t stop = (uint64_t)__ldg(P.seg_end + f) < end ? (uint64_t)__ldg(P.seg_end + f) : end;
     const int c = (int)f;
@@ -101,19 +104,20 @@ __global__ void __launch_bounds__(THREADS, (LOG2N >= 8 ? 1 : 2)) hygt_segment_ke
     for (uint32_t i = tid; i < gw; i += THREADS) s_gidx[i] = __ldg(P.gidx + (size_t)c * gw + i);
     __syncthreads();
     if constexpr (ENERGY) {
-#pragma unroll
-      for (int s = 0; s < E; ++s) acc[s] = 0.f;
+#pragma unroll 8
+      for (int s = 0; s < E; ++s) s_acc[s * 32] = 0.f;
     }
     int acc_rows = 0;
     auto flush = [&]() {
       if constexpr (ENERGY) {
-        // fp32 partial sums of <= 32 rows per lane, reduced across the lane groups in fp64
-#pragma unroll
+        // fp32 partial sums of <= 128 rows per lane (relative rounding error < 128 * 2^-24),
+        // reduced across the lane groups in fp64
+#pragma unroll 4
         for (int s = 0; s < E; ++s) {
-          double d = (double)acc[s];
+          double d = (double)s_acc[s * 32];
 #pragma unroll
           for (int o = TPV; o < 32; o <<= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-          acc[s] = 0.f;
+          s_acc[s * 32] = 0.f;
           if (g == 0) atomicAdd(P.energy + (size_t)c * N + LY.elem(t, s), d);
         }
       }
@@ -176,14 +180,14 @@ __global__ void __launch_bounds__(THREADS, (LOG2N >= 8 ? 1 : 2)) hygt_segment_ke
         if constexpr (ENERGY) {
 #pragma unroll
           for (int k = 0; k < NP; ++k) {
-            acc[2 * k] = fmaf(v[r][k].x, v[r][k].x, acc[2 * k]);
-            acc[2 * k + 1] = fmaf(v[r][k].y, v[r][k].y, acc[2 * k + 1]);
+            s_acc[(2 * k) * 32] = fmaf(v[r][k].x, v[r][k].x, s_acc[(2 * k) * 32]);
+            s_acc[(2 * k + 1) * 32] = fmaf(v[r][k].y, v[r][k].y, s_acc[(2 * k + 1) * 32]);
           }
         }
       }
       if constexpr (ENERGY) {
         acc_rows += VPT;
-        if (acc_rows >= 32) {
+        if (acc_rows >= 128) {
           flush();
           acc_rows = 0;
         }
