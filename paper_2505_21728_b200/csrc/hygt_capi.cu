@@ -525,6 +525,7 @@ int setup_tile(hygt_plan* p, const double* angles, const uint16_t* perms) {
       TileFn fn = select_tile(p->log2n, l, vpt, p->algo == 0, d == 0, en == 1);
       if (fn) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->tile_smem[d]);
     }
+  cudaGetLastError();  // no sticky error from the attribute calls
   p->tile = true;
   p->tile_l = l;
   p->tile_vpt = vpt;
@@ -566,12 +567,17 @@ int setup_segment(hygt_plan* p, const double* angles, const uint16_t* perms) {
     if (d == 0)  // fused energy: per-warp fp32 partial sums [E][32] (seg_energy_smem)
       p->seg_energy_smem = p->seg_smem[0] + (size_t)(SEG_THREADS / 32) * ((1u << p->log2n) >> sv.l) * 32 * 4;
     if (p->seg_smem[d] > 220 * 1024) return HYGT_OK;
-    for (int en = 0; en < 2; ++en) {
-      SegFn fn = select_seg(variant, p->algo == 0, d == 0, en == 1);
-      if (fn) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(en ? p->seg_energy_smem : p->seg_smem[d]));
-    }
+    SegFn fn = select_seg(variant, p->algo == 0, d == 0, false);
+    if (fn) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->seg_smem[d]);
   }
+  // fused energy (forward only): its per-warp partial sums must fit next to the tables
+  if (p->seg_energy_smem <= 227 * 1024) {
+    SegFn fe = select_seg(variant, p->algo == 0, true, true);
+    if (fe) cudaFuncSetAttribute(fe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->seg_energy_smem);
+  } else {
+    p->seg_energy_smem = 0;  // energy requests use the bucketed apply kernel instead
+  }
+  cudaGetLastError();  // attribute calls must not leave a sticky error for the next launch check
   p->seg = true;
   p->seg_variant = variant;
   p->chunk_rows = 0;  // global class buckets
@@ -640,7 +646,7 @@ int run_apply(const hygt_plan* p, int dir, const float* x, float* y, const uint1
                     d_cls ? reinterpret_cast<uint32_t*>(static_cast<char*>(d_ws) + w.err) : nullptr, st);
   }
   const bool bucketed = d_cls && p->classes > 1;
-  if (p->seg && bucketed) {
+  if (p->seg && bucketed && (!energy || p->seg_energy_smem)) {
     if (!d_ws || ws_bytes < w.total) return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
     if (!(flags & HYGT_REUSE_BUCKETS)) {
       const int s = run_bucket(p, p->classes, 0, d_cls, count, d_ws, ws_bytes, st);
@@ -759,6 +765,7 @@ extern "C" int hygt_plan_create(int log2_n, int rounds, int class_count, const d
       if (fn && apply_smem(p, d) > 48 * 1024)
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)apply_smem(p, d));
   }
+  cudaGetLastError();
   if (jit_supported(log2_n, class_count, rounds) && env_int("HYGT_JIT", 1) != 0) {
     std::string err;
     if (jit_build(log2_n, rounds, class_count, angles, perms, p->perm_mask, p->algo == 0, p->jit, err)) {
