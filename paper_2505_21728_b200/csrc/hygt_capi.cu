@@ -444,11 +444,12 @@ int run_tile(const hygt_plan* p, int dir, const float* x, float* y, const uint16
   P.err = err;
   P.load_policy = env_int("HYGT_LOAD_POLICY", 1);
   int occ = 0;
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, TILE_THREADS, p->tile_smem[dir]));
+  const int tthreads = p->tile_vpt >= 8 ? 256 : TILE_THREADS;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, tthreads, p->tile_smem[dir]));
   if (occ < 1) return fail(HYGT_ERR_CUDA, "hygt: tile kernel does not fit on an SM");
   const uint64_t tiles = (count + p->tile_rows - 1) / p->tile_rows;
   const uint64_t ctas = std::min<uint64_t>(tiles, (uint64_t)p->num_sms * occ);
-  fn<<<(unsigned)ctas, TILE_THREADS, p->tile_smem[dir], st>>>(P);
+  fn<<<(unsigned)ctas, tthreads, p->tile_smem[dir], st>>>(P);
   CU(cudaGetLastError());
   return ok();
 }
@@ -510,13 +511,15 @@ int setup_tile(hygt_plan* p, const double* angles, const uint16_t* perms) {
     vpt = ev;
   }
   if (l < 0 || env_int("HYGT_TILE", 1) == 0) return HYGT_OK;
-  const int rows = 8 * TILE_THREADS;  // the tile sort loads 8 class ids per thread
+  const int tthreads = vpt >= 8 ? 256 : TILE_THREADS;
+  const int rows = (vpt >= 8 ? 16 : 8) * tthreads;  // the tile sort loads 8 or 16 ids per thread
   size_t cb[2], gb[2];
-  if (int s = build_interleaved(p, angles, perms, l, vpt, cb, gb)) return s;
+  const int vpt_real = vpt >= 8 ? vpt - 8 : vpt;
+  if (int s = build_interleaved(p, angles, perms, l, vpt_real, cb, gb)) return s;
   size_t smem_max = 0;
   for (int d = 0; d < 2; ++d) {
     p->tile_smem[d] = tile_smem_bytes(cb[d] * p->classes, gb[d] * p->classes, p->classes, rows,
-                                      TILE_THREADS / 32, tile_scratch_floats(p->log2n, l, vpt));
+                                      tthreads / 32, tile_scratch_floats(p->log2n, l, vpt_real));
     smem_max = std::max(smem_max, p->tile_smem[d]);
   }
   if (smem_max > 200 * 1024) return HYGT_OK;  // tables too large: stay on another path

@@ -259,7 +259,7 @@ HYGT_HD constexpr size_t tile_smem_bytes(size_t coef_bytes, size_t gidx_bytes, i
 }
 
 template <int LOG2N, int L, int VPT, bool STD, bool FWD, bool ENERGY, int THREADS>
-__global__ void __launch_bounds__(THREADS, 2) hygt_tile_kernel(const TileParams P) {
+__global__ void __launch_bounds__(THREADS, THREADS >= 512 ? 2 : 3) hygt_tile_kernel(const TileParams P) {
   using G = TileGeom<LOG2N, L>;
   constexpr Layout LY = G::LY;
   constexpr int N = G::N, TPV = G::TPV, E = G::E, CH = G::CH, NP = G::NP, V = G::V;
@@ -290,21 +290,26 @@ __global__ void __launch_bounds__(THREADS, 2) hygt_tile_kernel(const TileParams 
   const uint32_t gstep_words = ((E + 7) / 8) * TPV;
   const uint64_t tiles = (P.count + T - 1) / T;
 
-  // class ids of a tile: 8 consecutive rows per thread (T == 8 * THREADS), one 128-bit load,
+  // class ids of a tile: IDS consecutive rows per thread (T == IDS * THREADS), 128-bit loads,
   // prefetched one tile ahead so the sort never waits on HBM
-  auto load_ids = [&](uint64_t tl, uint32_t (&q)[4]) {
-    q[0] = q[1] = q[2] = q[3] = 0;
+  constexpr int IDS = THREADS >= 512 ? 8 : 16;
+  auto load_ids = [&](uint64_t tl, uint32_t (&q)[IDS / 2]) {
+#pragma unroll
+    for (int w = 0; w < IDS / 2; ++w) q[w] = 0;
     if (!sorted || tl >= tiles) return;
-    const uint64_t r0 = tl * T + (uint64_t)tid * 8;
-    if (r0 + 8 <= P.count && ((reinterpret_cast<uintptr_t>(P.cls + r0) & 15) == 0)) {
-      const uint4 v = __ldcs(reinterpret_cast<const uint4*>(P.cls + r0));
-      q[0] = v.x; q[1] = v.y; q[2] = v.z; q[3] = v.w;
+    const uint64_t r0 = tl * T + (uint64_t)tid * IDS;
+    if (r0 + IDS <= P.count && ((reinterpret_cast<uintptr_t>(P.cls + r0) & 15) == 0)) {
+#pragma unroll
+      for (int w = 0; w < IDS / 8; ++w) {
+        const uint4 v = __ldcs(reinterpret_cast<const uint4*>(P.cls + r0) + w);
+        q[4 * w] = v.x; q[4 * w + 1] = v.y; q[4 * w + 2] = v.z; q[4 * w + 3] = v.w;
+      }
     } else {
-      for (int h = 0; h < 8; ++h)
+      for (int h = 0; h < IDS; ++h)
         if (r0 + h < P.count) q[h >> 1] |= (uint32_t)P.cls[r0 + h] << (16 * (h & 1));
     }
   };
-  uint32_t ids[4], ids_next[4];
+  uint32_t ids[IDS / 2], ids_next[IDS / 2];
   load_ids(blockIdx.x, ids);
   for (uint64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const uint64_t row0 = tile * T;
@@ -316,10 +321,10 @@ __global__ void __launch_bounds__(THREADS, 2) hygt_tile_kernel(const TileParams 
       for (int i = tid; i < C + 2; i += THREADS) s_off[i] = 0;
       __syncthreads();
 #pragma unroll
-      for (int h = 0; h < 8; ++h) {
+      for (int h = 0; h < IDS; ++h) {
         int c = (ids[h >> 1] >> (16 * (h & 1))) & 0xffff;
         c = c < C ? c : C;
-        if (tid * 8 + h < rows) atomicAdd(&s_off[c + 1], 1u);  // lanes serialise in the ATOMS unit
+        if (tid * IDS + h < rows) atomicAdd(&s_off[c + 1], 1u);  // lanes serialise in the ATOMS unit
       }
       __syncthreads();
       if (warp == 0) {
@@ -338,8 +343,8 @@ __global__ void __launch_bounds__(THREADS, 2) hygt_tile_kernel(const TileParams 
       }
       __syncthreads();
 #pragma unroll
-      for (int h = 0; h < 8; ++h) {
-        const int i = tid * 8 + h;
+      for (int h = 0; h < IDS; ++h) {
+        const int i = tid * IDS + h;
         int c = (ids[h >> 1] >> (16 * (h & 1))) & 0xffff;
         if (i < rows) {
           if (c >= C) {
@@ -354,7 +359,7 @@ __global__ void __launch_bounds__(THREADS, 2) hygt_tile_kernel(const TileParams 
       load_ids(tile + gridDim.x, ids_next);
       __syncthreads();
 #pragma unroll
-      for (int h = 0; h < 4; ++h) ids[h] = ids_next[h];
+      for (int h = 0; h < IDS / 2; ++h) ids[h] = ids_next[h];
     }
 
     // entry of sorted position p: (class << 16) | local row; inactive positions map to row 0
