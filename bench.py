@@ -246,6 +246,7 @@ def impl_klt(args, rank, world, local, dev):
     achieved = rows * bpr / (launch_ms * 1e-3) / 1e9
     flops = 2.0 * n * n  # algorithmic per row and direction (3xTF32 issues 3x this on the tensor cores)
     err = (xr - x).abs().max().item() / x.abs().max().item()
+    traffic, traffic_src = measured_traffic(w.cfg.name) if rows == w.cfg.count else (None, None)
     if rank == 0:
         print(json.dumps({
             "metric": "KLT fwd+inv vectors/s (config 4 comparison path)", "value": rows / (ms * 1e-3),
@@ -255,7 +256,7 @@ def impl_klt(args, rank, world, local, dev):
             "config": {"workload": w.cfg.name, "rows_per_gpu": rows, "N": n, "classes": w.cfg.classes,
                        "kernel": "klt_tc_kernel<64> tcgen05.mma kind::tf32 M=128 N=64, 3xTF32"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": None},
+                         "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src},
             "tflops_algorithmic": rows * flops / (launch_ms * 1e-3) / 1e12,
             "tflops_tensor_issued": 3 * rows * flops / (launch_ms * 1e-3) / 1e12,
             "memory_ratio_units": memory_footprint(TransformKind.klt, 6, 1, 35) /
