@@ -84,7 +84,10 @@ int hygt_plan_algorithm(const hygt_plan* plan);
  * 1 = tile kernel (class sort inside each CTA, no bucketing pass; N <= 32),
  * 2 = class-segment kernel (global class buckets, one class table staged per CTA segment),
  * 3 = plan-specialised kernel compiled at plan creation (NVRTC, sm_100a; N <= 64): coefficients
- *     are instruction immediates and permutations register renames. */
+ *     are instruction immediates and permutations register renames,
+ * 4 = TMA-staged tile kernel (N = 16): tiles of rows moved HBM <-> shared memory by the bulk-copy
+ *     engine, class-sorted in shared memory, no bucketing pass. Forward-with-energy calls run on
+ *     the tile kernel instead. */
 int hygt_plan_path(const hygt_plan* plan);
 
 /* Device workspace for class bucketing of `count` rows. */
@@ -94,7 +97,8 @@ size_t hygt_workspace_bytes(const hygt_plan* plan, uint64_t count);
  * by hygt_sync_status(). */
 int hygt_bucket(const hygt_plan* plan, const uint16_t* d_cls, uint64_t count, void* d_ws,
                 size_t ws_bytes, void* stream);
-/* y = forward(x) row-wise (in place allowed). */
+/* y = forward(x) row-wise (in place allowed). d_x and d_y must be aligned to min(16, 4N) bytes
+ * (HYGT_ERR_ARGUMENT otherwise); class ids need no alignment. */
 int hygt_forward_f32(const hygt_plan* plan, const float* d_x, float* d_y, const uint16_t* d_cls,
                      uint64_t count, void* d_ws, size_t ws_bytes, uint32_t flags, void* stream);
 /* x = inverse(y) row-wise (in place allowed). */

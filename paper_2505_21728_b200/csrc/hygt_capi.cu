@@ -87,6 +87,12 @@ struct hygt_plan {
   uint32_t tunits[2] = {0, 0};
   uint4* d_tgidx[2] = {nullptr, nullptr};
   size_t tile_smem[2] = {0, 0};
+  // stage path (N = 16): TMA-staged tiles, element-ordered tables
+  bool stage = false;
+  uint32_t stage_rows = 0, stage_cw = 0, stage_block_words = 0;
+  float4* d_scoef[2] = {nullptr, nullptr};
+  uint16_t* d_sgtab[2] = {nullptr, nullptr};
+  size_t stage_smem[2] = {0, 0};
   // JIT path (N <= 64): NVRTC-specialised kernels, coefficients as immediates
   JitKernels jit;
   // segment path (N >= 64): same interleaved tables, one class staged per CTA segment
@@ -119,6 +125,8 @@ void free_plan(hygt_plan* p) {
     cudaFree(p->d_fgather[d]);
     cudaFree(p->d_tcoef[d]);
     cudaFree(p->d_tgidx[d]);
+    cudaFree(p->d_scoef[d]);
+    cudaFree(p->d_sgtab[d]);
   }
   cudaFree(p->d_codes);
   cudaFree(p->d_cos);
@@ -536,6 +544,156 @@ int setup_tile(hygt_plan* p, const double* angles, const uint16_t* perms) {
   return HYGT_OK;
 }
 
+// ---- stage path (hygt_stage.cuh) ----------------------------------------------------------
+unsigned long long* g_stage_trace = nullptr;  // debug hook, see hygt_debug_stage_trace
+// Element-ordered tables: per class, per execution step (round, pass) N/4 float4 units of the
+// per-element coefficient k_i of y_i = x_i + k_i x_{i^2^p} (scale-folded: k_m = t1, k_n = -t2;
+// standard: N/4 units of c_i then N/4 units of s'_i with s'_m = s, s'_n = -s), then N/4 units of
+// final scales (scale-folded only). Gathers: [C][R+1][N] u16 scratch offsets src * 128.
+int setup_stage(hygt_plan* p, const double* angles, const uint16_t* perms) {
+  StageFn probe = select_stage(p->log2n, p->algo == 0, true);
+  if (!probe || env_int("HYGT_STAGE", 1) == 0 || p->classes > STAGE_MAX_CLASSES) return HYGT_OK;
+  const int n = 1 << p->log2n, nc = n / 4, C = p->classes, R = p->rounds;
+  const bool standard = p->algo == 0;
+  const uint32_t step_units = (uint32_t)nc * (standard ? 2 : 1);
+  const uint32_t cw = (uint32_t)R * p->log2n * step_units + (standard ? 0u : (uint32_t)nc);
+  for (int d = 0; d < 2; ++d) {
+    std::vector<ClassProgram> progs;
+    if (!build_programs(p->log2n, R, C, angles, perms, p->perm_mask, d == 0, standard, progs))
+      return fail(HYGT_ERR_NUMERICAL, "hygt: stage table build failed");
+    std::vector<float4> coef((size_t)C * cw, make_float4(0.f, 0.f, 0.f, 0.f));
+    const uint32_t gs = stage_gstride(p->log2n, R) / 2;  // u16 per class
+    std::vector<uint16_t> gt((size_t)C * gs, 0);
+    std::vector<float> kc(n), ks(n);
+    for (int c = 0; c < C; ++c) {
+      float4* cc = &coef[(size_t)c * cw];
+      uint32_t step = 0;
+      int in_pass = 0;
+      for (const ProgOp& op : progs[c].ops) {
+        if (op.kind == 0) {
+          if (standard) {
+            kc[op.m] = kc[op.n] = op.a;
+            ks[op.m] = op.b;
+            ks[op.n] = -op.b;
+          } else {
+            kc[op.m] = op.a;
+            kc[op.n] = op.b;  // build_programs stores -k2 for the n side
+          }
+          if (++in_pass == n / 2) {
+            for (int u = 0; u < nc; ++u) {
+              cc[step * step_units + u] = make_float4(kc[4 * u], kc[4 * u + 1], kc[4 * u + 2], kc[4 * u + 3]);
+              if (standard)
+                cc[step * step_units + nc + u] =
+                    make_float4(ks[4 * u], ks[4 * u + 1], ks[4 * u + 2], ks[4 * u + 3]);
+            }
+            ++step;
+            in_pass = 0;
+          }
+        } else if (op.kind == 2) {
+          const std::vector<float>& sc = progs[c].scales;
+          for (int u = 0; u < nc; ++u)
+            cc[(size_t)R * p->log2n * step_units + u] = make_float4(sc[4 * u], sc[4 * u + 1], sc[4 * u + 2], sc[4 * u + 3]);
+        }
+      }
+      if (step != (uint32_t)R * p->log2n) return fail(HYGT_ERR_NUMERICAL, "hygt: stage step count");
+      uint64_t gm = 0;
+      const auto g = exec_gathers(p->log2n, R, perms ? perms + (size_t)c * R * n : nullptr,
+                                  p->perm_mask, d == 0, &gm);
+      for (int k = 0; k <= R; ++k)
+        for (size_t i = 0; i < g[k].size(); ++i)
+          gt[(size_t)c * gs + (size_t)k * n + i] = (uint16_t)(g[k][i] * 128);
+    }
+    int s = upload(&p->d_scoef[d], coef.data(), coef.size());
+    if (!s && p->gmask[d]) s = upload(&p->d_sgtab[d], gt.data(), gt.size());
+    if (s) return s;
+  }
+  // Tile rows: one batch of 32 * VPT sorted positions per consumer warp, including the padding
+  // of every class run to VPT; rows are indexed with 10 bits in the sort entries.
+  const long long tenv = env_int("HYGT_STAGE_ROWS", -1);
+  uint32_t T = (uint32_t)std::max(0, STAGE_WARPS * 32 * STAGE_VPT - (STAGE_VPT - 1) * C);
+  if (tenv > 0) T = (uint32_t)tenv;
+  T = std::min<uint32_t>(T, 1016) / 8 * 8;
+  size_t smem[2] = {0, 0};
+  for (; T >= 128; T -= 8) {
+    for (int d = 0; d < 2; ++d)
+      smem[d] = stage_smem_layout(p->log2n, STAGE_VPT, STAGE_WARPS, C, cw, R, T, p->gmask[d] != 0).total;
+    if (std::max(smem[0], smem[1]) <= 227 * 1024) break;
+  }
+  if (T < 128) return HYGT_OK;  // tables too large for the staged layout
+  for (int d = 0; d < 2; ++d) {
+    cudaFuncSetAttribute(select_stage(p->log2n, standard, d == 0),
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem[d]);
+    p->stage_smem[d] = smem[d];
+  }
+  cudaGetLastError();
+  p->stage = true;
+  p->stage_rows = T;
+  p->stage_cw = cw;
+  p->stage_block_words = stage_block_words(T, STAGE_VPT, C);
+  return HYGT_OK;
+}
+
+// Workspace of the stage path: error word, then one sorted entry block per tile.
+size_t stage_ws_bytes(const hygt_plan* p, uint64_t count) {
+  const uint64_t tiles = (count + p->stage_rows - 1) / p->stage_rows;
+  return 256 + tiles * p->stage_block_words * 2;
+}
+
+int run_stage_sort(const hygt_plan* p, const uint16_t* d_cls, uint64_t count, void* d_ws,
+                   size_t ws_bytes, cudaStream_t st) {
+  if (!d_ws || ws_bytes < stage_ws_bytes(p, count)) return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
+  if (count == 0) return ok();
+  StageSortParams S{};
+  S.cls = d_cls;
+  S.count = count;
+  S.classes = p->classes;
+  S.tile_rows = p->stage_rows;
+  S.block_words = p->stage_block_words;
+  S.ent = reinterpret_cast<uint16_t*>(static_cast<char*>(d_ws) + 256);
+  S.err = static_cast<uint32_t*>(d_ws);
+  const uint64_t tiles = (count + p->stage_rows - 1) / p->stage_rows;
+  const size_t smem = stage_align((uint32_t)(p->classes + 1) * 4u, 16) + p->stage_block_words * 2;
+  const uint64_t ctas = std::min<uint64_t>(tiles, (uint64_t)p->num_sms * 8);
+  select_stage_sort()<<<(unsigned)ctas, 256, smem, st>>>(S);
+  CU(cudaGetLastError());
+  return ok();
+}
+
+bool stage_usable(const hygt_plan* p, const float* x, const float* y, const double* energy) {
+  (void)x; (void)y;
+  return p->stage && !energy;  // run_apply has checked the 16 B row alignment
+}
+
+int run_stage(const hygt_plan* p, int dir, const float* x, float* y, const uint16_t* d_cls,
+              uint64_t count, void* d_ws, size_t ws_bytes, uint32_t flags, cudaStream_t st) {
+  const bool sorted = d_cls && p->classes > 1;
+  if (sorted && !(flags & HYGT_REUSE_BUCKETS))
+    if (int s = run_stage_sort(p, d_cls, count, d_ws, ws_bytes, st)) return s;
+  if (sorted && (!d_ws || ws_bytes < stage_ws_bytes(p, count)))
+    return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
+  StageFn fn = select_stage(p->log2n, p->algo == 0, dir == 0);
+  StageParams P{};
+  P.x = x;
+  P.y = y;
+  P.count = count;
+  P.classes = p->classes;
+  P.rounds = p->rounds;
+  P.coef = p->d_scoef[dir];
+  P.cw = p->stage_cw;
+  P.gtab = p->d_sgtab[dir];
+  P.gmask = p->gmask[dir];
+  P.tile_rows = p->stage_rows;
+  P.ent = sorted ? reinterpret_cast<const uint16_t*>(static_cast<const char*>(d_ws) + 256) : nullptr;
+  P.block_words = p->stage_block_words;
+  P.trace = g_stage_trace;
+  P.debug_skip = g_stage_trace ? (uint32_t)env_int("HYGT_STAGE_DEBUG_SKIP", 0) : 0u;
+  const uint64_t tiles = (count + p->stage_rows - 1) / p->stage_rows;
+  const uint64_t ctas = std::min<uint64_t>(tiles, (uint64_t)p->num_sms);
+  fn<<<(unsigned)ctas, (STAGE_WARPS + 1) * 32, p->stage_smem[dir], st>>>(P);
+  CU(cudaGetLastError());
+  return ok();
+}
+
 // ---- segment path -----------------------------------------------------------------------
 
 struct SegVariant {
@@ -625,6 +783,11 @@ int run_apply(const hygt_plan* p, int dir, const float* x, float* y, const uint1
   if (count == 0) return ok();
   if (!x || !y) return fail(HYGT_ERR_ARGUMENT, "hygt: null data pointer");
   if (count > 0xFFFFFFFFull) return fail(HYGT_ERR_ARGUMENT, "hygt: at most 2^32-1 rows per call");
+  {  // rows are moved in chunks of min(4, N) floats
+    const uintptr_t al = (uintptr_t)4 << (p->log2n < 2 ? p->log2n : 2);
+    if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & (al - 1)) != 0)
+      return fail(HYGT_ERR_ARGUMENT, "hygt: x and y must be aligned to min(16, 4N) bytes");
+  }
   const WsLayout w = ws_layout(p->classes, p->chunk_rows, count);
   if (p->jit.ok && !energy) {
     const bool bk = d_cls && p->classes > 1;
@@ -643,6 +806,7 @@ int run_apply(const hygt_plan* p, int dir, const float* x, float* y, const uint1
       return fail(HYGT_ERR_CUDA, std::string("hygt: jit launch failed: ") + cudaGetErrorString(cudaGetLastError()));
     return ok();
   }
+  if (stage_usable(p, x, y, energy)) return run_stage(p, dir, x, y, d_cls, count, d_ws, ws_bytes, flags, st);
   if (p->tile) {
     if (d_cls && (!d_ws || ws_bytes < 256)) return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
     return run_tile(p, dir, x, y, d_cls, count, energy,
@@ -785,12 +949,22 @@ extern "C" int hygt_plan_create(int log2_n, int rounds, int class_count, const d
     free_plan(p);
     return s;
   }
+  if (int s = setup_stage(p, angles, perms)) {
+    free_plan(p);
+    return s;
+  }
   if (int s = setup_segment(p, angles, perms)) {
     free_plan(p);
     return s;
   }
   *out = p;
   return ok();
+}
+
+// Debug hook (not part of the public header): per-tile clock64 events of CTA 0 of the staged
+// kernel are written to dev[k * 8 + e] (k < 64) while set; nullptr switches it off.
+extern "C" void hygt_debug_stage_trace(void* dev) {
+  g_stage_trace = static_cast<unsigned long long*>(dev);
 }
 
 extern "C" int hygt_plan_destroy(hygt_plan* plan) {
@@ -801,11 +975,12 @@ extern "C" int hygt_plan_destroy(hygt_plan* plan) {
 extern "C" int hygt_plan_algorithm(const hygt_plan* plan) { return plan ? plan->algo : -1; }
 
 extern "C" int hygt_plan_path(const hygt_plan* plan) {
-  return plan ? (plan->jit.ok ? 3 : plan->tile ? 1 : plan->seg ? 2 : 0) : -1;
+  return plan ? (plan->jit.ok ? 3 : plan->stage ? 4 : plan->tile ? 1 : plan->seg ? 2 : 0) : -1;
 }
 
 extern "C" size_t hygt_workspace_bytes(const hygt_plan* plan, uint64_t count) {
   if (!plan) return 0;
+  if (plan->stage && !plan->jit.ok) return std::max<size_t>(stage_ws_bytes(plan, count), 256);
   if (plan->tile && !plan->jit.ok) return 256;
   return ws_layout(plan->classes, plan->chunk_rows, count).total;
 }
@@ -813,6 +988,8 @@ extern "C" size_t hygt_workspace_bytes(const hygt_plan* plan, uint64_t count) {
 extern "C" int hygt_bucket(const hygt_plan* plan, const uint16_t* d_cls, uint64_t count,
                            void* d_ws, size_t ws_bytes, void* stream) {
   if (!plan) return fail(HYGT_ERR_ARGUMENT, "hygt_bucket: null plan");
+  if (plan->stage && !plan->jit.ok)  // per-tile class sort of the staged kernel
+    return plan->classes > 1 ? run_stage_sort(plan, d_cls, count, d_ws, ws_bytes, as_stream(stream)) : ok();
   if (plan->tile && !plan->jit.ok) return ok();  // tile plans sort each tile in shared memory
   return run_bucket(plan, plan->classes, plan->chunk_rows, d_cls, count, d_ws, ws_bytes,
                     as_stream(stream));

@@ -3,15 +3,22 @@
 #pragma once
 #include "hygt_kernels.cuh"
 #include "hygt_segment.cuh"
+#include "hygt_stage.cuh"
 #include "hygt_tile.cuh"
 
 namespace hygt_gpu {
 using ApplyFn = void (*)(ApplyParams);
 using TileFn = void (*)(TileParams);
 using SegFn = void (*)(SegParams);
+using StageFn = void (*)(StageParams);
+using StageSortFn = void (*)(StageSortParams);
 constexpr int TILE_THREADS = 512;
 constexpr int SEG_THREADS = 256;
+constexpr int STAGE_WARPS = 7;  // consumer warps (+ one producer warp)
+constexpr int STAGE_VPT = 4;
 ApplyFn select_apply(int log2n, int l, bool standard, bool fwd, bool energy);
 TileFn select_tile(int log2n, int l, int vpt, bool standard, bool fwd, bool energy);
 SegFn select_seg(int variant, bool standard, bool fwd, bool energy);
+StageFn select_stage(int log2n, bool standard, bool fwd);
+StageSortFn select_stage_sort();
 }  // namespace hygt_gpu

@@ -125,11 +125,11 @@ class HyGTPlan:
     @property
     def path(self) -> str:
         """Kernel family serving this plan (include/hygt_gpu.h, hygt_plan_path)."""
-        return {0: "bucketed", 1: "tile", 2: "segment", 3: "jit"}[_lib.lib().hygt_plan_path(self._h)]
+        return {0: "bucketed", 1: "tile", 2: "segment", 3: "jit", 4: "stage"}[_lib.lib().hygt_plan_path(self._h)]
 
     def launches_per_step(self) -> int:
         """Kernels launched by bucket + forward + inverse on this plan."""
-        return 2 if self.path == "tile" else 5
+        return 2 if self.path in ("tile", "stage") else 5
 
     def workspace_bytes(self, count: int) -> int:
         return _lib.lib().hygt_workspace_bytes(self._h, count)

@@ -59,15 +59,20 @@ TILE_LAYOUTS = {2: [(0, 2)], 3: [(1, 2), (0, 2)], 4: [(1, 2), (2, 2), (0, 1)],
 
 
 SEG_VARIANTS = {6: [0, 1, 2, 3], 7: [4, 5], 8: [6, 7, 8, 9]}
+STAGE_LOG2N = (4,)
 
 
 def _variants(log2n):
-    out = [{"HYGT_JIT": "0", "HYGT_TILE": "0", "HYGT_SEGMENT": "0", "HYGT_LANES_LOG2": str(l)}
-           for l in LAYOUTS[log2n]]
+    out = [{"HYGT_JIT": "0", "HYGT_STAGE": "0", "HYGT_TILE": "0", "HYGT_SEGMENT": "0",
+            "HYGT_LANES_LOG2": str(l)} for l in LAYOUTS[log2n]]
     for v in SEG_VARIANTS.get(log2n, []):
         out.append({"HYGT_SEGMENT": "1", "HYGT_SEG_VARIANT": str(v)})
     for l, v in TILE_LAYOUTS.get(log2n, []):
-        out.append({"HYGT_JIT": "0", "HYGT_TILE": "1", "HYGT_TILE_L": str(l), "HYGT_TILE_VPT": str(v)})
+        out.append({"HYGT_JIT": "0", "HYGT_STAGE": "0", "HYGT_TILE": "1", "HYGT_TILE_L": str(l),
+                    "HYGT_TILE_VPT": str(v)})
+    if log2n in STAGE_LOG2N:  # TMA-staged tile kernel
+        out.append({"HYGT_JIT": "0", "HYGT_STAGE": "1"})
+        out.append({"HYGT_JIT": "0", "HYGT_STAGE": "1", "HYGT_STAGE_ROWS": "136"})
     if log2n <= 5:  # plan-specialised NVRTC kernel (served for plans with <= 4 classes)
         out.append({"HYGT_JIT": "1"})
     return out
@@ -345,3 +350,54 @@ def test_jit_plan_matches_oracle(cuda, oracle_mod):
                 plan.forward(xd, cd)
                 with pytest.raises(ArgumentError):
                     plan.sync_status()
+
+
+@pytest.mark.parametrize("standard", [False, True])
+def test_stage_path_edges(cuda, oracle_mod, standard, monkeypatch):
+    """TMA-staged kernel (plan path 'stage'): partial and multi-tile batches, class ids staged by
+    TMA and (misaligned) by plain loads, in place, unaligned rows falling back to the tile
+    kernel, invalid ids passed through and reported."""
+    from paper_2505_21728_b200 import ArgumentError, HyGTModel
+    from oracle import oracle as O
+    monkeypatch.setenv("HYGT_JIT", "0")
+    rng = np.random.default_rng(21)
+    C, R = 7, 3
+    angles = rng.uniform(-np.pi, np.pi, (C, R * 4 * 8))
+    perms = np.stack([np.stack([rng.permutation(16) for _ in range(R)]) for _ in range(C)]).astype(np.uint16)
+    models = [HyGTModel(4, R, angles[c], perms[c, R - 1]) for c in range(C)]
+    plan = _plan(models, perms[:, : R - 1].copy(), standard)
+    assert plan.path == "stage"
+    for count in [0, 1, 7, 8, 33, 811, 2 * 811 + 5, 50000]:
+        xh = (rng.standard_normal((count + 1, 16)) * 16).astype(np.float32)
+        ch = rng.integers(0, C, count + 1).astype(np.uint16)
+        xd = torch.from_numpy(xh).to(cuda)
+        cd = torch.from_numpy(ch).to(cuda)
+        y = plan.forward(xd[:count], cd[:count])
+        plan.sync_status()
+        if not count:
+            continue
+        ref = O.apply_batch(4, R, angles, perms, (1 << R) - 1, xh[:count], ch[:count])
+        check_close(y.cpu().numpy(), ref, xh[:count], f"stage fwd count={count}")
+        back = plan.inverse(y, cd[:count])
+        check_close(back.cpu().numpy(), xh[:count], xh[:count], f"stage roundtrip count={count}")
+        # class ids at an odd u16 offset: not 16 B aligned -> loaded by the consumer warps
+        y2 = plan.forward(xd[:count], cd[1:])
+        ref2 = O.apply_batch(4, R, angles, perms, (1 << R) - 1, xh[:count], ch[1:])
+        check_close(y2.cpu().numpy(), ref2, xh[:count], f"stage misaligned ids count={count}")
+        # rows at a 16-byte offset stay on the staged path; a 4-byte offset is rejected
+        xm = xd.view(-1)[4:4 + count * 16].view(count, 16)
+        xm_h = xh.reshape(-1)[4:4 + count * 16].reshape(count, 16)
+        refm = O.apply_batch(4, R, angles, perms, (1 << R) - 1, xm_h, ch[:count])
+        check_close(plan.forward(xm, cd[:count]).cpu().numpy(), refm, xm_h, f"stage offset count={count}")
+        with pytest.raises(ArgumentError):
+            plan.forward(xd.view(-1)[1:1 + count * 16].view(count, 16), cd[:count])
+        xi = xd[:count].clone()
+        plan.forward(xi, cd[:count], out=xi)  # in place
+        assert torch.equal(xi, y)
+    x = torch.randn(5000, 16, device=cuda)
+    cls = torch.from_numpy(rng.integers(0, C, 5000).astype(np.uint16)).to(cuda)
+    cls[1234] = C
+    y = plan.forward(x, cls)
+    with pytest.raises(ArgumentError):
+        plan.sync_status()
+    assert torch.equal(y[1234], x[1234])

@@ -7,7 +7,7 @@ timeout 300 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/
 timeout 300 python bench.py --config 5 --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/plain5.log 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_cfg5.csv python bench.py --config 5 --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_l5.log 2>&1
 prof() {  # name, kernel regex, bench args
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$2" -s 4 -c 1 -o /tmp/prof_$1 python bench.py $3 --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_$1.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$2" -s 4 -c 1 -f -o /tmp/prof_$1 python bench.py $3 --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_$1.log 2>&1
   ncu -i /tmp/prof_$1.ncu-rep --page raw --csv > gpurun_out/prof_$1_raw.csv 2>/dev/null
   ncu -i /tmp/prof_$1.ncu-rep --page details --csv > gpurun_out/prof_$1_details.csv 2>/dev/null
 }
