@@ -630,6 +630,9 @@ int setup_stage(hygt_plan* p, const double* angles, const uint16_t* perms) {
   p->stage_rows = T;
   p->stage_cw = cw;
   p->stage_block_words = stage_block_words(T, STAGE_VPT, C);
+  cudaFuncSetAttribute(select_stage_sort(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(STAGE_SORT_WARPS * stage_sort_warp_bytes(C, p->stage_block_words)));
+  cudaGetLastError();
   return HYGT_OK;
 }
 
@@ -652,9 +655,13 @@ int run_stage_sort(const hygt_plan* p, const uint16_t* d_cls, uint64_t count, vo
   S.ent = reinterpret_cast<uint16_t*>(static_cast<char*>(d_ws) + 256);
   S.err = static_cast<uint32_t*>(d_ws);
   const uint64_t tiles = (count + p->stage_rows - 1) / p->stage_rows;
-  const size_t smem = stage_align((uint32_t)(p->classes + 1) * 4u, 16) + p->stage_block_words * 2;
-  const uint64_t ctas = std::min<uint64_t>(tiles, (uint64_t)p->num_sms * 8);
-  select_stage_sort()<<<(unsigned)ctas, 256, smem, st>>>(S);
+  const size_t smem = (size_t)STAGE_SORT_WARPS * stage_sort_warp_bytes(p->classes, p->stage_block_words);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, select_stage_sort(), 32 * STAGE_SORT_WARPS, smem);
+  if (occ < 1) occ = 1;
+  const uint64_t ctas = std::min<uint64_t>((tiles + STAGE_SORT_WARPS - 1) / STAGE_SORT_WARPS,
+                                           (uint64_t)p->num_sms * occ);
+  select_stage_sort()<<<(unsigned)ctas, 32 * STAGE_SORT_WARPS, smem, st>>>(S);
   CU(cudaGetLastError());
   return ok();
 }

@@ -282,87 +282,101 @@ __device__ __forceinline__ void stage_gather(float2 (&v)[VPT][(1 << LOG2N) / 2],
 }
 
 // ------------------------------------------------------------------------- per-tile sort ----
-// One CTA (256 threads) per tile, grid-stride. 4 ids per thread (T <= 1024), one shared atomic
-// per row for its rank inside the class, padded class starts by a warp scan.
+// One warp per tile (many tiles in flight per SM: this pass is latency-, not bandwidth-bound).
+// Ranks come from shared atomics on (class, row parity) counters; inside a class, even and odd
+// rows alternate (the shorter parity runs out first) so that each thread of the staged kernel
+// gets rows from both halves of a 128 B bank line. Class starts: warp scan of the padded counts.
+constexpr int STAGE_SORT_WARPS = 8;
+
+HYGT_HD constexpr uint32_t stage_sort_warp_bytes(int classes, uint32_t block_words) {
+  return stage_align((uint32_t)(3 * classes + 1) * 4u, 16) + stage_align((block_words - 8) * 2u, 16);
+}
+
 template <int VPT>
-__global__ void __launch_bounds__(256) hygt_stage_sort_kernel(const StageSortParams P) {
+__global__ void __launch_bounds__(32 * STAGE_SORT_WARPS) hygt_stage_sort_kernel(const StageSortParams P) {
   constexpr int BATCH = 32 * VPT;
+  constexpr int H = 1024 / 128;  // groups of 4 consecutive ids per lane (T <= 1024)
   extern __shared__ __align__(16) unsigned char sm[];
   const int C = P.classes;
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(sm);       // [C] counts, then starts
-  uint32_t* s_total = cnt + C;
-  uint16_t* ents = reinterpret_cast<uint16_t*>(sm + stage_align((uint32_t)(C + 1) * 4u, 16));
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned char* mine = sm + warp * stage_sort_warp_bytes(C, P.block_words);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(mine);  // [C][2] counts per (class, row parity)
+  uint32_t* start = cnt + 2 * C;                       // [C] padded class starts
+  uint16_t* ents = reinterpret_cast<uint16_t*>(mine + stage_align((uint32_t)(3 * C + 1) * 4u, 16));
   const uint32_t T = P.tile_rows;
   const uint64_t tiles = (P.count + T - 1) / T;
   bool bad = false;
-  for (uint64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+  for (uint64_t tile = (uint64_t)blockIdx.x * STAGE_SORT_WARPS + warp; tile < tiles;
+       tile += (uint64_t)gridDim.x * STAGE_SORT_WARPS) {
     const uint64_t row0 = tile * T;
     const uint32_t rows = (uint32_t)((P.count - row0) < T ? (P.count - row0) : T);
-    for (int c = tid; c < C; c += 256) cnt[c] = 0;
-    uint32_t c4[4], r4[4];
-    const uint32_t j0 = 4u * tid;
-    uint2 w = make_uint2(0xffffffffu, 0xffffffffu);
-    if (j0 + 4 <= rows && ((reinterpret_cast<uintptr_t>(P.cls + row0 + j0) & 7) == 0)) {
-      w = __ldcs(reinterpret_cast<const uint2*>(P.cls + row0 + j0));
-    } else if (j0 < rows) {
-      uint32_t q[4];
+    for (int c = lane; c < 2 * C; c += 32) cnt[c] = 0;
+    uint2 w[H];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) q[e] = j0 + e < rows ? (uint32_t)P.cls[row0 + j0 + e] : 0xffffu;
-      w = make_uint2(q[0] | (q[1] << 16), q[2] | (q[3] << 16));
-    }
-    __syncthreads();
+    for (int h = 0; h < H; ++h) {
+      const uint32_t j0 = 128u * h + 4u * lane;
+      w[h] = make_uint2(0xffffffffu, 0xffffffffu);
+      if (j0 + 4 <= rows && ((reinterpret_cast<uintptr_t>(P.cls + row0 + j0) & 7) == 0)) {
+        w[h] = __ldcs(reinterpret_cast<const uint2*>(P.cls + row0 + j0));
+      } else if (j0 < rows) {
+        uint32_t q[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const uint32_t c = ((e < 2 ? w.x : w.y) >> (16 * (e & 1))) & 0xffffu;
-      const bool in = j0 + e < rows, ok = in && c < (uint32_t)C;
-      bad |= in && !ok;  // passed through: no entry, the stage slot keeps x
-      c4[e] = ok ? c : 0xffffffffu;
-      r4[e] = ok ? atomicAdd(&cnt[c], 1u) : 0u;
-    }
-    __syncthreads();
-    if (warp == 0) {
-      uint32_t carry = 0;
-      for (int base = 0; base < C; base += 32) {
-        const int c = base + lane;
-        const uint32_t n = c < C ? cnt[c] : 0u;
-        const uint32_t padded = (n + VPT - 1) / VPT * VPT;
-        uint32_t incl = padded;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += t;
-        }
-        const uint32_t start = carry + incl - padded;
-        if (c < C) {
-          cnt[c] = start;
-          for (uint32_t q = start + n; q < start + padded; ++q) ents[q] = (uint16_t)STAGE_PAD;
-        }
-        carry += __shfl_sync(0xffffffffu, incl, 31);
+        for (int e = 0; e < 4; ++e) q[e] = j0 + e < rows ? (uint32_t)P.cls[row0 + j0 + e] : 0xffffu;
+        w[h] = make_uint2(q[0] | (q[1] << 16), q[2] | (q[3] << 16));
       }
-      const uint32_t end = (carry + BATCH - 1) / BATCH * BATCH;
-      for (uint32_t q = carry + lane; q < end; q += 32) ents[q] = (uint16_t)STAGE_PAD;
-      if (lane == 0) *s_total = carry;
     }
-    __syncthreads();
+    __syncwarp();
+    uint32_t pk[4 * H];  // (class << 16) | rank within (class, parity), or 0xffffffff
 #pragma unroll
-    for (int e = 0; e < 4; ++e)
-      if (c4[e] != 0xffffffffu) ents[cnt[c4[e]] + r4[e]] = (uint16_t)((c4[e] << 10) | (j0 + e));
-    __syncthreads();
-    const uint32_t total = *s_total;
-    const uint32_t words = 8u + (total + BATCH - 1) / BATCH * BATCH;  // header + used positions
+    for (int h = 0; h < H; ++h)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t j = 128u * h + 4u * lane + e;
+        const uint32_t c = ((e < 2 ? w[h].x : w[h].y) >> (16 * (e & 1))) & 0xffffu;
+        const bool in = j < rows, ok = in && c < (uint32_t)C;
+        bad |= in && !ok;  // passed through: no entry, the stage slot keeps x
+        pk[4 * h + e] = ok ? ((c << 16) | atomicAdd(&cnt[2 * c + (j & 1u)], 1u)) : 0xffffffffu;
+      }
+    __syncwarp();
+    uint32_t carry = 0;
+    for (int base = 0; base < C; base += 32) {
+      const int c = base + lane;
+      const uint32_t n = c < C ? cnt[2 * c] + cnt[2 * c + 1] : 0u;
+      const uint32_t padded = (n + VPT - 1) / VPT * VPT;
+      uint32_t incl = padded;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (c < C) {
+        const uint32_t st = carry + incl - padded;
+        start[c] = st | (min(cnt[2 * c], cnt[2 * c + 1]) << 16);  // start, interleaved pairs
+        for (uint32_t q = st + n; q < st + padded; ++q) ents[q] = (uint16_t)STAGE_PAD;
+      }
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    const uint32_t end = (carry + BATCH - 1) / BATCH * BATCH;
+    for (uint32_t q = carry + lane; q < end; q += 32) ents[q] = (uint16_t)STAGE_PAD;
+    __syncwarp();
+#pragma unroll
+    for (int g = 0; g < 4 * H; ++g)
+      if (pk[g] != 0xffffffffu) {
+        const uint32_t c = pk[g] >> 16, r = pk[g] & 0xffffu;
+        const uint32_t j = 128u * (g >> 2) + 4u * lane + (g & 3);
+        const uint32_t sm_ = start[c], m = sm_ >> 16;
+        ents[(sm_ & 0xffffu) + (r < m ? 2 * r + (j & 1u) : m + r)] = (uint16_t)((c << 10) | j);
+      }
+    __syncwarp();
     uint16_t* dst = P.ent + tile * P.block_words;
-    for (uint32_t i = tid; i < words / 8; i += 256) {
-      uint4 v;
-      if (i == 0) v = make_uint4(total, 0u, 0u, 0u);
-      else v = reinterpret_cast<const uint4*>(ents)[i - 1];
+    for (uint32_t i = lane; i < (8u + end) / 8; i += 32) {
+      const uint4 v = i == 0 ? make_uint4(carry, 0u, 0u, 0u) : reinterpret_cast<const uint4*>(ents)[i - 1];
       __stcs(reinterpret_cast<uint4*>(dst) + i, v);
     }
-    __syncthreads();
+    __syncwarp();
   }
-  if (__syncthreads_or(bad) && tid == 0) atomicOr(P.err, 1u);
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(P.err, 1u);
 }
-
 
 template <int LOG2N, int VPT, bool STD, bool FWD, int WARPS>
 __global__ void __launch_bounds__((WARPS + 1) * 32, 1) hygt_stage_kernel(const StageParams P) {
