@@ -357,7 +357,7 @@ def impl_ours(args):
     traffic, traffic_src = measured_traffic(w.cfg.name) if rows == w.cfg.count else (None, None)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
-                "kernel": f"{plan.path} kernel (forward / inverse), class bucketing included",
+                "kernel": f"hygt_{plan.path}_kernel (mean of the forward and inverse launches)",
                 "bytes_per_launch": rows * bpr, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({hbm_kind})"}
     launches_per_step = plan.launches_per_step()
 

@@ -128,8 +128,9 @@ class HyGTPlan:
         return {0: "bucketed", 1: "tile", 2: "segment", 3: "jit", 4: "stage"}[_lib.lib().hygt_plan_path(self._h)]
 
     def launches_per_step(self) -> int:
-        """Kernels launched by bucket + forward + inverse on this plan."""
-        return 2 if self.path in ("tile", "stage") else 5
+        """Kernels launched by bucket + forward + inverse on this plan (the stage path sorts each
+        tile once in hygt_bucket; the tile path sorts inside its kernel)."""
+        return {"tile": 2, "stage": 3}.get(self.path, 5)
 
     def workspace_bytes(self, count: int) -> int:
         return _lib.lib().hygt_workspace_bytes(self._h, count)
