@@ -87,7 +87,10 @@ int hygt_plan_algorithm(const hygt_plan* plan);
  *     are instruction immediates and permutations register renames,
  * 4 = TMA-staged tile kernel (N = 16): tiles of rows moved HBM <-> shared memory by the bulk-copy
  *     engine, class-sorted in shared memory, no bucketing pass. Forward-with-energy calls run on
- *     the tile kernel instead. */
+ *     the tile kernel instead,
+ * 5 = thread-per-row kernel over global class buckets (N = 64): rows staged through shared
+ *     memory by cp.async, class tables one segment at a time. Forward-with-energy calls run on
+ *     the class-segment kernel instead. */
 int hygt_plan_path(const hygt_plan* plan);
 
 /* Device workspace for class bucketing of `count` rows. */

@@ -93,6 +93,9 @@ struct hygt_plan {
   float4* d_scoef[2] = {nullptr, nullptr};
   uint16_t* d_sgtab[2] = {nullptr, nullptr};
   size_t stage_smem[2] = {0, 0};
+  // seg2 path (N = 64): thread-per-row over global class buckets, element-ordered tables
+  bool seg2 = false;
+  size_t seg2_smem[2] = {0, 0};
   // JIT path (N <= 64): NVRTC-specialised kernels, coefficients as immediates
   JitKernels jit;
   // segment path (N >= 64): same interleaved tables, one class staged per CTA segment
@@ -550,9 +553,8 @@ unsigned long long* g_stage_trace = nullptr;  // debug hook, see hygt_debug_stag
 // per-element coefficient k_i of y_i = x_i + k_i x_{i^2^p} (scale-folded: k_m = t1, k_n = -t2;
 // standard: N/4 units of c_i then N/4 units of s'_i with s'_m = s, s'_n = -s), then N/4 units of
 // final scales (scale-folded only). Gathers: [C][R+1][N] u16 scratch offsets src * 128.
-int setup_stage(hygt_plan* p, const double* angles, const uint16_t* perms) {
-  StageFn probe = select_stage(p->log2n, p->algo == 0, true);
-  if (!probe || env_int("HYGT_STAGE", 1) == 0 || p->classes > STAGE_MAX_CLASSES) return HYGT_OK;
+// Element-ordered tables of both directions into p->d_scoef / p->d_sgtab (stage and seg2 paths).
+int build_elem_tables(hygt_plan* p, const double* angles, const uint16_t* perms, uint32_t* cw_out) {
   const int n = 1 << p->log2n, nc = n / 4, C = p->classes, R = p->rounds;
   const bool standard = p->algo == 0;
   const uint32_t step_units = (uint32_t)nc * (standard ? 2 : 1);
@@ -560,7 +562,7 @@ int setup_stage(hygt_plan* p, const double* angles, const uint16_t* perms) {
   for (int d = 0; d < 2; ++d) {
     std::vector<ClassProgram> progs;
     if (!build_programs(p->log2n, R, C, angles, perms, p->perm_mask, d == 0, standard, progs))
-      return fail(HYGT_ERR_NUMERICAL, "hygt: stage table build failed");
+      return fail(HYGT_ERR_NUMERICAL, "hygt: element table build failed");
     std::vector<float4> coef((size_t)C * cw, make_float4(0.f, 0.f, 0.f, 0.f));
     const uint32_t gs = stage_gstride(p->log2n, R) / 2;  // u16 per class
     std::vector<uint16_t> gt((size_t)C * gs, 0);
@@ -595,7 +597,7 @@ int setup_stage(hygt_plan* p, const double* angles, const uint16_t* perms) {
             cc[(size_t)R * p->log2n * step_units + u] = make_float4(sc[4 * u], sc[4 * u + 1], sc[4 * u + 2], sc[4 * u + 3]);
         }
       }
-      if (step != (uint32_t)R * p->log2n) return fail(HYGT_ERR_NUMERICAL, "hygt: stage step count");
+      if (step != (uint32_t)R * p->log2n) return fail(HYGT_ERR_NUMERICAL, "hygt: element table step count");
       uint64_t gm = 0;
       const auto g = exec_gathers(p->log2n, R, perms ? perms + (size_t)c * R * n : nullptr,
                                   p->perm_mask, d == 0, &gm);
@@ -607,6 +609,17 @@ int setup_stage(hygt_plan* p, const double* angles, const uint16_t* perms) {
     if (!s && p->gmask[d]) s = upload(&p->d_sgtab[d], gt.data(), gt.size());
     if (s) return s;
   }
+  *cw_out = cw;
+  return HYGT_OK;
+}
+
+int setup_stage(hygt_plan* p, const double* angles, const uint16_t* perms) {
+  StageFn probe = select_stage(p->log2n, p->algo == 0, true);
+  if (!probe || env_int("HYGT_STAGE", 1) == 0 || p->classes > STAGE_MAX_CLASSES) return HYGT_OK;
+  const int C = p->classes, R = p->rounds;
+  const bool standard = p->algo == 0;
+  uint32_t cw = 0;
+  if (int s = build_elem_tables(p, angles, perms, &cw)) return s;
   // Tile rows: one batch of 32 * VPT sorted positions per consumer warp, including the padding
   // of every class run to VPT; rows are indexed with 10 bits in the sort entries.
   const long long tenv = env_int("HYGT_STAGE_ROWS", -1);
@@ -752,6 +765,48 @@ int setup_segment(hygt_plan* p, const double* angles, const uint16_t* perms) {
   return HYGT_OK;
 }
 
+int setup_seg2(hygt_plan* p, const double* angles, const uint16_t* perms) {
+  if (!select_seg2(p->log2n, p->algo == 0, true) || env_int("HYGT_SEG2", 1) == 0) return HYGT_OK;
+  uint32_t cw = 0;
+  if (int s = build_elem_tables(p, angles, perms, &cw)) return s;
+  for (int d = 0; d < 2; ++d) {
+    p->seg2_smem[d] = seg2_smem_bytes(p->log2n, SEG2_VPT, SEG2_WARPS, cw, stage_gstride(p->log2n, p->rounds));
+    if (p->seg2_smem[d] > 227 * 1024) return HYGT_OK;
+    cudaFuncSetAttribute(select_seg2(p->log2n, p->algo == 0, d == 0),
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->seg2_smem[d]);
+  }
+  cudaGetLastError();
+  p->stage_cw = cw;
+  p->seg2 = true;
+  p->chunk_rows = 0;  // global class buckets
+  return HYGT_OK;
+}
+
+int run_seg2(const hygt_plan* p, int dir, const float* x, float* y, uint64_t count,
+             const WsLayout& w, char* ws, cudaStream_t st) {
+  Seg2Fn fn = select_seg2(p->log2n, p->algo == 0, dir == 0);
+  Seg2Params P{};
+  P.x = x;
+  P.y = y;
+  P.idx = reinterpret_cast<const uint32_t*>(ws + w.idx);
+  P.seg_end = reinterpret_cast<const uint32_t*>(ws + w.seg);
+  P.classes = p->classes;
+  P.rounds = p->rounds;
+  P.count = count;
+  P.coef = p->d_scoef[dir];
+  P.cw = p->stage_cw;
+  P.gtab = p->d_sgtab[dir];
+  P.gstride = stage_gstride(p->log2n, p->rounds);
+  P.gmask = p->gmask[dir];
+  const uint64_t min_span = 4096;
+  uint64_t ctas = std::min<uint64_t>((uint64_t)p->num_sms, (count + min_span - 1) / min_span);
+  if (ctas < 1) ctas = 1;
+  P.cta_span = (count + ctas - 1) / ctas;
+  fn<<<(unsigned)ctas, SEG2_WARPS * 32, p->seg2_smem[dir], st>>>(P);
+  CU(cudaGetLastError());
+  return ok();
+}
+
 int run_segment(const hygt_plan* p, int dir, const float* x, float* y, uint64_t count,
                 double* energy, const WsLayout& w, char* ws, bool bucketed, cudaStream_t st) {
   SegFn fn = select_seg(p->seg_variant, p->algo == 0, dir == 0, energy != nullptr);
@@ -820,6 +875,14 @@ int run_apply(const hygt_plan* p, int dir, const float* x, float* y, const uint1
                     d_cls ? reinterpret_cast<uint32_t*>(static_cast<char*>(d_ws) + w.err) : nullptr, st);
   }
   const bool bucketed = d_cls && p->classes > 1;
+  if (p->seg2 && bucketed && !energy) {
+    if (!d_ws || ws_bytes < w.total) return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
+    if (!(flags & HYGT_REUSE_BUCKETS)) {
+      const int s = run_bucket(p, p->classes, 0, d_cls, count, d_ws, ws_bytes, st);
+      if (s) return s;
+    }
+    return run_seg2(p, dir, x, y, count, w, static_cast<char*>(d_ws), st);
+  }
   if (p->seg && bucketed && (!energy || p->seg_energy_smem)) {
     if (!d_ws || ws_bytes < w.total) return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
     if (!(flags & HYGT_REUSE_BUCKETS)) {
@@ -964,6 +1027,10 @@ extern "C" int hygt_plan_create(int log2_n, int rounds, int class_count, const d
     free_plan(p);
     return s;
   }
+  if (int s = setup_seg2(p, angles, perms)) {
+    free_plan(p);
+    return s;
+  }
   *out = p;
   return ok();
 }
@@ -982,7 +1049,7 @@ extern "C" int hygt_plan_destroy(hygt_plan* plan) {
 extern "C" int hygt_plan_algorithm(const hygt_plan* plan) { return plan ? plan->algo : -1; }
 
 extern "C" int hygt_plan_path(const hygt_plan* plan) {
-  return plan ? (plan->jit.ok ? 3 : plan->stage ? 4 : plan->tile ? 1 : plan->seg ? 2 : 0) : -1;
+  return plan ? (plan->jit.ok ? 3 : plan->stage ? 4 : plan->tile ? 1 : plan->seg2 ? 5 : plan->seg ? 2 : 0) : -1;
 }
 
 extern "C" size_t hygt_workspace_bytes(const hygt_plan* plan, uint64_t count) {

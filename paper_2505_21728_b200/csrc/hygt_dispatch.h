@@ -4,6 +4,7 @@
 #include "hygt_kernels.cuh"
 #include "hygt_segment.cuh"
 #include "hygt_stage.cuh"
+#include "hygt_seg2.cuh"
 #include "hygt_tile.cuh"
 
 namespace hygt_gpu {
@@ -12,13 +13,17 @@ using TileFn = void (*)(TileParams);
 using SegFn = void (*)(SegParams);
 using StageFn = void (*)(StageParams);
 using StageSortFn = void (*)(StageSortParams);
+using Seg2Fn = void (*)(Seg2Params);
 constexpr int TILE_THREADS = 512;
 constexpr int SEG_THREADS = 256;
 constexpr int STAGE_WARPS = 7;  // consumer warps (+ one producer warp)
 constexpr int STAGE_VPT = 4;
+constexpr int SEG2_WARPS = 8;
+constexpr int SEG2_VPT = 2;
 ApplyFn select_apply(int log2n, int l, bool standard, bool fwd, bool energy);
 TileFn select_tile(int log2n, int l, int vpt, bool standard, bool fwd, bool energy);
 SegFn select_seg(int variant, bool standard, bool fwd, bool energy);
 StageFn select_stage(int log2n, bool standard, bool fwd);
 StageSortFn select_stage_sort();
+Seg2Fn select_seg2(int log2n, bool standard, bool fwd);
 }  // namespace hygt_gpu

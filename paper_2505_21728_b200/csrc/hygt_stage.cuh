@@ -250,6 +250,32 @@ template <int LOG2N, int VPT, int SR>
 __device__ __forceinline__ void stage_gather(float2 (&v)[VPT][(1 << LOG2N) / 2], uint32_t scr,
                                              uint32_t gt, uint32_t x, uint32_t xs) {
   constexpr int N = 1 << LOG2N, NW = N / 2, NC = N / 4;
+  if constexpr (SR >= VPT) {  // all rows in one round trip; offsets read per chunk
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < VPT; ++r)
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        stage_detail::sts32(scr + (uint32_t)((r * N + 2 * w) * 128), v[r][w].x);
+        stage_detail::sts32(scr + (uint32_t)((r * N + 2 * w + 1) * 128), v[r][w].y);
+      }
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      uint2 g;
+      asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(g.x), "=r"(g.y) : "r"(gt + ((c ^ x) << 3)));
+      const uint32_t a0 = scr + ((g.x & 0xffffu) ^ xs), a1 = scr + ((g.x >> 16) ^ xs);
+      const uint32_t a2 = scr + ((g.y & 0xffffu) ^ xs), a3 = scr + ((g.y >> 16) ^ xs);
+#pragma unroll
+      for (int r = 0; r < VPT; ++r) {
+        v[r][2 * c].x = stage_detail::lds32(a0 + r * N * 128);
+        v[r][2 * c].y = stage_detail::lds32(a1 + r * N * 128);
+        v[r][2 * c + 1].x = stage_detail::lds32(a2 + r * N * 128);
+        v[r][2 * c + 1].y = stage_detail::lds32(a3 + r * N * 128);
+      }
+    }
+    return;
+  }
   uint32_t a[N];
 #pragma unroll
   for (int c = 0; c < NC; ++c) {

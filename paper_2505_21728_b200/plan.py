@@ -125,7 +125,7 @@ class HyGTPlan:
     @property
     def path(self) -> str:
         """Kernel family serving this plan (include/hygt_gpu.h, hygt_plan_path)."""
-        return {0: "bucketed", 1: "tile", 2: "segment", 3: "jit", 4: "stage"}[_lib.lib().hygt_plan_path(self._h)]
+        return {0: "bucketed", 1: "tile", 2: "segment", 3: "jit", 4: "stage", 5: "seg2"}[_lib.lib().hygt_plan_path(self._h)]
 
     def launches_per_step(self) -> int:
         """Kernels launched by bucket + forward + inverse on this plan (the stage path sorts each

@@ -60,13 +60,16 @@ TILE_LAYOUTS = {2: [(0, 2)], 3: [(1, 2), (0, 2)], 4: [(1, 2), (2, 2), (0, 1)],
 
 SEG_VARIANTS = {6: [0, 1, 2, 3], 7: [4, 5], 8: [6, 7, 8, 9]}
 STAGE_LOG2N = (4,)
+SEG2_LOG2N = (6,)
 
 
 def _variants(log2n):
     out = [{"HYGT_JIT": "0", "HYGT_STAGE": "0", "HYGT_TILE": "0", "HYGT_SEGMENT": "0",
             "HYGT_LANES_LOG2": str(l)} for l in LAYOUTS[log2n]]
     for v in SEG_VARIANTS.get(log2n, []):
-        out.append({"HYGT_SEGMENT": "1", "HYGT_SEG_VARIANT": str(v)})
+        out.append({"HYGT_SEG2": "0", "HYGT_SEGMENT": "1", "HYGT_SEG_VARIANT": str(v)})
+    if log2n in SEG2_LOG2N:  # thread-per-row kernel over global class buckets
+        out.append({"HYGT_SEG2": "1"})
     for l, v in TILE_LAYOUTS.get(log2n, []):
         out.append({"HYGT_JIT": "0", "HYGT_STAGE": "0", "HYGT_TILE": "1", "HYGT_TILE_L": str(l),
                     "HYGT_TILE_VPT": str(v)})
@@ -401,3 +404,42 @@ def test_stage_path_edges(cuda, oracle_mod, standard, monkeypatch):
     with pytest.raises(ArgumentError):
         plan.sync_status()
     assert torch.equal(y[1234], x[1234])
+
+
+@pytest.mark.parametrize("standard", [False, True])
+def test_seg2_path_edges(cuda, oracle_mod, standard):
+    """Thread-per-row bucketed kernel (plan path 'seg2', N = 64): partial batches, a class with a
+    single row, in place, invalid ids passed through and reported."""
+    from paper_2505_21728_b200 import ArgumentError, HyGTModel
+    from oracle import oracle as O
+    rng = np.random.default_rng(33)
+    C, R, n = 6, 4, 64
+    angles = rng.uniform(-np.pi, np.pi, (C, R * 6 * 32))
+    perms = np.stack([np.stack([rng.permutation(n) for _ in range(R)]) for _ in range(C)]).astype(np.uint16)
+    models = [HyGTModel(6, R, angles[c], perms[c, R - 1]) for c in range(C)]
+    plan = _plan(models, perms[:, : R - 1].copy(), standard)
+    assert plan.path == "seg2"
+    for count in [1, 5, 63, 64, 65, 1000, 70001]:
+        xh = (rng.standard_normal((count, n)) * 16).astype(np.float32)
+        ch = rng.integers(0, C, count).astype(np.uint16)
+        if count > 10:
+            ch[ch == 5] = 4
+            ch[7] = 5  # one class with a single row
+        ref = O.apply_batch(6, R, angles, perms, (1 << R) - 1, xh, ch)
+        xd = torch.from_numpy(xh).to(cuda)
+        cd = torch.from_numpy(ch).to(cuda)
+        y = plan.forward(xd, cd)
+        plan.sync_status()
+        check_close(y.cpu().numpy(), ref, xh, f"seg2 fwd count={count}")
+        back = plan.inverse(y, cd)
+        check_close(back.cpu().numpy(), xh, xh, f"seg2 roundtrip count={count}")
+        xi = xd.clone()
+        plan.forward(xi, cd, out=xi)  # in place
+        assert torch.equal(xi, y)
+    x = torch.randn(3000, n, device=cuda)
+    cls = torch.from_numpy(rng.integers(0, C, 3000).astype(np.uint16)).to(cuda)
+    cls[123] = C
+    y = plan.forward(x, cls)
+    with pytest.raises(ArgumentError):
+        plan.sync_status()
+    assert torch.equal(y[123], x[123])
