@@ -182,14 +182,21 @@ __global__ void __launch_bounds__(WARPS * 32, 1) hygt_seg2_kernel(const Seg2Para
       for (uint32_t i = tid; i < P.gstride / 4; i += THREADS)
         s_gt[i] = __ldg(reinterpret_cast<const uint32_t*>(P.gtab) + (size_t)c * (P.gstride / 4) + i);
     __syncthreads();
-    for (uint64_t bb = pos + (uint64_t)warp * BATCH; bb < stop; bb += (uint64_t)WARPS * BATCH) {
-      const uint32_t nb = stop - bb < (uint64_t)BATCH ? (uint32_t)(stop - bb) : (uint32_t)BATCH;
-      __syncwarp();  // the previous batch's slot reads are done
+    // row ids of a batch, loaded one batch ahead so their latency hides behind the arithmetic
+    auto load_ids = [&](uint64_t b0, uint32_t (&ids)[VPT]) {
 #pragma unroll
       for (int r = 0; r < VPT; ++r) {
-        const uint32_t i = lane + 32u * r;
-        s_row[i] = i < nb ? __ldg(P.idx + bb + i) : 0xffffffffu;
+        const uint64_t i = b0 + lane + 32u * r;
+        ids[r] = i < stop ? __ldg(P.idx + i) : 0xffffffffu;
       }
+    };
+    uint32_t ids_next[VPT];
+    load_ids(pos + (uint64_t)warp * BATCH, ids_next);
+    for (uint64_t bb = pos + (uint64_t)warp * BATCH; bb < stop; bb += (uint64_t)WARPS * BATCH) {
+      __syncwarp();  // the previous batch's slot reads are done
+#pragma unroll
+      for (int r = 0; r < VPT; ++r) s_row[lane + 32u * r] = ids_next[r];
+      load_ids(bb + (uint64_t)WARPS * BATCH, ids_next);
       __syncwarp();
       // rows -> slots: RPI rows of N / 4 chunks per warp instruction, 16 B cp.async each
 #pragma unroll 4
