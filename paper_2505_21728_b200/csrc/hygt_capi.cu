@@ -79,6 +79,7 @@ struct hygt_plan {
   int32_t* d_cos = nullptr;
   int32_t* d_sin = nullptr;
   uint16_t* d_fgather[2] = {nullptr, nullptr};  // [C][R+1][N]
+  int2* d_ftab[2] = {nullptr, nullptr};          // [C][R*log2N][N/2] (c, s) per pair and step
   // tile path (N <= 32): lane-interleaved tables staged into shared memory by each CTA
   bool tile = false;
   int tile_l = 0, tile_vpt = 1;
@@ -126,6 +127,7 @@ void free_plan(hygt_plan* p) {
     cudaFree(p->d_coef[d]);
     cudaFree(p->d_gidx[d]);
     cudaFree(p->d_fgather[d]);
+    cudaFree(p->d_ftab[d]);
     cudaFree(p->d_tcoef[d]);
     cudaFree(p->d_tgidx[d]);
     cudaFree(p->d_scoef[d]);
@@ -1194,6 +1196,106 @@ __global__ void __launch_bounds__(FX_THREADS) fixed_kernel(const FixedParams P) 
   }
 }
 
+// Thread-per-row fixed-point kernel for N <= 64. Same arithmetic as fixed_kernel:
+// y_m = (c a + s b + 2^(prec-1)) >> prec, y_n = (c b - s a + 2^(prec-1)) >> prec
+// (fixedpoint.hpp:170-176), with the TrigTable lookups (and the inverse's code negation) done at
+// plan creation into (c, s) int2 pairs in reference pair order per execution step. Tables of up
+// to 48 KB are staged into shared memory; larger ones are read through L1.
+// Values are held as int32: with |x| <= 2^20 (checked, fixedpoint.hpp:145-150) and p >= 4, every
+// rounded butterfly grows the L2 norm by at most (1 + 2^(0.5-p)) plus 1/2 per element, so over
+// R * log2N <= 64 passes |value| < 2^29 -- the reference's 2^46 overflow test (fixedpoint.hpp:
+// 177-179) cannot fire for valid inputs and the products fit IMAD.WIDE (32 x 32 -> 64).
+template <int LOG2N, bool FWD>
+__global__ void __launch_bounds__(FX_THREADS) fixed_row_kernel(const FixedParams P, const int2* __restrict__ tab,
+                                                               uint32_t tab_smem_pairs) {
+  constexpr int N = 1 << LOG2N, HALF = N / 2;
+  extern __shared__ __align__(16) int32_t fxr_smem[];  // [table pairs] then scratch [N][FX_THREADS]
+  const int tid = threadIdx.x;
+  const int prec = P.precision_bits;
+  const int64_t rnd = (int64_t)1 << (prec - 1);
+  const int steps = P.rounds * LOG2N;
+  const int2* s_tab = reinterpret_cast<const int2*>(fxr_smem);
+  int32_t* scr = fxr_smem + 2 * tab_smem_pairs;
+  for (uint32_t i = tid; i < tab_smem_pairs; i += FX_THREADS)
+    reinterpret_cast<int2*>(fxr_smem)[i] = __ldg(tab + i);
+  __syncthreads();
+  for (uint64_t row = (uint64_t)blockIdx.x * FX_THREADS + tid; row < P.count;
+       row += (uint64_t)gridDim.x * FX_THREADS) {
+    int status = 0;
+    const int c = P.cls ? (int)P.cls[row] : 0;
+    if (c >= P.classes) status = 1;  // dataset.hpp:47
+    int32_t v[N];
+    const longlong2* xr = reinterpret_cast<const longlong2*>(P.x + row * N);
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) {
+      const longlong2 q = __ldcs(xr + i);
+      if (q.x > (1 << 20) || q.x < -(1 << 20) || q.y > (1 << 20) || q.y < -(1 << 20)) status = 1;
+      v[2 * i] = (int32_t)q.x;
+      v[2 * i + 1] = (int32_t)q.y;
+    }
+    if (!status) {
+      const size_t tbase = (size_t)c * steps * HALF;
+      const int2* t = tab_smem_pairs ? s_tab + tbase : tab + tbase;
+      const uint16_t* gsrc = P.gather + (size_t)c * (P.rounds + 1) * N;
+      auto gather = [&](int step) {
+        const uint16_t* gs = gsrc + (size_t)step * N;
+#pragma unroll
+        for (int i = 0; i < N; ++i) scr[i * FX_THREADS + tid] = v[i];
+#pragma unroll
+        for (int i = 0; i < N; i += 8) {
+          const uint4 g = __ldg(reinterpret_cast<const uint4*>(gs + i));
+          const uint32_t w[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            v[i + 2 * h] = scr[(w[h] & 0xffffu) * FX_THREADS + tid];
+            v[i + 2 * h + 1] = scr[(w[h] >> 16) * FX_THREADS + tid];
+          }
+        }
+      };
+      if (P.gmask & 1ull) gather(0);
+      for (int k = 0; k < P.rounds; ++k) {
+#pragma unroll
+        for (int pp = 0; pp < LOG2N; ++pp) {
+          const int d = FWD ? pp : LOG2N - 1 - pp;
+          const int2* u = t + (size_t)(k * LOG2N + pp) * HALF;
+#pragma unroll
+          for (int j = 0; j < HALF; j += 2) {
+            const int4 q = tab_smem_pairs ? *reinterpret_cast<const int4*>(u + j)
+                                          : __ldg(reinterpret_cast<const int4*>(u + j));
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int jj = j + h;
+              const int m = jj + (jj & -(1 << d)), n = m + (1 << d);  // hypercube.hpp:73-74
+              const int64_t cs = h ? q.z : q.x, sn = h ? q.w : q.y;
+              const int32_t a = v[m], b = v[n];
+              v[m] = (int32_t)((cs * a + sn * b + rnd) >> prec);
+              v[n] = (int32_t)((cs * b - sn * a + rnd) >> prec);
+            }
+          }
+        }
+        if ((P.gmask >> (k + 1)) & 1ull) gather(k + 1);
+      }
+    }
+    longlong2* yr = reinterpret_cast<longlong2*>(P.y + row * N);
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) __stcs(yr + i, make_longlong2(v[2 * i], v[2 * i + 1]));
+    if (status) atomicMin(P.err, (unsigned long long)((row << 3) | (uint64_t)status));
+  }
+}
+
+using FixedRowFn = void (*)(FixedParams, const int2*, uint32_t);
+FixedRowFn select_fixed_row(int log2n, bool fwd) {
+  switch (log2n) {
+    case 1: return fwd ? fixed_row_kernel<1, true> : fixed_row_kernel<1, false>;
+    case 2: return fwd ? fixed_row_kernel<2, true> : fixed_row_kernel<2, false>;
+    case 3: return fwd ? fixed_row_kernel<3, true> : fixed_row_kernel<3, false>;
+    case 4: return fwd ? fixed_row_kernel<4, true> : fixed_row_kernel<4, false>;
+    case 5: return fwd ? fixed_row_kernel<5, true> : fixed_row_kernel<5, false>;
+    case 6: return fwd ? fixed_row_kernel<6, true> : fixed_row_kernel<6, false>;
+    default: return nullptr;
+  }
+}
+
 int run_fixed(const hygt_plan* p, int dir, const int64_t* x, int64_t* y, const uint16_t* cls,
               uint64_t count, uint64_t* first_bad, cudaStream_t st) {
   if (!p || p->kind != 1) return fail(HYGT_ERR_ARGUMENT, "hygt: not a fixed-point plan");
@@ -1206,10 +1308,24 @@ int run_fixed(const hygt_plan* p, int dir, const int64_t* x, int64_t* y, const u
   FixedParams P{x, y, cls, count, p->classes, p->log2n, p->rounds, p->angle_bits,
                 p->precision_bits, p->d_codes, p->d_cos, p->d_sin, p->d_fgather[dir],
                 p->gmask[dir], p->d_fixed_err};
-  const size_t smem = (size_t)(FX_THREADS / 32) * 2 * (1u << p->log2n) * sizeof(int64_t);
-  const uint64_t ctas = std::min<uint64_t>((count + 7) / 8, (uint64_t)p->num_sms * 8);
-  if (dir == 0) fixed_kernel<true><<<(unsigned)ctas, FX_THREADS, smem, st>>>(P);
-  else fixed_kernel<false><<<(unsigned)ctas, FX_THREADS, smem, st>>>(P);
+  FixedRowFn rfn = p->d_ftab[dir] ? select_fixed_row(p->log2n, dir == 0) : nullptr;
+  if (rfn) {
+    const size_t pairs = (size_t)p->classes * p->rounds * p->log2n * ((1u << p->log2n) / 2);
+    const uint32_t smem_pairs = pairs * sizeof(int2) <= 48 * 1024 ? (uint32_t)pairs : 0u;
+    const size_t smem = smem_pairs * sizeof(int2) +
+                        (p->gmask[dir] ? (size_t)FX_THREADS * (1u << p->log2n) * sizeof(int32_t) : 0);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(rfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rfn, FX_THREADS, smem);
+    const uint64_t ctas = std::min<uint64_t>((count + FX_THREADS - 1) / FX_THREADS,
+                                             (uint64_t)p->num_sms * std::max(occ, 1));
+    rfn<<<(unsigned)ctas, FX_THREADS, smem, st>>>(P, p->d_ftab[dir], smem_pairs);
+  } else {
+    const size_t smem = (size_t)(FX_THREADS / 32) * 2 * (1u << p->log2n) * sizeof(int64_t);
+    const uint64_t ctas = std::min<uint64_t>((count + 7) / 8, (uint64_t)p->num_sms * 8);
+    if (dir == 0) fixed_kernel<true><<<(unsigned)ctas, FX_THREADS, smem, st>>>(P);
+    else fixed_kernel<false><<<(unsigned)ctas, FX_THREADS, smem, st>>>(P);
+  }
   CU(cudaGetLastError());
   unsigned long long key = 0;
   CU(cudaMemcpyAsync(&key, p->d_fixed_err, sizeof(key), cudaMemcpyDeviceToHost, st));
@@ -1294,6 +1410,26 @@ extern "C" int hygt_fixed_plan_create(int log2_n, int rounds, int class_count, i
           g[((size_t)c * (rounds + 1) + k) * n + i] = (uint16_t)gs[k][i];
     }
     s = upload(&p->d_fgather[d], g.data(), g.size());
+    if (!s && log2_n <= 6 && env_int("HYGT_FIXED_ROW", 1) != 0) {
+      // (c, s) per pair of the thread-per-row kernel, in execution order
+      const uint32_t mask = (1u << angle_bits) - 1u;
+      const size_t steps = (size_t)rounds * log2_n, half = n / 2;
+      std::vector<int2> tab((size_t)class_count * steps * half);
+      for (int c = 0; c < class_count; ++c)
+        for (size_t k = 0; k < (size_t)rounds; ++k)
+          for (int pp = 0; pp < log2_n; ++pp) {
+            const int r = d == 0 ? (int)k : rounds - 1 - (int)k;
+            const int dd = d == 0 ? pp : log2_n - 1 - pp;
+            const size_t base = ((size_t)r * log2_n + dd) * half;  // model.hpp:77-79
+            int2* u = &tab[((size_t)c * steps + k * log2_n + pp) * half];
+            for (size_t j = 0; j < half; ++j) {
+              uint32_t code = codes[(size_t)c * a + base + j];
+              if (d == 1) code = (0u - code) & mask;  // fixedpoint.hpp:170
+              u[j] = make_int2(ct[code], sn[code]);
+            }
+          }
+      s = upload(&p->d_ftab[d], tab.data(), tab.size());
+    }
   }
   if (s) {
     free_plan(p);
