@@ -254,7 +254,7 @@ def impl_klt(args, rank, world, local, dev):
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32 (3xTF32 tensor cores)", "data": "synthetic (config-3 rows)",
             "config": {"workload": w.cfg.name, "rows_per_gpu": rows, "N": n, "classes": w.cfg.classes,
-                       "kernel": "klt_tc_kernel<64> tcgen05.mma kind::tf32 M=128 N=64, 3xTF32"},
+                       "kernel": "klt_sw_kernel<64> tcgen05.mma kind::tf32 M=128 N=64, 3xTF32, SWIZZLE_128B operands, double-buffered"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src},
             "tflops_algorithmic": rows * flops / (launch_ms * 1e-3) / 1e12,

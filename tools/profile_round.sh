@@ -11,9 +11,12 @@ prof() {  # name, kernel regex, bench args
   ncu -i /tmp/prof_$1.ncu-rep --page raw --csv > gpurun_out/prof_$1_raw.csv 2>/dev/null
   ncu -i /tmp/prof_$1.ncu-rep --page details --csv > gpurun_out/prof_$1_details.csv 2>/dev/null
 }
-prof cfg2 hygt_tile_kernel ""
+prof cfg2 hygt_stage_kernel ""
 prof cfg1 hygt_jit_kernel "--config 1"
-prof cfg3 hygt_segment_kernel "--config 3"
+prof cfg3 hygt_seg2_kernel "--config 3"
 prof cfg5 hygt_segment_kernel "--config 5"
-prof cfg4 klt_tc_kernel "--config 4"
+prof cfg4 klt_sw_kernel "--config 4"
+prof sort2 hygt_stage_sort "--config 2"
+timeout 300 python tools/fixed_bench.py --config 2 > gpurun_out/fixed_cfg2.json 2>&1
+timeout 300 python tools/fixed_bench.py --config 3 > gpurun_out/fixed_cfg3.json 2>&1
 ls -la gpurun_out | head -40
