@@ -707,6 +707,11 @@ int run_stage(const hygt_plan* p, int dir, const float* x, float* y, const uint1
   P.tile_rows = p->stage_rows;
   P.ent = sorted ? reinterpret_cast<const uint16_t*>(static_cast<const char*>(d_ws) + 256) : nullptr;
   P.block_words = p->stage_block_words;
+  if (!sorted && d_cls) {  // one class: the kernel validates the ids itself (ResidualDataset)
+    if (!d_ws || ws_bytes < 256) return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
+    P.cls = d_cls;
+    P.err = static_cast<uint32_t*>(d_ws);
+  }
   P.trace = g_stage_trace;
   P.debug_skip = g_stage_trace ? (uint32_t)env_int("HYGT_STAGE_DEBUG_SKIP", 0) : 0u;
   const uint64_t tiles = (count + p->stage_rows - 1) / p->stage_rows;
@@ -1005,7 +1010,11 @@ extern "C" int hygt_plan_create(int log2_n, int rounds, int class_count, const d
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)apply_smem(p, d));
   }
   cudaGetLastError();
-  if (jit_supported(log2_n, class_count, rounds) && env_int("HYGT_JIT", 1) != 0) {
+  // The staged kernel (N = 16) matches the NVRTC path's kernel time without its bucketing pass
+  // or its seconds of compilation at plan creation; HYGT_JIT=2 forces the JIT path anyway.
+  const bool stage_first = select_stage(log2_n, standard, true) && env_int("HYGT_STAGE", 1) != 0 &&
+                           class_count <= STAGE_MAX_CLASSES && env_int("HYGT_JIT", 1) != 2;
+  if (!stage_first && jit_supported(log2_n, class_count, rounds) && env_int("HYGT_JIT", 1) != 0) {
     std::string err;
     if (jit_build(log2_n, rounds, class_count, angles, perms, p->perm_mask, p->algo == 0, p->jit, err)) {
       jit_release(p->jit);  // stay on the precompiled kernels

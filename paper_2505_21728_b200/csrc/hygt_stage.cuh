@@ -59,6 +59,8 @@ struct StageParams {
   uint32_t tile_rows;      // T (multiple of 8, <= 1016)
   const uint16_t* ent;     // [tiles][block_words] sorted entry blocks, nullptr: identity order
   uint32_t block_words;    // u16 per entry block: 8 (header: total) + positions
+  const uint16_t* cls;     // identity order with class ids given (one class): validated here
+  uint32_t* err;           // invalid class id flag (identity order)
   unsigned long long* trace;  // debug: per-tile clock64 events of CTA 0 (nullptr = off)
   uint32_t debug_skip;        // debug: consumers skip the arithmetic (timing of the other roles)
 };
@@ -440,14 +442,20 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) hygt_stage_kernel(const S
     return left < T ? (uint32_t)left : T;
   };
 
+  // one class with ids given: the tile's ids ride along in the entry region when aligned
+  auto ids_tma = [&](uint32_t rows) -> bool {
+    return P.cls && !P.ent && (rows % 8u) == 0 && ((reinterpret_cast<uintptr_t>(P.cls) & 15) == 0);
+  };
+
   if (warp == WARPS) {  // ------------------------------------------------ producer warp
     if (lane != 0) return;
     auto load = [&](uint32_t k) {
       const uint32_t s = k % STAGES, rows = tile_rows(k);
       unsigned char* st = smem + L.stage + s * L.stage_bytes;
-      const uint32_t eb = P.ent ? P.block_words * 2u : 0u;
+      const uint32_t eb = P.ent ? P.block_words * 2u : ids_tma(rows) ? rows * 2u : 0u;
       mbar_expect_tx(&full[s], rows * N * 4u + eb);
-      if (eb) bulk_g2s(st + L.ent_off, P.ent + tile_id(k) * P.block_words, eb, &full[s]);
+      if (P.ent) bulk_g2s(st + L.ent_off, P.ent + tile_id(k) * P.block_words, eb, &full[s]);
+      else if (eb) bulk_g2s(st + L.ent_off, P.cls + tile_id(k) * T, eb, &full[s]);  // one class: ids
       bulk_g2s(st, P.x + tile_id(k) * T * N, rows * N * 4u, &full[s]);
     };
     auto store = [&](uint32_t k) {
@@ -509,6 +517,18 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) hygt_stage_kernel(const S
       } else {
 #pragma unroll
         for (int r = 0; r < VPT; ++r) en[r] = p0 + r < rows ? p0 + r : STAGE_PAD;
+        if (P.cls) {  // one class: rows with an id >= 1 pass through unchanged, flagged
+          const uint16_t* ids = ids_tma(rows) ? reinterpret_cast<const uint16_t*>(st + L.ent_off) + p0
+                                              : P.cls + tile_id(k) * T + p0;
+          bool bad = false;
+#pragma unroll
+          for (int r = 0; r < VPT; ++r)
+            if (en[r] != STAGE_PAD && ids[r] != 0) {
+              en[r] = STAGE_PAD;
+              bad = true;
+            }
+          if (bad) atomicOr(P.err, 1u);
+        }
       }
       const uint32_t cls = en[0] == STAGE_PAD ? 0u : en[0] >> 10;
       // Row order inside the thread is free (the VPT rows share every coefficient): put rows of

@@ -77,7 +77,7 @@ def _variants(log2n):
         out.append({"HYGT_JIT": "0", "HYGT_STAGE": "1"})
         out.append({"HYGT_JIT": "0", "HYGT_STAGE": "1", "HYGT_STAGE_ROWS": "136"})
     if log2n <= 5:  # plan-specialised NVRTC kernel (served for plans with <= 4 classes)
-        out.append({"HYGT_JIT": "1"})
+        out.append({"HYGT_JIT": "2"})
     return out
 
 
@@ -322,11 +322,12 @@ def test_reference_adapter(cuda):
     assert "adapter_check: ok" in r.stdout
 
 
-def test_jit_plan_matches_oracle(cuda, oracle_mod):
+def test_jit_plan_matches_oracle(cuda, oracle_mod, monkeypatch):
     """The NVRTC plan-specialised path (coefficients as immediates, permutations as register
     renames) on config-1 style plans: 1-4 classes, inter-round and final permutations, both
     arithmetic forms, tails, invalid class ids."""
     from paper_2505_21728_b200 import ArgumentError, HyGTModel
+    monkeypatch.setenv("HYGT_STAGE", "0")  # N = 16 plans otherwise take the staged kernel
     rng = np.random.default_rng(21)
     for log2n, rounds, classes in [(2, 2, 1), (3, 3, 2), (4, 2, 1), (4, 3, 4), (5, 2, 3)]:
         n = 1 << log2n
