@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) hygt_seg2_kernel(const Seg2Para
   constexpr uint32_t RS = seg2_row_stride(LOG2N);
   constexpr int RPI = 32 / NC;  // rows per coalesced warp instruction
   static_assert(NC <= 32 && 32 % NC == 0, "seg2: N in {16, ..., 128}");
-  static_assert(2 * N * 128 <= BATCH * RS, "seg2: permutation scratch must fit the slot area");
+  static_assert(VPT * N * 128 <= BATCH * RS, "seg2: permutation scratch must fit the slot area");
   extern __shared__ __align__(128) unsigned char smem[];
   const int C = P.classes;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
