@@ -129,6 +129,19 @@ int hygt_forward_i64(const hygt_plan* plan, const int64_t* d_x, int64_t* d_y,
 int hygt_inverse_i64(const hygt_plan* plan, const int64_t* d_y, int64_t* d_x,
                      const uint16_t* d_cls, uint64_t count, uint64_t* first_bad, void* stream);
 
+/* ---- per-class correlation accumulation -------------------------------------
+ * <- hygt::CorrelationAccumulator::add / count (include/hygt/statistics.hpp:63-99), one per class
+ *    as `hygt train` builds them (tools/hygt_main.cpp:85-87). Accumulates, stream-ordered:
+ *    d_sum[c] += sum over rows of class c of r r^T (fp64, [C][N][N], full symmetric matrix) and
+ *    d_count[c] += rows. Products of the fp32 samples are exact in fp64 and summed in fp64.
+ *    finalize() is d_sum[c] / d_count[c]; shards merge by adding sums and counts
+ *    (merge_correlation, statistics.hpp:110-120). Rows with a class id >= class_count are not
+ *    counted and are reported by hygt_sync_status(NULL, d_ws, stream). log2_n in [2, 8]. */
+size_t hygt_correlation_workspace_bytes(int class_count, uint64_t count);
+int hygt_correlation_f64(int log2_n, int class_count, const float* d_x, const uint16_t* d_cls,
+                         uint64_t count, double* d_sum, unsigned long long* d_count, void* d_ws,
+                         size_t ws_bytes, void* stream);
+
 /* ---- dense per-class KLT (comparison path) ------------------------------------------------
  * k: host [class_count][n][n] fp64 row-major (rows = basis vectors, KLTResult::basis). */
 int hygt_klt_plan_create(int n, int class_count, const double* k, uint32_t flags,

@@ -298,6 +298,39 @@ int hygt_oracle_class_energy(int log2_n, int rounds, int classes, const double* 
   return run_jobs(&p, count, threads, 1);
 }
 
+/* ============================== correlation (f3) ========================================= */
+
+/* CorrelationAccumulator::add (statistics.hpp:69-76): sum(i, j) += r_i * r_j for j >= i, in row
+ * order, on the fp64 values of the fp32 samples (read_rblk widens them, dataset.hpp:106). */
+int hygt_oracle_correlation(int log2_n, int classes, const float* x, const uint16_t* cls,
+                            uint64_t count, double* sum, uint64_t* counts) {
+  const size_t n = (size_t)1 << log2_n;
+  for (uint64_t k = 0; k < count; ++k) {
+    const int c = cls ? (int)cls[k] : 0;
+    if (c >= classes) return HYGT_ORACLE_ARGUMENT;
+    double* s = sum + (size_t)c * n * n;
+    const float* r = x + k * n;
+    for (size_t i = 0; i < n; ++i) {
+      const double ri = (double)r[i];
+      for (size_t j = i; j < n; ++j) s[i * n + j] += ri * (double)r[j];
+    }
+    counts[c] += 1;
+  }
+  for (int c = 0; c < classes; ++c) {  /* mirrored as finalize does (:86-91) */
+    double* s = sum + (size_t)c * n * n;
+    for (size_t i = 0; i < n; ++i)
+      for (size_t j = i + 1; j < n; ++j) s[j * n + i] = s[i * n + j];
+  }
+  return HYGT_ORACLE_OK;
+}
+
+/* CorrelationAccumulator::finalize (statistics.hpp:81-94): phi(i, j) = sum(i, j) * (1 / count). */
+void hygt_oracle_correlation_finalize(int log2_n, const double* sum, uint64_t count, double* phi) {
+  const size_t n = (size_t)1 << log2_n;
+  const double inv = 1.0 / (double)count;
+  for (size_t i = 0; i < n * n; ++i) phi[i] = sum[i] * inv;
+}
+
 /* ============================== fixed point ============================================== */
 
 /* fixedpoint.hpp:37-52: entries lround(cos/sin(2*pi*q/2^b) * 2^p). */

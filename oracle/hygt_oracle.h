@@ -111,6 +111,14 @@ int hygt_oracle_klt_apply(int n, int classes, const double* k, const float* x,
                           const uint16_t* cls, uint64_t count, int inverse, double* y,
                           int threads);
 
+/* ---- per-class correlation accumulation: statistics.hpp:63-99 ---------------- */
+/* sum[c] += r r^T over the rows of class c (upper triangle accumulated in row order as
+ * CorrelationAccumulator::add, :69-76, then mirrored), count[c] += rows; rows with a class id
+ * >= classes return HYGT_ORACLE_ARGUMENT. phi = sum * (1 / count) as finalize (:81-94). */
+int hygt_oracle_correlation(int log2_n, int classes, const float* x, const uint16_t* cls,
+                            uint64_t count, double* sum, uint64_t* counts);
+void hygt_oracle_correlation_finalize(int log2_n, const double* sum, uint64_t count, double* phi);
+
 /* ---- synthetic fixtures --------------------------------------------------- */
 /* Seeded Fisher-Yates permutation as tests/oracles.hpp:94-100. */
 void hygt_oracle_fisher_yates(hygt_oracle_rng* r, uint16_t* perm, int n);

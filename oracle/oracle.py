@@ -47,6 +47,9 @@ def lib():
         L = C.CDLL(_ORACLE_SO)
         L.hygt_oracle_apply_batch.argtypes = [_i, _i, _i, _p, _p, _u32, _p, _p, _u64, _i, _p, _i]
         L.hygt_oracle_class_energy.argtypes = [_i, _i, _i, _p, _p, _u32, _p, _p, _u64, _p, _i]
+        L.hygt_oracle_correlation.argtypes = [_i, _i, _p, _p, _u64, _p, _p]
+        L.hygt_oracle_correlation_finalize.argtypes = [_i, _p, _u64, _p]
+        L.hygt_oracle_correlation_finalize.restype = None
         L.hygt_oracle_forward_chain.argtypes = [_i, _i, _p, _p, _u32, _p]
         L.hygt_oracle_inverse_chain.argtypes = [_i, _i, _p, _p, _u32, _p]
         L.hygt_oracle_to_matrix.argtypes = [_i, _i, _p, _p, _u32, _p]
@@ -171,6 +174,27 @@ def class_energy(log2_n, rounds, angles, perms, perm_mask, x, cls=None, threads=
                                    perm_mask, _ptr(x), _ptr(_c(cls, np.uint16)), x.size // n,
                                    _ptr(e), threads or os.cpu_count())
     return e
+
+
+def correlation(log2_n, classes, x, cls=None):
+    """(sum [C][N][N], counts [C]) of r r^T per class (CorrelationAccumulator::add restated)."""
+    x = _c(x, np.float32)
+    n = 1 << log2_n
+    s = np.zeros((classes, n, n), np.float64)
+    k = np.zeros(classes, np.uint64)
+    st = lib().hygt_oracle_correlation(log2_n, classes, _ptr(x), _ptr(_c(cls, np.uint16)), x.size // n,
+                                       _ptr(s), _ptr(k))
+    if st:
+        raise ValueError("oracle: class id out of range")
+    return s, k
+
+
+def correlation_finalize(log2_n, sums, count):
+    n = 1 << log2_n
+    sums = _c(sums, np.float64)
+    phi = np.empty((n, n), np.float64)
+    lib().hygt_oracle_correlation_finalize(log2_n, _ptr(sums), int(count), _ptr(phi))
+    return phi
 
 
 def trig_table(angle_bits, precision_bits):

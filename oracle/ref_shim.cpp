@@ -291,6 +291,31 @@ int ref_rng_stream(std::uint64_t seed, int kind, std::uint64_t bound, std::uint6
   return 0;
 }
 
+// Per-class CorrelationAccumulator (statistics.hpp:63-99): phi[c] = finalize() over the rows of
+// class c (fp64 values of the fp32 samples), counts[c] = count().
+int ref_correlation(int log2_n, int classes, const float* x, const std::uint16_t* cls,
+                    std::uint64_t count, double* phi, std::uint64_t* counts) {
+  try {
+    const std::size_t n = std::size_t{1} << log2_n;
+    std::vector<hygt::CorrelationAccumulator> acc;
+    for (int c = 0; c < classes; ++c) acc.emplace_back(n);
+    std::vector<double> r(n);
+    for (std::uint64_t k = 0; k < count; ++k) {
+      for (std::size_t i = 0; i < n; ++i) r[i] = static_cast<double>(x[k * n + i]);
+      acc.at(cls ? cls[k] : 0).add(r);
+    }
+    for (int c = 0; c < classes; ++c) {
+      counts[c] = acc[c].count();
+      if (!acc[c].count()) continue;
+      const auto m = acc[c].finalize();
+      std::memcpy(phi + (std::size_t)c * n * n, m.values().data().data(), n * n * sizeof(double));
+    }
+    return 0;
+  } catch (...) {
+    return status_of_current();
+  }
+}
+
 int ref_ar1_covariance_2d(int block_size, double rho, double* out) {
   try {
     const auto phi = hygt::ar1_covariance_2d(block_size, rho);

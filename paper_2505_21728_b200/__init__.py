@@ -11,8 +11,8 @@ from .errors import (ArgumentError, CudaError, IoError, NumericalError,  # noqa:
 from .model import (HyGTModel, ModelBundle, QuantizedHyGTModel, TransformKind,  # noqa: F401
                     TrigTable, build_trig_table, dequantize_model, hypercube_indices,
                     memory_footprint, num_parameters, quantize_model, validate_permutation)
-from .plan import (FixedPlan, HyGTPlan, KLTPlan, forward, forward_fixed, inverse,  # noqa: F401
-                   inverse_fixed)
+from .plan import (FixedPlan, HyGTPlan, KLTPlan, correlation, finalize_correlation,  # noqa: F401
+                   forward, forward_fixed, inverse, inverse_fixed)
 
 __all__ = [
     "ArgumentError", "IoError", "NumericalError", "OverflowError", "CudaError",
@@ -20,4 +20,5 @@ __all__ = [
     "build_trig_table", "quantize_model", "dequantize_model", "hypercube_indices",
     "memory_footprint", "num_parameters", "validate_permutation",
     "HyGTPlan", "FixedPlan", "KLTPlan", "forward", "inverse", "forward_fixed", "inverse_fixed",
+    "correlation", "finalize_correlation",
 ]

@@ -49,3 +49,12 @@ def sharded_forward_energy(plan, x_shard, cls_shard, energy, out=None, workspace
     y = plan.forward_energy(x_shard, cls_shard, energy, out=out, workspace=workspace)
     allreduce_energy(energy, group)
     return y
+
+
+def allreduce_correlation(sums, counts, group=None):
+    """Shards of the per-class second moments merge by addition (merge_correlation,
+    statistics.hpp:110-120 weights by counts, which is the same as adding sums and counts)."""
+    import torch.distributed as dist
+    dist.all_reduce(sums, group=group)
+    dist.all_reduce(counts, group=group)
+    return sums, counts

@@ -360,3 +360,36 @@ def forward_fixed(model: QuantizedHyGTModel, table: TrigTable, x) -> np.ndarray:
 def inverse_fixed(model: QuantizedHyGTModel, table: TrigTable, y) -> np.ndarray:
     """hygt::inverse_fixed (fixedpoint.hpp:210-224), bit-exact, on the GPU."""
     return _fixed(model, table, y, True)
+
+
+# ---- per-class correlation accumulation (SURVEY 8 f3) ------------------------------------------
+def correlation(x: torch.Tensor, cls: Optional[torch.Tensor], classes: int,
+                sums: Optional[torch.Tensor] = None, counts: Optional[torch.Tensor] = None,
+                workspace: Optional[torch.Tensor] = None, stream=None):
+    """sums[c] += sum of r r^T over the rows of class c, counts[c] += rows (fp64, on the GPU):
+    CorrelationAccumulator::add per class (statistics.hpp:63-99). Returns (sums, counts)."""
+    if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dtype != torch.float32 or not x.is_contiguous():
+        raise ArgumentError("correlation: x must be a contiguous CUDA float32 tensor")
+    n = x.shape[-1]
+    log2_n = n.bit_length() - 1
+    if n != 1 << log2_n:
+        raise ArgumentError("correlation: row length must be a power of two")
+    count = x.numel() // n
+    if sums is None:
+        sums = torch.zeros(classes, n, n, dtype=torch.float64, device=x.device)
+    if counts is None:
+        counts = torch.zeros(classes, dtype=torch.int64, device=x.device)
+    nbytes = _lib.lib().hygt_correlation_workspace_bytes(classes, count)
+    if workspace is None or workspace.numel() < nbytes:
+        workspace = torch.zeros(nbytes, dtype=torch.uint8, device=x.device)
+    _check(_lib.lib().hygt_correlation_f64(log2_n, classes, x.data_ptr(), _dev_ptr(cls), count,
+                                           sums.data_ptr(), counts.data_ptr(), workspace.data_ptr(),
+                                           workspace.numel(), _stream_ptr(stream)))
+    _check(_lib.lib().hygt_sync_status(None, workspace.data_ptr(), _stream_ptr(stream)))
+    return sums, counts
+
+
+def finalize_correlation(sums: torch.Tensor, counts: torch.Tensor) -> torch.Tensor:
+    """phi[c] = sums[c] * (1 / counts[c]) (CorrelationAccumulator::finalize, statistics.hpp:81-94)."""
+    inv = 1.0 / counts.to(torch.float64).clamp(min=1)
+    return sums * inv[:, None, None]

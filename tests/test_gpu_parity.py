@@ -444,3 +444,41 @@ def test_seg2_path_edges(cuda, oracle_mod, standard):
     with pytest.raises(ArgumentError):
         plan.sync_status()
     assert torch.equal(y[123], x[123])
+
+
+@pytest.mark.parametrize("log2n,classes,count", [(2, 1, 1000), (4, 3, 20000), (6, 5, 30001), (8, 2, 3000)])
+def test_correlation_vs_oracle(cuda, oracle_mod, log2n, classes, count):
+    """Per-class r r^T sums and counts against the oracle restatement of
+    CorrelationAccumulator (pinned bit for bit to the reference in test_oracle.py). Products of
+    fp32 samples are exact in fp64; only the order of the fp64 additions differs."""
+    from paper_2505_21728_b200 import correlation, finalize_correlation
+    from oracle import oracle as O
+    rng = np.random.default_rng(60 + log2n)
+    n = 1 << log2n
+    x = (rng.standard_normal((count, n)) * 16).astype(np.float32)
+    cls = rng.integers(0, classes, count).astype(np.uint16)
+    ref_s, ref_k = O.correlation(log2n, classes, x, cls)
+    xd, cd = torch.from_numpy(x).to(cuda), torch.from_numpy(cls).to(cuda)
+    s, k = correlation(xd, cd, classes)
+    assert np.array_equal(k.cpu().numpy().astype(np.uint64), ref_k)
+    s = s.cpu().numpy()
+    assert np.abs(s - ref_s).max() <= 1e-12 * np.abs(ref_s).max()
+    # two shards accumulate into the same sums == the whole batch (merge_correlation)
+    half = count // 2
+    s2, k2 = correlation(xd[:half].contiguous(), cd[:half], classes)
+    correlation(xd[half:].contiguous(), cd[half:], classes, sums=s2, counts=k2)
+    assert np.abs(s2.cpu().numpy() - ref_s).max() <= 1e-12 * np.abs(ref_s).max()
+    phi = finalize_correlation(s2, k2).cpu().numpy()
+    for c in range(classes):
+        ref_phi = O.correlation_finalize(log2n, ref_s[c], ref_k[c])
+        assert np.abs(phi[c] - ref_phi).max() <= 1e-12 * np.abs(ref_phi).max()
+
+
+def test_correlation_invalid_ids(cuda):
+    from paper_2505_21728_b200 import ArgumentError, correlation
+    x = torch.randn(100, 16, device=cuda)
+    cls = torch.zeros(100, dtype=torch.int16, device=cuda).view(torch.uint16) if hasattr(torch, "uint16") else None
+    c = torch.from_numpy(np.zeros(100, np.uint16)).to(cuda)
+    c[5] = 2
+    with pytest.raises(ArgumentError):
+        correlation(x, c, 2)

@@ -166,3 +166,30 @@ def test_ref_shim_matches_oracle_randomised(oracle_mod):
             a = O.apply_batch(log2n, rounds, ang, perms, mask, x, cls, inverse=inv)
             b = O.ref_apply_batch(log2n, rounds, ang, perms, mask, x, cls, inverse=inv)
             assert np.array_equal(a, b)
+
+
+def test_correlation_oracle_matches_reference_accumulator(oracle_mod):
+    """hygt_oracle_correlation restates CorrelationAccumulator (statistics.hpp:63-99); pinned
+    bit for bit against the unmodified reference (oracle/_ref/libhygt_ref.so, ref_correlation)."""
+    import ctypes
+    import os
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "libhygt_ref.so")
+    if not os.path.exists(path):
+        pytest.skip("oracle/_ref/libhygt_ref.so not built")
+    ref = ctypes.CDLL(path)
+    p = ctypes.c_void_p
+    ref.ref_correlation.argtypes = [ctypes.c_int, ctypes.c_int, p, p, ctypes.c_uint64, p, p]
+    rng = np.random.default_rng(7)
+    for log2n, classes, count in [(2, 1, 50), (4, 3, 500), (6, 5, 300)]:
+        n = 1 << log2n
+        x = (rng.standard_normal((count, n)) * 16).astype(np.float32)
+        cls = rng.integers(0, classes, count).astype(np.uint16)
+        sums, counts = oracle_mod.correlation(log2n, classes, x, cls)
+        phi_ref = np.zeros((classes, n, n))
+        cnt_ref = np.zeros(classes, np.uint64)
+        assert ref.ref_correlation(log2n, classes, x.ctypes.data, cls.ctypes.data, count,
+                                   phi_ref.ctypes.data, cnt_ref.ctypes.data) == 0
+        assert np.array_equal(counts, cnt_ref)
+        for c in range(classes):
+            phi = oracle_mod.correlation_finalize(log2n, sums[c], counts[c])
+            assert np.array_equal(phi, phi_ref[c])  # same loop order: bit-exact
