@@ -73,3 +73,44 @@ def test_energy_allreduce_world2_gloo():
     for _, _, e, t in res:
         np.testing.assert_allclose(e, full, rtol=1e-12)
         assert t == 2.0
+
+
+def _corr_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle as O
+        from paper_2505_21728_b200.dist import allreduce_correlation, shard_range
+        rng = np.random.default_rng(4)
+        x = (rng.standard_normal((777, 16)) * 16).astype(np.float32)
+        cls = rng.integers(0, 3, 777).astype(np.uint16)
+        a, b = shard_range(777, rank, world)
+        s, k = O.correlation(4, 3, x[a:b], cls[a:b])
+        s, k = torch.from_numpy(s), torch.from_numpy(k.astype(np.int64))
+        allreduce_correlation(s, k)
+        q.put((rank, s.numpy(), k.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_correlation_allreduce_world2_gloo():
+    """Per-class second moments of two shards all-reduce to the whole batch's (SURVEY 8 f3;
+    merge_correlation, statistics.hpp:110-120)."""
+    from oracle import oracle as O
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_corr_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rng = np.random.default_rng(4)
+    x = (rng.standard_normal((777, 16)) * 16).astype(np.float32)
+    cls = rng.integers(0, 3, 777).astype(np.uint16)
+    s_full, k_full = O.correlation(4, 3, x, cls)
+    for _, s, k in res:
+        np.testing.assert_allclose(s, s_full, rtol=1e-12)
+        assert np.array_equal(k, k_full.astype(np.int64))
