@@ -112,5 +112,5 @@ def test_correlation_allreduce_world2_gloo():
     cls = rng.integers(0, 3, 777).astype(np.uint16)
     s_full, k_full = O.correlation(4, 3, x, cls)
     for _, s, k in res:
-        np.testing.assert_allclose(s, s_full, rtol=1e-12)
+        assert np.abs(s - s_full).max() <= 1e-12 * np.abs(s_full).max()  # fp64 addition order only
         assert np.array_equal(k, k_full.astype(np.int64))
