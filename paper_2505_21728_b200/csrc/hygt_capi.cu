@@ -805,6 +805,7 @@ int run_seg2(const hygt_plan* p, int dir, const float* x, float* y, uint64_t cou
   P.gtab = p->d_sgtab[dir];
   P.gstride = stage_gstride(p->log2n, p->rounds);
   P.gmask = p->gmask[dir];
+  P.use_tma = env_int("HYGT_SEG2_TMA", 0);  // per-row bulk copies measured slower (2.73e9 vs 3.00e9 vec/s)
   const uint64_t min_span = 4096;
   uint64_t ctas = std::min<uint64_t>((uint64_t)p->num_sms, (count + min_span - 1) / min_span);
   if (ctas < 1) ctas = 1;
