@@ -70,6 +70,7 @@ def _variants(log2n):
         out.append({"HYGT_SEG2": "0", "HYGT_SEGMENT": "1", "HYGT_SEG_VARIANT": str(v)})
     if log2n in SEG2_LOG2N:  # thread-per-row kernel over global class buckets
         out.append({"HYGT_SEG2": "1"})
+        out.append({"HYGT_SEG2": "1", "HYGT_SEG2_TMA": "1"})
     for l, v in TILE_LAYOUTS.get(log2n, []):
         out.append({"HYGT_JIT": "0", "HYGT_STAGE": "0", "HYGT_TILE": "1", "HYGT_TILE_L": str(l),
                     "HYGT_TILE_VPT": str(v)})
