@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include <new>
 #include <string>
 #include <vector>
@@ -80,6 +81,14 @@ struct hygt_plan {
   int32_t* d_sin = nullptr;
   uint16_t* d_fgather[2] = {nullptr, nullptr};  // [C][R+1][N]
   int2* d_ftab[2] = {nullptr, nullptr};          // [C][R*log2N][N/2] (c, s) per pair and step
+  // staged fixed-point kernel (N = 16): element-pair (c, s', c, s') units, sort workspace
+  bool stagefx = false;
+  int4* d_fxtab[2] = {nullptr, nullptr};
+  uint16_t* d_fxgt[2] = {nullptr, nullptr};
+  uint32_t fx_rows = 0, fx_block_words = 0;
+  size_t fx_smem[2] = {0, 0};
+  void* d_fx_ws = nullptr;
+  size_t fx_ws_bytes = 0;
   // tile path (N <= 32): lane-interleaved tables staged into shared memory by each CTA
   bool tile = false;
   int tile_l = 0, tile_vpt = 1;
@@ -128,6 +137,8 @@ void free_plan(hygt_plan* p) {
     cudaFree(p->d_gidx[d]);
     cudaFree(p->d_fgather[d]);
     cudaFree(p->d_ftab[d]);
+    cudaFree(p->d_fxtab[d]);
+    cudaFree(p->d_fxgt[d]);
     cudaFree(p->d_tcoef[d]);
     cudaFree(p->d_tgidx[d]);
     cudaFree(p->d_scoef[d]);
@@ -137,6 +148,7 @@ void free_plan(hygt_plan* p) {
   cudaFree(p->d_cos);
   cudaFree(p->d_sin);
   cudaFree(p->d_fixed_err);
+  cudaFree(p->d_fx_ws);
   jit_release(p->jit);
   delete p->fixed_mu;
   delete p;
@@ -163,6 +175,23 @@ int check_perms(int log2n, int rounds, int classes, const uint16_t* perms, uint3
 int env_int(const char* name, int dflt) {
   const char* v = std::getenv(name);
   return v && *v ? std::atoi(v) : dflt;
+}
+
+// Kernels' dynamic shared-memory limits are per function, shared by every plan; plans need
+// different sizes, so the attribute only ever grows (a smaller later plan must not shrink it
+// under an earlier, larger one).
+void smem_attr(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> set;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& cur = set[fn];
+  if (bytes <= cur) return;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess) cur = bytes;
+  cudaGetLastError();
+}
+template <typename F>
+void smem_attr(F* fn, size_t bytes) {
+  smem_attr(reinterpret_cast<const void*>(fn), bytes);
 }
 
 }  // namespace
@@ -374,7 +403,7 @@ int run_bucket(const hygt_plan* p, int classes, uint64_t chunk_rows, const uint1
   const size_t smem_sc = (size_t)(((classes + 2 + 3) & ~3) + ((classes + 1 + 3) & ~3)) * 4 + BK_TILE * 4;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(bucket_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+    smem_attr(bucket_scatter_kernel, 112 * 1024);
     attr_set = true;
   }
   bucket_scatter_kernel<<<w.tiles, BK_THREADS, smem_sc, st>>>(d_cls, count, classes, base, w.tiles, idx);
@@ -539,7 +568,7 @@ int setup_tile(hygt_plan* p, const double* angles, const uint16_t* perms) {
   for (int d = 0; d < 2; ++d)
     for (int en = 0; en < 2; ++en) {
       TileFn fn = select_tile(p->log2n, l, vpt, p->algo == 0, d == 0, en == 1);
-      if (fn) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->tile_smem[d]);
+      if (fn) smem_attr(fn, (int)p->tile_smem[d]);
     }
   cudaGetLastError();  // no sticky error from the attribute calls
   p->tile = true;
@@ -636,8 +665,7 @@ int setup_stage(hygt_plan* p, const double* angles, const uint16_t* perms) {
   }
   if (T < 128) return HYGT_OK;  // tables too large for the staged layout
   for (int d = 0; d < 2; ++d) {
-    cudaFuncSetAttribute(select_stage(p->log2n, standard, d == 0),
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem[d]);
+    smem_attr(select_stage(p->log2n, standard, d == 0), (int)smem[d]);
     p->stage_smem[d] = smem[d];
   }
   cudaGetLastError();
@@ -645,8 +673,7 @@ int setup_stage(hygt_plan* p, const double* angles, const uint16_t* perms) {
   p->stage_rows = T;
   p->stage_cw = cw;
   p->stage_block_words = stage_block_words(T, STAGE_VPT, C);
-  cudaFuncSetAttribute(select_stage_sort(), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)(STAGE_SORT_WARPS * stage_sort_warp_bytes(C, p->stage_block_words)));
+  smem_attr(select_stage_sort(), (int)(STAGE_SORT_WARPS * stage_sort_warp_bytes(C, p->stage_block_words)));
   cudaGetLastError();
   return HYGT_OK;
 }
@@ -657,28 +684,35 @@ size_t stage_ws_bytes(const hygt_plan* p, uint64_t count) {
   return 256 + tiles * p->stage_block_words * 2;
 }
 
-int run_stage_sort(const hygt_plan* p, const uint16_t* d_cls, uint64_t count, void* d_ws,
-                   size_t ws_bytes, cudaStream_t st) {
-  if (!d_ws || ws_bytes < stage_ws_bytes(p, count)) return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
+// Per-tile class sort of the staged kernels into d_ws (error word, then one entry block per tile).
+int stage_sort(int classes, uint32_t T, uint32_t block_words, int vpt, int num_sms, const uint16_t* d_cls,
+               uint64_t count, void* d_ws, cudaStream_t st) {
   if (count == 0) return ok();
   StageSortParams S{};
   S.cls = d_cls;
   S.count = count;
-  S.classes = p->classes;
-  S.tile_rows = p->stage_rows;
-  S.block_words = p->stage_block_words;
+  S.classes = classes;
+  S.tile_rows = T;
+  S.block_words = block_words;
   S.ent = reinterpret_cast<uint16_t*>(static_cast<char*>(d_ws) + 256);
   S.err = static_cast<uint32_t*>(d_ws);
-  const uint64_t tiles = (count + p->stage_rows - 1) / p->stage_rows;
-  const size_t smem = (size_t)STAGE_SORT_WARPS * stage_sort_warp_bytes(p->classes, p->stage_block_words);
+  const uint64_t tiles = (count + T - 1) / T;
+  StageSortFn fn = select_stage_sort(vpt);
+  const size_t smem = (size_t)STAGE_SORT_WARPS * stage_sort_warp_bytes(classes, block_words);
+  if (smem > 48 * 1024) smem_attr(fn, (int)smem);
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, select_stage_sort(), 32 * STAGE_SORT_WARPS, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 32 * STAGE_SORT_WARPS, smem);
   if (occ < 1) occ = 1;
-  const uint64_t ctas = std::min<uint64_t>((tiles + STAGE_SORT_WARPS - 1) / STAGE_SORT_WARPS,
-                                           (uint64_t)p->num_sms * occ);
-  select_stage_sort()<<<(unsigned)ctas, 32 * STAGE_SORT_WARPS, smem, st>>>(S);
+  const uint64_t ctas = std::min<uint64_t>((tiles + STAGE_SORT_WARPS - 1) / STAGE_SORT_WARPS, (uint64_t)num_sms * occ);
+  fn<<<(unsigned)ctas, 32 * STAGE_SORT_WARPS, smem, st>>>(S);
   CU(cudaGetLastError());
   return ok();
+}
+
+int run_stage_sort(const hygt_plan* p, const uint16_t* d_cls, uint64_t count, void* d_ws,
+                   size_t ws_bytes, cudaStream_t st) {
+  if (!d_ws || ws_bytes < stage_ws_bytes(p, count)) return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
+  return stage_sort(p->classes, p->stage_rows, p->stage_block_words, STAGE_VPT, p->num_sms, d_cls, count, d_ws, st);
 }
 
 bool stage_usable(const hygt_plan* p, const float* x, const float* y, const double* energy) {
@@ -756,12 +790,12 @@ int setup_segment(hygt_plan* p, const double* angles, const uint16_t* perms) {
       p->seg_energy_smem = p->seg_smem[0] + (size_t)(SEG_THREADS / 32) * ((1u << p->log2n) >> sv.l) * 32 * 4;
     if (p->seg_smem[d] > 220 * 1024) return HYGT_OK;
     SegFn fn = select_seg(variant, p->algo == 0, d == 0, false);
-    if (fn) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->seg_smem[d]);
+    if (fn) smem_attr(fn, (int)p->seg_smem[d]);
   }
   // fused energy (forward only): its per-warp partial sums must fit next to the tables
   if (p->seg_energy_smem <= 227 * 1024) {
     SegFn fe = select_seg(variant, p->algo == 0, true, true);
-    if (fe) cudaFuncSetAttribute(fe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->seg_energy_smem);
+    if (fe) smem_attr(fe, (int)p->seg_energy_smem);
   } else {
     p->seg_energy_smem = 0;  // energy requests use the bucketed apply kernel instead
   }
@@ -779,8 +813,7 @@ int setup_seg2(hygt_plan* p, const double* angles, const uint16_t* perms) {
   for (int d = 0; d < 2; ++d) {
     p->seg2_smem[d] = seg2_smem_bytes(p->log2n, SEG2_VPT, SEG2_WARPS, cw, stage_gstride(p->log2n, p->rounds));
     if (p->seg2_smem[d] > 227 * 1024) return HYGT_OK;
-    cudaFuncSetAttribute(select_seg2(p->log2n, p->algo == 0, d == 0),
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->seg2_smem[d]);
+    smem_attr(select_seg2(p->log2n, p->algo == 0, d == 0), (int)p->seg2_smem[d]);
   }
   cudaGetLastError();
   p->stage_cw = cw;
@@ -1008,7 +1041,7 @@ extern "C" int hygt_plan_create(int log2_n, int rounds, int class_count, const d
                       select_apply(log2_n, l, standard, d == 0, d == 0)};
     for (ApplyFn fn : fns)
       if (fn && apply_smem(p, d) > 48 * 1024)
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)apply_smem(p, d));
+        smem_attr(fn, (int)apply_smem(p, d));
   }
   cudaGetLastError();
   // The staged kernel (N = 16) matches the NVRTC path's kernel time without its bucketing pass
@@ -1306,6 +1339,56 @@ FixedRowFn select_fixed_row(int log2n, bool fwd) {
   }
 }
 
+// Staged fixed-point path (hygt_stage_fixed.cuh). Returns a status, or -1 when the sort pass met
+// invalid class ids (the caller re-runs the row kernel, which reports the first failing row).
+// Called with the plan mutex held.
+int run_fixed_staged(const hygt_plan* p, int dir, const int64_t* x, int64_t* y, const uint16_t* cls,
+                     uint64_t count, uint64_t* first_bad, cudaStream_t st) {
+  hygt_plan* mp = const_cast<hygt_plan*>(p);  // the sort workspace is plan-owned, guarded by fixed_mu
+  const bool sorted = cls != nullptr;
+  if (sorted) {
+    const uint64_t tiles = (count + p->fx_rows - 1) / p->fx_rows;
+    const size_t need = 256 + tiles * p->fx_block_words * 2;
+    if (mp->fx_ws_bytes < need) {
+      cudaFree(mp->d_fx_ws);
+      mp->d_fx_ws = nullptr;
+      mp->fx_ws_bytes = 0;
+      CU(cudaMalloc(&mp->d_fx_ws, need));
+      mp->fx_ws_bytes = need;
+    }
+    CU(cudaMemsetAsync(mp->d_fx_ws, 0, 4, st));
+    if (int s = stage_sort(p->classes, p->fx_rows, p->fx_block_words, STAGE_FX_VPT, p->num_sms, cls, count, mp->d_fx_ws, st))
+      return s;
+  }
+  StageFxParams F{};
+  F.x = x;
+  F.y = y;
+  F.count = count;
+  F.classes = p->classes;
+  F.rounds = p->rounds;
+  F.precision_bits = p->precision_bits;
+  F.tab = p->d_fxtab[dir];
+  F.gtab = p->d_fxgt[dir];
+  F.gmask = p->gmask[dir];
+  F.tile_rows = p->fx_rows;
+  F.ent = sorted ? reinterpret_cast<const uint16_t*>(static_cast<char*>(mp->d_fx_ws) + 256) : nullptr;
+  F.block_words = p->fx_block_words;
+  F.err = p->d_fixed_err;
+  const uint64_t tiles = (count + p->fx_rows - 1) / p->fx_rows;
+  StageFxFn fn = select_stage_fixed(p->log2n, dir == 0);
+  fn<<<(unsigned)std::min<uint64_t>(tiles, (uint64_t)p->num_sms), (STAGE_FX_WARPS + 1) * 32, p->fx_smem[dir], st>>>(F);
+  CU(cudaGetLastError());
+  unsigned long long key = 0;
+  uint32_t bad_ids = 0;
+  CU(cudaMemcpyAsync(&key, p->d_fixed_err, sizeof(key), cudaMemcpyDeviceToHost, st));
+  if (sorted) CU(cudaMemcpyAsync(&bad_ids, mp->d_fx_ws, sizeof(bad_ids), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (bad_ids) return -1;
+  if (key == ~0ull) return ok();
+  if (first_bad) *first_bad = key >> 3;
+  return fail(HYGT_ERR_ARGUMENT, "fixed transform: input magnitude exceeds 2^20");
+}
+
 int run_fixed(const hygt_plan* p, int dir, const int64_t* x, int64_t* y, const uint16_t* cls,
               uint64_t count, uint64_t* first_bad, cudaStream_t st) {
   if (!p || p->kind != 1) return fail(HYGT_ERR_ARGUMENT, "hygt: not a fixed-point plan");
@@ -1318,13 +1401,18 @@ int run_fixed(const hygt_plan* p, int dir, const int64_t* x, int64_t* y, const u
   FixedParams P{x, y, cls, count, p->classes, p->log2n, p->rounds, p->angle_bits,
                 p->precision_bits, p->d_codes, p->d_cos, p->d_sin, p->d_fgather[dir],
                 p->gmask[dir], p->d_fixed_err};
+  if (p->stagefx && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
+    const int s = run_fixed_staged(p, dir, x, y, cls, count, first_bad, st);
+    if (s != -1) return s;  // -1: invalid class ids -> the exact first failing row from below
+    CU(cudaMemcpyAsync(p->d_fixed_err, &init, sizeof(init), cudaMemcpyHostToDevice, st));
+  }
   FixedRowFn rfn = p->d_ftab[dir] ? select_fixed_row(p->log2n, dir == 0) : nullptr;
   if (rfn) {
     const size_t pairs = (size_t)p->classes * p->rounds * p->log2n * ((1u << p->log2n) / 2);
     const uint32_t smem_pairs = pairs * sizeof(int2) <= 48 * 1024 ? (uint32_t)pairs : 0u;
     const size_t smem = smem_pairs * sizeof(int2) +
                         (p->gmask[dir] ? (size_t)FX_THREADS * (1u << p->log2n) * sizeof(int32_t) : 0);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(rfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (smem > 48 * 1024) smem_attr(rfn, (int)smem);
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rfn, FX_THREADS, smem);
     const uint64_t ctas = std::min<uint64_t>((count + FX_THREADS - 1) / FX_THREADS,
@@ -1420,6 +1508,63 @@ extern "C" int hygt_fixed_plan_create(int log2_n, int rounds, int class_count, i
           g[((size_t)c * (rounds + 1) + k) * n + i] = (uint16_t)gs[k][i];
     }
     s = upload(&p->d_fgather[d], g.data(), g.size());
+    if (!s && log2_n == 4 && class_count <= STAGE_MAX_CLASSES && env_int("HYGT_FIXED_STAGE", 1) != 0) {
+      // element-pair (c, s', c, s') units per execution step for the staged kernel, and its
+      // permutation offsets (src * 128 into the [element][lane] int32 scratch)
+      const uint32_t mask = (1u << angle_bits) - 1u;
+      const size_t steps = (size_t)rounds * log2_n, half = n / 2;
+      std::vector<int4> tab((size_t)class_count * steps * half);
+      std::vector<int32_t> ce(n), se(n);
+      for (int c = 0; c < class_count; ++c)
+        for (size_t k = 0; k < (size_t)rounds; ++k)
+          for (int pp = 0; pp < log2_n; ++pp) {
+            const int r = d == 0 ? (int)k : rounds - 1 - (int)k;
+            const int dd = d == 0 ? pp : log2_n - 1 - pp;
+            const uint32_t kk = 1u << dd;
+            const size_t base = ((size_t)r * log2_n + dd) * half;  // model.hpp:77-79
+            for (uint32_t j = 0; j < half; ++j) {
+              const uint32_t m = j + (j & (0u - kk)), nn = m + kk;  // hypercube.hpp:73-74
+              uint32_t code = codes[(size_t)c * a + base + j];
+              if (d == 1) code = (0u - code) & mask;  // fixedpoint.hpp:170
+              ce[m] = ce[nn] = ct[code];
+              se[m] = sn[code];
+              se[nn] = -sn[code];
+            }
+            int4* u = &tab[((size_t)c * steps + k * log2_n + pp) * half];
+            for (size_t j = 0; j < half; ++j) u[j] = make_int4(ce[2 * j], se[2 * j], ce[2 * j + 1], se[2 * j + 1]);
+          }
+      const uint32_t gs = stage_gstride(log2_n, rounds) / 2;
+      std::vector<uint16_t> gt((size_t)class_count * gs, 0);
+      for (int c = 0; c < class_count; ++c) {
+        uint64_t gm = 0;
+        const auto g = exec_gathers(log2_n, rounds, perms ? perms + (size_t)c * rounds * n : nullptr,
+                                    p->perm_mask, d == 0, &gm);
+        for (int k = 0; k <= rounds; ++k)
+          for (size_t i = 0; i < g[k].size(); ++i) gt[(size_t)c * gs + (size_t)k * n + i] = (uint16_t)(g[k][i] * 128);
+      }
+      s = upload(&p->d_fxtab[d], tab.data(), tab.size());
+      if (!s) s = upload(&p->d_fxgt[d], gt.data(), gt.size());
+      if (!s && d == 1) {  // both directions built: size the tiles to the shared memory
+        uint32_t T = (uint32_t)std::max(0, STAGE_FX_WARPS * 32 * STAGE_FX_VPT - (STAGE_FX_VPT - 1) * class_count);
+        T = std::min<uint32_t>(T, 1016) / 8 * 8;
+        size_t sm[2] = {0, 0};
+        for (; T >= 64; T -= 8) {
+          for (int e = 0; e < 2; ++e)
+            sm[e] = stage_fx_smem_layout(log2_n, STAGE_FX_VPT, STAGE_FX_WARPS, class_count, rounds, T, p->gmask[e] != 0).total;
+          if (std::max(sm[0], sm[1]) <= 227 * 1024) break;
+        }
+        if (T >= 64) {
+          for (int e = 0; e < 2; ++e) {
+            smem_attr(select_stage_fixed(log2_n, e == 0), (int)sm[e]);
+            p->fx_smem[e] = sm[e];
+          }
+          cudaGetLastError();
+          p->fx_rows = T;
+          p->fx_block_words = stage_block_words(T, STAGE_FX_VPT, class_count);
+          p->stagefx = true;
+        }
+      }
+    }
     if (!s && log2_n <= 6 && env_int("HYGT_FIXED_ROW", 1) != 0) {
       // (c, s) per pair of the thread-per-row kernel, in execution order
       const uint32_t mask = (1u << angle_bits) - 1u;

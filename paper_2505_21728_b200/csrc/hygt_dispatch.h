@@ -5,6 +5,7 @@
 #include "hygt_segment.cuh"
 #include "hygt_stage.cuh"
 #include "hygt_seg2.cuh"
+#include "hygt_stage_fixed.cuh"
 #include "hygt_tile.cuh"
 
 namespace hygt_gpu {
@@ -14,6 +15,7 @@ using SegFn = void (*)(SegParams);
 using StageFn = void (*)(StageParams);
 using StageSortFn = void (*)(StageSortParams);
 using Seg2Fn = void (*)(Seg2Params);
+using StageFxFn = void (*)(StageFxParams);
 constexpr int TILE_THREADS = 512;
 constexpr int SEG_THREADS = 256;
 constexpr int STAGE_WARPS = 7;  // consumer warps (+ one producer warp)
@@ -24,6 +26,9 @@ ApplyFn select_apply(int log2n, int l, bool standard, bool fwd, bool energy);
 TileFn select_tile(int log2n, int l, int vpt, bool standard, bool fwd, bool energy);
 SegFn select_seg(int variant, bool standard, bool fwd, bool energy);
 StageFn select_stage(int log2n, bool standard, bool fwd);
-StageSortFn select_stage_sort();
+StageSortFn select_stage_sort(int vpt = STAGE_VPT);
+constexpr int STAGE_FX_VPT = 2;
+constexpr int STAGE_FX_WARPS = 7;
+StageFxFn select_stage_fixed(int log2n, bool fwd);
 Seg2Fn select_seg2(int log2n, bool standard, bool fwd);
 }  // namespace hygt_gpu

@@ -12,6 +12,14 @@ StageFn select_stage(int log2n, bool standard, bool fwd) {
   return nullptr;
 }
 
-StageSortFn select_stage_sort() { return hygt_stage_sort_kernel<STAGE_VPT>; }
+StageSortFn select_stage_sort(int vpt) {
+  return vpt == 2 ? hygt_stage_sort_kernel<2> : hygt_stage_sort_kernel<STAGE_VPT>;
+}
+
+StageFxFn select_stage_fixed(int log2n, bool fwd) {
+  if (log2n != 4) return nullptr;
+  return fwd ? hygt_stage_fixed_kernel<4, STAGE_FX_VPT, true, STAGE_FX_WARPS>
+             : hygt_stage_fixed_kernel<4, STAGE_FX_VPT, false, STAGE_FX_WARPS>;
+}
 
 }  // namespace hygt_gpu

@@ -256,8 +256,15 @@ def test_fixed_golden_bit_exact(cuda, golden, k):
     assert np.array_equal(z, golden[f"x{k}_inv"][ok2])
 
 
-def test_fixed_random_multiclass_vs_oracle(cuda, oracle_mod):
+@pytest.mark.parametrize("kernel", ["default", "row", "warp"])
+def test_fixed_random_multiclass_vs_oracle(cuda, oracle_mod, kernel, monkeypatch):
+    """Bit-exact vs the oracle through every fixed-point kernel: the staged one (N = 16), the
+    thread-per-row one (N <= 64) and the warp-per-row one."""
     from paper_2505_21728_b200 import FixedPlan, QuantizedHyGTModel, TrigTable
+    if kernel != "default":
+        monkeypatch.setenv("HYGT_FIXED_STAGE", "0")
+    if kernel == "warp":
+        monkeypatch.setenv("HYGT_FIXED_ROW", "0")
     rng = np.random.default_rng(11)
     for log2n, rounds, classes in [(4, 3, 35), (6, 4, 5), (8, 2, 3)]:
         n = 1 << log2n
@@ -483,3 +490,67 @@ def test_correlation_invalid_ids(cuda):
     c[5] = 2
     with pytest.raises(ArgumentError):
         correlation(x, c, 2)
+
+
+def test_fixed_staged_edges(cuda, oracle_mod):
+    """Staged fixed-point kernel (N = 16): partial and multi-tile batches, no class ids, in place,
+    the first failing row for oversized inputs and for invalid class ids."""
+    from paper_2505_21728_b200 import ArgumentError, FixedPlan, QuantizedHyGTModel, TrigTable
+    rng = np.random.default_rng(12)
+    C, R, n = 6, 3, 16
+    codes = rng.integers(0, 256, (C, R * 4 * 8)).astype(np.uint16)
+    inter = np.stack([np.stack([rng.permutation(n) for _ in range(R - 1)]) for _ in range(C)]).astype(np.uint16)
+    full = np.concatenate([inter, np.tile(np.arange(n, dtype=np.uint16), (C, 1, 1))], 1)
+    plan = FixedPlan([QuantizedHyGTModel(4, R, 8, codes[c]) for c in range(C)], TrigTable(8, 10), inter)
+    for count in [1, 7, 100, 333, 5000, 70001]:
+        x = rng.integers(-(1 << 20), (1 << 20) + 1, (count, n)).astype(np.int64)
+        cls = rng.integers(0, C, count).astype(np.uint16)
+        xd, cd = torch.from_numpy(x).cuda(), torch.from_numpy(cls).cuda()
+        st, _, ref = oracle_mod.apply_batch_fixed(4, R, 8, 10, codes, full, (1 << (R - 1)) - 1, x, cls)
+        assert st == 0
+        y = plan.forward(xd, cd)
+        assert np.array_equal(y.cpu().numpy(), ref)
+        xi = xd.clone()
+        plan.forward(xi, cd, out=xi)  # in place
+        assert torch.equal(xi, y)
+    one = FixedPlan(QuantizedHyGTModel(4, R, 8, codes[0]), TrigTable(8, 10))
+    x = rng.integers(-(1 << 20), (1 << 20) + 1, (4000, n)).astype(np.int64)
+    st, _, ref = oracle_mod.apply_batch_fixed(4, R, 8, 10, codes[:1], None, 0, x, None)
+    assert np.array_equal(one.forward(torch.from_numpy(x).cuda()).cpu().numpy(), ref)
+    x[2345, 3] = (1 << 20) + 1
+    x[3000, 0] = -(1 << 21)
+    with pytest.raises(ArgumentError):
+        one.forward(torch.from_numpy(x).cuda())
+    assert one.first_bad == 2345
+    x[2345, 3] = 0
+    cls = rng.integers(0, C, 4000).astype(np.uint16)
+    cls[1500] = C
+    with pytest.raises(ArgumentError):
+        plan.forward(torch.from_numpy(x).cuda(), torch.from_numpy(cls).cuda())
+    assert plan.first_bad == 1500  # invalid class id before the oversized row at 3000
+
+
+def test_plans_of_different_sizes_coexist(cuda):
+    """Kernel shared-memory limits are per function: a smaller plan created later must not break
+    an earlier, larger plan of the same kernel family (stage, seg2, fixed)."""
+    from paper_2505_21728_b200 import FixedPlan, HyGTModel, QuantizedHyGTModel, TrigTable
+    rng = np.random.default_rng(70)
+    for log2n in (4, 6):
+        n = 1 << log2n
+        big = _plan([HyGTModel(log2n, 3, rng.uniform(-3, 3, 3 * log2n * n // 2)) for _ in range(35)],
+                    np.stack([np.stack([rng.permutation(n) for _ in range(2)]) for _ in range(35)]).astype(np.uint16))
+        small = _plan([HyGTModel(log2n, 1, rng.uniform(-3, 3, log2n * n // 2)) for _ in range(2)])
+        x = torch.randn(5000, n, device=cuda)
+        ch = rng.integers(0, 35, 5000).astype(np.uint16)
+        cls = torch.from_numpy(ch).to(cuda)
+        small.forward(x, torch.from_numpy(ch % 2).to(cuda))
+        y = big.forward(x, cls)
+        check_close(big.inverse(y, cls).cpu().numpy(), x.cpu().numpy(), x.cpu().numpy(), f"N={n} big after small")
+    codes = rng.integers(0, 256, (20, 3 * 4 * 8)).astype(np.uint16)
+    inter = np.stack([np.stack([rng.permutation(16) for _ in range(2)]) for _ in range(20)]).astype(np.uint16)
+    fbig = FixedPlan([QuantizedHyGTModel(4, 3, 8, codes[c]) for c in range(20)], TrigTable(8, 10), inter)
+    fsmall = FixedPlan(QuantizedHyGTModel(4, 1, 8, codes[0][:32]), TrigTable(8, 10))
+    xi = torch.from_numpy(rng.integers(-1000, 1000, (3000, 16)).astype(np.int64)).to(cuda)
+    ci = torch.from_numpy(rng.integers(0, 20, 3000).astype(np.uint16)).to(cuda)
+    fsmall.forward(xi)
+    fbig.forward(xi, ci)
