@@ -409,7 +409,8 @@ def measure_e2e(plan, w, x, cls, rows, dev, stream, args, world=1):
     ch = cls.cpu().pin_memory()
     yh = torch.empty_like(xh).pin_memory()
     rh = torch.empty_like(xh).pin_memory()
-    pipe = HostPipeline(plan, rows_per_chunk=min(rows, 1 << 21), device=dev)
+    pipe = HostPipeline(plan, rows_per_chunk=min(rows, int(os.environ.get("HYGT_E2E_CHUNK", 1 << 20))), device=dev,
+                        streams=int(os.environ.get("HYGT_E2E_STREAMS", 4)))
     for _ in range(2):
         pipe.roundtrip(xh, ch, yh, rh)
     torch.cuda.synchronize()
