@@ -102,6 +102,8 @@ struct hygt_plan {
   uint32_t stage_rows = 0, stage_cw = 0, stage_block_words = 0;
   float4* d_scoef[2] = {nullptr, nullptr};
   uint16_t* d_sgtab[2] = {nullptr, nullptr};
+  uint2* d_sbnet[2] = {nullptr, nullptr};  // Beneš swap masks [C][R+1][4 rotations] (N = 16)
+  uint32_t sbnet_steps[2] = {0u, 0u};      // gather steps the Beneš network serves, per direction
   size_t stage_smem[2] = {0, 0};
   // seg2 path (N = 64): thread-per-row over global class buckets, element-ordered tables
   bool seg2 = false;
@@ -143,6 +145,7 @@ void free_plan(hygt_plan* p) {
     cudaFree(p->d_tgidx[d]);
     cudaFree(p->d_scoef[d]);
     cudaFree(p->d_sgtab[d]);
+    cudaFree(p->d_sbnet[d]);
   }
   cudaFree(p->d_codes);
   cudaFree(p->d_cos);
@@ -644,6 +647,13 @@ int build_elem_tables(hygt_plan* p, const double* angles, const uint16_t* perms,
   return HYGT_OK;
 }
 
+// Gather steps the Beneš network serves: all (mode 1) or only the first one (mode 2).
+uint32_t stage_benes_steps(uint64_t gmask, int mode) {
+  if (mode == 1) return (uint32_t)gmask;
+  if (mode == 2) return (uint32_t)(gmask & (0 - gmask));
+  return 0u;
+}
+
 int setup_stage(hygt_plan* p, const double* angles, const uint16_t* perms) {
   StageFn probe = select_stage(p->log2n, p->algo == 0, true);
   if (!probe || env_int("HYGT_STAGE", 1) == 0 || p->classes > STAGE_MAX_CLASSES) return HYGT_OK;
@@ -651,6 +661,41 @@ int setup_stage(hygt_plan* p, const double* angles, const uint16_t* perms) {
   const bool standard = p->algo == 0;
   uint32_t cw = 0;
   if (int s = build_elem_tables(p, angles, perms, &cw)) return s;
+  // In-register permutations: each gather routed through a Beneš network (7 layers of
+  // conditional swaps at N = 16), its swap bits re-indexed for each lane rotation X = x << 2.
+  const int benes_mode = env_int("HYGT_STAGE_BENES", 0);  // 0 off, 1 every gather, 2 the first one
+  const bool benes = (p->gmask[0] || p->gmask[1]) && benes_mode != 0;
+  if (benes) {
+    const int n = 1 << p->log2n, layers = 2 * p->log2n - 1;
+    for (int d = 0; d < 2; ++d) {
+      std::vector<uint2> tab((size_t)C * (R + 1) * 4, make_uint2(0, 0));
+      for (int c = 0; c < C; ++c) {
+        uint64_t gm = 0;
+        const auto g = exec_gathers(p->log2n, R, perms ? perms + (size_t)c * R * n : nullptr, p->perm_mask, d == 0, &gm);
+        for (int k = 0; k <= R; ++k) {
+          if (g[k].empty()) continue;
+          std::vector<std::vector<int>> sw;
+          if (!benes_route(p->log2n, g[k], sw)) return fail(HYGT_ERR_NUMERICAL, "hygt: Benes routing failed");
+          for (int x = 0; x < 4; ++x) {
+            const int X = x << 2;
+            uint64_t bits = 0;
+            for (int l = 0; l < layers; ++l) {
+              const int b = l < p->log2n ? p->log2n - 1 - l : l - p->log2n + 1;
+              int j = 0;
+              for (int i = 0; i < n; ++i) {
+                if (i & (1 << b)) continue;
+                if (sw[l][pair_index((i ^ X) & ~(1 << b), b)]) bits |= 1ull << (8 * l + j);
+                ++j;
+              }
+            }
+            tab[((size_t)c * (R + 1) + k) * 4 + x] = make_uint2((uint32_t)bits, (uint32_t)(bits >> 32));
+          }
+        }
+      }
+      if (int s = upload(&p->d_sbnet[d], tab.data(), tab.size())) return s;
+      p->sbnet_steps[d] = stage_benes_steps(p->gmask[d], benes_mode);
+    }
+  }
   // Tile rows: one batch of 32 * VPT sorted positions per consumer warp, including the padding
   // of every class run to VPT; rows are indexed with 10 bits in the sort entries.
   const long long tenv = env_int("HYGT_STAGE_ROWS", -1);
@@ -660,7 +705,8 @@ int setup_stage(hygt_plan* p, const double* angles, const uint16_t* perms) {
   size_t smem[2] = {0, 0};
   for (; T >= 128; T -= 8) {
     for (int d = 0; d < 2; ++d)
-      smem[d] = stage_smem_layout(p->log2n, STAGE_VPT, STAGE_WARPS, C, cw, R, T, p->gmask[d] != 0).total;
+      smem[d] = stage_smem_layout(p->log2n, STAGE_VPT, STAGE_WARPS, C, cw, R, T, p->gmask[d] != 0, benes,
+                                  benes && (p->gmask[d] & ~(uint64_t)stage_benes_steps(p->gmask[d], benes_mode)) != 0).total;
     if (std::max(smem[0], smem[1]) <= 227 * 1024) break;
   }
   if (T < 128) return HYGT_OK;  // tables too large for the staged layout
@@ -737,6 +783,8 @@ int run_stage(const hygt_plan* p, int dir, const float* x, float* y, const uint1
   P.coef = p->d_scoef[dir];
   P.cw = p->stage_cw;
   P.gtab = p->d_sgtab[dir];
+  P.bnet = p->d_sbnet[dir];
+  P.bnet_steps = p->sbnet_steps[dir];
   P.gmask = p->gmask[dir];
   P.tile_rows = p->stage_rows;
   P.ent = sorted ? reinterpret_cast<const uint16_t*>(static_cast<const char*>(d_ws) + 256) : nullptr;

@@ -77,6 +77,8 @@ def _variants(log2n):
     if log2n in STAGE_LOG2N:  # TMA-staged tile kernel
         out.append({"HYGT_JIT": "0", "HYGT_STAGE": "1"})
         out.append({"HYGT_JIT": "0", "HYGT_STAGE": "1", "HYGT_STAGE_ROWS": "136"})
+        out.append({"HYGT_JIT": "0", "HYGT_STAGE": "1", "HYGT_STAGE_BENES": "1"})  # in-register
+        out.append({"HYGT_JIT": "0", "HYGT_STAGE": "1", "HYGT_STAGE_BENES": "2"})  # mixed
     if log2n <= 5:  # plan-specialised NVRTC kernel (served for plans with <= 4 classes)
         out.append({"HYGT_JIT": "2"})
     return out
