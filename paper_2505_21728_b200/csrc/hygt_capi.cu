@@ -711,7 +711,7 @@ int setup_stage(hygt_plan* p, const double* angles, const uint16_t* perms) {
   }
   if (T < 128) return HYGT_OK;  // tables too large for the staged layout
   for (int d = 0; d < 2; ++d) {
-    smem_attr(select_stage(p->log2n, standard, d == 0), (int)smem[d]);
+    smem_attr(select_stage(p->log2n, standard, d == 0, p->d_sbnet[d] != nullptr), (int)smem[d]);
     p->stage_smem[d] = smem[d];
   }
   cudaGetLastError();
@@ -773,7 +773,9 @@ int run_stage(const hygt_plan* p, int dir, const float* x, float* y, const uint1
     if (int s = run_stage_sort(p, d_cls, count, d_ws, ws_bytes, st)) return s;
   if (sorted && (!d_ws || ws_bytes < stage_ws_bytes(p, count)))
     return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
-  StageFn fn = select_stage(p->log2n, p->algo == 0, dir == 0);
+  // The debug build (trace hook set) is a separate instantiation with the same smem layout.
+  StageFn fn = select_stage(p->log2n, p->algo == 0, dir == 0, p->d_sbnet[dir] != nullptr, g_stage_trace != nullptr);
+  if (g_stage_trace) smem_attr(fn, (int)p->stage_smem[dir]);
   StageParams P{};
   P.x = x;
   P.y = y;

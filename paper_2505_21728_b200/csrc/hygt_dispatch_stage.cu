@@ -3,13 +3,18 @@
 
 namespace hygt_gpu {
 
-StageFn select_stage(int log2n, bool standard, bool fwd) {
+template <int VAR>
+static StageFn stage_variant(bool standard, bool fwd) {
   constexpr int V = STAGE_VPT, W = STAGE_WARPS;
-  if (log2n == 4) {
-    if (standard) return fwd ? hygt_stage_kernel<4, V, true, true, W> : hygt_stage_kernel<4, V, true, false, W>;
-    return fwd ? hygt_stage_kernel<4, V, false, true, W> : hygt_stage_kernel<4, V, false, false, W>;
-  }
-  return nullptr;
+  if (standard) return fwd ? hygt_stage_kernel<4, V, true, true, W, VAR> : hygt_stage_kernel<4, V, true, false, W, VAR>;
+  return fwd ? hygt_stage_kernel<4, V, false, true, W, VAR> : hygt_stage_kernel<4, V, false, false, W, VAR>;
+}
+
+StageFn select_stage(int log2n, bool standard, bool fwd, bool benes, bool debug) {
+  if (log2n != 4) return nullptr;
+  if (debug) return benes ? stage_variant<STAGE_VAR_BENES | STAGE_VAR_DEBUG>(standard, fwd)
+                         : stage_variant<STAGE_VAR_DEBUG>(standard, fwd);
+  return benes ? stage_variant<STAGE_VAR_BENES>(standard, fwd) : stage_variant<0>(standard, fwd);
 }
 
 StageSortFn select_stage_sort(int vpt) {

@@ -55,8 +55,6 @@ struct StageParams {
   const float4* coef;      // [C][cw] float4, element-ordered units per step (see setup_stage)
   uint32_t cw;             // float4 units per class
   const uint16_t* gtab;    // [C][gstride] bytes: [R+1][N] u16 scratch offsets src * 128
-  const uint2* bnet;       // [C][R+1][4] Beneš swap masks per lane rotation (nullptr: scratch gathers)
-  uint32_t bnet_steps;     // gather steps done by the Beneš network (the others via the scratch)
   uint64_t gmask;
   uint32_t tile_rows;      // T (multiple of 8, <= 1016)
   const uint16_t* ent;     // [tiles][block_words] sorted entry blocks, nullptr: identity order
@@ -65,6 +63,8 @@ struct StageParams {
   uint32_t* err;           // invalid class id flag (identity order)
   unsigned long long* trace;  // debug: per-tile clock64 events of CTA 0 (nullptr = off)
   uint32_t debug_skip;        // debug: consumers skip the arithmetic (timing of the other roles)
+  const uint2* bnet;       // [C][R+1][4] Beneš swap masks per lane rotation (nullptr: scratch gathers)
+  uint32_t bnet_steps;     // gather steps done by the Beneš network (the others via the scratch)
 };
 
 struct StageSortParams {
@@ -127,7 +127,7 @@ __device__ __forceinline__ uint32_t su32(const void* p) {
 }
 #define STAGE_TRACE(k, e)                                                           \
   do {                                                                              \
-    if (P.trace && blockIdx.x == 0 && (k) < 64) P.trace[(k) * 16 + (e)] = clock64(); \
+    if (DEBUG && P.trace && blockIdx.x == 0 && (k) < 64) P.trace[(k) * 16 + (e)] = clock64(); \
   } while (0)
 
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
@@ -442,8 +442,13 @@ __global__ void __launch_bounds__(32 * STAGE_SORT_WARPS) hygt_stage_sort_kernel(
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(P.err, 1u);
 }
 
-template <int LOG2N, int VPT, bool STD, bool FWD, int WARPS>
+// Build variants (VAR bits): STAGE_VAR_BENES may route gathers through stage_benes (P.bnet);
+// STAGE_VAR_DEBUG honours P.trace / P.debug_skip. The default build compiles neither: their
+// never-taken branches alone cost ~1-3% of the kernel's time.
+constexpr int STAGE_VAR_BENES = 1, STAGE_VAR_DEBUG = 2;
+template <int LOG2N, int VPT, bool STD, bool FWD, int WARPS, int VAR = 0>
 __global__ void __launch_bounds__((WARPS + 1) * 32, 1) hygt_stage_kernel(const StageParams P) {
+  constexpr bool BENES = (VAR & STAGE_VAR_BENES) != 0, DEBUG = (VAR & STAGE_VAR_DEBUG) != 0;
   using namespace stage_detail;
   constexpr int N = 1 << LOG2N, NW = N / 2, NC = N / 4;
   constexpr int CT = WARPS * 32;  // consumer threads
@@ -455,8 +460,9 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) hygt_stage_kernel(const S
   const int C = P.classes;
   const uint32_t T = P.tile_rows;
   const bool gathers = P.gmask != 0;
-  const bool mixed = P.bnet && (P.gmask & ~(uint64_t)P.bnet_steps);
-  const StageSmem L = stage_smem_layout(LOG2N, VPT, WARPS, C, P.cw, P.rounds, T, gathers, P.bnet != nullptr, mixed);
+  const bool bn = BENES && P.bnet != nullptr;
+  const bool mixed = bn && (P.gmask & ~(uint64_t)P.bnet_steps);
+  const StageSmem L = stage_smem_layout(LOG2N, VPT, WARPS, C, P.cw, P.rounds, T, gathers, bn, mixed);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar);
   uint64_t* computed = full + STAGES;
   uint64_t* tables = full + 2 * STAGES;
@@ -504,8 +510,8 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) hygt_stage_kernel(const S
     };
     {  // the direction's tables, once per CTA
       const uint32_t cb = (uint32_t)C * P.cw * 16u;
-      const uint32_t gb = gathers && (!P.bnet || mixed) ? (uint32_t)C * L.gstride : 0u;
-      const uint32_t nb = gathers && P.bnet ? (uint32_t)C * (P.rounds + 1) * 32u : 0u;
+      const uint32_t gb = gathers && (!bn || mixed) ? (uint32_t)C * L.gstride : 0u;
+      const uint32_t nb = gathers && bn ? (uint32_t)C * (P.rounds + 1) * 32u : 0u;
       mbar_expect_tx(tables, cb + gb + nb);
       bulk_g2s(smem + L.coef, P.coef, cb, tables);
       if (gb) bulk_g2s(smem + L.gtab, P.gtab, gb, tables);
@@ -545,7 +551,7 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) hygt_stage_kernel(const S
     const uint32_t rows_s = su32(st);
 
     // ---- transform: VPT consecutive sorted positions per thread ----
-    for (uint32_t b = warp; b * BATCH < total && !P.debug_skip; b += WARPS) {
+    for (uint32_t b = warp; b * BATCH < total && !(DEBUG && P.debug_skip); b += WARPS) {
       uint32_t en[VPT];
       const uint32_t p0 = b * BATCH + lane * VPT;
       if (P.ent) {
@@ -607,7 +613,7 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) hygt_stage_kernel(const S
       const uint32_t gbase = gtab_s + cls * L.gstride;
       const uint32_t nbase = bnet_s + (cls * (uint32_t)(P.rounds + 1) * 4u + x) * 8u;
       auto permute = [&](int step) {
-        if (P.bnet && ((P.bnet_steps >> step) & 1u)) {
+        if (BENES && bn && ((P.bnet_steps >> step) & 1u)) {
           uint2 m;
           asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(m.x), "=r"(m.y) : "r"(nbase + (uint32_t)step * 32u));
           stage_benes<LOG2N, VPT>(v, m);
