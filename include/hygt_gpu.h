@@ -142,6 +142,35 @@ int hygt_correlation_f64(int log2_n, int class_count, const float* d_x, const ui
                          uint64_t count, double* d_sum, unsigned long long* d_count, void* d_ws,
                          size_t ws_bytes, void* stream);
 
+/* ---- coordinate-descent trainer ----------------------------------------------
+ * <- hygt::optimize(const CorrelationMatrix&, int log2_n, int rounds, const OptimizerConfig&)
+ *    (include/hygt/optimizer.hpp:311-371), batched over `problems` covariances (one per class,
+ *    as `hygt train` calls it, tools/hygt_main.cpp:93-99). The whole search -- greedy_init or
+ *    random starts, coordinate-descent sweeps with the 33-point grid and golden-section line
+ *    search, the tolerance rule -- runs on the device, one CTA per (problem, restart); the KLT
+ *    gain (jacobi_eigen, statistics.hpp:141-199) is a device kernel too. Offline API: host
+ *    buffers in and out, device memory allocated per call, returns when done.
+ *    phi: [problems][N][N] fp64; seeds: per-problem OptimizerConfig::seed (NULL: cfg->seed);
+ *    angles: [problems][A] the best restart's angles (A = rounds * log2_n * N / 2);
+ *    restart_gains: [problems][restarts]; best_restart: [problems] (ties to the lowest index);
+ *    klt_gain: [problems] or NULL; trajectories: [problems][restarts][max_sweeps + 1] (NaN
+ *    padded) or NULL; trajectory_len: [problems][restarts] or NULL; variances: [problems][N]
+ *    diagonal of propagate_covariance(best model, phi) (what variance_permutation sorts) or NULL.
+ *    Errors as the reference: HYGT_ERR_ARGUMENT for restarts < 1, max_sweeps < 1, tolerance <= 0
+ *    or a covariance that is not positive semi-definite; HYGT_ERR_NUMERICAL if jacobi_eigen does
+ *    not converge. log2_n in [1, 8]. Gains match the reference to rounding. */
+typedef struct hygt_optimize_config {
+  int restarts;             /* OptimizerConfig::restarts (optimizer.hpp:37), default 4 */
+  int max_sweeps;           /* :38, default 50 */
+  double gain_tolerance_db; /* :39, default 1e-4 */
+  uint64_t seed;            /* :40 */
+  int init_mode;            /* :41 InitMode: 0 greedy_jacobi (default), 1 random, 2 zero */
+} hygt_optimize_config;
+int hygt_optimize_f64(int log2_n, int rounds, int problems, const double* phi,
+                      const hygt_optimize_config* cfg, const uint64_t* seeds, double* angles,
+                      double* restart_gains, int* best_restart, double* klt_gain,
+                      double* trajectories, int* trajectory_len, double* variances, void* stream);
+
 /* ---- dense per-class KLT (comparison path) ------------------------------------------------
  * k: host [class_count][n][n] fp64 row-major (rows = basis vectors, KLTResult::basis). */
 int hygt_klt_plan_create(int n, int class_count, const double* k, uint32_t flags,

@@ -584,3 +584,293 @@ void hygt_oracle_random_orthogonal(uint64_t seed, int n, double* q) {
   free(v);
   free(d);
 }
+
+/* ============================ optimizer (optimizer.hpp) ================================== */
+/* the coordinate-descent trainer, restated line by line so that the oracle takes
+ * the same search path as the reference (same comparisons, same libm calls, no FMA
+ * contraction at -O2 on x86-64). Matrices are n x n row-major. */
+
+/* optimizer.hpp:55-71 (conjugate_pair): A <- G A G^T, rows first, then columns. */
+static void opt_conjugate_pair(double* a, size_t dim, uint32_t m, uint32_t n, double c, double s) {
+  double* row_m = a + (size_t)m * dim;
+  double* row_n = a + (size_t)n * dim;
+  for (size_t j = 0; j < dim; ++j) {
+    const double am = row_m[j], an = row_n[j];
+    row_m[j] = c * am + s * an;
+    row_n[j] = c * an - s * am;
+  }
+  for (size_t i = 0; i < dim; ++i) {
+    const double aim = a[i * dim + m], ain = a[i * dim + n];
+    a[i * dim + m] = c * aim + s * ain;
+    a[i * dim + n] = c * ain - s * aim;
+  }
+}
+
+/* statistics.hpp:262-280 (coding_gain) over the diagonal of a (optimizer.hpp:100-105). */
+double hygt_oracle_coding_gain_db(const double* v, size_t n) {
+  double mean = 0.0;
+  for (size_t i = 0; i < n; ++i) mean += v[i];
+  mean /= (double)n;
+  if (!(mean > 0.0)) return 0.0;
+  const double floor_v = 1e-30 * mean;
+  double log_sum = 0.0;
+  for (size_t i = 0; i < n; ++i) log_sum += log10(v[i] > floor_v ? v[i] : floor_v);
+  return 10.0 * (log10(mean) - log_sum / (double)n);
+}
+
+static double opt_gain_diag(const double* a, size_t dim, double* scratch) {
+  for (size_t i = 0; i < dim; ++i) scratch[i] = a[i * dim + i];
+  return hygt_oracle_coding_gain_db(scratch, dim);
+}
+
+/* optimizer.hpp:81-96 (pair_schedule): step t = (m, n); the angle index is t itself. */
+static void opt_schedule(int log2_n, int rounds, uint32_t* sm, uint32_t* sn) {
+  const uint32_t half = 1u << (log2_n - 1);
+  size_t t = 0;
+  for (int r = 0; r < rounds; ++r)
+    for (int p = 0; p < log2_n; ++p) {
+      const uint32_t k = 1u << p;
+      for (uint32_t j = 0; j < half; ++j, ++t) {
+        sm[t] = j + (j & (0u - k));
+        sn[t] = sm[t] + k;
+      }
+    }
+}
+
+/* statistics.hpp:141-199 (jacobi_eigen): eigenvalues only (the rotation of `a` does not read
+ * the eigenvector accumulator), sorted descending with ties in index order. Returns 0, or 3
+ * (NumericalError) after 100 sweeps. */
+int hygt_oracle_jacobi_eigenvalues(const double* phi, int n, double* ev) {
+  double* a = (double*)malloc(sizeof(double) * (size_t)n * n);
+  memcpy(a, phi, sizeof(double) * (size_t)n * n);
+  double trace = 0.0;
+  for (int i = 0; i < n; ++i) trace += phi[(size_t)i * n + i];
+  const double at = fabs(trace);
+  const double thresh = 1e-12 * (at > 1e-300 ? at : 1e-300);
+  int sweep = 0;
+  for (; sweep < 100; ++sweep) {
+    double off = 0.0;
+    for (int p = 0; p < n; ++p)
+      for (int q = p + 1; q < n; ++q) off = fmax(off, fabs(a[(size_t)p * n + q]));
+    if (off < thresh) break;
+    for (int p = 0; p < n; ++p)
+      for (int q = p + 1; q < n; ++q) {
+        const double apq = a[(size_t)p * n + q];
+        if (fabs(apq) < thresh * 1e-4) continue;
+        const double tau = (a[(size_t)q * n + q] - a[(size_t)p * n + p]) / (2.0 * apq);
+        const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(tau * tau + 1.0));
+        const double c = 1.0 / sqrt(t * t + 1.0);
+        const double s = t * c;
+        const double app = a[(size_t)p * n + p], aqq = a[(size_t)q * n + q];
+        a[(size_t)p * n + p] = app - t * apq;
+        a[(size_t)q * n + q] = aqq + t * apq;
+        a[(size_t)p * n + q] = 0.0;
+        a[(size_t)q * n + p] = 0.0;
+        for (int r = 0; r < n; ++r) {
+          if (r == p || r == q) continue;
+          const double arp = a[(size_t)r * n + p], arq = a[(size_t)r * n + q];
+          a[(size_t)r * n + p] = c * arp - s * arq;
+          a[(size_t)p * n + r] = a[(size_t)r * n + p];
+          a[(size_t)r * n + q] = c * arq + s * arp;
+          a[(size_t)q * n + r] = a[(size_t)r * n + q];
+        }
+      }
+  }
+  for (int i = 0; i < n; ++i) ev[i] = a[(size_t)i * n + i];
+  free(a);
+  if (sweep == 100) return HYGT_ORACLE_NUMERICAL;
+  /* stable descending insertion sort (std::stable_sort with '>' keeps equal keys in order) */
+  for (int i = 1; i < n; ++i) {
+    const double v = ev[i];
+    int j = i - 1;
+    while (j >= 0 && v > ev[j]) {
+      ev[j + 1] = ev[j];
+      --j;
+    }
+    ev[j + 1] = v;
+  }
+  return 0;
+}
+
+/* optimizer.hpp:150-166 (greedy_init) */
+void hygt_oracle_greedy_init(const double* phi, int log2_n, int rounds, double* angles) {
+  const size_t dim = (size_t)1 << log2_n, steps = (size_t)rounds * log2_n * (dim / 2);
+  uint32_t* sm = (uint32_t*)malloc(sizeof(uint32_t) * steps);
+  uint32_t* sn = (uint32_t*)malloc(sizeof(uint32_t) * steps);
+  double* cov = (double*)malloc(sizeof(double) * dim * dim);
+  opt_schedule(log2_n, rounds, sm, sn);
+  memcpy(cov, phi, sizeof(double) * dim * dim);
+  for (size_t t = 0; t < steps; ++t) {
+    const uint32_t m = sm[t], n = sn[t];
+    /* optimizer.hpp:144-146 (jacobi_angle) */
+    const double th = 0.5 * atan2(2.0 * cov[m * dim + n], cov[m * dim + m] - cov[n * dim + n]);
+    angles[t] = th;
+    opt_conjugate_pair(cov, dim, m, n, cos(th), sin(th));
+  }
+  free(sm), free(sn), free(cov);
+}
+
+typedef struct {
+  size_t dim, steps;
+  const double* phi;
+  uint32_t *sm, *sn;
+  double *prefix, *work, *cs, *sn_, *diag;
+} opt_engine;
+
+/* optimizer.hpp:193-198 (full_gain) */
+static double opt_full_gain(opt_engine* e, const double* angles) {
+  memcpy(e->work, e->phi, sizeof(double) * e->dim * e->dim);
+  for (size_t t = 0; t < e->steps; ++t)
+    opt_conjugate_pair(e->work, e->dim, e->sm[t], e->sn[t], cos(angles[t]), sin(angles[t]));
+  return opt_gain_diag(e->work, e->dim, e->diag);
+}
+
+/* optimizer.hpp:257-266 (candidate_gain) */
+static double opt_candidate_gain(opt_engine* e, size_t t, double theta) {
+  memcpy(e->work, e->prefix, sizeof(double) * e->dim * e->dim);
+  opt_conjugate_pair(e->work, e->dim, e->sm[t], e->sn[t], cos(theta), sin(theta));
+  for (size_t u = t + 1; u < e->steps; ++u)
+    opt_conjugate_pair(e->work, e->dim, e->sm[u], e->sn[u], e->cs[u], e->sn_[u]);
+  return opt_gain_diag(e->work, e->dim, e->diag);
+}
+
+/* optimizer.hpp:268-291 (golden_section) */
+static double opt_golden(opt_engine* e, size_t t, double lo, double hi, double* gain) {
+  const double ratio = 0.6180339887498949;
+  double a = lo, b = hi;
+  double c = b - ratio * (b - a), d = a + ratio * (b - a);
+  double fc = opt_candidate_gain(e, t, c), fd = opt_candidate_gain(e, t, d);
+  for (int it = 0; it < 28; ++it) {
+    if (fc > fd) {
+      b = d, d = c, fd = fc;
+      c = b - ratio * (b - a);
+      fc = opt_candidate_gain(e, t, c);
+    } else {
+      a = c, c = d, fc = fd;
+      d = a + ratio * (b - a);
+      fd = opt_candidate_gain(e, t, d);
+    }
+  }
+  *gain = fc > fd ? fc : fd;
+  return fc > fd ? c : d;
+}
+
+/* optimizer.hpp:201-244 (sweep) */
+static double opt_sweep(opt_engine* e, double* angles) {
+  for (size_t t = 0; t < e->steps; ++t) e->cs[t] = cos(angles[t]), e->sn_[t] = sin(angles[t]);
+  memcpy(e->prefix, e->phi, sizeof(double) * e->dim * e->dim);
+  for (size_t t = 0; t < e->steps; ++t) {
+    double best_theta = angles[t];
+    double best_gain = opt_candidate_gain(e, t, best_theta);
+    const int grid = 33;
+    double grid_best_theta = 0.0, grid_best_gain = -1.0;
+    for (int g = 0; g < grid; ++g) {
+      const double theta = PI_D * (double)g / grid;
+      const double gain = opt_candidate_gain(e, t, theta);
+      if (gain > grid_best_gain) grid_best_gain = gain, grid_best_theta = theta;
+    }
+    if (grid_best_gain > best_gain) best_gain = grid_best_gain, best_theta = grid_best_theta;
+    const double delta = PI_D / grid;
+    double ref_gain;
+    const double ref_theta = opt_golden(e, t, grid_best_theta - delta, grid_best_theta + delta, &ref_gain);
+    if (ref_gain > best_gain) best_gain = ref_gain, best_theta = ref_theta;
+    if (best_theta != angles[t]) {
+      angles[t] = best_theta;
+      e->cs[t] = cos(best_theta);
+      e->sn_[t] = sin(best_theta);
+    }
+    opt_conjugate_pair(e->prefix, e->dim, e->sm[t], e->sn[t], e->cs[t], e->sn_[t]);
+  }
+  return opt_gain_diag(e->prefix, e->dim, e->diag);
+}
+
+/* optimizer.hpp:311-371 (optimize). trajectories: [restarts][max_sweeps + 1] (NaN-padded),
+ * traj_len: [restarts]. Returns 0, 1 (ArgumentError) or 3 (NumericalError from jacobi_eigen). */
+int hygt_oracle_optimize(const double* phi, int log2_n, int rounds, const hygt_oracle_opt_config* cfg,
+                         double* angles_out, double* restart_gains, int* best_restart,
+                         double* klt_gain, double* trajectories, int* traj_len) {
+  if (log2_n < 1 || log2_n > 16 || rounds < 1) return HYGT_ORACLE_ARGUMENT;
+  if (cfg->restarts < 1 || cfg->max_sweeps < 1 || !(cfg->gain_tolerance_db > 0.0))
+    return HYGT_ORACLE_ARGUMENT;
+  const size_t dim = (size_t)1 << log2_n, steps = (size_t)rounds * log2_n * (dim / 2);
+  double* ev = (double*)malloc(sizeof(double) * dim);
+  int st = hygt_oracle_jacobi_eigenvalues(phi, (int)dim, ev);
+  if (st) {
+    free(ev);
+    return st;
+  }
+  double trace = 0.0;
+  for (size_t i = 0; i < dim; ++i) trace += phi[i * dim + i];
+  const double eigen_floor = -1e-10 * fabs(trace);
+  for (size_t i = 0; i < dim; ++i)
+    if (ev[i] < eigen_floor) {
+      free(ev);
+      return HYGT_ORACLE_ARGUMENT; /* not positive semi-definite */
+    }
+  *klt_gain = hygt_oracle_coding_gain_db(ev, dim);
+  free(ev);
+
+  opt_engine e = {dim, steps, phi, NULL, NULL, NULL, NULL, NULL, NULL, NULL};
+  e.sm = (uint32_t*)malloc(sizeof(uint32_t) * steps);
+  e.sn = (uint32_t*)malloc(sizeof(uint32_t) * steps);
+  e.prefix = (double*)malloc(sizeof(double) * dim * dim);
+  e.work = (double*)malloc(sizeof(double) * dim * dim);
+  e.cs = (double*)malloc(sizeof(double) * steps);
+  e.sn_ = (double*)malloc(sizeof(double) * steps);
+  e.diag = (double*)malloc(sizeof(double) * dim);
+  opt_schedule(log2_n, rounds, e.sm, e.sn);
+  double* angles = (double*)malloc(sizeof(double) * steps);
+  double best_gain = 0.0;
+  int have_best = 0;
+  for (int r = 0; r < cfg->restarts; ++r) {
+    if (r == 0 && cfg->init_mode == 0) {
+      hygt_oracle_greedy_init(phi, log2_n, rounds, angles);
+    } else if (r == 0 && cfg->init_mode == 2) {
+      for (size_t t = 0; t < steps; ++t) angles[t] = 0.0;
+    } else { /* optimizer.hpp:294-299 (random_angles) */
+      hygt_oracle_rng g;
+      hygt_oracle_rng_seed(&g, hygt_oracle_derive_seed(cfg->seed, (uint64_t)r));
+      for (size_t t = 0; t < steps; ++t) angles[t] = hygt_oracle_rng_uniform(&g, 0.0, 2.0 * PI_D);
+    }
+    double* traj = trajectories ? trajectories + (size_t)r * (cfg->max_sweeps + 1) : NULL;
+    int len = 0;
+    double last = opt_full_gain(&e, angles);
+    if (traj) traj[len] = last;
+    ++len;
+    for (int s = 0; s < cfg->max_sweeps; ++s) {
+      const double gained = opt_sweep(&e, angles);
+      const double improvement = gained - last;
+      last = gained > last ? gained : last;
+      if (traj) traj[len] = last;
+      ++len;
+      if (improvement < cfg->gain_tolerance_db) break;
+    }
+    if (traj)
+      for (int k = len; k <= cfg->max_sweeps; ++k) traj[k] = NAN;
+    if (traj_len) traj_len[r] = len;
+    restart_gains[r] = last;
+    if (!have_best || last > best_gain) {
+      have_best = 1;
+      best_gain = last;
+      memcpy(angles_out, angles, sizeof(double) * steps);
+      *best_restart = r;
+    }
+  }
+  free(angles);
+  free(e.sm), free(e.sn), free(e.prefix), free(e.work), free(e.cs), free(e.sn_), free(e.diag);
+  return 0;
+}
+
+/* optimizer.hpp:111-124 (propagate_covariance, whole model, no permutation) -> diagonal. */
+void hygt_oracle_propagated_variances(const double* phi, int log2_n, int rounds,
+                                      const double* angles, double* var) {
+  const size_t dim = (size_t)1 << log2_n, steps = (size_t)rounds * log2_n * (dim / 2);
+  uint32_t* sm = (uint32_t*)malloc(sizeof(uint32_t) * steps);
+  uint32_t* sn = (uint32_t*)malloc(sizeof(uint32_t) * steps);
+  double* cov = (double*)malloc(sizeof(double) * dim * dim);
+  opt_schedule(log2_n, rounds, sm, sn);
+  memcpy(cov, phi, sizeof(double) * dim * dim);
+  for (size_t t = 0; t < steps; ++t) opt_conjugate_pair(cov, dim, sm[t], sn[t], cos(angles[t]), sin(angles[t]));
+  for (size_t i = 0; i < dim; ++i) var[i] = cov[i * dim + i];
+  free(sm), free(sn), free(cov);
+}

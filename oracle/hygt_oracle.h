@@ -21,6 +21,7 @@ extern "C" {
 /* Status codes: same numbering as include/hygt_gpu.h (errors.hpp:23-45 / hygt_main.cpp:275-284). */
 #define HYGT_ORACLE_OK 0
 #define HYGT_ORACLE_ARGUMENT 1
+#define HYGT_ORACLE_NUMERICAL 3
 #define HYGT_ORACLE_OVERFLOW 4
 
 /* ---- RNG: rng.hpp:26-77 ------------------------------------------------------------------ */
@@ -118,6 +119,26 @@ int hygt_oracle_klt_apply(int n, int classes, const double* k, const float* x,
 int hygt_oracle_correlation(int log2_n, int classes, const float* x, const uint16_t* cls,
                             uint64_t count, double* sum, uint64_t* counts);
 void hygt_oracle_correlation_finalize(int log2_n, const double* sum, uint64_t count, double* phi);
+
+/* ---- coordinate-descent trainer: optimizer.hpp ------------------------------ */
+typedef struct {
+  int restarts;              /* OptimizerConfig::restarts (optimizer.hpp:37) */
+  int max_sweeps;            /* :38 */
+  double gain_tolerance_db;  /* :39 */
+  uint64_t seed;             /* :40 */
+  int init_mode;             /* :41, InitMode: 0 greedy_jacobi, 1 random, 2 zero */
+} hygt_oracle_opt_config;
+double hygt_oracle_coding_gain_db(const double* v, size_t n);              /* statistics.hpp:262-282 */
+int hygt_oracle_jacobi_eigenvalues(const double* phi, int n, double* ev); /* statistics.hpp:141-199 */
+void hygt_oracle_greedy_init(const double* phi, int log2_n, int rounds, double* angles); /* :150-166 */
+/* optimize (optimizer.hpp:311-371): best angles [A], per-restart gains, best restart, KLT gain,
+ * trajectories [restarts][max_sweeps + 1] (NaN padded; may be NULL) and their lengths. */
+int hygt_oracle_optimize(const double* phi, int log2_n, int rounds, const hygt_oracle_opt_config* cfg,
+                         double* angles_out, double* restart_gains, int* best_restart,
+                         double* klt_gain, double* trajectories, int* traj_len);
+/* diagonal of propagate_covariance(model, phi) (optimizer.hpp:111-124) */
+void hygt_oracle_propagated_variances(const double* phi, int log2_n, int rounds,
+                                      const double* angles, double* var);
 
 /* ---- synthetic fixtures --------------------------------------------------- */
 /* Seeded Fisher-Yates permutation as tests/oracles.hpp:94-100. */

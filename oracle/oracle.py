@@ -77,6 +77,14 @@ def lib():
         L.hygt_oracle_random_orthogonal.argtypes = [_u64, _i, _p]
         L.hygt_oracle_memory_footprint.argtypes = [_i, _i, _i, _i]
         L.hygt_oracle_memory_footprint.restype = C.c_size_t
+        L.hygt_oracle_coding_gain_db.argtypes = [_p, C.c_size_t]
+        L.hygt_oracle_coding_gain_db.restype = _d
+        L.hygt_oracle_jacobi_eigenvalues.argtypes = [_p, _i, _p]
+        L.hygt_oracle_greedy_init.argtypes = [_p, _i, _i, _p]
+        L.hygt_oracle_greedy_init.restype = None
+        L.hygt_oracle_optimize.argtypes = [_p, _i, _i, _p, _p, _p, _p, _p, _p, _p]
+        L.hygt_oracle_propagated_variances.argtypes = [_p, _i, _i, _p, _p]
+        L.hygt_oracle_propagated_variances.restype = None
         _lib = L
     return _lib
 
@@ -105,6 +113,8 @@ def ref():
         L.ref_class_energy.argtypes = [_i, _i, _i, _p, _p, _u32, _p, _p, _u64, _p]
         L.ref_rng_stream.argtypes = [_u64, _i, _u64, _u64, _p, _p]
         L.ref_ar1_covariance_2d.argtypes = [_i, _d, _p]
+        L.ref_optimize.argtypes = [_p, _i, _i, _i, _i, _d, _u64, _i, _p, _p, _p, _p, _p, _p]
+        L.ref_variance_permutation.argtypes = [_p, _i, _i, _p, _p, _p]
         _ref = L
     return _ref
 
@@ -284,3 +294,91 @@ def ref_apply_batch(log2_n, rounds, angles, perms, perm_mask, x, cls=None, inver
     if st:
         raise ValueError(f"reference apply failed with status {st}")
     return y
+
+
+# ---------------------------------------------------------------- optimizer ----
+
+INIT_MODES = {"greedy_jacobi": 0, "random": 1, "zero": 2}
+
+
+class _OptConfig(C.Structure):
+    _fields_ = [("restarts", C.c_int), ("max_sweeps", C.c_int), ("gain_tolerance_db", C.c_double),
+                ("seed", C.c_uint64), ("init_mode", C.c_int)]
+
+
+def _opt_result(n_angles, restarts, max_sweeps):
+    return (np.zeros(n_angles, np.float64), np.zeros(restarts, np.float64), C.c_int(0), C.c_double(0.0),
+            np.full((restarts, max_sweeps + 1), np.nan), np.zeros(restarts, np.int32))
+
+
+def _opt_report(st, angles, gains, best, klt, traj, tlen):
+    if st:
+        raise ValueError(f"optimize failed with status {st}")
+    trajectories = [traj[r, :tlen[r]].tolist() for r in range(len(gains))]
+    b = int(best.value)
+    return angles, {"restart_gains_db": gains, "best_restart": b, "klt_gain_db": float(klt.value),
+                    "gain_ratio": gains[b] / klt.value if klt.value > 1e-15 else 1.0,
+                    "trajectories": trajectories}
+
+
+def coding_gain_db(v):
+    v = _c(v, np.float64)
+    return lib().hygt_oracle_coding_gain_db(_ptr(v), v.size)
+
+
+def jacobi_eigenvalues(phi):
+    phi = _c(phi, np.float64)
+    ev = np.zeros(phi.shape[0], np.float64)
+    if lib().hygt_oracle_jacobi_eigenvalues(_ptr(phi), phi.shape[0], _ptr(ev)):
+        raise ValueError("jacobi_eigen: no convergence")
+    return ev
+
+
+def greedy_init(phi, log2_n, rounds):
+    phi = _c(phi, np.float64)
+    a = np.zeros(rounds * log2_n * (1 << (log2_n - 1)), np.float64)
+    lib().hygt_oracle_greedy_init(_ptr(phi), log2_n, rounds, _ptr(a))
+    return a
+
+
+def optimize(phi, log2_n, rounds, restarts=4, max_sweeps=50, gain_tolerance_db=1e-4, seed=0,
+             init_mode="greedy_jacobi"):
+    """optimizer.hpp:311-371 restated: (best angles, report dict)."""
+    phi = _c(phi, np.float64)
+    cfg = _OptConfig(restarts, max_sweeps, gain_tolerance_db, seed, INIT_MODES[init_mode])
+    res = _opt_result(rounds * log2_n * (1 << (log2_n - 1)), max(restarts, 0), max_sweeps)
+    angles, gains, best, klt, traj, tlen = res
+    st = lib().hygt_oracle_optimize(_ptr(phi), log2_n, rounds, C.byref(cfg), _ptr(angles), _ptr(gains),
+                                    C.byref(best), C.byref(klt), _ptr(traj), _ptr(tlen))
+    return _opt_report(st, *res)
+
+
+def propagated_variances(phi, log2_n, rounds, angles):
+    phi = _c(phi, np.float64)
+    v = np.zeros(1 << log2_n, np.float64)
+    lib().hygt_oracle_propagated_variances(_ptr(phi), log2_n, rounds, _ptr(_c(angles, np.float64)), _ptr(v))
+    return v
+
+
+def ref_optimize(phi, log2_n, rounds, restarts=4, max_sweeps=50, gain_tolerance_db=1e-4, seed=0,
+                 init_mode="greedy_jacobi"):
+    """The reference's own hygt::optimize through the shim."""
+    phi = _c(phi, np.float64)
+    res = _opt_result(rounds * log2_n * (1 << (log2_n - 1)), max(restarts, 0), max_sweeps)
+    angles, gains, best, klt, traj, tlen = res
+    st = ref().ref_optimize(_ptr(phi), log2_n, rounds, restarts, max_sweeps, gain_tolerance_db, seed,
+                            INIT_MODES[init_mode], _ptr(angles), _ptr(gains), C.byref(best), C.byref(klt),
+                            _ptr(traj), _ptr(tlen))
+    return _opt_report(st, *res)
+
+
+def ref_variance_permutation(phi, log2_n, rounds, angles):
+    phi = _c(phi, np.float64)
+    n = 1 << log2_n
+    perm = np.zeros(n, np.uint16)
+    var = np.zeros(n, np.float64)
+    st = ref().ref_variance_permutation(_ptr(phi), log2_n, rounds, _ptr(_c(angles, np.float64)),
+                                        _ptr(perm), _ptr(var))
+    if st:
+        raise ValueError(f"variance_permutation failed with status {st}")
+    return perm, var

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <limits>
 #include <optional>
 #include <thread>
 #include <vector>
@@ -19,6 +20,7 @@
 #include "hygt/hypercube.hpp"
 #include "hygt/matrix.hpp"
 #include "hygt/model.hpp"
+#include "hygt/optimizer.hpp"
 #include "hygt/rng.hpp"
 #include "hygt/statistics.hpp"
 #include "hygt/transform.hpp"
@@ -320,6 +322,59 @@ int ref_ar1_covariance_2d(int block_size, double rho, double* out) {
   try {
     const auto phi = hygt::ar1_covariance_2d(block_size, rho);
     std::memcpy(out, phi.values().data().data(), phi.n() * phi.n() * sizeof(double));
+    return 0;
+  } catch (...) {
+    return status_of_current();
+  }
+}
+
+// optimizer.hpp:311-371 through the reference's own optimize(); trajectories are NaN padded
+// to max_sweeps + 1 entries per restart.
+int ref_optimize(const double* phi, int log2_n, int rounds, int restarts, int max_sweeps,
+                 double tol, std::uint64_t seed, int init_mode, double* angles, double* gains,
+                 int* best, double* klt_gain, double* traj, int* traj_len) {
+  try {
+    const std::size_t n = std::size_t{1} << log2_n;
+    hygt::Matrix m(n);
+    std::memcpy(m.data().data(), phi, n * n * sizeof(double));
+    const hygt::CorrelationMatrix cm(std::move(m), 0);
+    hygt::OptimizerConfig cfg;
+    cfg.restarts = restarts;
+    cfg.max_sweeps = max_sweeps;
+    cfg.gain_tolerance_db = tol;
+    cfg.seed = seed;
+    cfg.init_mode = static_cast<hygt::InitMode>(init_mode);
+    auto [model, rep] = hygt::optimize(cm, log2_n, rounds, cfg);
+    std::memcpy(angles, model.angles().data(), model.angles().size() * sizeof(double));
+    for (int r = 0; r < restarts; ++r) {
+      gains[r] = rep.restart_gains_db[r];
+      traj_len[r] = static_cast<int>(rep.trajectories[r].size());
+      for (int k = 0; k <= max_sweeps; ++k)
+        traj[(std::size_t)r * (max_sweeps + 1) + k] =
+            k < traj_len[r] ? rep.trajectories[r][k] : std::numeric_limits<double>::quiet_NaN();
+    }
+    *best = static_cast<int>(rep.best_restart);
+    *klt_gain = rep.klt_gain_db;
+    return 0;
+  } catch (...) {
+    return status_of_current();
+  }
+}
+
+// optimizer.hpp:378-390 (variance_permutation) and the propagated diagonal it sorts.
+int ref_variance_permutation(const double* phi, int log2_n, int rounds, const double* angles,
+                             std::uint16_t* perm, double* var) {
+  try {
+    const std::size_t n = std::size_t{1} << log2_n;
+    hygt::Matrix m(n);
+    std::memcpy(m.data().data(), phi, n * n * sizeof(double));
+    const hygt::CorrelationMatrix cm(std::move(m), 0);
+    const hygt::HyGTModel model(log2_n, rounds,
+                                std::vector<double>(angles, angles + hygt::num_parameters(log2_n, rounds)));
+    const auto prop = hygt::propagate_covariance(model, cm);
+    for (std::size_t i = 0; i < n; ++i) var[i] = prop.values()(i, i);
+    const auto sorted = hygt::variance_permutation(model, cm);
+    std::memcpy(perm, sorted.permutation()->data(), n * sizeof(std::uint16_t));
     return 0;
   } catch (...) {
     return status_of_current();

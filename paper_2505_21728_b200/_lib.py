@@ -36,6 +36,7 @@ SIGNATURES = {
     "hygt_inverse_i64": (_i, [_p, _p, _p, _p, _u64, C.POINTER(_u64), _p]),
     "hygt_correlation_workspace_bytes": (_sz, [_i, _u64]),
     "hygt_correlation_f64": (_i, [_i, _i, _p, _p, _u64, _p, _p, _p, _sz, _p]),
+    "hygt_optimize_f64": (_i, [_i, _i, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "hygt_klt_plan_create": (_i, [_i, _i, _p, _u32, C.POINTER(_p)]),
     "hygt_klt_plan_destroy": (_i, [_p]),
     "hygt_klt_workspace_bytes": (_sz, [_p, _u64]),

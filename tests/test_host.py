@@ -148,3 +148,20 @@ def test_synthetic_workloads_are_deterministic():
     assert np.all((w.rho >= 0.5) & (w.rho <= 0.95))
     q = make_workload(4).klt_bases()
     assert np.abs(q[0] @ q[0].T - np.eye(64)).max() < 1e-12
+
+
+def test_trainer_host_logic_mirrors_reference(oracle_mod):
+    """derive_seed (rng.hpp:36-38) and variance_permutation's stable descending order
+    (optimizer.hpp:378-390; test_optimizer.cpp:209-224) -- host-side, no GPU needed."""
+    from paper_2505_21728_b200 import train
+    from paper_2505_21728_b200.model import HyGTModel
+    for base, stream in [(0, 0), (1, 5), (2**63 + 7, 34)]:
+        assert train.derive_seed(base, stream) == oracle_mod.derive_seed(base, stream)
+    m = train.variance_permutation(HyGTModel.zeros(2, 1), [1.0, 5.0, 3.0, 3.0])
+    assert list(m.permutation) == [1, 2, 3, 0]
+    m = train.variance_permutation(HyGTModel.zeros(2, 1), [4.0, 3.0, 2.0, 1.0])
+    assert list(m.permutation) == [0, 1, 2, 3]
+    import pytest
+    from paper_2505_21728_b200.errors import ArgumentError
+    with pytest.raises(ArgumentError):
+        train.variance_permutation(m, [1.0, 2.0, 3.0, 4.0])

@@ -193,3 +193,65 @@ def test_correlation_oracle_matches_reference_accumulator(oracle_mod):
         for c in range(classes):
             phi = oracle_mod.correlation_finalize(log2n, sums[c], counts[c])
             assert np.array_equal(phi, phi_ref[c])  # same loop order: bit-exact
+
+
+# ---- optimizer -----------------------------------------------------------------
+
+def _opt_golden():
+    import os
+    return np.load(os.path.join(os.path.dirname(__file__), "golden", "optimize_v1.npz"))
+
+
+_OPT_FAST = ["n16r2_seed7", "n4r2_seed99", "n8r2_psd", "n4r1_random_init", "n4r2_zero_init",
+             "n8r1_diagonal", "n2r1_psd0", "n2r1_psd3"]
+
+
+@pytest.mark.parametrize("name", _OPT_FAST)
+def test_optimizer_oracle_bit_exact_against_golden(oracle_mod, name):
+    """hygt_oracle_optimize restates optimizer.hpp:177-371 line by line: same search path, same
+    libm calls, so it reproduces the reference's hygt::optimize outputs bit for bit."""
+    g = _opt_golden()
+    log2n, rounds, restarts, sweeps = (int(v) for v in g[f"{name}/shape"])
+    ang, rep = oracle_mod.optimize(g[f"{name}/phi"], log2n, rounds, restarts=restarts, max_sweeps=sweeps,
+                                   seed=int(g[f"{name}/seed"][0]), init_mode=str(g[f"{name}/init_mode"]))
+    assert np.array_equal(ang, g[f"{name}/angles"])
+    assert np.array_equal(rep["restart_gains_db"], g[f"{name}/gains"])
+    assert rep["best_restart"] == int(g[f"{name}/best"][0])
+    assert rep["klt_gain_db"] == g[f"{name}/klt"][0]
+    assert [len(t) for t in rep["trajectories"]] == g[f"{name}/traj_len"].tolist()
+    var = oracle_mod.propagated_variances(g[f"{name}/phi"], log2n, rounds, ang)
+    assert np.array_equal(var, g[f"{name}/variances"])
+
+
+def test_optimizer_oracle_acceptance_pin(oracle_mod):
+    """acceptance.cpp:66-68: N=16 R=2, 2-D AR(1) rho=0.95, restarts 4, seed 1 -> 15.164931 dB."""
+    g = _opt_golden()
+    ang, rep = oracle_mod.optimize(g["n16r2_acceptance/phi"], 4, 2, restarts=4, seed=1)
+    assert abs(rep["restart_gains_db"][rep["best_restart"]] - 15.164931) < 1e-3
+    assert np.array_equal(ang, g["n16r2_acceptance/angles"])
+
+
+def test_optimizer_oracle_matches_reference_live(oracle_mod):
+    """Fresh random covariances through both the oracle and the reference shim."""
+    if not oracle_mod.ref_available():
+        pytest.skip("reference shim not built here")
+    rng = np.random.default_rng(11)
+    for log2n, rounds, restarts in [(2, 2, 2), (3, 1, 3), (4, 1, 2)]:
+        n = 1 << log2n
+        a = rng.standard_normal((n, n))
+        phi = a @ a.T + 0.01 * np.eye(n)
+        seed = int(rng.integers(1 << 30))
+        x1, r1 = oracle_mod.optimize(phi, log2n, rounds, restarts=restarts, seed=seed)
+        x2, r2 = oracle_mod.ref_optimize(phi, log2n, rounds, restarts=restarts, seed=seed)
+        assert np.array_equal(x1, x2)
+        assert np.array_equal(r1["restart_gains_db"], r2["restart_gains_db"])
+        for t1, t2 in zip(r1["trajectories"], r2["trajectories"]):
+            assert t1 == t2
+
+
+def test_optimizer_oracle_errors(oracle_mod):
+    """optimizer.hpp:313-326: bad config and indefinite covariances are ArgumentErrors."""
+    with pytest.raises(ValueError):
+        oracle_mod.optimize(np.diag([1.0, -1.0]), 1, 1)
+    with pytest.raises(ValueError):
+        oracle_mod.optimize(np.eye(4), 2, 1, restarts=0)
