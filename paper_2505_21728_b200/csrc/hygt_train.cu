@@ -14,7 +14,7 @@
 // of W_t and D = [[c - 1, s], [-s, c - 1]]. Its diagonal is closed-form:
 //   d_i = F_ii + 2 (al_i ya_i + be_i yb_i) + al_i^2 Zaa + 2 al_i be_i Zab + be_i^2 Zbb,
 //   al_i = (c - 1) a_i - s b_i,  be_i = (c - 1) b_i + s a_i,  y = F K,  Z = K^T F K,
-// so a candidate costs O(N) (one warp), a position costs two mat-vecs, and accepting a new
+// so a candidate costs O(N) (one 16-lane group), a position costs two mat-vecs, and accepting a new
 // angle is one symmetric rank-4 update of F. Advancing t peels G_{t+1} off the tail (two rows
 // of WT). The search itself -- the current angle, the 33-point grid over [0, pi), 28
 // golden-section steps around the best grid point, strict '>' comparisons, trajectory and
@@ -33,6 +33,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdint>
 #include <random>
@@ -52,6 +53,20 @@ constexpr double GOLDEN_RATIO = 0.6180339887498949;  // optimizer.hpp:269
 constexpr double PI_D = 3.14159265358979323846;
 constexpr double LOG10_2 = 0.30102999566398119521;
 constexpr int SMEM_MAX_LOG2N = 6;
+// Candidate evaluations run in groups of G(N) lanes (about 4-8 samples per lane), NG = TT / G
+// of them in flight; the golden-section search resolves SPEC(N) iterations per round, which
+// takes 2^(SPEC+1) - 2 <= NG speculative evaluations. Work is skipped per warp, never per group:
+// groups without a point in a working warp evaluate a dummy one, so the full-mask shuffles
+// never diverge.
+template <int N>
+__host__ __device__ constexpr int group_lanes() { return N <= 16 ? 4 : 16; }
+template <int N>
+__host__ __device__ constexpr int spec_depth() {
+  int d = 1;
+  while ((4 << d) - 2 <= TT / group_lanes<N>()) ++d;
+  return d;
+}
+constexpr int KEY_SLOTS = 192;  // [0, 34) grid, [34, 36) golden start, 2 x tree banks of <= 62
 
 struct TrainParams {
   const double* phi;   // [P][N][N]
@@ -117,6 +132,52 @@ __device__ __forceinline__ double warp_coding_gain(V val, int lane) {
   return 10.0 * (log10(mean) - log_sum / N);
 }
 
+// A product of positive values as exponent + mantissa in [0.5, 1): compares exactly.
+struct Key {
+  int e;
+  double m;
+};
+// gain(a) > gain(b) <=> prod(a) < prod(b) (same trace)
+__device__ __forceinline__ bool better(Key a, Key b) { return a.e < b.e || (a.e == b.e && a.m < b.m); }
+
+// x = m * 2^e, m in [0.5, 1), for positive finite x: bit fields for normal values (the usual
+// case), frexp for subnormals.
+__device__ __forceinline__ double split_exp(double x, int& e) {
+  const long long b = __double_as_longlong(x);
+  const int f = (int)((b >> 52) & 0x7ff);
+  if (f == 0) return frexp(x, &e);
+  e = f - 1022;
+  return __longlong_as_double((b & 0x800fffffffffffffll) | 0x3fe0000000000000ll);
+}
+
+// prod_i max(val(i), floor) over N values by a G-lane group, normalised. Every lane of the group
+// returns the same key.
+template <int N, class V>
+__device__ __forceinline__ Key group_key(V val, int gl, double floor_v) {
+  constexpr int G = group_lanes<N>();
+  constexpr int K = (N + G - 1) / G;
+  double mp = 1.0;
+  int es = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int i = gl + G * k;
+    if (i < N) {
+      const double x = val(i);
+      int e;
+      mp *= split_exp(x > floor_v ? x : floor_v, e);
+      es += e;
+    }
+  }
+#pragma unroll
+  for (int o = G / 2; o; o >>= 1) {
+    mp *= __shfl_xor_sync(0xffffffffu, mp, o);
+    es += __shfl_xor_sync(0xffffffffu, es, o);
+  }
+  int e2;
+  mp = split_exp(mp, e2);
+  return Key{es + e2, mp};
+}
+
 // A <- G A G^T on rows/columns m, n (conjugate_pair, optimizer.hpp:55-71): rows first, then
 // columns, unfused products as the reference. Needs N <= TT; ends with a barrier.
 template <int N>
@@ -148,7 +209,9 @@ template <int LOG2N>
 __global__ void __launch_bounds__(TT) hygt_train_kernel(const TrainParams P) {
   constexpr int N = 1 << LOG2N, LD = N + 1, Q = TT / N < N ? TT / N : N, JL = N / Q;
   extern __shared__ __align__(16) double sm[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int G = group_lanes<N>(), NG = TT / G, SPEC = spec_depth<N>();
+  static_assert((2 << SPEC) - 2 <= NG && 36 + 2 * ((2 << SPEC) - 2) <= KEY_SLOTS, "key slots");
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gid = tid / G, glane = tid % G;
   const int prob = blockIdx.x / P.restarts, rs = blockIdx.x % P.restarts;
   const int A = P.rounds * LOG2N * (N / 2);
   double *F, *X, *v;
@@ -167,8 +230,9 @@ __global__ void __launch_bounds__(TT) hygt_train_kernel(const TrainParams P) {
   double* al = v + 3 * N;
   double* be = v + 4 * N;
   double* part = v + 5 * N;   // [2][TT] mat-vec partials
-  double* cg = part + 2 * TT;  // [GRID_POINTS + 1] grid-phase gains
-  double* misc = cg + 40;      // [0] chosen angle, [1] gain of F
+  double* km = part + 2 * TT;  // [KEY_SLOTS] candidate keys: mantissas (grid, golden start, tree)
+  int* ke = reinterpret_cast<int*>(km + KEY_SLOTS);  // [KEY_SLOTS] exponents
+  double* misc = km + KEY_SLOTS + KEY_SLOTS / 2;     // [1] gain of F
   const double* phi = P.phi + (size_t)prob * N * N;
   const size_t slot = (size_t)prob * P.restarts + rs;
   double* ang = P.angles + slot * A;
@@ -262,8 +326,8 @@ __global__ void __launch_bounds__(TT) hygt_train_kernel(const TrainParams P) {
         yb[tid] = sb;
       }
       __syncthreads();
-      // Z = K^T F K, per warp (identical in every warp)
-      double zaa = 0.0, zab = 0.0, zbb = 0.0;
+      // Z = K^T F K and the trace of F, per warp (identical in every warp)
+      double zaa = 0.0, zab = 0.0, zbb = 0.0, tr = 0.0;
 #pragma unroll
       for (int k = 0; k < (N + 31) / 32; ++k) {
         const int i = lane + 32 * k;
@@ -271,6 +335,7 @@ __global__ void __launch_bounds__(TT) hygt_train_kernel(const TrainParams P) {
           zaa = fma(a[i], ya[i], zaa);
           zab = fma(a[i], yb[i], zab);
           zbb = fma(b[i], yb[i], zbb);
+          tr += fd[i];
         }
       }
 #pragma unroll
@@ -278,65 +343,128 @@ __global__ void __launch_bounds__(TT) hygt_train_kernel(const TrainParams P) {
         zaa += __shfl_xor_sync(0xffffffffu, zaa, o);
         zab += __shfl_xor_sync(0xffffffffu, zab, o);
         zbb += __shfl_xor_sync(0xffffffffu, zbb, o);
+        tr += __shfl_xor_sync(0xffffffffu, tr, o);
       }
-      // candidate_gain(t, theta) in closed form (see the header)
-      auto cand = [&](double theta) -> double {
+      // The search compares gains of one position only. Every candidate's diagonal has the same
+      // sum (the trace), so gain_a > gain_b <=> prod_i d_i(a) < prod_i d_i(b): candidates carry
+      // the product as a normalised (exponent, mantissa) key and no logarithm is taken.
+      const double mean = tr / N;
+      const bool degenerate = !(mean > 0.0);  // coding_gain returns 0 for every candidate
+      const double floor_v = 1e-30 * mean;
+      // candidate_gain(t, theta) in closed form (see the header), one 16-lane group
+      auto cand = [&](double theta) -> Key {
         double sh, ch;
         sincos(0.5 * (theta - cur), &sh, &ch);
         const double c1 = -2.0 * sh * sh, s = 2.0 * sh * ch;
-        return warp_coding_gain<N>(
+        const Key k = group_key<N>(
             [&](int i) {
               const double ai = a[i], bi = b[i];
               const double p = c1 * ai - s * bi, r = c1 * bi + s * ai;
               return fd[i] + 2.0 * (p * ya[i] + r * yb[i]) + p * p * zaa + 2.0 * p * r * zab + r * r * zbb;
             },
-            lane);
+            glane, floor_v);
+        return degenerate ? Key{0, 0.5} : k;
       };
-      // the current angle and the 33-point grid, one warp per candidate (optimizer.hpp:205-221)
-      for (int k = warp; k <= GRID_POINTS; k += TW) {
-        const double th = k == 0 ? cur : PI_D * static_cast<double>(k - 1) / GRID_POINTS;
-        const double g = cand(th);
-        if (lane == 0) cg[k] = g;
+      // the current angle and the 33-point grid (optimizer.hpp:205-221)
+      constexpr int GPW = 32 / G;  // groups per warp; a warp works if any of its groups has a point
+      for (int k0 = 0; k0 <= GRID_POINTS; k0 += NG) {
+        const int k = k0 + gid;
+        if (k0 + warp * GPW > GRID_POINTS) continue;
+        const double th = k == 0 || k > GRID_POINTS ? cur : PI_D * static_cast<double>(k - 1) / GRID_POINTS;
+        const Key g = cand(th);
+        if (glane == 0 && k <= GRID_POINTS) {
+          ke[k] = g.e;
+          km[k] = g.m;
+        }
       }
       __syncthreads();
-      if (warp == 0) {
-        double best_theta = cur, best_gain = cg[0];
-        double grid_theta = 0.0, grid_gain = -1.0;
-        for (int g = 0; g < GRID_POINTS; ++g)
-          if (cg[g + 1] > grid_gain) {
-            grid_gain = cg[g + 1];
-            grid_theta = PI_D * static_cast<double>(g) / GRID_POINTS;
-          }
-        if (grid_gain > best_gain) {
-          best_gain = grid_gain;
-          best_theta = grid_theta;
+      // every thread resolves the search identically from shared memory
+      Key best_key{ke[0], km[0]};
+      double best_theta = cur;
+      Key grid_key{INT_MAX, 1.0};  // worse than any candidate (grid_best_gain = -1)
+      double grid_theta = 0.0;
+      for (int g = 0; g < GRID_POINTS; ++g)
+        if (better(Key{ke[g + 1], km[g + 1]}, grid_key)) {
+          grid_key = Key{ke[g + 1], km[g + 1]};
+          grid_theta = PI_D * static_cast<double>(g) / GRID_POINTS;
         }
-        // golden_section (optimizer.hpp:268-291)
-        const double delta = PI_D / GRID_POINTS;
-        double lo = grid_theta - delta, hi = grid_theta + delta;
-        double c = hi - GOLDEN_RATIO * (hi - lo), d = lo + GOLDEN_RATIO * (hi - lo);
-        double fc = cand(c), fd_ = cand(d);
-        for (int it = 0; it < GOLDEN_ITERATIONS; ++it) {
-          if (fc > fd_) {
+      if (better(grid_key, best_key)) {
+        best_key = grid_key;
+        best_theta = grid_theta;
+      }
+      // golden_section (optimizer.hpp:268-291), SPEC iterations per round: the groups evaluate
+      // every point the next SPEC iterations can reach (heap nodes 1..2^(SPEC+1) - 2; node h's
+      // children are 2h + 1 for fc > fd and 2h + 2 otherwise), then all threads replay the
+      // iterations with the reference's comparisons.
+      const double delta = PI_D / GRID_POINTS;
+      double lo = grid_theta - delta, hi = grid_theta + delta;
+      double c = hi - GOLDEN_RATIO * (hi - lo), d = lo + GOLDEN_RATIO * (hi - lo);
+      if (warp * GPW < 2) {
+        const Key g = cand(gid == 0 ? c : d);
+        if (glane == 0 && gid < 2) {
+          ke[GRID_POINTS + 1 + gid] = g.e;
+          km[GRID_POINTS + 1 + gid] = g.m;
+        }
+      }
+      __syncthreads();
+      Key fc{ke[GRID_POINTS + 1], km[GRID_POINTS + 1]}, fdk{ke[GRID_POINTS + 2], km[GRID_POINTS + 2]};
+      for (int it = 0, bank = 0; it < GOLDEN_ITERATIONS; bank ^= 1) {
+        const int depth = GOLDEN_ITERATIONS - it < SPEC ? GOLDEN_ITERATIONS - it : SPEC;
+        const int nodes = (2 << depth) - 2;
+        const int base = GRID_POINTS + 3 + bank * ((2 << SPEC) - 2);  // alternate banks: no WAR barrier
+        if (warp * GPW < nodes) {
+          int h = gid < nodes ? gid + 1 : 0, path = 0, len = 0;
+          while (h > 0) {  // branches from the root, last one in bit 0
+            path |= ((h & 1) ? 0 : 1) << len;
+            ++len;
+            h = (h - 1) >> 1;
+          }
+          double l2 = lo, h2 = hi, c2 = c, d2 = d, pt = cur;
+          for (int q = len - 1; q >= 0; --q) {
+            if (!((path >> q) & 1)) {  // fc > fd
+              h2 = d2;
+              d2 = c2;
+              c2 = h2 - GOLDEN_RATIO * (h2 - l2);
+              pt = c2;
+            } else {
+              l2 = c2;
+              c2 = d2;
+              d2 = l2 + GOLDEN_RATIO * (h2 - l2);
+              pt = d2;
+            }
+          }
+          const Key g = cand(pt);
+          if (glane == 0 && gid < nodes) {
+            ke[base + gid] = g.e;
+            km[base + gid] = g.m;
+          }
+        }
+        __syncthreads();
+        int h = 0;
+        for (int q = 0; q < depth; ++q) {
+          if (better(fc, fdk)) {
             hi = d;
             d = c;
-            fd_ = fc;
+            fdk = fc;
             c = hi - GOLDEN_RATIO * (hi - lo);
-            fc = cand(c);
+            h = 2 * h + 1;
+            fc = Key{ke[base + h - 1], km[base + h - 1]};
           } else {
             lo = c;
             c = d;
-            fc = fd_;
+            fc = fdk;
             d = lo + GOLDEN_RATIO * (hi - lo);
-            fd_ = cand(d);
+            h = 2 * h + 2;
+            fdk = Key{ke[base + h - 1], km[base + h - 1]};
           }
         }
-        const double ref_theta = fc > fd_ ? c : d, ref_gain = fc > fd_ ? fc : fd_;
-        if (ref_gain > best_gain) best_theta = ref_theta;
-        if (lane == 0) misc[0] = best_theta;
+        it += depth;
       }
-      __syncthreads();
-      const double best = misc[0];
+      {
+        const bool cwin = better(fc, fdk);
+        if (better(cwin ? fc : fdk, best_key)) best_theta = cwin ? c : d;
+      }
+      const double best = best_theta;
       if (best != cur) {  // accept: F <- R F R^T, a symmetric rank-4 update
         double sh, ch;
         sincos(0.5 * (best - cur), &sh, &ch);
@@ -527,7 +655,7 @@ void pick(int log2n, TrainFn& t, KltFn& k) {
 size_t train_smem(int log2n) {
   const size_t n = size_t{1} << log2n;
   const size_t mats = log2n <= SMEM_MAX_LOG2N ? 2 * n * (n + 1) : 0;
-  return (mats + 5 * n + 2 * TT + 40 + 8) * sizeof(double);
+  return (mats + 5 * n + 2 * TT + KEY_SLOTS + KEY_SLOTS / 2 + 8) * sizeof(double);
 }
 
 size_t klt_smem(int log2n) {
