@@ -25,6 +25,8 @@
 #include "hygt/errors.hpp"
 #include "hygt/fixedpoint.hpp"
 #include "hygt/model.hpp"
+#include "hygt/optimizer.hpp"
+#include "hygt/statistics.hpp"
 #include "hygt_gpu.h"
 
 namespace hygt::gpu {
@@ -247,6 +249,33 @@ inline ResidualDataset apply(const ModelBundle& bundle, const ResidualDataset& d
       out[r] = {cls[r], std::vector<double>(x.begin() + r * n, x.begin() + (r + 1) * n)};
   }
   return ResidualDataset(ds.log2_n(), ds.class_count(), std::move(out));
+}
+
+// hygt::optimize (optimizer.hpp:311-371) with the reference's types, searched on the GPU
+// (hygt_optimize_f64). Gains agree with the reference to rounding; a near-tie in the search may
+// pick an equivalent angle.
+inline std::pair<HyGTModel, TrainingReport> optimize(const CorrelationMatrix& phi, int log2_n, int rounds,
+                                                     const OptimizerConfig& config) {
+  if (log2_n < 1 || log2_n > kMaxLog2N) throw ArgumentError("optimize: log2_n out of range [1, 16]");
+  if (phi.n() != (std::size_t{1} << log2_n)) throw ArgumentError("optimize: dimension mismatch");
+  const hygt_optimize_config c{config.restarts, config.max_sweeps, config.gain_tolerance_db, config.seed,
+                               static_cast<int>(config.init_mode)};
+  const std::size_t r = config.restarts > 0 ? static_cast<std::size_t>(config.restarts) : 1;
+  const std::size_t s = config.max_sweeps > 0 ? static_cast<std::size_t>(config.max_sweeps) : 0;
+  std::vector<double> angles(num_parameters(log2_n, rounds)), gains(r), traj(r * (s + 1));
+  std::vector<int> tlen(r);
+  int best = 0;
+  double klt = 0.0;
+  check(hygt_optimize_f64(log2_n, rounds, 1, phi.values().data().data(), &c, nullptr, angles.data(),
+                          gains.data(), &best, &klt, traj.data(), tlen.data(), nullptr, nullptr));
+  TrainingReport rep;
+  rep.restart_gains_db = gains;
+  rep.best_restart = static_cast<std::size_t>(best);
+  for (std::size_t k = 0; k < r; ++k)
+    rep.trajectories.emplace_back(traj.begin() + k * (s + 1), traj.begin() + k * (s + 1) + tlen[k]);
+  rep.klt_gain_db = klt;
+  rep.gain_ratio = klt > 1e-15 ? gains[best] / klt : 1.0;
+  return {HyGTModel(log2_n, rounds, std::move(angles)), std::move(rep)};
 }
 
 }  // namespace hygt::gpu

@@ -94,6 +94,31 @@ int main() {
     EXPECT(ef <= 1e-5 * sc, "gpu::apply float log2n=%d max err %.3g", log2n, ef);
     EXPECT(mism == 0, "gpu::apply fixed log2n=%d: %lld mismatches (must be bit-exact)", log2n, mism);
   }
+  // --- hygt::gpu::optimize vs hygt::optimize (optimizer.hpp:311-371), acceptance case N=16 R=2
+  {
+    const hygt::CorrelationMatrix phi = hygt::ar1_covariance_2d(4, 0.95);
+    hygt::OptimizerConfig cfg;
+    cfg.restarts = 2;
+    cfg.seed = 1;
+    cfg.max_sweeps = 5;
+    const auto [mr, rr] = hygt::optimize(phi, 4, 2, cfg);
+    const auto [mg, rg] = hygt::gpu::optimize(phi, 4, 2, cfg);
+    for (std::size_t k = 0; k < rr.restart_gains_db.size(); ++k)
+      EXPECT(std::abs(rr.restart_gains_db[k] - rg.restart_gains_db[k]) < 1e-5, "gpu::optimize restart %zu gain %.9f vs %.9f", k,
+             rg.restart_gains_db[k], rr.restart_gains_db[k]);
+    EXPECT(std::abs(rr.klt_gain_db - rg.klt_gain_db) < 1e-9, "gpu::optimize klt gain");
+    EXPECT(rr.best_restart == rg.best_restart, "gpu::optimize best restart");
+    bool threw = false;
+    try {
+      hygt::Matrix bad(2);
+      bad(0, 0) = 1.0;
+      bad(1, 1) = -1.0;
+      hygt::gpu::optimize(hygt::CorrelationMatrix(std::move(bad), 0), 1, 1, hygt::OptimizerConfig{});
+    } catch (const hygt::ArgumentError&) {
+      threw = true;
+    }
+    EXPECT(threw, "gpu::optimize must throw ArgumentError on an indefinite covariance");
+  }
   std::printf("adapter_check: %s (%d failures)\n", failures ? "FAILED" : "ok", failures);
   return failures ? 1 : 0;
 }
