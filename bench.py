@@ -66,6 +66,16 @@ def measured_traffic(workload: str):
     return None, None
 
 
+# what one "launch" of each plan path is (include/hygt_gpu.h, hygt_plan_path)
+KERNEL_NAMES = {
+    "stage": "hygt_stage_kernel",
+    "jit": "hygt_jit_kernel (NVRTC)",
+    "clsjit": "hygt_cls_f / hygt_cls_i (one NVRTC kernel per class; a launch = the chain of per-class "
+              "grids of one direction, event-timed as a whole)",
+    "cls": "hygt_cls_kernel (a launch = the chain of per-class grids of one direction)",
+}
+
+
 def bytes_per_row(n: int, classes: int) -> int:
     """Algorithmic HBM bytes of one direction for one row: N fp32 in + N fp32 out + u16 class id
     (SURVEY.md §8 d2)."""
@@ -357,7 +367,7 @@ def impl_ours(args):
     traffic, traffic_src = measured_traffic(w.cfg.name) if rows == w.cfg.count else (None, None)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
-                "kernel": f"hygt_{plan.path}_kernel (mean of the forward and inverse launches)",
+                "kernel": KERNEL_NAMES.get(plan.path, f"hygt_{plan.path}_kernel") + " (mean of the forward and inverse launches)",
                 "bytes_per_launch": rows * bpr, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({hbm_kind})"}
     launches_per_step = plan.launches_per_step()
 

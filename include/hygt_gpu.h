@@ -90,7 +90,14 @@ int hygt_plan_algorithm(const hygt_plan* plan);
  *     the tile kernel instead,
  * 5 = thread-per-row kernel over global class buckets (N = 64): rows staged through shared
  *     memory by cp.async, class tables one segment at a time. Forward-with-energy calls run on
- *     the class-segment kernel instead. */
+ *     the class-segment kernel instead,
+ * 6 = one grid per class over global class buckets (N = 64, R <= 4, scale-folded form): the
+ *     class's coefficients and gather offsets are kernel parameters (constant-bank operands),
+ *     the class grids chained by programmatic dependent launch. Forward-with-energy calls run
+ *     on the class-segment kernel instead,
+ * 7 = the chain of 6 with one plan-specialised kernel per class and direction (NVRTC at plan
+ *     creation, N = 64, R <= 8): coefficients are FFMA immediates and permutations register
+ *     renames, so the class's rows touch shared memory only on their way in and out. */
 int hygt_plan_path(const hygt_plan* plan);
 
 /* Device workspace for class bucketing of `count` rows. */

@@ -108,6 +108,12 @@ struct hygt_plan {
   // seg2 path (N = 64): thread-per-row over global class buckets, element-ordered tables
   bool seg2 = false;
   size_t seg2_smem[2] = {0, 0};
+  // cls path (N = 64): one launch per class, class tables as kernel parameters (hygt_cls.cuh)
+  bool cls = false;
+  std::vector<unsigned char> cls_blk[2];  // [C] parameter blocks per direction
+  unsigned cls_grid = 0;
+  int cls_vpt = 2;  // rows per thread
+  JitClsKernels cls_jit;  // the same chain with per-class NVRTC kernels (coefficients immediate)
   // JIT path (N <= 64): NVRTC-specialised kernels, coefficients as immediates
   JitKernels jit;
   // segment path (N >= 64): same interleaved tables, one class staged per CTA segment
@@ -153,6 +159,7 @@ void free_plan(hygt_plan* p) {
   cudaFree(p->d_fixed_err);
   cudaFree(p->d_fx_ws);
   jit_release(p->jit);
+  jit_cls_release(p->cls_jit);
   delete p->fixed_mu;
   delete p;
 }
@@ -588,18 +595,21 @@ unsigned long long* g_stage_trace = nullptr;  // debug hook, see hygt_debug_stag
 // standard: N/4 units of c_i then N/4 units of s'_i with s'_m = s, s'_n = -s), then N/4 units of
 // final scales (scale-folded only). Gathers: [C][R+1][N] u16 scratch offsets src * 128.
 // Element-ordered tables of both directions into p->d_scoef / p->d_sgtab (stage and seg2 paths).
-int build_elem_tables(hygt_plan* p, const double* angles, const uint16_t* perms, uint32_t* cw_out) {
+// Host copies of one direction's element tables: coef [C][cw] float4, gt [C][gs] u16 with
+// gs = stage_gstride / 2 (gather offsets src * 128 per step).
+int elem_tables_host(hygt_plan* p, const double* angles, const uint16_t* perms, int d,
+                     std::vector<float4>& coef, std::vector<uint16_t>& gt, uint32_t* cw_out) {
   const int n = 1 << p->log2n, nc = n / 4, C = p->classes, R = p->rounds;
   const bool standard = p->algo == 0;
   const uint32_t step_units = (uint32_t)nc * (standard ? 2 : 1);
   const uint32_t cw = (uint32_t)R * p->log2n * step_units + (standard ? 0u : (uint32_t)nc);
-  for (int d = 0; d < 2; ++d) {
+  {
     std::vector<ClassProgram> progs;
     if (!build_programs(p->log2n, R, C, angles, perms, p->perm_mask, d == 0, standard, progs))
       return fail(HYGT_ERR_NUMERICAL, "hygt: element table build failed");
-    std::vector<float4> coef((size_t)C * cw, make_float4(0.f, 0.f, 0.f, 0.f));
+    coef.assign((size_t)C * cw, make_float4(0.f, 0.f, 0.f, 0.f));
     const uint32_t gs = stage_gstride(p->log2n, R) / 2;  // u16 per class
-    std::vector<uint16_t> gt((size_t)C * gs, 0);
+    gt.assign((size_t)C * gs, 0);
     std::vector<float> kc(n), ks(n);
     for (int c = 0; c < C; ++c) {
       float4* cc = &coef[(size_t)c * cw];
@@ -639,11 +649,20 @@ int build_elem_tables(hygt_plan* p, const double* angles, const uint16_t* perms,
         for (size_t i = 0; i < g[k].size(); ++i)
           gt[(size_t)c * gs + (size_t)k * n + i] = (uint16_t)(g[k][i] * 128);
     }
+  }
+  *cw_out = cw;
+  return HYGT_OK;
+}
+
+int build_elem_tables(hygt_plan* p, const double* angles, const uint16_t* perms, uint32_t* cw_out) {
+  for (int d = 0; d < 2; ++d) {
+    std::vector<float4> coef;
+    std::vector<uint16_t> gt;
+    if (int s = elem_tables_host(p, angles, perms, d, coef, gt, cw_out)) return s;
     int s = upload(&p->d_scoef[d], coef.data(), coef.size());
     if (!s && p->gmask[d]) s = upload(&p->d_sgtab[d], gt.data(), gt.size());
     if (s) return s;
   }
-  *cw_out = cw;
   return HYGT_OK;
 }
 
@@ -872,6 +891,65 @@ int setup_seg2(hygt_plan* p, const double* angles, const uint16_t* perms) {
   return HYGT_OK;
 }
 
+// ---- cls path (hygt_cls.cuh) ----------------------------------------------------------------
+int setup_cls(hygt_plan* p, const double* angles, const uint16_t* perms) {
+  if (p->algo == 1 && jit_cls_supported(p->log2n, p->classes, p->rounds) && env_int("HYGT_CLS_JIT", 1) != 0) {
+    std::string err;
+    if (jit_cls_build(p->log2n, p->rounds, p->classes, angles, perms, p->perm_mask, false, p->cls_jit, err)) {
+      jit_cls_release(p->cls_jit);  // stay on the precompiled kernels
+      if (env_int("HYGT_JIT_REQUIRED", 0)) return fail(HYGT_ERR_CUDA, err);
+    } else {
+      p->cls = true;
+      p->chunk_rows = 0;  // global class buckets
+      return HYGT_OK;
+    }
+  }
+  const size_t bytes = cls_param_bytes(p->log2n, p->rounds);
+  if (!bytes || p->algo != 1 || p->classes < 2 || env_int("HYGT_CLS", 1) == 0) return HYGT_OK;
+  const int C = p->classes;
+  const uint32_t gs = stage_gstride(p->log2n, p->rounds) / 2;
+  for (int d = 0; d < 2; ++d) {
+    std::vector<float4> coef;
+    std::vector<uint16_t> gt;
+    uint32_t cw = 0;
+    if (int s = elem_tables_host(p, angles, perms, d, coef, gt, &cw)) return s;
+    p->cls_blk[d].assign((size_t)C * bytes, 0);
+    for (int c = 0; c < C; ++c)
+      cls_fill(p->log2n, p->rounds, p->cls_blk[d].data() + (size_t)c * bytes, &coef[(size_t)c * cw], cw,
+               &gt[(size_t)c * gs], (uint32_t)p->gmask[d]);
+  }
+  p->cls_vpt = env_int("HYGT_CLS_VPT", 1) == 2 ? 2 : 1;
+  for (int d = 0; d < 2; ++d)
+    smem_attr(cls_kernel(p->log2n, p->rounds, d == 0, p->cls_vpt), cls_smem_bytes(p->log2n, p->cls_vpt));
+  cudaGetLastError();
+  int occ = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cls_kernel(p->log2n, p->rounds, true, p->cls_vpt), 32,
+                                                   cls_smem_bytes(p->log2n, p->cls_vpt)));
+  if (occ < 1) return HYGT_OK;
+  // grids of a fraction of the SMs' warp slots: each warp takes several batches (its next
+  // batch's rows prefetched), and the PDL chain keeps grids of several classes in flight
+  const int div = std::max(1, env_int("HYGT_CLS_GRID_DIV", 1));
+  p->cls_grid = (unsigned)std::max(1, p->num_sms * occ / div);
+  p->cls = true;
+  p->chunk_rows = 0;  // global class buckets
+  return HYGT_OK;
+}
+
+int run_cls(const hygt_plan* p, int dir, const float* x, float* y, const WsLayout& w, char* ws,
+            cudaStream_t st) {
+  if (p->cls_jit.ok) {
+    if (jit_cls_launch(p->cls_jit, dir, x, y, reinterpret_cast<const uint32_t*>(ws + w.idx),
+                       reinterpret_cast<const uint32_t*>(ws + w.seg), p->classes, st))
+      return fail(HYGT_ERR_CUDA, std::string("hygt: class launch failed: ") + cudaGetErrorString(cudaGetLastError()));
+    return ok();
+  }
+  const cudaError_t e = cls_launch_chain(p->log2n, p->rounds, dir == 0, p->cls_blk[dir].data(), p->classes, x, y,
+                                         reinterpret_cast<const uint32_t*>(ws + w.idx),
+                                         reinterpret_cast<const uint32_t*>(ws + w.seg), p->cls_grid, p->cls_vpt, st);
+  if (e != cudaSuccess) return fail(HYGT_ERR_CUDA, std::string("hygt: class launch failed: ") + cudaGetErrorString(e));
+  return ok();
+}
+
 int run_seg2(const hygt_plan* p, int dir, const float* x, float* y, uint64_t count,
              const WsLayout& w, char* ws, cudaStream_t st) {
   Seg2Fn fn = select_seg2(p->log2n, p->algo == 0, dir == 0);
@@ -966,6 +1044,14 @@ int run_apply(const hygt_plan* p, int dir, const float* x, float* y, const uint1
                     d_cls ? reinterpret_cast<uint32_t*>(static_cast<char*>(d_ws) + w.err) : nullptr, st);
   }
   const bool bucketed = d_cls && p->classes > 1;
+  if (p->cls && bucketed && !energy) {
+    if (!d_ws || ws_bytes < w.total) return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
+    if (!(flags & HYGT_REUSE_BUCKETS)) {
+      const int s = run_bucket(p, p->classes, 0, d_cls, count, d_ws, ws_bytes, st);
+      if (s) return s;
+    }
+    return run_cls(p, dir, x, y, w, static_cast<char*>(d_ws), st);
+  }
   if (p->seg2 && bucketed && !energy) {
     if (!d_ws || ws_bytes < w.total) return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
     if (!(flags & HYGT_REUSE_BUCKETS)) {
@@ -1126,6 +1212,10 @@ extern "C" int hygt_plan_create(int log2_n, int rounds, int class_count, const d
     free_plan(p);
     return s;
   }
+  if (int s = setup_cls(p, angles, perms)) {
+    free_plan(p);
+    return s;
+  }
   *out = p;
   return ok();
 }
@@ -1144,7 +1234,7 @@ extern "C" int hygt_plan_destroy(hygt_plan* plan) {
 extern "C" int hygt_plan_algorithm(const hygt_plan* plan) { return plan ? plan->algo : -1; }
 
 extern "C" int hygt_plan_path(const hygt_plan* plan) {
-  return plan ? (plan->jit.ok ? 3 : plan->stage ? 4 : plan->tile ? 1 : plan->seg2 ? 5 : plan->seg ? 2 : 0) : -1;
+  return plan ? (plan->jit.ok ? 3 : plan->stage ? 4 : plan->tile ? 1 : plan->cls_jit.ok ? 7 : plan->cls ? 6 : plan->seg2 ? 5 : plan->seg ? 2 : 0) : -1;
 }
 
 extern "C" size_t hygt_workspace_bytes(const hygt_plan* plan, uint64_t count) {

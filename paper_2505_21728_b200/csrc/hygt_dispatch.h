@@ -31,4 +31,13 @@ constexpr int STAGE_FX_VPT = 2;
 constexpr int STAGE_FX_WARPS = 7;
 StageFxFn select_stage_fixed(int log2n, bool fwd);
 Seg2Fn select_seg2(int log2n, bool standard, bool fwd);
+// per-class launch kernel (hygt_cls.cuh, hygt_dispatch_cls.cu)
+size_t cls_param_bytes(int log2n, int rounds);  // 0: unsupported shape
+uint32_t cls_smem_bytes(int log2n, int vpt);
+const void* cls_kernel(int log2n, int rounds, bool fwd, int vpt);
+void cls_fill(int log2n, int rounds, void* blk, const float4* coef, uint32_t cw, const uint16_t* gt,
+              uint32_t gmask);
+cudaError_t cls_launch_chain(int log2n, int rounds, bool fwd, const unsigned char* blks, int classes,
+                             const float* x, float* y, const uint32_t* idx, const uint32_t* seg_end,
+                             unsigned grid, int vpt, cudaStream_t st);
 }  // namespace hygt_gpu

@@ -19,6 +19,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
+#include <atomic>
 #include <mutex>
 #include <sstream>
 #include <thread>
@@ -140,6 +142,46 @@ const char* kEpilogue = R"CUDA(
 }
 )CUDA";
 
+// Straight-line body of one class in SSA form: every butterfly defines two new values, gathers
+// only rename (the generator tracks which value holds logical sample i), so the front end sees
+// scalar code with no arrays to promote. Reads and finally rewrites v[0..n).
+void emit_body(std::ostringstream& o, const ClassProgram& pr, int n, bool standard) {
+  std::vector<std::string> cur(n);
+  for (int i = 0; i < n; ++i) cur[i] = "v[" + std::to_string(i) + "]";
+  int k = 0;
+  auto fresh = [&]() { return "t" + std::to_string(k++); };
+  for (const ProgOp& op : pr.ops) {
+    if (op.kind == 0) {
+      const std::string a = cur[op.m], b = cur[op.n], ym = fresh(), yn = fresh();
+      if (!standard)  // a' = a + t1 b ; b' = b - t2 a   (op.b = -t2)
+        o << "const float " << ym << "=fmaf(" << b << "," << lit(op.a) << "," << a << ");const float "
+          << yn << "=fmaf(" << a << "," << lit(op.b) << "," << b << ");\n";
+      else  // y_m = c a + s b ; y_n = c b - s a   (givens.hpp:44-47)
+        o << "const float " << ym << "=fmaf(" << a << "," << lit(op.a) << "," << b << "*" << lit(op.b)
+          << ");const float " << yn << "=fmaf(" << b << "," << lit(op.a) << ",-(" << a << "*"
+          << lit(op.b) << "));\n";
+      cur[op.m] = ym;
+      cur[op.n] = yn;
+    } else if (op.kind == 1) {
+      const auto& g = pr.gathers[op.arg];
+      std::vector<std::string> nxt(n);
+      for (int i = 0; i < n; ++i) nxt[i] = cur[g[i]];
+      cur.swap(nxt);
+    } else {
+      for (int i = 0; i < n; ++i) {
+        const std::string t = fresh();
+        o << "const float " << t << "=" << cur[i] << "*" << lit(pr.scales[i]) << ";";
+        cur[i] = t;
+      }
+      o << "\n";
+    }
+  }
+  // all samples were rewritten by the first pass, so these assignments never read an
+  // already-overwritten input
+  for (int i = 0; i < n; ++i) o << "v[" << i << "]=" << cur[i] << ";";
+  o << "\n";
+}
+
 std::string generate(int log2n, int classes, int warps, int minb, bool standard,
                      const std::vector<ClassProgram>& progs) {
   const int n = 1 << log2n;
@@ -149,48 +191,100 @@ std::string generate(int log2n, int classes, int warps, int minb, bool standard,
   o << "#define N " << n << "\n#define NQ " << n / 4 << "\n#define WARPS " << warps
     << "\n#define MINB " << minb << "\n#define SWZ " << kSwizzle[log2n - 2] << "\n";
   o << kPrologue;
-  // Each class body is emitted in SSA form: every butterfly defines two new values, gathers only
-  // rename (the generator tracks which value holds logical sample i), so the front end sees
-  // straight-line scalar code with no arrays to promote.
   for (int c = 0; c < classes; ++c) {
     o << "      case " << c << ": {\n";
-    const ClassProgram& pr = progs[c];
-    std::vector<std::string> cur(n);
-    for (int i = 0; i < n; ++i) cur[i] = "v[" + std::to_string(i) + "]";
-    int k = 0;
-    auto fresh = [&]() { return "t" + std::to_string(k++); };
-    for (const ProgOp& op : pr.ops) {
-      if (op.kind == 0) {
-        const std::string a = cur[op.m], b = cur[op.n], ym = fresh(), yn = fresh();
-        if (!standard)  // a' = a + t1 b ; b' = b - t2 a   (op.b = -t2)
-          o << "const float " << ym << "=fmaf(" << b << "," << lit(op.a) << "," << a << ");const float "
-            << yn << "=fmaf(" << a << "," << lit(op.b) << "," << b << ");\n";
-        else  // y_m = c a + s b ; y_n = c b - s a   (givens.hpp:44-47)
-          o << "const float " << ym << "=fmaf(" << a << "," << lit(op.a) << "," << b << "*" << lit(op.b)
-            << ");const float " << yn << "=fmaf(" << b << "," << lit(op.a) << ",-(" << a << "*"
-            << lit(op.b) << "));\n";
-        cur[op.m] = ym;
-        cur[op.n] = yn;
-      } else if (op.kind == 1) {
-        const auto& g = pr.gathers[op.arg];
-        std::vector<std::string> nxt(n);
-        for (int i = 0; i < n; ++i) nxt[i] = cur[g[i]];
-        cur.swap(nxt);
-      } else {
-        for (int i = 0; i < n; ++i) {
-          const std::string t = fresh();
-          o << "const float " << t << "=" << cur[i] << "*" << lit(pr.scales[i]) << ";";
-          cur[i] = t;
-        }
-        o << "\n";
-      }
-    }
-    // all samples were rewritten by the first pass, so these assignments never read an
-    // already-overwritten input
-    for (int i = 0; i < n; ++i) o << "v[" << i << "]=" << cur[i] << ";";
-    o << "\n      } break;\n";
+    emit_body(o, progs[c], n, standard);
+    o << "      } break;\n";
   }
   o << kEpilogue;
+  return o.str();
+}
+
+// ---- per-class kernels (plan path "clsjit") -------------------------------------------------
+// One kernel per class and direction, launched over that class's bucketed run (the launch chain
+// of hygt_cls.cuh): the class body above between a cp.async row stage-in and a coalesced
+// stage-out through a per-warp slot area. One warp per CTA, one row per lane.
+const char* kClsPrologue = R"CUDA(
+typedef unsigned int u32;
+typedef unsigned long long u64;
+#define RS (NQ + 1)
+extern "C" __global__ void __launch_bounds__(32, MINB)
+KNAME(const float* __restrict__ x, float* __restrict__ y, const u32* __restrict__ idx,
+      const u32* __restrict__ seg_end, u32 bin, u32 copy_bin) {
+  __shared__ __align__(16) float4 slot[32 * RS];
+  __shared__ u32 s_row[32];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int lane = threadIdx.x;
+  const u64 beg = bin ? __ldg(seg_end + bin - 1) : 0u;
+  const u64 end = __ldg(seg_end + bin);
+  const u64 nb = (end - beg + 31) / 32;
+  auto row_id = [&](u64 b) -> u32 {
+    const u64 p = beg + b * 32 + lane;
+    return b < nb && p < end ? __ldg(idx + p) : 0xffffffffu;
+  };
+  const u32 slot_s = (u32)__cvta_generic_to_shared(slot);
+  u32 id_next = row_id(blockIdx.x);
+  for (u64 b = blockIdx.x; b < nb; b += gridDim.x) {
+    __syncwarp();
+    s_row[lane] = id_next;
+    id_next = row_id(b + gridDim.x);
+    __syncwarp();
+#pragma unroll
+    for (int i0 = 0; i0 < 32; i0 += 32 / NQ) {
+      const int i = i0 + lane / NQ, q = lane % NQ;
+      const u32 row = s_row[i];
+      if (row != 0xffffffffu)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(slot_s + (u32)(i * RS + q) * 16u),
+                     "l"(x + (size_t)row * N + q * 4) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+    float v[N];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const float4 a = slot[lane * RS + q];
+      v[4 * q] = a.x; v[4 * q + 1] = a.y; v[4 * q + 2] = a.z; v[4 * q + 3] = a.w;
+    }
+    if (id_next != 0xffffffffu)  // the next batch's rows: in L2 by the time this one is done
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(x + (size_t)id_next * N), "n"(N * 4) : "memory");
+    {
+)CUDA";
+
+const char* kClsEpilogue = R"CUDA(
+    }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) slot[lane * RS + q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    __syncwarp();
+#pragma unroll
+    for (int i0 = 0; i0 < 32; i0 += 32 / NQ) {
+      const int i = i0 + lane / NQ, q = lane % NQ;
+      const u32 row = s_row[i];
+      if (row != 0xffffffffu) __stcs((float4*)(y + (size_t)row * N) + q, slot[i * RS + q]);
+    }
+  }
+  if (copy_bin) {  // rows with invalid class ids pass through (hygt_bucket flags them)
+    const u64 e2 = __ldg(seg_end + bin + 1);
+    for (u64 p = end + (u64)blockIdx.x * (32 / NQ) + lane / NQ; p < e2; p += (u64)gridDim.x * (32 / NQ)) {
+      const u32 row = __ldg(idx + p);
+      ((float4*)(y + (size_t)row * N))[lane % NQ] = ((const float4*)(x + (size_t)row * N))[lane % NQ];
+    }
+  }
+  // complete only after the previous class grid: the last grid's completion implies the chain's
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+#undef KNAME
+)CUDA";
+
+// Source of one class's two kernels (hygt_cls_f, hygt_cls_i).
+std::string generate_class(int log2n, int minb, bool standard, const ClassProgram& fwd, const ClassProgram& inv) {
+  const int n = 1 << log2n;
+  std::ostringstream o;
+  o << "#define N " << n << "\n#define NQ " << n / 4 << "\n#define MINB " << minb << "\n";
+  for (int d = 0; d < 2; ++d) {
+    o << "#define KNAME " << (d == 0 ? "hygt_cls_f" : "hygt_cls_i") << "\n" << kClsPrologue;
+    emit_body(o, d == 0 ? fwd : inv, n, standard);
+    o << kClsEpilogue;
+  }
   return o.str();
 }
 
@@ -351,6 +445,85 @@ int jit_launch(const JitKernels& k, int dir, const float* x, float* y, const uin
   void* args[] = {(void*)&x, (void*)&y, (void*)&idx, (void*)&seg_end, (void*)&nseg, (void*)&count,
                   (void*)&classes, (void*)&span};
   return cudaLaunchKernel((const void*)k.fn[dir], dim3((unsigned)grid), dim3(k.warps * 32), args, k.smem, st) == cudaSuccess ? 0 : 5;
+}
+
+bool jit_cls_supported(int log2n, int classes, int rounds) {
+  return log2n == 6 && classes >= 2 && rounds >= 1 && rounds <= 8;
+}
+
+int jit_cls_build(int log2n, int rounds, int classes, const double* angles, const uint16_t* perms,
+                  uint32_t mask, bool standard, JitClsKernels& out, std::string& err) {
+  std::vector<ClassProgram> progs[2];
+  for (int d = 0; d < 2; ++d)
+    if (!build_programs(log2n, rounds, classes, angles, perms, mask, d == 0, standard, progs[d])) {
+      err = "jit: scale-folded program unsafe";
+      return 3;
+    }
+  const int minb = 16;
+  // one NVRTC program per class, compiled on all host threads
+  std::vector<std::vector<char>> cubins(classes);
+  std::vector<std::string> logs(classes);
+  std::vector<int> status(classes, 0);
+  std::atomic<int> next{0};
+  auto worker = [&]() {
+    for (int c; (c = next.fetch_add(1)) < classes;)
+      if (compile(generate_class(log2n, minb, standard, progs[0][c], progs[1][c]), cubins[c], logs[c])) status[c] = 5;
+  };
+  const int nt = std::max(1, std::min<int>(classes, (int)std::thread::hardware_concurrency()));
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nt; ++t) pool.emplace_back(worker);
+  worker();
+  for (auto& t : pool) t.join();
+  out.lib.assign(classes, nullptr);
+  out.fn[0].assign(classes, nullptr);
+  out.fn[1].assign(classes, nullptr);
+  for (int c = 0; c < classes; ++c) {
+    if (status[c]) {
+      err = "jit: NVRTC compilation failed: " + logs[c].substr(0, 2000);
+      return 5;
+    }
+    if (cudaLibraryLoadData(&out.lib[c], cubins[c].data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess ||
+        cudaLibraryGetKernel(&out.fn[0][c], out.lib[c], "hygt_cls_f") != cudaSuccess ||
+        cudaLibraryGetKernel(&out.fn[1][c], out.lib[c], "hygt_cls_i") != cudaSuccess) {
+      err = "jit: cannot load the compiled module";
+      return 5;
+    }
+  }
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)out.fn[0][0], 32, 0) != cudaSuccess || occ < 1)
+    occ = 1;
+  cudaGetLastError();
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  out.grid = (unsigned)(sms * occ);
+  out.ok = true;
+  return 0;
+}
+
+void jit_cls_release(JitClsKernels& k) {
+  for (cudaLibrary_t l : k.lib)
+    if (l) cudaLibraryUnload(l);
+  k = JitClsKernels{};
+}
+
+int jit_cls_launch(const JitClsKernels& k, int dir, const float* x, float* y, const uint32_t* idx,
+                   const uint32_t* seg_end, int classes, cudaStream_t st) {
+  for (int c = 0; c < classes; ++c) {
+    uint32_t bin = (uint32_t)c, copy_bin = c == classes - 1 ? 1u : 0u;
+    void* args[] = {(void*)&x, (void*)&y, (void*)&idx, (void*)&seg_end, (void*)&bin, (void*)&copy_bin};
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(k.grid);
+    cfg.blockDim = dim3(32);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = c > 0 ? 1 : 0;  // the first grid follows the bucketing normally
+    if (cudaLaunchKernelExC(&cfg, (const void*)k.fn[dir][c], args) != cudaSuccess) return 5;
+  }
+  return 0;
 }
 
 }  // namespace hygt_gpu

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "hygt_plan.h"
 
@@ -33,5 +34,20 @@ int jit_compile_only(int log2n, int rounds, int classes, const double* angles,
 int jit_launch(const JitKernels& k, int dir, const float* x, float* y, const uint32_t* idx,
                const uint32_t* seg_end, uint32_t nseg, uint64_t count, int classes, int num_sms,
                cudaStream_t st);
+
+// Per-class kernels for N = 64 (plan path "clsjit"): one NVRTC module per class holding its
+// forward and inverse kernels, launched as one programmatic chain over the class buckets.
+struct JitClsKernels {
+  bool ok = false;
+  std::vector<cudaLibrary_t> lib;
+  std::vector<cudaKernel_t> fn[2];
+  unsigned grid = 0;
+};
+bool jit_cls_supported(int log2n, int classes, int rounds);
+int jit_cls_build(int log2n, int rounds, int classes, const double* angles, const uint16_t* perms,
+                  uint32_t mask, bool standard, JitClsKernels& out, std::string& err);
+void jit_cls_release(JitClsKernels& k);
+int jit_cls_launch(const JitClsKernels& k, int dir, const float* x, float* y, const uint32_t* idx,
+                   const uint32_t* seg_end, int classes, cudaStream_t st);
 
 }  // namespace hygt_gpu

@@ -125,12 +125,16 @@ class HyGTPlan:
     @property
     def path(self) -> str:
         """Kernel family serving this plan (include/hygt_gpu.h, hygt_plan_path)."""
-        return {0: "bucketed", 1: "tile", 2: "segment", 3: "jit", 4: "stage", 5: "seg2"}[_lib.lib().hygt_plan_path(self._h)]
+        return {0: "bucketed", 1: "tile", 2: "segment", 3: "jit", 4: "stage", 5: "seg2", 6: "cls", 7: "clsjit"}[_lib.lib().hygt_plan_path(self._h)]
 
     def launches_per_step(self) -> int:
         """Kernels launched by bucket + forward + inverse on this plan (the stage path sorts each
-        tile once in hygt_bucket; the tile path sorts inside its kernel)."""
-        return {"tile": 2, "stage": 3}.get(self.path, 5)
+        tile once in hygt_bucket; the tile path sorts inside its kernel; the cls paths launch one
+        grid per class and direction after the three bucketing kernels)."""
+        path = self.path
+        if path in ("cls", "clsjit"):
+            return 3 + 2 * self.classes
+        return {"tile": 2, "stage": 3}.get(path, 5)
 
     def workspace_bytes(self, count: int) -> int:
         return _lib.lib().hygt_workspace_bytes(self._h, count)

@@ -64,13 +64,15 @@ SEG2_LOG2N = (6,)
 
 
 def _variants(log2n):
-    out = [{"HYGT_JIT": "0", "HYGT_STAGE": "0", "HYGT_TILE": "0", "HYGT_SEGMENT": "0",
-            "HYGT_LANES_LOG2": str(l)} for l in LAYOUTS[log2n]]
+    out = [{"HYGT_JIT": "0", "HYGT_STAGE": "0", "HYGT_TILE": "0", "HYGT_SEGMENT": "0", "HYGT_SEG2": "0",
+            "HYGT_CLS": "0", "HYGT_CLS_JIT": "0", "HYGT_LANES_LOG2": str(l)} for l in LAYOUTS[log2n]]
     for v in SEG_VARIANTS.get(log2n, []):
-        out.append({"HYGT_SEG2": "0", "HYGT_SEGMENT": "1", "HYGT_SEG_VARIANT": str(v)})
-    if log2n in SEG2_LOG2N:  # thread-per-row kernel over global class buckets
-        out.append({"HYGT_SEG2": "1"})
-        out.append({"HYGT_SEG2": "1", "HYGT_SEG2_TMA": "1"})
+        out.append({"HYGT_SEG2": "0", "HYGT_CLS": "0", "HYGT_CLS_JIT": "0", "HYGT_SEGMENT": "1", "HYGT_SEG_VARIANT": str(v)})
+    if log2n in SEG2_LOG2N:  # thread-per-row kernels over global class buckets
+        out.append({"HYGT_SEG2": "1", "HYGT_CLS": "0", "HYGT_CLS_JIT": "0"})
+        out.append({"HYGT_SEG2": "1", "HYGT_CLS": "0", "HYGT_CLS_JIT": "0", "HYGT_SEG2_TMA": "1"})
+        out.append({"HYGT_CLS": "1", "HYGT_CLS_JIT": "0"})  # per-class launches, parameter tables
+        out.append({"HYGT_CLS_JIT": "1"})  # per-class launches, NVRTC-specialised kernels
     for l, v in TILE_LAYOUTS.get(log2n, []):
         out.append({"HYGT_JIT": "0", "HYGT_STAGE": "0", "HYGT_TILE": "1", "HYGT_TILE_L": str(l),
                     "HYGT_TILE_VPT": str(v)})
@@ -417,33 +419,39 @@ def test_stage_path_edges(cuda, oracle_mod, standard, monkeypatch):
     assert torch.equal(y[1234], x[1234])
 
 
-@pytest.mark.parametrize("standard", [False, True])
-def test_seg2_path_edges(cuda, oracle_mod, standard):
-    """Thread-per-row bucketed kernel (plan path 'seg2', N = 64): partial batches, a class with a
-    single row, in place, invalid ids passed through and reported."""
+@pytest.mark.parametrize("standard,cls_env,jit_env,path,R", [
+    (False, "1", "1", "clsjit", 4), (False, "1", "1", "clsjit", 5), (False, "1", "0", "cls", 4),
+    (False, "1", "0", "cls", 2), (False, "0", "0", "seg2", 4), (True, "1", "1", "seg2", 4),
+    (False, "1", "0", "seg2", 5)])
+def test_seg2_path_edges(cuda, oracle_mod, standard, cls_env, jit_env, path, R, monkeypatch):
+    """Thread-per-row bucketed kernels (plan paths 'cls' and 'seg2', N = 64): partial batches, a
+    class with a single row, in place, invalid ids passed through and reported."""
     from paper_2505_21728_b200 import ArgumentError, HyGTModel
     from oracle import oracle as O
+    monkeypatch.setenv("HYGT_CLS", cls_env)
+    monkeypatch.setenv("HYGT_CLS_JIT", jit_env)
     rng = np.random.default_rng(33)
-    C, R, n = 6, 4, 64
+    C, n = 6, 64
     angles = rng.uniform(-np.pi, np.pi, (C, R * 6 * 32))
     perms = np.stack([np.stack([rng.permutation(n) for _ in range(R)]) for _ in range(C)]).astype(np.uint16)
     models = [HyGTModel(6, R, angles[c], perms[c, R - 1]) for c in range(C)]
     plan = _plan(models, perms[:, : R - 1].copy(), standard)
-    assert plan.path == "seg2"
+    assert plan.path == path
     for count in [1, 5, 63, 64, 65, 1000, 70001]:
         xh = (rng.standard_normal((count, n)) * 16).astype(np.float32)
         ch = rng.integers(0, C, count).astype(np.uint16)
         if count > 10:
             ch[ch == 5] = 4
+            ch[ch == 3] = 2  # an empty class
             ch[7] = 5  # one class with a single row
         ref = O.apply_batch(6, R, angles, perms, (1 << R) - 1, xh, ch)
         xd = torch.from_numpy(xh).to(cuda)
         cd = torch.from_numpy(ch).to(cuda)
         y = plan.forward(xd, cd)
         plan.sync_status()
-        check_close(y.cpu().numpy(), ref, xh, f"seg2 fwd count={count}")
+        check_close(y.cpu().numpy(), ref, xh, f"{path} fwd count={count}")
         back = plan.inverse(y, cd)
-        check_close(back.cpu().numpy(), xh, xh, f"seg2 roundtrip count={count}")
+        check_close(back.cpu().numpy(), xh, xh, f"{path} roundtrip count={count}")
         xi = xd.clone()
         plan.forward(xi, cd, out=xi)  # in place
         assert torch.equal(xi, y)
