@@ -29,6 +29,41 @@ __global__ void __launch_bounds__(32) k_ldcu(const __grid_constant__ Blk p, floa
   out[blockIdx.x * 32 + threadIdx.x] = s;
 }
 
+// the same with a warp-varying table offset (LDC R, c[0x0][R + imm]: per-thread registers)
+template <int REUSE>
+__global__ void __launch_bounds__(32) k_ldc(const __grid_constant__ Blk p, float* out, int iters) {
+  float v[64];
+#pragma unroll
+  for (int i = 0; i < 64; ++i) v[i] = threadIdx.x + i;
+#ifdef LDC_THREAD
+  const int w = (int)(threadIdx.x >> 5) * (NK / 2);  // 0, but not provably warp-uniform: LDC
+#else
+  const int w = (int)(blockIdx.x & 1) * (NK / 2);  // warp-uniform: LDCU c[0x0][UR + imm]
+#endif
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int j = 0; j < NK / 2 / REUSE; ++j) {
+#pragma unroll
+      for (int r = 0; r < REUSE; ++r) {
+        const int a = (j * REUSE + r) & 63, b = (a + 17 + j) & 63;
+        v[a] = fmaf(p.k[w + j], v[b], v[a]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NK / 2 / REUSE; ++j) {
+#pragma unroll
+      for (int r = 0; r < REUSE; ++r) {
+        const int a = (j * REUSE + r) & 63, b = (a + 23 + j) & 63;
+        v[a] = fmaf(p.k[w + j], v[b], v[a]);
+      }
+    }
+  }
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < 64; ++i) s += v[i];
+  out[blockIdx.x * 32 + threadIdx.x] = s;
+}
+
 __global__ void __launch_bounds__(32) k_reg(float* out, int iters, float c0) {
   float v[64];
 #pragma unroll
@@ -84,6 +119,10 @@ int main() {
     timeit(nm, [&] { k_ldcu<2><<<grid, 32>>>(h, out, iters); }, (double)grid * iters * NK);
     snprintf(nm, sizeof nm, "ldcu reuse=4 warps/SM=%d", warps);
     timeit(nm, [&] { k_ldcu<4><<<grid, 32>>>(h, out, iters); }, (double)grid * iters * NK);
+    snprintf(nm, sizeof nm, "ldc-idx reuse=1 warps/SM=%d", warps);
+    timeit(nm, [&] { k_ldc<1><<<grid, 32>>>(h, out, iters); }, (double)grid * iters * NK);
+    snprintf(nm, sizeof nm, "ldc-idx reuse=2 warps/SM=%d", warps);
+    timeit(nm, [&] { k_ldc<2><<<grid, 32>>>(h, out, iters); }, (double)grid * iters * NK);
   }
   printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
