@@ -893,7 +893,8 @@ int setup_seg2(hygt_plan* p, const double* angles, const uint16_t* perms) {
 
 // ---- cls path (hygt_cls.cuh) ----------------------------------------------------------------
 int setup_cls(hygt_plan* p, const double* angles, const uint16_t* perms) {
-  if (p->algo == 1 && jit_cls_supported(p->log2n, p->classes, p->rounds) && env_int("HYGT_CLS_JIT", 1) != 0) {
+  if (p->algo == 1 && !p->jit.ok && jit_cls_supported(p->log2n, p->classes, p->rounds) &&
+      env_int("HYGT_CLS_JIT", 1) != 0) {
     std::string err;
     if (jit_cls_build(p->log2n, p->rounds, p->classes, angles, perms, p->perm_mask, false, p->cls_jit, err)) {
       jit_cls_release(p->cls_jit);  // stay on the precompiled kernels
@@ -1038,19 +1039,19 @@ int run_apply(const hygt_plan* p, int dir, const float* x, float* y, const uint1
     return ok();
   }
   if (stage_usable(p, x, y, energy)) return run_stage(p, dir, x, y, d_cls, count, d_ws, ws_bytes, flags, st);
-  if (p->tile) {
-    if (d_cls && (!d_ws || ws_bytes < 256)) return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
-    return run_tile(p, dir, x, y, d_cls, count, energy,
-                    d_cls ? reinterpret_cast<uint32_t*>(static_cast<char*>(d_ws) + w.err) : nullptr, st);
-  }
   const bool bucketed = d_cls && p->classes > 1;
-  if (p->cls && bucketed && !energy) {
+  if (p->cls && bucketed && !energy) {  // per-class launch chain (N = 32 / 64)
     if (!d_ws || ws_bytes < w.total) return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
     if (!(flags & HYGT_REUSE_BUCKETS)) {
       const int s = run_bucket(p, p->classes, 0, d_cls, count, d_ws, ws_bytes, st);
       if (s) return s;
     }
     return run_cls(p, dir, x, y, w, static_cast<char*>(d_ws), st);
+  }
+  if (p->tile) {
+    if (d_cls && (!d_ws || ws_bytes < 256)) return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
+    return run_tile(p, dir, x, y, d_cls, count, energy,
+                    d_cls ? reinterpret_cast<uint32_t*>(static_cast<char*>(d_ws) + w.err) : nullptr, st);
   }
   if (p->seg2 && bucketed && !energy) {
     if (!d_ws || ws_bytes < w.total) return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
@@ -1234,13 +1235,13 @@ extern "C" int hygt_plan_destroy(hygt_plan* plan) {
 extern "C" int hygt_plan_algorithm(const hygt_plan* plan) { return plan ? plan->algo : -1; }
 
 extern "C" int hygt_plan_path(const hygt_plan* plan) {
-  return plan ? (plan->jit.ok ? 3 : plan->stage ? 4 : plan->tile ? 1 : plan->cls_jit.ok ? 7 : plan->cls ? 6 : plan->seg2 ? 5 : plan->seg ? 2 : 0) : -1;
+  return plan ? (plan->jit.ok ? 3 : plan->stage ? 4 : plan->cls_jit.ok ? 7 : plan->cls ? 6 : plan->tile ? 1 : plan->seg2 ? 5 : plan->seg ? 2 : 0) : -1;
 }
 
 extern "C" size_t hygt_workspace_bytes(const hygt_plan* plan, uint64_t count) {
   if (!plan) return 0;
   if (plan->stage && !plan->jit.ok) return std::max<size_t>(stage_ws_bytes(plan, count), 256);
-  if (plan->tile && !plan->jit.ok) return 256;
+  if (plan->tile && !plan->jit.ok && !plan->cls) return 256;
   return ws_layout(plan->classes, plan->chunk_rows, count).total;
 }
 
@@ -1249,7 +1250,7 @@ extern "C" int hygt_bucket(const hygt_plan* plan, const uint16_t* d_cls, uint64_
   if (!plan) return fail(HYGT_ERR_ARGUMENT, "hygt_bucket: null plan");
   if (plan->stage && !plan->jit.ok)  // per-tile class sort of the staged kernel
     return plan->classes > 1 ? run_stage_sort(plan, d_cls, count, d_ws, ws_bytes, as_stream(stream)) : ok();
-  if (plan->tile && !plan->jit.ok) return ok();  // tile plans sort each tile in shared memory
+  if (plan->tile && !plan->jit.ok && !plan->cls) return ok();  // tile plans sort each tile in shared memory
   return run_bucket(plan, plan->classes, plan->chunk_rows, d_cls, count, d_ws, ws_bytes,
                     as_stream(stream));
 }

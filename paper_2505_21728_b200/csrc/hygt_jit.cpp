@@ -447,8 +447,16 @@ int jit_launch(const JitKernels& k, int dir, const float* x, float* y, const uin
   return cudaLaunchKernel((const void*)k.fn[dir], dim3((unsigned)grid), dim3(k.warps * 32), args, k.smem, st) == cudaSuccess ? 0 : 5;
 }
 
+bool env_on(const char* name) {
+  const char* v = std::getenv(name);
+  return v && std::atoi(v) != 0;
+}
+
 bool jit_cls_supported(int log2n, int classes, int rounds) {
-  return log2n == 6 && classes >= 2 && rounds >= 1 && rounds <= 8;
+  // N = 16 rows (64 B) are half a 128 B line: gathered per class they cost twice the staged
+  // kernel's time (profiles/r01/cls_experiments.log), so N = 16 is opt-in (experiments only).
+  return log2n >= 4 && log2n <= 6 && classes >= 2 && rounds >= 1 && rounds <= 8 &&
+         (log2n >= 5 || env_on("HYGT_CLS_JIT_SHORT"));
 }
 
 int jit_cls_build(int log2n, int rounds, int classes, const double* angles, const uint16_t* perms,

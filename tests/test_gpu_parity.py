@@ -74,8 +74,10 @@ def _variants(log2n):
         out.append({"HYGT_CLS": "1", "HYGT_CLS_JIT": "0"})  # per-class launches, parameter tables
         out.append({"HYGT_CLS_JIT": "1"})  # per-class launches, NVRTC-specialised kernels
     for l, v in TILE_LAYOUTS.get(log2n, []):
-        out.append({"HYGT_JIT": "0", "HYGT_STAGE": "0", "HYGT_TILE": "1", "HYGT_TILE_L": str(l),
-                    "HYGT_TILE_VPT": str(v)})
+        out.append({"HYGT_JIT": "0", "HYGT_STAGE": "0", "HYGT_TILE": "1", "HYGT_CLS_JIT": "0",
+                    "HYGT_TILE_L": str(l), "HYGT_TILE_VPT": str(v)})
+    if log2n == 5:  # per-class NVRTC chain (multi-class plans the all-class JIT does not take)
+        out.append({"HYGT_JIT": "0", "HYGT_CLS_JIT": "1"})
     if log2n in STAGE_LOG2N:  # TMA-staged tile kernel
         out.append({"HYGT_JIT": "0", "HYGT_STAGE": "1"})
         out.append({"HYGT_JIT": "0", "HYGT_STAGE": "1", "HYGT_STAGE_ROWS": "136"})
@@ -419,11 +421,11 @@ def test_stage_path_edges(cuda, oracle_mod, standard, monkeypatch):
     assert torch.equal(y[1234], x[1234])
 
 
-@pytest.mark.parametrize("standard,cls_env,jit_env,path,R", [
-    (False, "1", "1", "clsjit", 4), (False, "1", "1", "clsjit", 5), (False, "1", "0", "cls", 4),
-    (False, "1", "0", "cls", 2), (False, "0", "0", "seg2", 4), (True, "1", "1", "seg2", 4),
-    (False, "1", "0", "seg2", 5)])
-def test_seg2_path_edges(cuda, oracle_mod, standard, cls_env, jit_env, path, R, monkeypatch):
+@pytest.mark.parametrize("standard,cls_env,jit_env,path,R,log2n", [
+    (False, "1", "1", "clsjit", 4, 6), (False, "1", "1", "clsjit", 5, 6), (False, "1", "0", "cls", 4, 6),
+    (False, "1", "0", "cls", 2, 6), (False, "0", "0", "seg2", 4, 6), (True, "1", "1", "seg2", 4, 6),
+    (False, "1", "0", "seg2", 5, 6), (False, "1", "1", "clsjit", 3, 5)])
+def test_seg2_path_edges(cuda, oracle_mod, standard, cls_env, jit_env, path, R, log2n, monkeypatch):
     """Thread-per-row bucketed kernels (plan paths 'cls' and 'seg2', N = 64): partial batches, a
     class with a single row, in place, invalid ids passed through and reported."""
     from paper_2505_21728_b200 import ArgumentError, HyGTModel
@@ -431,10 +433,10 @@ def test_seg2_path_edges(cuda, oracle_mod, standard, cls_env, jit_env, path, R, 
     monkeypatch.setenv("HYGT_CLS", cls_env)
     monkeypatch.setenv("HYGT_CLS_JIT", jit_env)
     rng = np.random.default_rng(33)
-    C, n = 6, 64
-    angles = rng.uniform(-np.pi, np.pi, (C, R * 6 * 32))
+    C, n = 6, 1 << log2n
+    angles = rng.uniform(-np.pi, np.pi, (C, R * log2n * n // 2))
     perms = np.stack([np.stack([rng.permutation(n) for _ in range(R)]) for _ in range(C)]).astype(np.uint16)
-    models = [HyGTModel(6, R, angles[c], perms[c, R - 1]) for c in range(C)]
+    models = [HyGTModel(log2n, R, angles[c], perms[c, R - 1]) for c in range(C)]
     plan = _plan(models, perms[:, : R - 1].copy(), standard)
     assert plan.path == path
     for count in [1, 5, 63, 64, 65, 1000, 70001]:
@@ -444,7 +446,7 @@ def test_seg2_path_edges(cuda, oracle_mod, standard, cls_env, jit_env, path, R, 
             ch[ch == 5] = 4
             ch[ch == 3] = 2  # an empty class
             ch[7] = 5  # one class with a single row
-        ref = O.apply_batch(6, R, angles, perms, (1 << R) - 1, xh, ch)
+        ref = O.apply_batch(log2n, R, angles, perms, (1 << R) - 1, xh, ch)
         xd = torch.from_numpy(xh).to(cuda)
         cd = torch.from_numpy(ch).to(cuda)
         y = plan.forward(xd, cd)
