@@ -122,6 +122,10 @@ struct hygt_plan {
   size_t seg_smem[2] = {0, 0};
   size_t seg_energy_smem = 0;
   unsigned long long* d_fixed_err = nullptr;
+  // fixed point, per-class NVRTC chain (hygt_jit.cpp): kernels and a plan-owned bucket workspace
+  JitClsKernels fx_jit;
+  void* d_fx_bws = nullptr;
+  size_t fx_bws_bytes = 0;
   std::mutex* fixed_mu = nullptr;
 };
 
@@ -160,6 +164,8 @@ void free_plan(hygt_plan* p) {
   cudaFree(p->d_fx_ws);
   jit_release(p->jit);
   jit_cls_release(p->cls_jit);
+  jit_cls_release(p->fx_jit);
+  cudaFree(p->d_fx_bws);
   delete p->fixed_mu;
   delete p;
 }
@@ -1530,6 +1536,43 @@ int run_fixed_staged(const hygt_plan* p, int dir, const int64_t* x, int64_t* y, 
   return fail(HYGT_ERR_ARGUMENT, "fixed transform: input magnitude exceeds 2^20");
 }
 
+// Per-class NVRTC chain for fixed plans (hygt_jit.cpp). Same contract as run_fixed_staged:
+// a status, or -1 when the bucketing met invalid class ids. Called with the plan mutex held.
+int run_fixed_jit(const hygt_plan* p, int dir, const int64_t* x, int64_t* y, const uint16_t* cls,
+                  uint64_t count, uint64_t* first_bad, cudaStream_t st) {
+  hygt_plan* mp = const_cast<hygt_plan*>(p);  // the bucket workspace is plan-owned, guarded by fixed_mu
+  const bool bucketed = cls && p->classes > 1;
+  const uint32_t* idx = nullptr;
+  const uint32_t* seg = nullptr;
+  if (cls) {
+    const WsLayout w = ws_layout(p->classes, 0, count);
+    if (mp->fx_bws_bytes < w.total) {
+      cudaFree(mp->d_fx_bws);
+      mp->d_fx_bws = nullptr;
+      mp->fx_bws_bytes = 0;
+      CU(cudaMalloc(&mp->d_fx_bws, w.total));
+      mp->fx_bws_bytes = w.total;
+    }
+    CU(cudaMemsetAsync(mp->d_fx_bws, 0, 4, st));
+    if (int s = run_bucket(p, p->classes, 0, cls, count, mp->d_fx_bws, mp->fx_bws_bytes, st)) return s;
+    if (bucketed) {
+      idx = reinterpret_cast<const uint32_t*>(static_cast<char*>(mp->d_fx_bws) + w.idx);
+      seg = reinterpret_cast<const uint32_t*>(static_cast<char*>(mp->d_fx_bws) + w.seg);
+    }
+  }
+  if (jit_fixed_launch(p->fx_jit, dir, x, y, idx, seg, p->classes, count, p->d_fixed_err, st))
+    return fail(HYGT_ERR_CUDA, std::string("hygt: fixed class launch failed: ") + cudaGetErrorString(cudaGetLastError()));
+  unsigned long long key = 0;
+  uint32_t bad_ids = 0;
+  CU(cudaMemcpyAsync(&key, p->d_fixed_err, sizeof(key), cudaMemcpyDeviceToHost, st));
+  if (cls) CU(cudaMemcpyAsync(&bad_ids, mp->d_fx_bws, sizeof(bad_ids), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (bad_ids) return -1;
+  if (key == ~0ull) return ok();
+  if (first_bad) *first_bad = key >> 3;
+  return fail(HYGT_ERR_ARGUMENT, "fixed transform: input magnitude exceeds 2^20");
+}
+
 int run_fixed(const hygt_plan* p, int dir, const int64_t* x, int64_t* y, const uint16_t* cls,
               uint64_t count, uint64_t* first_bad, cudaStream_t st) {
   if (!p || p->kind != 1) return fail(HYGT_ERR_ARGUMENT, "hygt: not a fixed-point plan");
@@ -1542,7 +1585,12 @@ int run_fixed(const hygt_plan* p, int dir, const int64_t* x, int64_t* y, const u
   FixedParams P{x, y, cls, count, p->classes, p->log2n, p->rounds, p->angle_bits,
                 p->precision_bits, p->d_codes, p->d_cos, p->d_sin, p->d_fgather[dir],
                 p->gmask[dir], p->d_fixed_err};
-  if (p->stagefx && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
+  const bool aligned16 = (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0;
+  if (p->fx_jit.ok && aligned16) {
+    const int s = run_fixed_jit(p, dir, x, y, cls, count, first_bad, st);
+    if (s != -1) return s;  // -1: invalid class ids -> the exact first failing row from below
+    CU(cudaMemcpyAsync(p->d_fixed_err, &init, sizeof(init), cudaMemcpyHostToDevice, st));
+  } else if (p->stagefx && aligned16) {
     const int s = run_fixed_staged(p, dir, x, y, cls, count, first_bad, st);
     if (s != -1) return s;  // -1: invalid class ids -> the exact first failing row from below
     CU(cudaMemcpyAsync(p->d_fixed_err, &init, sizeof(init), cudaMemcpyHostToDevice, st));
@@ -1730,6 +1778,12 @@ extern "C" int hygt_fixed_plan_create(int log2_n, int rounds, int class_count, i
   if (s) {
     free_plan(p);
     return s;
+  }
+  if (!s && jit_fixed_supported(log2_n, rounds) && env_int("HYGT_FIXED_JIT", 1) != 0) {
+    std::string err;
+    if (jit_fixed_build(log2_n, rounds, class_count, angle_bits, precision_bits, codes, ct.data(), sn.data(),
+                        perms, p->perm_mask, p->fx_jit, err))
+      jit_cls_release(p->fx_jit);  // stay on the precompiled kernels
   }
   *out = p;
   return ok();

@@ -288,6 +288,154 @@ std::string generate_class(int log2n, int minb, bool standard, const ClassProgra
   return o.str();
 }
 
+// ---- per-class fixed-point kernels (fixed plans, N = 16 / 32 / 64) -------------------------
+// Same chain and row movement as above with int64 rows: y_m = (c a + s b + 2^(p-1)) >> p,
+// y_n = (c b - s a + 2^(p-1)) >> p (fixedpoint.hpp:170-176) with c, s as IMAD.WIDE immediates
+// (the TrigTable lookups and the inverse's code negation done here on the host), permutations
+// as register renames. Values are int32 in registers: |input| <= 2^20 is checked per row
+// (fixedpoint.hpp:145-150) and keeps every rounded butterfly below 2^29 (the bound proved at
+// fixed_row_kernel, hygt_capi.cu), so the 2^46 overflow test cannot fire. A row with an
+// out-of-range input is written back unchanged (as int32) and reported through *err as
+// (row << 3 | 1); the host turns the minimum into the first failing row.
+const char* kFxPrologue = R"CUDA(
+typedef unsigned int u32;
+typedef unsigned long long u64;
+typedef long long i64;
+#define RS (NQ + 1)
+#define FXS_(v) #v
+#define FXS(v) FXS_(v)
+// d = (a c + b s + 2^(p-1)) >> p, low word (|d| < 2^29): two IMAD.WIDE with immediates + a funnel shift
+#define FX(d, a, c, b, s)                                                                          \
+  asm("{.reg .s64 t;.reg .u32 l,h;mad.wide.s32 t,%1," #c "," FXS(RND) ";mad.wide.s32 t,%2," #s   \
+      ",t;mov.b64 {l,h},t;shf.r.clamp.b32 %0,l,h," FXS(PREC) ";}"                                  \
+      : "=r"(d) : "r"(a), "r"(b))
+extern "C" __global__ void __launch_bounds__(32, MINB)
+KNAME(const i64* __restrict__ x, i64* __restrict__ y, const u32* __restrict__ idx,
+      const u32* __restrict__ seg_end, u32 bin, u64 count, u64* err) {
+  __shared__ __align__(16) longlong2 slot[32 * RS];
+  __shared__ u32 s_row[32];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int lane = threadIdx.x;
+  const u64 beg = idx ? (bin ? __ldg(seg_end + bin - 1) : 0u) : 0u;
+  const u64 end = idx ? __ldg(seg_end + bin) : count;
+  const u64 nb = (end - beg + 31) / 32;
+  auto row_id = [&](u64 b) -> u32 {
+    const u64 p = beg + b * 32 + lane;
+    return b < nb && p < end ? (idx ? __ldg(idx + p) : (u32)p) : 0xffffffffu;
+  };
+  const u32 slot_s = (u32)__cvta_generic_to_shared(slot);
+  u32 id_next = row_id(blockIdx.x);
+  for (u64 b = blockIdx.x; b < nb; b += gridDim.x) {
+    __syncwarp();
+    s_row[lane] = id_next;
+    id_next = row_id(b + gridDim.x);
+    __syncwarp();
+#pragma unroll
+    for (int i0 = 0; i0 < 32; i0 += (32 / NQ > 0 ? 32 / NQ : 1)) {
+#pragma unroll
+      for (int qq = 0; qq < (NQ > 32 ? NQ / 32 : 1); ++qq) {
+        const int i = i0 + (NQ >= 32 ? 0 : lane / NQ), q = NQ >= 32 ? lane + 32 * qq : lane % NQ;
+        const u32 row = s_row[i];
+        if (row != 0xffffffffu)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(slot_s + (u32)(i * RS + q) * 16u),
+                       "l"(x + (size_t)row * N + q * 2) : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+    int v[N];
+    bool bad = false;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const longlong2 a = slot[lane * RS + q];
+      bad |= a.x > (1 << 20) || a.x < -(1 << 20) || a.y > (1 << 20) || a.y < -(1 << 20);
+      v[2 * q] = (int)a.x; v[2 * q + 1] = (int)a.y;
+    }
+    if (id_next != 0xffffffffu)  // the next batch's rows: in L2 by the time this one is done
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(x + (size_t)id_next * N), "n"(N * 8) : "memory");
+    if (!bad) {
+)CUDA";
+
+const char* kFxEpilogue = R"CUDA(
+    }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) slot[lane * RS + q] = make_longlong2(v[2 * q], v[2 * q + 1]);
+    if (bad && s_row[lane] != 0xffffffffu) atomicMin(err, ((u64)s_row[lane] << 3) | 1u);
+    __syncwarp();
+#pragma unroll
+    for (int i0 = 0; i0 < 32; i0 += (32 / NQ > 0 ? 32 / NQ : 1)) {
+#pragma unroll
+      for (int qq = 0; qq < (NQ > 32 ? NQ / 32 : 1); ++qq) {
+        const int i = i0 + (NQ >= 32 ? 0 : lane / NQ), q = NQ >= 32 ? lane + 32 * qq : lane % NQ;
+        const u32 row = s_row[i];
+        if (row != 0xffffffffu) __stcs((longlong2*)(y + (size_t)row * N) + q, slot[i * RS + q]);
+      }
+    }
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+#undef KNAME
+)CUDA";
+
+struct FxOp {
+  uint8_t kind;  // 0 butterfly, 1 gather
+  uint16_t m, n;
+  int32_t c, s;
+  uint32_t arg;
+};
+
+// Execution-order program of one class and direction, as fixed_row_kernel runs it.
+std::vector<FxOp> fixed_program(int log2n, int rounds, const uint16_t* codes_c, const int32_t* ct,
+                                const int32_t* sn, uint32_t code_mask, const std::vector<std::vector<int>>& g,
+                                bool fwd) {
+  const int half = 1 << (log2n - 1);
+  std::vector<FxOp> ops;
+  auto gather = [&](int k) {
+    if (!g[k].empty()) ops.push_back(FxOp{1, 0, 0, 0, 0, (uint32_t)k});
+  };
+  gather(0);
+  for (int k = 0; k < rounds; ++k) {
+    const int r = fwd ? k : rounds - 1 - k;
+    for (int pp = 0; pp < log2n; ++pp) {
+      const int d = fwd ? pp : log2n - 1 - pp;
+      const uint32_t kk = 1u << d;
+      const size_t base = ((size_t)r * log2n + d) * half;  // model.hpp:77-79
+      for (int j = 0; j < half; ++j) {
+        const uint32_t m = j + (j & (0u - kk)), n = m + kk;  // hypercube.hpp:73-74
+        uint32_t code = codes_c[base + j];
+        if (!fwd) code = (0u - code) & code_mask;  // fixedpoint.hpp:170
+        ops.push_back(FxOp{0, (uint16_t)m, (uint16_t)n, ct[code], sn[code], 0});
+      }
+    }
+    gather(k + 1);
+  }
+  return ops;
+}
+
+void emit_fixed_body(std::ostringstream& o, const std::vector<FxOp>& ops, const std::vector<std::vector<int>>& g,
+                     int n) {
+  std::vector<std::string> cur(n);
+  for (int i = 0; i < n; ++i) cur[i] = "v[" + std::to_string(i) + "]";
+  int k = 0;
+  for (const FxOp& op : ops) {
+    if (op.kind == 0) {
+      const std::string a = cur[op.m], b = cur[op.n];
+      const std::string ym = "t" + std::to_string(k++), yn = "t" + std::to_string(k++);
+      o << "int " << ym << "," << yn << ";FX(" << ym << "," << a << "," << op.c << "," << b << "," << op.s
+        << ");FX(" << yn << "," << b << "," << op.c << "," << a << "," << -(int64_t)op.s << ");\n";
+      cur[op.m] = ym;
+      cur[op.n] = yn;
+    } else {
+      const auto& gg = g[op.arg];
+      std::vector<std::string> nxt(n);
+      for (int i = 0; i < n; ++i) nxt[i] = cur[gg[i]];
+      cur.swap(nxt);
+    }
+  }
+  for (int i = 0; i < n; ++i) o << "v[" << i << "]=" << cur[i] << ";";
+  o << "\n";
+}
+
 std::mutex g_cache_mu;
 std::unordered_map<std::string, std::vector<char>> g_cubin_cache;  // source -> cubin
 
@@ -447,35 +595,17 @@ int jit_launch(const JitKernels& k, int dir, const float* x, float* y, const uin
   return cudaLaunchKernel((const void*)k.fn[dir], dim3((unsigned)grid), dim3(k.warps * 32), args, k.smem, st) == cudaSuccess ? 0 : 5;
 }
 
-bool env_on(const char* name) {
-  const char* v = std::getenv(name);
-  return v && std::atoi(v) != 0;
-}
-
-bool jit_cls_supported(int log2n, int classes, int rounds) {
-  // N = 16 rows (64 B) are half a 128 B line: gathered per class they cost twice the staged
-  // kernel's time (profiles/r01/cls_experiments.log), so N = 16 is opt-in (experiments only).
-  return log2n >= 4 && log2n <= 6 && classes >= 2 && rounds >= 1 && rounds <= 8 &&
-         (log2n >= 5 || env_on("HYGT_CLS_JIT_SHORT"));
-}
-
-int jit_cls_build(int log2n, int rounds, int classes, const double* angles, const uint16_t* perms,
-                  uint32_t mask, bool standard, JitClsKernels& out, std::string& err) {
-  std::vector<ClassProgram> progs[2];
-  for (int d = 0; d < 2; ++d)
-    if (!build_programs(log2n, rounds, classes, angles, perms, mask, d == 0, standard, progs[d])) {
-      err = "jit: scale-folded program unsafe";
-      return 3;
-    }
-  const int minb = 16;
-  // one NVRTC program per class, compiled on all host threads
+// Compiles one NVRTC program per class (kernels hygt_cls_f / hygt_cls_i) on all host threads
+// and loads them; out.grid = one warp-CTA per resident slot on every SM.
+int load_class_modules(const std::vector<std::string>& srcs, JitClsKernels& out, std::string& err) {
+  const int classes = (int)srcs.size();
   std::vector<std::vector<char>> cubins(classes);
   std::vector<std::string> logs(classes);
   std::vector<int> status(classes, 0);
   std::atomic<int> next{0};
   auto worker = [&]() {
     for (int c; (c = next.fetch_add(1)) < classes;)
-      if (compile(generate_class(log2n, minb, standard, progs[0][c], progs[1][c]), cubins[c], logs[c])) status[c] = 5;
+      if (compile(srcs[c], cubins[c], logs[c])) status[c] = 5;
   };
   const int nt = std::max(1, std::min<int>(classes, (int)std::thread::hardware_concurrency()));
   std::vector<std::thread> pool;
@@ -509,6 +639,36 @@ int jit_cls_build(int log2n, int rounds, int classes, const double* angles, cons
   return 0;
 }
 
+bool env_on(const char* name) {
+  const char* v = std::getenv(name);
+  return v && std::atoi(v) != 0;
+}
+
+bool env_off(const char* name) {
+  const char* v = std::getenv(name);
+  return v && std::atoi(v) == 0;
+}
+
+bool jit_cls_supported(int log2n, int classes, int rounds) {
+  // N = 16 rows (64 B) are half a 128 B line: gathered per class they cost twice the staged
+  // kernel's time (profiles/r01/cls_experiments.log), so N = 16 is opt-in (experiments only).
+  return log2n >= 4 && log2n <= 6 && classes >= 2 && rounds >= 1 && rounds <= 8 &&
+         (log2n >= 5 || env_on("HYGT_CLS_JIT_SHORT"));
+}
+
+int jit_cls_build(int log2n, int rounds, int classes, const double* angles, const uint16_t* perms,
+                  uint32_t mask, bool standard, JitClsKernels& out, std::string& err) {
+  std::vector<ClassProgram> progs[2];
+  for (int d = 0; d < 2; ++d)
+    if (!build_programs(log2n, rounds, classes, angles, perms, mask, d == 0, standard, progs[d])) {
+      err = "jit: scale-folded program unsafe";
+      return 3;
+    }
+  std::vector<std::string> srcs(classes);
+  for (int c = 0; c < classes; ++c) srcs[c] = generate_class(log2n, 16, standard, progs[0][c], progs[1][c]);
+  return load_class_modules(srcs, out, err);
+}
+
 void jit_cls_release(JitClsKernels& k) {
   for (cudaLibrary_t l : k.lib)
     if (l) cudaLibraryUnload(l);
@@ -529,6 +689,56 @@ int jit_cls_launch(const JitClsKernels& k, int dir, const float* x, float* y, co
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = c > 0 ? 1 : 0;  // the first grid follows the bucketing normally
+    if (cudaLaunchKernelExC(&cfg, (const void*)k.fn[dir][c], args) != cudaSuccess) return 5;
+  }
+  return 0;
+}
+
+bool jit_fixed_supported(int log2n, int rounds) {
+  return log2n >= 4 && log2n <= 6 && rounds >= 1 && rounds * log2n <= 32 && !env_off("HYGT_FIXED_JIT");
+}
+
+int jit_fixed_build(int log2n, int rounds, int classes, int angle_bits, int precision_bits,
+                    const uint16_t* codes, const int32_t* ct, const int32_t* sn, const uint16_t* perms,
+                    uint32_t perm_mask, JitClsKernels& out, std::string& err) {
+  const int n = 1 << log2n;
+  const size_t a = (size_t)rounds * log2n * n / 2;
+  const uint32_t code_mask = (1u << angle_bits) - 1u;
+  std::vector<std::string> srcs(classes);
+  for (int c = 0; c < classes; ++c) {
+    std::ostringstream o;
+    o << "#define N " << n << "\n#define NQ " << n / 2 << "\n#define MINB 12\n#define PREC " << precision_bits
+      << "\n#define RND " << (1ll << (precision_bits - 1)) << "\n";
+    for (int d = 0; d < 2; ++d) {
+      uint64_t gm = 0;
+      const auto g = exec_gathers(log2n, rounds, perms ? perms + (size_t)c * rounds * n : nullptr, perm_mask,
+                                  d == 0, &gm);
+      const auto ops = fixed_program(log2n, rounds, codes + (size_t)c * a, ct, sn, code_mask, g, d == 0);
+      o << "#define KNAME " << (d == 0 ? "hygt_cls_f" : "hygt_cls_i") << "\n" << kFxPrologue;
+      emit_fixed_body(o, ops, g, n);
+      o << kFxEpilogue;
+    }
+    srcs[c] = o.str();
+  }
+  return load_class_modules(srcs, out, err);
+}
+
+int jit_fixed_launch(const JitClsKernels& k, int dir, const int64_t* x, int64_t* y, const uint32_t* idx,
+                     const uint32_t* seg_end, int classes, uint64_t count, unsigned long long* err,
+                     cudaStream_t st) {
+  const int launches = idx ? classes : 1;
+  for (int c = 0; c < launches; ++c) {
+    uint32_t bin = (uint32_t)c;
+    void* args[] = {(void*)&x, (void*)&y, (void*)&idx, (void*)&seg_end, (void*)&bin, (void*)&count, (void*)&err};
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(k.grid);
+    cfg.blockDim = dim3(32);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = c > 0 ? 1 : 0;
     if (cudaLaunchKernelExC(&cfg, (const void*)k.fn[dir][c], args) != cudaSuccess) return 5;
   }
   return 0;

@@ -50,4 +50,15 @@ void jit_cls_release(JitClsKernels& k);
 int jit_cls_launch(const JitClsKernels& k, int dir, const float* x, float* y, const uint32_t* idx,
                    const uint32_t* seg_end, int classes, cudaStream_t st);
 
+// The same chain for fixed-point plans (int64 rows, bit-exact with forward_fixed/inverse_fixed):
+// per-class kernels with the (c, s) TrigTable pairs as immediates. idx == nullptr: one launch
+// of class 0's kernels over rows [0, count) in order.
+bool jit_fixed_supported(int log2n, int rounds);
+int jit_fixed_build(int log2n, int rounds, int classes, int angle_bits, int precision_bits,
+                    const uint16_t* codes, const int32_t* ct, const int32_t* sn, const uint16_t* perms,
+                    uint32_t perm_mask, JitClsKernels& out, std::string& err);
+int jit_fixed_launch(const JitClsKernels& k, int dir, const int64_t* x, int64_t* y, const uint32_t* idx,
+                     const uint32_t* seg_end, int classes, uint64_t count, unsigned long long* err,
+                     cudaStream_t st);
+
 }  // namespace hygt_gpu

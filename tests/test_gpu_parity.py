@@ -239,8 +239,10 @@ def test_energy_vs_oracle_and_full_size(cuda, oracle_mod, golden):
 
 
 @pytest.mark.parametrize("k", range(7))
-def test_fixed_golden_bit_exact(cuda, golden, k):
+@pytest.mark.parametrize("fixed_jit", ["1", "0"])
+def test_fixed_golden_bit_exact(cuda, golden, k, fixed_jit, monkeypatch):
     from paper_2505_21728_b200 import ArgumentError, FixedPlan, QuantizedHyGTModel, TrigTable
+    monkeypatch.setenv("HYGT_FIXED_JIT", fixed_jit)
     log2n, rounds, b, p, with_perm = (int(v) for v in golden[f"x{k}_meta"])
     perm = golden[f"x{k}_perm"] if with_perm else None
     m = QuantizedHyGTModel(log2n, rounds, b, golden[f"x{k}_codes"], perm)
@@ -262,12 +264,15 @@ def test_fixed_golden_bit_exact(cuda, golden, k):
     assert np.array_equal(z, golden[f"x{k}_inv"][ok2])
 
 
-@pytest.mark.parametrize("kernel", ["default", "row", "warp"])
+@pytest.mark.parametrize("kernel", ["default", "stage", "row", "warp"])
 def test_fixed_random_multiclass_vs_oracle(cuda, oracle_mod, kernel, monkeypatch):
-    """Bit-exact vs the oracle through every fixed-point kernel: the staged one (N = 16), the
-    thread-per-row one (N <= 64) and the warp-per-row one."""
+    """Bit-exact vs the oracle through every fixed-point kernel: the per-class NVRTC chain
+    (default, N <= 64), the staged one (N = 16), the thread-per-row one (N <= 64) and the
+    warp-per-row one."""
     from paper_2505_21728_b200 import FixedPlan, QuantizedHyGTModel, TrigTable
     if kernel != "default":
+        monkeypatch.setenv("HYGT_FIXED_JIT", "0")
+    if kernel in ("row", "warp"):
         monkeypatch.setenv("HYGT_FIXED_STAGE", "0")
     if kernel == "warp":
         monkeypatch.setenv("HYGT_FIXED_ROW", "0")
@@ -504,10 +509,13 @@ def test_correlation_invalid_ids(cuda):
         correlation(x, c, 2)
 
 
-def test_fixed_staged_edges(cuda, oracle_mod):
-    """Staged fixed-point kernel (N = 16): partial and multi-tile batches, no class ids, in place,
-    the first failing row for oversized inputs and for invalid class ids."""
+@pytest.mark.parametrize("fixed_jit", ["1", "0"])
+def test_fixed_staged_edges(cuda, oracle_mod, fixed_jit, monkeypatch):
+    """Per-class NVRTC chain and staged fixed-point kernel (N = 16): partial and multi-tile
+    batches, no class ids, in place, the first failing row for oversized inputs and for invalid
+    class ids."""
     from paper_2505_21728_b200 import ArgumentError, FixedPlan, QuantizedHyGTModel, TrigTable
+    monkeypatch.setenv("HYGT_FIXED_JIT", fixed_jit)
     rng = np.random.default_rng(12)
     C, R, n = 6, 3, 16
     codes = rng.integers(0, 256, (C, R * 4 * 8)).astype(np.uint16)
