@@ -38,6 +38,7 @@ def parse():
     ap.add_argument("--rows", type=int, default=0, help="override rows per GPU (debug only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the config 3 / 5 side measurements")
     ap.add_argument("--verbose", action="store_true")
     return ap.parse_args()
 
@@ -277,21 +278,18 @@ def impl_klt(args, rank, world, local, dev):
     return 0
 
 
-def impl_ours(args):
+def measure_device(config, args, rank, world, local, dev, steps, warmup):
+    """Device-timed bucket + forward + inverse steps of one config (inputs resident in HBM, a
+    256 MiB L2 flush before each step, CUDA events on the launching stream, max over ranks).
+    Returns (summary dict, state needed for the e2e / CPU legs)."""
     import torch
     import torch.distributed as dist
-    rank, world, local = dist_setup(args.gpus)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    if args.config == 4:
-        return impl_klt(args, rank, world, local, dev)
     from paper_2505_21728_b200 import HyGTPlan
     from paper_2505_21728_b200.synth import make_workload
-    w = make_workload(args.config)
+    w = make_workload(config)
     rows = args.rows or w.cfg.count
-    if args.config == 5 and world > 1 and not args.rows:
+    strong = config == 5 and world > 1 and not args.rows
+    if strong:
         rows = w.cfg.count // world  # config 5: 2^24 rows sharded across the GPUs
     n = w.n
     row0 = rank * rows
@@ -324,21 +322,21 @@ def impl_ours(args):
         if energy is not None and world > 1:
             dist.all_reduce(energy)  # the one exchange step: 35 x 256 fp64 per-class energies
 
-    for _ in range(max(args.warmup, 3)):
+    for _ in range(max(warmup, 3)):
         step()
     plan.sync_status(ws)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
 
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         total_ms = 0.0
-        for k in range(args.steps):
+        for k in range(steps):
             l2_flush.zero_()  # inputs are > L2 already; flush anyway so no step starts L2-warm
             start.record(stream)
             step(evs[k])
@@ -348,7 +346,7 @@ def impl_ours(args):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-    ms = total_ms / args.steps
+    ms = total_ms / steps
     t_bucket = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
     t_fwd = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
     t_inv = statistics.mean(e[2].elapsed_time(e[3]) for e in evs)
@@ -358,7 +356,6 @@ def impl_ours(args):
         ms = float(t.item())
     plan.sync_status(ws)
     total_rows = rows * world
-    value = total_rows / (ms * 1e-3)
 
     hbm, hbm_kind = peaks()
     bpr = bytes_per_row(n, w.cfg.classes)
@@ -369,41 +366,75 @@ def impl_ours(args):
                 "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
                 "kernel": KERNEL_NAMES.get(plan.path, f"hygt_{plan.path}_kernel") + " (mean of the forward and inverse launches)",
                 "bytes_per_launch": rows * bpr, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({hbm_kind})"}
-    launches_per_step = plan.launches_per_step()
+    out = {"workload": w.cfg.name, "value": total_rows / (ms * 1e-3), "unit": "vectors/s",
+           "ms_per_step": ms, "steps": steps, "warmup": max(warmup, 3), "rows_per_gpu": rows,
+           "scaling": "strong" if strong else "weak", "N": n, "classes": w.cfg.classes,
+           "rounds": w.cfg.rounds, "inter_round_perms": w.perms is not None,
+           "energy_allreduce": bool(w.cfg.energy), "algorithm": plan.algorithm, "kernel_path": plan.path,
+           "breakdown_ms": {"bucket": t_bucket, "forward": t_fwd, "inverse": t_inv},
+           "roofline": roofline, "clocks": clocks.summary(),
+           "gpu_launches": plan.launches_per_step() * steps}
+    return out, (w, plan, x, cls, rows, stream)
 
+
+def impl_ours(args):
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if args.config == 4:
+        return impl_klt(args, rank, world, local, dev)
+    res, (w, plan, x, cls, rows, stream) = measure_device(args.config, args, rank, world, local, dev,
+                                                          args.steps, args.warmup)
     e2e = None
     if not args.no_e2e:
         e2e = measure_e2e(plan, w, x, cls, rows, dev, stream, args, world)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        srows = cpu_sample_rows(n, threads, seconds=5.0)
+        srows = cpu_sample_rows(w.n, threads, seconds=5.0)
         t = run_reference_sample(w, srows, threads)
         cpu = {"value": srows / t, "unit": "vectors/s", "cores": threads, "kind": "reference",
                "sample": f"{srows} rows of {w.cfg.name}: hygt::forward+hygt::inverse per row "
                          f"(unmodified reference headers via oracle/_ref, g++ -O2), {threads} threads"}
+    del plan, x, cls
+    # The metric names N = 16 / 64 / 256: the default run also times configs 3 and 5 (same
+    # rules, fewer steps) and reports them beside the headline.
+    others = []
+    if args.config == 2 and not args.no_extra and not args.rows:
+        for c in (3, 5):
+            torch.cuda.empty_cache()
+            o, _ = measure_device(c, args, rank, world, local, dev, max(3, min(args.steps, 10)), args.warmup)
+            others.append(o)
+            torch.cuda.empty_cache()
     if rank == 0:
         line = {
-            "metric": "HyGT fwd+inv vectors/s", "value": value, "unit": "vectors/s",
-            "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "metric": "HyGT fwd+inv vectors/s", "value": res["value"], "unit": "vectors/s",
+            "n_gpus": world, "steps": args.steps, "warmup": res["warmup"],
+            "ms_per_step": res["ms_per_step"], "higher_is_better": True, "scaling": res["scaling"],
+            "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (device-generated separable AR(1) rows, seeded)",
-            "config": {"workload": w.cfg.name, "rows_per_gpu": rows, "N": n,
-                       "classes": w.cfg.classes, "rounds": w.cfg.rounds,
-                       "inter_round_perms": w.perms is not None,
+            "config": {"workload": res["workload"], "rows_per_gpu": res["rows_per_gpu"], "N": res["N"],
+                       "classes": res["classes"], "rounds": res["rounds"],
+                       "inter_round_perms": res["inter_round_perms"],
                        "step": "class bucketing + forward + inverse",
                        "l2": "inputs larger than L2 (>=1 GiB per array) and a 256 MiB L2 flush between steps",
-                       "parallelism": f"dp{world}", "algorithm": plan.algorithm,
-                       "kernel_path": plan.path},
-            "breakdown_ms": {"bucket": t_bucket, "forward": t_fwd, "inverse": t_inv},
-            "roofline": roofline,
-            "clocks": clocks.summary(),
-            "gpu_launches": launches_per_step * args.steps,
+                       "parallelism": f"dp{world}", "algorithm": res["algorithm"],
+                       "kernel_path": res["kernel_path"]},
+            "breakdown_ms": res["breakdown_ms"],
+            "roofline": res["roofline"],
+            "clocks": res["clocks"],
+            "gpu_launches": res["gpu_launches"],
         }
         if e2e:
             line["e2e"] = e2e
         if cpu:
             line["cpu_baseline"] = cpu
+        if others:
+            line["other_configs"] = others
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
