@@ -96,10 +96,11 @@ int hygt_plan_algorithm(const hygt_plan* plan);
  *     the class grids chained by programmatic dependent launch. Forward-with-energy calls run
  *     on the class-segment kernel instead,
  * 7 = the chain of 6 with one plan-specialised kernel per class and direction (NVRTC at plan
- *     creation, N = 32 / 64, R <= 8, >= 2 classes not served by 3): coefficients are FFMA
+ *     creation, N = 32 / 64 / 256, R <= 8, >= 2 classes not served by 3): coefficients are FFMA
  *     immediates and permutations register renames, so the class's rows touch shared memory
- *     only on their way in and out. Forward-with-energy calls of N = 32 plans run on the tile
- *     kernel instead. */
+ *     only on their way in and out (N = 256: a row is split over a warp pair that exchanges half
+ *     its samples once per round; forward-with-energy fused). Forward-with-energy calls of
+ *     N = 32 / 64 plans run on the tile / segment kernels instead. */
 int hygt_plan_path(const hygt_plan* plan);
 
 /* Device workspace for class bucketing of `count` rows. */

@@ -943,10 +943,10 @@ int setup_cls(hygt_plan* p, const double* angles, const uint16_t* perms) {
 }
 
 int run_cls(const hygt_plan* p, int dir, const float* x, float* y, const WsLayout& w, char* ws,
-            cudaStream_t st) {
+            cudaStream_t st, double* energy = nullptr) {
   if (p->cls_jit.ok) {
     if (jit_cls_launch(p->cls_jit, dir, x, y, reinterpret_cast<const uint32_t*>(ws + w.idx),
-                       reinterpret_cast<const uint32_t*>(ws + w.seg), p->classes, st))
+                       reinterpret_cast<const uint32_t*>(ws + w.seg), p->classes, st, energy))
       return fail(HYGT_ERR_CUDA, std::string("hygt: class launch failed: ") + cudaGetErrorString(cudaGetLastError()));
     return ok();
   }
@@ -1046,13 +1046,14 @@ int run_apply(const hygt_plan* p, int dir, const float* x, float* y, const uint1
   }
   if (stage_usable(p, x, y, energy)) return run_stage(p, dir, x, y, d_cls, count, d_ws, ws_bytes, flags, st);
   const bool bucketed = d_cls && p->classes > 1;
-  if (p->cls && bucketed && !energy) {  // per-class launch chain (N = 32 / 64)
+  // per-class launch chain (N = 32 / 64 / 256; the N = 256 kernels also fuse the energy)
+  if (p->cls && bucketed && (!energy || (p->cls_jit.ok && !p->cls_jit.fn_e.empty()))) {
     if (!d_ws || ws_bytes < w.total) return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
     if (!(flags & HYGT_REUSE_BUCKETS)) {
       const int s = run_bucket(p, p->classes, 0, d_cls, count, d_ws, ws_bytes, st);
       if (s) return s;
     }
-    return run_cls(p, dir, x, y, w, static_cast<char*>(d_ws), st);
+    return run_cls(p, dir, x, y, w, static_cast<char*>(d_ws), st, energy);
   }
   if (p->tile) {
     if (d_cls && (!d_ws || ws_bytes < 256)) return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");

@@ -78,6 +78,8 @@ def _variants(log2n):
                     "HYGT_TILE_L": str(l), "HYGT_TILE_VPT": str(v)})
     if log2n == 5:  # per-class NVRTC chain (multi-class plans the all-class JIT does not take)
         out.append({"HYGT_JIT": "0", "HYGT_CLS_JIT": "1"})
+    if log2n == 8:  # opt-in warp-pair variant of the chain
+        out.append({"HYGT_JIT": "0", "HYGT_CLS_JIT": "1", "HYGT_CLS_JIT256": "1"})
     if log2n in STAGE_LOG2N:  # TMA-staged tile kernel
         out.append({"HYGT_JIT": "0", "HYGT_STAGE": "1"})
         out.append({"HYGT_JIT": "0", "HYGT_STAGE": "1", "HYGT_STAGE_ROWS": "136"})
@@ -215,8 +217,10 @@ def test_bucketing_large_batch_roundtrip(cuda):
     check_close(y[idx].cpu().numpy(), ref, x[idx].cpu().numpy(), "cfg2 full-size sample")
 
 
-def test_energy_vs_oracle_and_full_size(cuda, oracle_mod, golden):
+@pytest.mark.parametrize("jit256", ["0", "1"])
+def test_energy_vs_oracle_and_full_size(cuda, oracle_mod, golden, jit256, monkeypatch):
     from paper_2505_21728_b200 import HyGTModel, HyGTPlan
+    monkeypatch.setenv("HYGT_CLS_JIT256", jit256)  # segment kernel / opt-in warp-pair chain
     log2n, rounds, classes = (int(v) for v in golden["en_meta"])
     angles = golden["en_angles"]
     plan = HyGTPlan([HyGTModel(log2n, rounds, angles[c]) for c in range(classes)])
