@@ -32,6 +32,16 @@ namespace hygt_gpu {
 
 namespace {
 
+bool env_on(const char* name) {
+  const char* v = std::getenv(name);
+  return v && std::atoi(v) != 0;
+}
+
+bool env_off(const char* name) {
+  const char* v = std::getenv(name);
+  return v && std::atoi(v) == 0;
+}
+
 std::string lit(float f) {
   uint32_t u;
   std::memcpy(&u, &f, 4);
@@ -275,15 +285,100 @@ const char* kClsEpilogue = R"CUDA(
 #undef KNAME
 )CUDA";
 
+// Double-buffered variant: the next batch's rows are copied into the second slot area while
+// this batch computes (HYGT_CLS_DB=1).
+const char* kClsPrologueDB = R"CUDA(
+typedef unsigned int u32;
+typedef unsigned long long u64;
+#define RS (NQ + 1)
+extern "C" __global__ void __launch_bounds__(32, MINB)
+KNAME(const float* __restrict__ x, float* __restrict__ y, const u32* __restrict__ idx,
+      const u32* __restrict__ seg_end, u32 bin, u32 copy_bin) {
+  __shared__ __align__(16) float4 slot[2][32 * RS];
+  __shared__ u32 s_row[2][32];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int lane = threadIdx.x;
+  const u64 beg = bin ? __ldg(seg_end + bin - 1) : 0u;
+  const u64 end = __ldg(seg_end + bin);
+  const u64 nb = (end - beg + 31) / 32;
+  auto row_id = [&](u64 b) -> u32 {
+    const u64 p = beg + b * 32 + lane;
+    return b < nb && p < end ? __ldg(idx + p) : 0xffffffffu;
+  };
+  auto issue = [&](int buf, u32 id) {
+    __syncwarp();
+    s_row[buf][lane] = id;
+    __syncwarp();
+    const u32 ss = (u32)__cvta_generic_to_shared(slot[buf]);
+#pragma unroll
+    for (int i0 = 0; i0 < 32; i0 += 32 / NQ) {
+      const int i = i0 + lane / NQ, q = lane % NQ;
+      const u32 row = s_row[buf][i];
+      if (row != 0xffffffffu)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ss + (u32)(i * RS + q) * 16u),
+                     "l"(x + (size_t)row * N + q * 4) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  u64 b = blockIdx.x;
+  if (b < nb) issue(0, row_id(b));
+  u32 id_next = row_id(b + gridDim.x);
+  int cur = 0;
+  for (; b < nb; b += gridDim.x, cur ^= 1) {
+    const bool more = b + gridDim.x < nb;
+    if (more) {
+      issue(cur ^ 1, id_next);
+      id_next = row_id(b + 2 * (u64)gridDim.x);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncwarp();
+    float4* sl = slot[cur];
+    const u32* sr = s_row[cur];
+    float v[N];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const float4 a = sl[lane * RS + q];
+      v[4 * q] = a.x; v[4 * q + 1] = a.y; v[4 * q + 2] = a.z; v[4 * q + 3] = a.w;
+    }
+    {
+)CUDA";
+
+const char* kClsEpilogueDB = R"CUDA(
+    }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) sl[lane * RS + q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    __syncwarp();
+#pragma unroll
+    for (int i0 = 0; i0 < 32; i0 += 32 / NQ) {
+      const int i = i0 + lane / NQ, q = lane % NQ;
+      const u32 row = sr[i];
+      if (row != 0xffffffffu) __stcs((float4*)(y + (size_t)row * N) + q, sl[i * RS + q]);
+    }
+  }
+  if (copy_bin) {  // rows with invalid class ids pass through (hygt_bucket flags them)
+    const u64 e2 = __ldg(seg_end + bin + 1);
+    for (u64 p = end + (u64)blockIdx.x * (32 / NQ) + lane / NQ; p < e2; p += (u64)gridDim.x * (32 / NQ)) {
+      const u32 row = __ldg(idx + p);
+      ((float4*)(y + (size_t)row * N))[lane % NQ] = ((const float4*)(x + (size_t)row * N))[lane % NQ];
+    }
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+#undef KNAME
+)CUDA";
+
 // Source of one class's two kernels (hygt_cls_f, hygt_cls_i).
 std::string generate_class(int log2n, int minb, bool standard, const ClassProgram& fwd, const ClassProgram& inv) {
   const int n = 1 << log2n;
   std::ostringstream o;
   o << "#define N " << n << "\n#define NQ " << n / 4 << "\n#define MINB " << minb << "\n";
+  const bool dbuf = env_on("HYGT_CLS_DB");
   for (int d = 0; d < 2; ++d) {
-    o << "#define KNAME " << (d == 0 ? "hygt_cls_f" : "hygt_cls_i") << "\n" << kClsPrologue;
+    o << "#define KNAME " << (d == 0 ? "hygt_cls_f" : "hygt_cls_i") << "\n" << (dbuf ? kClsPrologueDB : kClsPrologue);
     emit_body(o, d == 0 ? fwd : inv, n, standard);
-    o << kClsEpilogue;
+    o << (dbuf ? kClsEpilogueDB : kClsEpilogue);
   }
   return o.str();
 }
@@ -919,15 +1014,7 @@ int load_class_modules(const std::vector<std::string>& srcs, JitClsKernels& out,
   return 0;
 }
 
-bool env_on(const char* name) {
-  const char* v = std::getenv(name);
-  return v && std::atoi(v) != 0;
-}
 
-bool env_off(const char* name) {
-  const char* v = std::getenv(name);
-  return v && std::atoi(v) == 0;
-}
 
 bool jit_cls_supported(int log2n, int classes, int rounds) {
   // N = 16 rows (64 B) are half a 128 B line: gathered per class they cost twice the staged
