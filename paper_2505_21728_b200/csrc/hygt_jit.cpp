@@ -285,6 +285,71 @@ const char* kClsEpilogue = R"CUDA(
 #undef KNAME
 )CUDA";
 
+const char* kClsProloguePTX = R"CUDA(
+typedef unsigned int u32;
+typedef unsigned long long u64;
+#define RS (NQ + 1)
+extern "C" __global__ void __launch_bounds__(32, MINB)
+KNAME(const float* __restrict__ x, float* __restrict__ y, const u32* __restrict__ idx,
+      const u32* __restrict__ seg_end, u32 bin, u32 copy_bin) {
+  __shared__ __align__(16) float4 slot[32 * RS];
+  __shared__ u32 s_row[32];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int lane = threadIdx.x;
+  const u64 beg = bin ? __ldg(seg_end + bin - 1) : 0u;
+  const u64 end = __ldg(seg_end + bin);
+  const u64 nb = (end - beg + 31) / 32;
+  auto row_id = [&](u64 b) -> u32 {
+    const u64 p = beg + b * 32 + lane;
+    return b < nb && p < end ? __ldg(idx + p) : 0xffffffffu;
+  };
+  const u32 slot_s = (u32)__cvta_generic_to_shared(slot);
+  u32 id_next = row_id(blockIdx.x);
+  for (u64 b = blockIdx.x; b < nb; b += gridDim.x) {
+    __syncwarp();
+    s_row[lane] = id_next;
+    id_next = row_id(b + gridDim.x);
+    __syncwarp();
+#pragma unroll
+    for (int i0 = 0; i0 < 32; i0 += 32 / NQ) {
+      const int i = i0 + lane / NQ, q = lane % NQ;
+      const u32 row = s_row[i];
+      if (row != 0xffffffffu)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(slot_s + (u32)(i * RS + q) * 16u),
+                     "l"(x + (size_t)row * N + q * 4) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+    const u32 rb = slot_s + (u32)lane * (RS * 16u);  // this lane's row: the PTX body reads and rewrites it
+    if (id_next != 0xffffffffu)  // the next batch's rows: in L2 by the time this one is done
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(x + (size_t)id_next * N), "n"(N * 4) : "memory");
+    {
+)CUDA";
+
+const char* kClsEpiloguePTX = R"CUDA(
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i0 = 0; i0 < 32; i0 += 32 / NQ) {
+      const int i = i0 + lane / NQ, q = lane % NQ;
+      const u32 row = s_row[i];
+      if (row != 0xffffffffu) __stcs((float4*)(y + (size_t)row * N) + q, slot[i * RS + q]);
+    }
+  }
+  if (copy_bin) {  // rows with invalid class ids pass through (hygt_bucket flags them)
+    const u64 e2 = __ldg(seg_end + bin + 1);
+    for (u64 p = end + (u64)blockIdx.x * (32 / NQ) + lane / NQ; p < e2; p += (u64)gridDim.x * (32 / NQ)) {
+      const u32 row = __ldg(idx + p);
+      ((float4*)(y + (size_t)row * N))[lane % NQ] = ((const float4*)(x + (size_t)row * N))[lane % NQ];
+    }
+  }
+  // complete only after the previous class grid: the last grid's completion implies the chain's
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+#undef KNAME
+)CUDA";
+
+
 // Double-buffered variant: the next batch's rows are copied into the second slot area while
 // this batch computes (HYGT_CLS_DB=1).
 const char* kClsPrologueDB = R"CUDA(
@@ -370,15 +435,24 @@ const char* kClsEpilogueDB = R"CUDA(
 )CUDA";
 
 // Source of one class's two kernels (hygt_cls_f, hygt_cls_i).
+void emit_body_ptx(std::ostringstream& o, const ClassProgram& pr, int n, bool standard);
+
 std::string generate_class(int log2n, int minb, bool standard, const ClassProgram& fwd, const ClassProgram& inv) {
   const int n = 1 << log2n;
   std::ostringstream o;
   o << "#define N " << n << "\n#define NQ " << n / 4 << "\n#define MINB " << minb << "\n";
   const bool dbuf = env_on("HYGT_CLS_DB");
+  // PTX bodies (HYGT_CLS_PTX=1) skip the NVVM pass: 0.7 s instead of 2.5 s per class, but the
+  // N = 64 kernels run 15% slower than NVVM's (profiles/r01/cls_experiments.log), so opt-in
+  const bool ptx = !dbuf && env_on("HYGT_CLS_PTX");
   for (int d = 0; d < 2; ++d) {
-    o << "#define KNAME " << (d == 0 ? "hygt_cls_f" : "hygt_cls_i") << "\n" << (dbuf ? kClsPrologueDB : kClsPrologue);
-    emit_body(o, d == 0 ? fwd : inv, n, standard);
-    o << (dbuf ? kClsEpilogueDB : kClsEpilogue);
+    o << "#define KNAME " << (d == 0 ? "hygt_cls_f" : "hygt_cls_i") << "\n"
+      << (dbuf ? kClsPrologueDB : ptx ? kClsProloguePTX : kClsPrologue);
+    if (ptx)
+      emit_body_ptx(o, d == 0 ? fwd : inv, n, standard);
+    else
+      emit_body(o, d == 0 ? fwd : inv, n, standard);
+    o << (dbuf ? kClsEpilogueDB : ptx ? kClsEpiloguePTX : kClsEpilogue);
   }
   return o.str();
 }
@@ -621,6 +695,58 @@ std::string hexf(float f) {
   char b[16];
   std::snprintf(b, sizeof b, "0f%08X", u);
   return b;
+}
+
+// The class body as one PTX block over the lane's row in its slot (operand %0: shared address):
+// the front end never sees the straight-line code, so NVRTC time is ptxas time.
+void emit_body_ptx(std::ostringstream& o, const ClassProgram& pr, int n, bool standard) {
+  std::ostringstream b;
+  int nreg = 0;
+  auto R = [](int r) { return "%%hv" + std::to_string(r); };
+  std::vector<int> cur(n);
+  for (int q = 0; q < n / 4; ++q) {
+    b << "ld.shared.v4.f32 {" << R(nreg) << "," << R(nreg + 1) << "," << R(nreg + 2) << "," << R(nreg + 3) << "}, [%0+"
+      << q * 16 << "];\n";
+    for (int t = 0; t < 4; ++t) cur[4 * q + t] = nreg++;
+  }
+  for (const ProgOp& op : pr.ops) {
+    if (op.kind == 0) {
+      const int a = cur[op.m], bb = cur[op.n];
+      if (!standard) {  // a' = a + t1 b ; b' = b - t2 a   (op.b = -t2)
+        b << "fma.rn.f32 " << R(nreg) << ", " << R(bb) << ", " << hexf(op.a) << ", " << R(a) << ";\n"
+          << "fma.rn.f32 " << R(nreg + 1) << ", " << R(a) << ", " << hexf(op.b) << ", " << R(bb) << ";\n";
+        cur[op.m] = nreg;
+        cur[op.n] = nreg + 1;
+        nreg += 2;
+      } else {  // y_m = c a + s b ; y_n = c b - s a   (givens.hpp:44-47)
+        b << "mul.rn.f32 " << R(nreg) << ", " << R(bb) << ", " << hexf(op.b) << ";\n"
+          << "fma.rn.f32 " << R(nreg + 1) << ", " << R(a) << ", " << hexf(op.a) << ", " << R(nreg) << ";\n"
+          << "mul.rn.f32 " << R(nreg + 2) << ", " << R(a) << ", " << hexf(-op.b) << ";\n"
+          << "fma.rn.f32 " << R(nreg + 3) << ", " << R(bb) << ", " << hexf(op.a) << ", " << R(nreg + 2) << ";\n";
+        cur[op.m] = nreg + 1;
+        cur[op.n] = nreg + 3;
+        nreg += 4;
+      }
+    } else if (op.kind == 1) {
+      const auto& g = pr.gathers[op.arg];
+      std::vector<int> nxt(n);
+      for (int i = 0; i < n; ++i) nxt[i] = cur[g[i]];
+      cur.swap(nxt);
+    } else {
+      for (int i = 0; i < n; ++i) {
+        b << "mul.rn.f32 " << R(nreg) << ", " << R(cur[i]) << ", " << hexf(pr.scales[i]) << ";\n";
+        cur[i] = nreg++;
+      }
+    }
+  }
+  for (int q = 0; q < n / 4; ++q)
+    b << "st.shared.v4.f32 [%0+" << q * 16 << "], {" << R(cur[4 * q]) << "," << R(cur[4 * q + 1]) << ","
+      << R(cur[4 * q + 2]) << "," << R(cur[4 * q + 3]) << "};\n";
+  o << "asm volatile(\"{\\n.reg .f32 %%hv<" << nreg << ">;\\n\"\n";
+  std::istringstream lines(b.str());
+  std::string ln;
+  while (std::getline(lines, ln)) o << "\"" << ln << "\\n\"\n";
+  o << "\"}\" :: \"r\"(rb) : \"memory\");\n";
 }
 
 // Emits both warps' bodies for one class and direction as PTX (one inline-asm block per warp, so

@@ -73,6 +73,7 @@ def _variants(log2n):
         out.append({"HYGT_SEG2": "1", "HYGT_CLS": "0", "HYGT_CLS_JIT": "0", "HYGT_SEG2_TMA": "1"})
         out.append({"HYGT_CLS": "1", "HYGT_CLS_JIT": "0"})  # per-class launches, parameter tables
         out.append({"HYGT_CLS_JIT": "1"})  # per-class launches, NVRTC-specialised kernels
+        out.append({"HYGT_CLS_JIT": "1", "HYGT_CLS_PTX": "1"})  # the same with PTX bodies
     for l, v in TILE_LAYOUTS.get(log2n, []):
         out.append({"HYGT_JIT": "0", "HYGT_STAGE": "0", "HYGT_TILE": "1", "HYGT_CLS_JIT": "0",
                     "HYGT_TILE_L": str(l), "HYGT_TILE_VPT": str(v)})
