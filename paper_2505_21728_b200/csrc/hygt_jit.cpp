@@ -972,6 +972,7 @@ int compile(const std::string& src, std::vector<char>& cubin, std::string& log) 
     }
   }
   std::lock_guard<std::mutex> lk(g_cache_mu);
+  if (g_cubin_cache.size() >= 512) g_cubin_cache.clear();  // bound the process's cache (~0.5 MB per class)
   g_cubin_cache.emplace(src, cubin);
   return 0;
 }
