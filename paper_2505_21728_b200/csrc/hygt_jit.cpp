@@ -1174,7 +1174,7 @@ int jit_cls_build(int log2n, int rounds, int classes, const double* angles, cons
       return 3;
     }
   std::vector<std::string> srcs(classes);
-  for (int c = 0; c < classes; ++c) srcs[c] = generate_class(log2n, 16, standard, progs[0][c], progs[1][c]);
+  for (int c = 0; c < classes; ++c) srcs[c] = generate_class(log2n, std::getenv("HYGT_CLS_MINB") ? std::atoi(std::getenv("HYGT_CLS_MINB")) : 16, standard, progs[0][c], progs[1][c]);
   return load_class_modules(srcs, out, err);
 }
 
