@@ -255,8 +255,15 @@ KNAME(const float* __restrict__ x, float* __restrict__ y, const u32* __restrict_
       const float4 a = slot[lane * RS + q];
       v[4 * q] = a.x; v[4 * q + 1] = a.y; v[4 * q + 2] = a.z; v[4 * q + 3] = a.w;
     }
-    if (id_next != 0xffffffffu)  // the next batch's rows: in L2 by the time this one is done
+    if (id_next != 0xffffffffu) {  // the next batch's rows: in L2 by the time this one is done
+#if PFMODE == 1
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(x + (size_t)id_next * N), "n"(N * 4) : "memory");
+#elif PFMODE == 2
+#pragma unroll
+      for (int l = 0; l < (N * 4 + 127) / 128; ++l)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(x + (size_t)id_next * N + l * 32) : "memory");
+#endif
+    }
     {
 )CUDA";
 
@@ -321,8 +328,15 @@ KNAME(const float* __restrict__ x, float* __restrict__ y, const u32* __restrict_
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
     __syncwarp();
     const u32 rb = slot_s + (u32)lane * (RS * 16u);  // this lane's row: the PTX body reads and rewrites it
-    if (id_next != 0xffffffffu)  // the next batch's rows: in L2 by the time this one is done
+    if (id_next != 0xffffffffu) {  // the next batch's rows: in L2 by the time this one is done
+#if PFMODE == 1
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(x + (size_t)id_next * N), "n"(N * 4) : "memory");
+#elif PFMODE == 2
+#pragma unroll
+      for (int l = 0; l < (N * 4 + 127) / 128; ++l)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(x + (size_t)id_next * N + l * 32) : "memory");
+#endif
+    }
     {
 )CUDA";
 
@@ -441,6 +455,9 @@ std::string generate_class(int log2n, int minb, bool standard, const ClassProgra
   const int n = 1 << log2n;
   std::ostringstream o;
   o << "#define N " << n << "\n#define NQ " << n / 4 << "\n#define MINB " << minb << "\n";
+  // next-batch L2 prefetch, measured per row length (profiles/r01/cls_experiments.log): the bulk
+  // prefetch (a uniform loop of UBLKPF) pays off for 256 B rows, per-lane line prefetches for 128 B
+  o << "#define PFMODE " << (std::getenv("HYGT_CLS_PF") ? std::atoi(std::getenv("HYGT_CLS_PF")) : n >= 64 ? 1 : 2) << "\n";
   const bool dbuf = env_on("HYGT_CLS_DB");
   // PTX bodies (HYGT_CLS_PTX=1) skip the NVVM pass: 0.7 s instead of 2.5 s per class, but the
   // N = 64 kernels run 15% slower than NVVM's (profiles/r01/cls_experiments.log), so opt-in
@@ -520,8 +537,15 @@ KNAME(const i64* __restrict__ x, i64* __restrict__ y, const u32* __restrict__ id
       bad |= a.x > (1 << 20) || a.x < -(1 << 20) || a.y > (1 << 20) || a.y < -(1 << 20);
       v[2 * q] = (int)a.x; v[2 * q + 1] = (int)a.y;
     }
-    if (id_next != 0xffffffffu)  // the next batch's rows: in L2 by the time this one is done
+    if (id_next != 0xffffffffu) {  // the next batch's rows: in L2 by the time this one is done
+#if PFMODE == 1
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(x + (size_t)id_next * N), "n"(N * 8) : "memory");
+#elif PFMODE == 2
+#pragma unroll
+      for (int l = 0; l < (N * 8 + 127) / 128; ++l)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(x + (size_t)id_next * N + l * 16) : "memory");
+#endif
+    }
     if (!bad) {
 )CUDA";
 
@@ -1217,6 +1241,7 @@ int jit_fixed_build(int log2n, int rounds, int classes, int angle_bits, int prec
   std::vector<std::string> srcs(classes);
   for (int c = 0; c < classes; ++c) {
     std::ostringstream o;
+    o << "#define PFMODE " << (std::getenv("HYGT_FIXED_PF") ? std::atoi(std::getenv("HYGT_FIXED_PF")) : n >= 64 ? 0 : 2) << "\n";
     o << "#define N " << n << "\n#define NQ " << n / 2 << "\n#define MINB 12\n#define PREC " << precision_bits
       << "\n#define RND " << (1ll << (precision_bits - 1)) << "\n";
     for (int d = 0; d < 2; ++d) {
