@@ -16,6 +16,7 @@
 
 #include <nvrtc.h>
 
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -1280,3 +1281,52 @@ int jit_fixed_launch(const JitClsKernels& k, int dir, const int64_t* x, int64_t*
 }
 
 }  // namespace hygt_gpu
+
+// Debug hook (not in the public header; used by the CPU test suite): generates and compiles class
+// 0's per-class kernels without touching a GPU and returns the cubin size. kind 0: float
+// (N = 32 / 64 C++ bodies, N = 256 PTX warp-pair bodies; ptx != 0 selects PTX bodies for N <= 64),
+// kind 1: fixed point (8-bit codes, p = 10). Returns 0 or the failing status.
+extern "C" int hygt_debug_jit_compile(int kind, int log2n, int rounds, const double* angles,
+                                      const uint16_t* codes, const uint16_t* perms, uint32_t mask, int ptx,
+                                      unsigned long long* cubin_bytes) {
+  using namespace hygt_gpu;
+  std::string src;
+  if (kind == 0) {
+    std::vector<ClassProgram> progs[2];
+    for (int d = 0; d < 2; ++d)
+      if (!build_programs(log2n, rounds, 1, angles, perms, mask, d == 0, false, progs[d])) return 3;
+    if (log2n == 8) {
+      src = generate_class_256(false, progs[0][0], progs[1][0]);
+    } else {
+      const char* prev = std::getenv("HYGT_CLS_PTX");
+      const std::string keep = prev ? prev : "";
+      setenv("HYGT_CLS_PTX", ptx ? "1" : "0", 1);
+      src = generate_class(log2n, 16, false, progs[0][0], progs[1][0]);
+      if (prev) setenv("HYGT_CLS_PTX", keep.c_str(), 1); else unsetenv("HYGT_CLS_PTX");
+    }
+  } else {
+    const int n = 1 << log2n;
+    std::vector<int32_t> ct(256), sn(256);
+    for (int q = 0; q < 256; ++q) {
+      const double ang = 2.0 * 3.14159265358979323846 * q / 256.0;
+      ct[q] = (int32_t)std::lround(std::cos(ang) * 1024.0);
+      sn[q] = (int32_t)std::lround(std::sin(ang) * 1024.0);
+    }
+    std::ostringstream o;
+    o << "#define PFMODE 1\n#define N " << n << "\n#define NQ " << n / 2 << "\n#define MINB 12\n#define PREC 10\n#define RND 512\n";
+    for (int d = 0; d < 2; ++d) {
+      uint64_t gm = 0;
+      const auto g = exec_gathers(log2n, rounds, perms, mask, d == 0, &gm);
+      const auto ops = fixed_program(log2n, rounds, codes, ct.data(), sn.data(), 255u, g, d == 0);
+      o << "#define KNAME " << (d == 0 ? "hygt_cls_f" : "hygt_cls_i") << "\n" << kFxPrologue;
+      emit_fixed_body(o, ops, g, n);
+      o << kFxEpilogue;
+    }
+    src = o.str();
+  }
+  std::vector<char> cubin;
+  std::string log;
+  if (compile(src, cubin, log)) return 5;
+  if (cubin_bytes) *cubin_bytes = cubin.size();
+  return 0;
+}

@@ -165,3 +165,24 @@ def test_trainer_host_logic_mirrors_reference(oracle_mod):
     from paper_2505_21728_b200.errors import ArgumentError
     with pytest.raises(ArgumentError):
         train.variance_permutation(m, [1.0, 2.0, 3.0, 4.0])
+
+
+@pytest.mark.parametrize("kind,log2n,rounds,ptx", [(0, 6, 4, 0), (0, 6, 4, 1), (0, 5, 3, 0), (0, 8, 2, 0), (1, 4, 3, 0), (1, 6, 2, 0)])
+def test_per_class_kernels_compile_without_gpu(kind, log2n, rounds, ptx):
+    """The per-class NVRTC generators (float N = 32/64/256, fixed point) emit source that compiles
+    for sm_100a; NVRTC needs no GPU, so this runs in the CPU suite (hygt_debug_jit_compile)."""
+    import ctypes as C
+    from paper_2505_21728_b200 import _lib
+    lib = _lib.lib()
+    fn = lib.hygt_debug_jit_compile
+    fn.restype = C.c_int
+    n = 1 << log2n
+    rng = np.random.default_rng(4)
+    angles = np.ascontiguousarray(rng.uniform(-np.pi, np.pi, rounds * log2n * n // 2))
+    codes = np.ascontiguousarray(rng.integers(0, 256, rounds * log2n * n // 2).astype(np.uint16))
+    perms = np.ascontiguousarray(np.stack([rng.permutation(n) for _ in range(rounds)]).astype(np.uint16))
+    mask = (1 << (rounds - 1)) - 1 if log2n < 8 else 0
+    out = C.c_ulonglong(0)
+    st = fn(kind, log2n, rounds, angles.ctypes.data_as(C.c_void_p), codes.ctypes.data_as(C.c_void_p),
+            perms.ctypes.data_as(C.c_void_p) if mask else None, C.c_uint32(mask), ptx, C.byref(out))
+    assert st == 0 and out.value > 10000
