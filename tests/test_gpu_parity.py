@@ -333,6 +333,27 @@ def test_klt_config4_vs_oracle(cuda, oracle_mod):
     check_close(ys.cpu().numpy(), ref1, xs.cpu().numpy(), "klt single class")
 
 
+def test_klt_multi_tile_pipeline(cuda, oracle_mod):
+    """Config-4 KLT at a size where every CTA runs several tiles per class (the software
+    pipeline's steady state): round trip over all rows, a random sample against the oracle."""
+    from paper_2505_21728_b200 import KLTPlan
+    from paper_2505_21728_b200.synth import make_workload
+    w = make_workload(4)
+    k = w.klt_bases()
+    plan = KLTPlan(k)
+    rows = 1 << 21  # ~60K rows = ~470 tiles of 128 per class, > 3 per CTA
+    cls = w.make_classes(rows)
+    x = w.make_rows(rows, cls)
+    y = plan.forward(x, cls)
+    back = plan.inverse(y, cls)
+    err = (torch.linalg.vector_norm(back - x) / torch.linalg.vector_norm(x)).item()
+    assert err < 1e-6, err
+    idx = np.random.default_rng(3).choice(rows, 4096, replace=False)
+    xs, cs = x.cpu().numpy()[idx], cls.cpu().numpy()[idx]
+    ref = oracle_mod.klt_apply(k, xs, cs)
+    check_close(y.cpu().numpy()[idx], ref, xs, "klt multi-tile sample")
+
+
 def test_reference_adapter(cuda):
     """include/hygt_gpu_adapter.hpp driven with the reference's own C++ types (HyGTModel,
     ModelBundle, ResidualDataset, QuantizedHyGTModel, TrigTable) against the reference's own
