@@ -354,6 +354,59 @@ def test_klt_multi_tile_pipeline(cuda, oracle_mod):
     check_close(y.cpu().numpy()[idx], ref, xs, "klt multi-tile sample")
 
 
+@pytest.mark.parametrize("log2n", [5, 6])
+def test_clsjit_steady_state(cuda, oracle_mod, log2n):
+    """Per-class NVRTC chain at a size where each warp runs several batches of its class (the
+    next-batch id / L2 prefetch path): round trip over all rows, a sample against the oracle."""
+    from paper_2505_21728_b200 import HyGTModel
+    rng = np.random.default_rng(21)
+    C, R, n = 6, 3, 1 << log2n  # > 4 classes: N = 32 plans would otherwise take the all-class JIT
+    angles = rng.uniform(-np.pi, np.pi, (C, R * log2n * n // 2))
+    perms = np.stack([np.stack([rng.permutation(n) for _ in range(R)]) for _ in range(C)]).astype(np.uint16)
+    plan = _plan([HyGTModel(log2n, R, angles[c], perms[c, R - 1]) for c in range(C)], perms[:, : R - 1].copy())
+    assert plan.path == "clsjit"
+    rows = (1 << 27) // (4 * n)  # 128 MiB per array
+    cls = torch.from_numpy(rng.integers(0, C, rows).astype(np.uint16)).to(cuda)
+    x = torch.randn(rows, n, device=cuda) * 16
+    y = plan.forward(x, cls)
+    back = plan.inverse(y, cls)
+    plan.sync_status()
+    err = (torch.linalg.vector_norm(back - x) / torch.linalg.vector_norm(x)).item()
+    assert err < 1e-6, err
+    idx = rng.choice(rows, 2048, replace=False)
+    xs, cs = x.cpu().numpy()[idx], cls.cpu().numpy()[idx]
+    ref = oracle_mod.apply_batch(log2n, R, angles, perms, (1 << R) - 1, xs, cs)
+    check_close(y.cpu().numpy()[idx], ref, xs, f"clsjit N={n} steady-state sample")
+
+
+@pytest.mark.parametrize("log2n", [4, 6])
+def test_fixed_jit_steady_state(cuda, oracle_mod, log2n):
+    """Fixed-point NVRTC chain with several batches per warp: bit-exact on a sample, exact
+    first-failing-row report for an oversized input deep in the batch."""
+    from paper_2505_21728_b200 import ArgumentError, FixedPlan, QuantizedHyGTModel, TrigTable
+    rng = np.random.default_rng(22)
+    C, R, n = 4, 3, 1 << log2n
+    a = R * n * log2n // 2
+    codes = rng.integers(0, 256, (C, a)).astype(np.uint16)
+    inter = np.stack([np.stack([rng.permutation(n) for _ in range(R - 1)]) for _ in range(C)]).astype(np.uint16)
+    full = np.concatenate([inter, np.tile(np.arange(n, dtype=np.uint16), (C, 1, 1))], 1)
+    plan = FixedPlan([QuantizedHyGTModel(log2n, R, 8, codes[c]) for c in range(C)], TrigTable(8, 10), inter)
+    rows = (1 << 27) // (8 * n)
+    x = torch.from_numpy(rng.integers(-(1 << 20), (1 << 20) + 1, (rows, n)).astype(np.int64)).to(cuda)
+    cls = torch.from_numpy(rng.integers(0, C, rows).astype(np.uint16)).to(cuda)
+    y = plan.forward(x, cls).cpu().numpy()
+    idx = rng.choice(rows, 2048, replace=False)
+    st, _, ref = oracle_mod.apply_batch_fixed(log2n, R, 8, 10, codes, full, (1 << (R - 1)) - 1,
+                                              x.cpu().numpy()[idx], cls.cpu().numpy()[idx])
+    assert st == 0 and np.array_equal(y[idx], ref)
+    bad = rows - 12345
+    x[bad, 1] = (1 << 20) + 7
+    x[bad + 100, 0] = -(1 << 21)
+    with pytest.raises(ArgumentError):
+        plan.forward(x, cls)
+    assert plan.first_bad == bad
+
+
 def test_reference_adapter(cuda):
     """include/hygt_gpu_adapter.hpp driven with the reference's own C++ types (HyGTModel,
     ModelBundle, ResidualDataset, QuantizedHyGTModel, TrigTable) against the reference's own
