@@ -1587,7 +1587,7 @@ int run_fixed(const hygt_plan* p, int dir, const int64_t* x, int64_t* y, const u
                 p->precision_bits, p->d_codes, p->d_cos, p->d_sin, p->d_fgather[dir],
                 p->gmask[dir], p->d_fixed_err};
   const bool aligned16 = (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0;
-  if (p->fx_jit.ok && aligned16) {
+  if (p->fx_jit.ok && aligned16 && count < 0xFFFFFFFFull) {  // u32 row ids
     const int s = run_fixed_jit(p, dir, x, y, cls, count, first_bad, st);
     if (s != -1) return s;  // -1: invalid class ids -> the exact first failing row from below
     CU(cudaMemcpyAsync(p->d_fixed_err, &init, sizeof(init), cudaMemcpyHostToDevice, st));
