@@ -30,6 +30,7 @@ SegFn select_seg(int variant, bool standard, bool fwd, bool energy) {
     case 7: return pick_seg<8, 2, 1, true>(standard, fwd, energy);
     case 8: return pick_seg<8, 1, 1, false>(standard, fwd, energy);
     case 9: return pick_seg<8, 3, 2, false>(standard, fwd, energy);
+    case 10: return pick_seg<8, 2, 2, false>(standard, fwd, energy);
     default: return nullptr;
   }
 }

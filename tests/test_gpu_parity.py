@@ -58,7 +58,7 @@ TILE_LAYOUTS = {2: [(0, 2)], 3: [(1, 2), (0, 2)], 4: [(1, 2), (2, 2), (0, 1)],
                 5: [(2, 2), (3, 2)]}
 
 
-SEG_VARIANTS = {6: [0, 1, 2, 3], 7: [4, 5], 8: [6, 7, 8, 9]}
+SEG_VARIANTS = {6: [0, 1, 2, 3], 7: [4, 5], 8: [6, 7, 8, 9, 10]}
 STAGE_LOG2N = (4,)
 SEG2_LOG2N = (6,)
 
