@@ -452,7 +452,9 @@ const char* kClsEpilogueDB = R"CUDA(
 // Source of one class's two kernels (hygt_cls_f, hygt_cls_i).
 void emit_body_ptx(std::ostringstream& o, const ClassProgram& pr, int n, bool standard);
 
-std::string generate_class(int log2n, int minb, bool standard, const ClassProgram& fwd, const ClassProgram& inv) {
+// ptx: -1 = HYGT_CLS_PTX decides, 0 / 1 = C++ / PTX class bodies
+std::string generate_class(int log2n, int minb, bool standard, const ClassProgram& fwd, const ClassProgram& inv,
+                           int ptx_mode = -1) {
   const int n = 1 << log2n;
   std::ostringstream o;
   o << "#define N " << n << "\n#define NQ " << n / 4 << "\n#define MINB " << minb << "\n";
@@ -462,7 +464,7 @@ std::string generate_class(int log2n, int minb, bool standard, const ClassProgra
   const bool dbuf = env_on("HYGT_CLS_DB");
   // PTX bodies (HYGT_CLS_PTX=1) skip the NVVM pass: 0.7 s instead of 2.5 s per class, but the
   // N = 64 kernels run 15% slower than NVVM's (profiles/r01/cls_experiments.log), so opt-in
-  const bool ptx = !dbuf && env_on("HYGT_CLS_PTX");
+  const bool ptx = !dbuf && (ptx_mode >= 0 ? ptx_mode == 1 : env_on("HYGT_CLS_PTX"));
   for (int d = 0; d < 2; ++d) {
     o << "#define KNAME " << (d == 0 ? "hygt_cls_f" : "hygt_cls_i") << "\n"
       << (dbuf ? kClsPrologueDB : ptx ? kClsProloguePTX : kClsPrologue);
@@ -1298,11 +1300,7 @@ extern "C" int hygt_debug_jit_compile(int kind, int log2n, int rounds, const dou
     if (log2n == 8) {
       src = generate_class_256(false, progs[0][0], progs[1][0]);
     } else {
-      const char* prev = std::getenv("HYGT_CLS_PTX");
-      const std::string keep = prev ? prev : "";
-      setenv("HYGT_CLS_PTX", ptx ? "1" : "0", 1);
-      src = generate_class(log2n, 16, false, progs[0][0], progs[1][0]);
-      if (prev) setenv("HYGT_CLS_PTX", keep.c_str(), 1); else unsetenv("HYGT_CLS_PTX");
+      src = generate_class(log2n, 16, false, progs[0][0], progs[1][0], ptx ? 1 : 0);
     }
   } else {
     const int n = 1 << log2n;
