@@ -407,6 +407,52 @@ def test_fixed_jit_steady_state(cuda, oracle_mod, log2n):
     assert plan.first_bad == bad
 
 
+@pytest.mark.parametrize("log2n", [4, 6])
+def test_one_plan_two_host_threads(cuda, log2n):
+    """A plan is immutable after creation: two host threads, each with its own stream and
+    workspace, run the same plan concurrently (staged kernel at N = 16, the per-class launch
+    chain at N = 64) and get exactly the results of a serial run."""
+    import threading
+    from paper_2505_21728_b200 import HyGTModel
+    rng = np.random.default_rng(31)
+    C, R, n = 35, 3, 1 << log2n
+    angles = rng.uniform(-np.pi, np.pi, (C, R * log2n * n // 2))
+    perms = np.stack([np.stack([rng.permutation(n) for _ in range(R - 1)]) for _ in range(C)]).astype(np.uint16)
+    plan = _plan([HyGTModel(log2n, R, angles[c]) for c in range(C)], perms)
+    rows = 1 << 18
+    xs = [torch.randn(rows, n, device=cuda) for _ in range(2)]
+    cs = [torch.from_numpy(rng.integers(0, C, rows).astype(np.uint16)).to(cuda) for _ in range(2)]
+    ref = [plan.inverse(plan.forward(xs[i], cs[i]), cs[i]) for i in range(2)]
+    refy = [plan.forward(xs[i], cs[i]) for i in range(2)]
+    torch.cuda.synchronize()
+    out = [None, None]
+    errs = []
+
+    def work(i):
+        try:
+            torch.cuda.set_device(cuda)
+            st = torch.cuda.Stream()
+            ws = torch.zeros(plan.workspace_bytes(rows), dtype=torch.uint8, device=cuda)
+            with torch.cuda.stream(st):
+                for _ in range(5):
+                    y = plan.forward(xs[i], cs[i], stream=st, workspace=ws)
+                    z = plan.inverse(y, cs[i], stream=st, workspace=ws, reuse_buckets=True)
+                st.synchronize()
+            out[i] = (y, z)
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for i in range(2):
+        assert torch.equal(out[i][0], refy[i])
+        assert torch.equal(out[i][1], ref[i])
+
+
 def test_reference_adapter(cuda):
     """include/hygt_gpu_adapter.hpp driven with the reference's own C++ types (HyGTModel,
     ModelBundle, ResidualDataset, QuantizedHyGTModel, TrigTable) against the reference's own
