@@ -43,20 +43,25 @@ struct CorrParams {
   uint64_t cta_span;
 };
 
+// Per chunk, the tile's two row slices are staged once as fp64 (each sample converted once, not
+// once per thread that reads it); the j slice is stored element-interleaved (k = b E + w at
+// w TD + b) so a warp's 16 column threads read 16 consecutive doubles. Diagonal tiles compute
+// only the 4 x 4 blocks on or above the diagonal (the rest is their mirror).
 template <int N>
 __global__ void __launch_bounds__(CORR_THREADS) corr_kernel(const CorrParams P) {
   constexpr int OT = N < 64 ? N : 64;           // output tile side
   constexpr int TD = OT < 16 ? OT : 16;         // threads per tile side
   constexpr int E = OT / TD;                    // accumulators per thread per side
   constexpr int TILES = N / OT;
-  __shared__ __align__(16) float rows[CORR_RT][N];
+  __shared__ __align__(16) double si[CORR_RT][OT];  // rows' samples i0 .. of the tile, natural order
+  __shared__ __align__(16) double sj[CORR_RT][OT];  // samples j0 .., element-interleaved
   // upper block-triangle tile (ti <= tj) of this CTA
   int ti = 0, tj = (int)blockIdx.y;
   while (tj >= TILES - ti) { tj -= TILES - ti; ++ti; }
   tj += ti;
   const int tid = threadIdx.x;
-  const bool active = tid < TD * TD;
   const int a = tid / TD, b = tid % TD;
+  const bool active = tid < TD * TD && (ti != tj || a <= b);
   const int i0 = ti * OT + a * E, j0 = tj * OT + b * E;
 
   const uint64_t beg = (uint64_t)blockIdx.x * P.cta_span;
@@ -85,10 +90,21 @@ __global__ void __launch_bounds__(CORR_THREADS) corr_kernel(const CorrParams P) 
     for (uint64_t r0 = pos; r0 < stop; r0 += CORR_RT) {
       const int nr = (int)(stop - r0 < (uint64_t)CORR_RT ? stop - r0 : (uint64_t)CORR_RT);
       __syncthreads();
-      for (int q = tid; q < nr * (N / 4); q += CORR_THREADS) {  // coalesced 16 B pieces of rows
-        const int r = q / (N / 4), k = q % (N / 4);
+      // coalesced 16 B pieces of the two slices, converted to fp64 once
+      constexpr int Q = OT / 4;
+      for (int q = tid; q < nr * Q * 2; q += CORR_THREADS) {
+        const int half = q / (nr * Q), qq = q % (nr * Q);
+        const int r = qq / Q, k4 = qq % Q;
+        if (half == 1 && ti == tj) continue;  // diagonal tile: one slice serves both sides
         const uint64_t row = P.idx ? (uint64_t)__ldg(P.idx + r0 + r) : r0 + r;
-        reinterpret_cast<float4*>(rows[r])[k] = __ldcs(reinterpret_cast<const float4*>(P.x + row * N) + k);
+        const float4 v = __ldcs(reinterpret_cast<const float4*>(P.x + row * N + (half ? tj : ti) * OT) + k4);
+        const float e4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int k = 4 * k4 + t;
+          if (!half) si[r][k] = (double)e4[t];
+          if (half || ti == tj) sj[r][(k % E) * TD + k / E] = (double)e4[t];
+        }
       }
       __syncthreads();
       if (active)
@@ -96,8 +112,8 @@ __global__ void __launch_bounds__(CORR_THREADS) corr_kernel(const CorrParams P) 
           double xi[E], xj[E];
 #pragma unroll
           for (int u = 0; u < E; ++u) {
-            xi[u] = (double)rows[r][i0 + u];
-            xj[u] = (double)rows[r][j0 + u];
+            xi[u] = si[r][a * E + u];
+            xj[u] = sj[r][u * TD + b];
           }
 #pragma unroll
           for (int u = 0; u < E; ++u)
@@ -107,12 +123,13 @@ __global__ void __launch_bounds__(CORR_THREADS) corr_kernel(const CorrParams P) 
     }
     if (active) {
       double* s = P.sum + (size_t)f * N * N;
+      const bool mirror = ti != tj || a < b;  // diagonal blocks of diagonal tiles hold both halves
 #pragma unroll
       for (int u = 0; u < E; ++u)
 #pragma unroll
         for (int w = 0; w < E; ++w) {
           atomicAdd(s + (size_t)(i0 + u) * N + (j0 + w), acc[u][w]);
-          if (ti != tj) atomicAdd(s + (size_t)(j0 + w) * N + (i0 + u), acc[u][w]);  // mirror
+          if (mirror) atomicAdd(s + (size_t)(j0 + w) * N + (i0 + u), acc[u][w]);
         }
     }
     if (blockIdx.y == 0 && tid == 0) atomicAdd(P.cnt + f, (unsigned long long)(stop - pos));
