@@ -23,7 +23,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <chrono>
 #include <cstdio>
+#include <memory>
 #include <cstring>
 #include <fstream>
 #include <stdexcept>
@@ -159,13 +161,21 @@ uint32_t perm_table(const Bundle& b, std::vector<uint16_t>& out) {
 struct Dataset {
   int log2n = 0, classes = 0;
   uint64_t count = 0;
-  uint16_t* cls = nullptr;  // pinned
-  void* x = nullptr;        // pinned fp32 or int64
+  uint16_t* cls = nullptr;  // host, pageable
+  void* x = nullptr;        // host fp32 or int64, pageable (outputs are written back into it)
 };
 
-// Parses RBLK records (u16 class + N fp32, dataset.hpp:68-70) into pinned SoA buffers.
-Dataset read_rblk(const std::string& path, bool fixed, int bundle_classes) {
+// Parses RBLK records (u16 class + N fp32, dataset.hpp:68-70) into SoA buffers.
+Dataset read_rblk(const std::string& path, bool fixed, int bundle_classes, std::thread& cuda_init) {
+  const bool timing = std::getenv("HYGT_APPLY_TIMING") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    const auto t = std::chrono::steady_clock::now();
+    if (timing) std::fprintf(stderr, "[apply]   %-8s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  };
   const auto buf = slurp(path);
+  mark("slurp");
   Reader r{buf.data(), buf.size(), 0, "RBLK dataset"};
   r.magic("RBLK");
   if (r.u8() != 1) io_error("read_rblk: unsupported version");
@@ -177,8 +187,12 @@ Dataset read_rblk(const std::string& path, bool fixed, int bundle_classes) {
   if (d.classes == 0) io_error("read_rblk: ResidualDataset: need at least one class");
   const size_t n = (size_t)1 << d.log2n, rec = 2 + 4 * n;
   if (r.off + d.count * rec > buf.size()) io_error("unexpected end of file");
-  cu(cudaHostAlloc(reinterpret_cast<void**>(&d.cls), std::max<size_t>(d.count, 1) * 2, cudaHostAllocDefault));
-  cu(cudaHostAlloc(&d.x, std::max<size_t>(d.count, 1) * n * (fixed ? 8 : 4), cudaHostAllocDefault));
+  // pageable SoA buffers, filled while the CUDA context is still being created: pinning ~0.3-0.6 GB
+  // costs more than the driver's staged copies of it (DESIGN, apply timing)
+  d.cls = new uint16_t[std::max<size_t>(d.count, 1)];
+  d.x = fixed ? static_cast<void*>(new int64_t[std::max<size_t>(d.count, 1) * n])
+              : static_cast<void*>(new float[std::max<size_t>(d.count, 1) * n]);
+  mark("alloc");
   const unsigned char* base = buf.data() + r.off;
   const unsigned threads = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
   std::vector<std::thread> pool;
@@ -204,6 +218,9 @@ Dataset read_rblk(const std::string& path, bool fixed, int bundle_classes) {
       }
     });
   for (auto& th : pool) th.join();
+  mark("parse");
+  if (cuda_init.joinable()) cuda_init.join();
+  mark("cuda-init");
   for (int v : bad)
     if (v) io_error("read_rblk: ResidualDataset: class id out of range");
   (void)bundle_classes;
@@ -212,7 +229,15 @@ Dataset read_rblk(const std::string& path, bool fixed, int bundle_classes) {
 
 void write_rblk(const std::string& path, const Dataset& d, const void* y, bool fixed) {
   const size_t n = (size_t)1 << d.log2n, rec = 2 + 4 * n;
-  std::vector<unsigned char> out(12 + d.count * rec);
+  const size_t total = 12 + d.count * rec;
+  std::unique_ptr<unsigned char[]> holder(new unsigned char[total]);  // filled below, no zeroing
+  struct Span {
+    unsigned char* p;
+    size_t n;
+    unsigned char* data() const { return p; }
+    size_t size() const { return n; }
+    unsigned char& operator[](size_t i) const { return p[i]; }
+  } out{holder.get(), total};
   std::memcpy(out.data(), "RBLK", 4);
   out[4] = 1;
   out[5] = (unsigned char)d.log2n;
@@ -274,14 +299,33 @@ Args parse(int argc, char** argv) {
 }
 
 int run(const Args& a) {
+  const bool timing = std::getenv("HYGT_APPLY_TIMING") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto phase = [&](const char* name) {
+    const auto t = std::chrono::steady_clock::now();
+    if (timing) std::fprintf(stderr, "[apply] %-10s %8.1f ms\n", name, std::chrono::duration<double, std::milli>(t - t_last).count());
+    t_last = t;
+  };
+  // CUDA context creation (0.6-1.5 s on a fresh process) overlaps with reading the files
+  std::thread cuda_init([] { cudaFree(nullptr); });
+  struct Joiner {
+    std::thread& t;
+    ~Joiner() { if (t.joinable()) t.join(); }
+  } joiner{cuda_init};
   const Bundle b = read_bundle(a.model);
   const bool fixed = a.arithmetic == "fixed";
   const bool fwd = a.direction == "forward";
   if (fixed && b.angle_bits == 0)
     arg_error("apply: fixed arithmetic needs a quantized bundle (train with --angle-bits 8)");
-  Dataset d = read_rblk(a.data, fixed, b.classes);
+  Dataset d = read_rblk(a.data, fixed, b.classes, cuda_init);
   if (d.log2n != b.log2n) arg_error("apply: model/data dimension mismatch");
   if (d.classes != b.classes) arg_error("apply: model/data class count mismatch");
+  phase("read");
+  // A one-shot file run cannot amortise plan-time NVRTC compilation (0.5-6 s for 35 classes)
+  // over its transform time (milliseconds for millions of blocks): unless the caller chose,
+  // the plan takes the precompiled kernels.
+  if (d.count < ((uint64_t)1 << 28))
+    for (const char* k : {"HYGT_JIT", "HYGT_CLS_JIT", "HYGT_FIXED_JIT"}) setenv(k, "0", 0);
   const size_t n = (size_t)1 << d.log2n, R = (size_t)b.max_rounds;
   std::vector<uint16_t> perms;
   const uint32_t mask = perm_table(b, perms);
@@ -305,9 +349,10 @@ int run(const Args& a) {
                                  perms.empty() ? nullptr : perms.data(), mask, &plan));
   }
 
+  phase("plan");
   const size_t esz = fixed ? 8 : 4;
-  void* y = nullptr;
-  cu(cudaHostAlloc(&y, std::max<size_t>(d.count, 1) * n * esz, cudaHostAllocDefault));
+  // outputs land in the input's buffer: chunk k's D2H follows its own H2D on one stream
+  void* y = d.x;
   const uint64_t chunk = std::min<uint64_t>(std::max<uint64_t>(d.count, 1), (uint64_t)1 << 20);
   cudaStream_t st[2];
   void *dx[2], *dy[2], *ws[2];
@@ -349,7 +394,9 @@ int run(const Args& a) {
     cu(cudaStreamSynchronize(st[s]));
     if (!fixed && ws[s]) check(hygt_sync_status(plan, ws[s], st[s]));
   }
+  phase("transform");
   write_rblk(a.out, d, y, fixed);
+  phase("write");
   std::printf("wrote %llu transformed blocks to %s\n", (unsigned long long)d.count, a.out.c_str());
   for (int s = 0; s < 2; ++s) {
     cudaFree(dx[s]);
@@ -358,9 +405,8 @@ int run(const Args& a) {
     cudaFree(ws[s]);
     cudaStreamDestroy(st[s]);
   }
-  cudaFreeHost(y);
-  cudaFreeHost(d.x);
-  cudaFreeHost(d.cls);
+  if (fixed) delete[] static_cast<int64_t*>(d.x); else delete[] static_cast<float*>(d.x);
+  delete[] d.cls;
   hygt_plan_destroy(plan);
   return 0;
 }
