@@ -417,11 +417,7 @@ int run_bucket(const hygt_plan* p, int classes, uint64_t chunk_rows, const uint1
                                                       w.tiles_per_chunk, classes, count);
   CU(cudaGetLastError());
   const size_t smem_sc = (size_t)(((classes + 2 + 3) & ~3) + ((classes + 1 + 3) & ~3)) * 4 + BK_TILE * 4;
-  static bool attr_set = false;
-  if (!attr_set) {
-    smem_attr(bucket_scatter_kernel, 112 * 1024);
-    attr_set = true;
-  }
+  smem_attr(bucket_scatter_kernel, 112 * 1024);  // thread-safe, idempotent
   bucket_scatter_kernel<<<w.tiles, BK_THREADS, smem_sc, st>>>(d_cls, count, classes, base, w.tiles, idx);
   CU(cudaGetLastError());
   return ok();
