@@ -11,6 +11,8 @@ from __future__ import annotations
 import ctypes as C
 from typing import Optional, Sequence, Union
 
+import threading
+
 import numpy as np
 import torch
 
@@ -71,13 +73,31 @@ def _perm_table(models, rounds: int, n: int, inter_round_perms):
 
 
 class _Workspace:
-    def __init__(self):
-        self.buf = None
+    """Default device workspaces of a plan, one per (host thread, device, stream): calls that share
+    a workspace must be stream-ordered, so concurrent callers that pass none never share one."""
 
-    def get(self, nbytes: int, device) -> torch.Tensor:
-        if self.buf is None or self.buf.numel() < nbytes or self.buf.device != device:
-            self.buf = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
-        return self.buf
+    def __init__(self):
+        self.bufs = {}
+        self.lock = threading.Lock()
+
+    def get(self, nbytes: int, device, stream=None) -> torch.Tensor:
+        key = (threading.get_ident(), str(device), _stream_ptr(stream))
+        with self.lock:
+            buf = self.bufs.get(key)
+            if buf is None or buf.numel() < nbytes:
+                buf = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
+                self.bufs[key] = buf
+            return buf
+
+    def find(self, stream=None) -> Optional[torch.Tensor]:
+        """This thread's workspace on `stream` (the current stream by default), if any."""
+        sp = _stream_ptr(stream)
+        tid = threading.get_ident()
+        with self.lock:
+            for (t, _, s), buf in self.bufs.items():
+                if t == tid and s == sp:
+                    return buf
+        return None
 
 
 class HyGTPlan:
@@ -157,7 +177,7 @@ class HyGTPlan:
     def _run(self, fn, x, cls, out, stream, workspace, reuse_buckets, energy=None):
         count, out = self._prep(x, cls, out)
         nbytes = self.workspace_bytes(count)
-        ws = workspace if workspace is not None else self._ws.get(nbytes, x.device)
+        ws = workspace if workspace is not None else self._ws.get(nbytes, x.device, stream)
         flags = HYGT_REUSE_BUCKETS if reuse_buckets else 0
         args = [self._h, x.data_ptr(), out.data_ptr(), _dev_ptr(cls), count]
         if energy is not None:
@@ -188,7 +208,7 @@ class HyGTPlan:
 
     def sync_status(self, workspace=None, stream=None):
         """Synchronise and raise the device-recorded error (invalid class ids) if any."""
-        ws = workspace if workspace is not None else self._ws.buf
+        ws = workspace if workspace is not None else self._ws.find(stream)
         _check(_lib.lib().hygt_sync_status(self._h, _dev_ptr(ws), _stream_ptr(stream)))
 
     # ---- end-to-end on host buffers (the run_apply call a user makes) ----------------------

@@ -407,8 +407,9 @@ def test_fixed_jit_steady_state(cuda, oracle_mod, log2n):
     assert plan.first_bad == bad
 
 
+@pytest.mark.parametrize("default_ws", [False, True])
 @pytest.mark.parametrize("log2n", [4, 6])
-def test_one_plan_two_host_threads(cuda, log2n):
+def test_one_plan_two_host_threads(cuda, log2n, default_ws):
     """A plan is immutable after creation: two host threads, each with its own stream and
     workspace, run the same plan concurrently (staged kernel at N = 16, the per-class launch
     chain at N = 64) and get exactly the results of a serial run."""
@@ -432,12 +433,13 @@ def test_one_plan_two_host_threads(cuda, log2n):
         try:
             torch.cuda.set_device(cuda)
             st = torch.cuda.Stream()
-            ws = torch.zeros(plan.workspace_bytes(rows), dtype=torch.uint8, device=cuda)
+            # explicit workspaces, or the plan's defaults (one per host thread and stream)
+            ws = None if default_ws else torch.zeros(plan.workspace_bytes(rows), dtype=torch.uint8, device=cuda)
             with torch.cuda.stream(st):
                 for _ in range(5):
                     y = plan.forward(xs[i], cs[i], stream=st, workspace=ws)
                     z = plan.inverse(y, cs[i], stream=st, workspace=ws, reuse_buckets=True)
-                st.synchronize()
+                plan.sync_status(ws, stream=st)
             out[i] = (y, z)
         except Exception as e:  # surfaced below
             errs.append(e)
