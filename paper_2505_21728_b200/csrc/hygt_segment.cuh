@@ -55,6 +55,8 @@ __global__ void __launch_bounds__(THREADS, (LOG2N >= 8 ? 1 : 2)) hygt_segment_ke
   constexpr int ROWS = V * VPT;
   constexpr int WARPS = THREADS / 32;
   constexpr int S = G::template stride<VPT>();
+  // energy by shuffle reduce-scatter (lanes per row >= 4, at least one full group per lane)
+  constexpr bool SEG_RS = L >= 2 && E >= (2 << (5 - L));
   extern __shared__ __align__(16) unsigned char seg_smem[];
   const int C = P.classes;
   const uint32_t cw = P.units * TPV;                                   // float4 per class
@@ -177,12 +179,48 @@ __global__ void __launch_bounds__(THREADS, (LOG2N >= 8 ? 1 : 2)) hygt_segment_ke
         for (int u = 0; u < E / G::CH; ++u)
           __stcs(yr + t + TPV * u,
                  make_float4(v[r][2 * u].x, v[r][2 * u].y, v[r][2 * u + 1].x, v[r][2 * u + 1].y));
-        if constexpr (ENERGY) {
+        if constexpr (ENERGY && !SEG_RS) {
 #pragma unroll
           for (int k = 0; k < NP; ++k) {
             s_acc[(2 * k) * 32] = fmaf(v[r][k].x, v[r][k].x, s_acc[(2 * k) * 32]);
             s_acc[(2 * k + 1) * 32] = fmaf(v[r][k].y, v[r][k].y, s_acc[(2 * k + 1) * 32]);
           }
+        }
+      }
+      if constexpr (ENERGY && SEG_RS) {
+        // y^2 of the warp's rows reduce-scattered over the row-group lane bits with shuffles, in
+        // groups of GS slots: each lane adds 2 sums per group to its partials (instead of one
+        // shared-memory read-modify-write per sample and row)
+        constexpr int S = 5 - L, GS = 2 << S;
+#pragma unroll
+        for (int g0 = 0; g0 < E; g0 += GS) {
+          float q[GS];
+#pragma unroll
+          for (int i = 0; i < GS; ++i) {
+            float acc = 0.f;
+#pragma unroll
+            for (int r = 0; r < VPT; ++r)
+              if (ok[r]) {
+                const float e = ((g0 + i) & 1) ? v[r][(g0 + i) >> 1].y : v[r][(g0 + i) >> 1].x;
+                acc = fmaf(e, e, acc);
+              }
+            q[i] = acc;
+          }
+          int m = GS, off = 0;
+#pragma unroll
+          for (int o = 16; o >= TPV; o >>= 1) {  // lanes with bit o keep the upper half
+            m >>= 1;
+            const bool up = (lane & o) != 0;
+#pragma unroll
+            for (int i = 0; i < m; ++i) {
+              const float send = up ? q[i] : q[i + m];
+              const float keep = up ? q[i + m] : q[i];
+              q[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+            off += up ? m : 0;
+          }
+          s_acc[(g0 + off) * 32] += q[0];
+          s_acc[(g0 + off + 1) * 32] += q[1];
         }
       }
       if constexpr (ENERGY) {
