@@ -740,7 +740,8 @@ int setup_stage(hygt_plan* p, const double* angles, const uint16_t* perms) {
   p->stage_rows = T;
   p->stage_cw = cw;
   p->stage_block_words = stage_block_words(T, STAGE_VPT, C);
-  smem_attr(select_stage_sort(), (int)(STAGE_SORT_WARPS * stage_sort_warp_bytes(C, p->stage_block_words)));
+  for (uint32_t t : {7u * 128u, 8u * 128u})
+    smem_attr(select_stage_sort(STAGE_VPT, t), (int)(STAGE_SORT_WARPS * stage_sort_warp_bytes(C, p->stage_block_words)));
   cudaGetLastError();
   return HYGT_OK;
 }
@@ -764,7 +765,7 @@ int stage_sort(int classes, uint32_t T, uint32_t block_words, int vpt, int num_s
   S.ent = reinterpret_cast<uint16_t*>(static_cast<char*>(d_ws) + 256);
   S.err = static_cast<uint32_t*>(d_ws);
   const uint64_t tiles = (count + T - 1) / T;
-  StageSortFn fn = select_stage_sort(vpt);
+  StageSortFn fn = select_stage_sort(vpt, T);
   const size_t smem = (size_t)STAGE_SORT_WARPS * stage_sort_warp_bytes(classes, block_words);
   if (smem > 48 * 1024) smem_attr(fn, (int)smem);
   int occ = 0;

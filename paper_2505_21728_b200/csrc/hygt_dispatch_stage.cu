@@ -17,8 +17,11 @@ StageFn select_stage(int log2n, bool standard, bool fwd, bool benes, bool debug)
   return benes ? stage_variant<STAGE_VAR_BENES>(standard, fwd) : stage_variant<0>(standard, fwd);
 }
 
-StageSortFn select_stage_sort(int vpt) {
-  return vpt == 2 ? hygt_stage_sort_kernel<2> : hygt_stage_sort_kernel<STAGE_VPT>;
+StageSortFn select_stage_sort(int vpt, uint32_t tile_rows) {
+  // slot groups of 128 ids per warp: only as many as the tile needs (T = 784 -> 7, not 8)
+  const bool seven = tile_rows <= 7 * 128;
+  if (vpt == 2) return seven ? hygt_stage_sort_kernel<2, 7> : hygt_stage_sort_kernel<2, 8>;
+  return seven ? hygt_stage_sort_kernel<STAGE_VPT, 7> : hygt_stage_sort_kernel<STAGE_VPT, 8>;
 }
 
 StageFxFn select_stage_fixed(int log2n, bool fwd) {

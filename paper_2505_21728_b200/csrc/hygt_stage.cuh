@@ -356,10 +356,9 @@ HYGT_HD constexpr uint32_t stage_sort_warp_bytes(int classes, uint32_t block_wor
   return stage_align((uint32_t)(3 * classes + 1) * 4u, 16) + stage_align((block_words - 8) * 2u, 16);
 }
 
-template <int VPT>
+template <int VPT, int H>  // H groups of 4 consecutive ids per lane: T <= 128 H
 __global__ void __launch_bounds__(32 * STAGE_SORT_WARPS) hygt_stage_sort_kernel(const StageSortParams P) {
   constexpr int BATCH = 32 * VPT;
-  constexpr int H = 1024 / 128;  // groups of 4 consecutive ids per lane (T <= 1024)
   extern __shared__ __align__(16) unsigned char sm[];
   const int C = P.classes;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
