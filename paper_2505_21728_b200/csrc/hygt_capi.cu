@@ -1777,7 +1777,7 @@ extern "C" int hygt_fixed_plan_create(int log2_n, int rounds, int class_count, i
     free_plan(p);
     return s;
   }
-  if (!s && jit_fixed_supported(log2_n, rounds) && env_int("HYGT_FIXED_JIT", 1) != 0) {
+  if (!s && jit_fixed_supported(log2_n, rounds, class_count) && env_int("HYGT_FIXED_JIT", 1) != 0) {
     std::string err;
     if (jit_fixed_build(log2_n, rounds, class_count, angle_bits, precision_bits, codes, ct.data(), sn.data(),
                         perms, p->perm_mask, p->fx_jit, err))

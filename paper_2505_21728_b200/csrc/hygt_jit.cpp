@@ -1170,7 +1170,15 @@ int load_class_modules(const std::vector<std::string>& srcs, JitClsKernels& out,
 
 
 
+// One NVRTC module per class: plans with very many classes would spend minutes compiling, so the
+// per-class chains are limited to HYGT_CLS_JIT_MAX_CLASSES (default 64) classes.
+int max_jit_classes() {
+  const char* v = std::getenv("HYGT_CLS_JIT_MAX_CLASSES");
+  return v && *v ? std::atoi(v) : 64;
+}
+
 bool jit_cls_supported(int log2n, int classes, int rounds) {
+  if (classes > max_jit_classes()) return false;
   // N = 16 rows (64 B) are half a 128 B line: gathered per class they cost twice the staged
   // kernel's time (profiles/r01/cls_experiments.log), so N = 16 is opt-in (experiments only).
   // N = 256: correct, but 131 KB of straight-line code per class and direction thrashes the
@@ -1231,7 +1239,8 @@ int jit_cls_launch(const JitClsKernels& k, int dir, const float* x, float* y, co
   return 0;
 }
 
-bool jit_fixed_supported(int log2n, int rounds) {
+bool jit_fixed_supported(int log2n, int rounds, int classes) {
+  if (classes > max_jit_classes()) return false;
   return log2n >= 4 && log2n <= 6 && rounds >= 1 && rounds * log2n <= 32 && !env_off("HYGT_FIXED_JIT");
 }
 

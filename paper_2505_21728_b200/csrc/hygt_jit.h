@@ -55,7 +55,7 @@ int jit_cls_launch(const JitClsKernels& k, int dir, const float* x, float* y, co
 // The same chain for fixed-point plans (int64 rows, bit-exact with forward_fixed/inverse_fixed):
 // per-class kernels with the (c, s) TrigTable pairs as immediates. idx == nullptr: one launch
 // of class 0's kernels over rows [0, count) in order.
-bool jit_fixed_supported(int log2n, int rounds);
+bool jit_fixed_supported(int log2n, int rounds, int classes);
 int jit_fixed_build(int log2n, int rounds, int classes, int angle_bits, int precision_bits,
                     const uint16_t* codes, const int32_t* ct, const int32_t* sn, const uint16_t* perms,
                     uint32_t perm_mask, JitClsKernels& out, std::string& err);
