@@ -455,6 +455,22 @@ def test_one_plan_two_host_threads(cuda, log2n, default_ws):
         assert torch.equal(out[i][1], ref[i])
 
 
+def test_many_classes_skip_per_class_jit(cuda, oracle_mod):
+    """Plans with more classes than HYGT_CLS_JIT_MAX_CLASSES (64) stay on the precompiled
+    kernels (no per-class NVRTC modules) and still match the oracle."""
+    from paper_2505_21728_b200 import HyGTModel
+    rng = np.random.default_rng(41)
+    C, R, n = 70, 2, 64
+    angles = rng.uniform(-np.pi, np.pi, (C, R * 6 * 32))
+    plan = _plan([HyGTModel(6, R, angles[c]) for c in range(C)])
+    assert plan.path in ("cls", "seg2")  # parameter-table chain or thread-per-row kernel
+    x = (rng.standard_normal((5000, n)) * 16).astype(np.float32)
+    cls = rng.integers(0, C, 5000).astype(np.uint16)
+    y = plan.forward(torch.from_numpy(x).to(cuda), torch.from_numpy(cls).to(cuda))
+    plan.sync_status()
+    check_close(y.cpu().numpy(), oracle_mod.apply_batch(6, R, angles, None, 0, x, cls), x, "70 classes")
+
+
 def test_reference_adapter(cuda):
     """include/hygt_gpu_adapter.hpp driven with the reference's own C++ types (HyGTModel,
     ModelBundle, ResidualDataset, QuantizedHyGTModel, TrigTable) against the reference's own
