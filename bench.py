@@ -178,6 +178,18 @@ def run_reference_sample(w, rows, threads, data=None):
     return time.perf_counter() - t0
 
 
+def cpu_model() -> str:
+    """Host CPU model (SURVEY 8 d4 asks for it next to the core count)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_sample_rows(n, threads, seconds=1.0):
     """Rows for a bounded CPU sample: the reference does ~3e5 (N=16) / 3e4 (N=64) / 4e3 (N=256)
     fwd+inv rows/s per core, so this is about `seconds` of work on `threads` cores."""
@@ -209,6 +221,7 @@ def impl_reference(args):
         "config": {"workload": w.cfg.name, "rows_sampled": rows, "N": w.n,
                    "classes": w.cfg.classes, "rounds": w.cfg.rounds},
         "cpu_baseline": {"value": v, "unit": "vectors/s", "cores": threads, "kind": "reference",
+                         "cpu_model": cpu_model(),
                          "sample": f"{rows} rows of {w.cfg.name}, hygt::forward+hygt::inverse per row "
                                    f"(unmodified reference headers, g++ -O2), {threads} std::threads"},
         "e2e": {"value": v, "unit": "vectors/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -398,6 +411,7 @@ def impl_ours(args):
         srows = cpu_sample_rows(w.n, threads, seconds=5.0)
         t = run_reference_sample(w, srows, threads)
         cpu = {"value": srows / t, "unit": "vectors/s", "cores": threads, "kind": "reference",
+               "cpu_model": cpu_model(),
                "sample": f"{srows} rows of {w.cfg.name}: hygt::forward+hygt::inverse per row "
                          f"(unmodified reference headers via oracle/_ref, g++ -O2), {threads} threads"}
     del plan, x, cls
