@@ -471,6 +471,26 @@ def test_many_classes_skip_per_class_jit(cuda, oracle_mod):
     check_close(y.cpu().numpy(), oracle_mod.apply_batch(6, R, angles, None, 0, x, cls), x, "70 classes")
 
 
+@pytest.mark.parametrize("config", [1, 2, 5])
+def test_synthetic_rows_follow_ar1_covariance(cuda, config):
+    """The device generator's rows have the separable AR(1) covariance sigma^2 (A kron A)
+    (statistics.hpp:287-305), checked at 5% as test_statistics.cpp:61-70 checks sample_residuals
+    (SURVEY 8 d3); config 2 per class (rho_c), on its most populated class."""
+    from paper_2505_21728_b200.synth import make_workload
+    from test_oracle import _ar1_2d
+    w = make_workload(config)
+    rows = {1: 1 << 19, 2: 1 << 21, 5: 1 << 17}[config]
+    cls = w.make_classes(rows)
+    x = w.make_rows(rows, cls).double()
+    c = 0
+    if w.cfg.rho is None:  # per-class rho: one class's rows
+        c = int(torch.bincount(cls.to(torch.int64)).argmax().item())
+        x = x[cls.to(torch.int64) == c]
+    emp = (x.T @ x / x.shape[0]).cpu().numpy()
+    ref = _ar1_2d(w.block_size(), float(w.rho[c]), w.cfg.sigma)
+    assert np.abs(emp - ref).max() <= 0.05 * np.abs(ref).max()
+
+
 def test_reference_adapter(cuda):
     """include/hygt_gpu_adapter.hpp driven with the reference's own C++ types (HyGTModel,
     ModelBundle, ResidualDataset, QuantizedHyGTModel, TrigTable) against the reference's own

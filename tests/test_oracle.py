@@ -255,3 +255,24 @@ def test_optimizer_oracle_errors(oracle_mod):
         oracle_mod.optimize(np.diag([1.0, -1.0]), 1, 1)
     with pytest.raises(ValueError):
         oracle_mod.optimize(np.eye(4), 2, 1, restarts=0)
+
+
+def _ar1_2d(bs, rho, sigma=1.0):
+    """sigma^2 (A kron A), A_ij = rho^|i-j|, raster order: statistics.hpp:287-305 restated."""
+    i = np.arange(bs)
+    a = rho ** np.abs(i[:, None] - i[None, :])
+    return sigma * sigma * np.kron(a, a)
+
+
+@pytest.mark.parametrize("bs,rho", [(4, 0.9), (8, 0.6), (2, 0.95)])
+def test_ar1_covariance_formula_matches_reference(bs, rho):
+    """The separable AR(1) covariance the synthetic rows follow is the reference's
+    ar1_covariance_2d, checked through the unmodified reference where it is built."""
+    from oracle import oracle as O
+    try:
+        lib = O.ref()
+    except Exception:
+        pytest.skip("oracle/_ref not built")
+    out = np.zeros((bs * bs, bs * bs))
+    lib.ref_ar1_covariance_2d(bs, rho, out.ctypes.data)
+    np.testing.assert_allclose(_ar1_2d(bs, rho), out, rtol=1e-12, atol=1e-15)
