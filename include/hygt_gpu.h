@@ -73,7 +73,8 @@ int hygt_last_error(char* buf, size_t len);
  *          perm_mask is set. Bit rounds-1 is the reference's final sorting permutation;
  *          lower bits are the inter-round permutations of the BASELINE configs. Every present
  *          permutation must be a bijection (model.hpp:37-44).
- * Supported on the GPU: 1 <= log2_n <= 8, rounds >= 1, 1 <= class_count <= 4096. */
+ * Supported on the GPU: 1 <= log2_n <= 8, rounds >= 1 (rounds <= 32 when perms are given),
+ * 1 <= class_count <= 4096. */
 int hygt_plan_create(int log2_n, int rounds, int class_count, const double* angles,
                      const uint16_t* perms, uint32_t perm_mask, uint32_t flags,
                      hygt_plan** out);
@@ -103,7 +104,10 @@ int hygt_plan_algorithm(const hygt_plan* plan);
  *     N = 32 / 64 plans run on the tile / segment kernels instead. */
 int hygt_plan_path(const hygt_plan* plan);
 
-/* Device workspace for class bucketing of `count` rows. */
+/* Device workspace for class bucketing of `count` rows. The first word of a workspace is the
+ * device-side error word that the kernels OR into and hygt_sync_status() reads and clears: a
+ * workspace must be ZERO-INITIALISED (cudaMemset) before its first use, and may then be reused
+ * by any number of stream-ordered calls. */
 size_t hygt_workspace_bytes(const hygt_plan* plan, uint64_t count);
 /* Groups rows by class (histogram + scan + scatter into the workspace). The transforms call it
  * themselves unless HYGT_REUSE_BUCKETS is passed. Invalid class ids are recorded and reported

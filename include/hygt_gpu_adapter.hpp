@@ -27,6 +27,8 @@
 #include "hygt/model.hpp"
 #include "hygt/optimizer.hpp"
 #include "hygt/statistics.hpp"
+#include <algorithm>
+
 #include "hygt_gpu.h"
 
 namespace hygt::gpu {
@@ -57,12 +59,19 @@ struct DeviceBuffer {
   ~DeviceBuffer() { cudaFree(p); }
   DeviceBuffer(const DeviceBuffer&) = delete;
   DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  // Grows the buffer. New storage is zeroed: the transforms only ever OR error bits into a
+  // workspace's first word (hygt_workspace_bytes), so a recycled allocation must not carry
+  // stale bits. A pending error word of the old buffer is carried over.
   void resize(std::size_t count) {
     if (count <= n) return;
+    T* q = nullptr;
+    if (count) {
+      cuda_check(cudaMalloc(reinterpret_cast<void**>(&q), count * sizeof(T)));
+      cuda_check(cudaMemset(q, 0, count * sizeof(T)));
+      if (p) cuda_check(cudaMemcpy(q, p, std::min<std::size_t>(n * sizeof(T), 16), cudaMemcpyDeviceToDevice));
+    }
     cudaFree(p);
-    p = nullptr;
-    n = 0;
-    if (count) cuda_check(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)));
+    p = q;
     n = count;
   }
 };

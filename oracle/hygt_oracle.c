@@ -141,6 +141,75 @@ void hygt_oracle_run_passes(int log2_n, int rounds, const double* angles, double
   }
 }
 
+/* The same passes with (cos t, sin t) read from a table cs[A][2] computed once per class and
+ * direction by hygt_oracle_trig_pairs (t = +theta forward, -theta inverse). cos and sin are
+ * deterministic functions, so the result is bit-identical to hygt_oracle_run_passes; the batch
+ * drivers use it ("hoisted trig") only to make full-size checks affordable, and
+ * tests/test_oracle.py pins the two modes against each other. */
+void hygt_oracle_run_passes_cs(int log2_n, int rounds, const double* cs, double* x, int dir) {
+  const size_t half = (size_t)1 << (log2_n - 1);
+  const int fwd = dir > 0;
+  for (int step = 0; step < rounds * log2_n; ++step) {
+    const int r = fwd ? step / log2_n : rounds - 1 - step / log2_n;
+    const int p = fwd ? step % log2_n : log2_n - 1 - step % log2_n;
+    const uint32_t k = 1u << p;
+    const size_t base = ((size_t)r * log2_n + p) * half; /* model.hpp:77-79 */
+    for (uint32_t j = 0; j < half; ++j) {
+      const uint32_t m = j + (j & (0u - k));
+      const uint32_t n = m + k;
+      const double c = cs[2 * (base + j)], s = cs[2 * (base + j) + 1];
+      const double a = x[m], b = x[n];
+      x[m] = c * a + s * b;
+      x[n] = c * b - s * a;
+    }
+  }
+}
+
+void hygt_oracle_trig_pairs(size_t count, const double* angles, int dir, double* cs) {
+  for (size_t i = 0; i < count; ++i) {
+    const double t = dir > 0 ? angles[i] : -angles[i];
+    cs[2 * i] = cos(t);
+    cs[2 * i + 1] = sin(t);
+  }
+}
+
+static void oracle_gather(size_t n, const uint16_t* perm, double* x) {
+  double local[256];
+  double* heap = n <= 256 ? NULL : (double*)malloc(n * sizeof(double));
+  double* buf = heap ? heap : local;
+  memcpy(buf, x, n * sizeof(double));
+  for (size_t i = 0; i < n; ++i) x[i] = buf[perm[i]];
+  free(heap);
+}
+
+static void oracle_scatter(size_t n, const uint16_t* perm, double* x) {
+  double local[256];
+  double* heap = n <= 256 ? NULL : (double*)malloc(n * sizeof(double));
+  double* buf = heap ? heap : local;
+  memcpy(buf, x, n * sizeof(double));
+  for (size_t i = 0; i < n; ++i) x[perm[i]] = buf[i];
+  free(heap);
+}
+
+/* forward_chain / inverse_chain (below) with tabled trig: cs is the class's [A][2] table of the
+ * direction. */
+static void chain_cs(int log2_n, int rounds, const double* cs, const uint16_t* perms,
+                     uint32_t perm_mask, double* x, int inverse) {
+  const size_t n = (size_t)1 << log2_n;
+  const size_t a1 = n / 2 * (size_t)log2_n;
+  if (!inverse) {
+    for (int r = 0; r < rounds; ++r) {
+      hygt_oracle_run_passes_cs(log2_n, 1, cs + 2 * (size_t)r * a1, x, +1);
+      if (perms && ((perm_mask >> r) & 1u)) oracle_gather(n, perms + (size_t)r * n, x);
+    }
+  } else {
+    for (int r = rounds - 1; r >= 0; --r) {
+      if (perms && ((perm_mask >> r) & 1u)) oracle_scatter(n, perms + (size_t)r * n, x);
+      hygt_oracle_run_passes_cs(log2_n, 1, cs + 2 * (size_t)r * a1, x, -1);
+    }
+  }
+}
+
 /* transform.hpp:72-82: passes, then gather out[i] = pre[perm[i]]. */
 void hygt_oracle_forward(int log2_n, int rounds, const double* angles, const uint16_t* perm,
                          double* x) {
@@ -222,6 +291,7 @@ typedef struct {
   double* y;        /* apply: [count][N]; NULL for energy */
   double* energy;   /* energy: private [classes][N] accumulator */
   int bad;
+  const double* cs; /* NULL: per-butterfly cos/sin; else [classes][A][2] tables (hoisted trig) */
 } batch_job;
 
 static void* batch_worker(void* arg) {
@@ -238,7 +308,9 @@ static void* batch_worker(void* arg) {
     for (size_t i = 0; i < n; ++i) v[i] = (double)j->x[row * n + i]; /* dataset.hpp:106 */
     const double* ang = j->angles + (size_t)c * a;
     const uint16_t* pp = j->perms ? j->perms + (size_t)c * (size_t)j->rounds * n : NULL;
-    if (j->inverse)
+    if (j->cs)
+      chain_cs(j->log2_n, j->rounds, j->cs + 2 * (size_t)c * a, pp, j->perm_mask, v, j->inverse);
+    else if (j->inverse)
       hygt_oracle_inverse_chain(j->log2_n, j->rounds, ang, pp, j->perm_mask, v);
     else
       hygt_oracle_forward_chain(j->log2_n, j->rounds, ang, pp, j->perm_mask, v);
@@ -279,23 +351,52 @@ static int run_jobs(batch_job* proto, uint64_t count, int threads, int energy) {
   return bad ? HYGT_ORACLE_ARGUMENT : HYGT_ORACLE_OK;
 }
 
+static double* class_tables(int log2_n, int rounds, int classes, const double* angles, int inverse) {
+  const size_t a = hygt_oracle_num_parameters(log2_n, rounds);
+  double* cs = (double*)malloc((size_t)classes * a * 2 * sizeof(double));
+  if (cs) hygt_oracle_trig_pairs((size_t)classes * a, angles, inverse ? -1 : +1, cs);
+  return cs;
+}
+
+int hygt_oracle_apply_batch2(int log2_n, int rounds, int classes, const double* angles,
+                             const uint16_t* perms, uint32_t perm_mask, const float* x,
+                             const uint16_t* cls, uint64_t count, int inverse, double* y,
+                             int threads, int hoist_trig) {
+  double* cs = hoist_trig ? class_tables(log2_n, rounds, classes, angles, inverse) : NULL;
+  batch_job p = {log2_n, rounds, classes, angles, perms, perm_mask, x, cls, 0, count,
+                 inverse, y, NULL, 0, cs};
+  const int st = run_jobs(&p, count, threads, 0);
+  free(cs);
+  return st;
+}
+
 int hygt_oracle_apply_batch(int log2_n, int rounds, int classes, const double* angles,
                             const uint16_t* perms, uint32_t perm_mask, const float* x,
                             const uint16_t* cls, uint64_t count, int inverse, double* y,
                             int threads) {
+  return hygt_oracle_apply_batch2(log2_n, rounds, classes, angles, perms, perm_mask, x, cls, count,
+                                  inverse, y, threads, 0);
+}
+
+int hygt_oracle_class_energy2(int log2_n, int rounds, int classes, const double* angles,
+                              const uint16_t* perms, uint32_t perm_mask, const float* x,
+                              const uint16_t* cls, uint64_t count, double* energy, int threads,
+                              int hoist_trig) {
+  const size_t n = (size_t)1 << log2_n;
+  memset(energy, 0, (size_t)classes * n * sizeof(double));
+  double* cs = hoist_trig ? class_tables(log2_n, rounds, classes, angles, 0) : NULL;
   batch_job p = {log2_n, rounds, classes, angles, perms, perm_mask, x, cls, 0, count,
-                 inverse, y, NULL, 0};
-  return run_jobs(&p, count, threads, 0);
+                 0, NULL, energy, 0, cs};
+  const int st = run_jobs(&p, count, threads, 1);
+  free(cs);
+  return st;
 }
 
 int hygt_oracle_class_energy(int log2_n, int rounds, int classes, const double* angles,
                              const uint16_t* perms, uint32_t perm_mask, const float* x,
                              const uint16_t* cls, uint64_t count, double* energy, int threads) {
-  const size_t n = (size_t)1 << log2_n;
-  memset(energy, 0, (size_t)classes * n * sizeof(double));
-  batch_job p = {log2_n, rounds, classes, angles, perms, perm_mask, x, cls, 0, count,
-                 0, NULL, energy, 0};
-  return run_jobs(&p, count, threads, 1);
+  return hygt_oracle_class_energy2(log2_n, rounds, classes, angles, perms, perm_mask, x, cls, count,
+                                   energy, threads, 0);
 }
 
 /* ============================== correlation (f3) ========================================= */

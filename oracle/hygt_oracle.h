@@ -79,6 +79,20 @@ int hygt_oracle_class_energy(int log2_n, int rounds, int classes, const double* 
                              const uint16_t* perms, uint32_t perm_mask, const float* x,
                              const uint16_t* cls, uint64_t count, double* energy, int threads);
 
+/* The same two drivers with hoist_trig != 0: cos/sin of every angle are computed once per class
+ * and direction (hygt_oracle_trig_pairs) instead of per butterfly and vector. Bit-identical
+ * results (cos/sin are deterministic); used for the full-size checks. */
+int hygt_oracle_apply_batch2(int log2_n, int rounds, int classes, const double* angles,
+                             const uint16_t* perms, uint32_t perm_mask, const float* x,
+                             const uint16_t* cls, uint64_t count, int inverse, double* y,
+                             int threads, int hoist_trig);
+int hygt_oracle_class_energy2(int log2_n, int rounds, int classes, const double* angles,
+                              const uint16_t* perms, uint32_t perm_mask, const float* x,
+                              const uint16_t* cls, uint64_t count, double* energy, int threads,
+                              int hoist_trig);
+void hygt_oracle_run_passes_cs(int log2_n, int rounds, const double* cs, double* x, int dir);
+void hygt_oracle_trig_pairs(size_t count, const double* angles, int dir, double* cs);
+
 /* ---- fixed point: fixedpoint.hpp:35-224 --------------------------------------------------- */
 int hygt_oracle_trig_table(int angle_bits, int precision_bits, int32_t* cos_tab,
                            int32_t* sin_tab); /* fixedpoint.hpp:37-52 */

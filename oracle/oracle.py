@@ -47,6 +47,8 @@ def lib():
         L = C.CDLL(_ORACLE_SO)
         L.hygt_oracle_apply_batch.argtypes = [_i, _i, _i, _p, _p, _u32, _p, _p, _u64, _i, _p, _i]
         L.hygt_oracle_class_energy.argtypes = [_i, _i, _i, _p, _p, _u32, _p, _p, _u64, _p, _i]
+        L.hygt_oracle_apply_batch2.argtypes = [_i, _i, _i, _p, _p, _u32, _p, _p, _u64, _i, _p, _i, _i]
+        L.hygt_oracle_class_energy2.argtypes = [_i, _i, _i, _p, _p, _u32, _p, _p, _u64, _p, _i, _i]
         L.hygt_oracle_correlation.argtypes = [_i, _i, _p, _p, _u64, _p, _p]
         L.hygt_oracle_correlation_finalize.argtypes = [_i, _p, _u64, _p]
         L.hygt_oracle_correlation_finalize.restype = None
@@ -158,31 +160,34 @@ def derive_seed(base, stream):
     return lib().hygt_oracle_derive_seed(base, stream)
 
 
-def apply_batch(log2_n, rounds, angles, perms, perm_mask, x, cls=None, inverse=False, threads=None):
-    """fp64 outputs of the chained reference transform over fp32 rows."""
+def apply_batch(log2_n, rounds, angles, perms, perm_mask, x, cls=None, inverse=False, threads=None,
+                hoist=False):
+    """fp64 outputs of the chained reference transform over fp32 rows. hoist=True tables cos/sin
+    once per class (bit-identical, for full-size checks)."""
     angles = _c(angles, np.float64)
     classes = angles.shape[0] if angles.ndim == 2 else 1
     x = _c(x, np.float32)
     n = 1 << log2_n
     count = x.size // n
     y = np.empty((count, n), np.float64)
-    st = lib().hygt_oracle_apply_batch(log2_n, rounds, classes, _ptr(angles), _ptr(_c(perms, np.uint16)),
-                                       perm_mask, _ptr(x), _ptr(_c(cls, np.uint16)), count,
-                                       int(bool(inverse)), _ptr(y), threads or os.cpu_count())
+    st = lib().hygt_oracle_apply_batch2(log2_n, rounds, classes, _ptr(angles), _ptr(_c(perms, np.uint16)),
+                                        perm_mask, _ptr(x), _ptr(_c(cls, np.uint16)), count,
+                                        int(bool(inverse)), _ptr(y), threads or os.cpu_count(),
+                                        int(bool(hoist)))
     if st:
         raise ValueError("oracle: class id out of range")
     return y
 
 
-def class_energy(log2_n, rounds, angles, perms, perm_mask, x, cls=None, threads=None):
+def class_energy(log2_n, rounds, angles, perms, perm_mask, x, cls=None, threads=None, hoist=False):
     angles = _c(angles, np.float64)
     classes = angles.shape[0] if angles.ndim == 2 else 1
     x = _c(x, np.float32)
     n = 1 << log2_n
     e = np.zeros((classes, n), np.float64)
-    lib().hygt_oracle_class_energy(log2_n, rounds, classes, _ptr(angles), _ptr(_c(perms, np.uint16)),
-                                   perm_mask, _ptr(x), _ptr(_c(cls, np.uint16)), x.size // n,
-                                   _ptr(e), threads or os.cpu_count())
+    lib().hygt_oracle_class_energy2(log2_n, rounds, classes, _ptr(angles), _ptr(_c(perms, np.uint16)),
+                                    perm_mask, _ptr(x), _ptr(_c(cls, np.uint16)), x.size // n,
+                                    _ptr(e), threads or os.cpu_count(), int(bool(hoist)))
     return e
 
 

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <unordered_map>
 #include <new>
@@ -122,6 +123,7 @@ struct hygt_plan {
   size_t seg_smem[2] = {0, 0};
   size_t seg_energy_smem = 0;
   unsigned long long* d_fixed_err = nullptr;
+  bool fx_int32 = false;  // fixed point: the int32 kernels are provably safe for this plan
   // fixed point, per-class NVRTC chain (hygt_jit.cpp): kernels and a plan-owned bucket workspace
   JitClsKernels fx_jit;
   void* d_fx_bws = nullptr;
@@ -188,6 +190,21 @@ int check_perms(int log2n, int rounds, int classes, const uint16_t* perms, uint3
   return HYGT_OK;
 }
 
+}  // namespace
+
+void hygt_smem_attr(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> set;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& cur = set[{dev, fn}];
+  if (bytes <= cur) return;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess) cur = bytes;
+  cudaGetLastError();
+}
+
+namespace {
 int env_int(const char* name, int dflt) {
   const char* v = std::getenv(name);
   return v && *v ? std::atoi(v) : dflt;
@@ -196,15 +213,9 @@ int env_int(const char* name, int dflt) {
 // Kernels' dynamic shared-memory limits are per function, shared by every plan; plans need
 // different sizes, so the attribute only ever grows (a smaller later plan must not shrink it
 // under an earlier, larger one).
-void smem_attr(const void* fn, size_t bytes) {
-  static std::mutex mu;
-  static std::unordered_map<const void*, size_t> set;
-  std::lock_guard<std::mutex> lock(mu);
-  size_t& cur = set[fn];
-  if (bytes <= cur) return;
-  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess) cur = bytes;
-  cudaGetLastError();
-}
+// The attribute is set per (device, function): a process driving several GPUs sets it on each
+// device its plans are created on.
+void smem_attr(const void* fn, size_t bytes) { hygt_smem_attr(fn, bytes); }
 template <typename F>
 void smem_attr(F* fn, size_t bytes) {
   smem_attr(reinterpret_cast<const void*>(fn), bytes);
@@ -858,8 +869,8 @@ int setup_segment(hygt_plan* p, const double* angles, const uint16_t* perms) {
     // the permutation scratch exists only when the plan has permutations
     p->seg_smem[d] = cb[d] + gb[d] +
                      (p->gmask[d] ? (size_t)(SEG_THREADS / 32) * tile_scratch_floats(p->log2n, sv.l, sv.vpt) * 4 : 0);
-    if (d == 0)  // fused energy: per-warp fp32 partial sums [E][32] (seg_energy_smem)
-      p->seg_energy_smem = p->seg_smem[0] + (size_t)(SEG_THREADS / 32) * ((1u << p->log2n) >> sv.l) * 32 * 4;
+    if (d == 0)  // fused energy: per-warp fp64 partial sums [E][32] (seg_energy_smem)
+      p->seg_energy_smem = (p->seg_smem[0] + 7) / 8 * 8 + (size_t)(SEG_THREADS / 32) * ((1u << p->log2n) >> sv.l) * 32 * 8;
     if (p->seg_smem[d] > 220 * 1024) return HYGT_OK;
     SegFn fn = select_seg(variant, p->algo == 0, d == 0, false);
     if (fn) smem_attr(fn, (int)p->seg_smem[d]);
@@ -1389,10 +1400,10 @@ __global__ void __launch_bounds__(FX_THREADS) fixed_kernel(const FixedParams P) 
 // (fixedpoint.hpp:170-176), with the TrigTable lookups (and the inverse's code negation) done at
 // plan creation into (c, s) int2 pairs in reference pair order per execution step. Tables of up
 // to 48 KB are staged into shared memory; larger ones are read through L1.
-// Values are held as int32: with |x| <= 2^20 (checked, fixedpoint.hpp:145-150) and p >= 4, every
-// rounded butterfly grows the L2 norm by at most (1 + 2^(0.5-p)) plus 1/2 per element, so over
-// R * log2N <= 64 passes |value| < 2^29 -- the reference's 2^46 overflow test (fixedpoint.hpp:
-// 177-179) cannot fire for valid inputs and the products fit IMAD.WIDE (32 x 32 -> 64).
+// Values are held as int32. The plan selects this kernel only when fixed_int32_safe() proves,
+// from the plan's own TrigTable gains and R * log2N, that no value of a valid row (|x| <= 2^20,
+// checked, fixedpoint.hpp:145-150) reaches 2^30: then the reference's 2^46 overflow test
+// (fixedpoint.hpp:177-179) cannot fire and the products fit IMAD.WIDE (32 x 32 -> 64).
 template <int LOG2N, bool FWD>
 __global__ void __launch_bounds__(FX_THREADS) fixed_row_kernel(const FixedParams P, const int2* __restrict__ tab,
                                                                uint32_t tab_smem_pairs) {
@@ -1630,6 +1641,36 @@ int run_fixed(const hygt_plan* p, int dir, const int64_t* x, int64_t* y, const u
 
 }  // namespace
 
+namespace {
+// Norm bound for the rounded integer butterflies of forward_fixed / inverse_fixed
+// (fixedpoint.hpp:170-176). One pass maps a pair (a, b) to (round((c a + s b) / 2^p),
+// round((c b - s a) / 2^p)) with (c, s) = TrigTable[code]; the exact part has L2 gain
+// g_code = sqrt(c^2 + s^2) / 2^p and each rounding adds at most 1/2 per element, so over the
+// N/2 disjoint pairs of a pass ||x'|| <= g ||x|| + sqrt(N)/2 with g the largest gain among the
+// codes the plan uses (the inverse's negated codes have the same gain). Permutations keep the
+// norm, and |value| <= ||x||. Inputs are at most 2^20 per element (checked per row,
+// fixedpoint.hpp:142-150), so after T = R log2N passes
+//   |value| <= g^T sqrt(N) 2^20 + sqrt(N)/2 * sum_{i<T} g^i.
+// The int32 kernels are safe when this stays below 2^30 (products c*a then fit IMAD.WIDE and
+// the int64 sums cannot wrap); the bound is evaluated in long double, monotone in every term.
+bool fixed_int32_safe(int log2n, int rounds, int classes, size_t a, const uint16_t* codes,
+                      const int32_t* ct, const int32_t* sn, int prec) {
+  long double g = 0;
+  for (size_t i = 0; i < a * (size_t)classes; ++i) {
+    const long double c = ct[codes[i]], s = sn[codes[i]];
+    g = std::max(g, sqrtl(c * c + s * s) / (long double)((int64_t)1 << prec));
+  }
+  const long double rn = sqrtl((long double)((size_t)1 << log2n));
+  long double bound = rn * 1048576.0L;
+  const int T = rounds * log2n;
+  for (int t = 0; t < T; ++t) {
+    bound = g * bound + rn / 2;
+    if (bound >= 1073741824.0L) return false;
+  }
+  return true;
+}
+}  // namespace
+
 extern "C" int hygt_fixed_plan_create(int log2_n, int rounds, int class_count, int angle_bits,
                                       int precision_bits, const uint16_t* codes,
                                       const uint16_t* perms, uint32_t perm_mask,
@@ -1683,6 +1724,13 @@ extern "C" int hygt_fixed_plan_create(int log2_n, int rounds, int class_count, i
     if (cudaMalloc(&e, sizeof(*e)) != cudaSuccess) s = fail(HYGT_ERR_CUDA, "cudaMalloc");
     p->d_fixed_err = e;
   }
+  // The int32 kernels (staged N = 16, thread-per-row N <= 64, per-class NVRTC chain) hold values
+  // in 32 bits. They are used only when a bound computed from this plan's own table proves that
+  // no value can reach 2^31 (so the reference's 2^46 test, fixedpoint.hpp:177-179, cannot fire
+  // either); otherwise every row runs on the int64 fixed_kernel, which applies that test.
+  const bool int32_ok = fixed_int32_safe(log2_n, rounds, class_count, a, codes, ct.data(), sn.data(),
+                                         precision_bits);
+  p->fx_int32 = int32_ok;
   for (int d = 0; d < 2 && !s; ++d) {
     std::vector<uint16_t> g((size_t)class_count * (rounds + 1) * n, 0);
     for (int c = 0; c < class_count; ++c) {
@@ -1695,7 +1743,7 @@ extern "C" int hygt_fixed_plan_create(int log2_n, int rounds, int class_count, i
           g[((size_t)c * (rounds + 1) + k) * n + i] = (uint16_t)gs[k][i];
     }
     s = upload(&p->d_fgather[d], g.data(), g.size());
-    if (!s && log2_n == 4 && class_count <= STAGE_MAX_CLASSES && env_int("HYGT_FIXED_STAGE", 1) != 0) {
+    if (!s && int32_ok && log2_n == 4 && class_count <= STAGE_MAX_CLASSES && env_int("HYGT_FIXED_STAGE", 1) != 0) {
       // element-pair (c, s', c, s') units per execution step for the staged kernel, and its
       // permutation offsets (src * 128 into the [element][lane] int32 scratch)
       const uint32_t mask = (1u << angle_bits) - 1u;
@@ -1752,7 +1800,7 @@ extern "C" int hygt_fixed_plan_create(int log2_n, int rounds, int class_count, i
         }
       }
     }
-    if (!s && log2_n <= 6 && env_int("HYGT_FIXED_ROW", 1) != 0) {
+    if (!s && int32_ok && log2_n <= 6 && env_int("HYGT_FIXED_ROW", 1) != 0) {
       // (c, s) per pair of the thread-per-row kernel, in execution order
       const uint32_t mask = (1u << angle_bits) - 1u;
       const size_t steps = (size_t)rounds * log2_n, half = n / 2;
@@ -1777,7 +1825,7 @@ extern "C" int hygt_fixed_plan_create(int log2_n, int rounds, int class_count, i
     free_plan(p);
     return s;
   }
-  if (!s && jit_fixed_supported(log2_n, rounds, class_count) && env_int("HYGT_FIXED_JIT", 1) != 0) {
+  if (!s && int32_ok && jit_fixed_supported(log2_n, rounds, class_count) && env_int("HYGT_FIXED_JIT", 1) != 0) {
     std::string err;
     if (jit_fixed_build(log2_n, rounds, class_count, angle_bits, precision_bits, codes, ct.data(), sn.data(),
                         perms, p->perm_mask, p->fx_jit, err))

@@ -482,8 +482,9 @@ std::string generate_class(int log2n, int minb, bool standard, const ClassProgra
 // y_n = (c b - s a + 2^(p-1)) >> p (fixedpoint.hpp:170-176) with c, s as IMAD.WIDE immediates
 // (the TrigTable lookups and the inverse's code negation done here on the host), permutations
 // as register renames. Values are int32 in registers: |input| <= 2^20 is checked per row
-// (fixedpoint.hpp:145-150) and keeps every rounded butterfly below 2^29 (the bound proved at
-// fixed_row_kernel, hygt_capi.cu), so the 2^46 overflow test cannot fire. A row with an
+// (fixedpoint.hpp:145-150); the plan builds these kernels only when fixed_int32_safe()
+// (hygt_capi.cu) proves every rounded butterfly stays below 2^30 for its codes and R * log2N,
+// so the 2^46 overflow test cannot fire. A row with an
 // out-of-range input is written back unchanged (as int32) and reported through *err as
 // (row << 3 | 1); the host turns the minimum into the first failing row.
 const char* kFxPrologue = R"CUDA(
@@ -493,7 +494,7 @@ typedef long long i64;
 #define RS (NQ + 1)
 #define FXS_(v) #v
 #define FXS(v) FXS_(v)
-// d = (a c + b s + 2^(p-1)) >> p, low word (|d| < 2^29): two IMAD.WIDE with immediates + a funnel shift
+// d = (a c + b s + 2^(p-1)) >> p, low word (|d| < 2^30): two IMAD.WIDE with immediates + a funnel shift
 #define FX(d, a, c, b, s)                                                                          \
   asm("{.reg .s64 t;.reg .u32 l,h;mad.wide.s32 t,%1," #c "," FXS(RND) ";mad.wide.s32 t,%2," #s   \
       ",t;mov.b64 {l,h},t;shf.r.clamp.b32 %0,l,h," FXS(PREC) ";}"                                  \

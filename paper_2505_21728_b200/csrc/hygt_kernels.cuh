@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(256) hygt_apply_kernel(const ApplyParams P) {
             __stcs(reinterpret_cast<float2*>(yr) + q, v[u]);
         }
         if constexpr (ENERGY) {
-          if (c != acc_class || acc_rows >= 64) {
+          if (c != acc_class || acc_rows >= 16) {  // fp32 partials of at most 16 rows
             flush();
             acc_class = c;
           }

@@ -25,6 +25,7 @@
 #include "../../include/hygt_gpu.h"
 
 int hygt_set_error(int status, const char* msg);  // hygt_capi.cu
+void hygt_smem_attr(const void* fn, size_t bytes);  // hygt_capi.cu: per (device, kernel), only grows
 namespace hygt_gpu {
 size_t bucket_ws_bytes(int classes, uint64_t chunk_rows, uint64_t count);
 int bucket_rows(int classes, uint64_t chunk_rows, const uint16_t* d_cls, uint64_t count,
@@ -644,8 +645,7 @@ template <int NN>
 int launch_tc(const hygt_klt_plan* p, int dir, const float* in, float* out, const uint32_t* idx,
               const uint32_t* seg_end, uint64_t count, cudaStream_t st) {
   const size_t smem = (size_t)2 * 128 * NN * 4 + (size_t)2 * NN * NN * 4;
-  static std::once_flag attr;  // the attribute is per function; set once, thread-safe
-  std::call_once(attr, [&] { cudaFuncSetAttribute(klt_tc_kernel<NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
+  hygt_smem_attr(reinterpret_cast<const void*>(klt_tc_kernel<NN>), smem);
   KltTcParams P{in, out, idx, seg_end, p->classes, count, p->d_b[dir]};
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, klt_tc_kernel<NN>, 128, smem);
@@ -663,13 +663,11 @@ int launch_pipe(const hygt_klt_plan* p, int dir, const float* in, float* out, co
   if (getenv("HYGT_KLT_PIPE") && atoi(getenv("HYGT_KLT_PIPE")) == 0)
     return launch_tc<NN>(p, dir, in, out, idx, seg_end, count, st);
   const size_t smem = (size_t)4 * 128 * NN * 4 + (size_t)2 * NN * NN * 4;
-  static std::once_flag attr;  // the attribute is per function; set once, thread-safe
-  std::call_once(attr, [&] { cudaFuncSetAttribute(klt_tc_pipe_kernel<NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
+  hygt_smem_attr(reinterpret_cast<const void*>(klt_tc_pipe_kernel<NN>), smem);
   const uint64_t tiles = (count + 127) / 128;
   const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)p->num_sms, tiles);
   if (p->d_bsw[dir] && !(getenv("HYGT_KLT_SW") && atoi(getenv("HYGT_KLT_SW")) == 0)) {
-    static std::once_flag attr_sw;  // the attribute is per function; set once, thread-safe
-    std::call_once(attr_sw, [&] { cudaFuncSetAttribute(klt_sw_kernel<NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
+    hygt_smem_attr(reinterpret_cast<const void*>(klt_sw_kernel<NN>), smem);
     KltTcParams Q{in, out, idx, seg_end, p->classes, count, p->d_bsw[dir]};
     klt_sw_kernel<NN><<<grid, KLT_PIPE_THREADS, smem, st>>>(Q);
   } else {

@@ -64,10 +64,11 @@ __global__ void __launch_bounds__(THREADS, (LOG2N >= 8 ? 1 : 2)) hygt_segment_ke
   float4* s_coef = reinterpret_cast<float4*>(seg_smem);
   uint4* s_gidx = reinterpret_cast<uint4*>(s_coef + cw);
   float* s_scratch = reinterpret_cast<float*>(s_gidx + gw);
-  // fused energy: per-lane fp32 partial sums in shared memory, [E][32] per warp (keeps the
-  // accumulators out of the register file, which the E samples of a long row already fill)
-  float* s_acc = s_scratch + (P.gmask ? (size_t)WARPS * N * S : 0) + (size_t)(threadIdx.x >> 5) * E * 32 +
-                 (threadIdx.x & 31);
+  // fused energy: per-lane fp64 partial sums in shared memory, [E][32] per warp (keeps the
+  // accumulators out of the register file, which the E samples of a long row already fill).
+  // Each addition is an fp32 sum of at most 32 squares of one step's rows.
+  double* s_acc = reinterpret_cast<double*>(s_scratch + (((P.gmask ? (size_t)WARPS * N * S : 0) + 1) & ~(size_t)1)) +
+                  (size_t)(threadIdx.x >> 5) * E * 32 + (threadIdx.x & 31);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> L, t = lane & (TPV - 1);
   float* wscr = s_scratch + (size_t)warp * N * S;
@@ -107,19 +108,18 @@ __global__ void __launch_bounds__(THREADS, (LOG2N >= 8 ? 1 : 2)) hygt_segment_ke
     __syncthreads();
     if constexpr (ENERGY) {
 #pragma unroll 8
-      for (int s = 0; s < E; ++s) s_acc[s * 32] = 0.f;
+      for (int s = 0; s < E; ++s) s_acc[s * 32] = 0.0;
     }
     int acc_rows = 0;
     auto flush = [&]() {
       if constexpr (ENERGY) {
-        // fp32 partial sums of <= 128 rows per lane (relative rounding error < 128 * 2^-24),
-        // reduced across the lane groups in fp64
+        // fp64 partial sums, reduced across the lane groups in fp64
 #pragma unroll 4
         for (int s = 0; s < E; ++s) {
-          double d = (double)s_acc[s * 32];
+          double d = s_acc[s * 32];
 #pragma unroll
           for (int o = TPV; o < 32; o <<= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-          s_acc[s * 32] = 0.f;
+          s_acc[s * 32] = 0.0;
           if (g == 0) atomicAdd(P.energy + (size_t)c * N + LY.elem(t, s), d);
         }
       }
@@ -182,8 +182,8 @@ __global__ void __launch_bounds__(THREADS, (LOG2N >= 8 ? 1 : 2)) hygt_segment_ke
         if constexpr (ENERGY && !SEG_RS) {
 #pragma unroll
           for (int k = 0; k < NP; ++k) {
-            s_acc[(2 * k) * 32] = fmaf(v[r][k].x, v[r][k].x, s_acc[(2 * k) * 32]);
-            s_acc[(2 * k + 1) * 32] = fmaf(v[r][k].y, v[r][k].y, s_acc[(2 * k + 1) * 32]);
+            s_acc[(2 * k) * 32] += (double)(v[r][k].x * v[r][k].x);
+            s_acc[(2 * k + 1) * 32] += (double)(v[r][k].y * v[r][k].y);
           }
         }
       }
@@ -219,8 +219,8 @@ __global__ void __launch_bounds__(THREADS, (LOG2N >= 8 ? 1 : 2)) hygt_segment_ke
             }
             off += up ? m : 0;
           }
-          s_acc[(g0 + off) * 32] += q[0];
-          s_acc[(g0 + off + 1) * 32] += q[1];
+          s_acc[(g0 + off) * 32] += (double)q[0];
+          s_acc[(g0 + off + 1) * 32] += (double)q[1];
         }
       }
       if constexpr (ENERGY) {

@@ -5,8 +5,8 @@
 // Per tile of T rows: the producer warp moves the int64 rows (128 B each) and the tile's sorted
 // entry block into a ring of STAGES shared-memory stages with cp.async.bulk and streams the
 // results back the same way; each consumer thread takes VPT sorted rows of one class.
-//   * values are int32 in registers (|x| <= 2^20 is checked on input; the growth bound of the
-//     rounded butterflies keeps |value| < 2^29, see fixed_row_kernel in hygt_capi.cu), products
+//   * values are int32 in registers (|x| <= 2^20 is checked on input; the plan takes this kernel
+//     only when fixed_int32_safe() in hygt_capi.cu bounds |value| < 2^30), products
 //     and the rounding add in int64: y = (c x_e + s' x_partner + 2^(p-1)) >> p per element with
 //     (c, s') = (c, s) on the pair's low element and (c, -s) on its high element
 //     (fixedpoint.hpp:170-176), looked up from the TrigTable at plan creation;

@@ -9,10 +9,47 @@ collective runs over NCCL / NVLink; the same host logic runs over gloo in the CP
 """
 from __future__ import annotations
 
+import os
 from typing import Optional, Tuple
 
 import torch
 import torch.distributed as dist
+
+
+def _active(group=None) -> bool:
+    return dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
+
+
+def init_process_group_from_env(device: Optional[torch.device] = None) -> Tuple[int, int]:
+    """One process per GPU as torchrun launches it: join the NCCL group when WORLD_SIZE > 1
+    (gloo for a CPU device). Returns (rank, world)."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        if device is not None and device.type == "cuda":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group("gloo")
+    return rank, world
+
+
+def destroy() -> None:
+    if dist.is_available() and dist.is_initialized():
+        dist.destroy_process_group()
+
+
+def barrier(group=None) -> None:
+    if _active(group):
+        dist.barrier(group=group)
+
+
+def sum_over_ranks(value: int, device=None, group=None) -> int:
+    """Total units processed by all ranks (each rank's own count, so uneven shards add up)."""
+    if not _active(group):
+        return value
+    t = torch.tensor([value], dtype=torch.int64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return int(t.item())
 
 
 def shard_range(count: int, rank: int, world: int) -> Tuple[int, int]:
@@ -28,14 +65,14 @@ def allreduce_energy(energy: torch.Tensor, group: Optional[dist.ProcessGroup] = 
     """Sum the per-class energy accumulators of all ranks in place (fp64, [C][N])."""
     if energy.dtype != torch.float64:
         raise ValueError("allreduce_energy: energy must be float64")
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+    if _active(group):
         dist.all_reduce(energy, op=dist.ReduceOp.SUM, group=group)
     return energy
 
 
 def max_over_ranks(value: float, device=None, group=None) -> float:
     """Device-timed step durations are reported as the max over ranks."""
-    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+    if not _active(group):
         return value
     t = torch.tensor([value], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
@@ -54,7 +91,7 @@ def sharded_forward_energy(plan, x_shard, cls_shard, energy, out=None, workspace
 def allreduce_correlation(sums, counts, group=None):
     """Shards of the per-class second moments merge by addition (merge_correlation,
     statistics.hpp:110-120 weights by counts, which is the same as adding sums and counts)."""
-    import torch.distributed as dist
-    dist.all_reduce(sums, group=group)
-    dist.all_reduce(counts, group=group)
+    if _active(group):
+        dist.all_reduce(sums, group=group)
+        dist.all_reduce(counts, group=group)
     return sums, counts

@@ -40,6 +40,46 @@ def _dev_ptr(t: Optional[torch.Tensor]) -> Optional[int]:
     return None if t is None else t.data_ptr()
 
 
+_CLS_DTYPES = (torch.uint16, torch.int16)
+
+
+def _ensure(t: Optional[torch.Tensor], name: str, dtypes, numel: Optional[int], device,
+            optional: bool = False) -> None:
+    """Every tensor handed to the C ABI as a raw pointer is checked here first: a CUDA tensor on
+    the plan's device, contiguous, of an accepted dtype and the expected element count.
+    Anything else raises ArgumentError before the native call (a mis-sized or host buffer
+    would otherwise become an out-of-bounds device write)."""
+    if t is None:
+        if optional:
+            return
+        raise ArgumentError(f"{name}: missing tensor")
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ArgumentError(f"{name}: must be a CUDA tensor")
+    if device is not None and t.device != torch.device(device):
+        raise ArgumentError(f"{name}: must be on {device}, not {t.device}")
+    if not t.is_contiguous():
+        raise ArgumentError(f"{name}: must be contiguous")
+    if dtypes is not None and t.dtype not in dtypes:
+        raise ArgumentError(f"{name}: dtype {t.dtype} not in {tuple(dtypes)}")
+    if numel is not None and t.numel() != numel:
+        raise ArgumentError(f"{name}: {t.numel()} elements, expected {numel}")
+
+
+def _on_stream(stream):
+    """Context that makes `stream` current, so default buffers are allocated (and zero-filled)
+    on the stream the kernels run on: the caching allocator then orders their reuse after
+    that stream's work."""
+    return torch.cuda.stream(stream) if stream is not None else _nullctx()
+
+
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
 def _np_ptr(a: Optional[np.ndarray]):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
 
@@ -85,7 +125,10 @@ class _Workspace:
         with self.lock:
             buf = self.bufs.get(key)
             if buf is None or buf.numel() < nbytes:
-                buf = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
+                # allocated and zeroed on the stream the kernels use; a replaced buffer is
+                # released through the allocator, which orders its reuse after that stream
+                with _on_stream(stream):
+                    buf = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
                 self.bufs[key] = buf
             return buf
 
@@ -98,6 +141,19 @@ class _Workspace:
                 if t == tid and s == sp:
                     return buf
         return None
+
+
+_KERNEL_NAMES = {
+    "stage": "hygt_stage_kernel",
+    "jit": "hygt_jit_kernel (NVRTC)",
+    "clsjit": "hygt_cls_f (one NVRTC kernel per class; a launch = the chain of per-class grids of one "
+              "direction)",
+    "cls": "hygt_cls_kernel (a launch = the chain of per-class grids of one direction)",
+    "segment": "hygt_segment_kernel",
+    "seg2": "hygt_seg2_kernel",
+    "tile": "hygt_tile_kernel",
+    "bucketed": "hygt_apply_kernel",
+}
 
 
 class HyGTPlan:
@@ -156,27 +212,37 @@ class HyGTPlan:
             return 3 + 2 * self.classes
         return {"tile": 2, "stage": 3}.get(path, 5)
 
+    def kernel_name(self) -> str:
+        """The device kernel(s) one forward or inverse call launches (for reports)."""
+        return _KERNEL_NAMES.get(self.path, f"hygt_{self.path}_kernel")
+
     def workspace_bytes(self, count: int) -> int:
         return _lib.lib().hygt_workspace_bytes(self._h, count)
 
-    def _prep(self, x: torch.Tensor, cls: Optional[torch.Tensor], out: Optional[torch.Tensor]):
+    def _prep(self, x: torch.Tensor, cls: Optional[torch.Tensor], out: Optional[torch.Tensor],
+              stream=None):
         if not isinstance(x, torch.Tensor) or not x.is_cuda:
             raise ArgumentError("HyGTPlan: x must be a CUDA tensor (use apply() for host data)")
         if x.dtype != torch.float32 or x.shape[-1] != self.n or not x.is_contiguous():
             raise ArgumentError("forward: dimension mismatch")
         count = x.numel() // self.n
-        if cls is not None:
-            if cls.dtype not in (torch.uint16, torch.int16) or cls.numel() != count or not cls.is_cuda:
-                raise ArgumentError("HyGTPlan: cls must be a CUDA uint16 tensor with one id per row")
+        _ensure(cls, "HyGTPlan cls", _CLS_DTYPES, count, x.device, optional=True)
         if out is None:
-            out = torch.empty_like(x)
-        elif out.shape != x.shape or out.dtype != torch.float32 or not out.is_contiguous():
-            raise ArgumentError("HyGTPlan: bad output tensor")
+            with _on_stream(stream):
+                out = torch.empty_like(x)
+        else:
+            _ensure(out, "HyGTPlan out", (torch.float32,), x.numel(), x.device)
+            if out.shape[-1] != self.n:
+                raise ArgumentError("HyGTPlan out: dimension mismatch")
         return count, out
 
     def _run(self, fn, x, cls, out, stream, workspace, reuse_buckets, energy=None):
-        count, out = self._prep(x, cls, out)
+        count, out = self._prep(x, cls, out, stream)
         nbytes = self.workspace_bytes(count)
+        if workspace is not None:
+            _ensure(workspace, "workspace", (torch.uint8,), None, x.device)
+            if workspace.numel() < nbytes:
+                raise ArgumentError("hygt: workspace too small")
         ws = workspace if workspace is not None else self._ws.get(nbytes, x.device, stream)
         flags = HYGT_REUSE_BUCKETS if reuse_buckets else 0
         args = [self._h, x.data_ptr(), out.data_ptr(), _dev_ptr(cls), count]
@@ -197,12 +263,17 @@ class HyGTPlan:
     def forward_energy(self, x, cls, energy, out=None, stream=None, workspace=None,
                        reuse_buckets=False):
         """Forward plus energy[c][i] += sum of y[row][i]^2 over rows of class c (fp64)."""
-        if energy.dtype != torch.float64 or energy.shape != (self.classes, self.n):
+        _ensure(energy, "forward_energy energy", (torch.float64,), self.classes * self.n, x.device)
+        if tuple(energy.shape) != (self.classes, self.n):
             raise ArgumentError("forward_energy: energy must be float64 [classes][N]")
         return self._run(_lib.lib().hygt_forward_energy_f32, x, cls, out, stream, workspace,
                          reuse_buckets, energy=energy)
 
     def bucket(self, cls, count, workspace, stream=None):
+        _ensure(cls, "bucket cls", _CLS_DTYPES, count, None)
+        _ensure(workspace, "bucket workspace", (torch.uint8,), None, cls.device)
+        if workspace.numel() < self.workspace_bytes(count):
+            raise ArgumentError("hygt: workspace too small")
         _check(_lib.lib().hygt_bucket(self._h, _dev_ptr(cls), count, workspace.data_ptr(),
                                       workspace.numel(), _stream_ptr(stream)))
 
@@ -263,13 +334,27 @@ class FixedPlan:
         if x.shape[-1] != self.n or not x.is_contiguous():
             raise ArgumentError("fixed transform: dimension mismatch")
         count = x.numel() // self.n
-        out = torch.empty_like(x) if out is None else out
+        _ensure(cls, "FixedPlan cls", _CLS_DTYPES, count, x.device, optional=True)
+        if out is None:
+            with _on_stream(stream):
+                out = torch.empty_like(x)
+        else:
+            _ensure(out, "FixedPlan out", (torch.int64,), x.numel(), x.device)
         bad = C.c_uint64(0)
         st = fn(self._h, x.data_ptr(), out.data_ptr(), _dev_ptr(cls), count, C.byref(bad),
                 _stream_ptr(stream))
         self.first_bad = int(bad.value)
         _check(st)
         return out
+
+    @property
+    def path(self) -> str:
+        return "fixed"
+
+    def launches_per_call(self) -> int:
+        """Upper bound of kernels one forward or inverse call launches (bucketing + the
+        per-class chain)."""
+        return 3 + self.classes
 
     def forward(self, x, cls=None, out=None, stream=None):
         return self._run(_lib.lib().hygt_forward_i64, x, cls, out, stream)
@@ -301,16 +386,30 @@ class KLTPlan:
     def workspace_bytes(self, count: int) -> int:
         return _lib.lib().hygt_klt_workspace_bytes(self._h, count)
 
+    def kernel_name(self) -> str:
+        return "klt_sw_kernel<64> (tcgen05.mma kind::tf32, 3xTF32)" if self.n == 64 else "klt_tc_kernel"
+
+    def launches_per_call(self) -> int:
+        return 4 if self.classes > 1 else 1  # bucketing (3) + the GEMM kernel
+
     def _run(self, fn, x, cls, out, stream, workspace=None):
         if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dtype != torch.float32:
             raise ArgumentError("KLTPlan: x must be a CUDA float32 tensor")
         if x.shape[-1] != self.n or not x.is_contiguous():
             raise ArgumentError("matrix/vector dimension mismatch")
         count = x.numel() // self.n
-        out = torch.empty_like(x) if out is None else out
-        ws = workspace
-        if ws is None:
-            ws = torch.empty(max(256, self.workspace_bytes(count)), dtype=torch.uint8, device=x.device)
+        _ensure(cls, "KLTPlan cls", _CLS_DTYPES, count, x.device, optional=True)
+        nbytes = max(256, self.workspace_bytes(count))
+        with _on_stream(stream):
+            if out is None:
+                out = torch.empty_like(x)
+            ws = workspace
+            if ws is None:
+                ws = torch.empty(nbytes, dtype=torch.uint8, device=x.device)
+        _ensure(out, "KLTPlan out", (torch.float32,), x.numel(), x.device)
+        _ensure(ws, "KLTPlan workspace", (torch.uint8,), None, x.device)
+        if ws.numel() < nbytes:
+            raise ArgumentError("hygt_klt: workspace too small")
         _check(fn(self._h, x.data_ptr(), out.data_ptr(), _dev_ptr(cls), count, ws.data_ptr(),
                   ws.numel(), _stream_ptr(stream)))
         return out
@@ -399,13 +498,18 @@ def correlation(x: torch.Tensor, cls: Optional[torch.Tensor], classes: int,
     if n != 1 << log2_n:
         raise ArgumentError("correlation: row length must be a power of two")
     count = x.numel() // n
-    if sums is None:
-        sums = torch.zeros(classes, n, n, dtype=torch.float64, device=x.device)
-    if counts is None:
-        counts = torch.zeros(classes, dtype=torch.int64, device=x.device)
+    _ensure(cls, "correlation cls", _CLS_DTYPES, count, x.device, optional=True)
     nbytes = _lib.lib().hygt_correlation_workspace_bytes(classes, count)
-    if workspace is None or workspace.numel() < nbytes:
-        workspace = torch.zeros(nbytes, dtype=torch.uint8, device=x.device)
+    with _on_stream(stream):
+        if sums is None:
+            sums = torch.zeros(classes, n, n, dtype=torch.float64, device=x.device)
+        if counts is None:
+            counts = torch.zeros(classes, dtype=torch.int64, device=x.device)
+        if workspace is None or workspace.numel() < nbytes:
+            workspace = torch.zeros(nbytes, dtype=torch.uint8, device=x.device)
+    _ensure(sums, "correlation sums", (torch.float64,), classes * n * n, x.device)
+    _ensure(counts, "correlation counts", (torch.int64, torch.uint64), classes, x.device)
+    _ensure(workspace, "correlation workspace", (torch.uint8,), None, x.device)
     _check(_lib.lib().hygt_correlation_f64(log2_n, classes, x.data_ptr(), _dev_ptr(cls), count,
                                            sums.data_ptr(), counts.data_ptr(), workspace.data_ptr(),
                                            workspace.numel(), _stream_ptr(stream)))

@@ -114,3 +114,84 @@ def test_correlation_allreduce_world2_gloo():
     for _, s, k in res:
         assert np.abs(s - s_full).max() <= 1e-12 * np.abs(s_full).max()  # fp64 addition order only
         assert np.array_equal(k, k_full.astype(np.int64))
+
+
+def _helpers_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    from paper_2505_21728_b200 import dist as D
+    r, w = D.init_process_group_from_env(torch.device("cpu"))
+    try:
+        D.barrier()
+        a, b = D.shard_range(1001, r, w)
+        total = D.sum_over_ranks(b - a)
+        t = D.max_over_ranks(0.5 + r)
+        q.put((r, w, total, t))
+    finally:
+        D.destroy()
+
+
+def test_bench_dist_helpers_world2_gloo():
+    """The helpers bench.py's N > 1 path goes through (dist.py): process-group setup from the
+    torchrun environment, barrier, the units-processed sum and the max-over-ranks step time."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_helpers_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [r[:3] for r in res] == [(0, 2, 1001), (1, 2, 1001)]
+    assert all(r[3] == 1.5 for r in res)
+
+
+def _gpu_energy_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2505_21728_b200 import HyGTPlan
+        from paper_2505_21728_b200.dist import shard_range, sharded_forward_energy
+        from paper_2505_21728_b200.synth import make_workload
+        w = make_workload(5)
+        count = 1 << 18
+        a, b = shard_range(count, rank, world)
+        torch.cuda.set_device(0)
+        cls = w.make_classes(b - a, a)
+        x = w.make_rows(b - a, cls, a)
+        plan = HyGTPlan(w.models)
+        e = torch.zeros(35, 256, dtype=torch.float64, device="cuda")
+        sharded_forward_energy(plan, x, cls, e)
+        plan.sync_status()
+        q.put((rank, e.cpu().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_gpu_energy_two_shards_allreduce_vs_oracle():
+    """The GPU forward-with-energy kernel on two shards (two ranks, each a contiguous row range
+    generated on the device) plus the all-reduce of dist.sharded_forward_energy equals the
+    oracle's energy of the whole batch (config 5 shape, 2^18 rows). The ranks share one GPU
+    here (gloo carries the 70 KB exchange; the kernels never wait on each other); on a B200
+    node each rank owns a GPU and the same call runs over NCCL."""
+    from oracle import oracle as O
+    from paper_2505_21728_b200.synth import make_workload
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_energy_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    w = make_workload(5)
+    count = 1 << 18
+    cls = w.make_classes(count)
+    x = w.make_rows(count, cls)
+    ref = O.class_energy(8, 4, w.angles, None, 0, x.cpu().numpy(), cls.cpu().numpy(), hoist=True)
+    for _, e in res:
+        np.testing.assert_allclose(e, ref, rtol=1e-6)

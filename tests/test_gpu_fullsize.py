@@ -1,0 +1,123 @@
+"""GPU parity at the configured sizes: config 5 (2^24 rows x N = 256, 35
+classes, with the full [35][256] fp64 energy table) and config 3 (2^22 rows x N = 64, 35 classes,
+inter-round permutations, directional edges), exactly the shapes the bench times.
+
+What is checked, per config:
+  * round trip inverse(forward(x)) on ALL rows (max-abs <= 1e-5 * max|x|) and per-row norm
+    preservation (the transform is orthogonal, transform.hpp:45-66);
+  * forward against the oracle: every row (config 3) or a 65,536-row random sample (config 5),
+    within the fp32 bar (relative L2 <= 1e-6, max-abs <= 1e-5 * max|x|);
+  * inverse of the GPU's own forward output against the oracle on a sample;
+  * config 5: the full energy table E[c][i] = sum y[row][i]^2 over all 2^24 rows against the
+    oracle's full-batch energy (statistics.hpp:69-77 diagonal), rtol 1e-6.
+The oracle runs with cos/sin tabled once per class (hoist=True, pinned bit-identical to the
+per-butterfly form in tests/test_oracle.py) on all host threads, in chunks of host rows.
+"""
+import numpy as np
+import pytest
+import torch
+
+from test_gpu_parity import check_close
+
+pytestmark = pytest.mark.gpu
+
+CHUNK = 1 << 20
+ENERGY_RTOL = 1e-6
+
+
+def _roundtrip_and_norms(x, y, back):
+    scale = x.abs().max().item()
+    worst = 0.0
+    worst_norm = 0.0
+    for r0 in range(0, x.shape[0], CHUNK):
+        xs, ys, bs = x[r0:r0 + CHUNK], y[r0:r0 + CHUNK], back[r0:r0 + CHUNK]
+        worst = max(worst, (bs - xs).abs().max().item())
+        nx = xs.double().pow(2).sum(1)
+        ny = ys.double().pow(2).sum(1)
+        worst_norm = max(worst_norm, ((ny - nx).abs() / nx.clamp(min=1e-30)).max().item())
+    assert worst <= 1e-5 * scale, f"round trip max-abs {worst:.3e} vs {1e-5 * scale:.3e}"
+    assert worst_norm < 1e-5, f"norm preservation {worst_norm:.3e}"
+
+
+def _sample(count, k, device, seed=7):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    return torch.randperm(count, generator=g)[:k].sort().values.to(device)
+
+
+def test_config5_full_size_with_energy(cuda, oracle_mod):
+    from paper_2505_21728_b200 import HyGTPlan
+    from paper_2505_21728_b200.synth import make_workload
+    O = oracle_mod
+    w = make_workload(5)
+    count = w.cfg.count
+    assert count == 1 << 24 and w.n == 256 and w.cfg.classes == 35
+    cls = w.make_classes(count)
+    x = w.make_rows(count, cls)
+    plan = HyGTPlan(w.models)
+    ws = torch.zeros(plan.workspace_bytes(count), dtype=torch.uint8, device=cuda)
+    e = torch.zeros(35, 256, dtype=torch.float64, device=cuda)
+    y = plan.forward_energy(x, cls, e, workspace=ws)
+    back = plan.inverse(y, cls, workspace=ws, reuse_buckets=True)
+    plan.sync_status(ws)
+    torch.cuda.synchronize()
+    _roundtrip_and_norms(x, y, back)
+    del back
+    # forward and inverse on a 65,536-row random sample
+    idx = _sample(count, 1 << 16, cuda)
+    xs, cs = x[idx].cpu().numpy(), cls[idx].cpu().numpy()
+    ref = O.apply_batch(8, 4, w.angles, None, 0, xs, cs, hoist=True)
+    check_close(y[idx].cpu().numpy(), ref, xs, "cfg5 forward sample")
+    ys = y[idx].cpu().numpy()
+    refi = O.apply_batch(8, 4, w.angles, None, 0, ys, cs, inverse=True, hoist=True)
+    zs = plan.inverse(y[idx].contiguous(), cls[idx].contiguous()).cpu().numpy()
+    check_close(zs, refi, ys, "cfg5 inverse sample")
+    del y
+    # the full [35][256] energy table over all 2^24 rows
+    ref_e = np.zeros((35, 256))
+    for r0 in range(0, count, CHUNK):
+        ref_e += O.class_energy(8, 4, w.angles, None, 0, x[r0:r0 + CHUNK].cpu().numpy(),
+                                cls[r0:r0 + CHUNK].cpu().numpy(), hoist=True)
+    ge = e.cpu().numpy()
+    rel = np.abs(ge - ref_e) / np.abs(ref_e)
+    assert rel.max() <= ENERGY_RTOL, f"energy max rel {rel.max():.3e} at {np.unravel_index(rel.argmax(), rel.shape)}"
+    # every class and coefficient got rows (uniform class ids over 2^24 rows)
+    assert (ref_e > 0).all()
+
+
+def test_config3_full_size(cuda, oracle_mod):
+    from paper_2505_21728_b200 import HyGTPlan
+    from paper_2505_21728_b200.synth import make_workload
+    O = oracle_mod
+    w = make_workload(3)
+    count = w.cfg.count
+    assert count == 1 << 22 and w.n == 64 and w.cfg.classes == 35
+    cls = w.make_classes(count)
+    x = w.make_rows(count, cls)
+    plan = HyGTPlan(w.models, w.perms)
+    ws = torch.zeros(plan.workspace_bytes(count), dtype=torch.uint8, device=cuda)
+    y = plan.forward(x, cls, workspace=ws)
+    back = plan.inverse(y, cls, workspace=ws, reuse_buckets=True)
+    plan.sync_status(ws)
+    torch.cuda.synchronize()
+    _roundtrip_and_norms(x, y, back)
+    # forward of every row against the oracle
+    full = np.concatenate([w.perms, np.tile(np.arange(64, dtype=np.uint16), (35, 1, 1))], 1)
+    mask = (1 << 3) - 1
+    scale = x.abs().max().item()
+    num = den = 0.0
+    worst = 0.0
+    for r0 in range(0, count, CHUNK):
+        xs, cs = x[r0:r0 + CHUNK].cpu().numpy(), cls[r0:r0 + CHUNK].cpu().numpy()
+        ref = O.apply_batch(6, 4, w.angles, full, mask, xs, cs, hoist=True)
+        err = y[r0:r0 + CHUNK].cpu().numpy().astype(np.float64) - ref
+        num += float((err * err).sum())
+        den += float((ref * ref).sum())
+        worst = max(worst, float(np.abs(err).max()))
+    rel = (num / den) ** 0.5
+    assert rel <= 1e-6, f"cfg3 forward rel L2 {rel:.3e}"
+    assert worst <= 1e-5 * scale, f"cfg3 forward max-abs {worst:.3e}"
+    # inverse of the GPU's forward output on a sample
+    idx = _sample(count, 1 << 16, cuda)
+    ys, cs = y[idx].cpu().numpy(), cls[idx].cpu().numpy()
+    refi = O.apply_batch(6, 4, w.angles, full, mask, ys, cs, inverse=True, hoist=True)
+    check_close(back[idx].cpu().numpy(), refi, ys, "cfg3 inverse sample")

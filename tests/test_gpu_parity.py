@@ -269,6 +269,40 @@ def test_fixed_golden_bit_exact(cuda, golden, k, fixed_jit, monkeypatch):
     assert np.array_equal(z, golden[f"x{k}_inv"][ok2])
 
 
+@pytest.fixture(scope="module")
+def golden_long():
+    return np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_fixed_long.npz"))
+
+
+@pytest.mark.parametrize("name", ["grow16", "long64", "grow256", "mixed32"])
+def test_fixed_long_models_overflow_and_int32_gate(cuda, golden_long, name):
+    """Long low-precision models (tests/gen_golden_fixed_long.py, from the unmodified reference):
+    R * log2N = 160..480 passes at p = 4/5. Valid rows grow past 2^31 (grow16/grow256), so the
+    plan must leave the int32 kernels (their bound fails) for the int64 one; rows at 2^20
+    overflow 2^46 and the reference throws OverflowError (fixedpoint.hpp:177-179): the GPU
+    reports status 4 at the same first row. Every valid row is bit-exact."""
+    from paper_2505_21728_b200 import FixedPlan, QuantizedHyGTModel, TrigTable
+    from paper_2505_21728_b200.errors import OverflowError_
+    g = golden_long
+    log2n, rounds, b, p, with_perm = (int(v) for v in g[name + "_meta"])
+    perm = g[name + "_perm"] if with_perm else None
+    plan = FixedPlan(QuantizedHyGTModel(log2n, rounds, b, g[name + "_codes"], perm), TrigTable(b, p))
+    x = g[name + "_x"]
+    for d, key in ((0, "fwd"), (1, "inv")):
+        st = g[f"{name}_{key}_status"]
+        run = plan.forward if d == 0 else plan.inverse
+        xd = torch.from_numpy(x).to(cuda)
+        if (st != 0).any():
+            first = int(np.argmax(st != 0))
+            assert int(st[first]) == 4  # OverflowError in the reference
+            with pytest.raises(OverflowError_):
+                run(xd)
+            assert plan.first_bad == first
+        ok = np.nonzero(st == 0)[0]
+        y = run(torch.from_numpy(x[ok]).to(cuda)).cpu().numpy()
+        assert np.array_equal(y, g[f"{name}_{key}"][ok]), f"{name} {key}: not bit-exact"
+
+
 @pytest.mark.parametrize("kernel", ["default", "stage", "row", "warp"])
 def test_fixed_random_multiclass_vs_oracle(cuda, oracle_mod, kernel, monkeypatch):
     """Bit-exact vs the oracle through every fixed-point kernel: the per-class NVRTC chain

@@ -1,6 +1,7 @@
 """CPU: pin the oracle (oracle/hygt_oracle.c) against the reference's golden vectors and the
 reference's own known-answer tests. No GPU."""
 import math
+import os
 
 import numpy as np
 import pytest
@@ -276,3 +277,50 @@ def test_ar1_covariance_formula_matches_reference(bs, rho):
     out = np.zeros((bs * bs, bs * bs))
     lib.ref_ar1_covariance_2d(bs, rho, out.ctypes.data)
     np.testing.assert_allclose(_ar1_2d(bs, rho), out, rtol=1e-12, atol=1e-15)
+
+
+@pytest.mark.parametrize("name", ["grow16", "long64", "grow256", "mixed32"])
+def test_fixed_long_golden_bit_exact(oracle_mod, name):
+    """The oracle against the reference on long low-precision models (golden_fixed_long.npz):
+    values past 2^31 stay exact and rows at 2^20 throw OverflowError (status 4), row by row."""
+    O = oracle_mod
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_fixed_long.npz"))
+    log2n, rounds, b, p, with_perm = (int(v) for v in g[name + "_meta"])
+    n = 1 << log2n
+    codes = g[name + "_codes"]
+    perms, mask = None, 0
+    if with_perm:
+        perms = np.tile(np.arange(n, dtype=np.uint16), (1, rounds, 1))
+        perms[0, rounds - 1] = g[name + "_perm"]
+        mask = 1 << (rounds - 1)
+    x = g[name + "_x"]
+    for inv, key in ((False, "fwd"), (True, "inv")):
+        st_all = g[f"{name}_{key}_status"]
+        st, bad, y = O.apply_batch_fixed(log2n, rounds, b, p, codes[None], perms, mask, x, inverse=inv)
+        first = int(np.argmax(st_all != 0)) if (st_all != 0).any() else x.shape[0]
+        assert st == (int(st_all[first]) if first < x.shape[0] else 0)
+        assert bad == first
+        ok = np.nonzero(st_all == 0)[0]
+        st2, _, y2 = O.apply_batch_fixed(log2n, rounds, b, p, codes[None], perms, mask, x[ok], inverse=inv)
+        assert st2 == 0 and np.array_equal(y2, g[f"{name}_{key}"][ok])
+
+
+@pytest.mark.parametrize("log2n,rounds,classes,mask", [(4, 3, 35, 3), (6, 4, 5, 7), (8, 4, 3, 0), (8, 2, 2, 3)])
+def test_hoisted_trig_is_bit_identical(oracle_mod, log2n, rounds, classes, mask):
+    """The full-size checks use the oracle with cos/sin tabled once per class (hoist=True); pin
+    that mode bit for bit against the per-butterfly restatement of transform.hpp:57-59."""
+    O = oracle_mod
+    rng = np.random.default_rng(log2n * 10 + rounds)
+    n = 1 << log2n
+    a = rounds * n * log2n // 2
+    angles = rng.uniform(-np.pi, np.pi, (classes, a))
+    perms = np.stack([np.stack([rng.permutation(n) for _ in range(rounds)]) for _ in range(classes)]).astype(np.uint16)
+    x = (rng.standard_normal((257, n)) * 16).astype(np.float32)
+    cls = rng.integers(0, classes, 257).astype(np.uint16)
+    for inv in (False, True):
+        a0 = O.apply_batch(log2n, rounds, angles, perms, mask, x, cls, inverse=inv, threads=3)
+        a1 = O.apply_batch(log2n, rounds, angles, perms, mask, x, cls, inverse=inv, threads=2, hoist=True)
+        assert np.array_equal(a0, a1)
+    e0 = O.class_energy(log2n, rounds, angles, perms, mask, x, cls, threads=1)
+    e1 = O.class_energy(log2n, rounds, angles, perms, mask, x, cls, threads=1, hoist=True)
+    assert np.array_equal(e0, e1)
