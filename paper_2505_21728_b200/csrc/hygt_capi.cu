@@ -23,6 +23,7 @@
 #include "hygt_segment.cuh"
 #include "hygt_plan.h"
 #include "hygt_jit.h"
+#include "hygt_gemm.h"
 
 using namespace hygt_gpu;
 #include "hygt_dispatch.h"
@@ -129,6 +130,9 @@ struct hygt_plan {
   void* d_fx_bws = nullptr;
   size_t fx_bws_bytes = 0;
   std::mutex* fixed_mu = nullptr;
+  // composed-operator path (N = 64 / 128 / 256): per-class M_c / M_c^T on the tensor cores
+  bool gemm = false;
+  GemmOperands gemm_ops[2];
 };
 
 namespace {
@@ -168,6 +172,8 @@ void free_plan(hygt_plan* p) {
   jit_cls_release(p->cls_jit);
   jit_cls_release(p->fx_jit);
   cudaFree(p->d_fx_bws);
+  gemm_release(p->gemm_ops[0]);
+  gemm_release(p->gemm_ops[1]);
   delete p->fixed_mu;
   delete p;
 }
@@ -1022,6 +1028,32 @@ int run_segment(const hygt_plan* p, int dir, const float* x, float* y, uint64_t 
   return ok();
 }
 
+// Composed-operator path: M_c (forward) and M_c^T (inverse) per class, fp64 on the host, then
+// the fp16 hi/lo operand stages of hygt_gemm.cu. Default for N = 256, where the butterfly
+// kernels are bound by coefficient delivery through the LSU; HYGT_GEMM=1 takes
+// it at N = 64 / 128 as well, HYGT_GEMM=0 never.
+int setup_gemm(hygt_plan* p, const double* angles, const uint16_t* perms) {
+  const int n = 1 << p->log2n;
+  if (!gemm_supported(n, p->classes)) return HYGT_OK;
+  const int want = env_int("HYGT_GEMM", -1);
+  if (want == 0 || (want < 0 && n != 256)) return HYGT_OK;
+  const size_t a = (size_t)p->rounds * p->log2n * n / 2;
+  std::vector<double> fwd((size_t)p->classes * n * n), inv((size_t)p->classes * n * n);
+  for (int c = 0; c < p->classes; ++c) {
+    double* m = &fwd[(size_t)c * n * n];
+    compose_operator(p->log2n, p->rounds, angles + (size_t)c * a,
+                     perms ? perms + (size_t)c * p->rounds * n : nullptr, p->perm_mask, m);
+    double* t = &inv[(size_t)c * n * n];
+    for (int i = 0; i < n; ++i)
+      for (int k = 0; k < n; ++k) t[(size_t)i * n + k] = m[(size_t)k * n + i];
+  }
+  if (int s = gemm_build(n, p->classes, fwd.data(), p->gemm_ops[0])) return s;
+  if (int s = gemm_build(n, p->classes, inv.data(), p->gemm_ops[1])) return s;
+  p->gemm = true;
+  p->chunk_rows = 0;  // global class buckets
+  return HYGT_OK;
+}
+
 int run_apply(const hygt_plan* p, int dir, const float* x, float* y, const uint16_t* d_cls,
               uint64_t count, double* energy, void* d_ws, size_t ws_bytes, uint32_t flags,
               cudaStream_t st) {
@@ -1035,6 +1067,21 @@ int run_apply(const hygt_plan* p, int dir, const float* x, float* y, const uint1
       return fail(HYGT_ERR_ARGUMENT, "hygt: x and y must be aligned to min(16, 4N) bytes");
   }
   const WsLayout w = ws_layout(p->classes, p->chunk_rows, count);
+  if (p->gemm) {
+    if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) != 0)
+      return fail(HYGT_ERR_ARGUMENT, "hygt: x and y must be aligned to 16 bytes");
+    const bool bk = d_cls && p->classes > 1;
+    if (bk) {
+      if (!d_ws || ws_bytes < w.total) return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
+      if (!(flags & HYGT_REUSE_BUCKETS)) {
+        const int s = run_bucket(p, p->classes, 0, d_cls, count, d_ws, ws_bytes, st);
+        if (s) return s;
+      }
+    }
+    const char* ws = static_cast<const char*>(d_ws);
+    return gemm_run(p->gemm_ops[dir], x, y, bk ? reinterpret_cast<const uint32_t*>(ws + w.idx) : nullptr,
+                    bk ? reinterpret_cast<const uint32_t*>(ws + w.seg) : nullptr, count, energy, st);
+  }
   if (p->jit.ok && !energy) {
     const bool bk = d_cls && p->classes > 1;
     if (d_cls) {
@@ -1232,6 +1279,10 @@ extern "C" int hygt_plan_create(int log2_n, int rounds, int class_count, const d
     free_plan(p);
     return s;
   }
+  if (int s = setup_gemm(p, angles, perms)) {
+    free_plan(p);
+    return s;
+  }
   *out = p;
   return ok();
 }
@@ -1250,11 +1301,12 @@ extern "C" int hygt_plan_destroy(hygt_plan* plan) {
 extern "C" int hygt_plan_algorithm(const hygt_plan* plan) { return plan ? plan->algo : -1; }
 
 extern "C" int hygt_plan_path(const hygt_plan* plan) {
-  return plan ? (plan->jit.ok ? 3 : plan->stage ? 4 : plan->cls_jit.ok ? 7 : plan->cls ? 6 : plan->tile ? 1 : plan->seg2 ? 5 : plan->seg ? 2 : 0) : -1;
+  return plan ? (plan->gemm ? 8 : plan->jit.ok ? 3 : plan->stage ? 4 : plan->cls_jit.ok ? 7 : plan->cls ? 6 : plan->tile ? 1 : plan->seg2 ? 5 : plan->seg ? 2 : 0) : -1;
 }
 
 extern "C" size_t hygt_workspace_bytes(const hygt_plan* plan, uint64_t count) {
   if (!plan) return 0;
+  if (plan->gemm) return ws_layout(plan->classes, 0, count).total;
   if (plan->stage && !plan->jit.ok) return std::max<size_t>(stage_ws_bytes(plan, count), 256);
   if (plan->tile && !plan->jit.ok && !plan->cls) return 256;
   return ws_layout(plan->classes, plan->chunk_rows, count).total;
@@ -1263,6 +1315,8 @@ extern "C" size_t hygt_workspace_bytes(const hygt_plan* plan, uint64_t count) {
 extern "C" int hygt_bucket(const hygt_plan* plan, const uint16_t* d_cls, uint64_t count,
                            void* d_ws, size_t ws_bytes, void* stream) {
   if (!plan) return fail(HYGT_ERR_ARGUMENT, "hygt_bucket: null plan");
+  if (plan->gemm)
+    return plan->classes > 1 ? run_bucket(plan, plan->classes, 0, d_cls, count, d_ws, ws_bytes, as_stream(stream)) : ok();
   if (plan->stage && !plan->jit.ok)  // per-tile class sort of the staged kernel
     return plan->classes > 1 ? run_stage_sort(plan, d_cls, count, d_ws, ws_bytes, as_stream(stream)) : ok();
   if (plan->tile && !plan->jit.ok && !plan->cls) return ok();  // tile plans sort each tile in shared memory

@@ -1,0 +1,631 @@
+// hygt_gemm.cu -- per-class dense operators on the 5th-generation tensor cores (tcgen05).
+//
+// Serves two paths of SURVEY.md §8:
+//   * a10, the KLT comparison: y = K_c x (klt_forward, statistics.hpp:222-224 -> multiply,
+//     matrix.hpp:70-80) and x = K_c^T y (transposed, matrix.hpp:82-88);
+//   * a1-a3 at N = 64 / 128 / 256, the HyGT itself as its COMPOSED operator: for a class c the
+//     R rounds x log2N passes of Givens rotations (transform.hpp:45-66), the inter-round and
+//     final gathers included, are one orthogonal N x N matrix M_c (transform.hpp:100-117
+//     builds exactly this matrix column by column). The plan composes M_c once in fp64 from the
+//     class's angles, and every row is then y = M_c x (forward) or x = M_c^T y (inverse).
+//     At N = 256 the butterfly form needs 32 KB of rotation coefficients per row and direction
+//     delivered through the shared-memory/L1 pipe (bound at 37% of HBM); the
+//     composed form moves that work onto the tensor cores, whose operand reads bypass the LSU.
+//
+// Rows are bucketed by class (hygt_bucket). A tile is 128 rows of one class; per tile the
+// kernel computes OUT[128 x N] = IN[128 x N] . B^T with B[n][k] (N x K, K-major), B = M_c or
+// M_c^T (HyGT) / K_c or K_c^T (KLT).
+//
+// Precision (the fp32 bar of SURVEY.md c4: relative L2 <= 1e-6): fp16 operands with an exact
+// 2-way split on both sides, x = x_hi + x_lo, b = b_hi + b_lo, and three MMAs
+// lo.hi + hi.lo + hi.hi accumulated in fp32 in TMEM (the dropped lo.lo term is ~2^-22 relative).
+// fp16 has 5 exponent bits, so every row is scaled by a power of two chosen from its own
+// max |x| (max |x s| in [2^14, 2^15)) and every class operator by 2^kB (max |b 2^kB| in
+// [2^14, 2^15)); both scales are exact and undone in the epilogue.
+//
+// Kernel structure (one persistent CTA per SM, warp-specialised, all hand-offs on mbarriers):
+//   warps 0-3   epilogue : TMEM -> registers (tcgen05.ld, lane = row) -> unscale -> swizzled
+//                          staging -> coalesced STG rows; fused per-class energy (fp64)
+//   warps 4-11  split    : rows (LDG, coalesced) -> row max -> scale -> fp16 hi/lo into the
+//                          SWIZZLE_128B K-major A ring (one 64-column K atom per slot)
+//   warp 12     producer : cp.async.bulk of the class's B stages (L2 resident, 32 KB each)
+//   warp 13     MMA      : one thread issues tcgen05.mma kind::f16 M=128 N<=128 K=16
+//   TMEM: two N-column fp32 accumulators (tile t and t+1), so the epilogue of one tile
+//   overlaps the MMAs of the next.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/hygt_gpu.h"
+#include "hygt_gemm.h"
+
+int hygt_set_error(int status, const char* msg);       // hygt_capi.cu
+void hygt_smem_attr(const void* fn, size_t bytes);     // hygt_capi.cu
+
+namespace hygt_gpu {
+namespace {
+
+constexpr int GM = 128;           // rows per tile (MMA M)
+constexpr int EPI_WARPS = 4;
+constexpr int SPLIT_WARPS = 8;
+constexpr int PROD_WARP = EPI_WARPS + SPLIT_WARPS;
+constexpr int MMA_WARP = PROD_WARP + 1;
+constexpr int GEMM_THREADS = (MMA_WARP + 1) * 32;
+constexpr uint32_t ATOM_BYTES = GM * 128;  // one 64-column fp16 K atom of the A tile (16 KB)
+
+template <int NN>
+struct Shape {
+  static constexpr int KA = NN / 64;                 // K atoms
+  static constexpr int NW = NN < 128 ? NN : 128;     // N per MMA instruction
+  static constexpr int NH = NN / NW;                 // N halves
+  static constexpr int S = KA * NH;                  // B stages per tile
+  static constexpr uint32_t STAGE = 2u * NW * 128;   // hi + lo, SW128 K-major
+  static constexpr int NA = KA == 1 ? 2 : 3;         // A ring slots (hi + lo atom each)
+  static constexpr int NB = S == 1 ? 2 : 3;          // B ring slots
+  static constexpr uint32_t A_OFF = 0;
+  static constexpr uint32_t B_OFF = A_OFF + NA * 2 * ATOM_BYTES;
+  static constexpr uint32_t STG_OFF = B_OFF + NB * STAGE;
+  static constexpr uint32_t STG_BYTES = 32 * 128;    // per epilogue warp: 32 rows x 32 floats
+  static constexpr uint32_t EN_OFF = STG_OFF + EPI_WARPS * STG_BYTES;
+  static constexpr uint32_t FAC_OFF = EN_OFF + EPI_WARPS * NN * 8;
+  static constexpr uint32_t BAR_OFF = FAC_OFF + 4 * GM * 4;
+  static constexpr uint32_t SMEM = BAR_OFF + 256 + 1024;  // + alignment slack
+  static constexpr uint32_t TMEM_COLS = 2 * NN < 32 ? 32 : 2 * NN;
+  static constexpr int RG = GM / SPLIT_WARPS / 4;    // 4-row groups per split warp
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" :: "r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n\tW%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%0], %1;\n\t@!P bra W%=;\n\t}\n"
+      :: "r"(smem_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(smem_u32(b)) : "memory");
+}
+// SWIZZLE_128B K-major UMMA shared-memory descriptor: 8-row x 128 B atoms, 1024 B apart (SBO).
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;            // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;  // SBO
+  d |= (uint64_t)1 << 46;            // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+  return d;
+}
+// Instruction descriptor: D f32, A/B f16, both K-major, M = 128, N = n.
+__host__ __device__ constexpr uint32_t idesc_f16(int n) {
+  return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(GM >> 4) << 24);
+}
+// swizzled byte offset of 16 B chunk q of row r inside an SW128 atom
+__device__ __forceinline__ uint32_t swz(int r, int q) { return (uint32_t)r * 128u + (uint32_t)((q ^ (r & 7)) << 4); }
+
+__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
+  __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ float2 unpack_h2(uint32_t u) {
+  __half2 h = *reinterpret_cast<__half2*>(&u);
+  return __half22float2(h);
+}
+
+// Per-row power-of-two scale: max |x s| in [2^14, 2^15) (fp16 max is 65504). Zero rows get 1.
+__device__ __forceinline__ float row_scale(float mx) {
+  const uint32_t e = __float_as_uint(mx) >> 23;  // biased exponent of max |x|
+  if (mx == 0.f) return 1.f;
+  int f = 268 - (int)e;                          // 127 + 14 - (e - 127)
+  f = f < 1 ? 1 : (f > 254 ? 254 : f);
+  return __uint_as_float((uint32_t)f << 23);
+}
+
+// end of bucket c (bucket `classes` holds invalid ids); without buckets (one class, no ids) the
+// rows are in order: bucket 0 = [0, count)
+__device__ __forceinline__ uint64_t seg_at(const GemmParams& P, int c) {
+  return P.seg_end ? (uint64_t)__ldg(P.seg_end + c) : (c >= 0 ? P.count : 0ull);
+}
+__device__ __forceinline__ uint32_t row_at(const GemmParams& P, uint64_t p) {
+  return P.idx ? __ldg(P.idx + p) : (uint32_t)p;
+}
+
+// tile -> (class, first bucketed position, rows)
+struct TileMap {
+  const uint32_t* tile_end;  // shared: [C] cumulative tile counts
+  const GemmParams* P;
+  int classes;
+  __device__ void of(uint32_t t, int& c, uint64_t& p0, uint32_t& rows) const {
+    int lo = 0, hi = classes - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (tile_end[mid] <= t) lo = mid + 1; else hi = mid;
+    }
+    c = lo;
+    const uint32_t first_tile = c ? tile_end[c - 1] : 0u;
+    const uint64_t s0 = c ? seg_at(*P, c - 1) : 0ull;
+    const uint64_t s1 = seg_at(*P, c);
+    p0 = s0 + (uint64_t)(t - first_tile) * GM;
+    const uint64_t left = s1 - p0;
+    rows = left < GM ? (uint32_t)left : GM;
+  }
+};
+
+template <int NN, bool ENERGY>
+__global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmParams P) {
+  using SH = Shape<NN>;
+  extern __shared__ __align__(16) unsigned char gemm_smem_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gemm_smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + SH::BAR_OFF);
+  uint64_t* a_full = bars;                     // [NA]  count SPLIT_WARPS
+  uint64_t* a_empty = a_full + SH::NA;         // [NA]  tcgen05.commit
+  uint64_t* b_full = a_empty + SH::NA;         // [NB]  expect_tx
+  uint64_t* b_empty = b_full + SH::NB;         // [NB]  tcgen05.commit
+  uint64_t* d_full = b_empty + SH::NB;         // [2]   tcgen05.commit
+  uint64_t* d_empty = d_full + 2;              // [2]   count EPI_WARPS
+  uint64_t* f_full = d_empty + 2;              // [4]   row scales written, count SPLIT_WARPS
+  uint64_t* f_empty = f_full + 4;              // [4]   row scales read, count EPI_WARPS
+  uint32_t* tmem_sh = reinterpret_cast<uint32_t*>(f_empty + 4);
+  __shared__ uint32_t tile_end_sh[HYGT_GEMM_MAX_CLASSES];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int C = P.classes;
+  // per-class cumulative tile counts
+  if (warp == 0) {
+    uint32_t run = 0;
+    for (int c0 = 0; c0 < C; c0 += 32) {
+      const int c = c0 + lane;
+      uint32_t nt = 0;
+      if (c < C) {
+        const uint64_t s0 = c ? seg_at(P, c - 1) : 0ull;
+        const uint64_t s1 = seg_at(P, c);
+        nt = (uint32_t)((s1 - s0 + GM - 1) / GM);
+      }
+      uint32_t v = nt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+      }
+      if (c < C) tile_end_sh[c] = run + v;
+      run += __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  if (warp == MMA_WARP) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(smem_u32(tmem_sh)), "r"(SH::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < SH::NA; ++i) { mbar_init(&a_full[i], SPLIT_WARPS); mbar_init(&a_empty[i], 1); }
+    for (int i = 0; i < SH::NB; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&d_full[i], 1); mbar_init(&d_empty[i], EPI_WARPS); }
+    for (int i = 0; i < 4; ++i) { mbar_init(&f_full[i], SPLIT_WARPS); mbar_init(&f_empty[i], EPI_WARPS); }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_sh;
+  const TileMap tm{tile_end_sh, &P, C};
+  const uint32_t ntiles = C ? tile_end_sh[C - 1] : 0u;
+  float* fac = reinterpret_cast<float*>(sm + SH::FAC_OFF);  // [4][GM] per-row unscale factors
+
+  if (warp == MMA_WARP) {
+    // ------------------------------------------------------------------ MMA issuer ----
+    if (lane == 0) {
+      uint32_t ia = 0, ib = 0, k = 0;
+      for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+        const int db = (int)(k & 1);
+        if (k >= 2) mbar_wait(&d_empty[db], ((k >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t d0 = tmem + (uint32_t)(db * NN);
+        for (int ka = 0; ka < SH::KA; ++ka, ++ia) {
+          const int sa = (int)(ia % SH::NA);
+          mbar_wait(&a_full[sa], (ia / SH::NA) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t ahi = smem_u32(sm + SH::A_OFF + (uint32_t)sa * 2 * ATOM_BYTES);
+          const uint32_t alo = ahi + ATOM_BYTES;
+          for (int nh = 0; nh < SH::NH; ++nh, ++ib) {
+            const int sb = (int)(ib % SH::NB);
+            mbar_wait(&b_full[sb], (ib / SH::NB) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint32_t bhi = smem_u32(sm + SH::B_OFF + (uint32_t)sb * SH::STAGE);
+            const uint32_t blo = bhi + SH::STAGE / 2;
+            const uint32_t d = d0 + (uint32_t)(nh * SH::NW);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {  // K = 16 fp16 = 32 B per instruction
+              const uint32_t o = 32u * j;
+              const uint64_t da[3] = {desc_sw128(alo + o), desc_sw128(ahi + o), desc_sw128(ahi + o)};
+              const uint64_t dbd[3] = {desc_sw128(bhi + o), desc_sw128(blo + o), desc_sw128(bhi + o)};
+#pragma unroll
+              for (int term = 0; term < 3; ++term) {  // small terms first
+                const uint32_t acc = (ka | j | term) ? 1u : 0u;
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n"
+                    :: "r"(d), "l"(da[term]), "l"(dbd[term]), "r"(idesc_f16(SH::NW)), "r"(acc));
+              }
+            }
+            tc_commit(&b_empty[sb]);
+          }
+          tc_commit(&a_empty[sa]);
+        }
+        tc_commit(&d_full[db]);
+      }
+    }
+  } else if (warp == PROD_WARP) {
+    // ------------------------------------------------------------------ B producer ----
+    if (lane == 0) {
+      uint32_t ib = 0;
+      for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int c;
+        uint64_t p0;
+        uint32_t rows;
+        tm.of(t, c, p0, rows);
+        const unsigned char* src = P.bops + (size_t)c * SH::S * SH::STAGE;
+        for (int s = 0; s < SH::S; ++s, ++ib) {
+          const int sb = (int)(ib % SH::NB);
+          if (ib >= (uint32_t)SH::NB) mbar_wait(&b_empty[sb], ((ib / SH::NB) - 1) & 1);
+          mbar_expect_tx(&b_full[sb], SH::STAGE);
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+              :: "r"(smem_u32(sm + SH::B_OFF + (uint32_t)sb * SH::STAGE)), "l"(src + (size_t)s * SH::STAGE),
+                 "r"(SH::STAGE), "r"(smem_u32(&b_full[sb])) : "memory");
+        }
+      }
+    }
+  } else if (warp >= EPI_WARPS) {
+    // ------------------------------------------------------------------ split warps ---
+    const int sw = warp - EPI_WARPS;
+    const int g8 = lane >> 3, l8 = lane & 7;  // row within a 4-row group, lane within the row
+    uint32_t ia = 0, k = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+      int c;
+      uint64_t p0;
+      uint32_t rows;
+      tm.of(t, c, p0, rows);
+      // pass 1: row max -> scale (rows of this warp: sw * RG * 4 + g * 4 + g8)
+      float scl[SH::RG];
+      uint32_t rid[SH::RG];
+#pragma unroll
+      for (int g = 0; g < SH::RG; ++g) {
+        const int r = (sw * SH::RG + g) * 4 + g8;
+        const bool ok = (uint32_t)r < rows;
+        rid[g] = ok ? row_at(P, p0 + r) : 0xffffffffu;
+        float mx = 0.f;
+        if (ok) {
+          const float4* src = reinterpret_cast<const float4*>(P.x + (size_t)rid[g] * NN);
+#pragma unroll
+          for (int i = 0; i < NN / 32; ++i) {
+            const float4 v = __ldcg(src + i * 8 + l8);  // L2-allocating: pass 2 re-reads it
+            mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+          }
+        }
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+        scl[g] = row_scale(mx);
+      }
+      // row unscale factors for the epilogue: 1 / s (power of two, exact)
+      {
+        const int fb = (int)(k & 3);
+        if (k >= 4) mbar_wait(&f_empty[fb], ((k >> 2) - 1) & 1);  // tile k-4's factors were read
+        if (l8 == 0) {
+#pragma unroll
+          for (int g = 0; g < SH::RG; ++g) fac[fb * GM + (sw * SH::RG + g) * 4 + g8] = 1.f / scl[g];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&f_full[fb]);
+      }
+      // pass 2: per K atom, the atom's 64 columns of each row -> fp16 hi / lo in the A ring
+      for (int ka = 0; ka < SH::KA; ++ka, ++ia) {
+        const int sa = (int)(ia % SH::NA);
+        if (ia >= (uint32_t)SH::NA) mbar_wait(&a_empty[sa], ((ia / SH::NA) - 1) & 1);
+        unsigned char* ahi = sm + SH::A_OFF + (uint32_t)sa * 2 * ATOM_BYTES;
+        unsigned char* alo = ahi + ATOM_BYTES;
+#pragma unroll
+        for (int g = 0; g < SH::RG; ++g) {
+          const int r = (sw * SH::RG + g) * 4 + g8;
+          float4 v[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h)  // columns 64 ka + 32 h + 4 l8 .. +3
+            v[h] = rid[g] != 0xffffffffu
+                       ? __ldcs(reinterpret_cast<const float4*>(P.x + (size_t)rid[g] * NN + 64 * ka + 32 * h) + l8)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const float s = scl[g];
+            const float a0 = v[h].x * s, a1 = v[h].y * s, a2 = v[h].z * s, a3 = v[h].w * s;
+            const uint32_t h01 = pack_h2(a0, a1), h23 = pack_h2(a2, a3);
+            const float2 b01 = unpack_h2(h01), b23 = unpack_h2(h23);
+            const uint32_t l01 = pack_h2(a0 - b01.x, a1 - b01.y), l23 = pack_h2(a2 - b23.x, a3 - b23.y);
+            // element kk = 32 h + 4 l8 of the atom: chunk q = kk / 8, byte (kk % 8) * 2
+            const uint32_t off = swz(r, h * 4 + (l8 >> 1)) + (uint32_t)(l8 & 1) * 8u;
+            *reinterpret_cast<uint2*>(ahi + off) = make_uint2(h01, h23);
+            *reinterpret_cast<uint2*>(alo + off) = make_uint2(l01, l23);
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic stores -> tensor core reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&a_full[sa]);
+      }
+    }
+    // rows with an invalid class id (bucket C): copied through, the error is flagged by hygt_bucket
+    if (C > 0 && P.seg_end) {
+      const uint64_t s0 = seg_at(P, C - 1), s1 = seg_at(P, C);
+      for (uint64_t p = s0 + (uint64_t)blockIdx.x * SPLIT_WARPS * 4 + sw * 4 + g8; p < s1;
+           p += (uint64_t)gridDim.x * SPLIT_WARPS * 4) {
+        const uint32_t row = __ldg(P.idx + p);
+        const float4* src = reinterpret_cast<const float4*>(P.x + (size_t)row * NN);
+        float4* dst = reinterpret_cast<float4*>(P.y + (size_t)row * NN);
+        for (int i = l8; i < NN / 4; i += 8) dst[i] = src[i];
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ epilogue ------
+    unsigned char* stg = sm + SH::STG_OFF + (uint32_t)warp * SH::STG_BYTES;
+    double* en = reinterpret_cast<double*>(sm + SH::EN_OFF) + (size_t)warp * NN;
+    if (ENERGY)
+      for (int i = lane; i < NN; i += 32) en[i] = 0.0;
+    int en_class = -1;
+    auto flush_energy = [&]() {
+      if (ENERGY && en_class >= 0) {
+        __syncwarp();
+        for (int i = lane; i < NN; i += 32) {
+          const double v = en[i];
+          if (v != 0.0) atomicAdd(P.energy + (size_t)en_class * NN + i, v);
+          en[i] = 0.0;
+        }
+        __syncwarp();
+      }
+    };
+    const int r_th = warp * 32 + lane;  // TMEM lane = tile row of this thread
+    uint32_t k = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+      int c;
+      uint64_t p0;
+      uint32_t rows;
+      tm.of(t, c, p0, rows);
+      if (ENERGY && c != en_class) {
+        flush_energy();
+        en_class = c;
+      }
+      const int db = (int)(k & 1);
+      mbar_wait(&f_full[k & 3], (k >> 2) & 1);
+      mbar_wait(&d_full[db], (k >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const float f_row = fac[(k & 3) * GM + r_th] * __ldg(P.unscale + c);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&f_empty[k & 3]);
+      // row ids of the 4-row groups this lane stores (rows warp*32 + 4 i + lane/8)
+      uint32_t orow[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int r = warp * 32 + 4 * i + (lane >> 3);
+        orow[i] = (uint32_t)r < rows ? row_at(P, p0 + r) : 0xffffffffu;
+      }
+      for (int cb = 0; cb < NN / 32; ++cb) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(db * NN + cb * 32);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+        if (cb == NN / 32 - 1) {  // accumulator fully read: release it to the MMA of tile k + 2
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&d_empty[db]);
+        }
+        // unscale, then thread-per-row -> swizzled staging [32 rows][32 floats]
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<float4*>(stg + swz(lane, q)) =
+              make_float4(__uint_as_float(v[4 * q]) * f_row, __uint_as_float(v[4 * q + 1]) * f_row,
+                          __uint_as_float(v[4 * q + 2]) * f_row, __uint_as_float(v[4 * q + 3]) * f_row);
+        __syncwarp();
+        // coalesced: 8 lanes per row, 4 rows per instruction
+        float e0 = 0.f, e1 = 0.f, e2 = 0.f, e3 = 0.f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int rr = 4 * i + (lane >> 3);
+          const float4 o = *reinterpret_cast<const float4*>(stg + swz(rr, lane & 7));
+          if (orow[i] != 0xffffffffu) {
+            __stcs(reinterpret_cast<float4*>(P.y + (size_t)orow[i] * NN + cb * 32) + (lane & 7), o);
+            if (ENERGY) {
+              e0 = fmaf(o.x, o.x, e0);
+              e1 = fmaf(o.y, o.y, e1);
+              e2 = fmaf(o.z, o.z, e2);
+              e3 = fmaf(o.w, o.w, e3);
+            }
+          }
+        }
+        __syncwarp();  // staging reads done before the next column block overwrites it
+        if (ENERGY) {  // fp32 sums of 8 rows, then fp64 across the warp's 4 row groups
+          double d0 = e0, d1 = e1, d2 = e2, d3 = e3;
+#pragma unroll
+          for (int o = 8; o < 32; o <<= 1) {
+            d0 += __shfl_xor_sync(0xffffffffu, d0, o);
+            d1 += __shfl_xor_sync(0xffffffffu, d1, o);
+            d2 += __shfl_xor_sync(0xffffffffu, d2, o);
+            d3 += __shfl_xor_sync(0xffffffffu, d3, o);
+          }
+          if (lane < 8) {
+            double* e = en + cb * 32 + lane * 4;
+            e[0] += d0;
+            e[1] += d1;
+            e[2] += d2;
+            e[3] += d3;
+          }
+        }
+      }
+    }
+    flush_energy();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == MMA_WARP)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(SH::TMEM_COLS));
+}
+
+// ---------------------------------------------------------------- host: operand builder ----
+// Round to nearest even fp16 (bits) from fp64, no double rounding.
+uint16_t half_rn(double v) {
+  const uint16_t sign = std::signbit(v) ? 0x8000u : 0u;
+  double a = std::fabs(v);
+  if (a == 0.0) return sign;
+  if (!(a < 65520.0)) return (uint16_t)(sign | 0x7c00u);
+  int ex = 0;
+  std::frexp(a, &ex);
+  int E = ex - 1;  // a in [2^E, 2^(E+1))
+  if (E < -14) {   // subnormal: units of 2^-24
+    const double q = std::nearbyint(std::ldexp(a, 24));
+    return (uint16_t)(sign | (uint16_t)q);  // q == 1024 becomes the smallest normal
+  }
+  double q = std::nearbyint((std::ldexp(a, -E) - 1.0) * 1024.0);
+  if (q >= 1024.0) {
+    q = 0.0;
+    ++E;
+  }
+  if (E > 15) return (uint16_t)(sign | 0x7c00u);
+  return (uint16_t)(sign | (uint16_t)((E + 15) << 10) | (uint16_t)q);
+}
+double half_to_double(uint16_t h) {
+  const int e = (h >> 10) & 31, m = h & 1023;
+  const double v = e == 0 ? std::ldexp((double)m, -24) : std::ldexp(1.0 + m / 1024.0, e - 15);
+  return (h & 0x8000u) ? -v : v;
+}
+
+}  // namespace
+
+int gemm_smem_bytes(int n) {
+  switch (n) {
+    case 64: return (int)Shape<64>::SMEM;
+    case 128: return (int)Shape<128>::SMEM;
+    case 256: return (int)Shape<256>::SMEM;
+    default: return 0;
+  }
+}
+
+bool gemm_supported(int n, int classes) {
+  return (n == 64 || n == 128 || n == 256) && classes >= 1 && classes <= HYGT_GEMM_MAX_CLASSES;
+}
+
+// ops[c] = B_c (N x K row-major fp64): out[row] = B_c in[row]. Builds the per-class hi/lo fp16
+// stages in the SW128 K-major layout the kernel streams, and the per-class unscale 2^-kB.
+int gemm_build(int n, int classes, const double* ops, GemmOperands& out) {
+  if (!gemm_supported(n, classes)) return hygt_set_error(HYGT_ERR_ARGUMENT, "gemm: unsupported shape");
+  const int nw = n < 128 ? n : 128, ka = n / 64, nh = n / nw;
+  const size_t stage = (size_t)2 * nw * 128, per_class = stage * ka * nh;
+  std::vector<unsigned char> host(per_class * classes, 0);
+  std::vector<float> unscale(classes);
+  for (int c = 0; c < classes; ++c) {
+    const double* b = ops + (size_t)c * n * n;
+    double mx = 0;
+    for (size_t i = 0; i < (size_t)n * n; ++i) mx = std::max(mx, std::fabs(b[i]));
+    if (!std::isfinite(mx)) return hygt_set_error(HYGT_ERR_ARGUMENT, "gemm: non-finite operator");
+    int kb = 0;
+    if (mx > 0) {
+      int ex = 0;
+      std::frexp(mx, &ex);  // mx in [2^(ex-1), 2^ex)
+      kb = 15 - ex;         // mx 2^kb in [2^14, 2^15)
+    }
+    unscale[c] = (float)std::ldexp(1.0, -kb);
+    unsigned char* dst = host.data() + per_class * c;
+    for (int a = 0; a < ka; ++a)
+      for (int h = 0; h < nh; ++h) {
+        unsigned char* st = dst + stage * (size_t)(a * nh + h);
+        for (int r = 0; r < nw; ++r)
+          for (int kk = 0; kk < 64; ++kk) {
+            const double v = std::ldexp(b[(size_t)(h * nw + r) * n + a * 64 + kk], kb);
+            const uint16_t hi = half_rn(v);
+            const uint16_t lo = half_rn(v - half_to_double(hi));
+            const int q = kk / 8;
+            const size_t off = (size_t)r * 128 + (size_t)((q ^ (r & 7)) << 4) + (size_t)(kk % 8) * 2;
+            std::memcpy(st + off, &hi, 2);
+            std::memcpy(st + stage / 2 + off, &lo, 2);
+          }
+      }
+  }
+  gemm_release(out);
+  out.n = n;
+  out.classes = classes;
+  if (cudaMalloc(&out.d_ops, host.size()) != cudaSuccess || cudaMalloc(&out.d_unscale, classes * sizeof(float)) != cudaSuccess) {
+    gemm_release(out);
+    cudaGetLastError();
+    return hygt_set_error(HYGT_ERR_CUDA, "gemm: cudaMalloc failed");
+  }
+  if (cudaMemcpy(out.d_ops, host.data(), host.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(out.d_unscale, unscale.data(), classes * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess) {
+    gemm_release(out);
+    return hygt_set_error(HYGT_ERR_CUDA, "gemm: upload failed");
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&out.num_sms, cudaDevAttrMultiProcessorCount, dev);
+  if (out.num_sms <= 0) out.num_sms = 148;
+  return HYGT_OK;
+}
+
+void gemm_release(GemmOperands& g) {
+  cudaFree(g.d_ops);
+  cudaFree(g.d_unscale);
+  g.d_ops = nullptr;
+  g.d_unscale = nullptr;
+}
+
+namespace {
+template <int NN, bool E>
+int launch_one(const GemmParams& P, int num_sms, cudaStream_t st) {
+  const auto fn = hygt_gemm_kernel<NN, E>;
+  hygt_smem_attr(reinterpret_cast<const void*>(fn), Shape<NN>::SMEM);
+  fn<<<num_sms, GEMM_THREADS, Shape<NN>::SMEM, st>>>(P);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? HYGT_OK : hygt_set_error(HYGT_ERR_CUDA, cudaGetErrorString(e));
+}
+}  // namespace
+
+int gemm_run(const GemmOperands& g, const float* x, float* y, const uint32_t* idx,
+             const uint32_t* seg_end, uint64_t count, double* energy, cudaStream_t st) {
+  if (!count) return HYGT_OK;
+  GemmParams P{};
+  P.x = x;
+  P.y = y;
+  P.idx = idx;
+  P.seg_end = seg_end;
+  P.classes = g.classes;
+  P.count = count;
+  P.bops = g.d_ops;
+  P.unscale = g.d_unscale;
+  P.energy = energy;
+  const uint64_t tiles = (count + GM - 1) / GM + (uint64_t)g.classes;
+  const int grid = (int)std::min<uint64_t>((uint64_t)g.num_sms, tiles);
+  switch (g.n) {
+    case 64: return energy ? launch_one<64, true>(P, grid, st) : launch_one<64, false>(P, grid, st);
+    case 128: return energy ? launch_one<128, true>(P, grid, st) : launch_one<128, false>(P, grid, st);
+    case 256: return energy ? launch_one<256, true>(P, grid, st) : launch_one<256, false>(P, grid, st);
+    default: return hygt_set_error(HYGT_ERR_ARGUMENT, "gemm: unsupported N");
+  }
+}
+
+}  // namespace hygt_gpu

@@ -14,6 +14,9 @@
 // to the standard form (hygt_plan_algorithm() reports which).
 #include "hygt_plan.h"
 
+#include <algorithm>
+#include <vector>
+
 #include <cmath>
 #include <cstring>
 
@@ -315,6 +318,37 @@ bool benes_route(int log2n, const std::vector<int>& src, std::vector<std::vector
   for (int j = 0; j < n; ++j)
     if (v[j] != src[j]) return false;
   return true;
+}
+
+void compose_operator(int log2n, int rounds, const double* angles_c, const uint16_t* perms_c,
+                      uint32_t mask, double* out) {
+  const int n = 1 << log2n, half = n / 2;
+  // X[i][k] = sample i of the transform of unit vector e_k; the butterflies act on whole rows
+  std::vector<double> x((size_t)n * n, 0.0), tmp((size_t)n * n);
+  for (int i = 0; i < n; ++i) x[(size_t)i * n + i] = 1.0;
+  for (int r = 0; r < rounds; ++r) {
+    for (int p = 0; p < log2n; ++p) {
+      const uint32_t kk = 1u << p;
+      const size_t base = ((size_t)r * log2n + p) * half;  // model.hpp:77-79
+      for (int j = 0; j < half; ++j) {
+        const uint32_t m = j + (j & (0u - kk)), nn = m + kk;  // transform.hpp:55-56
+        const double t = angles_c[base + j], c = std::cos(t), s = std::sin(t);
+        double* a = &x[(size_t)m * n];
+        double* b = &x[(size_t)nn * n];
+        for (int k = 0; k < n; ++k) {
+          const double av = a[k], bv = b[k];
+          a[k] = c * av + s * bv;  // transform.hpp:60-63
+          b[k] = c * bv - s * av;
+        }
+      }
+    }
+    if (perms_c && ((mask >> r) & 1u)) {  // gather after round r: out[i] = pre[perm[i]]
+      const uint16_t* pr = perms_c + (size_t)r * n;
+      for (int i = 0; i < n; ++i) std::copy_n(&x[(size_t)pr[i] * n], n, &tmp[(size_t)i * n]);
+      x.swap(tmp);
+    }
+  }
+  std::copy(x.begin(), x.end(), out);
 }
 
 }  // namespace hygt_gpu

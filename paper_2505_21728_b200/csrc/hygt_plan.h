@@ -59,4 +59,11 @@ bool build_direction(const Layout& ly, int rounds, int classes, const double* an
 // routing fails its own simulation check.
 bool benes_route(int log2n, const std::vector<int>& src, std::vector<std::vector<int>>& swaps);
 
+// The class's whole forward transform as one N x N matrix, fp64: column k = forward(e_k) with the
+// reference's pass order and per-butterfly cos/sin (transform.hpp:45-66, the gathers after the
+// rounds whose mask bit is set as transform.hpp:75-80; transform.hpp:100-117 builds the same
+// matrix). out[i * N + k], so y = out . x.
+void compose_operator(int log2n, int rounds, const double* angles_c, const uint16_t* perms_c,
+                      uint32_t mask, double* out);
+
 }  // namespace hygt_gpu

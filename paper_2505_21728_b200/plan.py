@@ -153,6 +153,7 @@ _KERNEL_NAMES = {
     "seg2": "hygt_seg2_kernel",
     "tile": "hygt_tile_kernel",
     "bucketed": "hygt_apply_kernel",
+    "gemm": "hygt_gemm_kernel (composed per-class operator, tcgen05.mma kind::f16 3-term split)",
 }
 
 
@@ -201,7 +202,8 @@ class HyGTPlan:
     @property
     def path(self) -> str:
         """Kernel family serving this plan (include/hygt_gpu.h, hygt_plan_path)."""
-        return {0: "bucketed", 1: "tile", 2: "segment", 3: "jit", 4: "stage", 5: "seg2", 6: "cls", 7: "clsjit"}[_lib.lib().hygt_plan_path(self._h)]
+        return {0: "bucketed", 1: "tile", 2: "segment", 3: "jit", 4: "stage", 5: "seg2", 6: "cls", 7: "clsjit",
+                8: "gemm"}[_lib.lib().hygt_plan_path(self._h)]
 
     def launches_per_step(self) -> int:
         """Kernels launched by bucket + forward + inverse on this plan (the stage path sorts each
@@ -210,7 +212,7 @@ class HyGTPlan:
         path = self.path
         if path in ("cls", "clsjit"):
             return 3 + 2 * self.classes
-        return {"tile": 2, "stage": 3}.get(path, 5)
+        return {"tile": 2, "stage": 3}.get(path, 5)  # gemm: 3 bucketing kernels + 2 gemm launches
 
     def kernel_name(self) -> str:
         """The device kernel(s) one forward or inverse call launches (for reports)."""

@@ -39,6 +39,13 @@ def _roundtrip_and_norms(x, y, back):
     assert worst_norm < 1e-5, f"norm preservation {worst_norm:.3e}"
 
 
+def _take(t, idx):
+    """Rows idx of t (uint16 tensors are not indexable on CUDA: go through int16)."""
+    if t.dtype == torch.uint16:
+        return t.view(torch.int16)[idx].view(torch.uint16)
+    return t[idx]
+
+
 def _sample(count, k, device, seed=7):
     g = torch.Generator(device="cpu").manual_seed(seed)
     return torch.randperm(count, generator=g)[:k].sort().values.to(device)
@@ -64,12 +71,12 @@ def test_config5_full_size_with_energy(cuda, oracle_mod):
     del back
     # forward and inverse on a 65,536-row random sample
     idx = _sample(count, 1 << 16, cuda)
-    xs, cs = x[idx].cpu().numpy(), cls[idx].cpu().numpy()
+    xs, cs = x[idx].cpu().numpy(), _take(cls, idx).cpu().numpy()
     ref = O.apply_batch(8, 4, w.angles, None, 0, xs, cs, hoist=True)
     check_close(y[idx].cpu().numpy(), ref, xs, "cfg5 forward sample")
     ys = y[idx].cpu().numpy()
     refi = O.apply_batch(8, 4, w.angles, None, 0, ys, cs, inverse=True, hoist=True)
-    zs = plan.inverse(y[idx].contiguous(), cls[idx].contiguous()).cpu().numpy()
+    zs = plan.inverse(y[idx].contiguous(), _take(cls, idx).contiguous()).cpu().numpy()
     check_close(zs, refi, ys, "cfg5 inverse sample")
     del y
     # the full [35][256] energy table over all 2^24 rows
@@ -118,6 +125,6 @@ def test_config3_full_size(cuda, oracle_mod):
     assert worst <= 1e-5 * scale, f"cfg3 forward max-abs {worst:.3e}"
     # inverse of the GPU's forward output on a sample
     idx = _sample(count, 1 << 16, cuda)
-    ys, cs = y[idx].cpu().numpy(), cls[idx].cpu().numpy()
+    ys, cs = y[idx].cpu().numpy(), _take(cls, idx).cpu().numpy()
     refi = O.apply_batch(6, 4, w.angles, full, mask, ys, cs, inverse=True, hoist=True)
     check_close(back[idx].cpu().numpy(), refi, ys, "cfg3 inverse sample")

@@ -1,0 +1,102 @@
+"""GPU parity of the composed-operator path (hygt_gemm.cu: per-class M_c on tcgen05, fp16 3-term
+split with per-row power-of-two scaling) against the oracle, over the shapes and edge cases the
+bench does not exercise: N = 64 / 128 / 256, 1 / 3 / 35 classes, ragged tile tails (0, 1, 127,
+128, 129 rows), inter-round and final permutations, in place, rows at extreme magnitudes, zero
+rows, invalid class ids, the fused energy. Tolerances as tests/test_gpu_parity.py."""
+import numpy as np
+import pytest
+import torch
+
+from test_gpu_parity import check_close
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _gemm_on(monkeypatch):
+    monkeypatch.setenv("HYGT_GEMM", "1")
+
+
+def _case(log2n, rounds, classes, perms_kind, seed):
+    from paper_2505_21728_b200 import HyGTModel, HyGTPlan
+    rng = np.random.default_rng(seed)
+    n = 1 << log2n
+    a = rounds * n * log2n // 2
+    angles = rng.uniform(-np.pi, np.pi, (classes, a))
+    perms = np.stack([np.stack([rng.permutation(n) for _ in range(rounds)]) for _ in range(classes)]).astype(np.uint16)
+    mask = {"none": 0, "final": 1 << (rounds - 1), "inter+final": (1 << rounds) - 1}[perms_kind]
+    final = (mask >> (rounds - 1)) & 1
+    models = [HyGTModel(log2n, rounds, angles[c], perms[c, rounds - 1] if final else None) for c in range(classes)]
+    inter = perms[:, : rounds - 1].copy() if mask & ((1 << (rounds - 1)) - 1) else None
+    plan = HyGTPlan(models, inter)
+    assert plan.path == "gemm"
+    return plan, angles, (perms if mask else None), mask, rng
+
+
+@pytest.mark.parametrize("log2n,rounds,classes,perms_kind", [
+    (6, 4, 35, "inter+final"), (6, 2, 1, "none"), (7, 3, 3, "final"), (8, 4, 35, "none"),
+    (8, 2, 3, "inter+final"), (8, 1, 1, "final")])
+@pytest.mark.parametrize("rows", [1, 127, 129, 5000])
+def test_gemm_vs_oracle(cuda, oracle_mod, log2n, rounds, classes, perms_kind, rows):
+    plan, angles, perms, mask, rng = _case(log2n, rounds, classes, perms_kind, 100 * log2n + rows)
+    n = 1 << log2n
+    x = (rng.standard_normal((rows, n)) * 16).astype(np.float32)
+    cls = rng.integers(0, classes, rows).astype(np.uint16)
+    xd = torch.from_numpy(x).to(cuda)
+    cd = torch.from_numpy(cls).to(cuda) if classes > 1 else None
+    y = plan.forward(xd, cd)
+    z = plan.inverse(xd, cd)
+    plan.sync_status()
+    ref = oracle_mod.apply_batch(log2n, rounds, angles, perms, mask, x, cls)
+    refi = oracle_mod.apply_batch(log2n, rounds, angles, perms, mask, x, cls, inverse=True)
+    check_close(y.cpu().numpy(), ref, x, f"gemm fwd N={n}")
+    check_close(z.cpu().numpy(), refi, x, f"gemm inv N={n}")
+    back = plan.inverse(y, cd)
+    check_close(back.cpu().numpy(), x, x, "gemm roundtrip")
+
+
+def test_gemm_empty_inplace_and_energy(cuda, oracle_mod):
+    plan, angles, perms, mask, rng = _case(8, 4, 5, "none", 7)
+    e = torch.zeros(5, 256, dtype=torch.float64, device=cuda)
+    empty = torch.empty(0, 256, device=cuda)
+    plan.forward(empty, torch.empty(0, dtype=torch.uint16, device=cuda))
+    x = (rng.standard_normal((3001, 256)) * 16).astype(np.float32)
+    cls = rng.integers(0, 5, 3001).astype(np.uint16)
+    xd = torch.from_numpy(x).to(cuda)
+    cd = torch.from_numpy(cls).to(cuda)
+    buf = xd.clone()
+    plan.forward_energy(buf, cd, e, out=buf)  # in place
+    plan.sync_status()
+    ref = oracle_mod.apply_batch(8, 4, angles, None, 0, x, cls)
+    check_close(buf.cpu().numpy(), ref, x, "gemm in place")
+    np.testing.assert_allclose(e.cpu().numpy(), oracle_mod.class_energy(8, 4, angles, None, 0, x, cls), rtol=1e-6)
+
+
+@pytest.mark.parametrize("scale", [1e-30, 1e-6, 1.0, 1e6, 1e30])
+def test_gemm_row_scaling_extremes(cuda, oracle_mod, scale):
+    """Each row is scaled by its own power of two before the fp16 split: rows at any magnitude,
+    rows mixing magnitudes, and zero rows keep the fp32 bar relative to their own size."""
+    plan, angles, perms, mask, rng = _case(8, 2, 2, "final", 3)
+    x = (rng.standard_normal((300, 256)) * scale).astype(np.float32)
+    x[5] = 0.0
+    x[7, ::2] *= 1e-4  # mixed magnitudes inside one row
+    cls = rng.integers(0, 2, 300).astype(np.uint16)
+    y = plan.forward(torch.from_numpy(x).to(cuda), torch.from_numpy(cls).to(cuda)).cpu().numpy()
+    ref = oracle_mod.apply_batch(8, 2, angles, perms, mask, x, cls)
+    assert np.all(y[5] == 0.0)
+    for r in range(300):
+        if r == 5:
+            continue
+        err = np.linalg.norm(y[r] - ref[r]) / np.linalg.norm(ref[r])
+        assert err <= 1e-6, f"row {r}: rel {err:.2e}"
+
+
+def test_gemm_invalid_class_ids(cuda):
+    from paper_2505_21728_b200 import ArgumentError
+    plan, angles, perms, mask, rng = _case(8, 2, 3, "none", 9)
+    x = torch.randn(1000, 256, device=cuda)
+    cls = torch.randint(0, 3, (1000,), device=cuda).to(torch.int16).view(torch.uint16)
+    cls.view(torch.int16)[17] = 9
+    plan.forward(x, cls)
+    with pytest.raises(ArgumentError):
+        plan.sync_status()

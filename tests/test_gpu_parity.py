@@ -64,6 +64,18 @@ SEG2_LOG2N = (6,)
 
 
 def _variants(log2n):
+    out = _variants_butterfly(log2n)
+    for v in out:
+        v.setdefault("HYGT_GEMM", "0")
+    if log2n in GEMM_LOG2N:  # composed operator on the tensor cores
+        out.append({"HYGT_GEMM": "1"})
+    return out
+
+
+GEMM_LOG2N = (6, 7, 8)
+
+
+def _variants_butterfly(log2n):
     out = [{"HYGT_JIT": "0", "HYGT_STAGE": "0", "HYGT_TILE": "0", "HYGT_SEGMENT": "0", "HYGT_SEG2": "0",
             "HYGT_CLS": "0", "HYGT_CLS_JIT": "0", "HYGT_LANES_LOG2": str(l)} for l in LAYOUTS[log2n]]
     for v in SEG_VARIANTS.get(log2n, []):
