@@ -27,11 +27,16 @@
 //   warps 0-3   epilogue : TMEM -> registers (tcgen05.ld, lane = row) -> unscale -> swizzled
 //                          staging -> coalesced STG rows; fused per-class energy (fp64)
 //   warps 4-11  split    : rows (LDG, coalesced) -> row max -> scale -> fp16 hi/lo into the
-//                          SWIZZLE_128B K-major A ring (one 64-column K atom per slot)
+//                          tile's SWIZZLE_128B K-major A (KA 64-column K atoms); the row-max
+//                          pass of tile t+1 overlaps the MMAs of tile t
 //   warp 12     producer : cp.async.bulk of the class's B stages (L2 resident, 32 KB each)
 //   warp 13     MMA      : one thread issues tcgen05.mma kind::f16 M=128 N<=128 K=16
-//   TMEM: two N-column fp32 accumulators (tile t and t+1), so the epilogue of one tile
-//   overlaps the MMAs of the next.
+//   warp 14     prefetch : L2 prefetch of the rows two tiles ahead (prefetch.global.L2)
+//   A tile is issued as NH "units" of up to 128 output columns. TMEM: per unit two fp32
+//   accumulators, hi.hi and the two correction terms apart (tensor-core accumulation rounds
+//   each K step against the running sum, so keeping the 2^-11-sized terms out of the big sum
+//   keeps their rounding negligible), double-buffered over units (4 x 128 columns at N >= 128),
+//   so the epilogue of one unit overlaps the MMAs of the next.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -56,27 +61,28 @@ constexpr int EPI_WARPS = 4;
 constexpr int SPLIT_WARPS = 8;
 constexpr int PROD_WARP = EPI_WARPS + SPLIT_WARPS;
 constexpr int MMA_WARP = PROD_WARP + 1;
-constexpr int GEMM_THREADS = (MMA_WARP + 1) * 32;
+constexpr int PF_WARP = MMA_WARP + 1;
+constexpr int GEMM_THREADS = (PF_WARP + 1) * 32;
 constexpr uint32_t ATOM_BYTES = GM * 128;  // one 64-column fp16 K atom of the A tile (16 KB)
 
 template <int NN>
 struct Shape {
-  static constexpr int KA = NN / 64;                 // K atoms
-  static constexpr int NW = NN < 128 ? NN : 128;     // N per MMA instruction
-  static constexpr int NH = NN / NW;                 // N halves
-  static constexpr int S = KA * NH;                  // B stages per tile
-  static constexpr uint32_t STAGE = 2u * NW * 128;   // hi + lo, SW128 K-major
-  static constexpr int NA = KA == 1 ? 2 : 3;         // A ring slots (hi + lo atom each)
-  static constexpr int NB = S == 1 ? 2 : 3;          // B ring slots
-  static constexpr uint32_t A_OFF = 0;
-  static constexpr uint32_t B_OFF = A_OFF + NA * 2 * ATOM_BYTES;
+  static constexpr int KA = NN / 64;                 // K atoms (64 fp16 = one 128 B swizzle row)
+  static constexpr int NW = NN < 128 ? NN : 128;     // N per MMA instruction = columns per unit
+  static constexpr int NH = NN / NW;                 // units (N halves) per tile
+  static constexpr uint32_t STAGE = 2u * NW * 128;   // B stage (one K atom of one unit): hi + lo
+  static constexpr int NB = 2;                       // B ring stages
+  static constexpr uint32_t A_OFF = 0;               // the tile's whole A (KA atoms, hi + lo)
+  static constexpr uint32_t B_OFF = A_OFF + KA * 2 * ATOM_BYTES;
   static constexpr uint32_t STG_OFF = B_OFF + NB * STAGE;
   static constexpr uint32_t STG_BYTES = 32 * 128;    // per epilogue warp: 32 rows x 32 floats
   static constexpr uint32_t EN_OFF = STG_OFF + EPI_WARPS * STG_BYTES;
   static constexpr uint32_t FAC_OFF = EN_OFF + EPI_WARPS * NN * 8;
   static constexpr uint32_t BAR_OFF = FAC_OFF + 4 * GM * 4;
-  static constexpr uint32_t SMEM = BAR_OFF + 256 + 1024;  // + alignment slack
-  static constexpr uint32_t TMEM_COLS = 2 * NN < 32 ? 32 : 2 * NN;
+  static constexpr uint32_t SMEM = BAR_OFF + 256;
+  // TMEM: per unit a "big" accumulator (hi.hi) and a "small" one (lo.hi + hi.lo), NW columns
+  // each, double-buffered over units: 4 NW <= 512 columns
+  static constexpr uint32_t TMEM_COLS = 4 * NW < 32 ? 32 : 4 * NW;
   static constexpr int RG = GM / SPLIT_WARPS / 4;    // 4-row groups per split warp
 };
 
@@ -165,15 +171,21 @@ struct TileMap {
   }
 };
 
+// debug trace (hygt_debug_gemm_trace): clock64 of per-tile pipeline events in CTA 0
+#define GEMM_TRACE(k, e)                                                   \
+  do {                                                                     \
+    if (P.trace && blockIdx.x == 0 && (k) < 64) P.trace[(k) * 16 + (e)] = clock64(); \
+  } while (0)
+
 template <int NN, bool ENERGY>
 __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmParams P) {
   using SH = Shape<NN>;
-  extern __shared__ __align__(16) unsigned char gemm_smem_raw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gemm_smem_raw) + 1023) & ~(uintptr_t)1023);
+  // 1024 B aligned (SWIZZLE_128B atoms); declared shared so every access compiles to LDS/STS
+  extern __shared__ __align__(1024) unsigned char sm[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + SH::BAR_OFF);
-  uint64_t* a_full = bars;                     // [NA]  count SPLIT_WARPS
-  uint64_t* a_empty = a_full + SH::NA;         // [NA]  tcgen05.commit
-  uint64_t* b_full = a_empty + SH::NA;         // [NB]  expect_tx
+  uint64_t* a_full = bars;                     // [KA]  atom written, count SPLIT_WARPS
+  uint64_t* a_empty = a_full + SH::KA;         // [1]   all units of the tile issued (commit)
+  uint64_t* b_full = a_empty + 1;              // [NB]  expect_tx
   uint64_t* b_empty = b_full + SH::NB;         // [NB]  tcgen05.commit
   uint64_t* d_full = b_empty + SH::NB;         // [2]   tcgen05.commit
   uint64_t* d_empty = d_full + 2;              // [2]   count EPI_WARPS
@@ -211,7 +223,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    for (int i = 0; i < SH::NA; ++i) { mbar_init(&a_full[i], SPLIT_WARPS); mbar_init(&a_empty[i], 1); }
+    for (int i = 0; i < SH::KA; ++i) mbar_init(&a_full[i], SPLIT_WARPS);
+    mbar_init(a_empty, 1);
     for (int i = 0; i < SH::NB; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&d_full[i], 1); mbar_init(&d_empty[i], EPI_WARPS); }
     for (int i = 0; i < 4; ++i) { mbar_init(&f_full[i], SPLIT_WARPS); mbar_init(&f_empty[i], EPI_WARPS); }
@@ -227,34 +240,38 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
 
   if (warp == MMA_WARP) {
     // ------------------------------------------------------------------ MMA issuer ----
+    // Per tile, NH units (N halves) in order; per unit all K atoms x 4 K steps x 3 terms.
+    // Unit u accumulates into buffer u & 1: big at 2 NW (u & 1), small NW columns after it.
     if (lane == 0) {
-      uint32_t ia = 0, ib = 0, k = 0;
+      uint32_t ib = 0, u = 0, k = 0;
       for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
-        const int db = (int)(k & 1);
-        if (k >= 2) mbar_wait(&d_empty[db], ((k >> 1) - 1) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t d0 = tmem + (uint32_t)(db * NN);
-        for (int ka = 0; ka < SH::KA; ++ka, ++ia) {
-          const int sa = (int)(ia % SH::NA);
-          mbar_wait(&a_full[sa], (ia / SH::NA) & 1);
+        for (int nh = 0; nh < SH::NH; ++nh, ++u) {
+          const int db = (int)(u & 1);
+          if (u >= 2) mbar_wait(&d_empty[db], ((u >> 1) - 1) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
-          const uint32_t ahi = smem_u32(sm + SH::A_OFF + (uint32_t)sa * 2 * ATOM_BYTES);
-          const uint32_t alo = ahi + ATOM_BYTES;
-          for (int nh = 0; nh < SH::NH; ++nh, ++ib) {
+          if (nh == 0) GEMM_TRACE(k, 3);
+          const uint32_t dbig = tmem + (uint32_t)(db * 2 * SH::NW), dsmall = dbig + (uint32_t)SH::NW;
+          for (int ka = 0; ka < SH::KA; ++ka, ++ib) {
+            if (nh == 0) mbar_wait(&a_full[ka], k & 1);
             const int sb = (int)(ib % SH::NB);
             mbar_wait(&b_full[sb], (ib / SH::NB) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
+            if (nh < 2 && ka < 4) GEMM_TRACE(k, 8 + nh * 4 + ka);
+            const uint32_t ahi = smem_u32(sm + SH::A_OFF + (uint32_t)ka * 2 * ATOM_BYTES);
+            const uint32_t alo = ahi + ATOM_BYTES;
             const uint32_t bhi = smem_u32(sm + SH::B_OFF + (uint32_t)sb * SH::STAGE);
             const uint32_t blo = bhi + SH::STAGE / 2;
-            const uint32_t d = d0 + (uint32_t)(nh * SH::NW);
+            // hi.hi accumulates into the big accumulator; the two correction terms (2^-11 of it)
+            // into the small one, so only 16 K steps per output round against the full-size sum
 #pragma unroll
             for (int j = 0; j < 4; ++j) {  // K = 16 fp16 = 32 B per instruction
               const uint32_t o = 32u * j;
               const uint64_t da[3] = {desc_sw128(alo + o), desc_sw128(ahi + o), desc_sw128(ahi + o)};
               const uint64_t dbd[3] = {desc_sw128(bhi + o), desc_sw128(blo + o), desc_sw128(bhi + o)};
 #pragma unroll
-              for (int term = 0; term < 3; ++term) {  // small terms first
-                const uint32_t acc = (ka | j | term) ? 1u : 0u;
+              for (int term = 0; term < 3; ++term) {
+                const uint32_t acc = (ka | j | (term == 1)) ? 1u : 0u;
+                const uint32_t d = term < 2 ? dsmall : dbig;
                 asm volatile(
                     "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                     "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n"
@@ -263,13 +280,48 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
             }
             tc_commit(&b_empty[sb]);
           }
-          tc_commit(&a_empty[sa]);
+          tc_commit(&d_full[db]);
         }
-        tc_commit(&d_full[db]);
+        tc_commit(a_empty);  // the tile's A may be overwritten once these MMAs completed
+        GEMM_TRACE(k, 4);
       }
+    }
+  } else if (warp == PF_WARP) {
+    // ------------------------------------------------------------------ row prefetch --
+    // L2 prefetch (prefetch.global.L2, per 128 B line: the LSU path, so the B stage copies in
+    // the bulk-copy engine never queue behind this HBM traffic) of the rows of the tile
+    // PF_AHEAD steps ahead, paced by the split warps' progress (f_full: row maxima of tile k
+    // done), so the split's loads hit L2.
+    constexpr int PF_AHEAD = 2;
+    auto prefetch_rows = [&](uint32_t tp) {
+      if (tp >= ntiles) return;
+      int c;
+      uint64_t p0;
+      uint32_t rows;
+      tm.of(tp, c, p0, rows);
+      uint32_t id[GM / 32];
+#pragma unroll
+      for (int i = 0; i < GM / 32; ++i) {
+        const uint32_t r = (uint32_t)(lane + 32 * i);
+        id[i] = r < rows ? row_at(P, p0 + r) : 0xffffffffu;
+      }
+#pragma unroll
+      for (int i = 0; i < GM / 32; ++i)
+        if (id[i] != 0xffffffffu)
+#pragma unroll
+          for (int l = 0; l < NN / 32; ++l)
+            asm volatile("prefetch.global.L2 [%0];" :: "l"(P.x + (size_t)id[i] * NN + l * 32) : "memory");
+    };
+    for (int a = 0; a < PF_AHEAD; ++a) prefetch_rows(blockIdx.x + (uint32_t)a * gridDim.x);
+    uint32_t k = 0;
+    for (uint32_t t = blockIdx.x + PF_AHEAD * gridDim.x; t < ntiles; t += gridDim.x, ++k) {
+      mbar_wait(&f_full[k & 3], (k >> 2) & 1);
+      prefetch_rows(t);
     }
   } else if (warp == PROD_WARP) {
     // ------------------------------------------------------------------ B producer ----
+    // Lane 0: the B stages of each unit of each tile, in the MMA's order (unit outer, K atom
+    // inner), into the NB-stage ring.
     if (lane == 0) {
       uint32_t ib = 0;
       for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -277,78 +329,108 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
         uint64_t p0;
         uint32_t rows;
         tm.of(t, c, p0, rows);
-        const unsigned char* src = P.bops + (size_t)c * SH::S * SH::STAGE;
-        for (int s = 0; s < SH::S; ++s, ++ib) {
-          const int sb = (int)(ib % SH::NB);
-          if (ib >= (uint32_t)SH::NB) mbar_wait(&b_empty[sb], ((ib / SH::NB) - 1) & 1);
-          mbar_expect_tx(&b_full[sb], SH::STAGE);
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-              :: "r"(smem_u32(sm + SH::B_OFF + (uint32_t)sb * SH::STAGE)), "l"(src + (size_t)s * SH::STAGE),
-                 "r"(SH::STAGE), "r"(smem_u32(&b_full[sb])) : "memory");
-        }
+        const unsigned char* src = P.bops + (size_t)c * SH::KA * SH::NH * SH::STAGE;
+        for (int nh = 0; nh < SH::NH; ++nh)
+          for (int ka = 0; ka < SH::KA; ++ka, ++ib) {
+            const int sb = (int)(ib % SH::NB);
+            if (ib >= (uint32_t)SH::NB) mbar_wait(&b_empty[sb], ((ib / SH::NB) - 1) & 1);
+            mbar_expect_tx(&b_full[sb], SH::STAGE);
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                :: "r"(smem_u32(sm + SH::B_OFF + (uint32_t)sb * SH::STAGE)),
+                   "l"(src + (size_t)(ka * SH::NH + nh) * SH::STAGE), "r"(SH::STAGE),
+                   "r"(smem_u32(&b_full[sb])) : "memory");
+          }
       }
     }
   } else if (warp >= EPI_WARPS) {
     // ------------------------------------------------------------------ split warps ---
     const int sw = warp - EPI_WARPS;
     const int g8 = lane >> 3, l8 = lane & 7;  // row within a 4-row group, lane within the row
-    uint32_t ia = 0, k = 0;
+    // Rows of 4-row group g: one 64-bit store instruction writes 64 B of each of its 4 rows
+    // and is served in two 16-lane phases. Rows {0, 4} (lanes 0-15) and {1, 5} (lanes 16-31)
+    // of an 8-row block fall in opposite halves of the SWIZZLE_128B pattern, so each phase
+    // covers all 32 banks once: 2 wavefronts per instruction, the minimum.
+    auto row_of_group = [&](int g) {
+      const int b16 = (sw * SH::RG + g) >> 2, gg = (sw * SH::RG + g) & 3;
+      return b16 * 16 + (gg & 1) * 2 + (gg >> 1) * 8 + (g8 >> 1) + (g8 & 1) * 4;
+    };
+    uint32_t k = 0;
     for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
       int c;
       uint64_t p0;
       uint32_t rows;
       tm.of(t, c, p0, rows);
-      // pass 1: row max -> scale (rows of this warp: sw * RG * 4 + g * 4 + g8)
+      if (sw == 0 && lane == 0) GEMM_TRACE(k, 0);
+      // pass 1 (overlaps the MMAs of the previous tile): row max -> power-of-two scale
       float scl[SH::RG];
       uint32_t rid[SH::RG];
 #pragma unroll
       for (int g = 0; g < SH::RG; ++g) {
-        const int r = (sw * SH::RG + g) * 4 + g8;
-        const bool ok = (uint32_t)r < rows;
-        rid[g] = ok ? row_at(P, p0 + r) : 0xffffffffu;
-        float mx = 0.f;
-        if (ok) {
-          const float4* src = reinterpret_cast<const float4*>(P.x + (size_t)rid[g] * NN);
+        const int r = row_of_group(g);
+        rid[g] = (uint32_t)r < rows ? row_at(P, p0 + r) : 0xffffffffu;
+      }
+      float mxs[SH::RG];
+      constexpr int NV = NN / 32;
 #pragma unroll
-          for (int i = 0; i < NN / 32; ++i) {
-            const float4 v = __ldcg(src + i * 8 + l8);  // L2-allocating: pass 2 re-reads it
-            mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
-          }
+      for (int g0 = 0; g0 < SH::RG; g0 += 2) {  // two row groups' loads in flight at a time
+        float4 v[2][NV];
+#pragma unroll
+        for (int gg = 0; gg < 2; ++gg) {
+          const uint32_t id = rid[g0 + gg];
+          const float4* src = reinterpret_cast<const float4*>(P.x + (size_t)(id != 0xffffffffu ? id : 0u) * NN);
+#pragma unroll
+          for (int i = 0; i < NV; ++i)
+            v[gg][i] = id != 0xffffffffu ? __ldcg(src + i * 8 + l8) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
+#pragma unroll
+        for (int gg = 0; gg < 2; ++gg) {
+          float mx = 0.f;
+#pragma unroll
+          for (int i = 0; i < NV; ++i)
+            mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[gg][i].x), fabsf(v[gg][i].y)), fmaxf(fabsf(v[gg][i].z), fabsf(v[gg][i].w))));
+          mxs[g0 + gg] = mx;
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < SH::RG; ++g) {
+        float mx = mxs[g];
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
         scl[g] = row_scale(mx);
       }
-      // row unscale factors for the epilogue: 1 / s (power of two, exact)
-      {
+      if (sw == 0 && lane == 0) GEMM_TRACE(k, 1);
+      {  // row unscale factors for the epilogue: 1 / s (power of two, exact)
         const int fb = (int)(k & 3);
         if (k >= 4) mbar_wait(&f_empty[fb], ((k >> 2) - 1) & 1);  // tile k-4's factors were read
         if (l8 == 0) {
 #pragma unroll
-          for (int g = 0; g < SH::RG; ++g) fac[fb * GM + (sw * SH::RG + g) * 4 + g8] = 1.f / scl[g];
+          for (int g = 0; g < SH::RG; ++g) fac[fb * GM + row_of_group(g)] = 1.f / scl[g];
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&f_full[fb]);
       }
-      // pass 2: per K atom, the atom's 64 columns of each row -> fp16 hi / lo in the A ring
-      for (int ka = 0; ka < SH::KA; ++ka, ++ia) {
-        const int sa = (int)(ia % SH::NA);
-        if (ia >= (uint32_t)SH::NA) mbar_wait(&a_empty[sa], ((ia / SH::NA) - 1) & 1);
-        unsigned char* ahi = sm + SH::A_OFF + (uint32_t)sa * 2 * ATOM_BYTES;
+      // pass 2: once the previous tile's MMAs have read A, each K atom's 64 columns of every
+      // row -> fp16 hi / lo (L2 hits), one a_full arrival per atom so the MMAs follow closely
+      if (k >= 1) mbar_wait(a_empty, (k - 1) & 1);
+      for (int ka = 0; ka < SH::KA; ++ka) {
+        unsigned char* ahi = sm + SH::A_OFF + (uint32_t)ka * 2 * ATOM_BYTES;
         unsigned char* alo = ahi + ATOM_BYTES;
+        float4 va[SH::RG][2];
 #pragma unroll
-        for (int g = 0; g < SH::RG; ++g) {
-          const int r = (sw * SH::RG + g) * 4 + g8;
-          float4 v[2];
+        for (int g = 0; g < SH::RG; ++g)
 #pragma unroll
           for (int h = 0; h < 2; ++h)  // columns 64 ka + 32 h + 4 l8 .. +3
-            v[h] = rid[g] != 0xffffffffu
-                       ? __ldcs(reinterpret_cast<const float4*>(P.x + (size_t)rid[g] * NN + 64 * ka + 32 * h) + l8)
-                       : make_float4(0.f, 0.f, 0.f, 0.f);
+            va[g][h] = rid[g] != 0xffffffffu
+                           ? __ldcs(reinterpret_cast<const float4*>(P.x + (size_t)rid[g] * NN + 64 * ka + 32 * h) + l8)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int g = 0; g < SH::RG; ++g) {
+          const int r = row_of_group(g);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
+            const float4* v = va[g];
             const float s = scl[g];
             const float a0 = v[h].x * s, a1 = v[h].y * s, a2 = v[h].z * s, a3 = v[h].w * s;
             const uint32_t h01 = pack_h2(a0, a1), h23 = pack_h2(a2, a3);
@@ -362,8 +444,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic stores -> tensor core reads
         __syncwarp();
-        if (lane == 0) mbar_arrive(&a_full[sa]);
+        if (lane == 0) mbar_arrive(&a_full[ka]);
       }
+      if (sw == 0 && lane == 0) GEMM_TRACE(k, 2);
     }
     // rows with an invalid class id (bucket C): copied through, the error is flagged by hygt_bucket
     if (C > 0 && P.seg_end) {
@@ -395,7 +478,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
       }
     };
     const int r_th = warp * 32 + lane;  // TMEM lane = tile row of this thread
-    uint32_t k = 0;
+    uint32_t k = 0, u = 0;
     for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
       int c;
       uint64_t p0;
@@ -405,10 +488,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
         flush_energy();
         en_class = c;
       }
-      const int db = (int)(k & 1);
       mbar_wait(&f_full[k & 3], (k >> 2) & 1);
-      mbar_wait(&d_full[db], (k >> 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;");
       const float f_row = fac[(k & 3) * GM + r_th] * __ldg(P.unscale + c);
       __syncwarp();
       if (lane == 0) mbar_arrive(&f_empty[k & 3]);
@@ -419,65 +499,81 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
         const int r = warp * 32 + 4 * i + (lane >> 3);
         orow[i] = (uint32_t)r < rows ? row_at(P, p0 + r) : 0xffffffffu;
       }
-      for (int cb = 0; cb < NN / 32; ++cb) {
-        uint32_t v[32];
-        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(db * NN + cb * 32);
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;");
-        if (cb == NN / 32 - 1) {  // accumulator fully read: release it to the MMA of tile k + 2
-          asm volatile("tcgen05.fence::before_thread_sync;");
+      for (int nh = 0; nh < SH::NH; ++nh, ++u) {
+        const int db = (int)(u & 1);
+        mbar_wait(&d_full[db], (u >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (nh == 0 && warp == 0 && lane == 0) GEMM_TRACE(k, 5);
+        for (int cb = 0; cb < SH::NW / 32; ++cb) {
+          uint32_t v[32], w[32];
+          const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(db * 2 * SH::NW + cb * 32);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+              "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+              : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]),
+                "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]), "=r"(w[15]),
+                "=r"(w[16]), "=r"(w[17]), "=r"(w[18]), "=r"(w[19]), "=r"(w[20]), "=r"(w[21]), "=r"(w[22]), "=r"(w[23]),
+                "=r"(w[24]), "=r"(w[25]), "=r"(w[26]), "=r"(w[27]), "=r"(w[28]), "=r"(w[29]), "=r"(w[30]), "=r"(w[31])
+              : "r"(taddr + (uint32_t)SH::NW));
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+              "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+                "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+                "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;");
+          if (cb == SH::NW / 32 - 1) {  // unit accumulators fully read: release them to unit u + 2
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&d_empty[db]);
+          }
+          // big + small, unscale, then thread-per-row -> swizzled staging [32 rows][32 floats]
+          auto acc_at = [&](int i) { return (__uint_as_float(v[i]) + __uint_as_float(w[i])) * f_row; };
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            *reinterpret_cast<float4*>(stg + swz(lane, q)) =
+                make_float4(acc_at(4 * q), acc_at(4 * q + 1), acc_at(4 * q + 2), acc_at(4 * q + 3));
           __syncwarp();
-          if (lane == 0) mbar_arrive(&d_empty[db]);
-        }
-        // unscale, then thread-per-row -> swizzled staging [32 rows][32 floats]
+          // coalesced: 8 lanes per row, 4 rows per instruction
+          const int col0 = nh * SH::NW + cb * 32;
+          float e0 = 0.f, e1 = 0.f, e2 = 0.f, e3 = 0.f;
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          *reinterpret_cast<float4*>(stg + swz(lane, q)) =
-              make_float4(__uint_as_float(v[4 * q]) * f_row, __uint_as_float(v[4 * q + 1]) * f_row,
-                          __uint_as_float(v[4 * q + 2]) * f_row, __uint_as_float(v[4 * q + 3]) * f_row);
-        __syncwarp();
-        // coalesced: 8 lanes per row, 4 rows per instruction
-        float e0 = 0.f, e1 = 0.f, e2 = 0.f, e3 = 0.f;
+          for (int i = 0; i < 8; ++i) {
+            const int rr = 4 * i + (lane >> 3);
+            const float4 o = *reinterpret_cast<const float4*>(stg + swz(rr, lane & 7));
+            if (orow[i] != 0xffffffffu) {
+              __stcs(reinterpret_cast<float4*>(P.y + (size_t)orow[i] * NN + col0) + (lane & 7), o);
+              if (ENERGY) {
+                e0 = fmaf(o.x, o.x, e0);
+                e1 = fmaf(o.y, o.y, e1);
+                e2 = fmaf(o.z, o.z, e2);
+                e3 = fmaf(o.w, o.w, e3);
+              }
+            }
+          }
+          __syncwarp();  // staging reads done before the next column block overwrites it
+          if (ENERGY) {  // fp32 sums of 8 rows, then fp64 across the warp's 4 row groups
+            double d0 = e0, d1 = e1, d2 = e2, d3 = e3;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int rr = 4 * i + (lane >> 3);
-          const float4 o = *reinterpret_cast<const float4*>(stg + swz(rr, lane & 7));
-          if (orow[i] != 0xffffffffu) {
-            __stcs(reinterpret_cast<float4*>(P.y + (size_t)orow[i] * NN + cb * 32) + (lane & 7), o);
-            if (ENERGY) {
-              e0 = fmaf(o.x, o.x, e0);
-              e1 = fmaf(o.y, o.y, e1);
-              e2 = fmaf(o.z, o.z, e2);
-              e3 = fmaf(o.w, o.w, e3);
+            for (int o = 8; o < 32; o <<= 1) {
+              d0 += __shfl_xor_sync(0xffffffffu, d0, o);
+              d1 += __shfl_xor_sync(0xffffffffu, d1, o);
+              d2 += __shfl_xor_sync(0xffffffffu, d2, o);
+              d3 += __shfl_xor_sync(0xffffffffu, d3, o);
+            }
+            if (lane < 8) {
+              double* e = en + col0 + lane * 4;
+              e[0] += d0;
+              e[1] += d1;
+              e[2] += d2;
+              e[3] += d3;
             }
           }
         }
-        __syncwarp();  // staging reads done before the next column block overwrites it
-        if (ENERGY) {  // fp32 sums of 8 rows, then fp64 across the warp's 4 row groups
-          double d0 = e0, d1 = e1, d2 = e2, d3 = e3;
-#pragma unroll
-          for (int o = 8; o < 32; o <<= 1) {
-            d0 += __shfl_xor_sync(0xffffffffu, d0, o);
-            d1 += __shfl_xor_sync(0xffffffffu, d1, o);
-            d2 += __shfl_xor_sync(0xffffffffu, d2, o);
-            d3 += __shfl_xor_sync(0xffffffffu, d3, o);
-          }
-          if (lane < 8) {
-            double* e = en + cb * 32 + lane * 4;
-            e[0] += d0;
-            e[1] += d1;
-            e[2] += d2;
-            e[3] += d3;
-          }
-        }
       }
+      if (warp == 0 && lane == 0) GEMM_TRACE(k, 6);
     }
     flush_energy();
   }
@@ -605,10 +701,13 @@ int launch_one(const GemmParams& P, int num_sms, cudaStream_t st) {
 }
 }  // namespace
 
+unsigned long long* g_gemm_trace = nullptr;  // debug hook (hygt_debug_gemm_trace)
+
 int gemm_run(const GemmOperands& g, const float* x, float* y, const uint32_t* idx,
              const uint32_t* seg_end, uint64_t count, double* energy, cudaStream_t st) {
   if (!count) return HYGT_OK;
   GemmParams P{};
+  P.trace = g_gemm_trace;
   P.x = x;
   P.y = y;
   P.idx = idx;
@@ -629,3 +728,10 @@ int gemm_run(const GemmOperands& g, const float* x, float* y, const uint32_t* id
 }
 
 }  // namespace hygt_gpu
+
+// Debug hook (not part of the public header): per-tile clock64 events of CTA 0 of the next
+// tensor-core launches are written to dev[k * 8 + e] (k < 64; e: 0/1/2 split pass-1 start /
+// pass-1 end / atoms written, 3/4 MMA start / committed, 5/6 epilogue start / end); nullptr off.
+extern "C" void hygt_debug_gemm_trace(void* dev) {
+  hygt_gpu::g_gemm_trace = static_cast<unsigned long long*>(dev);
+}

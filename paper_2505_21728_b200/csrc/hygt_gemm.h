@@ -19,6 +19,7 @@ struct GemmParams {
   const unsigned char* bops; // [C][stages][hi | lo][NW x 128 B] fp16, SWIZZLE_128B K-major
   const float* unscale;      // [C] 2^-kB
   double* energy;            // [C][N] fp64 (forward with energy) or nullptr
+  unsigned long long* trace; // debug: per-tile clock64 events of CTA 0 ([64][16]) or nullptr
 };
 
 struct GemmOperands {  // one direction
