@@ -43,6 +43,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -65,13 +66,15 @@ constexpr int PF_WARP = MMA_WARP + 1;
 constexpr int GEMM_THREADS = (PF_WARP + 1) * 32;
 constexpr uint32_t ATOM_BYTES = GM * 128;  // one 64-column fp16 K atom of the A tile (16 KB)
 
-template <int NN>
+template <int NN, bool PAIR>
 struct Shape {
   static constexpr int KA = NN / 64;                 // K atoms (64 fp16 = one 128 B swizzle row)
   static constexpr int NW = NN < 128 ? NN : 128;     // N per MMA instruction = columns per unit
   static constexpr int NH = NN / NW;                 // units (N halves) per tile
-  static constexpr uint32_t STAGE = 2u * NW * 128;   // B stage (one K atom of one unit): hi + lo
-  static constexpr int NB = 2;                       // B ring stages
+  static constexpr int BW = PAIR ? NW / 2 : NW;      // B rows (output columns) held by this CTA
+  static constexpr uint32_t STAGE = 2u * BW * 128;   // B stage (one K atom of one unit): hi + lo
+  static constexpr int NB = PAIR ? 4 : 2;            // B ring stages
+  static constexpr int TG = PAIR ? 2 * GM : GM;      // rows per tile (a CTA pair: 128 each)
   static constexpr uint32_t A_OFF = 0;               // the tile's whole A (KA atoms, hi + lo)
   static constexpr uint32_t B_OFF = A_OFF + KA * 2 * ATOM_BYTES;
   static constexpr uint32_t STG_OFF = B_OFF + NB * STAGE;
@@ -79,7 +82,7 @@ struct Shape {
   static constexpr uint32_t EN_OFF = STG_OFF + EPI_WARPS * STG_BYTES;
   static constexpr uint32_t FAC_OFF = EN_OFF + EPI_WARPS * NN * 8;
   static constexpr uint32_t BAR_OFF = FAC_OFF + 4 * GM * 4;
-  static constexpr uint32_t SMEM = BAR_OFF + 256;
+  static constexpr uint32_t SMEM = BAR_OFF + 512;  // barriers (<= 40 x 8 B) + the TMEM address
   // TMEM: per unit a "big" accumulator (hi.hi) and a "small" one (lo.hi + hi.lo), NW columns
   // each, double-buffered over units: 4 NW <= 512 columns
   static constexpr uint32_t TMEM_COLS = 4 * NW < 32 ? 32 : 4 * NW;
@@ -97,14 +100,49 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(b)), "r"(bytes) : "memory");
 }
+// CTA-scope acquire, also for the barriers the peer CTA arrives on: what crosses CTAs is
+// shared-memory data read by the tensor cores (ordered by fence.proxy.async before the
+// arrival) and TMEM (ordered by the tcgen05 fences); a cluster-scope acquire would invalidate
+// L1 (CCTL.IVALL) on every wait
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P;\n\tW%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%0], %1;\n\t@!P bra W%=;\n\t}\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t@!P bra W%=;\n\t}\n"
       :: "r"(smem_u32(b)), "r"(parity) : "memory");
 }
+// arrive on the barrier at the same offset in CTA `cta` of the cluster (default semantics:
+// a cluster-scope release would drain every outstanding global access first)
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* b, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}\n"
+      :: "r"(smem_u32(b)), "r"(cta) : "memory");
+}
+template <bool PAIR>
 __device__ __forceinline__ void tc_commit(uint64_t* b) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(smem_u32(b)) : "memory");
+  if constexpr (PAIR)  // the pair's MMAs done: arrive on the barrier in both CTAs
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 :: "r"(smem_u32(b)), "h"((uint16_t)3) : "memory");
+  else
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id() {
+  uint32_t r;
+  asm("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_count() {
+  uint32_t r;
+  asm("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 // SWIZZLE_128B K-major UMMA shared-memory descriptor: 8-row x 128 B atoms, 1024 B apart (SBO).
 __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
@@ -116,9 +154,9 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
   d |= (uint64_t)2 << 61;            // SWIZZLE_128B
   return d;
 }
-// Instruction descriptor: D f32, A/B f16, both K-major, M = 128, N = n.
-__host__ __device__ constexpr uint32_t idesc_f16(int n) {
-  return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(GM >> 4) << 24);
+// Instruction descriptor: D f32, A/B f16, both K-major, M = m, N = n.
+__host__ __device__ constexpr uint32_t idesc_f16(int n, int m = GM) {
+  return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 // swizzled byte offset of 16 B chunk q of row r inside an SW128 atom
 __device__ __forceinline__ uint32_t swz(int r, int q) { return (uint32_t)r * 128u + (uint32_t)((q ^ (r & 7)) << 4); }
@@ -150,11 +188,13 @@ __device__ __forceinline__ uint32_t row_at(const GemmParams& P, uint64_t p) {
   return P.idx ? __ldg(P.idx + p) : (uint32_t)p;
 }
 
-// tile -> (class, first bucketed position, rows)
+// tile -> (class, first bucketed position, rows) of this CTA's part of the tile: a tile is TG
+// rows of one class; in the CTA-pair variant rank 0 takes its first 128 rows, rank 1 the rest
 struct TileMap {
   const uint32_t* tile_end;  // shared: [C] cumulative tile counts
   const GemmParams* P;
   int classes;
+  uint32_t tg, part;         // rows per tile, this CTA's offset in the tile (0 or 128)
   __device__ void of(uint32_t t, int& c, uint64_t& p0, uint32_t& rows) const {
     int lo = 0, hi = classes - 1;
     while (lo < hi) {
@@ -165,8 +205,8 @@ struct TileMap {
     const uint32_t first_tile = c ? tile_end[c - 1] : 0u;
     const uint64_t s0 = c ? seg_at(*P, c - 1) : 0ull;
     const uint64_t s1 = seg_at(*P, c);
-    p0 = s0 + (uint64_t)(t - first_tile) * GM;
-    const uint64_t left = s1 - p0;
+    p0 = s0 + (uint64_t)(t - first_tile) * tg + part;
+    const uint64_t left = s1 > p0 ? s1 - p0 : 0ull;
     rows = left < GM ? (uint32_t)left : GM;
   }
 };
@@ -177,25 +217,34 @@ struct TileMap {
     if (P.trace && blockIdx.x == 0 && (k) < 64) P.trace[(k) * 16 + (e)] = clock64(); \
   } while (0)
 
-template <int NN, bool ENERGY>
+template <int NN, bool ENERGY, bool PAIR>
 __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmParams P) {
-  using SH = Shape<NN>;
+  using SH = Shape<NN, PAIR>;
   // 1024 B aligned (SWIZZLE_128B atoms); declared shared so every access compiles to LDS/STS
   extern __shared__ __align__(1024) unsigned char sm[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + SH::BAR_OFF);
   uint64_t* a_full = bars;                     // [KA]  atom written, count SPLIT_WARPS
-  uint64_t* a_empty = a_full + SH::KA;         // [1]   all units of the tile issued (commit)
-  uint64_t* b_full = a_empty + 1;              // [NB]  expect_tx
+  uint64_t* a_empty = a_full + SH::KA;         // [KA]  atom read by the tile's last unit (commit)
+  uint64_t* b_full = a_empty + SH::KA;         // [NB]  expect_tx
   uint64_t* b_empty = b_full + SH::NB;         // [NB]  tcgen05.commit
   uint64_t* d_full = b_empty + SH::NB;         // [2]   tcgen05.commit
   uint64_t* d_empty = d_full + 2;              // [2]   count EPI_WARPS
   uint64_t* f_full = d_empty + 2;              // [4]   row scales written, count SPLIT_WARPS
   uint64_t* f_empty = f_full + 4;              // [4]   row scales read, count EPI_WARPS
-  uint32_t* tmem_sh = reinterpret_cast<uint32_t*>(f_empty + 4);
+  uint64_t* b_peer = f_empty + 4;              // [NB]  pair: the peer's B half landed (count 1)
+  uint32_t* tmem_sh = reinterpret_cast<uint32_t*>(b_peer + SH::NB);
+  static_assert(SH::KA * 2 + SH::NB * 3 + 12 <= 62, "barrier area");
   __shared__ uint32_t tile_end_sh[HYGT_GEMM_MAX_CLASSES];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int C = P.classes;
+  // CTA pair (cluster of 2, tcgen05 cta_group::2): rank 0 issues the MMAs of both; every
+  // hand-off the MMA issuer waits for is counted on rank 0's barriers, every completion it
+  // signals is multicast to both CTAs
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  const uint32_t t_first = PAIR ? cluster_id() : blockIdx.x;
+  const uint32_t t_step = PAIR ? cluster_count() : gridDim.x;
+  const uint32_t pn = PAIR ? 2u : 1u;  // arrivals per hand-off counted on rank 0
   // per-class cumulative tile counts
   if (warp == 0) {
     uint32_t run = 0;
@@ -205,7 +254,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
       if (c < C) {
         const uint64_t s0 = c ? seg_at(P, c - 1) : 0ull;
         const uint64_t s1 = seg_at(P, c);
-        nt = (uint32_t)((s1 - s0 + GM - 1) / GM);
+        nt = (uint32_t)((s1 - s0 + SH::TG - 1) / SH::TG);
       }
       uint32_t v = nt;
 #pragma unroll
@@ -217,24 +266,29 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
       run += __shfl_sync(0xffffffffu, v, 31);
     }
   }
-  if (warp == MMA_WARP) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                 :: "r"(smem_u32(tmem_sh)), "r"(SH::TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  if (warp == MMA_WARP) {  // in the pair variant both CTAs allocate, with the same warp
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                   :: "r"(smem_u32(tmem_sh)), "r"(SH::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                   :: "r"(smem_u32(tmem_sh)), "r"(SH::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   if (tid == 0) {
-    for (int i = 0; i < SH::KA; ++i) mbar_init(&a_full[i], SPLIT_WARPS);
-    mbar_init(a_empty, 1);
-    for (int i = 0; i < SH::NB; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&d_full[i], 1); mbar_init(&d_empty[i], EPI_WARPS); }
+    for (int i = 0; i < SH::KA; ++i) { mbar_init(&a_full[i], SPLIT_WARPS * pn); mbar_init(&a_empty[i], 1); }
+    for (int i = 0; i < SH::NB; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); mbar_init(&b_peer[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&d_full[i], 1); mbar_init(&d_empty[i], EPI_WARPS * pn); }
     for (int i = 0; i < 4; ++i) { mbar_init(&f_full[i], SPLIT_WARPS); mbar_init(&f_empty[i], EPI_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync(); else __syncthreads();  // barriers initialised in both CTAs
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_sh;
-  const TileMap tm{tile_end_sh, &P, C};
+  const TileMap tm{tile_end_sh, &P, C, (uint32_t)SH::TG, rank * (uint32_t)GM};
   const uint32_t ntiles = C ? tile_end_sh[C - 1] : 0u;
   float* fac = reinterpret_cast<float*>(sm + SH::FAC_OFF);  // [4][GM] per-row unscale factors
 
@@ -242,9 +296,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
     // ------------------------------------------------------------------ MMA issuer ----
     // Per tile, NH units (N halves) in order; per unit all K atoms x 4 K steps x 3 terms.
     // Unit u accumulates into buffer u & 1: big at 2 NW (u & 1), small NW columns after it.
-    if (lane == 0) {
+    if (PAIR && rank == 1) {
+      // the peer forwards "my B half landed" for each stage to rank 0's issuer
+      if (lane == 0) {
+        uint32_t ib = 0;
+        for (uint32_t t = t_first; t < ntiles; t += t_step)
+          for (int s = 0; s < SH::NH * SH::KA; ++s, ++ib) {
+            const int sb = (int)(ib % SH::NB);
+            mbar_wait(&b_full[sb], (ib / SH::NB) & 1);
+            mbar_arrive_remote(&b_peer[sb], 0);
+          }
+      }
+    } else if (lane == 0) {
       uint32_t ib = 0, u = 0, k = 0;
-      for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+      for (uint32_t t = t_first; t < ntiles; t += t_step, ++k) {
         for (int nh = 0; nh < SH::NH; ++nh, ++u) {
           const int db = (int)(u & 1);
           if (u >= 2) mbar_wait(&d_empty[db], ((u >> 1) - 1) & 1);
@@ -255,34 +320,43 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
             if (nh == 0) mbar_wait(&a_full[ka], k & 1);
             const int sb = (int)(ib % SH::NB);
             mbar_wait(&b_full[sb], (ib / SH::NB) & 1);
+            if constexpr (PAIR) mbar_wait(&b_peer[sb], (ib / SH::NB) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
             if (nh < 2 && ka < 4) GEMM_TRACE(k, 8 + nh * 4 + ka);
-            const uint32_t ahi = smem_u32(sm + SH::A_OFF + (uint32_t)ka * 2 * ATOM_BYTES);
-            const uint32_t alo = ahi + ATOM_BYTES;
-            const uint32_t bhi = smem_u32(sm + SH::B_OFF + (uint32_t)sb * SH::STAGE);
-            const uint32_t blo = bhi + SH::STAGE / 2;
+            // descriptors of the atom's / stage's first K step; the next K step (32 B further)
+            // is +2 in the 16 B-unit start-address field (no carry: addresses < 2^18)
+            const uint64_t ahi = desc_sw128(smem_u32(sm + SH::A_OFF + (uint32_t)ka * 2 * ATOM_BYTES));
+            const uint64_t alo = ahi + (ATOM_BYTES >> 4);
+            const uint64_t bhi = desc_sw128(smem_u32(sm + SH::B_OFF + (uint32_t)sb * SH::STAGE));
+            const uint64_t blo = bhi + (SH::STAGE / 2 >> 4);
             // hi.hi accumulates into the big accumulator; the two correction terms (2^-11 of it)
             // into the small one, so only 16 K steps per output round against the full-size sum
 #pragma unroll
             for (int j = 0; j < 4; ++j) {  // K = 16 fp16 = 32 B per instruction
-              const uint32_t o = 32u * j;
-              const uint64_t da[3] = {desc_sw128(alo + o), desc_sw128(ahi + o), desc_sw128(ahi + o)};
-              const uint64_t dbd[3] = {desc_sw128(bhi + o), desc_sw128(blo + o), desc_sw128(bhi + o)};
+              const uint64_t o = 2u * j;
+              const uint64_t da[3] = {alo + o, ahi + o, ahi + o};
+              const uint64_t dbd[3] = {bhi + o, blo + o, bhi + o};
 #pragma unroll
               for (int term = 0; term < 3; ++term) {
                 const uint32_t acc = (ka | j | (term == 1)) ? 1u : 0u;
                 const uint32_t d = term < 2 ? dsmall : dbig;
-                asm volatile(
-                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                    "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n"
-                    :: "r"(d), "l"(da[term]), "l"(dbd[term]), "r"(idesc_f16(SH::NW)), "r"(acc));
+                if constexpr (PAIR)  // M = 256: A rows and B columns from both CTAs
+                  asm volatile(
+                      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n"
+                      :: "r"(d), "l"(da[term]), "l"(dbd[term]), "r"(idesc_f16(SH::NW, 2 * GM)), "r"(acc));
+                else
+                  asm volatile(
+                      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n"
+                      :: "r"(d), "l"(da[term]), "l"(dbd[term]), "r"(idesc_f16(SH::NW)), "r"(acc));
               }
             }
-            tc_commit(&b_empty[sb]);
+            tc_commit<PAIR>(&b_empty[sb]);
+            if (nh == SH::NH - 1) tc_commit<PAIR>(&a_empty[ka]);  // atom ka of the next tile may be written
           }
-          tc_commit(&d_full[db]);
+          tc_commit<PAIR>(&d_full[db]);
         }
-        tc_commit(a_empty);  // the tile's A may be overwritten once these MMAs completed
         GEMM_TRACE(k, 4);
       }
     }
@@ -312,9 +386,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
           for (int l = 0; l < NN / 32; ++l)
             asm volatile("prefetch.global.L2 [%0];" :: "l"(P.x + (size_t)id[i] * NN + l * 32) : "memory");
     };
-    for (int a = 0; a < PF_AHEAD; ++a) prefetch_rows(blockIdx.x + (uint32_t)a * gridDim.x);
+    for (int a = 0; a < PF_AHEAD; ++a) prefetch_rows(t_first + (uint32_t)a * t_step);
     uint32_t k = 0;
-    for (uint32_t t = blockIdx.x + PF_AHEAD * gridDim.x; t < ntiles; t += gridDim.x, ++k) {
+    for (uint32_t t = t_first + PF_AHEAD * t_step; t < ntiles; t += t_step, ++k) {
       mbar_wait(&f_full[k & 3], (k >> 2) & 1);
       prefetch_rows(t);
     }
@@ -322,24 +396,30 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
     // ------------------------------------------------------------------ B producer ----
     // Lane 0: the B stages of each unit of each tile, in the MMA's order (unit outer, K atom
     // inner), into the NB-stage ring.
+    // Global stages hold hi then lo of the unit's NW output columns; a CTA of a pair copies
+    // its NW / 2 rows of each (rows 64 rank ..), the layout cta_group::2 expects.
     if (lane == 0) {
+      constexpr uint32_t GSTAGE = 2u * SH::NW * 128, PART = (uint32_t)SH::BW * 128;
       uint32_t ib = 0;
-      for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (uint32_t t = t_first; t < ntiles; t += t_step) {
         int c;
         uint64_t p0;
         uint32_t rows;
         tm.of(t, c, p0, rows);
-        const unsigned char* src = P.bops + (size_t)c * SH::KA * SH::NH * SH::STAGE;
+        const unsigned char* src = P.bops + (size_t)c * SH::KA * SH::NH * GSTAGE;
         for (int nh = 0; nh < SH::NH; ++nh)
           for (int ka = 0; ka < SH::KA; ++ka, ++ib) {
             const int sb = (int)(ib % SH::NB);
             if (ib >= (uint32_t)SH::NB) mbar_wait(&b_empty[sb], ((ib / SH::NB) - 1) & 1);
             mbar_expect_tx(&b_full[sb], SH::STAGE);
+            const unsigned char* g = src + (size_t)(ka * SH::NH + nh) * GSTAGE + rank * PART;
+            const uint32_t d = smem_u32(sm + SH::B_OFF + (uint32_t)sb * SH::STAGE);
             asm volatile(
                 "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                :: "r"(smem_u32(sm + SH::B_OFF + (uint32_t)sb * SH::STAGE)),
-                   "l"(src + (size_t)(ka * SH::NH + nh) * SH::STAGE), "r"(SH::STAGE),
-                   "r"(smem_u32(&b_full[sb])) : "memory");
+                :: "r"(d), "l"(g), "r"(PART), "r"(smem_u32(&b_full[sb])) : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                :: "r"(d + PART), "l"(g + GSTAGE / 2), "r"(PART), "r"(smem_u32(&b_full[sb])) : "memory");
           }
       }
     }
@@ -356,7 +436,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
       return b16 * 16 + (gg & 1) * 2 + (gg >> 1) * 8 + (g8 >> 1) + (g8 & 1) * 4;
     };
     uint32_t k = 0;
-    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+    for (uint32_t t = t_first; t < ntiles; t += t_step, ++k) {
       int c;
       uint64_t p0;
       uint32_t rows;
@@ -411,10 +491,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
         __syncwarp();
         if (lane == 0) mbar_arrive(&f_full[fb]);
       }
-      // pass 2: once the previous tile's MMAs have read A, each K atom's 64 columns of every
-      // row -> fp16 hi / lo (L2 hits), one a_full arrival per atom so the MMAs follow closely
-      if (k >= 1) mbar_wait(a_empty, (k - 1) & 1);
+      // pass 2: each K atom's 64 columns of every row -> fp16 hi / lo (L2 hits), as soon as the
+      // previous tile's last unit has read that atom; one a_full arrival per atom so the MMAs
+      // follow closely
       for (int ka = 0; ka < SH::KA; ++ka) {
+        if (k >= 1) mbar_wait(&a_empty[ka], (k - 1) & 1);
         unsigned char* ahi = sm + SH::A_OFF + (uint32_t)ka * 2 * ATOM_BYTES;
         unsigned char* alo = ahi + ATOM_BYTES;
         float4 va[SH::RG][2];
@@ -444,7 +525,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic stores -> tensor core reads
         __syncwarp();
-        if (lane == 0) mbar_arrive(&a_full[ka]);
+        if (lane == 0) {
+          if constexpr (PAIR) mbar_arrive_remote(&a_full[ka], 0); else mbar_arrive(&a_full[ka]);
+        }
       }
       if (sw == 0 && lane == 0) GEMM_TRACE(k, 2);
     }
@@ -479,7 +562,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
     };
     const int r_th = warp * 32 + lane;  // TMEM lane = tile row of this thread
     uint32_t k = 0, u = 0;
-    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+    for (uint32_t t = t_first; t < ntiles; t += t_step, ++k) {
       int c;
       uint64_t p0;
       uint32_t rows;
@@ -527,7 +610,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
           if (cb == SH::NW / 32 - 1) {  // unit accumulators fully read: release them to unit u + 2
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
-            if (lane == 0) mbar_arrive(&d_empty[db]);
+            if (lane == 0) {
+              if constexpr (PAIR) mbar_arrive_remote(&d_empty[db], 0); else mbar_arrive(&d_empty[db]);
+            }
           }
           // big + small, unscale, then thread-per-row -> swizzled staging [32 rows][32 floats]
           auto acc_at = [&](int i) { return (__uint_as_float(v[i]) + __uint_as_float(w[i])) * f_row; };
@@ -578,10 +663,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
     flush_energy();
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync(); else __syncthreads();  // no peer access after this point
   asm volatile("tcgen05.fence::after_thread_sync;");
-  if (warp == MMA_WARP)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(SH::TMEM_COLS));
+  if (warp == MMA_WARP) {
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(SH::TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(SH::TMEM_COLS));
+  }
 }
 
 // ---------------------------------------------------------------- host: operand builder ----
@@ -616,9 +705,9 @@ double half_to_double(uint16_t h) {
 
 int gemm_smem_bytes(int n) {
   switch (n) {
-    case 64: return (int)Shape<64>::SMEM;
-    case 128: return (int)Shape<128>::SMEM;
-    case 256: return (int)Shape<256>::SMEM;
+    case 64: return (int)Shape<64, true>::SMEM;
+    case 128: return (int)Shape<128, true>::SMEM;
+    case 256: return (int)Shape<256, true>::SMEM;
     default: return 0;
   }
 }
@@ -680,6 +769,8 @@ int gemm_build(int n, int classes, const double* ops, GemmOperands& out) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&out.num_sms, cudaDevAttrMultiProcessorCount, dev);
   if (out.num_sms <= 0) out.num_sms = 148;
+  const char* pe = std::getenv("HYGT_GEMM_PAIR");
+  out.pair = !(pe && pe[0] == '0');
   return HYGT_OK;
 }
 
@@ -691,13 +782,29 @@ void gemm_release(GemmOperands& g) {
 }
 
 namespace {
-template <int NN, bool E>
+template <int NN, bool E, bool PAIR>
 int launch_one(const GemmParams& P, int num_sms, cudaStream_t st) {
-  const auto fn = hygt_gemm_kernel<NN, E>;
-  hygt_smem_attr(reinterpret_cast<const void*>(fn), Shape<NN>::SMEM);
-  fn<<<num_sms, GEMM_THREADS, Shape<NN>::SMEM, st>>>(P);
-  const cudaError_t e = cudaGetLastError();
+  const auto fn = hygt_gemm_kernel<NN, E, PAIR>;
+  hygt_smem_attr(reinterpret_cast<const void*>(fn), Shape<NN, PAIR>::SMEM);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  cfg.gridDim = dim3(PAIR ? (unsigned)(num_sms / 2 * 2) : (unsigned)num_sms);
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = Shape<NN, PAIR>::SMEM;
+  cfg.stream = st;
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = PAIR ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, fn, P);
   return e == cudaSuccess ? HYGT_OK : hygt_set_error(HYGT_ERR_CUDA, cudaGetErrorString(e));
+}
+template <int NN>
+int launch_n(const GemmParams& P, int grid, bool pair, cudaStream_t st) {
+  if (pair) return P.energy ? launch_one<NN, true, true>(P, grid, st) : launch_one<NN, false, true>(P, grid, st);
+  return P.energy ? launch_one<NN, true, false>(P, grid, st) : launch_one<NN, false, false>(P, grid, st);
 }
 }  // namespace
 
@@ -718,11 +825,12 @@ int gemm_run(const GemmOperands& g, const float* x, float* y, const uint32_t* id
   P.unscale = g.d_unscale;
   P.energy = energy;
   const uint64_t tiles = (count + GM - 1) / GM + (uint64_t)g.classes;
-  const int grid = (int)std::min<uint64_t>((uint64_t)g.num_sms, tiles);
+  const bool pair = g.pair && g.num_sms >= 2;
+  const int grid = (int)std::min<uint64_t>((uint64_t)g.num_sms, pair ? 2 * ((tiles + 1) / 2) : tiles);
   switch (g.n) {
-    case 64: return energy ? launch_one<64, true>(P, grid, st) : launch_one<64, false>(P, grid, st);
-    case 128: return energy ? launch_one<128, true>(P, grid, st) : launch_one<128, false>(P, grid, st);
-    case 256: return energy ? launch_one<256, true>(P, grid, st) : launch_one<256, false>(P, grid, st);
+    case 64: return launch_n<64>(P, grid, pair, st);
+    case 128: return launch_n<128>(P, grid, pair, st);
+    case 256: return launch_n<256>(P, grid, pair, st);
     default: return hygt_set_error(HYGT_ERR_ARGUMENT, "gemm: unsupported N");
   }
 }

@@ -24,6 +24,7 @@ struct GemmParams {
 
 struct GemmOperands {  // one direction
   int n = 0, classes = 0, num_sms = 148;
+  bool pair = true;  // CTA pairs (tcgen05 cta_group::2, M = 256): each SM streams half of B
   unsigned char* d_ops = nullptr;
   float* d_unscale = nullptr;
 };
