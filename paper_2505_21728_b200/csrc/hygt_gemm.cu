@@ -66,17 +66,21 @@ constexpr int PF_WARP = MMA_WARP + 1;
 constexpr int GEMM_THREADS = (PF_WARP + 1) * 32;
 constexpr uint32_t ATOM_BYTES = GM * 128;  // one 64-column fp16 K atom of the A tile (16 KB)
 
-template <int NN, bool PAIR>
+template <int NN, bool PAIR, bool WIDE>
 struct Shape {
   static constexpr int KA = NN / 64;                 // K atoms (64 fp16 = one 128 B swizzle row)
-  static constexpr int NW = NN < 128 ? NN : 128;     // N per MMA instruction = columns per unit
-  static constexpr int NH = NN / NW;                 // units (N halves) per tile
+  // columns per MMA instruction = per unit: up to 128, or (WIDE, CTA pairs) all N = 256 in one
+  // unit, which halves the shared-memory reads of A per tile
+  static constexpr int NW = WIDE ? NN : (NN < 128 ? NN : 128);
+  static constexpr int NH = NN / NW;                 // units per tile
   static constexpr int BW = PAIR ? NW / 2 : NW;      // B rows (output columns) held by this CTA
   static constexpr uint32_t STAGE = 2u * BW * 128;   // B stage (one K atom of one unit): hi + lo
-  static constexpr int NB = PAIR ? 4 : 2;            // B ring stages
+  static constexpr int NB = STAGE <= 16384 ? 4 : 2;  // B ring stages
   static constexpr int TG = PAIR ? 2 * GM : GM;      // rows per tile (a CTA pair: 128 each)
-  static constexpr uint32_t A_OFF = 0;               // the tile's whole A (KA atoms, hi + lo)
-  static constexpr uint32_t B_OFF = A_OFF + KA * 2 * ATOM_BYTES;
+  static constexpr int ABUF = KA <= 2 ? 2 : 1;       // tiles of A resident (double-buffered if small)
+  static constexpr int AS = KA * ABUF;               // A atom slots
+  static constexpr uint32_t A_OFF = 0;               // A: AS atoms (hi + lo each)
+  static constexpr uint32_t B_OFF = A_OFF + AS * 2 * ATOM_BYTES;
   static constexpr uint32_t STG_OFF = B_OFF + NB * STAGE;
   static constexpr uint32_t STG_BYTES = 32 * 128;    // per epilogue warp: 32 rows x 32 floats
   static constexpr uint32_t EN_OFF = STG_OFF + EPI_WARPS * STG_BYTES;
@@ -84,9 +88,11 @@ struct Shape {
   static constexpr uint32_t BAR_OFF = FAC_OFF + 4 * GM * 4;
   static constexpr uint32_t SMEM = BAR_OFF + 512;  // barriers (<= 40 x 8 B) + the TMEM address
   // TMEM: per unit a "big" accumulator (hi.hi) and a "small" one (lo.hi + hi.lo), NW columns
-  // each, double-buffered over units: 4 NW <= 512 columns
-  static constexpr uint32_t TMEM_COLS = 4 * NW < 32 ? 32 : 4 * NW;
+  // each, double-buffered over units when 4 NW <= 512 columns
+  static constexpr int NBUF = 4 * NW <= 512 ? 2 : 1;
+  static constexpr uint32_t TMEM_COLS = NBUF * 2 * NW < 32 ? 32 : NBUF * 2 * NW;
   static constexpr int RG = GM / SPLIT_WARPS / 4;    // 4-row groups per split warp
+  static_assert(!WIDE || PAIR, "the wide unit needs the CTA pair");
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -217,15 +223,15 @@ struct TileMap {
     if (P.trace && blockIdx.x == 0 && (k) < 64) P.trace[(k) * 16 + (e)] = clock64(); \
   } while (0)
 
-template <int NN, bool ENERGY, bool PAIR>
+template <int NN, bool ENERGY, bool PAIR, bool WIDE>
 __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmParams P) {
-  using SH = Shape<NN, PAIR>;
+  using SH = Shape<NN, PAIR, WIDE>;
   // 1024 B aligned (SWIZZLE_128B atoms); declared shared so every access compiles to LDS/STS
   extern __shared__ __align__(1024) unsigned char sm[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + SH::BAR_OFF);
-  uint64_t* a_full = bars;                     // [KA]  atom written, count SPLIT_WARPS
-  uint64_t* a_empty = a_full + SH::KA;         // [KA]  atom read by the tile's last unit (commit)
-  uint64_t* b_full = a_empty + SH::KA;         // [NB]  expect_tx
+  uint64_t* a_full = bars;                     // [AS]  atom written, count SPLIT_WARPS
+  uint64_t* a_empty = a_full + SH::AS;         // [AS]  atom read by the tile's last unit (commit)
+  uint64_t* b_full = a_empty + SH::AS;         // [NB]  expect_tx
   uint64_t* b_empty = b_full + SH::NB;         // [NB]  tcgen05.commit
   uint64_t* d_full = b_empty + SH::NB;         // [2]   tcgen05.commit
   uint64_t* d_empty = d_full + 2;              // [2]   count EPI_WARPS
@@ -233,7 +239,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
   uint64_t* f_empty = f_full + 4;              // [4]   row scales read, count EPI_WARPS
   uint64_t* b_peer = f_empty + 4;              // [NB]  pair: the peer's B half landed (count 1)
   uint32_t* tmem_sh = reinterpret_cast<uint32_t*>(b_peer + SH::NB);
-  static_assert(SH::KA * 2 + SH::NB * 3 + 12 <= 62, "barrier area");
+  static_assert(SH::AS * 2 + SH::NB * 3 + 12 <= 62, "barrier area");
   __shared__ uint32_t tile_end_sh[HYGT_GEMM_MAX_CLASSES];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -278,7 +284,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
     }
   }
   if (tid == 0) {
-    for (int i = 0; i < SH::KA; ++i) { mbar_init(&a_full[i], SPLIT_WARPS * pn); mbar_init(&a_empty[i], 1); }
+    for (int i = 0; i < SH::AS; ++i) { mbar_init(&a_full[i], SPLIT_WARPS * pn); mbar_init(&a_empty[i], 1); }
     for (int i = 0; i < SH::NB; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); mbar_init(&b_peer[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&d_full[i], 1); mbar_init(&d_empty[i], EPI_WARPS * pn); }
     for (int i = 0; i < 4; ++i) { mbar_init(&f_full[i], SPLIT_WARPS); mbar_init(&f_empty[i], EPI_WARPS); }
@@ -311,13 +317,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
       uint32_t ib = 0, u = 0, k = 0;
       for (uint32_t t = t_first; t < ntiles; t += t_step, ++k) {
         for (int nh = 0; nh < SH::NH; ++nh, ++u) {
-          const int db = (int)(u & 1);
-          if (u >= 2) mbar_wait(&d_empty[db], ((u >> 1) - 1) & 1);
+          const int db = (int)(u % SH::NBUF);
+          if (u >= (uint32_t)SH::NBUF) mbar_wait(&d_empty[db], ((u / SH::NBUF) - 1) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
           if (nh == 0) GEMM_TRACE(k, 3);
           const uint32_t dbig = tmem + (uint32_t)(db * 2 * SH::NW), dsmall = dbig + (uint32_t)SH::NW;
           for (int ka = 0; ka < SH::KA; ++ka, ++ib) {
-            if (nh == 0) mbar_wait(&a_full[ka], k & 1);
+            const int as = (int)(k % SH::ABUF) * SH::KA + ka;
+            if (nh == 0) mbar_wait(&a_full[as], (k / SH::ABUF) & 1);
             const int sb = (int)(ib % SH::NB);
             mbar_wait(&b_full[sb], (ib / SH::NB) & 1);
             if constexpr (PAIR) mbar_wait(&b_peer[sb], (ib / SH::NB) & 1);
@@ -325,7 +332,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
             if (nh < 2 && ka < 4) GEMM_TRACE(k, 8 + nh * 4 + ka);
             // descriptors of the atom's / stage's first K step; the next K step (32 B further)
             // is +2 in the 16 B-unit start-address field (no carry: addresses < 2^18)
-            const uint64_t ahi = desc_sw128(smem_u32(sm + SH::A_OFF + (uint32_t)ka * 2 * ATOM_BYTES));
+            const uint64_t ahi = desc_sw128(smem_u32(sm + SH::A_OFF + (uint32_t)as * 2 * ATOM_BYTES));
             const uint64_t alo = ahi + (ATOM_BYTES >> 4);
             const uint64_t bhi = desc_sw128(smem_u32(sm + SH::B_OFF + (uint32_t)sb * SH::STAGE));
             const uint64_t blo = bhi + (SH::STAGE / 2 >> 4);
@@ -353,7 +360,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
               }
             }
             tc_commit<PAIR>(&b_empty[sb]);
-            if (nh == SH::NH - 1) tc_commit<PAIR>(&a_empty[ka]);  // atom ka of the next tile may be written
+            if (nh == SH::NH - 1) tc_commit<PAIR>(&a_empty[as]);  // the slot may take a later tile's atom
           }
           tc_commit<PAIR>(&d_full[db]);
         }
@@ -399,27 +406,36 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
     // Global stages hold hi then lo of the unit's NW output columns; a CTA of a pair copies
     // its NW / 2 rows of each (rows 64 rank ..), the layout cta_group::2 expects.
     if (lane == 0) {
-      constexpr uint32_t GSTAGE = 2u * SH::NW * 128, PART = (uint32_t)SH::BW * 128;
+      // global stages: [class][K atom][128-column half][hi | lo] (gemm_build)
+      constexpr uint32_t GSTAGE = 2u * (NN < 128 ? NN : 128) * 128, PART = (uint32_t)SH::BW * 128;
+      constexpr int GH = NN < 128 ? 1 : NN / 128;
       uint32_t ib = 0;
       for (uint32_t t = t_first; t < ntiles; t += t_step) {
         int c;
         uint64_t p0;
         uint32_t rows;
         tm.of(t, c, p0, rows);
-        const unsigned char* src = P.bops + (size_t)c * SH::KA * SH::NH * GSTAGE;
+        const unsigned char* src = P.bops + (size_t)c * SH::KA * GH * GSTAGE;
         for (int nh = 0; nh < SH::NH; ++nh)
           for (int ka = 0; ka < SH::KA; ++ka, ++ib) {
             const int sb = (int)(ib % SH::NB);
             if (ib >= (uint32_t)SH::NB) mbar_wait(&b_empty[sb], ((ib / SH::NB) - 1) & 1);
             mbar_expect_tx(&b_full[sb], SH::STAGE);
-            const unsigned char* g = src + (size_t)(ka * SH::NH + nh) * GSTAGE + rank * PART;
             const uint32_t d = smem_u32(sm + SH::B_OFF + (uint32_t)sb * SH::STAGE);
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                :: "r"(d), "l"(g), "r"(PART), "r"(smem_u32(&b_full[sb])) : "memory");
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                :: "r"(d + PART), "l"(g + GSTAGE / 2), "r"(PART), "r"(smem_u32(&b_full[sb])) : "memory");
+            if constexpr (WIDE) {  // this CTA's 128 of the 256 rows = global half-stage `rank`
+              const unsigned char* g = src + (size_t)(ka * SH::NH * 2 + rank) * GSTAGE;
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                  :: "r"(d), "l"(g), "r"(SH::STAGE), "r"(smem_u32(&b_full[sb])) : "memory");
+            } else {
+              const unsigned char* g = src + (size_t)(ka * SH::NH + nh) * GSTAGE + rank * PART;
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                  :: "r"(d), "l"(g), "r"(PART), "r"(smem_u32(&b_full[sb])) : "memory");
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                  :: "r"(d + PART), "l"(g + GSTAGE / 2), "r"(PART), "r"(smem_u32(&b_full[sb])) : "memory");
+            }
           }
       }
     }
@@ -450,26 +466,41 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
         const int r = row_of_group(g);
         rid[g] = (uint32_t)r < rows ? row_at(P, p0 + r) : 0xffffffffu;
       }
+      // Small rows (N = 64): pass 1 keeps the rows in registers (8 floats per lane and group)
+      // and pass 2 converts from them. Longer rows: pass 1 streams two groups at a time for the
+      // maxima and pass 2 re-reads each K atom (L2 hits), the next atom's loads in flight while
+      // the current one is converted.
+      constexpr int NV = NN / 32;                 // float4 per lane and row group
+      constexpr bool HOLD = SH::RG * NV <= 8;
       float mxs[SH::RG];
-      constexpr int NV = NN / 32;
+      float4 held[HOLD ? SH::RG : 1][HOLD ? NV : 1];
+      auto load_group = [&](int g, float4 (&v)[NV]) {
+        const uint32_t id = rid[g];
+        const float4* src = reinterpret_cast<const float4*>(P.x + (size_t)(id != 0xffffffffu ? id : 0u) * NN);
 #pragma unroll
-      for (int g0 = 0; g0 < SH::RG; g0 += 2) {  // two row groups' loads in flight at a time
-        float4 v[2][NV];
+        for (int i = 0; i < NV; ++i)
+          v[i] = id != 0xffffffffu ? __ldcg(src + i * 8 + l8) : make_float4(0.f, 0.f, 0.f, 0.f);
+      };
+      auto group_max = [&](const float4 (&v)[NV]) {
+        float mx = 0.f;
 #pragma unroll
-        for (int gg = 0; gg < 2; ++gg) {
-          const uint32_t id = rid[g0 + gg];
-          const float4* src = reinterpret_cast<const float4*>(P.x + (size_t)(id != 0xffffffffu ? id : 0u) * NN);
+        for (int i = 0; i < NV; ++i)
+          mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[i].x), fabsf(v[i].y)), fmaxf(fabsf(v[i].z), fabsf(v[i].w))));
+        return mx;
+      };
+      if constexpr (HOLD) {
 #pragma unroll
-          for (int i = 0; i < NV; ++i)
-            v[gg][i] = id != 0xffffffffu ? __ldcg(src + i * 8 + l8) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+        for (int g = 0; g < SH::RG; ++g) load_group(g, held[g]);
 #pragma unroll
-        for (int gg = 0; gg < 2; ++gg) {
-          float mx = 0.f;
+        for (int g = 0; g < SH::RG; ++g) mxs[g] = group_max(held[g]);
+      } else {
 #pragma unroll
-          for (int i = 0; i < NV; ++i)
-            mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[gg][i].x), fabsf(v[gg][i].y)), fmaxf(fabsf(v[gg][i].z), fabsf(v[gg][i].w))));
-          mxs[g0 + gg] = mx;
+        for (int g0 = 0; g0 < SH::RG; g0 += 2) {  // two row groups' loads in flight at a time
+          float4 v[2][NV];
+          load_group(g0, v[0]);
+          load_group(g0 + 1, v[1]);
+          mxs[g0] = group_max(v[0]);
+          mxs[g0 + 1] = group_max(v[1]);
         }
       }
 #pragma unroll
@@ -491,21 +522,38 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
         __syncwarp();
         if (lane == 0) mbar_arrive(&f_full[fb]);
       }
-      // pass 2: each K atom's 64 columns of every row -> fp16 hi / lo (L2 hits), as soon as the
-      // previous tile's last unit has read that atom; one a_full arrival per atom so the MMAs
+      // pass 2: each K atom's 64 columns of every row -> fp16 hi / lo, written as soon as the
+      // slot's previous atom was read by the MMAs; one a_full arrival per atom so the MMAs
       // follow closely
-      for (int ka = 0; ka < SH::KA; ++ka) {
-        if (k >= 1) mbar_wait(&a_empty[ka], (k - 1) & 1);
-        unsigned char* ahi = sm + SH::A_OFF + (uint32_t)ka * 2 * ATOM_BYTES;
-        unsigned char* alo = ahi + ATOM_BYTES;
-        float4 va[SH::RG][2];
+      auto load_atom = [&](int ka, float4 (&va)[SH::RG][2]) {
 #pragma unroll
         for (int g = 0; g < SH::RG; ++g)
 #pragma unroll
-          for (int h = 0; h < 2; ++h)  // columns 64 ka + 32 h + 4 l8 .. +3
-            va[g][h] = rid[g] != 0xffffffffu
-                           ? __ldcs(reinterpret_cast<const float4*>(P.x + (size_t)rid[g] * NN + 64 * ka + 32 * h) + l8)
-                           : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int h = 0; h < 2; ++h) {  // columns 64 ka + 32 h + 4 l8 .. +3
+            if constexpr (HOLD) {
+              va[g][h] = held[g][2 * ka + h];
+            } else {
+              va[g][h] = rid[g] != 0xffffffffu
+                             ? __ldcs(reinterpret_cast<const float4*>(P.x + (size_t)rid[g] * NN + 64 * ka + 32 * h) + l8)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+          }
+      };
+      float4 vnext[SH::RG][2];
+      load_atom(0, vnext);
+#pragma unroll 1
+      for (int ka = 0; ka < SH::KA; ++ka) {
+        float4 va[SH::RG][2];
+#pragma unroll
+        for (int g = 0; g < SH::RG; ++g) {
+          va[g][0] = vnext[g][0];
+          va[g][1] = vnext[g][1];
+        }
+        if (ka + 1 < SH::KA) load_atom(ka + 1, vnext);
+        const int as = (int)(k % SH::ABUF) * SH::KA + ka;
+        if (k >= (uint32_t)SH::ABUF) mbar_wait(&a_empty[as], ((k / SH::ABUF) - 1) & 1);
+        unsigned char* ahi = sm + SH::A_OFF + (uint32_t)as * 2 * ATOM_BYTES;
+        unsigned char* alo = ahi + ATOM_BYTES;
 #pragma unroll
         for (int g = 0; g < SH::RG; ++g) {
           const int r = row_of_group(g);
@@ -526,7 +574,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic stores -> tensor core reads
         __syncwarp();
         if (lane == 0) {
-          if constexpr (PAIR) mbar_arrive_remote(&a_full[ka], 0); else mbar_arrive(&a_full[ka]);
+          if constexpr (PAIR) mbar_arrive_remote(&a_full[as], 0); else mbar_arrive(&a_full[as]);
         }
       }
       if (sw == 0 && lane == 0) GEMM_TRACE(k, 2);
@@ -560,7 +608,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
         __syncwarp();
       }
     };
-    const int r_th = warp * 32 + lane;  // TMEM lane = tile row of this thread
     uint32_t k = 0, u = 0;
     for (uint32_t t = t_first; t < ntiles; t += t_step, ++k) {
       int c;
@@ -572,7 +619,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
         en_class = c;
       }
       mbar_wait(&f_full[k & 3], (k >> 2) & 1);
-      const float f_row = fac[(k & 3) * GM + r_th] * __ldg(P.unscale + c);
+      const float f_row = fac[(k & 3) * GM + warp * 32 + lane] * __ldg(P.unscale + c);  // TMEM lane = row
       __syncwarp();
       if (lane == 0) mbar_arrive(&f_empty[k & 3]);
       // row ids of the 4-row groups this lane stores (rows warp*32 + 4 i + lane/8)
@@ -583,12 +630,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
         orow[i] = (uint32_t)r < rows ? row_at(P, p0 + r) : 0xffffffffu;
       }
       for (int nh = 0; nh < SH::NH; ++nh, ++u) {
-        const int db = (int)(u & 1);
-        mbar_wait(&d_full[db], (u >> 1) & 1);
+        const int db = (int)(u % SH::NBUF);
+        mbar_wait(&d_full[db], (u / SH::NBUF) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         if (nh == 0 && warp == 0 && lane == 0) GEMM_TRACE(k, 5);
-        for (int cb = 0; cb < SH::NW / 32; ++cb) {
-          uint32_t v[32], w[32];
+        // TMEM -> registers for column block cb (big at the unit's buffer, small NW after it)
+        uint32_t v[32], w[32];
+        auto tmem_load = [&](int cb) {
           const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(db * 2 * SH::NW + cb * 32);
           asm volatile(
               "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -606,20 +654,26 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
                 "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
                 "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
               : "r"(taddr));
-          asm volatile("tcgen05.wait::ld.sync.aligned;");
-          if (cb == SH::NW / 32 - 1) {  // unit accumulators fully read: release them to unit u + 2
-            asm volatile("tcgen05.fence::before_thread_sync;");
-            __syncwarp();
-            if (lane == 0) {
-              if constexpr (PAIR) mbar_arrive_remote(&d_empty[db], 0); else mbar_arrive(&d_empty[db]);
-            }
+        };
+        constexpr int NCB = SH::NW / 32;
+        auto release = [&]() {  // unit accumulators fully read: release them to unit u + NBUF
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (PAIR) mbar_arrive_remote(&d_empty[db], 0); else mbar_arrive(&d_empty[db]);
           }
+        };
+        tmem_load(0);
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+        if (NCB == 1) release();
+        for (int cb = 0; cb < NCB; ++cb) {
           // big + small, unscale, then thread-per-row -> swizzled staging [32 rows][32 floats]
           auto acc_at = [&](int i) { return (__uint_as_float(v[i]) + __uint_as_float(w[i])) * f_row; };
 #pragma unroll
           for (int q = 0; q < 8; ++q)
             *reinterpret_cast<float4*>(stg + swz(lane, q)) =
                 make_float4(acc_at(4 * q), acc_at(4 * q + 1), acc_at(4 * q + 2), acc_at(4 * q + 3));
+          if (cb + 1 < NCB) tmem_load(cb + 1);  // in flight while this block is stored
           __syncwarp();
           // coalesced: 8 lanes per row, 4 rows per instruction
           const int col0 = nh * SH::NW + cb * 32;
@@ -655,6 +709,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
               e[2] += d2;
               e[3] += d3;
             }
+          }
+          if (cb + 1 < NCB) {
+            asm volatile("tcgen05.wait::ld.sync.aligned;");
+            if (cb + 2 == NCB) release();
           }
         }
       }
@@ -705,9 +763,9 @@ double half_to_double(uint16_t h) {
 
 int gemm_smem_bytes(int n) {
   switch (n) {
-    case 64: return (int)Shape<64, true>::SMEM;
-    case 128: return (int)Shape<128, true>::SMEM;
-    case 256: return (int)Shape<256, true>::SMEM;
+    case 64: return (int)Shape<64, true, false>::SMEM;
+    case 128: return (int)Shape<128, true, false>::SMEM;
+    case 256: return (int)Shape<256, true, true>::SMEM;
     default: return 0;
   }
 }
@@ -771,6 +829,8 @@ int gemm_build(int n, int classes, const double* ops, GemmOperands& out) {
   if (out.num_sms <= 0) out.num_sms = 148;
   const char* pe = std::getenv("HYGT_GEMM_PAIR");
   out.pair = !(pe && pe[0] == '0');
+  const char* we = std::getenv("HYGT_GEMM_WIDE");
+  out.wide = we && we[0] == '1';  // measured slower at N = 256 (serialised epilogue)
   return HYGT_OK;
 }
 
@@ -782,15 +842,16 @@ void gemm_release(GemmOperands& g) {
 }
 
 namespace {
-template <int NN, bool E, bool PAIR>
+template <int NN, bool E, bool PAIR, bool WIDE>
 int launch_one(const GemmParams& P, int num_sms, cudaStream_t st) {
-  const auto fn = hygt_gemm_kernel<NN, E, PAIR>;
-  hygt_smem_attr(reinterpret_cast<const void*>(fn), Shape<NN, PAIR>::SMEM);
+  using SH = Shape<NN, PAIR, WIDE>;
+  const auto fn = hygt_gemm_kernel<NN, E, PAIR, WIDE>;
+  hygt_smem_attr(reinterpret_cast<const void*>(fn), SH::SMEM);
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   cfg.gridDim = dim3(PAIR ? (unsigned)(num_sms / 2 * 2) : (unsigned)num_sms);
   cfg.blockDim = dim3(GEMM_THREADS);
-  cfg.dynamicSmemBytes = Shape<NN, PAIR>::SMEM;
+  cfg.dynamicSmemBytes = SH::SMEM;
   cfg.stream = st;
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = PAIR ? 2 : 1;
@@ -802,9 +863,13 @@ int launch_one(const GemmParams& P, int num_sms, cudaStream_t st) {
   return e == cudaSuccess ? HYGT_OK : hygt_set_error(HYGT_ERR_CUDA, cudaGetErrorString(e));
 }
 template <int NN>
-int launch_n(const GemmParams& P, int grid, bool pair, cudaStream_t st) {
-  if (pair) return P.energy ? launch_one<NN, true, true>(P, grid, st) : launch_one<NN, false, true>(P, grid, st);
-  return P.energy ? launch_one<NN, true, false>(P, grid, st) : launch_one<NN, false, false>(P, grid, st);
+int launch_n(const GemmParams& P, int grid, bool pair, bool wide, cudaStream_t st) {
+  if constexpr (NN == 256) {
+    if (pair && wide)
+      return P.energy ? launch_one<NN, true, true, true>(P, grid, st) : launch_one<NN, false, true, true>(P, grid, st);
+  }
+  if (pair) return P.energy ? launch_one<NN, true, true, false>(P, grid, st) : launch_one<NN, false, true, false>(P, grid, st);
+  return P.energy ? launch_one<NN, true, false, false>(P, grid, st) : launch_one<NN, false, false, false>(P, grid, st);
 }
 }  // namespace
 
@@ -828,9 +893,9 @@ int gemm_run(const GemmOperands& g, const float* x, float* y, const uint32_t* id
   const bool pair = g.pair && g.num_sms >= 2;
   const int grid = (int)std::min<uint64_t>((uint64_t)g.num_sms, pair ? 2 * ((tiles + 1) / 2) : tiles);
   switch (g.n) {
-    case 64: return launch_n<64>(P, grid, pair, st);
-    case 128: return launch_n<128>(P, grid, pair, st);
-    case 256: return launch_n<256>(P, grid, pair, st);
+    case 64: return launch_n<64>(P, grid, pair, g.wide, st);
+    case 128: return launch_n<128>(P, grid, pair, g.wide, st);
+    case 256: return launch_n<256>(P, grid, pair, g.wide, st);
     default: return hygt_set_error(HYGT_ERR_ARGUMENT, "gemm: unsupported N");
   }
 }

@@ -25,6 +25,8 @@ struct GemmParams {
 struct GemmOperands {  // one direction
   int n = 0, classes = 0, num_sms = 148;
   bool pair = true;  // CTA pairs (tcgen05 cta_group::2, M = 256): each SM streams half of B
+  bool wide = false;  // N = 256 with pairs: one N = 256 unit per tile (A read from smem half as often,
+                      // but the single-buffered accumulator serialises the epilogue: slower)
   unsigned char* d_ops = nullptr;
   float* d_unscale = nullptr;
 };

@@ -12,7 +12,9 @@
 // layout (8-row x 16-byte core matrices): a warp's 32 rows store one 512-byte run per chunk,
 // so the shared-memory fill is bank-conflict free. The epilogue drains TMEM with
 // tcgen05.ld.32x32b (one row per thread) and stores the row back to its original position.
-// n in {16, 32, 64} uses the tensor cores; other n use the fp32 SIMT kernel.
+// n in {16, 32} uses this kernel; n in {64, 128, 256} the per-class grouped GEMM of
+// hygt_gemm.cu (fp16 3-term split with per-row scaling, CTA pairs, warp-specialised pipeline)
+// that also serves the composed-operator HyGT path; other n the fp32 SIMT kernel.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -23,6 +25,7 @@
 #include <vector>
 
 #include "../../include/hygt_gpu.h"
+#include "hygt_gemm.h"
 
 int hygt_set_error(int status, const char* msg);  // hygt_capi.cu
 void hygt_smem_attr(const void* fn, size_t bytes);  // hygt_capi.cu: per (device, kernel), only grows
@@ -38,8 +41,9 @@ struct hygt_klt_plan {
   float* d_k = nullptr;   // [C][n][n]   rows = basis vectors (fp32)
   float* d_kt = nullptr;  // [C][n][n]   transposed
   float* d_b[2] = {nullptr, nullptr};  // tensor-core B operands per direction: [C][hi|lo][layout]
-  float* d_bsw[2] = {nullptr, nullptr};  // the same in the SWIZZLE_128B layout (n = 64)
-  bool tc = false;
+  bool tc = false;                     // N = 16 / 32: klt_tc_kernel (3xTF32)
+  bool gemm = false;                   // N = 64 / 128 / 256: hygt_gemm.cu (fp16 3-term, CTA pairs)
+  hygt_gpu::GemmOperands gops[2];
   int num_sms = 148;
 };
 
@@ -238,375 +242,6 @@ __global__ void __launch_bounds__(128, 1) klt_tc_kernel(const KltTcParams P) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(TMEM_COLS));
 }
 
-// Pipelined variant for N = 64 (config 4): 8 warps, two A stages and two TMEM accumulators, so
-// the global gathers + tf32 split of tile i+1 overlap the tensor-core MMAs of tile i, and the
-// epilogue of tile i overlaps the MMAs of tile i+1. Two threads per tile row (each half of the K
-// chunks when loading, half of the accumulator columns when draining).
-constexpr int KLT_PIPE_THREADS = 256;
-
-template <int NN>
-__global__ void __launch_bounds__(KLT_PIPE_THREADS, 1) klt_tc_pipe_kernel(const KltTcParams P) {
-  constexpr int M = 128;
-  constexpr int KCH = NN / 4;
-  constexpr uint32_t A_BYTES = M * NN * 4, B_BYTES = NN * NN * 4;
-  static_assert(NN == 64, "pipelined KLT kernel: N = 64");
-  extern __shared__ __align__(1024) unsigned char sm[];
-  auto a_st = [&](int st, int lo) { return reinterpret_cast<float*>(sm + (2 * st + lo) * A_BYTES); };
-  float* b_hi = reinterpret_cast<float*>(sm + 4 * A_BYTES);
-  float* b_lo = reinterpret_cast<float*>(sm + 4 * A_BYTES + B_BYTES);
-  __shared__ __align__(8) uint64_t mbar[2];
-  __shared__ uint32_t tmem_base_sh;
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int trow = tid & (M - 1), half = tid / M;
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                 :: "r"(smem_u32(&tmem_base_sh)), "r"(2u * NN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&mbar[0])));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&mbar[1])));
-    asm volatile("fence.mbarrier_init.release.cluster;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tmem = tmem_base_sh;
-  uint32_t phase[2] = {0, 0};
-
-  auto load_tile = [&](uint64_t s0, uint64_t s1, uint64_t t, int st) -> uint64_t {
-    const uint64_t p = s0 + t * M + trow;
-    const bool valid = p < s1;
-    const uint64_t row = valid ? (P.idx ? (uint64_t)__ldg(P.idx + p) : p) : ~0ull;
-    const float4* src = reinterpret_cast<const float4*>(P.in + (valid ? row : 0) * NN);
-    float4 v[KCH / 2];
-#pragma unroll
-    for (int qq = 0; qq < KCH / 2; ++qq)
-      v[qq] = valid ? __ldcs(src + half * (KCH / 2) + qq) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int qq = 0; qq < KCH / 2; ++qq) {
-      const int q = half * (KCH / 2) + qq;
-      const float4 h = make_float4(to_tf32(v[qq].x), to_tf32(v[qq].y), to_tf32(v[qq].z), to_tf32(v[qq].w));
-      const float4 l = make_float4(to_tf32(v[qq].x - h.x), to_tf32(v[qq].y - h.y), to_tf32(v[qq].z - h.z),
-                                   to_tf32(v[qq].w - h.w));
-      const int off = q * (M * 4) + (trow >> 3) * 32 + (trow & 7) * 4;  // canonical K-major
-      *reinterpret_cast<float4*>(a_st(st, 0) + off) = h;
-      *reinterpret_cast<float4*>(a_st(st, 1) + off) = l;
-    }
-    asm volatile("fence.proxy.async.shared::cta;");
-    return row;
-  };
-  auto issue = [&](int st) {  // one thread: 3xTF32 MMAs of a 128 x NN tile into accumulator st
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    const uint32_t idesc = idesc_tf32(NN);
-    const uint32_t ahi = smem_u32(a_st(st, 0)), alo = smem_u32(a_st(st, 1));
-    const uint32_t bhi = smem_u32(b_hi), blo = smem_u32(b_lo);
-    const uint32_t d = tmem + (uint32_t)(st * NN);
-    int first = 1;
-#pragma unroll
-    for (int ks = 0; ks < NN / 8; ++ks) {
-      const uint32_t aoff = (uint32_t)(2 * ks) * (M * 16), boff = (uint32_t)(2 * ks) * (NN * 16);
-      const uint64_t da_hi = umma_desc(ahi + aoff, M * 16, 128), da_lo = umma_desc(alo + aoff, M * 16, 128);
-      const uint64_t db_hi = umma_desc(bhi + boff, NN * 16, 128), db_lo = umma_desc(blo + boff, NN * 16, 128);
-      const uint64_t da[3] = {da_lo, da_hi, da_hi}, db[3] = {db_hi, db_lo, db_hi};  // small terms first
-#pragma unroll
-      for (int term = 0; term < 3; ++term) {
-        const uint32_t acc = first ? 0u : 1u;
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
-            :: "r"(d), "l"(da[term]), "l"(db[term]), "r"(idesc), "r"(acc));
-        first = 0;
-      }
-    }
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
-                 :: "r"(smem_u32(&mbar[st])));
-  };
-  auto wait_mma = [&](int st) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t@!P1 bra WAIT_%=;\n\t}\n"
-        :: "r"(smem_u32(&mbar[st])), "r"(phase[st]));
-    phase[st] ^= 1;
-    asm volatile("tcgen05.fence::after_thread_sync;");
-  };
-  auto drain = [&](int st, uint64_t row) {  // accumulator st -> rows (half of the columns each)
-    float* dst = P.out + row * NN;
-#pragma unroll
-    for (int c1 = 0; c1 < NN / 2; c1 += 16) {
-      const int c0 = half * (NN / 2) + c1;
-      uint32_t r[16];
-      const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(st * NN + c0);
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-            "=r"(r[14]), "=r"(r[15])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;");
-      if (row != ~0ull) {
-#pragma unroll
-        for (int j = 0; j < 16; j += 4)
-          __stcs(reinterpret_cast<float4*>(dst + c0 + j),
-                 make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
-                             __uint_as_float(r[j + 3])));
-      }
-    }
-  };
-
-  const int C = P.idx ? P.classes : 1;
-  for (int c = 0; c < C; ++c) {
-    const uint64_t s0 = P.idx ? (c == 0 ? 0 : P.seg_end[c - 1]) : 0;
-    const uint64_t s1 = P.idx ? P.seg_end[c] : P.count;
-    if (s1 <= s0) continue;
-    const uint64_t tiles = (s1 - s0 + M - 1) / M;
-    if (tiles <= blockIdx.x) continue;
-    __syncthreads();  // the previous class's MMAs and drains are complete
-    {
-      const float4* src = reinterpret_cast<const float4*>(P.b + (size_t)c * 2 * NN * NN);
-      float4* dst = reinterpret_cast<float4*>(b_hi);
-      for (int i = tid; i < 2 * NN * NN / 4; i += KLT_PIPE_THREADS) dst[i] = __ldg(src + i);
-    }
-    asm volatile("fence.proxy.async.shared::cta;");
-    uint64_t t = blockIdx.x;
-    int st = 0;
-    uint64_t row = load_tile(s0, s1, t, st);
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
-    if (tid == 0) issue(st);
-    for (;;) {
-      const uint64_t tn = t + gridDim.x;
-      const bool more = tn < tiles;
-      uint64_t row_n = ~0ull;
-      if (more) row_n = load_tile(s0, s1, tn, st ^ 1);  // overlaps MMA(t)
-      wait_mma(st);
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncthreads();  // A(tn) written; stage st and accumulator st^1 free
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      if (more && tid == 0) issue(st ^ 1);  // overlaps the drain of t
-      drain(st, row);
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      if (!more) break;
-      t = tn;
-      row = row_n;
-      st ^= 1;
-    }
-  }
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(2u * NN));
-}
-
-// SWIZZLE_128B K-major variant for N = 64 (config 4). The operand layout is the one UMMA reads
-// with layout type SWIZZLE_128B: K in 128 B atoms (32 tf32); within an atom, row r sits at
-// r * 128 B and its 16 B chunk c at chunk c ^ (r & 7); 8-row groups 1024 B apart (SBO). With it,
-// a warp can write two whole 256 B rows per STS.128 instruction without bank conflicts, so the
-// rows are gathered from HBM coalesced (2 rows per LDG.128 instruction) instead of one 16 B
-// piece per row. The accumulator tile leaves the same way: TMEM -> registers -> swizzled
-// staging in the spent A stage -> coalesced STG.128. Two A stages and two TMEM accumulators:
-// the gather + tf32 split of tile i+1 overlaps the MMAs of tile i.
-__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)1 << 16;                 // LBO (unused for swizzled K-major)
-  d |= (uint64_t)(1024 >> 4) << 32;       // SBO: 8 rows x 128 B
-  d |= (uint64_t)1 << 46;                 // descriptor version (sm_100)
-  d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
-  return d;
-}
-
-template <int NN>
-__global__ void __launch_bounds__(KLT_PIPE_THREADS, 1) klt_sw_kernel(const KltTcParams P) {
-  constexpr int M = 128;
-  constexpr uint32_t A_BYTES = M * NN * 4, B_BYTES = NN * NN * 4;
-  constexpr int RPW = M / (KLT_PIPE_THREADS / 32);  // rows gathered per warp
-  static_assert(NN == 64, "swizzled KLT kernel: N = 64 (two 128 B K atoms)");
-  extern __shared__ __align__(1024) unsigned char sm[];
-  auto a_st = [&](int st, int lo) { return sm + (2 * st + lo) * A_BYTES; };
-  unsigned char* b_hi = sm + 4 * A_BYTES;
-  unsigned char* b_lo = sm + 4 * A_BYTES + B_BYTES;
-  __shared__ __align__(8) uint64_t mbar[2];
-  __shared__ uint32_t tmem_base_sh;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int half = tid / M;
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                 :: "r"(smem_u32(&tmem_base_sh)), "r"(2u * NN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&mbar[0])));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&mbar[1])));
-    asm volatile("fence.mbarrier_init.release.cluster;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tmem = tmem_base_sh;
-  uint32_t phase[2] = {0, 0};
-  // swizzled byte offset of (row r, 16 B chunk q of the full 256 B row) inside an operand tile
-  auto swz = [&](int rows, int r, int q) -> uint32_t {
-    return (uint32_t)(q >> 3) * (rows * 128u) + (uint32_t)r * 128u + (uint32_t)(((q & 7) ^ (r & 7)) << 4);
-  };
-  auto row_of = [&](uint64_t s0, uint64_t s1, uint64_t t, int r) -> uint64_t {
-    const uint64_t p = s0 + t * M + r;
-    return p < s1 ? (P.idx ? (uint64_t)__ldg(P.idx + p) : p) : ~0ull;
-  };
-
-  // row ids this lane gathers for a tile (rows warp*RPW + 2i + lane/16), loaded a tile ahead
-  auto gather_rows = [&](uint64_t s0, uint64_t s1, uint64_t t, uint64_t (&rows)[RPW / 2]) {
-#pragma unroll
-    for (int i = 0; i < RPW / 2; ++i) rows[i] = row_of(s0, s1, t, warp * RPW + 2 * i + (lane >> 4));
-  };
-  auto fetch = [&](const uint64_t (&rows)[RPW / 2], float4 (&v)[RPW / 2]) {
-    const int q = lane & 15;
-#pragma unroll
-    for (int i = 0; i < RPW / 2; ++i)  // chunk lane%16 of rows warp*RPW + 2i + lane/16
-      v[i] = rows[i] != ~0ull ? __ldcs(reinterpret_cast<const float4*>(P.in + rows[i] * NN) + q)
-                              : make_float4(0.f, 0.f, 0.f, 0.f);
-  };
-  auto stash = [&](const float4 (&v)[RPW / 2], int st) {  // tf32 split into the swizzled A stage
-    const int q = lane & 15;
-#pragma unroll
-    for (int i = 0; i < RPW / 2; ++i) {
-      const int r = warp * RPW + 2 * i + (lane >> 4);
-      const float4 h = make_float4(to_tf32(v[i].x), to_tf32(v[i].y), to_tf32(v[i].z), to_tf32(v[i].w));
-      const float4 l = make_float4(to_tf32(v[i].x - h.x), to_tf32(v[i].y - h.y), to_tf32(v[i].z - h.z),
-                                   to_tf32(v[i].w - h.w));
-      const uint32_t off = swz(M, r, q);
-      *reinterpret_cast<float4*>(a_st(st, 0) + off) = h;
-      *reinterpret_cast<float4*>(a_st(st, 1) + off) = l;
-    }
-    asm volatile("fence.proxy.async.shared::cta;");
-  };
-  auto issue = [&](int st) {  // one thread: 3xTF32 MMAs of a 128 x NN tile into accumulator st
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    const uint32_t idesc = idesc_tf32(NN);
-    const uint32_t ahi = smem_u32(a_st(st, 0)), alo = smem_u32(a_st(st, 1));
-    const uint32_t bhi = smem_u32(b_hi), blo = smem_u32(b_lo);
-    const uint32_t d = tmem + (uint32_t)(st * NN);
-    int first = 1;
-#pragma unroll
-    for (int ks = 0; ks < NN / 8; ++ks) {  // K = 8 tf32 = 32 B per instruction
-      const uint32_t aoff = (uint32_t)(ks >> 2) * (M * 128) + (uint32_t)(ks & 3) * 32;
-      const uint32_t boff = (uint32_t)(ks >> 2) * (NN * 128) + (uint32_t)(ks & 3) * 32;
-      const uint64_t da[3] = {umma_desc_sw128(alo + aoff), umma_desc_sw128(ahi + aoff), umma_desc_sw128(ahi + aoff)};
-      const uint64_t db[3] = {umma_desc_sw128(bhi + boff), umma_desc_sw128(blo + boff), umma_desc_sw128(bhi + boff)};
-#pragma unroll
-      for (int term = 0; term < 3; ++term) {  // small terms first
-        const uint32_t acc = first ? 0u : 1u;
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
-            :: "r"(d), "l"(da[term]), "l"(db[term]), "r"(idesc), "r"(acc));
-        first = 0;
-      }
-    }
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
-                 :: "r"(smem_u32(&mbar[st])));
-  };
-  auto wait_mma = [&](int st) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t@!P1 bra WAIT_%=;\n\t}\n"
-        :: "r"(smem_u32(&mbar[st])), "r"(phase[st]));
-    phase[st] ^= 1;
-    asm volatile("tcgen05.fence::after_thread_sync;");
-  };
-  // accumulator st -> swizzled staging (the spent A-hi stage, row r at r*256 B) -> coalesced rows
-  auto drain = [&](uint64_t s0, uint64_t s1, uint64_t t, int st) {
-    unsigned char* stg = a_st(st, 0);
-    const int r = (warp & 3) * 32 + lane;  // TMEM lane = tile row
-#pragma unroll
-    for (int c1 = 0; c1 < NN / 2; c1 += 16) {
-      const int c0 = half * (NN / 2) + c1;
-      uint32_t v[16];
-      const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(st * NN + c0);
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-            "=r"(v[14]), "=r"(v[15])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;");
-#pragma unroll
-      for (int j = 0; j < 16; j += 4) {
-        const int q = (c0 + j) >> 2;
-        *reinterpret_cast<uint4*>(stg + (uint32_t)r * 256u + (uint32_t)(((q & 8) | ((q & 7) ^ (r & 7))) << 4)) =
-            make_uint4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-      }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
-    const int q = lane & 15;
-#pragma unroll
-    for (int i = 0; i < RPW / 2; ++i) {
-      const int rr = warp * RPW + 2 * i + (lane >> 4);
-      const uint64_t row = row_of(s0, s1, t, rr);
-      const float4 o = *reinterpret_cast<const float4*>(stg + (uint32_t)rr * 256u +
-                                                        (uint32_t)(((q & 8) | ((q & 7) ^ (rr & 7))) << 4));
-      if (row != ~0ull) __stcs(reinterpret_cast<float4*>(P.out + row * NN) + q, o);
-    }
-  };
-
-  const int C = P.idx ? P.classes : 1;
-  for (int c = 0; c < C; ++c) {
-    const uint64_t s0 = P.idx ? (c == 0 ? 0 : P.seg_end[c - 1]) : 0;
-    const uint64_t s1 = P.idx ? P.seg_end[c] : P.count;
-    if (s1 <= s0) continue;
-    const uint64_t tiles = (s1 - s0 + M - 1) / M;
-    if (tiles <= blockIdx.x) continue;
-    __syncthreads();  // the previous class's MMAs and drains are complete
-    {  // this class's B operand (hi then lo), prepared on the host in the swizzled layout
-      const float4* src = reinterpret_cast<const float4*>(P.b + (size_t)c * 2 * NN * NN);
-      float4* dst = reinterpret_cast<float4*>(b_hi);
-      for (int i = tid; i < 2 * NN * NN / 4; i += KLT_PIPE_THREADS) dst[i] = __ldg(src + i);
-    }
-    // Software pipeline: the rows of tile t+1 are in registers while tile t is in the tensor
-    // cores; their ids were fetched one tile earlier still.
-    uint64_t t = blockIdx.x;
-    int st = 0;
-    uint64_t rows[RPW / 2];
-    float4 v[RPW / 2];
-    gather_rows(s0, s1, t, rows);
-    fetch(rows, v);
-    stash(v, st);
-    const bool two = t + gridDim.x < tiles;
-    if (two) {
-      gather_rows(s0, s1, t + gridDim.x, rows);
-      fetch(rows, v);
-      gather_rows(s0, s1, t + 2 * (uint64_t)gridDim.x, rows);
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
-    if (tid == 0) issue(st);
-    for (;;) {
-      const uint64_t tn = t + gridDim.x;
-      const bool more = tn < tiles;
-      if (more) stash(v, st ^ 1);  // rows of tile tn (loaded during the previous iteration)
-      wait_mma(st);
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncthreads();  // A(tn) written; accumulator st^1 free
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      if (more && tid == 0) issue(st ^ 1);  // overlaps the drain of t
-      if (tn + gridDim.x < tiles) {           // rows of the tile after tn: in flight over the drain
-        fetch(rows, v);
-        gather_rows(s0, s1, tn + 2 * (uint64_t)gridDim.x, rows);
-      }
-      drain(s0, s1, t, st);
-      __syncthreads();  // staging reads done before stage st is refilled
-      if (!more) break;
-      t = tn;
-      st ^= 1;
-    }
-  }
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(2u * NN));
-}
-
 // Host: B operand of one class in the canonical layout, split into tf32 hi/lo.
 float host_tf32(float x) {  // round to nearest (ties away), 10 explicit mantissa bits
   uint32_t u;
@@ -628,19 +263,6 @@ void build_b(const float* m /*[n][n] row-major: B[nrow][k]*/, int n, float* out 
     }
 }
 
-// Host: B operand of one class in the SWIZZLE_128B K-major layout (64 x 64), hi then lo.
-void build_b_sw128(const float* m /*[n][n]: B[nrow][k]*/, int n, float* out) {
-  for (int r = 0; r < n; ++r)
-    for (int k = 0; k < n; ++k) {
-      const float v = m[(size_t)r * n + k];
-      const float h = host_tf32(v), l = host_tf32(v - h);
-      const int q = k / 4, atom = q >> 3;
-      const size_t byte = (size_t)atom * (n * 128) + (size_t)r * 128 + (size_t)(((q & 7) ^ (r & 7)) << 4) + (k % 4) * 4;
-      out[byte / 4] = h;
-      out[(size_t)n * n + byte / 4] = l;
-    }
-}
-
 template <int NN>
 int launch_tc(const hygt_klt_plan* p, int dir, const float* in, float* out, const uint32_t* idx,
               const uint32_t* seg_end, uint64_t count, cudaStream_t st) {
@@ -657,31 +279,25 @@ int launch_tc(const hygt_klt_plan* p, int dir, const float* in, float* out, cons
   return e == cudaSuccess ? HYGT_OK : kfail(HYGT_ERR_CUDA, cudaGetErrorString(e));
 }
 
-template <int NN>
-int launch_pipe(const hygt_klt_plan* p, int dir, const float* in, float* out, const uint32_t* idx,
-                const uint32_t* seg_end, uint64_t count, cudaStream_t st) {
-  if (getenv("HYGT_KLT_PIPE") && atoi(getenv("HYGT_KLT_PIPE")) == 0)
-    return launch_tc<NN>(p, dir, in, out, idx, seg_end, count, st);
-  const size_t smem = (size_t)4 * 128 * NN * 4 + (size_t)2 * NN * NN * 4;
-  hygt_smem_attr(reinterpret_cast<const void*>(klt_tc_pipe_kernel<NN>), smem);
-  const uint64_t tiles = (count + 127) / 128;
-  const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)p->num_sms, tiles);
-  if (p->d_bsw[dir] && !(getenv("HYGT_KLT_SW") && atoi(getenv("HYGT_KLT_SW")) == 0)) {
-    hygt_smem_attr(reinterpret_cast<const void*>(klt_sw_kernel<NN>), smem);
-    KltTcParams Q{in, out, idx, seg_end, p->classes, count, p->d_bsw[dir]};
-    klt_sw_kernel<NN><<<grid, KLT_PIPE_THREADS, smem, st>>>(Q);
-  } else {
-    KltTcParams P{in, out, idx, seg_end, p->classes, count, p->d_b[dir]};
-    klt_tc_pipe_kernel<NN><<<grid, KLT_PIPE_THREADS, smem, st>>>(P);
-  }
-  const cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? HYGT_OK : kfail(HYGT_ERR_CUDA, cudaGetErrorString(e));
-}
-
 int run_klt(const hygt_klt_plan* p, bool fwd, const float* in, float* out, const uint16_t* cls,
             uint64_t count, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (!p) return kfail(HYGT_ERR_ARGUMENT, "klt: null plan");
   if (!count) return HYGT_OK;
+  if (p->gemm) {  // per-class grouped GEMM on the tensor cores (in place allowed)
+    if (((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) != 0)
+      return kfail(HYGT_ERR_ARGUMENT, "klt: x and y must be aligned to 16 bytes");
+    if (count > 0xFFFFFFFFull) return kfail(HYGT_ERR_ARGUMENT, "klt: at most 2^32-1 rows per call");
+    const uint32_t* idx = nullptr;
+    const uint32_t* seg = nullptr;
+    uint32_t nseg = 0;
+    if (cls && p->classes > 1) {
+      if (!ws || ws_bytes < hygt_gpu::bucket_ws_bytes(p->classes, 0, count))
+        return kfail(HYGT_ERR_ARGUMENT, "klt: workspace too small");
+      if (int s = hygt_gpu::bucket_rows(p->classes, 0, cls, count, ws, ws_bytes, true, st, &idx, &seg, &nseg))
+        return s;
+    }
+    return hygt_gpu::gemm_run(p->gops[fwd ? 0 : 1], in, out, idx, seg, count, nullptr, st);
+  }
   if (in == out) return kfail(HYGT_ERR_ARGUMENT, "klt: in-place not supported");
   if (p->tc) {
     const uint32_t* idx = nullptr;
@@ -697,7 +313,6 @@ int run_klt(const hygt_klt_plan* p, bool fwd, const float* in, float* out, const
     switch (p->n) {
       case 16: return launch_tc<16>(p, dir, in, out, idx, seg, count, st);
       case 32: return launch_tc<32>(p, dir, in, out, idx, seg, count, st);
-      case 64: return launch_pipe<64>(p, dir, in, out, idx, seg, count, st);
       default: break;
     }
   }
@@ -733,7 +348,27 @@ extern "C" int hygt_klt_plan_create(int n, int class_count, const double* k, uin
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, dev);
-  p->tc = (n == 16 || n == 32 || n == 64) && !(flags & 1u);  // flag bit 0: force SIMT
+  p->tc = (n == 16 || n == 32) && !(flags & 1u);  // flag bit 0: force SIMT
+  if (!(flags & 1u) && hygt_gpu::gemm_supported(n, class_count)) {
+    // forward y = K x: B[nrow][k] = K[nrow][k]; inverse x = K^T y: B = K^T (fp64 from the caller)
+    std::vector<double> kt(nn);
+    for (int c = 0; c < class_count; ++c)
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) kt[((size_t)c * n + j) * n + i] = k[((size_t)c * n + i) * n + j];
+    hygt_klt_plan* q = new hygt_klt_plan();
+    q->n = n;
+    q->classes = class_count;
+    q->num_sms = 148;
+    int st = hygt_gpu::gemm_build(n, class_count, k, q->gops[0]);
+    if (!st) st = hygt_gpu::gemm_build(n, class_count, kt.data(), q->gops[1]);
+    if (st) {
+      hygt_klt_plan_destroy(q);
+      return st;
+    }
+    q->gemm = true;
+    *out = q;
+    return HYGT_OK;
+  }
   bool okk = cudaMalloc(&p->d_k, nn * sizeof(float)) == cudaSuccess &&
              cudaMalloc(&p->d_kt, nn * sizeof(float)) == cudaSuccess &&
              cudaMemcpy(p->d_k, kf.data(), nn * sizeof(float), cudaMemcpyHostToDevice) == cudaSuccess &&
@@ -746,12 +381,6 @@ extern "C" int hygt_klt_plan_create(int n, int class_count, const double* k, uin
         build_b((d == 0 ? kf.data() : ktf.data()) + (size_t)c * n * n, n, b.data() + (size_t)c * 2 * n * n);
       okk = cudaMalloc(&p->d_b[d], b.size() * sizeof(float)) == cudaSuccess &&
             cudaMemcpy(p->d_b[d], b.data(), b.size() * sizeof(float), cudaMemcpyHostToDevice) == cudaSuccess;
-      if (okk && n == 64) {
-        for (int c = 0; c < class_count; ++c)
-          build_b_sw128((d == 0 ? kf.data() : ktf.data()) + (size_t)c * n * n, n, b.data() + (size_t)c * 2 * n * n);
-        okk = cudaMalloc(&p->d_bsw[d], b.size() * sizeof(float)) == cudaSuccess &&
-              cudaMemcpy(p->d_bsw[d], b.data(), b.size() * sizeof(float), cudaMemcpyHostToDevice) == cudaSuccess;
-      }
     }
   }
   if (!okk) {
@@ -768,14 +397,14 @@ extern "C" int hygt_klt_plan_destroy(hygt_klt_plan* p) {
   cudaFree(p->d_kt);
   cudaFree(p->d_b[0]);
   cudaFree(p->d_b[1]);
-  cudaFree(p->d_bsw[0]);
-  cudaFree(p->d_bsw[1]);
+  hygt_gpu::gemm_release(p->gops[0]);
+  hygt_gpu::gemm_release(p->gops[1]);
   delete p;
   return HYGT_OK;
 }
 
 extern "C" size_t hygt_klt_workspace_bytes(const hygt_klt_plan* plan, uint64_t count) {
-  if (!plan || !plan->tc || plan->classes <= 1) return 256;
+  if (!plan || !(plan->tc || plan->gemm) || plan->classes <= 1) return 256;
   return hygt_gpu::bucket_ws_bytes(plan->classes, 0, count);
 }
 

@@ -389,7 +389,9 @@ class KLTPlan:
         return _lib.lib().hygt_klt_workspace_bytes(self._h, count)
 
     def kernel_name(self) -> str:
-        return "klt_sw_kernel<64> (tcgen05.mma kind::tf32, 3xTF32)" if self.n == 64 else "klt_tc_kernel"
+        if self.n in (64, 128, 256):
+            return "hygt_gemm_kernel (per-class grouped GEMM, tcgen05.mma kind::f16 3-term split, CTA pairs)"
+        return "klt_tc_kernel (tcgen05.mma kind::tf32, 3xTF32)" if self.n in (16, 32) else "klt_simt_kernel"
 
     def launches_per_call(self) -> int:
         return 4 if self.classes > 1 else 1  # bucketing (3) + the GEMM kernel
@@ -417,7 +419,7 @@ class KLTPlan:
         return out
 
     def forward(self, x, cls=None, out=None, stream=None, workspace=None):
-        """y = K_c x per row on the tensor cores (3xTF32), rows of class c = cls[row]."""
+        """y = K_c x per row on the tensor cores, rows of class c = cls[row]."""
         return self._run(_lib.lib().hygt_klt_forward_f32, x, cls, out, stream, workspace)
 
     def inverse(self, y, cls=None, out=None, stream=None, workspace=None):

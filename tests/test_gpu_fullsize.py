@@ -128,3 +128,28 @@ def test_config3_full_size(cuda, oracle_mod):
     ys, cs = y[idx].cpu().numpy(), _take(cls, idx).cpu().numpy()
     refi = O.apply_batch(6, 4, w.angles, full, mask, ys, cs, inverse=True, hoist=True)
     check_close(back[idx].cpu().numpy(), refi, ys, "cfg3 inverse sample")
+
+
+def test_config4_klt_full_size(cuda, oracle_mod):
+    """Config 4 at its configured size: 35 random orthogonal 64 x 64 bases on config 3's 2^22
+    class-tagged rows (the grouped GEMM on the tensor cores): round trip over all rows, forward
+    and inverse on a 65,536-row sample against the oracle's fp64 matvec (matrix.hpp:70-88)."""
+    from paper_2505_21728_b200 import KLTPlan
+    from paper_2505_21728_b200.synth import make_workload
+    O = oracle_mod
+    w = make_workload(4)
+    count = w.cfg.count
+    k = w.klt_bases()
+    plan = KLTPlan(k)
+    cls = w.make_classes(count)
+    x = w.make_rows(count, cls)
+    ws = torch.zeros(plan.workspace_bytes(count), dtype=torch.uint8, device=cuda)
+    y = plan.forward(x, cls, workspace=ws)
+    back = plan.inverse(y, cls, workspace=ws)
+    torch.cuda.synchronize()
+    _roundtrip_and_norms(x, y, back)
+    idx = _sample(count, 1 << 16, cuda)
+    xs, cs = x[idx].cpu().numpy(), _take(cls, idx).cpu().numpy()
+    check_close(y[idx].cpu().numpy(), O.klt_apply(k, xs, cs), xs, "cfg4 forward sample")
+    ys = y[idx].cpu().numpy()
+    check_close(back[idx].cpu().numpy(), O.klt_apply(k, ys, cs, inverse=True), ys, "cfg4 inverse sample")

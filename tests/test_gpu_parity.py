@@ -400,6 +400,27 @@ def test_klt_multi_tile_pipeline(cuda, oracle_mod):
     check_close(y.cpu().numpy()[idx], ref, xs, "klt multi-tile sample")
 
 
+@pytest.mark.parametrize("n,classes,rows", [(64, 3, 777), (128, 5, 3001), (256, 4, 2049), (256, 1, 300)])
+def test_klt_grouped_gemm_sizes(cuda, oracle_mod, n, classes, rows):
+    """The KLT on the tensor-core grouped GEMM at N = 64 / 128 / 256 (random orthogonal bases,
+    matrix.hpp:70-88), ragged class runs, in place, a single class without ids."""
+    from paper_2505_21728_b200 import KLTPlan
+    k = np.stack([oracle_mod.random_orthogonal(100 + c, n) for c in range(classes)])
+    plan = KLTPlan(k)
+    rng = np.random.default_rng(n + rows)
+    x = (rng.standard_normal((rows, n)) * 16).astype(np.float32)
+    cls = rng.integers(0, classes, rows).astype(np.uint16)
+    xd = torch.from_numpy(x).to(cuda)
+    cd = torch.from_numpy(cls).to(cuda) if classes > 1 else None
+    y = plan.forward(xd, cd)
+    ref = oracle_mod.klt_apply(k, x, cls if classes > 1 else None)
+    check_close(y.cpu().numpy(), ref, x, f"klt N={n} fwd")
+    refi = oracle_mod.klt_apply(k, x, cls if classes > 1 else None, inverse=True)
+    z = xd.clone()
+    plan.inverse(z, cd, out=z)  # in place
+    check_close(z.cpu().numpy(), refi, x, f"klt N={n} inv")
+
+
 @pytest.mark.parametrize("log2n", [5, 6])
 def test_clsjit_steady_state(cuda, oracle_mod, log2n):
     """Per-class NVRTC chain at a size where each warp runs several batches of its class (the
