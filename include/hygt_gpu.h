@@ -78,6 +78,28 @@ int hygt_last_error(char* buf, size_t len);
 int hygt_plan_create(int log2_n, int rounds, int class_count, const double* angles,
                      const uint16_t* perms, uint32_t perm_mask, uint32_t flags,
                      hygt_plan** out);
+
+/* Plan-creation options (the library reads no environment variables). Zero-initialise, set
+ * .size = sizeof(hygt_plan_options) and change the fields to override; NULL = all defaults. */
+#define HYGT_KERNEL_AUTO 0      /* the measured-best kernel family for the shape */
+#define HYGT_KERNEL_BUTTERFLY 1 /* rotation kernels only: the pass-by-pass butterfly form */
+#define HYGT_KERNEL_TENSOR 2    /* the composed-operator tensor-core path (N = 64 / 128 / 256,
+                                   <= 512 classes); HYGT_ERR_ARGUMENT for other shapes */
+typedef struct hygt_plan_options {
+  uint32_t size;       /* sizeof(hygt_plan_options) */
+  int kernel;          /* HYGT_KERNEL_AUTO / _BUTTERFLY / _TENSOR */
+  int allow_nvrtc;     /* 1 (default): plan-specialised kernels may be compiled with NVRTC at
+                          plan creation (seconds per plan, cached per process); 0: precompiled
+                          kernels only */
+  int cta_pairs;       /* tensor-core path: 1 (default) CTA pairs (tcgen05 cta_group::2, M = 256,
+                          each SM streams half of the class operator); 0 single CTAs */
+  int stage_tile_rows; /* N = 16 staged kernel: rows per tile (multiple of 8 in [128, 1016]);
+                          0 = sized to the shared memory (default) */
+} hygt_plan_options;
+/* hygt_plan_create with options (opts may be NULL). */
+int hygt_plan_create_ex(int log2_n, int rounds, int class_count, const double* angles,
+                        const uint16_t* perms, uint32_t perm_mask, uint32_t flags,
+                        const hygt_plan_options* opts, hygt_plan** out);
 int hygt_plan_destroy(hygt_plan* plan);
 /* 0 = standard rotations, 1 = scale-folded (fast Givens) form chosen at plan time. */
 int hygt_plan_algorithm(const hygt_plan* plan);
@@ -97,11 +119,15 @@ int hygt_plan_algorithm(const hygt_plan* plan);
  *     the class grids chained by programmatic dependent launch. Forward-with-energy calls run
  *     on the class-segment kernel instead,
  * 7 = the chain of 6 with one plan-specialised kernel per class and direction (NVRTC at plan
- *     creation, N = 32 / 64 / 256, R <= 8, >= 2 classes not served by 3): coefficients are FFMA
+ *     creation, N = 32 / 64, R <= 8, >= 2 classes not served by 3): coefficients are FFMA
  *     immediates and permutations register renames, so the class's rows touch shared memory
- *     only on their way in and out (N = 256: a row is split over a warp pair that exchanges half
- *     its samples once per round; forward-with-energy fused). Forward-with-energy calls of
- *     N = 32 / 64 plans run on the tile / segment kernels instead. */
+ *     only on their way in and out. Forward-with-energy calls run on the tile / segment
+ *     kernels instead,
+ * 8 = the composed-operator tensor-core path (N = 64 / 128 / 256; the default at N = 256): the
+ *     plan composes each class's rounds, passes and permutations into one N x N matrix (fp64)
+ *     and the rows are transformed by a per-class grouped GEMM on tcgen05 (fp16 3-term split
+ *     with per-row power-of-two scaling, fp32 accumulation in TMEM, CTA pairs), the per-class
+ *     energy fused in its epilogue. */
 int hygt_plan_path(const hygt_plan* plan);
 
 /* Device workspace for class bucketing of `count` rows. The first word of a workspace is the
@@ -138,6 +164,10 @@ int hygt_sync_status(const hygt_plan* plan, void* d_ws, void* stream);
 int hygt_fixed_plan_create(int log2_n, int rounds, int class_count, int angle_bits,
                            int precision_bits, const uint16_t* codes, const uint16_t* perms,
                            uint32_t perm_mask, hygt_plan** out);
+/* The same with options (opts may be NULL; only allow_nvrtc applies to fixed-point plans). */
+int hygt_fixed_plan_create_ex(int log2_n, int rounds, int class_count, int angle_bits,
+                              int precision_bits, const uint16_t* codes, const uint16_t* perms,
+                              uint32_t perm_mask, const hygt_plan_options* opts, hygt_plan** out);
 int hygt_forward_i64(const hygt_plan* plan, const int64_t* d_x, int64_t* d_y,
                      const uint16_t* d_cls, uint64_t count, uint64_t* first_bad, void* stream);
 int hygt_inverse_i64(const hygt_plan* plan, const int64_t* d_y, int64_t* d_x,

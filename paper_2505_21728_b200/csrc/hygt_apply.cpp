@@ -2,7 +2,7 @@
 // (tools/hygt_main.cpp:130-172, option surface :247-256, exit codes :275-284).
 //
 //   hygt_gpu_apply --model M.hygt --data D.rblk [--direction forward|inverse]
-//                  [--arithmetic float|fixed] --out O.rblk
+//                  [--arithmetic float|fixed] --out O.rblk [--timing]
 //
 // Reads the HYGT model bundle (bundle.hpp:105-191) and the RBLK dataset (dataset.hpp:72-119),
 // transforms every block on the GPU through the C ABI (include/hygt_gpu.h) and writes the RBLK
@@ -166,8 +166,10 @@ struct Dataset {
 };
 
 // Parses RBLK records (u16 class + N fp32, dataset.hpp:68-70) into SoA buffers.
+bool g_timing = false;  // --timing: per-phase wall times on stderr
+
 Dataset read_rblk(const std::string& path, bool fixed, int bundle_classes, std::thread& cuda_init) {
-  const bool timing = std::getenv("HYGT_APPLY_TIMING") != nullptr;
+  const bool timing = g_timing;
   auto t0 = std::chrono::steady_clock::now();
   auto mark = [&](const char* what) {
     const auto t = std::chrono::steady_clock::now();
@@ -275,6 +277,7 @@ void write_rblk(const std::string& path, const Dataset& d, const void* y, bool f
 
 struct Args {
   std::string model, data, direction = "forward", arithmetic = "float", out;
+  bool timing = false;
 };
 
 Args parse(int argc, char** argv) {
@@ -290,6 +293,7 @@ Args parse(int argc, char** argv) {
     else if (k == "--direction") a.direction = val();
     else if (k == "--arithmetic") a.arithmetic = val();
     else if (k == "--out") a.out = val();
+    else if (k == "--timing") a.timing = true;
     else arg_error("unknown option " + k);
   }
   if (a.model.empty() || a.data.empty() || a.out.empty()) arg_error("--model, --data and --out are required");
@@ -299,7 +303,8 @@ Args parse(int argc, char** argv) {
 }
 
 int run(const Args& a) {
-  const bool timing = std::getenv("HYGT_APPLY_TIMING") != nullptr;
+  g_timing = a.timing;
+  const bool timing = a.timing;
   auto t_last = std::chrono::steady_clock::now();
   auto phase = [&](const char* name) {
     const auto t = std::chrono::steady_clock::now();

@@ -24,6 +24,7 @@
 #include "hygt_plan.h"
 #include "hygt_jit.h"
 #include "hygt_gemm.h"
+#include "hygt_knobs.h"
 
 using namespace hygt_gpu;
 #include "hygt_dispatch.h"
@@ -66,6 +67,7 @@ extern "C" int hygt_last_error(char* buf, size_t len) {
 // ============================================================================ plan =======
 struct hygt_plan {
   int kind = 0;  // 0 float, 1 fixed
+  hygt_plan_options opt{};  // resolved creation options (include/hygt_gpu.h)
   int log2n = 0, rounds = 0, classes = 0, lanes_log2 = 0;
   int algo = 0;  // 0 standard, 1 scale-folded
   uint32_t perm_mask = 0;
@@ -104,8 +106,6 @@ struct hygt_plan {
   uint32_t stage_rows = 0, stage_cw = 0, stage_block_words = 0;
   float4* d_scoef[2] = {nullptr, nullptr};
   uint16_t* d_sgtab[2] = {nullptr, nullptr};
-  uint2* d_sbnet[2] = {nullptr, nullptr};  // Beneš swap masks [C][R+1][4 rotations] (N = 16)
-  uint32_t sbnet_steps[2] = {0u, 0u};      // gather steps the Beneš network serves, per direction
   size_t stage_smem[2] = {0, 0};
   // seg2 path (N = 64): thread-per-row over global class buckets, element-ordered tables
   bool seg2 = false;
@@ -161,7 +161,6 @@ void free_plan(hygt_plan* p) {
     cudaFree(p->d_tgidx[d]);
     cudaFree(p->d_scoef[d]);
     cudaFree(p->d_sgtab[d]);
-    cudaFree(p->d_sbnet[d]);
   }
   cudaFree(p->d_codes);
   cudaFree(p->d_cos);
@@ -176,6 +175,30 @@ void free_plan(hygt_plan* p) {
   gemm_release(p->gemm_ops[1]);
   delete p->fixed_mu;
   delete p;
+}
+
+// Options with the defaults filled in; HYGT_ERR_ARGUMENT for malformed ones.
+int resolve_options(const hygt_plan_options* in, hygt_plan_options& out) {
+  out = hygt_plan_options{};
+  out.size = sizeof(hygt_plan_options);
+  out.kernel = HYGT_KERNEL_AUTO;
+  out.allow_nvrtc = 1;
+  out.cta_pairs = 1;
+  out.stage_tile_rows = 0;
+  if (!in) return HYGT_OK;
+  if (in->size < sizeof(uint32_t) || in->size > sizeof(hygt_plan_options))
+    return fail(HYGT_ERR_ARGUMENT, "hygt_plan_options: size must be sizeof(hygt_plan_options)");
+  hygt_plan_options o = out;
+  std::memcpy(&o, in, in->size);
+  if (o.kernel < HYGT_KERNEL_AUTO || o.kernel > HYGT_KERNEL_TENSOR)
+    return fail(HYGT_ERR_ARGUMENT, "hygt_plan_options: unknown kernel family");
+  if (o.allow_nvrtc < 0) o.allow_nvrtc = 1;
+  if (o.cta_pairs < 0) o.cta_pairs = 1;
+  if (o.stage_tile_rows != 0 && (o.stage_tile_rows < 128 || o.stage_tile_rows > 1016 || o.stage_tile_rows % 8))
+    return fail(HYGT_ERR_ARGUMENT, "hygt_plan_options: stage_tile_rows must be a multiple of 8 in [128, 1016]");
+  out = o;
+  out.size = sizeof(hygt_plan_options);
+  return HYGT_OK;
 }
 
 int check_perms(int log2n, int rounds, int classes, const uint16_t* perms, uint32_t mask) {
@@ -211,10 +234,8 @@ void hygt_smem_attr(const void* fn, size_t bytes) {
 }
 
 namespace {
-int env_int(const char* name, int dflt) {
-  const char* v = std::getenv(name);
-  return v && *v ? std::atoi(v) : dflt;
-}
+// Development knobs (hygt_knobs.h): the test hook's value, or the measured-best default.
+int env_int(const char* name, int dflt) { return knob(name, dflt); }
 
 // Kernels' dynamic shared-memory limits are per function, shared by every plan; plans need
 // different sizes, so the attribute only ever grows (a smaller later plan must not shrink it
@@ -685,13 +706,6 @@ int build_elem_tables(hygt_plan* p, const double* angles, const uint16_t* perms,
   return HYGT_OK;
 }
 
-// Gather steps the Beneš network serves: all (mode 1) or only the first one (mode 2).
-uint32_t stage_benes_steps(uint64_t gmask, int mode) {
-  if (mode == 1) return (uint32_t)gmask;
-  if (mode == 2) return (uint32_t)(gmask & (0 - gmask));
-  return 0u;
-}
-
 int setup_stage(hygt_plan* p, const double* angles, const uint16_t* perms) {
   StageFn probe = select_stage(p->log2n, p->algo == 0, true);
   if (!probe || env_int("HYGT_STAGE", 1) == 0 || p->classes > STAGE_MAX_CLASSES) return HYGT_OK;
@@ -699,57 +713,21 @@ int setup_stage(hygt_plan* p, const double* angles, const uint16_t* perms) {
   const bool standard = p->algo == 0;
   uint32_t cw = 0;
   if (int s = build_elem_tables(p, angles, perms, &cw)) return s;
-  // In-register permutations: each gather routed through a Beneš network (7 layers of
-  // conditional swaps at N = 16), its swap bits re-indexed for each lane rotation X = x << 2.
-  const int benes_mode = env_int("HYGT_STAGE_BENES", 0);  // 0 off, 1 every gather, 2 the first one
-  const bool benes = (p->gmask[0] || p->gmask[1]) && benes_mode != 0;
-  if (benes) {
-    const int n = 1 << p->log2n, layers = 2 * p->log2n - 1;
-    for (int d = 0; d < 2; ++d) {
-      std::vector<uint2> tab((size_t)C * (R + 1) * 4, make_uint2(0, 0));
-      for (int c = 0; c < C; ++c) {
-        uint64_t gm = 0;
-        const auto g = exec_gathers(p->log2n, R, perms ? perms + (size_t)c * R * n : nullptr, p->perm_mask, d == 0, &gm);
-        for (int k = 0; k <= R; ++k) {
-          if (g[k].empty()) continue;
-          std::vector<std::vector<int>> sw;
-          if (!benes_route(p->log2n, g[k], sw)) return fail(HYGT_ERR_NUMERICAL, "hygt: Benes routing failed");
-          for (int x = 0; x < 4; ++x) {
-            const int X = x << 2;
-            uint64_t bits = 0;
-            for (int l = 0; l < layers; ++l) {
-              const int b = l < p->log2n ? p->log2n - 1 - l : l - p->log2n + 1;
-              int j = 0;
-              for (int i = 0; i < n; ++i) {
-                if (i & (1 << b)) continue;
-                if (sw[l][pair_index((i ^ X) & ~(1 << b), b)]) bits |= 1ull << (8 * l + j);
-                ++j;
-              }
-            }
-            tab[((size_t)c * (R + 1) + k) * 4 + x] = make_uint2((uint32_t)bits, (uint32_t)(bits >> 32));
-          }
-        }
-      }
-      if (int s = upload(&p->d_sbnet[d], tab.data(), tab.size())) return s;
-      p->sbnet_steps[d] = stage_benes_steps(p->gmask[d], benes_mode);
-    }
-  }
   // Tile rows: one batch of 32 * VPT sorted positions per consumer warp, including the padding
   // of every class run to VPT; rows are indexed with 10 bits in the sort entries.
-  const long long tenv = env_int("HYGT_STAGE_ROWS", -1);
+  const long long tenv = p->opt.stage_tile_rows > 0 ? p->opt.stage_tile_rows : env_int("HYGT_STAGE_ROWS", -1);
   uint32_t T = (uint32_t)std::max(0, STAGE_WARPS * 32 * STAGE_VPT - (STAGE_VPT - 1) * C);
   if (tenv > 0) T = (uint32_t)tenv;
   T = std::min<uint32_t>(T, 1016) / 8 * 8;
   size_t smem[2] = {0, 0};
   for (; T >= 128; T -= 8) {
     for (int d = 0; d < 2; ++d)
-      smem[d] = stage_smem_layout(p->log2n, STAGE_VPT, STAGE_WARPS, C, cw, R, T, p->gmask[d] != 0, benes,
-                                  benes && (p->gmask[d] & ~(uint64_t)stage_benes_steps(p->gmask[d], benes_mode)) != 0).total;
+      smem[d] = stage_smem_layout(p->log2n, STAGE_VPT, STAGE_WARPS, C, cw, R, T, p->gmask[d] != 0).total;
     if (std::max(smem[0], smem[1]) <= 227 * 1024) break;
   }
   if (T < 128) return HYGT_OK;  // tables too large for the staged layout
   for (int d = 0; d < 2; ++d) {
-    smem_attr(select_stage(p->log2n, standard, d == 0, p->d_sbnet[d] != nullptr), (int)smem[d]);
+    smem_attr(select_stage(p->log2n, standard, d == 0), (int)smem[d]);
     p->stage_smem[d] = smem[d];
   }
   cudaGetLastError();
@@ -813,7 +791,7 @@ int run_stage(const hygt_plan* p, int dir, const float* x, float* y, const uint1
   if (sorted && (!d_ws || ws_bytes < stage_ws_bytes(p, count)))
     return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
   // The debug build (trace hook set) is a separate instantiation with the same smem layout.
-  StageFn fn = select_stage(p->log2n, p->algo == 0, dir == 0, p->d_sbnet[dir] != nullptr, g_stage_trace != nullptr);
+  StageFn fn = select_stage(p->log2n, p->algo == 0, dir == 0, g_stage_trace != nullptr);
   if (g_stage_trace) smem_attr(fn, (int)p->stage_smem[dir]);
   StageParams P{};
   P.x = x;
@@ -824,8 +802,6 @@ int run_stage(const hygt_plan* p, int dir, const float* x, float* y, const uint1
   P.coef = p->d_scoef[dir];
   P.cw = p->stage_cw;
   P.gtab = p->d_sgtab[dir];
-  P.bnet = p->d_sbnet[dir];
-  P.bnet_steps = p->sbnet_steps[dir];
   P.gmask = p->gmask[dir];
   P.tile_rows = p->stage_rows;
   P.ent = sorted ? reinterpret_cast<const uint16_t*>(static_cast<const char*>(d_ws) + 256) : nullptr;
@@ -914,7 +890,7 @@ int setup_seg2(hygt_plan* p, const double* angles, const uint16_t* perms) {
 // ---- cls path (hygt_cls.cuh) ----------------------------------------------------------------
 int setup_cls(hygt_plan* p, const double* angles, const uint16_t* perms) {
   if (p->algo == 1 && !p->jit.ok && jit_cls_supported(p->log2n, p->classes, p->rounds) &&
-      env_int("HYGT_CLS_JIT", 1) != 0) {
+      p->opt.allow_nvrtc && env_int("HYGT_CLS_JIT", 1) != 0) {
     std::string err;
     if (jit_cls_build(p->log2n, p->rounds, p->classes, angles, perms, p->perm_mask, false, p->cls_jit, err)) {
       jit_cls_release(p->cls_jit);  // stay on the precompiled kernels
@@ -957,10 +933,10 @@ int setup_cls(hygt_plan* p, const double* angles, const uint16_t* perms) {
 }
 
 int run_cls(const hygt_plan* p, int dir, const float* x, float* y, const WsLayout& w, char* ws,
-            cudaStream_t st, double* energy = nullptr) {
+            cudaStream_t st) {
   if (p->cls_jit.ok) {
     if (jit_cls_launch(p->cls_jit, dir, x, y, reinterpret_cast<const uint32_t*>(ws + w.idx),
-                       reinterpret_cast<const uint32_t*>(ws + w.seg), p->classes, st, energy))
+                       reinterpret_cast<const uint32_t*>(ws + w.seg), p->classes, st))
       return fail(HYGT_ERR_CUDA, std::string("hygt: class launch failed: ") + cudaGetErrorString(cudaGetLastError()));
     return ok();
   }
@@ -987,7 +963,6 @@ int run_seg2(const hygt_plan* p, int dir, const float* x, float* y, uint64_t cou
   P.gtab = p->d_sgtab[dir];
   P.gstride = stage_gstride(p->log2n, p->rounds);
   P.gmask = p->gmask[dir];
-  P.use_tma = env_int("HYGT_SEG2_TMA", 0);  // per-row bulk copies measured slower (2.73e9 vs 3.00e9 vec/s)
   const uint64_t min_span = 4096;
   uint64_t ctas = std::min<uint64_t>((uint64_t)p->num_sms, (count + min_span - 1) / min_span);
   if (ctas < 1) ctas = 1;
@@ -1034,8 +1009,13 @@ int run_segment(const hygt_plan* p, int dir, const float* x, float* y, uint64_t 
 // it at N = 64 / 128 as well, HYGT_GEMM=0 never.
 int setup_gemm(hygt_plan* p, const double* angles, const uint16_t* perms) {
   const int n = 1 << p->log2n;
-  if (!gemm_supported(n, p->classes)) return HYGT_OK;
-  const int want = env_int("HYGT_GEMM", -1);
+  if (!gemm_supported(n, p->classes)) {
+    if (p->opt.kernel == HYGT_KERNEL_TENSOR)
+      return fail(HYGT_ERR_ARGUMENT, "hygt_plan_create: the tensor-core path needs N in {64, 128, 256} and <= 512 classes");
+    return HYGT_OK;
+  }
+  const int want = p->opt.kernel == HYGT_KERNEL_TENSOR ? 1 : p->opt.kernel == HYGT_KERNEL_BUTTERFLY ? 0
+                                                                                  : env_int("HYGT_GEMM", -1);
   if (want == 0 || (want < 0 && n != 256)) return HYGT_OK;
   const size_t a = (size_t)p->rounds * p->log2n * n / 2;
   std::vector<double> fwd((size_t)p->classes * n * n), inv((size_t)p->classes * n * n);
@@ -1049,6 +1029,10 @@ int setup_gemm(hygt_plan* p, const double* angles, const uint16_t* perms) {
   }
   if (int s = gemm_build(n, p->classes, fwd.data(), p->gemm_ops[0])) return s;
   if (int s = gemm_build(n, p->classes, inv.data(), p->gemm_ops[1])) return s;
+  for (int d = 0; d < 2; ++d) {
+    p->gemm_ops[d].pair = p->opt.cta_pairs != 0 && env_int("HYGT_GEMM_PAIR", 1) != 0;
+    p->gemm_ops[d].wide = env_int("HYGT_GEMM_WIDE", 0) != 0;  // measured slower
+  }
   p->gemm = true;
   p->chunk_rows = 0;  // global class buckets
   return HYGT_OK;
@@ -1101,14 +1085,14 @@ int run_apply(const hygt_plan* p, int dir, const float* x, float* y, const uint1
   }
   if (stage_usable(p, x, y, energy)) return run_stage(p, dir, x, y, d_cls, count, d_ws, ws_bytes, flags, st);
   const bool bucketed = d_cls && p->classes > 1;
-  // per-class launch chain (N = 32 / 64 / 256; the N = 256 kernels also fuse the energy)
-  if (p->cls && bucketed && (!energy || (p->cls_jit.ok && !p->cls_jit.fn_e.empty()))) {
+  // per-class launch chain (N = 32 / 64)
+  if (p->cls && bucketed && !energy) {
     if (!d_ws || ws_bytes < w.total) return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
     if (!(flags & HYGT_REUSE_BUCKETS)) {
       const int s = run_bucket(p, p->classes, 0, d_cls, count, d_ws, ws_bytes, st);
       if (s) return s;
     }
-    return run_cls(p, dir, x, y, w, static_cast<char*>(d_ws), st, energy);
+    return run_cls(p, dir, x, y, w, static_cast<char*>(d_ws), st);
   }
   if (p->tile) {
     if (d_cls && (!d_ws || ws_bytes < 256)) return fail(HYGT_ERR_ARGUMENT, "hygt: workspace too small");
@@ -1179,8 +1163,16 @@ int run_apply(const hygt_plan* p, int dir, const float* x, float* y, const uint1
 extern "C" int hygt_plan_create(int log2_n, int rounds, int class_count, const double* angles,
                                 const uint16_t* perms, uint32_t perm_mask, uint32_t flags,
                                 hygt_plan** out) {
+  return hygt_plan_create_ex(log2_n, rounds, class_count, angles, perms, perm_mask, flags, nullptr, out);
+}
+
+extern "C" int hygt_plan_create_ex(int log2_n, int rounds, int class_count, const double* angles,
+                                   const uint16_t* perms, uint32_t perm_mask, uint32_t flags,
+                                   const hygt_plan_options* opts, hygt_plan** out) {
   if (!out) return fail(HYGT_ERR_ARGUMENT, "hygt_plan_create: null out");
   *out = nullptr;
+  hygt_plan_options opt;
+  if (int s = resolve_options(opts, opt)) return s;
   if (log2_n < 1 || log2_n > 16) return fail(HYGT_ERR_ARGUMENT, "HyGTModel: log2_n out of range [1, 16]");
   if (log2_n > 8) return fail(HYGT_ERR_ARGUMENT, "hygt_plan_create: GPU path supports log2_n <= 8");
   if (rounds < 1) return fail(HYGT_ERR_ARGUMENT, "num_parameters: log2_n and rounds must be >= 1");
@@ -1195,6 +1187,7 @@ extern "C" int hygt_plan_create(int log2_n, int rounds, int class_count, const d
   hygt_plan* p = new (std::nothrow) hygt_plan();
   if (!p) return fail(HYGT_ERR_CUDA, "out of host memory");
   p->kind = 0;
+  p->opt = opt;
   p->log2n = log2_n;
   p->rounds = rounds;
   p->classes = class_count;
@@ -1247,7 +1240,8 @@ extern "C" int hygt_plan_create(int log2_n, int rounds, int class_count, const d
   // or its seconds of compilation at plan creation; HYGT_JIT=2 forces the JIT path anyway.
   const bool stage_first = select_stage(log2_n, standard, true) && env_int("HYGT_STAGE", 1) != 0 &&
                            class_count <= STAGE_MAX_CLASSES && env_int("HYGT_JIT", 1) != 2;
-  if (!stage_first && jit_supported(log2_n, class_count, rounds) && env_int("HYGT_JIT", 1) != 0) {
+  if (!stage_first && opt.allow_nvrtc && opt.kernel != HYGT_KERNEL_TENSOR &&
+      jit_supported(log2_n, class_count, rounds) && env_int("HYGT_JIT", 1) != 0) {
     std::string err;
     if (jit_build(log2_n, rounds, class_count, angles, perms, p->perm_mask, p->algo == 0, p->jit, err)) {
       jit_release(p->jit);  // stay on the precompiled kernels
@@ -1258,6 +1252,14 @@ extern "C" int hygt_plan_create(int log2_n, int rounds, int class_count, const d
     }
     // class runs long enough that a CTA range stays inside one or two class bodies
     if (p->jit.ok) p->chunk_rows = chunk_env >= 0 ? (uint64_t)chunk_env : ((uint64_t)1 << 18);
+  }
+  if (opt.kernel == HYGT_KERNEL_TENSOR) {  // every call runs on the composed-operator path
+    if (int s = setup_gemm(p, angles, perms)) {
+      free_plan(p);
+      return s;
+    }
+    *out = p;
+    return ok();
   }
   if (int s = setup_tile(p, angles, perms)) {
     free_plan(p);
@@ -1729,8 +1731,18 @@ extern "C" int hygt_fixed_plan_create(int log2_n, int rounds, int class_count, i
                                       int precision_bits, const uint16_t* codes,
                                       const uint16_t* perms, uint32_t perm_mask,
                                       hygt_plan** out) {
+  return hygt_fixed_plan_create_ex(log2_n, rounds, class_count, angle_bits, precision_bits, codes, perms,
+                                   perm_mask, nullptr, out);
+}
+
+extern "C" int hygt_fixed_plan_create_ex(int log2_n, int rounds, int class_count, int angle_bits,
+                                         int precision_bits, const uint16_t* codes,
+                                         const uint16_t* perms, uint32_t perm_mask,
+                                         const hygt_plan_options* opts, hygt_plan** out) {
   if (!out) return fail(HYGT_ERR_ARGUMENT, "hygt_fixed_plan_create: null out");
   *out = nullptr;
+  hygt_plan_options opt;
+  if (int s = resolve_options(opts, opt)) return s;
   if (log2_n < 1 || log2_n > 16) return fail(HYGT_ERR_ARGUMENT, "QuantizedHyGTModel: log2_n out of range [1, 16]");
   if (log2_n > 8) return fail(HYGT_ERR_ARGUMENT, "hygt_fixed_plan_create: GPU path supports log2_n <= 8");
   if (angle_bits < 1 || angle_bits > 12)
@@ -1751,6 +1763,7 @@ extern "C" int hygt_fixed_plan_create(int log2_n, int rounds, int class_count, i
   hygt_plan* p = new (std::nothrow) hygt_plan();
   if (!p) return fail(HYGT_ERR_CUDA, "out of host memory");
   p->kind = 1;
+  p->opt = opt;
   p->log2n = log2_n;
   p->rounds = rounds;
   p->classes = class_count;
@@ -1879,7 +1892,8 @@ extern "C" int hygt_fixed_plan_create(int log2_n, int rounds, int class_count, i
     free_plan(p);
     return s;
   }
-  if (!s && int32_ok && jit_fixed_supported(log2_n, rounds, class_count) && env_int("HYGT_FIXED_JIT", 1) != 0) {
+  if (!s && int32_ok && opt.allow_nvrtc && jit_fixed_supported(log2_n, rounds, class_count) &&
+      env_int("HYGT_FIXED_JIT", 1) != 0) {
     std::string err;
     if (jit_fixed_build(log2_n, rounds, class_count, angle_bits, precision_bits, codes, ct.data(), sn.data(),
                         perms, p->perm_mask, p->fx_jit, err))

@@ -25,7 +25,7 @@ constexpr int SEG2_VPT = 2;
 ApplyFn select_apply(int log2n, int l, bool standard, bool fwd, bool energy);
 TileFn select_tile(int log2n, int l, int vpt, bool standard, bool fwd, bool energy);
 SegFn select_seg(int variant, bool standard, bool fwd, bool energy);
-StageFn select_stage(int log2n, bool standard, bool fwd, bool benes = false, bool debug = false);
+StageFn select_stage(int log2n, bool standard, bool fwd, bool debug = false);
 StageSortFn select_stage_sort(int vpt, uint32_t tile_rows);
 constexpr int STAGE_FX_VPT = 2;
 constexpr int STAGE_FX_WARPS = 7;

@@ -10,11 +10,9 @@ static StageFn stage_variant(bool standard, bool fwd) {
   return fwd ? hygt_stage_kernel<4, V, false, true, W, VAR> : hygt_stage_kernel<4, V, false, false, W, VAR>;
 }
 
-StageFn select_stage(int log2n, bool standard, bool fwd, bool benes, bool debug) {
+StageFn select_stage(int log2n, bool standard, bool fwd, bool debug) {
   if (log2n != 4) return nullptr;
-  if (debug) return benes ? stage_variant<STAGE_VAR_BENES | STAGE_VAR_DEBUG>(standard, fwd)
-                         : stage_variant<STAGE_VAR_DEBUG>(standard, fwd);
-  return benes ? stage_variant<STAGE_VAR_BENES>(standard, fwd) : stage_variant<0>(standard, fwd);
+  return debug ? stage_variant<STAGE_VAR_DEBUG>(standard, fwd) : stage_variant<0>(standard, fwd);
 }
 
 StageSortFn select_stage_sort(int vpt, uint32_t tile_rows) {

@@ -827,10 +827,6 @@ int gemm_build(int n, int classes, const double* ops, GemmOperands& out) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&out.num_sms, cudaDevAttrMultiProcessorCount, dev);
   if (out.num_sms <= 0) out.num_sms = 148;
-  const char* pe = std::getenv("HYGT_GEMM_PAIR");
-  out.pair = !(pe && pe[0] == '0');
-  const char* we = std::getenv("HYGT_GEMM_WIDE");
-  out.wide = we && we[0] == '1';  // measured slower at N = 256 (serialised epilogue)
   return HYGT_OK;
 }
 

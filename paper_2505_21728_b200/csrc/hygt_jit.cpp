@@ -13,6 +13,7 @@
 // Reference arithmetic: butterflies and order as transform.hpp:45-66 / model.hpp:77-79, gathers
 // as transform.hpp:75-80 (inverse: scatter first, :88-93); coefficients from hygt_plan.cpp.
 #include "hygt_jit.h"
+#include "hygt_knobs.h"
 
 #include <nvrtc.h>
 
@@ -33,15 +34,8 @@ namespace hygt_gpu {
 
 namespace {
 
-bool env_on(const char* name) {
-  const char* v = std::getenv(name);
-  return v && std::atoi(v) != 0;
-}
-
-bool env_off(const char* name) {
-  const char* v = std::getenv(name);
-  return v && std::atoi(v) == 0;
-}
+bool env_on(const char* name) { return knob(name, 0) != 0; }    // development knob set and non-zero
+bool env_off(const char* name) { return knob(name, 1) == 0; }   // development knob set to 0
 
 std::string lit(float f) {
   uint32_t u;
@@ -197,8 +191,7 @@ std::string generate(int log2n, int classes, int warps, int minb, bool standard,
                      const std::vector<ClassProgram>& progs) {
   const int n = 1 << log2n;
   std::ostringstream o;
-  const char* ld = std::getenv("HYGT_JIT_LOAD");
-  o << "#define LOADX " << (ld ? ld : "__ldg") << "\n";
+  o << "#define LOADX __ldg\n";
   o << "#define N " << n << "\n#define NQ " << n / 4 << "\n#define WARPS " << warps
     << "\n#define MINB " << minb << "\n#define SWZ " << kSwizzle[log2n - 2] << "\n";
   o << kPrologue;
@@ -365,90 +358,6 @@ const char* kClsEpiloguePTX = R"CUDA(
 )CUDA";
 
 
-// Double-buffered variant: the next batch's rows are copied into the second slot area while
-// this batch computes (HYGT_CLS_DB=1).
-const char* kClsPrologueDB = R"CUDA(
-typedef unsigned int u32;
-typedef unsigned long long u64;
-#define RS (NQ + 1)
-extern "C" __global__ void __launch_bounds__(32, MINB)
-KNAME(const float* __restrict__ x, float* __restrict__ y, const u32* __restrict__ idx,
-      const u32* __restrict__ seg_end, u32 bin, u32 copy_bin) {
-  __shared__ __align__(16) float4 slot[2][32 * RS];
-  __shared__ u32 s_row[2][32];
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const int lane = threadIdx.x;
-  const u64 beg = bin ? __ldg(seg_end + bin - 1) : 0u;
-  const u64 end = __ldg(seg_end + bin);
-  const u64 nb = (end - beg + 31) / 32;
-  auto row_id = [&](u64 b) -> u32 {
-    const u64 p = beg + b * 32 + lane;
-    return b < nb && p < end ? __ldg(idx + p) : 0xffffffffu;
-  };
-  auto issue = [&](int buf, u32 id) {
-    __syncwarp();
-    s_row[buf][lane] = id;
-    __syncwarp();
-    const u32 ss = (u32)__cvta_generic_to_shared(slot[buf]);
-#pragma unroll
-    for (int i0 = 0; i0 < 32; i0 += 32 / NQ) {
-      const int i = i0 + lane / NQ, q = lane % NQ;
-      const u32 row = s_row[buf][i];
-      if (row != 0xffffffffu)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ss + (u32)(i * RS + q) * 16u),
-                     "l"(x + (size_t)row * N + q * 4) : "memory");
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  u64 b = blockIdx.x;
-  if (b < nb) issue(0, row_id(b));
-  u32 id_next = row_id(b + gridDim.x);
-  int cur = 0;
-  for (; b < nb; b += gridDim.x, cur ^= 1) {
-    const bool more = b + gridDim.x < nb;
-    if (more) {
-      issue(cur ^ 1, id_next);
-      id_next = row_id(b + 2 * (u64)gridDim.x);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
-    __syncwarp();
-    float4* sl = slot[cur];
-    const u32* sr = s_row[cur];
-    float v[N];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      const float4 a = sl[lane * RS + q];
-      v[4 * q] = a.x; v[4 * q + 1] = a.y; v[4 * q + 2] = a.z; v[4 * q + 3] = a.w;
-    }
-    {
-)CUDA";
-
-const char* kClsEpilogueDB = R"CUDA(
-    }
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) sl[lane * RS + q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-    __syncwarp();
-#pragma unroll
-    for (int i0 = 0; i0 < 32; i0 += 32 / NQ) {
-      const int i = i0 + lane / NQ, q = lane % NQ;
-      const u32 row = sr[i];
-      if (row != 0xffffffffu) __stcs((float4*)(y + (size_t)row * N) + q, sl[i * RS + q]);
-    }
-  }
-  if (copy_bin) {  // rows with invalid class ids pass through (hygt_bucket flags them)
-    const u64 e2 = __ldg(seg_end + bin + 1);
-    for (u64 p = end + (u64)blockIdx.x * (32 / NQ) + lane / NQ; p < e2; p += (u64)gridDim.x * (32 / NQ)) {
-      const u32 row = __ldg(idx + p);
-      ((float4*)(y + (size_t)row * N))[lane % NQ] = ((const float4*)(x + (size_t)row * N))[lane % NQ];
-    }
-  }
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-}
-#undef KNAME
-)CUDA";
-
 // Source of one class's two kernels (hygt_cls_f, hygt_cls_i).
 void emit_body_ptx(std::ostringstream& o, const ClassProgram& pr, int n, bool standard);
 
@@ -460,19 +369,18 @@ std::string generate_class(int log2n, int minb, bool standard, const ClassProgra
   o << "#define N " << n << "\n#define NQ " << n / 4 << "\n#define MINB " << minb << "\n";
   // next-batch L2 prefetch, measured per row length (profiles/r01/cls_experiments.log): the bulk
   // prefetch (a uniform loop of UBLKPF) pays off for 256 B rows, per-lane line prefetches for 128 B
-  o << "#define PFMODE " << (std::getenv("HYGT_CLS_PF") ? std::atoi(std::getenv("HYGT_CLS_PF")) : n >= 64 ? 1 : 2) << "\n";
-  const bool dbuf = env_on("HYGT_CLS_DB");
+  o << "#define PFMODE " << knob("HYGT_CLS_PF", n >= 64 ? 1 : 2) << "\n";
   // PTX bodies (HYGT_CLS_PTX=1) skip the NVVM pass: 0.7 s instead of 2.5 s per class, but the
   // N = 64 kernels run 15% slower than NVVM's (profiles/r01/cls_experiments.log), so opt-in
-  const bool ptx = !dbuf && (ptx_mode >= 0 ? ptx_mode == 1 : env_on("HYGT_CLS_PTX"));
+  const bool ptx = ptx_mode >= 0 ? ptx_mode == 1 : env_on("HYGT_CLS_PTX");
   for (int d = 0; d < 2; ++d) {
     o << "#define KNAME " << (d == 0 ? "hygt_cls_f" : "hygt_cls_i") << "\n"
-      << (dbuf ? kClsPrologueDB : ptx ? kClsProloguePTX : kClsPrologue);
+      << (ptx ? kClsProloguePTX : kClsPrologue);
     if (ptx)
       emit_body_ptx(o, d == 0 ? fwd : inv, n, standard);
     else
       emit_body(o, d == 0 ? fwd : inv, n, standard);
-    o << (dbuf ? kClsEpilogueDB : ptx ? kClsEpiloguePTX : kClsEpilogue);
+    o << (ptx ? kClsEpiloguePTX : kClsEpilogue);
   }
   return o.str();
 }
@@ -633,90 +541,6 @@ void emit_fixed_body(std::ostringstream& o, const std::vector<FxOp>& ops, const 
   o << "\n";
 }
 
-// ---- per-class kernels for N = 256 (plan path "clsjit", config 5) ---------------------------
-// A row is split over a warp pair: each thread of warp w holds the 128 samples whose bit `wb`
-// equals w, so the passes on the other 7 bits are in-register FFMAs with immediates. A pass on bit
-// wb first exchanges half of each thread's samples with the partner warp through shared memory
-// (a "swap": wb moves to the bit whose next use lies furthest ahead, so R rounds cost ~R swaps),
-// gathers are a full exchange. The two warps run different straight-line code (their halves'
-// coefficients) and meet at __syncthreads() for every exchange. Forward-with-energy kernels add
-// y^2 per sample: a shuffle reduce-scatter over the 32 rows of a batch leaves 4 sample sums per
-// lane, accumulated in fp64 and added to energy[c][*] once per CTA.
-const char* k256Prologue = R"CUDA(
-typedef unsigned int u32;
-typedef unsigned long long u64;
-#define N 256
-#define RS 65
-extern "C" __global__ void __launch_bounds__(64, MINB)
-KNAME(const float* __restrict__ x, float* __restrict__ y, const u32* __restrict__ idx,
-      const u32* __restrict__ seg_end, u32 bin, u32 copy_bin, double* __restrict__ energy) {
-  __shared__ __align__(16) float4 slot[32 * RS];
-  __shared__ u32 s_row[32];
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const int tid = threadIdx.x, lane = tid & 31, wpos = tid >> 5;
-  const u64 beg = bin ? __ldg(seg_end + bin - 1) : 0u;
-  const u64 end = __ldg(seg_end + bin);
-  const u64 nb = (end - beg + 31) / 32;
-  const u32 sb = (u32)__cvta_generic_to_shared(slot);
-  const u32 sbl = sb + lane * 4u;
-  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-  for (u64 b = blockIdx.x; b < nb; b += gridDim.x) {
-    __syncthreads();
-    if (tid < 32) {
-      const u64 p = beg + b * 32 + lane;
-      s_row[lane] = p < end ? __ldg(idx + p) : 0xffffffffu;
-    }
-    __syncthreads();
-#pragma unroll 8
-    for (int i = 0; i < 32; ++i) {
-      const u32 row = s_row[i];
-      if (row != 0xffffffffu)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + (u32)(i * RS + tid) * 16u),
-                     "l"(x + (size_t)row * N + tid * 4) : "memory");
-    }
-    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-    __syncthreads();
-    float en0, en1, en2, en3;
-    const u32 rb = sb + (u32)lane * (RS * 16u);  // row `lane`'s slot
-    const u32 valid = s_row[lane] != 0xffffffffu ? 1u : 0u;
-    if (wpos == 0) {
-)CUDA";
-
-const char* k256Epilogue = R"CUDA(
-    }
-    acc0 += en0; acc1 += en1; acc2 += en2; acc3 += en3;
-    __syncthreads();
-#pragma unroll 8
-    for (int i = 0; i < 32; ++i) {
-      const u32 row = s_row[i];
-      if (row != 0xffffffffu) __stcs((float4*)(y + (size_t)row * N) + tid, slot[i * RS + tid]);
-    }
-  }
-  if (ENERGY && energy) {  // lane's 4 sums: final-layout slots base(lane) + k, see the generator
-    const u32 base = ((lane >> 4) & 1) * 64 + ((lane >> 3) & 1) * 32 + ((lane >> 2) & 1) * 16 +
-                     ((lane >> 1) & 1) * 8 + (lane & 1) * 4;
-    const double a4[4] = {acc0, acc1, acc2, acc3};
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const u32 j = base + k;
-      const u32 e = ((j >> FINALWB) << (FINALWB + 1)) | ((u32)wpos << FINALWB) | (j & ((1u << FINALWB) - 1));
-      atomicAdd(energy + (size_t)bin * N + e, a4[k]);
-    }
-  }
-  if (copy_bin) {  // rows with invalid class ids pass through (hygt_bucket flags them)
-    const u64 e2 = __ldg(seg_end + bin + 1);
-    for (u64 p = end + blockIdx.x; p < e2; p += gridDim.x) {
-      const u32 row = __ldg(idx + p);
-      ((float4*)(y + (size_t)row * N))[tid] = ((const float4*)(x + (size_t)row * N))[tid];
-    }
-  }
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-}
-#undef KNAME
-#undef ENERGY
-#undef FINALWB
-)CUDA";
-
 std::string hexf(float f) {
   uint32_t u;
   std::memcpy(&u, &f, 4);
@@ -777,187 +601,6 @@ void emit_body_ptx(std::ostringstream& o, const ClassProgram& pr, int n, bool st
   o << "\"}\" :: \"r\"(rb) : \"memory\");\n";
 }
 
-// Emits both warps' bodies for one class and direction as PTX (one inline-asm block per warp, so
-// the C++ front end never sees the 8192-FFMA straight-line code; ptxas compiles it directly).
-// Operands: %0..%3 = energy sums out, %4 = shared address of row `lane`'s slot, %5 = shared
-// exchange base + lane * 4. Returns the final wb.
-int emit_256(std::ostringstream& o, const ClassProgram& pr, bool energy) {
-  const int n = 256;
-  auto bit = [](int e, int b) { return (e >> b) & 1; };
-  std::ostringstream path[2];
-  int nreg[2] = {0, 0};
-  std::vector<int> cur[2];  // element -> %hv register (held elements only), -1 if not held
-  auto R = [](int r) { return "%%hv" + std::to_string(r); };
-  for (int w = 0; w < 2; ++w) {
-    cur[w].assign(n, -1);
-    for (int q = 0; q < 32; ++q) {  // samples 128w + 4q .. +3 of row `lane` (the wb = 7 layout)
-      const int e = (w << 7) + 4 * q;
-      path[w] << "ld.shared.v4.f32 {" << R(nreg[w]) << "," << R(nreg[w] + 1) << "," << R(nreg[w] + 2) << ","
-              << R(nreg[w] + 3) << "}, [%4+" << e * 4 << "];\n";
-      for (int t = 0; t < 4; ++t) cur[w][e + t] = nreg[w]++;
-    }
-    path[w] << "bar.sync 0;\n";  // both halves read before the slot area becomes the exchange buffer
-  }
-  int wb = 7, xset = 0;
-  auto op_bit = [&](size_t i) -> int {
-    const ProgOp& op = pr.ops[i];
-    if (op.kind != 0) return -1;
-    return __builtin_ctz((unsigned)(op.m ^ op.n));
-  };
-  auto next_use = [&](size_t from, int b) -> size_t {  // index of the next butterfly on bit b
-    for (size_t i = from; i < pr.ops.size(); ++i) {
-      if (pr.ops[i].kind == 1) return pr.ops.size() + 1;  // a gather re-lays everything anyway
-      if (op_bit(i) == b) return i;
-    }
-    return pr.ops.size() + 2;
-  };
-  auto pick = [&](size_t from, int avoid) {  // the bit whose next use is furthest ahead
-    int best = -1;
-    size_t far = 0;
-    for (int b = 0; b < 8; ++b) {
-      if (b == avoid) continue;
-      const size_t u = next_use(from, b);
-      if (best < 0 || u > far) { best = b; far = u; }
-    }
-    return best;
-  };
-  auto barrier = [&]() {
-    for (int w = 0; w < 2; ++w) path[w] << "bar.sync 0;\n";
-  };
-  auto swap_to = [&](int nb) {  // half exchange: wb -> nb
-    const uint32_t base = (uint32_t)xset * 16384u;
-    xset ^= 1;
-    for (int w = 0; w < 2; ++w) {
-      int kk = 0;
-      for (int e = 0; e < n; ++e)
-        if (bit(e, wb) == w && bit(e, nb) != w)
-          path[w] << "st.shared.f32 [%5+" << base + (uint32_t)w * 8192u + (uint32_t)kk++ * 128u << "], " << R(cur[w][e]) << ";\n";
-    }
-    barrier();
-    for (int w = 0; w < 2; ++w) {
-      std::vector<int> nxt(n, -1);
-      int kk = 0;
-      for (int e = 0; e < n; ++e) {
-        if (bit(e, wb) == (1 - w) && bit(e, nb) == w) {  // partner's outgoing, in the partner's order
-          path[w] << "ld.shared.f32 " << R(nreg[w]) << ", [%5+" << base + (uint32_t)(1 - w) * 8192u + (uint32_t)kk++ * 128u << "];\n";
-          nxt[e] = nreg[w]++;
-        } else if (bit(e, wb) == w && bit(e, nb) == w) {
-          nxt[e] = cur[w][e];
-        }
-      }
-      cur[w].swap(nxt);
-    }
-    wb = nb;
-  };
-  for (size_t i = 0; i < pr.ops.size(); ++i) {
-    const ProgOp& op = pr.ops[i];
-    if (op.kind == 0) {
-      const int p = op_bit(i);
-      if (p == wb) swap_to(pick(i, wb));
-      const int w = bit(op.m, wb);
-      const int ra = cur[w][op.m], rbb = cur[w][op.n], ym = nreg[w]++, yn = nreg[w]++;
-      path[w] << "fma.rn.f32 " << R(ym) << ", " << R(rbb) << ", " << hexf(op.a) << ", " << R(ra) << ";\n"
-              << "fma.rn.f32 " << R(yn) << ", " << R(ra) << ", " << hexf(op.b) << ", " << R(rbb) << ";\n";
-      cur[w][op.m] = ym;
-      cur[w][op.n] = yn;
-    } else if (op.kind == 1) {  // full exchange through [element][lane]
-      const auto& g = pr.gathers[op.arg];
-      barrier();  // the last swap's reads are done
-      for (int w = 0; w < 2; ++w)
-        for (int e = 0; e < n; ++e)
-          if (cur[w][e] >= 0) path[w] << "st.shared.f32 [%5+" << e * 128 << "], " << R(cur[w][e]) << ";\n";
-      barrier();
-      const int nb = pick(i + 1, -1);
-      for (int w = 0; w < 2; ++w) {
-        std::vector<int> nxt(n, -1);
-        for (int e = 0; e < n; ++e)
-          if (bit(e, nb) == w) {
-            path[w] << "ld.shared.f32 " << R(nreg[w]) << ", [%5+" << g[e] * 128 << "];\n";
-            nxt[e] = nreg[w]++;
-          }
-        cur[w].swap(nxt);
-      }
-      wb = nb;
-      barrier();  // everyone has read before the buffer is written again
-      xset = 0;
-    } else {
-      for (int w = 0; w < 2; ++w)
-        for (int e = 0; e < n; ++e)
-          if (cur[w][e] >= 0) {
-            path[w] << "mul.rn.f32 " << R(nreg[w]) << ", " << R(cur[w][e]) << ", " << hexf(pr.scales[e]) << ";\n";
-            cur[w][e] = nreg[w]++;
-          }
-    }
-  }
-  for (int w = 0; w < 2; ++w) {
-    if (energy) {  // reduce-scatter of y^2 over the 32 lanes (rows): 4 sums per lane
-      std::vector<int> sq;
-      path[w] << "setp.ne.u32 %%hq4, %6, 0;\n";  // lanes past the class run contribute nothing
-      for (int e = 0; e < n; ++e)
-        if (cur[w][e] >= 0) {
-          path[w] << "mul.rn.f32 " << R(nreg[w]) << ", " << R(cur[w][e]) << ", " << R(cur[w][e]) << ";\n"
-                  << "selp.f32 " << R(nreg[w] + 1) << ", " << R(nreg[w]) << ", 0f00000000, %%hq4;\n";
-          sq.push_back(nreg[w] + 1);
-          nreg[w] += 2;
-        }
-      path[w] << "mov.u32 %%hl0, %%laneid;\n";
-      int pi = 0;
-      for (int off = 16; off >= 1; off >>= 1, ++pi) {
-        path[w] << "and.b32 %%hl1, %%hl0, " << off << ";\nsetp.ne.u32 %%hq" << pi << ", %%hl1, 0;\n";
-        const size_t h = sq.size() / 2;
-        std::vector<int> nx(h);
-        for (size_t q = 0; q < h; ++q) {
-          const int sv = nreg[w]++, rv = nreg[w]++, kv = nreg[w]++, t = nreg[w]++;
-          path[w] << "selp.f32 " << R(sv) << ", " << R(sq[q]) << ", " << R(sq[q + h]) << ", %%hq" << pi << ";\n"
-                  << "shfl.sync.bfly.b32 " << R(rv) << ", " << R(sv) << ", " << off << ", 31, -1;\n"
-                  << "selp.f32 " << R(kv) << ", " << R(sq[q + h]) << ", " << R(sq[q]) << ", %%hq" << pi << ";\n"
-                  << "add.rn.f32 " << R(t) << ", " << R(kv) << ", " << R(rv) << ";\n";
-          nx[q] = t;
-        }
-        sq.swap(nx);
-      }
-      for (int q = 0; q < 4; ++q) path[w] << "mov.f32 %" << q << ", " << R(sq[q]) << ";\n";
-    } else {
-      for (int q = 0; q < 4; ++q) path[w] << "mov.f32 %" << q << ", 0f00000000;\n";
-    }
-  }
-  // outputs -> row `lane`'s slot: the held samples form runs of 2^wb consecutive samples
-  barrier();
-  for (int w = 0; w < 2; ++w) {
-    const int run = wb >= 2 ? 4 : (1 << wb);
-    for (int e = 0; e < n; e += run) {
-      if (cur[w][e] < 0) continue;
-      if (run == 4)
-        path[w] << "st.shared.v4.f32 [%4+" << e * 4 << "], {" << R(cur[w][e]) << "," << R(cur[w][e + 1]) << ","
-                << R(cur[w][e + 2]) << "," << R(cur[w][e + 3]) << "};\n";
-      else
-        for (int q = 0; q < run; ++q) path[w] << "st.shared.f32 [%4+" << (e + q) * 4 << "], " << R(cur[w][e + q]) << ";\n";
-    }
-  }
-  for (int w = 0; w < 2; ++w) {
-    if (w == 1) o << "} else {\n";
-    o << "asm volatile(\"{\\n\"\n\".reg .f32 %%hv<" << nreg[w] << ">;\\n.reg .pred %%hq<5>;\\n.reg .b32 %%hl<2>;\\n\"\n";
-    std::istringstream lines(path[w].str());
-    std::string ln;
-    while (std::getline(lines, ln)) o << "\"" << ln << "\\n\"\n";
-    o << "\"}\" : \"=f\"(en0), \"=f\"(en1), \"=f\"(en2), \"=f\"(en3) : \"r\"(rb), \"r\"(sbl), \"r\"(valid) : \"memory\");\n";
-  }
-  return wb;
-}
-
-std::string generate_class_256(bool standard, const ClassProgram& fwd, const ClassProgram& inv) {
-  (void)standard;
-  std::ostringstream o;
-  o << "#define MINB 6\n";
-  for (int d = 0; d < 3; ++d) {  // forward, forward with energy, inverse
-    std::ostringstream body;
-    const int wb = emit_256(body, d == 2 ? inv : fwd, d == 1);
-    o << "#define KNAME " << (d == 0 ? "hygt_cls_f" : d == 1 ? "hygt_cls_fe" : "hygt_cls_i") << "\n#define ENERGY "
-      << (d == 1 ? 1 : 0) << "\n#define FINALWB " << wb << "\n" << k256Prologue << body.str() << k256Epilogue;
-  }
-  return o.str();
-}
-
 std::mutex g_cache_mu;
 std::unordered_map<std::string, std::vector<char>> g_cubin_cache;  // source -> cubin
 
@@ -973,10 +616,9 @@ int compile(const std::string& src, std::vector<char>& cubin, std::string& log) 
   nvrtcProgram prog;
   if (nvrtcCreateProgram(&prog, src.c_str(), "hygt_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
     return 1;
-  std::vector<const char*> opts = {(std::getenv("HYGT_JIT_ARCH") ? std::getenv("HYGT_JIT_ARCH") : "--gpu-architecture=sm_100a"), "-default-device", "-lineinfo",
-                                   "--std=c++17", "-DNDEBUG"};
-  if (const char* e = std::getenv("HYGT_JIT_OPTS")) opts.push_back(e);
-  const nvrtcResult r = nvrtcCompileProgram(prog, (int)opts.size(), opts.data());
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-default-device", "-lineinfo", "--std=c++17",
+                        "-DNDEBUG"};
+  const nvrtcResult r = nvrtcCompileProgram(prog, (int)(sizeof(opts) / sizeof(opts[0])), opts);
   size_t ls = 0;
   nvrtcGetProgramLogSize(prog, &ls);
   log.resize(ls);
@@ -986,19 +628,10 @@ int compile(const std::string& src, std::vector<char>& cubin, std::string& log) 
     return 1;
   }
   size_t cs = 0;
-  if (std::getenv("HYGT_JIT_ARCH")) nvrtcGetPTXSize(prog, &cs); else
   nvrtcGetCUBINSize(prog, &cs);
   cubin.resize(cs);
   nvrtcGetCUBIN(prog, cubin.data());
   nvrtcDestroyProgram(&prog);
-  if (const char* dump = std::getenv("HYGT_JIT_DUMP")) {  // development aid: keep the cubin
-    static int seq = 0;
-    const std::string path = std::string(dump) + "." + std::to_string(seq++) + ".cubin";
-    if (FILE* f = std::fopen(path.c_str(), "wb")) {
-      std::fwrite(cubin.data(), 1, cubin.size(), f);
-      std::fclose(f);
-    }
-  }
   std::lock_guard<std::mutex> lk(g_cache_mu);
   if (g_cubin_cache.size() >= 512) g_cubin_cache.clear();  // bound the process's cache (~0.5 MB per class)
   g_cubin_cache.emplace(src, cubin);
@@ -1149,13 +782,6 @@ int load_class_modules(const std::vector<std::string>& srcs, JitClsKernels& out,
       err = "jit: cannot load the compiled module";
       return 5;
     }
-    if (out.threads == 64) {
-      out.fn_e.resize(classes, nullptr);
-      if (cudaLibraryGetKernel(&out.fn_e[c], out.lib[c], "hygt_cls_fe") != cudaSuccess) {
-        err = "jit: cannot load the energy kernel";
-        return 5;
-      }
-    }
   }
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)out.fn[0][0], out.threads, 0) != cudaSuccess || occ < 1)
@@ -1173,36 +799,18 @@ int load_class_modules(const std::vector<std::string>& srcs, JitClsKernels& out,
 
 // One NVRTC module per class: plans with very many classes would spend minutes compiling, so the
 // per-class chains are limited to HYGT_CLS_JIT_MAX_CLASSES (default 64) classes.
-int max_jit_classes() {
-  const char* v = std::getenv("HYGT_CLS_JIT_MAX_CLASSES");
-  return v && *v ? std::atoi(v) : 64;
-}
+int max_jit_classes() { return knob("HYGT_CLS_JIT_MAX_CLASSES", 64); }
 
 bool jit_cls_supported(int log2n, int classes, int rounds) {
   if (classes > max_jit_classes()) return false;
   // N = 16 rows (64 B) are half a 128 B line: gathered per class they cost twice the staged
   // kernel's time (profiles/r01/cls_experiments.log), so N = 16 is opt-in (experiments only).
-  // N = 256: correct, but 131 KB of straight-line code per class and direction thrashes the
-  // instruction cache (26% of the roofline vs the segment kernel's 36%, DESIGN 5.7): opt-in only.
-  if (log2n == 8) return classes >= 2 && rounds >= 1 && rounds <= 8 && env_on("HYGT_CLS_JIT256");
   return log2n >= 4 && log2n <= 6 && classes >= 2 && rounds >= 1 && rounds <= 8 &&
          (log2n >= 5 || env_on("HYGT_CLS_JIT_SHORT"));
 }
 
 int jit_cls_build(int log2n, int rounds, int classes, const double* angles, const uint16_t* perms,
                   uint32_t mask, bool standard, JitClsKernels& out, std::string& err) {
-  if (log2n == 8) {  // warp-pair kernels (config 5)
-    std::vector<ClassProgram> progs[2];
-    for (int d = 0; d < 2; ++d)
-      if (!build_programs(log2n, rounds, classes, angles, perms, mask, d == 0, standard, progs[d])) {
-        err = "jit: scale-folded program unsafe";
-        return 3;
-      }
-    std::vector<std::string> srcs(classes);
-    for (int c = 0; c < classes; ++c) srcs[c] = generate_class_256(standard, progs[0][c], progs[1][c]);
-    out.threads = 64;
-    return load_class_modules(srcs, out, err);
-  }
   std::vector<ClassProgram> progs[2];
   for (int d = 0; d < 2; ++d)
     if (!build_programs(log2n, rounds, classes, angles, perms, mask, d == 0, standard, progs[d])) {
@@ -1210,7 +818,7 @@ int jit_cls_build(int log2n, int rounds, int classes, const double* angles, cons
       return 3;
     }
   std::vector<std::string> srcs(classes);
-  for (int c = 0; c < classes; ++c) srcs[c] = generate_class(log2n, std::getenv("HYGT_CLS_MINB") ? std::atoi(std::getenv("HYGT_CLS_MINB")) : 16, standard, progs[0][c], progs[1][c]);
+  for (int c = 0; c < classes; ++c) srcs[c] = generate_class(log2n, knob("HYGT_CLS_MINB", 16), standard, progs[0][c], progs[1][c]);
   return load_class_modules(srcs, out, err);
 }
 
@@ -1221,10 +829,10 @@ void jit_cls_release(JitClsKernels& k) {
 }
 
 int jit_cls_launch(const JitClsKernels& k, int dir, const float* x, float* y, const uint32_t* idx,
-                   const uint32_t* seg_end, int classes, cudaStream_t st, double* energy) {
+                   const uint32_t* seg_end, int classes, cudaStream_t st) {
   for (int c = 0; c < classes; ++c) {
     uint32_t bin = (uint32_t)c, copy_bin = c == classes - 1 ? 1u : 0u;
-    void* args[] = {(void*)&x, (void*)&y, (void*)&idx, (void*)&seg_end, (void*)&bin, (void*)&copy_bin, (void*)&energy};
+    void* args[] = {(void*)&x, (void*)&y, (void*)&idx, (void*)&seg_end, (void*)&bin, (void*)&copy_bin};
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(k.grid);
     cfg.blockDim = dim3(k.threads);
@@ -1234,7 +842,7 @@ int jit_cls_launch(const JitClsKernels& k, int dir, const float* x, float* y, co
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = c > 0 ? 1 : 0;  // the first grid follows the bucketing normally
-    const cudaKernel_t fn = energy && dir == 0 && !k.fn_e.empty() ? k.fn_e[c] : k.fn[dir][c];
+    const cudaKernel_t fn = k.fn[dir][c];
     if (cudaLaunchKernelExC(&cfg, (const void*)fn, args) != cudaSuccess) return 5;
   }
   return 0;
@@ -1254,7 +862,7 @@ int jit_fixed_build(int log2n, int rounds, int classes, int angle_bits, int prec
   std::vector<std::string> srcs(classes);
   for (int c = 0; c < classes; ++c) {
     std::ostringstream o;
-    o << "#define PFMODE " << (std::getenv("HYGT_FIXED_PF") ? std::atoi(std::getenv("HYGT_FIXED_PF")) : n >= 64 ? 0 : 2) << "\n";
+    o << "#define PFMODE " << knob("HYGT_FIXED_PF", n >= 64 ? 0 : 2) << "\n";
     o << "#define N " << n << "\n#define NQ " << n / 2 << "\n#define MINB 12\n#define PREC " << precision_bits
       << "\n#define RND " << (1ll << (precision_bits - 1)) << "\n";
     for (int d = 0; d < 2; ++d) {
@@ -1307,11 +915,8 @@ extern "C" int hygt_debug_jit_compile(int kind, int log2n, int rounds, const dou
     std::vector<ClassProgram> progs[2];
     for (int d = 0; d < 2; ++d)
       if (!build_programs(log2n, rounds, 1, angles, perms, mask, d == 0, false, progs[d])) return 3;
-    if (log2n == 8) {
-      src = generate_class_256(false, progs[0][0], progs[1][0]);
-    } else {
-      src = generate_class(log2n, 16, false, progs[0][0], progs[1][0], ptx ? 1 : 0);
-    }
+    if (log2n > 6) return 1;  // per-class kernels: N = 16 / 32 / 64
+    src = generate_class(log2n, 16, false, progs[0][0], progs[1][0], ptx ? 1 : 0);
   } else {
     const int n = 1 << log2n;
     std::vector<int32_t> ct(256), sn(256);

@@ -35,22 +35,21 @@ int jit_launch(const JitKernels& k, int dir, const float* x, float* y, const uin
                const uint32_t* seg_end, uint32_t nseg, uint64_t count, int classes, int num_sms,
                cudaStream_t st);
 
-// Per-class kernels for N = 64 (plan path "clsjit"): one NVRTC module per class holding its
+// Per-class kernels for N = 32 / 64 (plan path "clsjit"): one NVRTC module per class holding its
 // forward and inverse kernels, launched as one programmatic chain over the class buckets.
 struct JitClsKernels {
   bool ok = false;
   std::vector<cudaLibrary_t> lib;
   std::vector<cudaKernel_t> fn[2];
-  std::vector<cudaKernel_t> fn_e;  // forward with fused per-class energy (N = 256 kernels)
   unsigned grid = 0;
-  int threads = 32;  // 64: warp-pair kernels (N = 256)
+  int threads = 32;
 };
 bool jit_cls_supported(int log2n, int classes, int rounds);
 int jit_cls_build(int log2n, int rounds, int classes, const double* angles, const uint16_t* perms,
                   uint32_t mask, bool standard, JitClsKernels& out, std::string& err);
 void jit_cls_release(JitClsKernels& k);
 int jit_cls_launch(const JitClsKernels& k, int dir, const float* x, float* y, const uint32_t* idx,
-                   const uint32_t* seg_end, int classes, cudaStream_t st, double* energy = nullptr);
+                   const uint32_t* seg_end, int classes, cudaStream_t st);
 
 // The same chain for fixed-point plans (int64 rows, bit-exact with forward_fixed/inverse_fixed):
 // per-class kernels with the (c, s) TrigTable pairs as immediates. idx == nullptr: one launch

@@ -249,76 +249,6 @@ bool build_programs(int log2n, int rounds, int classes, const double* angles,
 
 namespace hygt_gpu {
 
-// Beneš routing (the looping algorithm) of a gather out[j] = in[src[j]] on n = 2^k elements into
-// 2k - 1 layers of conditional swaps; layer l exchanges the elements e, e ^ 2^bit(l) whose pair
-// index pair_index(e, bit) is set in masks[l], with bit(l) = k-1, k-2, ..., 0, ..., k-2, k-1.
-namespace {
-void benes_rec(const std::vector<int>& dst /* local input -> local output */, int k, int depth_lo,
-               int nlayers, const std::vector<int>& globl /* local index -> global element */,
-               int bit_shift, std::vector<std::vector<int>>& swaps /* [layer][pair] */) {
-  const int n = 1 << k, h = n / 2;
-  const int b = bit_shift + k - 1;  // global bit of this level's outer layers
-  auto mark = [&](int layer, int local_lo) {
-    const int e = globl[local_lo];
-    swaps[layer][pair_index(e & ~(1 << b), b)] = 1;
-  };
-  if (k == 1) {
-    if (dst[0] == 1) mark(depth_lo, 0);
-    return;
-  }
-  std::vector<int> src(n), sub(n, -1);
-  for (int i = 0; i < n; ++i) src[dst[i]] = i;
-  for (int start = 0; start < n; ++start) {  // 2-colour the cycles: partners in different halves
-    if (sub[start] >= 0) continue;
-    int i = start;
-    int s = 0;
-    while (sub[i] < 0) {
-      sub[i] = s;
-      sub[i ^ h] = 1 - s;
-      const int o = dst[i ^ h];        // partner's output; the output's partner comes via half s
-      i = src[o ^ h];
-    }
-  }
-  std::vector<int> up(h), lo(h);  // sub-permutations (local input -> local output)
-  for (int i = 0; i < h; ++i) {
-    if (sub[i] == 1) mark(depth_lo, i);  // input layer: send i down, i + h up
-    const int a = sub[i] == 0 ? i : i + h, c = sub[i] == 0 ? i + h : i;
-    up[i] = dst[a] & (h - 1);
-    lo[i] = dst[c] & (h - 1);
-  }
-  for (int o = 0; o < h; ++o) {  // output layer: swap if the upper half's element belongs at o + h
-    const int from_up = src[o] < n ? sub[src[o]] == 0 : true;
-    if (!from_up) mark(depth_lo + nlayers - 1, o);
-  }
-  std::vector<int> gu(h), gl(h);
-  for (int i = 0; i < h; ++i) {
-    gu[i] = globl[i];
-    gl[i] = globl[i + h];
-  }
-  benes_rec(up, k - 1, depth_lo + 1, nlayers - 2, gu, bit_shift, swaps);
-  benes_rec(lo, k - 1, depth_lo + 1, nlayers - 2, gl, bit_shift, swaps);
-}
-}  // namespace
-
-bool benes_route(int log2n, const std::vector<int>& src, std::vector<std::vector<int>>& swaps) {
-  const int n = 1 << log2n, layers = 2 * log2n - 1;
-  swaps.assign(layers, std::vector<int>(n / 2, 0));
-  std::vector<int> dst(n), g(n);
-  for (int j = 0; j < n; ++j) dst[src[j]] = j;
-  for (int i = 0; i < n; ++i) g[i] = i;
-  benes_rec(dst, log2n, 0, layers, g, 0, swaps);
-  // verify by simulation
-  std::vector<int> v(n);
-  for (int i = 0; i < n; ++i) v[i] = i;
-  for (int l = 0; l < layers; ++l) {
-    const int b = l < log2n ? log2n - 1 - l : l - log2n + 1;
-    for (int e = 0; e < n; ++e)
-      if (!(e & (1 << b)) && swaps[l][pair_index(e, b)]) std::swap(v[e], v[e | (1 << b)]);
-  }
-  for (int j = 0; j < n; ++j)
-    if (v[j] != src[j]) return false;
-  return true;
-}
 
 void compose_operator(int log2n, int rounds, const double* angles_c, const uint16_t* perms_c,
                       uint32_t mask, double* out) {

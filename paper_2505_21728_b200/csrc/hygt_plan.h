@@ -54,10 +54,6 @@ bool build_direction(const Layout& ly, int rounds, int classes, const double* an
                      const uint16_t* perms, uint32_t mask, bool fwd, bool standard,
                      DirTables& out);
 
-// Beneš network of a gather out[j] = in[src[j]] on 2^log2n elements: swaps[l][pair] for the
-// 2 log2n - 1 layers, layer l on bit (l < log2n ? log2n-1-l : l-log2n+1). Returns false if the
-// routing fails its own simulation check.
-bool benes_route(int log2n, const std::vector<int>& src, std::vector<std::vector<int>>& swaps);
 
 // The class's whole forward transform as one N x N matrix, fp64: column k = forward(e_k) with the
 // reference's pass order and per-butterfly cos/sin (transform.hpp:45-66, the gathers after the

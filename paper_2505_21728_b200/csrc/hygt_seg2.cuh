@@ -37,7 +37,6 @@ struct Seg2Params {
   uint32_t gstride;
   uint64_t gmask;
   uint64_t cta_span;        // bucketed positions per CTA
-  int use_tma;              // rows in and out by per-row bulk copies (no LSU traffic)
 };
 
 HYGT_HD constexpr uint32_t seg2_row_stride(int log2n) { return (4u << log2n) + 16u; }
@@ -149,11 +148,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) hygt_seg2_kernel(const Seg2Para
   const uint32_t slot_s = su32(wslot);
   const uint32_t scr = slot_s + lane * 4u;
   const uint32_t coef_s = su32(s_coef), gt_s = su32(s_gt);
-  __shared__ __align__(8) uint64_t wbar[WARPS];  // per-warp bulk-copy barrier
-  if (lane == 0) mbar_init(&wbar[warp], 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
-  uint32_t wphase = 0;
 
   const uint64_t beg = (uint64_t)blockIdx.x * P.cta_span;
   if (beg >= P.count) return;
@@ -204,33 +199,18 @@ __global__ void __launch_bounds__(WARPS * 32, 1) hygt_seg2_kernel(const Seg2Para
       for (int r = 0; r < VPT; ++r) s_row[lane + 32u * r] = ids_next[r];
       load_ids(bb + (uint64_t)WARPS * BATCH, ids_next);
       __syncwarp();
-      if (P.use_tma) {  // one bulk copy per row into its slot, completing on the warp's barrier
-        const uint32_t nb = stop - bb < (uint64_t)BATCH ? (uint32_t)(stop - bb) : (uint32_t)BATCH;
-        bulk_wait_read0();  // this lane's stores of the previous batch have left the slots
-        __syncwarp();
-        if (lane == 0) mbar_expect_tx(&wbar[warp], nb * N * 4u);
-        __syncwarp();
-#pragma unroll
-        for (int r = 0; r < VPT; ++r) {
-          const uint32_t i = lane + 32u * r;
-          if (i < nb) bulk_g2s(wslot + i * RS, P.x + (size_t)s_row[i] * N, N * 4u, &wbar[warp]);
-        }
-        mbar_wait(&wbar[warp], wphase);
-        wphase ^= 1u;
-      } else {
-        // rows -> slots: RPI rows of N / 4 chunks per warp instruction, 16 B cp.async each
+      // rows -> slots: RPI rows of N / 4 chunks per warp instruction, 16 B cp.async each
 #pragma unroll 4
-        for (uint32_t i0 = 0; i0 < BATCH; i0 += RPI) {
-          const uint32_t i = i0 + lane / NC, q = lane % NC;
-          const uint32_t row = s_row[i];
-          if (row != 0xffffffffu)
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(slot_s + i * RS + q * 16),
-                         "l"(P.x + (size_t)row * N + q * 4)
-                         : "memory");
-        }
-        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-        __syncwarp();
+      for (uint32_t i0 = 0; i0 < BATCH; i0 += RPI) {
+        const uint32_t i = i0 + lane / NC, q = lane % NC;
+        const uint32_t row = s_row[i];
+        if (row != 0xffffffffu)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(slot_s + i * RS + q * 16),
+                       "l"(P.x + (size_t)row * N + q * 4)
+                       : "memory");
       }
+      asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+      __syncwarp();
       float2 v[VPT][NW];
 #pragma unroll
       for (int r = 0; r < VPT; ++r)
@@ -267,28 +247,17 @@ __global__ void __launch_bounds__(WARPS * 32, 1) hygt_seg2_kernel(const Seg2Para
         for (int q = 0; q < NC; ++q)
           sts128(slot_s + (lane + 32u * r) * RS + q * 16,
                  make_float4(v[r][2 * q].x, v[r][2 * q].y, v[r][2 * q + 1].x, v[r][2 * q + 1].y));
-      if (P.use_tma) {  // each lane sends its own rows back with bulk copies
-        fence_async_smem();
-#pragma unroll
-        for (int r = 0; r < VPT; ++r) {
-          const uint32_t i = lane + 32u * r;
-          if (s_row[i] != 0xffffffffu) bulk_s2g(P.y + (size_t)s_row[i] * N, wslot + i * RS, N * 4u);
-        }
-        bulk_commit();
-      } else {
-        __syncwarp();
+      __syncwarp();
 #pragma unroll 4
-        for (uint32_t i0 = 0; i0 < BATCH; i0 += RPI) {
-          const uint32_t i = i0 + lane / NC, q = lane % NC;
-          const uint32_t row = s_row[i];
-          if (row != 0xffffffffu)
-            __stcs(reinterpret_cast<float4*>(P.y + (size_t)row * N) + q, lds128(slot_s + i * RS + q * 16));
-        }
+      for (uint32_t i0 = 0; i0 < BATCH; i0 += RPI) {
+        const uint32_t i = i0 + lane / NC, q = lane % NC;
+        const uint32_t row = s_row[i];
+        if (row != 0xffffffffu)
+          __stcs(reinterpret_cast<float4*>(P.y + (size_t)row * N) + q, lds128(slot_s + i * RS + q * 16));
       }
     }
     pos = stop;
   }
-  if (P.use_tma) bulk_wait0();
 }
 
 }  // namespace hygt_gpu

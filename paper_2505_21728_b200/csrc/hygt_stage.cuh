@@ -63,8 +63,6 @@ struct StageParams {
   uint32_t* err;           // invalid class id flag (identity order)
   unsigned long long* trace;  // debug: per-tile clock64 events of CTA 0 (nullptr = off)
   uint32_t debug_skip;        // debug: consumers skip the arithmetic (timing of the other roles)
-  const uint2* bnet;       // [C][R+1][4] Beneš swap masks per lane rotation (nullptr: scratch gathers)
-  uint32_t bnet_steps;     // gather steps done by the Beneš network (the others via the scratch)
 };
 
 struct StageSortParams {
@@ -93,12 +91,11 @@ HYGT_HD constexpr uint32_t stage_gstride(int log2n, int rounds) {
 
 // Shared-memory carve-up of hygt_stage_kernel, identical on host and device.
 struct StageSmem {
-  uint32_t coef, gtab, gstride, bnet, stage, stage_bytes, ent_off, scratch, bar, total;
+  uint32_t coef, gtab, gstride, stage, stage_bytes, ent_off, scratch, bar, total;
 };
 
 HYGT_HD StageSmem stage_smem_layout(int log2n, int vpt, int warps, int classes, uint32_t cw,
-                                    int rounds, uint32_t tile_rows, bool gathers, bool benes = false,
-                                    bool scratch_too = false) {
+                                    int rounds, uint32_t tile_rows, bool gathers) {
   const uint32_t n = 1u << log2n;
   StageSmem s{};
   uint32_t o = 0;
@@ -106,15 +103,13 @@ HYGT_HD StageSmem stage_smem_layout(int log2n, int vpt, int warps, int classes, 
   o += stage_align((uint32_t)classes * cw * 16u, 128);
   s.gtab = o;
   s.gstride = stage_gstride(log2n, rounds);
-  o += gathers && (!benes || scratch_too) ? stage_align((uint32_t)classes * s.gstride, 128) : 0u;
-  s.bnet = o;
-  o += gathers && benes ? stage_align((uint32_t)classes * (rounds + 1) * 4u * 8u, 128) : 0u;
+  o += gathers ? stage_align((uint32_t)classes * s.gstride, 128) : 0u;
   s.ent_off = tile_rows * n * 4u;
   s.stage_bytes = stage_align(s.ent_off + stage_block_words(tile_rows, vpt, classes) * 2u, 128);
   s.stage = o;
   o += STAGES * s.stage_bytes;
   s.scratch = o;
-  o += gathers && (!benes || scratch_too) ? (uint32_t)warps * (vpt < STAGE_SCR_ROWS ? vpt : STAGE_SCR_ROWS) * n * 128u : 0u;
+  o += gathers ? (uint32_t)warps * (vpt < STAGE_SCR_ROWS ? vpt : STAGE_SCR_ROWS) * n * 128u : 0u;
   s.bar = stage_align(o, 16);
   s.total = s.bar + (2 * STAGES + 1) * 8;
   return s;
@@ -314,37 +309,6 @@ __device__ __forceinline__ void stage_gather(float2 (&v)[VPT][(1 << LOG2N) / 2],
   }
 }
 
-// Permutation of VPT rows in registers by a Beneš network (2 log2N - 1 layers of conditional
-// swaps on register pairs (i, i ^ 2^b)), instead of a shared-memory round trip. m holds this
-// lane's swap bits: layer l in bits [8l, 8l + 8) (layers 0-3 in m.x, 4-6 in m.y), bit j = the
-// j-th register pair of the layer; the host routed each permutation (benes_route) and
-// re-indexed the bits for the lane's element relabelling X.
-template <int LOG2N, int VPT, int L = 0>
-__device__ __forceinline__ void stage_benes(float2 (&v)[VPT][(1 << LOG2N) / 2], uint2 m) {
-  constexpr int LAYERS = 2 * LOG2N - 1;
-  if constexpr (L < LAYERS) {
-    constexpr int B = L < LOG2N ? LOG2N - 1 - L : L - LOG2N + 1;
-    const uint32_t word = (L < 4 ? m.x : m.y) >> ((L & 3) * 8);
-    int j = 0;
-#pragma unroll
-    for (int i = 0; i < (1 << LOG2N); ++i) {
-      if (i & (1 << B)) continue;
-      const bool p = (word >> j) & 1u;
-      ++j;
-      const int k2 = i | (1 << B);
-#pragma unroll
-      for (int r = 0; r < VPT; ++r) {
-        float& a = (i & 1) ? v[r][i >> 1].y : v[r][i >> 1].x;
-        float& b = (k2 & 1) ? v[r][k2 >> 1].y : v[r][k2 >> 1].x;
-        const float ta = a, tb = b;
-        a = p ? tb : ta;
-        b = p ? ta : tb;
-      }
-    }
-    stage_benes<LOG2N, VPT, L + 1>(v, m);
-  }
-}
-
 // ------------------------------------------------------------------------- per-tile sort ----
 // One warp per tile (many tiles in flight per SM: this pass is latency-, not bandwidth-bound).
 // Ranks come from shared atomics on (class, row parity) counters; inside a class, even and odd
@@ -441,13 +405,12 @@ __global__ void __launch_bounds__(32 * STAGE_SORT_WARPS) hygt_stage_sort_kernel(
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(P.err, 1u);
 }
 
-// Build variants (VAR bits): STAGE_VAR_BENES may route gathers through stage_benes (P.bnet);
-// STAGE_VAR_DEBUG honours P.trace / P.debug_skip. The default build compiles neither: their
-// never-taken branches alone cost ~1-3% of the kernel's time.
-constexpr int STAGE_VAR_BENES = 1, STAGE_VAR_DEBUG = 2;
+// Build variants (VAR bits): STAGE_VAR_DEBUG honours P.trace / P.debug_skip. The default build
+// does not compile it: its never-taken branches alone cost ~1-3% of the kernel's time.
+constexpr int STAGE_VAR_DEBUG = 2;
 template <int LOG2N, int VPT, bool STD, bool FWD, int WARPS, int VAR = 0>
 __global__ void __launch_bounds__((WARPS + 1) * 32, 1) hygt_stage_kernel(const StageParams P) {
-  constexpr bool BENES = (VAR & STAGE_VAR_BENES) != 0, DEBUG = (VAR & STAGE_VAR_DEBUG) != 0;
+  constexpr bool DEBUG = (VAR & STAGE_VAR_DEBUG) != 0;
   using namespace stage_detail;
   constexpr int N = 1 << LOG2N, NW = N / 2, NC = N / 4;
   constexpr int CT = WARPS * 32;  // consumer threads
@@ -459,9 +422,7 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) hygt_stage_kernel(const S
   const int C = P.classes;
   const uint32_t T = P.tile_rows;
   const bool gathers = P.gmask != 0;
-  const bool bn = BENES && P.bnet != nullptr;
-  const bool mixed = bn && (P.gmask & ~(uint64_t)P.bnet_steps);
-  const StageSmem L = stage_smem_layout(LOG2N, VPT, WARPS, C, P.cw, P.rounds, T, gathers, bn, mixed);
+  const StageSmem L = stage_smem_layout(LOG2N, VPT, WARPS, C, P.cw, P.rounds, T, gathers);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar);
   uint64_t* computed = full + STAGES;
   uint64_t* tables = full + 2 * STAGES;
@@ -509,12 +470,10 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) hygt_stage_kernel(const S
     };
     {  // the direction's tables, once per CTA
       const uint32_t cb = (uint32_t)C * P.cw * 16u;
-      const uint32_t gb = gathers && (!bn || mixed) ? (uint32_t)C * L.gstride : 0u;
-      const uint32_t nb = gathers && bn ? (uint32_t)C * (P.rounds + 1) * 32u : 0u;
-      mbar_expect_tx(tables, cb + gb + nb);
+      const uint32_t gb = gathers ? (uint32_t)C * L.gstride : 0u;
+      mbar_expect_tx(tables, cb + gb);
       bulk_g2s(smem + L.coef, P.coef, cb, tables);
       if (gb) bulk_g2s(smem + L.gtab, P.gtab, gb, tables);
-      if (nb) bulk_g2s(smem + L.bnet, P.bnet, nb, tables);
     }
     for (uint32_t k = 0; k < my_tiles; ++k) {
       if (k >= STAGES) {
@@ -536,7 +495,6 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) hygt_stage_kernel(const S
   const uint32_t tpar = (lane >> 2) & 1;      // preferred row parity of row slot 0
   const uint32_t coef_s = su32(smem + L.coef);
   const uint32_t gtab_s = su32(smem + L.gtab);
-  const uint32_t bnet_s = su32(smem + L.bnet);
   const uint32_t scr = su32(smem + L.scratch) + (uint32_t)warp * SCR_ROWS * N * 128u + lane * 4u;
   mbar_wait(tables, 0);
   for (uint32_t k = 0; k < my_tiles; ++k) {
@@ -610,15 +568,8 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1) hygt_stage_kernel(const S
         }
       }
       const uint32_t gbase = gtab_s + cls * L.gstride;
-      const uint32_t nbase = bnet_s + (cls * (uint32_t)(P.rounds + 1) * 4u + x) * 8u;
       auto permute = [&](int step) {
-        if (BENES && bn && ((P.bnet_steps >> step) & 1u)) {
-          uint2 m;
-          asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(m.x), "=r"(m.y) : "r"(nbase + (uint32_t)step * 32u));
-          stage_benes<LOG2N, VPT>(v, m);
-        } else {
-          stage_gather<LOG2N, VPT, SCR_ROWS>(v, scr, gbase + (uint32_t)step * N * 2u, x, xs);
-        }
+        stage_gather<LOG2N, VPT, SCR_ROWS>(v, scr, gbase + (uint32_t)step * N * 2u, x, xs);
       };
       if (P.gmask & 1ull) permute(0);
       constexpr uint32_t ROUND = (uint32_t)LOG2N * NC * 16u * (STD ? 2u : 1u);

@@ -164,7 +164,14 @@ class HyGTPlan:
     inter_round_perms : optional [C][R-1][N] gathers applied after rounds 0..R-2
     """
 
-    def __init__(self, models, inter_round_perms=None, flags: int = 0):
+    def __init__(self, models, inter_round_perms=None, flags: int = 0, kernel: str = "auto",
+                 allow_nvrtc: bool = True, cta_pairs: bool = True, stage_tile_rows: int = 0):
+        """kernel: "auto" (the measured-best family), "butterfly" (rotation kernels only) or
+        "tensor" (the composed-operator tensor-core path, N = 64 / 128 / 256); see
+        hygt_plan_options in include/hygt_gpu.h for the other options."""
+        if kernel not in _lib.KERNELS:
+            raise ArgumentError(f"HyGTPlan: kernel must be one of {sorted(_lib.KERNELS)}")
+        opts = _lib.plan_options(kernel, allow_nvrtc, cta_pairs, stage_tile_rows)
         models = _models_of(models)
         if not models:
             raise ArgumentError("HyGTPlan: need at least one class")
@@ -178,8 +185,8 @@ class HyGTPlan:
         perms, mask = _perm_table(models, rounds, self.n, inter_round_perms)
         self.perm_mask = mask
         h = C.c_void_p()
-        _check(_lib.lib().hygt_plan_create(log2_n, rounds, self.classes, _np_ptr(angles),
-                                           _np_ptr(perms), mask, flags, C.byref(h)))
+        _check(_lib.lib().hygt_plan_create_ex(log2_n, rounds, self.classes, _np_ptr(angles),
+                                              _np_ptr(perms), mask, flags, C.byref(opts), C.byref(h)))
         self._h = h
         self._ws = _Workspace()
 
@@ -301,7 +308,7 @@ class HyGTPlan:
 class FixedPlan:
     """Bit-exact integer HyGT (forward_fixed / inverse_fixed) over per-class quantized models."""
 
-    def __init__(self, models, table: TrigTable, inter_round_perms=None):
+    def __init__(self, models, table: TrigTable, inter_round_perms=None, allow_nvrtc: bool = True):
         if isinstance(models, ModelBundle):
             models = [models.quantized_model(c) for c in range(models.class_count())]
         elif isinstance(models, QuantizedHyGTModel):
@@ -317,9 +324,11 @@ class FixedPlan:
         codes = np.ascontiguousarray(np.stack([m.codes for m in models]), dtype=np.uint16)
         perms, mask = _perm_table(models, self.rounds, self.n, inter_round_perms)
         h = C.c_void_p()
-        _check(_lib.lib().hygt_fixed_plan_create(self.log2_n, self.rounds, self.classes,
-                                                 table.angle_bits, table.precision_bits,
-                                                 _np_ptr(codes), _np_ptr(perms), mask, C.byref(h)))
+        opts = _lib.plan_options(allow_nvrtc=allow_nvrtc)
+        _check(_lib.lib().hygt_fixed_plan_create_ex(self.log2_n, self.rounds, self.classes,
+                                                    table.angle_bits, table.precision_bits,
+                                                    _np_ptr(codes), _np_ptr(perms), mask, C.byref(opts),
+                                                    C.byref(h)))
         self._h = h
 
     def __del__(self):

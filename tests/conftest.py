@@ -33,3 +33,17 @@ def cuda():
     import paper_2505_21728_b200._lib as L
     L.lib()  # fail loudly if the CUDA library is missing
     return torch.device("cuda:0")
+
+
+@pytest.fixture
+def knob():
+    """Sets development knobs of the kernel selection through the library's test hook
+    (hygt_debug_set_knob; the library reads no environment variables) and clears them after the
+    test. Usage: knob("HYGT_SEGMENT", "0")."""
+    import paper_2505_21728_b200._lib as L
+
+    def set_(name, value):
+        L.set_knob(name, int(value))
+
+    yield set_
+    L.clear_knobs()

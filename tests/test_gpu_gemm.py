@@ -12,11 +12,6 @@ from test_gpu_parity import check_close
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True)
-def _gemm_on(monkeypatch):
-    monkeypatch.setenv("HYGT_GEMM", "1")
-
-
 def _case(log2n, rounds, classes, perms_kind, seed):
     from paper_2505_21728_b200 import HyGTModel, HyGTPlan
     rng = np.random.default_rng(seed)
@@ -28,7 +23,7 @@ def _case(log2n, rounds, classes, perms_kind, seed):
     final = (mask >> (rounds - 1)) & 1
     models = [HyGTModel(log2n, rounds, angles[c], perms[c, rounds - 1] if final else None) for c in range(classes)]
     inter = perms[:, : rounds - 1].copy() if mask & ((1 << (rounds - 1)) - 1) else None
-    plan = HyGTPlan(models, inter)
+    plan = HyGTPlan(models, inter, kernel="tensor")  # hygt_plan_options: the tensor-core path
     assert plan.path == "gemm"
     return plan, angles, (perms if mask else None), mask, rng
 
@@ -100,3 +95,23 @@ def test_gemm_invalid_class_ids(cuda):
     plan.forward(x, cls)
     with pytest.raises(ArgumentError):
         plan.sync_status()
+
+
+def test_plan_options_select_and_validate(cuda):
+    """hygt_plan_options: "tensor" forces the composed-operator path where supported and is an
+    ArgumentError elsewhere; "butterfly" never takes it; single CTAs give the same results as
+    CTA pairs."""
+    from paper_2505_21728_b200 import ArgumentError, HyGTModel, HyGTPlan
+    rng = np.random.default_rng(5)
+    ms = [HyGTModel(8, 2, rng.uniform(-np.pi, np.pi, 2 * 8 * 128)) for _ in range(3)]
+    assert HyGTPlan(ms).path == "gemm"  # default at N = 256
+    assert HyGTPlan(ms, kernel="butterfly").path == "segment"
+    with pytest.raises(ArgumentError):
+        HyGTPlan([HyGTModel(4, 2, rng.uniform(-np.pi, np.pi, 2 * 4 * 8))], kernel="tensor")
+    with pytest.raises(ArgumentError):
+        HyGTPlan(ms, kernel="bogus")
+    x = torch.randn(4000, 256, device=cuda) * 16
+    cls = torch.randint(0, 3, (4000,), device=cuda).to(torch.int16).view(torch.uint16)
+    y1 = HyGTPlan(ms, kernel="tensor", cta_pairs=True).forward(x, cls)
+    y0 = HyGTPlan(ms, kernel="tensor", cta_pairs=False).forward(x, cls)
+    assert torch.equal(y0, y1)  # same per-row arithmetic, only the operand staging differs

@@ -82,7 +82,6 @@ def _variants_butterfly(log2n):
         out.append({"HYGT_SEG2": "0", "HYGT_CLS": "0", "HYGT_CLS_JIT": "0", "HYGT_SEGMENT": "1", "HYGT_SEG_VARIANT": str(v)})
     if log2n in SEG2_LOG2N:  # thread-per-row kernels over global class buckets
         out.append({"HYGT_SEG2": "1", "HYGT_CLS": "0", "HYGT_CLS_JIT": "0"})
-        out.append({"HYGT_SEG2": "1", "HYGT_CLS": "0", "HYGT_CLS_JIT": "0", "HYGT_SEG2_TMA": "1"})
         out.append({"HYGT_CLS": "1", "HYGT_CLS_JIT": "0"})  # per-class launches, parameter tables
         out.append({"HYGT_CLS_JIT": "1"})  # per-class launches, NVRTC-specialised kernels
         out.append({"HYGT_CLS_JIT": "1", "HYGT_CLS_PTX": "1"})  # the same with PTX bodies
@@ -91,13 +90,9 @@ def _variants_butterfly(log2n):
                     "HYGT_TILE_L": str(l), "HYGT_TILE_VPT": str(v)})
     if log2n == 5:  # per-class NVRTC chain (multi-class plans the all-class JIT does not take)
         out.append({"HYGT_JIT": "0", "HYGT_CLS_JIT": "1"})
-    if log2n == 8:  # opt-in warp-pair variant of the chain
-        out.append({"HYGT_JIT": "0", "HYGT_CLS_JIT": "1", "HYGT_CLS_JIT256": "1"})
     if log2n in STAGE_LOG2N:  # TMA-staged tile kernel
         out.append({"HYGT_JIT": "0", "HYGT_STAGE": "1"})
         out.append({"HYGT_JIT": "0", "HYGT_STAGE": "1", "HYGT_STAGE_ROWS": "136"})
-        out.append({"HYGT_JIT": "0", "HYGT_STAGE": "1", "HYGT_STAGE_BENES": "1"})  # in-register
-        out.append({"HYGT_JIT": "0", "HYGT_STAGE": "1", "HYGT_STAGE_BENES": "2"})  # mixed
     if log2n <= 5:  # plan-specialised NVRTC kernel (served for plans with <= 4 classes)
         out.append({"HYGT_JIT": "2"})
     return out
@@ -105,7 +100,7 @@ def _variants_butterfly(log2n):
 
 @pytest.mark.parametrize("standard", [False, True])
 @pytest.mark.parametrize("k", range(10))
-def test_golden_float_all_layouts(cuda, golden, k, standard, monkeypatch):
+def test_golden_float_all_layouts(cuda, golden, k, standard, knob):
     log2n, rounds, classes, mask = (int(v) for v in golden[f"f{k}_meta"])
     angles, perms = golden[f"f{k}_angles"], golden[f"f{k}_perms"]
     x, cls = golden[f"f{k}_x"], golden[f"f{k}_cls"]
@@ -113,7 +108,7 @@ def test_golden_float_all_layouts(cuda, golden, k, standard, monkeypatch):
     cd = torch.from_numpy(cls).to(cuda)
     for env in _variants(log2n):
         for k_, v_ in env.items():
-            monkeypatch.setenv(k_, v_)
+            knob(k_, v_)
         lanes = env
         plan = _plan(_models(log2n, rounds, angles, perms, mask), _inter(perms, mask, rounds), standard)
         y = plan.forward(xd, cd)
@@ -230,13 +225,14 @@ def test_bucketing_large_batch_roundtrip(cuda):
     check_close(y[idx].cpu().numpy(), ref, x[idx].cpu().numpy(), "cfg2 full-size sample")
 
 
-@pytest.mark.parametrize("jit256", ["0", "1"])
-def test_energy_vs_oracle_and_full_size(cuda, oracle_mod, golden, jit256, monkeypatch):
+@pytest.mark.parametrize("kernel", ["butterfly", "tensor"])
+def test_energy_vs_oracle_and_full_size(cuda, oracle_mod, golden, kernel):
+    """Fused per-class energy against the reference accumulator's golden (N = 64) and the
+    config-5 shape (N = 256, 35 classes) against the oracle, on both kernel families."""
     from paper_2505_21728_b200 import HyGTModel, HyGTPlan
-    monkeypatch.setenv("HYGT_CLS_JIT256", jit256)  # segment kernel / opt-in warp-pair chain
     log2n, rounds, classes = (int(v) for v in golden["en_meta"])
     angles = golden["en_angles"]
-    plan = HyGTPlan([HyGTModel(log2n, rounds, angles[c]) for c in range(classes)])
+    plan = HyGTPlan([HyGTModel(log2n, rounds, angles[c]) for c in range(classes)], kernel=kernel)
     x = torch.from_numpy(golden["en_x"]).to(cuda)
     cls = torch.from_numpy(golden["en_cls"]).to(cuda)
     e = torch.zeros(classes, 1 << log2n, dtype=torch.float64, device=cuda)
@@ -248,18 +244,18 @@ def test_energy_vs_oracle_and_full_size(cuda, oracle_mod, golden, jit256, monkey
     rows = 1 << 14
     cls = w.make_classes(rows)
     x = w.make_rows(rows, cls)
-    plan = HyGTPlan(w.models)
+    plan = HyGTPlan(w.models, kernel=kernel)
     e = torch.zeros(35, 256, dtype=torch.float64, device=cuda)
     plan.forward_energy(x, cls, e)
     ref = oracle_mod.class_energy(8, 4, w.angles, None, 0, x.cpu().numpy(), cls.cpu().numpy())
-    np.testing.assert_allclose(e.cpu().numpy(), ref, rtol=1e-5)
+    np.testing.assert_allclose(e.cpu().numpy(), ref, rtol=2e-6)
 
 
 @pytest.mark.parametrize("k", range(7))
 @pytest.mark.parametrize("fixed_jit", ["1", "0"])
-def test_fixed_golden_bit_exact(cuda, golden, k, fixed_jit, monkeypatch):
+def test_fixed_golden_bit_exact(cuda, golden, k, fixed_jit, knob):
     from paper_2505_21728_b200 import ArgumentError, FixedPlan, QuantizedHyGTModel, TrigTable
-    monkeypatch.setenv("HYGT_FIXED_JIT", fixed_jit)
+    knob("HYGT_FIXED_JIT", fixed_jit)
     log2n, rounds, b, p, with_perm = (int(v) for v in golden[f"x{k}_meta"])
     perm = golden[f"x{k}_perm"] if with_perm else None
     m = QuantizedHyGTModel(log2n, rounds, b, golden[f"x{k}_codes"], perm)
@@ -316,17 +312,17 @@ def test_fixed_long_models_overflow_and_int32_gate(cuda, golden_long, name):
 
 
 @pytest.mark.parametrize("kernel", ["default", "stage", "row", "warp"])
-def test_fixed_random_multiclass_vs_oracle(cuda, oracle_mod, kernel, monkeypatch):
+def test_fixed_random_multiclass_vs_oracle(cuda, oracle_mod, kernel, knob):
     """Bit-exact vs the oracle through every fixed-point kernel: the per-class NVRTC chain
     (default, N <= 64), the staged one (N = 16), the thread-per-row one (N <= 64) and the
     warp-per-row one."""
     from paper_2505_21728_b200 import FixedPlan, QuantizedHyGTModel, TrigTable
     if kernel != "default":
-        monkeypatch.setenv("HYGT_FIXED_JIT", "0")
+        knob("HYGT_FIXED_JIT", "0")
     if kernel in ("row", "warp"):
-        monkeypatch.setenv("HYGT_FIXED_STAGE", "0")
+        knob("HYGT_FIXED_STAGE", "0")
     if kernel == "warp":
-        monkeypatch.setenv("HYGT_FIXED_ROW", "0")
+        knob("HYGT_FIXED_ROW", "0")
     rng = np.random.default_rng(11)
     for log2n, rounds, classes in [(4, 3, 35), (6, 4, 5), (8, 2, 3)]:
         n = 1 << log2n
@@ -571,12 +567,12 @@ def test_reference_adapter(cuda):
     assert "adapter_check: ok" in r.stdout
 
 
-def test_jit_plan_matches_oracle(cuda, oracle_mod, monkeypatch):
+def test_jit_plan_matches_oracle(cuda, oracle_mod, knob):
     """The NVRTC plan-specialised path (coefficients as immediates, permutations as register
     renames) on config-1 style plans: 1-4 classes, inter-round and final permutations, both
     arithmetic forms, tails, invalid class ids."""
     from paper_2505_21728_b200 import ArgumentError, HyGTModel
-    monkeypatch.setenv("HYGT_STAGE", "0")  # N = 16 plans otherwise take the staged kernel
+    knob("HYGT_STAGE", "0")  # N = 16 plans otherwise take the staged kernel
     rng = np.random.default_rng(21)
     for log2n, rounds, classes in [(2, 2, 1), (3, 3, 2), (4, 2, 1), (4, 3, 4), (5, 2, 3)]:
         n = 1 << log2n
@@ -606,13 +602,13 @@ def test_jit_plan_matches_oracle(cuda, oracle_mod, monkeypatch):
 
 
 @pytest.mark.parametrize("standard", [False, True])
-def test_stage_path_edges(cuda, oracle_mod, standard, monkeypatch):
+def test_stage_path_edges(cuda, oracle_mod, standard, knob):
     """TMA-staged kernel (plan path 'stage'): partial and multi-tile batches, class ids staged by
     TMA and (misaligned) by plain loads, in place, unaligned rows falling back to the tile
     kernel, invalid ids passed through and reported."""
     from paper_2505_21728_b200 import ArgumentError, HyGTModel
     from oracle import oracle as O
-    monkeypatch.setenv("HYGT_JIT", "0")
+    knob("HYGT_JIT", "0")
     rng = np.random.default_rng(21)
     C, R = 7, 3
     angles = rng.uniform(-np.pi, np.pi, (C, R * 4 * 8))
@@ -660,13 +656,13 @@ def test_stage_path_edges(cuda, oracle_mod, standard, monkeypatch):
     (False, "1", "1", "clsjit", 4, 6), (False, "1", "1", "clsjit", 5, 6), (False, "1", "0", "cls", 4, 6),
     (False, "1", "0", "cls", 2, 6), (False, "0", "0", "seg2", 4, 6), (True, "1", "1", "seg2", 4, 6),
     (False, "1", "0", "seg2", 5, 6), (False, "1", "1", "clsjit", 3, 5)])
-def test_seg2_path_edges(cuda, oracle_mod, standard, cls_env, jit_env, path, R, log2n, monkeypatch):
+def test_seg2_path_edges(cuda, oracle_mod, standard, cls_env, jit_env, path, R, log2n, knob):
     """Thread-per-row bucketed kernels (plan paths 'cls' and 'seg2', N = 64): partial batches, a
     class with a single row, in place, invalid ids passed through and reported."""
     from paper_2505_21728_b200 import ArgumentError, HyGTModel
     from oracle import oracle as O
-    monkeypatch.setenv("HYGT_CLS", cls_env)
-    monkeypatch.setenv("HYGT_CLS_JIT", jit_env)
+    knob("HYGT_CLS", cls_env)
+    knob("HYGT_CLS_JIT", jit_env)
     rng = np.random.default_rng(33)
     C, n = 6, 1 << log2n
     angles = rng.uniform(-np.pi, np.pi, (C, R * log2n * n // 2))
@@ -740,12 +736,12 @@ def test_correlation_invalid_ids(cuda):
 
 
 @pytest.mark.parametrize("fixed_jit", ["1", "0"])
-def test_fixed_staged_edges(cuda, oracle_mod, fixed_jit, monkeypatch):
+def test_fixed_staged_edges(cuda, oracle_mod, fixed_jit, knob):
     """Per-class NVRTC chain and staged fixed-point kernel (N = 16): partial and multi-tile
     batches, no class ids, in place, the first failing row for oversized inputs and for invalid
     class ids."""
     from paper_2505_21728_b200 import ArgumentError, FixedPlan, QuantizedHyGTModel, TrigTable
-    monkeypatch.setenv("HYGT_FIXED_JIT", fixed_jit)
+    knob("HYGT_FIXED_JIT", fixed_jit)
     rng = np.random.default_rng(12)
     C, R, n = 6, 3, 16
     codes = rng.integers(0, 256, (C, R * 4 * 8)).astype(np.uint16)

@@ -167,9 +167,9 @@ def test_trainer_host_logic_mirrors_reference(oracle_mod):
         train.variance_permutation(m, [1.0, 2.0, 3.0, 4.0])
 
 
-@pytest.mark.parametrize("kind,log2n,rounds,ptx", [(0, 6, 4, 0), (0, 6, 4, 1), (0, 5, 3, 0), (0, 8, 2, 0), (1, 4, 3, 0), (1, 6, 2, 0)])
+@pytest.mark.parametrize("kind,log2n,rounds,ptx", [(0, 6, 4, 0), (0, 6, 4, 1), (0, 5, 3, 0), (1, 4, 3, 0), (1, 6, 2, 0)])
 def test_per_class_kernels_compile_without_gpu(kind, log2n, rounds, ptx):
-    """The per-class NVRTC generators (float N = 32/64/256, fixed point) emit source that compiles
+    """The per-class NVRTC generators (float N = 32/64, fixed point) emit source that compiles
     for sm_100a; NVRTC needs no GPU, so this runs in the CPU suite (hygt_debug_jit_compile)."""
     import ctypes as C
     from paper_2505_21728_b200 import _lib
@@ -186,3 +186,20 @@ def test_per_class_kernels_compile_without_gpu(kind, log2n, rounds, ptx):
     st = fn(kind, log2n, rounds, angles.ctypes.data_as(C.c_void_p), codes.ctypes.data_as(C.c_void_p),
             perms.ctypes.data_as(C.c_void_p) if mask else None, C.c_uint32(mask), ptx, C.byref(out))
     assert st == 0 and out.value > 10000
+
+
+def test_library_reads_no_environment():
+    """The reference contract has no environment variables: kernel choices come
+    from hygt_plan_options, development knobs only from the test hook (hygt_knobs.h)."""
+    import glob
+    import os
+    import re
+    root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2505_21728_b200", "csrc")
+    offenders = []
+    for p in glob.glob(os.path.join(root, "*")):
+        if p.endswith((".cu", ".cuh", ".cpp", ".h")):
+            for i, line in enumerate(open(p, encoding="utf-8", errors="replace"), 1):
+                code = line.split("//", 1)[0]
+                if re.search(r"\bgetenv\s*\(", code):
+                    offenders.append(f"{os.path.basename(p)}:{i}")
+    assert not offenders, offenders

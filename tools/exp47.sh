@@ -13,6 +13,6 @@ write_bundle("/tmp/q.hygt", 4, codes=[rng.integers(0, 256, A) for _ in range(C)]
 for ar, m in (("float", "/tmp/f.hygt"), ("fixed", "/tmp/q.hygt")):
     for rep in range(2):
         t = time.perf_counter()
-        r = subprocess.run(["paper_2505_21728_b200/hygt_gpu_apply", "--model", m, "--data", "/tmp/big.rblk", "--arithmetic", ar, "--out", "/tmp/o.rblk"], capture_output=True, text=True, env=dict(os.environ, HYGT_APPLY_TIMING="1"))
+        r = subprocess.run(["paper_2505_21728_b200/hygt_gpu_apply", "--model", m, "--data", "/tmp/big.rblk", "--arithmetic", ar, "--out", "/tmp/o.rblk"], capture_output=True, text=True, ) if False else subprocess.run(["paper_2505_21728_b200/hygt_gpu_apply", "--model", m, "--data", "/tmp/big.rblk", "--arithmetic", ar, "--out", "/tmp/o.rblk", "--timing"], capture_output=True, text=True)
         print(ar, rep, round(time.perf_counter() - t, 3), "s", r.stderr.replace("\n", " | "))
 PY

@@ -16,13 +16,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=5)
 ap.add_argument("--inverse", action="store_true")
 a = ap.parse_args()
-os.environ.setdefault("HYGT_GEMM", "1")
 w = make_workload(a.config)
 rows = w.cfg.count
 cls = w.make_classes(rows)
 x = w.make_rows(rows, cls)
 y = torch.empty_like(x)
-plan = HyGTPlan(w.models, w.perms)
+plan = HyGTPlan(w.models, w.perms, kernel="tensor")
 ws = torch.zeros(plan.workspace_bytes(rows), dtype=torch.uint8, device="cuda")
 plan.forward(x, cls, out=y, workspace=ws)
 tr = torch.zeros(64 * 16, dtype=torch.int64, device="cuda")

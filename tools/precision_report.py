@@ -35,9 +35,8 @@ def err(y, r):
     return {"rel_l2": float(np.linalg.norm(e) / np.linalg.norm(r)), "max_abs_over_max_x": float(np.abs(e).max() / np.abs(xh).max())}
 
 
-for gemm in ("0", "1"):
-    os.environ["HYGT_GEMM"] = gemm
-    plan = HyGTPlan(w.models, w.perms)
+for kernel in ("butterfly", "tensor"):
+    plan = HyGTPlan(w.models, w.perms, kernel=kernel)
     y = plan.forward(x, cls)
     z = plan.inverse(x, cls)
     b = plan.inverse(y, cls)
