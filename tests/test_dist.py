@@ -194,4 +194,7 @@ def test_gpu_energy_two_shards_allreduce_vs_oracle():
     x = w.make_rows(count, cls)
     ref = O.class_energy(8, 4, w.angles, None, 0, x.cpu().numpy(), cls.cpu().numpy(), hoist=True)
     for _, e in res:
-        np.testing.assert_allclose(e, ref, rtol=1e-6)
+        # the default N = 256 path is the tensor-core one: energies within its stated 2e-6 bar
+        # (tests/test_gpu_fullsize.py); the two ranks' tables are identical after the all-reduce
+        np.testing.assert_allclose(e, ref, rtol=2e-6)
+    assert np.array_equal(res[0][1], res[1][1])
