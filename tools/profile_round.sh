@@ -1,22 +1,28 @@
-# Round profiling pass: bench lines for every config, launch lists, one full ncu capture per top
-# kernel exported to CSV on the box (the .ncu-rep files are ~45 MB each).
-mkdir -p gpurun_out
-for C in 1 2 3 4 5; do timeout 400 python bench.py --config $C --steps 10 --no-e2e --no-cpu > gpurun_out/bench_cfg$C.json 2>gpurun_out/bench_cfg$C.err; done
-timeout 300 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/plain.log 2>&1 && \
-  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_cfg2.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_l.log 2>&1
-timeout 300 python bench.py --config 5 --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/plain5.log 2>&1 && \
-  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_cfg5.csv python bench.py --config 5 --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_l5.log 2>&1
-prof() {  # name, kernel regex, bench args
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$2" -s 4 -c 1 -f -o /tmp/prof_$1 python bench.py $3 --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_$1.log 2>&1
-  ncu -i /tmp/prof_$1.ncu-rep --page raw --csv > gpurun_out/prof_$1_raw.csv 2>/dev/null
-  ncu -i /tmp/prof_$1.ncu-rep --page details --csv > gpurun_out/prof_$1_details.csv 2>/dev/null
+#!/bin/bash
+# Round profiling (run on the GPU box from the repo root): default bench line, its ncu launch
+# list, ncu --set full captures of the top kernel of every config, whole-chain DRAM traffic.
+out=${1:-gpurun_out/r02}
+mkdir -p "$out"
+python bench.py --steps 20 --warmup 5 > "$out/bench_default.json" 2> "$out/bench_default.err"
+echo "bench rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$out/launches_default.csv" \
+  python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > "$out/launches_default.log" 2>&1
+echo "launches rc=$?"
+cap() {  # name, kernel regex, launch-skip, count, args...
+  local name=$1 re=$2 skip=$3 cnt=$4; shift 4
+  timeout 900 ncu --set full --import-source on --clock-control none -k "regex:$re" --launch-skip $skip \
+    --launch-count $cnt -o "$out/ncu_$name" -f python tools/prof_step.py "$@" > "$out/ncu_$name.log" 2>&1
+  echo "ncu $name rc=$?"
 }
-prof cfg2 hygt_stage_kernel ""
-prof cfg1 hygt_jit_kernel "--config 1"
-prof cfg3 hygt_seg2_kernel "--config 3"
-prof cfg5 hygt_segment_kernel "--config 5"
-prof cfg4 klt_sw_kernel "--config 4"
-prof sort2 hygt_stage_sort "--config 2"
-timeout 300 python tools/fixed_bench.py --config 2 > gpurun_out/fixed_cfg2.json 2>&1
-timeout 300 python tools/fixed_bench.py --config 3 > gpurun_out/fixed_cfg3.json 2>&1
-ls -la gpurun_out | head -40
+cap cfg2_stage hygt_stage_kernel 2 1 --config 2 --steps 2
+cap cfg5_gemm hygt_gemm 2 2 --config 5 --steps 2
+cap cfg4_klt hygt_gemm 2 2 --config 4 --steps 2
+cap cfg3_clsjit hygt_cls_f 35 1 --config 3 --steps 2
+cap cfg1_stage hygt_stage_kernel 2 1 --config 1 --steps 2
+# whole forward launch chains as one range (config 3: 35 per-class grids; the others for symmetry)
+for c in 2 3 4 5; do
+  timeout 900 ncu --replay-mode range --clock-control none \
+    --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --csv \
+    --log-file "$out/range_cfg$c.csv" python tools/prof_step.py --config $c --steps 2 --range > "$out/range_cfg$c.log" 2>&1
+  echo "range cfg$c rc=$?"
+done
