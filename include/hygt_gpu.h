@@ -103,6 +103,12 @@ int hygt_plan_create_ex(int log2_n, int rounds, int class_count, const double* a
 int hygt_plan_destroy(hygt_plan* plan);
 /* 0 = standard rotations, 1 = scale-folded (fast Givens) form chosen at plan time. */
 int hygt_plan_algorithm(const hygt_plan* plan);
+/* Largest max|x| per row for which the plan's arithmetic keeps every intermediate finite in
+ * fp32 (the transform itself is orthogonal: outputs are bounded by sqrt(N) max|x|). The
+ * scale-folded form divides by running cosine products sigma, so its limit is
+ * 2^127 sigma_min / sqrt(N); plans take it only when that is >= 2^40, and
+ * HYGT_PLAN_FORCE_STANDARD removes the limit (2^127 / sqrt(N)). */
+double hygt_plan_input_limit(const hygt_plan* plan);
 /* Kernel family serving the plan: 0 = bucketed apply kernel (hygt_bucket + per-row gather),
  * 1 = tile kernel (class sort inside each CTA, no bucketing pass; N <= 32),
  * 2 = class-segment kernel (global class buckets, one class table staged per CTA segment),

@@ -25,6 +25,7 @@ SIGNATURES = {
     "hygt_plan_create_ex": (_i, [_i, _i, _i, _p, _p, _u32, _u32, _p, C.POINTER(_p)]),
     "hygt_plan_destroy": (_i, [_p]),
     "hygt_plan_algorithm": (_i, [_p]),
+    "hygt_plan_input_limit": (C.c_double, [_p]),
     "hygt_plan_path": (_i, [_p]),
     "hygt_workspace_bytes": (_sz, [_p, _u64]),
     "hygt_bucket": (_i, [_p, _p, _u64, _p, _sz, _p]),

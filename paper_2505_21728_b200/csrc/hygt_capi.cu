@@ -68,6 +68,7 @@ extern "C" int hygt_last_error(char* buf, size_t len) {
 struct hygt_plan {
   int kind = 0;  // 0 float, 1 fixed
   hygt_plan_options opt{};  // resolved creation options (include/hygt_gpu.h)
+  double input_limit = 0;   // largest max|x| the plan's arithmetic form keeps finite
   int log2n = 0, rounds = 0, classes = 0, lanes_log2 = 0;
   int algo = 0;  // 0 standard, 1 scale-folded
   uint32_t perm_mask = 0;
@@ -1220,6 +1221,10 @@ extern "C" int hygt_plan_create_ex(int log2_n, int rounds, int class_count, cons
     standard = true;
   }
   p->algo = standard ? 0 : 1;
+  // input range: the scale-folded form's (hygt_plan.h), or the standard rotations' (orthogonal:
+  // |value| <= sqrt(N) max|x| within fp32)
+  p->input_limit = standard ? std::ldexp(1.0, 127 - (log2_n + 1) / 2)
+                            : std::min(fast_input_limit(log2_n, t[0].sigma_min), fast_input_limit(log2_n, t[1].sigma_min));
   for (int d = 0; d < 2; ++d) {
     int s = upload(&p->d_coef[d], reinterpret_cast<const float2*>(t[d].coef.data()), t[d].coef.size());
     if (!s) s = upload(&p->d_gidx[d], t[d].gidx.data(), t[d].gmask ? t[d].gidx.size() : 0);
@@ -1301,6 +1306,13 @@ extern "C" int hygt_plan_destroy(hygt_plan* plan) {
 }
 
 extern "C" int hygt_plan_algorithm(const hygt_plan* plan) { return plan ? plan->algo : -1; }
+
+extern "C" double hygt_plan_input_limit(const hygt_plan* plan) {
+  if (!plan) return 0.0;
+  // the tensor-core path scales every row by a power of two of its own: any finite input
+  if (plan->gemm) return std::ldexp(1.0, 127 - (plan->log2n + 1) / 2);
+  return plan->kind == 0 ? plan->input_limit : 1048576.0;  // fixed point: |x| <= 2^20 (fixedpoint.hpp:145)
+}
 
 extern "C" int hygt_plan_path(const hygt_plan* plan) {
   return plan ? (plan->gemm ? 8 : plan->jit.ok ? 3 : plan->stage ? 4 : plan->cls_jit.ok ? 7 : plan->cls ? 6 : plan->tile ? 1 : plan->seg2 ? 5 : plan->seg ? 2 : 0) : -1;

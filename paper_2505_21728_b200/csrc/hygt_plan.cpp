@@ -9,9 +9,9 @@
 //       a' = a + t1 b,  b' = b - t2 a,  t1 = s sig_n / (c sig_m),  t2 = s sig_m / (c sig_n),
 //     and sig_m, sig_n *= c; the true values are sig * stored, so one FFMA per output replaces
 //     an FMUL + FFMA. The remaining sig are applied once after the last pass.
-// The fast form is exact algebra; it is used only when every c != 0 and all scales stay in
-// [2^-96, 1] and all |t| <= 2^100 (fp32 headroom for |x| <= 2^20), otherwise the plan falls back
-// to the standard form (hygt_plan_algorithm() reports which).
+// The fast form is exact algebra; it is used only when every c != 0, all |t| <= 2^100 and the
+// scales keep the plan's input limit (hygt_plan.h: 2^127 sigma_min / sqrt(N)) at or above 2^40;
+// otherwise the plan falls back to the standard form (hygt_plan_algorithm() reports which).
 #include "hygt_plan.h"
 
 #include <algorithm>
@@ -78,6 +78,8 @@ bool build_direction(const Layout& ly, int rounds, int classes, const double* an
                      DirTables& out) {
   const int n = ly.n(), log2n = ly.log2n, half = n / 2, tpv = ly.tpv(), e = ly.e();
   const size_t a_count = (size_t)rounds * log2n * half;
+  const double sig_floor = fast_sigma_floor(log2n);
+  out.sigma_min = 1.0;
   uint32_t len = 0;
   for (int p = 0; p < log2n; ++p) len += ly.words_per_pass(standard, p);
   len *= rounds;
@@ -135,7 +137,8 @@ bool build_direction(const Layout& ly, int rounds, int classes, const double* an
             sig[m] *= cs;
             sig[nn] *= cs;
             if (!(std::fabs(k1) <= 0x1p100) || !(std::fabs(k2) <= 0x1p100)) return false;
-            if (!(std::fabs(sig[m]) >= 0x1p-96) || !(std::fabs(sig[nn]) >= 0x1p-96)) return false;
+            if (!(std::fabs(sig[m]) >= sig_floor) || !(std::fabs(sig[nn]) >= sig_floor)) return false;
+            out.sigma_min = std::min(out.sigma_min, std::min(std::fabs(sig[m]), std::fabs(sig[nn])));
             pass[j] = {k1, k2};
           }
         }
@@ -229,7 +232,8 @@ bool build_programs(int log2n, int rounds, int classes, const double* angles,
             sig[m] *= cs;
             sig[nn] *= cs;
             if (!(std::fabs(k1) <= 0x1p100) || !(std::fabs(k2) <= 0x1p100)) return false;
-            if (!(std::fabs(sig[m]) >= 0x1p-96) || !(std::fabs(sig[nn]) >= 0x1p-96)) return false;
+            if (!(std::fabs(sig[m]) >= fast_sigma_floor(log2n)) || !(std::fabs(sig[nn]) >= fast_sigma_floor(log2n)))
+              return false;
             pr.ops.push_back(ProgOp{0, (uint16_t)m, (uint16_t)nn, (float)k1, (float)-k2, 0});
           }
         }

@@ -3,6 +3,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <cmath>
 #include <vector>
 
 #include "layout.h"
@@ -19,7 +20,21 @@ struct DirTables {
   std::vector<uint16_t> gidx;  // [C][R+1][TPV][E] gather sources (element indices)
   uint64_t gmask = 0;          // bit k: gather step k present
   uint32_t stream_len = 0;     // float2 words per lane stream
+  double sigma_min = 1.0;      // scale-folded form: smallest running per-sample scale
 };
+
+// Input range of the scale-folded form. Its stored values are true / sigma with sigma the
+// running per-sample scale, and |true| <= ||x||_2 <= sqrt(N) max|x| (orthogonal passes), so every
+// intermediate stays finite in fp32 while max|x| < 2^127 sigma_min / sqrt(N): the plan's input
+// limit (hygt_plan_input_limit). The form is used only when that limit is at least
+// 2^FAST_FORM_MIN_INPUT_LOG2 (far above residual data); otherwise the standard rotations.
+constexpr int FAST_FORM_MIN_INPUT_LOG2 = 40;
+inline double fast_sigma_floor(int log2n) {
+  return std::ldexp(1.0, FAST_FORM_MIN_INPUT_LOG2 - 127 + (log2n + 1) / 2);
+}
+inline double fast_input_limit(int log2n, double sigma_min) {
+  return std::ldexp(sigma_min, 127 - (log2n + 1) / 2);
+}
 
 // One class's transform as straight-line operations in execution order (for code generation):
 //   kind 0: butterfly on (m, n) with coefficients (a, b): scale-folded (t1, -t2) or standard (c, s)

@@ -203,6 +203,11 @@ class HyGTPlan:
         return self._h
 
     @property
+    def input_limit(self) -> float:
+        """Largest max|x| per row the plan's fp32 arithmetic keeps finite (hygt_plan_input_limit)."""
+        return float(_lib.lib().hygt_plan_input_limit(self._h))
+
+    @property
     def algorithm(self) -> str:
         return "scale-folded" if _lib.lib().hygt_plan_algorithm(self._h) == 1 else "standard"
 

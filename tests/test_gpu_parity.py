@@ -800,3 +800,27 @@ def test_plans_of_different_sizes_coexist(cuda):
     ci = torch.from_numpy(rng.integers(0, 20, 3000).astype(np.uint16)).to(cuda)
     fsmall.forward(xi)
     fbig.forward(xi, ci)
+
+
+@pytest.mark.parametrize("config", [2, 3])
+def test_fast_form_input_limit(cuda, oracle_mod, config):
+    """The scale-folded form's fp32 range (hygt_plan_input_limit = 2^127 sigma_min / sqrt(N)):
+    plans take it only when the limit is >= 2^40; rows scaled up to 2^38 still match the oracle,
+    and HYGT_PLAN_FORCE_STANDARD lifts the limit to 2^127 / sqrt(N)."""
+    from paper_2505_21728_b200.synth import make_workload
+    w = make_workload(config)
+    plan = _plan(w.models, w.perms)
+    assert plan.algorithm == "scale-folded"
+    assert plan.input_limit >= 2.0 ** 40
+    std = _plan(w.models, w.perms, standard=True)
+    assert std.algorithm == "standard" and std.input_limit >= 2.0 ** 120
+    cls = w.make_classes(4096)
+    x = w.make_rows(4096, cls)
+    x = x * (2.0 ** 38 / x.abs().max().item())
+    full = np.concatenate([w.perms, np.tile(np.arange(w.n, dtype=np.uint16), (w.cfg.classes, 1, 1))], 1)
+    mask = (1 << (w.cfg.rounds - 1)) - 1
+    ref = oracle_mod.apply_batch(w.cfg.log2_n, w.cfg.rounds, w.angles, full, mask, x.cpu().numpy(), cls.cpu().numpy())
+    y = plan.forward(x, cls)
+    plan.sync_status()
+    assert torch.isfinite(y).all()
+    check_close(y.cpu().numpy(), ref, x.cpu().numpy(), f"cfg{config} at 2^38")
