@@ -1032,7 +1032,8 @@ int setup_gemm(hygt_plan* p, const double* angles, const uint16_t* perms) {
   if (int s = gemm_build(n, p->classes, inv.data(), p->gemm_ops[1])) return s;
   for (int d = 0; d < 2; ++d) {
     p->gemm_ops[d].pair = p->opt.cta_pairs != 0 && env_int("HYGT_GEMM_PAIR", 1) != 0;
-    p->gemm_ops[d].wide = env_int("HYGT_GEMM_WIDE", 0) != 0;  // measured slower
+    p->gemm_ops[d].wide = env_int("HYGT_GEMM_WIDE", 1) != 0;  // merged accumulator, one unit per tile
+    p->gemm_ops[d].dbg = env_int("HYGT_GEMM_DBG", 0);  // measured slower
   }
   p->gemm = true;
   p->chunk_rows = 0;  // global class buckets

@@ -21,22 +21,27 @@
 // lo.hi + hi.lo + hi.hi accumulated in fp32 in TMEM (the dropped lo.lo term is ~2^-22 relative).
 // fp16 has 5 exponent bits, so every row is scaled by a power of two chosen from its own
 // max |x| (max |x s| in [2^14, 2^15)) and every class operator by 2^kB (max |b 2^kB| in
-// [2^14, 2^15)); both scales are exact and undone in the epilogue.
+// [2^14, 2^15)); both scales are exact and undone in the epilogue. The tensor cores round each
+// K step's addition to the running fp32 sum, so per unit the two correction terms of ALL K are
+// accumulated first and the main term after them: only its 4 KA K steps round against the
+// full-size sum (as with separate accumulators, in half the TMEM).
 //
-// Kernel structure (one persistent CTA per SM, warp-specialised, all hand-offs on mbarriers):
+// Kernel structure (one persistent CTA per SM, or a CTA pair per two SMs with tcgen05
+// cta_group::2, warp-specialised, all hand-offs on mbarriers; 16 warps = 4 warpgroups whose
+// registers are rebalanced with setmaxnreg):
 //   warps 0-3   epilogue : TMEM -> registers (tcgen05.ld, lane = row) -> unscale -> swizzled
-//                          staging -> coalesced STG rows; fused per-class energy (fp64)
-//   warps 4-11  split    : rows (LDG, coalesced) -> row max -> scale -> fp16 hi/lo into the
-//                          tile's SWIZZLE_128B K-major A (KA 64-column K atoms); the row-max
-//                          pass of tile t+1 overlaps the MMAs of tile t
-//   warp 12     producer : cp.async.bulk of the class's B stages (L2 resident, 32 KB each)
-//   warp 13     MMA      : one thread issues tcgen05.mma kind::f16 M=128 N<=128 K=16
+//                          staging -> coalesced STG rows; fused per-class energy (compensated
+//                          fp32 per lane, fp64 at the class flush)
+//   warps 4-11  split    : each lane holds its share of a whole tile in registers (one read of
+//                          every row): row max -> power-of-two scale -> fp16 hi/lo into the
+//                          tile's SWIZZLE_128B K-major A (64-column K atoms); the next tile's
+//                          loads of an atom are issued as soon as the atom is converted
+//   warp 12     producer : cp.async.bulk of the class's B half-atom stages (L2 resident)
+//   warp 13     MMA      : one thread issues tcgen05.mma kind::f16 (M = 128 / 256, N <= 256, K = 16)
 //   warp 14     prefetch : L2 prefetch of the rows two tiles ahead (prefetch.global.L2)
-//   A tile is issued as NH "units" of up to 128 output columns. TMEM: per unit two fp32
-//   accumulators, hi.hi and the two correction terms apart (tensor-core accumulation rounds
-//   each K step against the running sum, so keeping the 2^-11-sized terms out of the big sum
-//   keeps their rounding negligible), double-buffered over units (4 x 128 columns at N >= 128),
-//   so the epilogue of one unit overlaps the MMAs of the next.
+//   warp 15     idle     (completes the fourth warpgroup)
+//   A tile is issued as NH units of NW output columns (wide: one unit of all N columns), each
+//   into one of two TMEM accumulators, so the epilogue of one unit overlaps the next unit's MMAs.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -63,7 +68,14 @@ constexpr int SPLIT_WARPS = 8;
 constexpr int PROD_WARP = EPI_WARPS + SPLIT_WARPS;
 constexpr int MMA_WARP = PROD_WARP + 1;
 constexpr int PF_WARP = MMA_WARP + 1;
-constexpr int GEMM_THREADS = (PF_WARP + 1) * 32;
+constexpr int GEMM_THREADS = (PF_WARP + 2) * 32;  // + one idle warp: four whole warpgroups
+// Register rebalancing (setmaxnreg, per warpgroup): 128 per thread at launch (64 K / 512);
+// the split warpgroups take what the epilogue and the single-thread roles give back, so that
+// a split lane holds its whole share of a tile (up to 128 floats at N = 256).
+constexpr int REG_EPI = 128, REG_SPLIT = 160, REG_MISC = 64;
+static_assert(REG_EPI + 2 * REG_SPLIT + REG_MISC <= 512, "register pool");
+template <int R> __device__ __forceinline__ void regs_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" :: "n"(R)); }
+template <int R> __device__ __forceinline__ void regs_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" :: "n"(R)); }
 constexpr uint32_t ATOM_BYTES = GM * 128;  // one 64-column fp16 K atom of the A tile (16 KB)
 
 template <int NN, bool PAIR, bool WIDE>
@@ -74,25 +86,28 @@ struct Shape {
   static constexpr int NW = WIDE ? NN : (NN < 128 ? NN : 128);
   static constexpr int NH = NN / NW;                 // units per tile
   static constexpr int BW = PAIR ? NW / 2 : NW;      // B rows (output columns) held by this CTA
-  static constexpr uint32_t STAGE = 2u * BW * 128;   // B stage (one K atom of one unit): hi + lo
-  static constexpr int NB = STAGE <= 16384 ? 4 : 2;  // B ring stages
+  // B stage: one half (hi or lo) of one K atom of one unit (this CTA's BW rows), streamed in
+  // the MMA order (per unit: per atom hi, lo for the correction terms, then hi again for the
+  // main term): SPT stages per tile
+  static constexpr uint32_t STAGE = (uint32_t)BW * 128;
+  static constexpr int NB = STAGE <= 8192 ? 8 : 4;  // B ring stages
+  static constexpr int SPT = 3 * KA * NH;
   static constexpr int TG = PAIR ? 2 * GM : GM;      // rows per tile (a CTA pair: 128 each)
   static constexpr int ABUF = KA <= 2 ? 2 : 1;       // tiles of A resident (double-buffered if small)
   static constexpr int AS = KA * ABUF;               // A atom slots
   static constexpr uint32_t A_OFF = 0;               // A: AS atoms (hi + lo each)
   static constexpr uint32_t B_OFF = A_OFF + AS * 2 * ATOM_BYTES;
   static constexpr uint32_t STG_OFF = B_OFF + NB * STAGE;
-  static constexpr uint32_t STG_BYTES = 32 * 128;    // per epilogue warp: 32 rows x 32 floats
-  static constexpr uint32_t EN_OFF = STG_OFF + EPI_WARPS * STG_BYTES;
-  static constexpr uint32_t FAC_OFF = EN_OFF + EPI_WARPS * NN * 8;
+  static constexpr uint32_t STG_BYTES = 32 * 128;    // per epilogue warp: 32 rows x 32 floats (swizzled)
+  static constexpr uint32_t FAC_OFF = STG_OFF + EPI_WARPS * STG_BYTES;
   static constexpr uint32_t BAR_OFF = FAC_OFF + 4 * GM * 4;
   static constexpr uint32_t SMEM = BAR_OFF + 512;  // barriers (<= 40 x 8 B) + the TMEM address
-  // TMEM: per unit a "big" accumulator (hi.hi) and a "small" one (lo.hi + hi.lo), NW columns
-  // each, double-buffered over units when 4 NW <= 512 columns
-  static constexpr int NBUF = 4 * NW <= 512 ? 2 : 1;
-  static constexpr uint32_t TMEM_COLS = NBUF * 2 * NW < 32 ? 32 : NBUF * 2 * NW;
+  // TMEM: one fp32 accumulator of NW columns per unit, double-buffered over units
+  static constexpr int NBUF = 2;
+  static constexpr int ACC = NW;
+  static constexpr uint32_t TMEM_COLS = NBUF * ACC < 32 ? 32 : NBUF * ACC;
   static constexpr int RG = GM / SPLIT_WARPS / 4;    // 4-row groups per split warp
-  static_assert(!WIDE || PAIR, "the wide unit needs the CTA pair");
+  static_assert(!WIDE || PAIR || NN <= 128, "N = 256 in one unit needs the CTA pair");
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -300,14 +315,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
 
   if (warp == MMA_WARP) {
     // ------------------------------------------------------------------ MMA issuer ----
-    // Per tile, NH units (N halves) in order; per unit all K atoms x 4 K steps x 3 terms.
-    // Unit u accumulates into buffer u & 1: big at 2 NW (u & 1), small NW columns after it.
+    regs_dec<REG_MISC>();
+    // Per tile, NH units of NW output columns in order, unit u into TMEM buffer u & 1. Per
+    // unit the correction terms of all K first (per K atom: lo.hi with the B hi stage, hi.lo
+    // with the B lo stage), then the main term hi.hi (B hi again): only the 4 KA main-term K
+    // steps round against the full-size sum (the tensor cores round each K step's addition).
     if (PAIR && rank == 1) {
       // the peer forwards "my B half landed" for each stage to rank 0's issuer
       if (lane == 0) {
         uint32_t ib = 0;
         for (uint32_t t = t_first; t < ntiles; t += t_step)
-          for (int s = 0; s < SH::NH * SH::KA; ++s, ++ib) {
+          for (int s = 0; s < SH::SPT; ++s, ++ib) {
+            if ((P.dbg & 1) && ib >= (uint32_t)SH::NB) break;
             const int sb = (int)(ib % SH::NB);
             mbar_wait(&b_full[sb], (ib / SH::NB) & 1);
             mbar_arrive_remote(&b_peer[sb], 0);
@@ -315,51 +334,66 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
       }
     } else if (lane == 0) {
       uint32_t ib = 0, u = 0, k = 0;
+      auto wait_stage = [&](uint32_t i) {
+        const int sb = (int)(i % SH::NB);
+        if ((!(P.dbg & 1) || i < (uint32_t)SH::NB) && !(P.dbg & 64)) {
+          mbar_wait(&b_full[sb], (i / SH::NB) & 1);
+          if constexpr (PAIR) mbar_wait(&b_peer[sb], (i / SH::NB) & 1);
+        }
+        return desc_sw128(smem_u32(sm + SH::B_OFF + (uint32_t)sb * SH::STAGE));
+      };
+      auto release_stage = [&](uint32_t i) {
+        if (!(P.dbg & 1)) tc_commit<PAIR>(&b_empty[i % SH::NB]);
+      };
+      auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+        if constexpr (PAIR)  // M = 256: A rows and B columns from both CTAs
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n"
+              :: "r"(d), "l"(a), "l"(b), "r"(idesc_f16(SH::NW, 2 * GM)), "r"(acc));
+        else
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n"
+              :: "r"(d), "l"(a), "l"(b), "r"(idesc_f16(SH::NW)), "r"(acc));
+      };
       for (uint32_t t = t_first; t < ntiles; t += t_step, ++k) {
         for (int nh = 0; nh < SH::NH; ++nh, ++u) {
-          const int db = (int)(u % SH::NBUF);
-          if (u >= (uint32_t)SH::NBUF) mbar_wait(&d_empty[db], ((u / SH::NBUF) - 1) & 1);
+          const int db = (int)(u & 1);
+          if (u >= 2 && !(P.dbg & 64)) mbar_wait(&d_empty[db], ((u >> 1) - 1) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
           if (nh == 0) GEMM_TRACE(k, 3);
-          const uint32_t dbig = tmem + (uint32_t)(db * 2 * SH::NW), dsmall = dbig + (uint32_t)SH::NW;
-          for (int ka = 0; ka < SH::KA; ++ka, ++ib) {
+          const uint32_t dacc = tmem + (uint32_t)(db * SH::ACC);
+#pragma unroll 1
+          for (int ka = 0; ka < SH::KA; ++ka, ib += 2) {  // correction terms
             const int as = (int)(k % SH::ABUF) * SH::KA + ka;
-            if (nh == 0) mbar_wait(&a_full[as], (k / SH::ABUF) & 1);
-            const int sb = (int)(ib % SH::NB);
-            mbar_wait(&b_full[sb], (ib / SH::NB) & 1);
-            if constexpr (PAIR) mbar_wait(&b_peer[sb], (ib / SH::NB) & 1);
+            if (nh == 0 && !(P.dbg & 64)) mbar_wait(&a_full[as], (k / SH::ABUF) & 1);
+            const uint64_t bhi = wait_stage(ib), blo = wait_stage(ib + 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
-            if (nh < 2 && ka < 4) GEMM_TRACE(k, 8 + nh * 4 + ka);
+            if (nh < 2 && ka < 2) GEMM_TRACE(k, 8 + nh * 4 + ka);
             // descriptors of the atom's / stage's first K step; the next K step (32 B further)
             // is +2 in the 16 B-unit start-address field (no carry: addresses < 2^18)
             const uint64_t ahi = desc_sw128(smem_u32(sm + SH::A_OFF + (uint32_t)as * 2 * ATOM_BYTES));
             const uint64_t alo = ahi + (ATOM_BYTES >> 4);
-            const uint64_t bhi = desc_sw128(smem_u32(sm + SH::B_OFF + (uint32_t)sb * SH::STAGE));
-            const uint64_t blo = bhi + (SH::STAGE / 2 >> 4);
-            // hi.hi accumulates into the big accumulator; the two correction terms (2^-11 of it)
-            // into the small one, so only 16 K steps per output round against the full-size sum
 #pragma unroll
             for (int j = 0; j < 4; ++j) {  // K = 16 fp16 = 32 B per instruction
               const uint64_t o = 2u * j;
-              const uint64_t da[3] = {alo + o, ahi + o, ahi + o};
-              const uint64_t dbd[3] = {bhi + o, blo + o, bhi + o};
-#pragma unroll
-              for (int term = 0; term < 3; ++term) {
-                const uint32_t acc = (ka | j | (term == 1)) ? 1u : 0u;
-                const uint32_t d = term < 2 ? dsmall : dbig;
-                if constexpr (PAIR)  // M = 256: A rows and B columns from both CTAs
-                  asm volatile(
-                      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n"
-                      :: "r"(d), "l"(da[term]), "l"(dbd[term]), "r"(idesc_f16(SH::NW, 2 * GM)), "r"(acc));
-                else
-                  asm volatile(
-                      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n"
-                      :: "r"(d), "l"(da[term]), "l"(dbd[term]), "r"(idesc_f16(SH::NW)), "r"(acc));
-              }
+              mma(dacc, alo + o, bhi + o, (ka | j) ? 1u : 0u);
+              mma(dacc, ahi + o, blo + o, 1u);
             }
-            tc_commit<PAIR>(&b_empty[sb]);
+            release_stage(ib);
+            release_stage(ib + 1);
+          }
+#pragma unroll 1
+          for (int ka = 0; ka < SH::KA; ++ka, ++ib) {  // main term
+            const int as = (int)(k % SH::ABUF) * SH::KA + ka;
+            const uint64_t bhi = wait_stage(ib);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            if (nh < 2 && ka < 2) GEMM_TRACE(k, 10 + nh * 4 + ka);
+            const uint64_t ahi = desc_sw128(smem_u32(sm + SH::A_OFF + (uint32_t)as * 2 * ATOM_BYTES));
+#pragma unroll
+            for (int j = 0; j < 4; ++j) mma(dacc, ahi + 2u * j, bhi + 2u * j, 1u);
+            release_stage(ib);
             if (nh == SH::NH - 1) tc_commit<PAIR>(&a_empty[as]);  // the slot may take a later tile's atom
           }
           tc_commit<PAIR>(&d_full[db]);
@@ -369,6 +403,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
     }
   } else if (warp == PF_WARP) {
     // ------------------------------------------------------------------ row prefetch --
+    regs_dec<REG_MISC>();
     // L2 prefetch (prefetch.global.L2, per 128 B line: the LSU path, so the B stage copies in
     // the bulk-copy engine never queue behind this HBM traffic) of the rows of the tile
     // PF_AHEAD steps ahead, paced by the split warps' progress (f_full: row maxima of tile k
@@ -393,18 +428,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
           for (int l = 0; l < NN / 32; ++l)
             asm volatile("prefetch.global.L2 [%0];" :: "l"(P.x + (size_t)id[i] * NN + l * 32) : "memory");
     };
+    if (!(P.dbg & 2)) {
     for (int a = 0; a < PF_AHEAD; ++a) prefetch_rows(t_first + (uint32_t)a * t_step);
     uint32_t k = 0;
     for (uint32_t t = t_first + PF_AHEAD * t_step; t < ntiles; t += t_step, ++k) {
       mbar_wait(&f_full[k & 3], (k >> 2) & 1);
       prefetch_rows(t);
     }
+    }
   } else if (warp == PROD_WARP) {
     // ------------------------------------------------------------------ B producer ----
-    // Lane 0: the B stages of each unit of each tile, in the MMA's order (unit outer, K atom
-    // inner), into the NB-stage ring.
-    // Global stages hold hi then lo of the unit's NW output columns; a CTA of a pair copies
-    // its NW / 2 rows of each (rows 64 rank ..), the layout cta_group::2 expects.
+    regs_dec<REG_MISC>();
+    // Lane 0: the B stages of each unit of each tile, in the MMA's order, into the NB-stage
+    // ring.
     if (lane == 0) {
       // global stages: [class][K atom][128-column half][hi | lo] (gemm_build)
       constexpr uint32_t GSTAGE = 2u * (NN < 128 ? NN : 128) * 128, PART = (uint32_t)SH::BW * 128;
@@ -416,31 +452,34 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
         uint32_t rows;
         tm.of(t, c, p0, rows);
         const unsigned char* src = P.bops + (size_t)c * SH::KA * GH * GSTAGE;
-        for (int nh = 0; nh < SH::NH; ++nh)
-          for (int ka = 0; ka < SH::KA; ++ka, ++ib) {
+        for (int s = 0; s < SH::SPT; ++s, ++ib) {
+            if ((P.dbg & 1) && ib >= (uint32_t)SH::NB) break;
             const int sb = (int)(ib % SH::NB);
             if (ib >= (uint32_t)SH::NB) mbar_wait(&b_empty[sb], ((ib / SH::NB) - 1) & 1);
             mbar_expect_tx(&b_full[sb], SH::STAGE);
             const uint32_t d = smem_u32(sm + SH::B_OFF + (uint32_t)sb * SH::STAGE);
-            if constexpr (WIDE) {  // this CTA's 128 of the 256 rows = global half-stage `rank`
-              const unsigned char* g = src + (size_t)(ka * SH::NH * 2 + rank) * GSTAGE;
-              asm volatile(
-                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                  :: "r"(d), "l"(g), "r"(SH::STAGE), "r"(smem_u32(&b_full[sb])) : "memory");
-            } else {
-              const unsigned char* g = src + (size_t)(ka * SH::NH + nh) * GSTAGE + rank * PART;
-              asm volatile(
-                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                  :: "r"(d), "l"(g), "r"(PART), "r"(smem_u32(&b_full[sb])) : "memory");
-              asm volatile(
-                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                  :: "r"(d + PART), "l"(g + GSTAGE / 2), "r"(PART), "r"(smem_u32(&b_full[sb])) : "memory");
-            }
+            // stage s of the tile: unit nh; per unit atom r / 2 hi / lo (r < 2 KA), then atom
+            // r - 2 KA hi. The unit's B rows of this CTA: with one N = 256 unit per tile and CTA
+            // pairs, global half `rank` (all its 128 rows); otherwise global half nh, rows from
+            // rank * BW (the layout cta_group::2 expects)
+            const int nh = s / (3 * SH::KA), r = s % (3 * SH::KA);
+            const int ka = r < 2 * SH::KA ? r >> 1 : r - 2 * SH::KA;
+            const int part = r < 2 * SH::KA ? (r & 1) : 0;
+            const int gh = (WIDE && NN == 256) ? (int)rank : nh;
+            const uint32_t roff = (WIDE && NN == 256) ? 0u : rank * PART;
+            const unsigned char* g = src + (size_t)(ka * GH + gh) * GSTAGE + (size_t)part * (GSTAGE / 2) + roff;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                :: "r"(d), "l"(g), "r"(SH::STAGE), "r"(smem_u32(&b_full[sb])) : "memory");
           }
       }
     }
+  } else if (warp > PF_WARP) {
+    // idle (completes the fourth warpgroup for the register rebalancing)
+    regs_dec<REG_MISC>();
   } else if (warp >= EPI_WARPS) {
     // ------------------------------------------------------------------ split warps ---
+    regs_inc<REG_SPLIT>();
     const int sw = warp - EPI_WARPS;
     const int g8 = lane >> 3, l8 = lane & 7;  // row within a 4-row group, lane within the row
     // Rows of 4-row group g: one 64-bit store instruction writes 64 B of each of its 4 rows
@@ -451,61 +490,53 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
       const int b16 = (sw * SH::RG + g) >> 2, gg = (sw * SH::RG + g) & 3;
       return b16 * 16 + (gg & 1) * 2 + (gg >> 1) * 8 + (g8 >> 1) + (g8 & 1) * 4;
     };
-    uint32_t k = 0;
-    for (uint32_t t = t_first; t < ntiles; t += t_step, ++k) {
+    // One pass per tile: each lane holds its 4 row groups x NN / 32 float4 of the tile in
+    // registers (the register rebalancing above gives the split warps room for a whole tile),
+    // so a row is read from memory once. The next tile's loads for K atom ka are issued as soon
+    // as this tile's atom ka is converted, so they are in flight while the split waits for the
+    // MMAs to release the A slots, and the row maxima of the next tile need no second read.
+    constexpr int NV = NN / 32;  // float4 per lane and row group: columns 32 i + 4 l8 .. + 3
+    float4 held[SH::RG][NV];
+    uint32_t rid[SH::RG];
+    auto tile_ids = [&](uint32_t t, uint32_t (&ids)[SH::RG]) {
+      if (t >= ntiles) {
+#pragma unroll
+        for (int g = 0; g < SH::RG; ++g) ids[g] = 0xffffffffu;
+        return;
+      }
       int c;
       uint64_t p0;
       uint32_t rows;
       tm.of(t, c, p0, rows);
-      if (sw == 0 && lane == 0) GEMM_TRACE(k, 0);
-      // pass 1 (overlaps the MMAs of the previous tile): row max -> power-of-two scale
-      float scl[SH::RG];
-      uint32_t rid[SH::RG];
 #pragma unroll
       for (int g = 0; g < SH::RG; ++g) {
         const int r = row_of_group(g);
-        rid[g] = (uint32_t)r < rows ? row_at(P, p0 + r) : 0xffffffffu;
+        ids[g] = (uint32_t)r < rows ? row_at(P, p0 + r) : 0xffffffffu;
       }
-      // Small rows (N = 64): pass 1 keeps the rows in registers (8 floats per lane and group)
-      // and pass 2 converts from them. Longer rows: pass 1 streams two groups at a time for the
-      // maxima and pass 2 re-reads each K atom (L2 hits), the next atom's loads in flight while
-      // the current one is converted.
-      constexpr int NV = NN / 32;                 // float4 per lane and row group
-      constexpr bool HOLD = SH::RG * NV <= 8;
-      float mxs[SH::RG];
-      float4 held[HOLD ? SH::RG : 1][HOLD ? NV : 1];
-      auto load_group = [&](int g, float4 (&v)[NV]) {
-        const uint32_t id = rid[g];
-        const float4* src = reinterpret_cast<const float4*>(P.x + (size_t)(id != 0xffffffffu ? id : 0u) * NN);
+    };
+    auto load_part = [&](const uint32_t (&ids)[SH::RG], int i) {  // float4 i of every row group
 #pragma unroll
-        for (int i = 0; i < NV; ++i)
-          v[i] = id != 0xffffffffu ? __ldcg(src + i * 8 + l8) : make_float4(0.f, 0.f, 0.f, 0.f);
-      };
-      auto group_max = [&](const float4 (&v)[NV]) {
+      for (int g = 0; g < SH::RG; ++g)
+        held[g][i] = ids[g] != 0xffffffffu
+                         ? __ldcs(reinterpret_cast<const float4*>(P.x + (size_t)ids[g] * NN) + i * 8 + l8)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
+    tile_ids(t_first, rid);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) load_part(rid, i);
+    uint32_t k = 0;
+    for (uint32_t t = t_first; t < ntiles; t += t_step, ++k) {
+      if (sw == 0 && lane == 0) GEMM_TRACE(k, 0);
+      uint32_t rnext[SH::RG];
+      tile_ids(t + t_step, rnext);
+      // row max -> power-of-two scale
+      float scl[SH::RG];
+#pragma unroll
+      for (int g = 0; g < SH::RG; ++g) {
         float mx = 0.f;
 #pragma unroll
         for (int i = 0; i < NV; ++i)
-          mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[i].x), fabsf(v[i].y)), fmaxf(fabsf(v[i].z), fabsf(v[i].w))));
-        return mx;
-      };
-      if constexpr (HOLD) {
-#pragma unroll
-        for (int g = 0; g < SH::RG; ++g) load_group(g, held[g]);
-#pragma unroll
-        for (int g = 0; g < SH::RG; ++g) mxs[g] = group_max(held[g]);
-      } else {
-#pragma unroll
-        for (int g0 = 0; g0 < SH::RG; g0 += 2) {  // two row groups' loads in flight at a time
-          float4 v[2][NV];
-          load_group(g0, v[0]);
-          load_group(g0 + 1, v[1]);
-          mxs[g0] = group_max(v[0]);
-          mxs[g0 + 1] = group_max(v[1]);
-        }
-      }
-#pragma unroll
-      for (int g = 0; g < SH::RG; ++g) {
-        float mx = mxs[g];
+          mx = fmaxf(mx, fmaxf(fmaxf(fabsf(held[g][i].x), fabsf(held[g][i].y)), fmaxf(fabsf(held[g][i].z), fabsf(held[g][i].w))));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
@@ -522,34 +553,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
         __syncwarp();
         if (lane == 0) mbar_arrive(&f_full[fb]);
       }
-      // pass 2: each K atom's 64 columns of every row -> fp16 hi / lo, written as soon as the
-      // slot's previous atom was read by the MMAs; one a_full arrival per atom so the MMAs
-      // follow closely
-      auto load_atom = [&](int ka, float4 (&va)[SH::RG][2]) {
+      // each K atom's 64 columns of every row -> fp16 hi / lo, written as soon as the slot's
+      // previous atom was read by the MMAs; one a_full arrival per atom
 #pragma unroll
-        for (int g = 0; g < SH::RG; ++g)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {  // columns 64 ka + 32 h + 4 l8 .. +3
-            if constexpr (HOLD) {
-              va[g][h] = held[g][2 * ka + h];
-            } else {
-              va[g][h] = rid[g] != 0xffffffffu
-                             ? __ldcs(reinterpret_cast<const float4*>(P.x + (size_t)rid[g] * NN + 64 * ka + 32 * h) + l8)
-                             : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-          }
-      };
-      float4 vnext[SH::RG][2];
-      load_atom(0, vnext);
-#pragma unroll 1
       for (int ka = 0; ka < SH::KA; ++ka) {
-        float4 va[SH::RG][2];
-#pragma unroll
-        for (int g = 0; g < SH::RG; ++g) {
-          va[g][0] = vnext[g][0];
-          va[g][1] = vnext[g][1];
-        }
-        if (ka + 1 < SH::KA) load_atom(ka + 1, vnext);
         const int as = (int)(k % SH::ABUF) * SH::KA + ka;
         if (k >= (uint32_t)SH::ABUF) mbar_wait(&a_empty[as], ((k / SH::ABUF) - 1) & 1);
         unsigned char* ahi = sm + SH::A_OFF + (uint32_t)as * 2 * ATOM_BYTES;
@@ -559,9 +566,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
           const int r = row_of_group(g);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const float4* v = va[g];
+            const float4 v = held[g][2 * ka + h];
             const float s = scl[g];
-            const float a0 = v[h].x * s, a1 = v[h].y * s, a2 = v[h].z * s, a3 = v[h].w * s;
+            const float a0 = v.x * s, a1 = v.y * s, a2 = v.z * s, a3 = v.w * s;
             const uint32_t h01 = pack_h2(a0, a1), h23 = pack_h2(a2, a3);
             const float2 b01 = unpack_h2(h01), b23 = unpack_h2(h23);
             const uint32_t l01 = pack_h2(a0 - b01.x, a1 - b01.y), l23 = pack_h2(a2 - b23.x, a3 - b23.y);
@@ -576,6 +583,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
         if (lane == 0) {
           if constexpr (PAIR) mbar_arrive_remote(&a_full[as], 0); else mbar_arrive(&a_full[as]);
         }
+        load_part(rnext, 2 * ka);  // the next tile's atom ka, in flight from here
+        load_part(rnext, 2 * ka + 1);
       }
       if (sw == 0 && lane == 0) GEMM_TRACE(k, 2);
     }
@@ -592,20 +601,30 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
     }
   } else {
     // ------------------------------------------------------------------ epilogue ------
+    // Thread = row (TMEM lane). Per 32-column block: tcgen05.ld (the next block's load in
+    // flight), unscale, swizzled staging [32 rows][32 floats], then coalesced 128-bit stores
+    // (8 lanes per row, 4 rows per instruction). Energy: each lane squares its 4 columns of
+    // 8 rows in fp32, a shuffle reduce-scatter over the 4 row groups (fp32 partials of 16
+    // rows, merged exactly) leaves every lane one column of the block summed over the warp's
+    // 32 rows, added to a per-lane compensated fp32 accumulator per block; flushed in fp64
+    // with atomics when the class changes.
+    regs_dec<REG_EPI>();
     unsigned char* stg = sm + SH::STG_OFF + (uint32_t)warp * SH::STG_BYTES;
-    double* en = reinterpret_cast<double*>(sm + SH::EN_OFF) + (size_t)warp * NN;
-    if (ENERGY)
-      for (int i = lane; i < NN; i += 32) en[i] = 0.0;
+    // the column of a block whose energy this lane accumulates (see the reduce-scatter below)
+    const int en_col = 4 * (lane & 7) + ((lane >> 3) & 1) * 2 + ((lane >> 4) & 1);
+    constexpr int NCT = NN / 32;  // column blocks per row
+    float ks[ENERGY ? NCT : 1], kc[ENERGY ? NCT : 1];  // per column block: compensated sum (value, error)
+#pragma unroll
+    for (int i = 0; i < (ENERGY ? NCT : 1); ++i) ks[i] = kc[i] = 0.f;
     int en_class = -1;
     auto flush_energy = [&]() {
       if (ENERGY && en_class >= 0) {
-        __syncwarp();
-        for (int i = lane; i < NN; i += 32) {
-          const double v = en[i];
-          if (v != 0.0) atomicAdd(P.energy + (size_t)en_class * NN + i, v);
-          en[i] = 0.0;
+#pragma unroll
+        for (int i = 0; i < NCT; ++i) {
+          const double v = (double)ks[i] + (double)kc[i];
+          if (v != 0.0) atomicAdd(P.energy + (size_t)en_class * NN + i * 32 + en_col, v);
+          ks[i] = kc[i] = 0.f;
         }
-        __syncwarp();
       }
     };
     uint32_t k = 0, u = 0;
@@ -629,23 +648,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
         const int r = warp * 32 + 4 * i + (lane >> 3);
         orow[i] = (uint32_t)r < rows ? row_at(P, p0 + r) : 0xffffffffu;
       }
+#pragma unroll
       for (int nh = 0; nh < SH::NH; ++nh, ++u) {
-        const int db = (int)(u % SH::NBUF);
-        mbar_wait(&d_full[db], (u / SH::NBUF) & 1);
+        const int db = (int)(u & 1);
+        mbar_wait(&d_full[db], (u >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         if (nh == 0 && warp == 0 && lane == 0) GEMM_TRACE(k, 5);
-        // TMEM -> registers for column block cb (big at the unit's buffer, small NW after it)
-        uint32_t v[32], w[32];
+        // TMEM -> registers for column block cb of the unit's accumulator
+        uint32_t v[32];
         auto tmem_load = [&](int cb) {
-          const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(db * 2 * SH::NW + cb * 32);
-          asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-              "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-              : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]),
-                "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]), "=r"(w[15]),
-                "=r"(w[16]), "=r"(w[17]), "=r"(w[18]), "=r"(w[19]), "=r"(w[20]), "=r"(w[21]), "=r"(w[22]), "=r"(w[23]),
-                "=r"(w[24]), "=r"(w[25]), "=r"(w[26]), "=r"(w[27]), "=r"(w[28]), "=r"(w[29]), "=r"(w[30]), "=r"(w[31])
-              : "r"(taddr + (uint32_t)SH::NW));
+          const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(db * SH::ACC + cb * 32);
           asm volatile(
               "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
               "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -666,50 +678,64 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
         tmem_load(0);
         asm volatile("tcgen05.wait::ld.sync.aligned;");
         if (NCB == 1) release();
-        for (int cb = 0; cb < NCB; ++cb) {
-          // big + small, unscale, then thread-per-row -> swizzled staging [32 rows][32 floats]
-          auto acc_at = [&](int i) { return (__uint_as_float(v[i]) + __uint_as_float(w[i])) * f_row; };
+        if (P.dbg & 32) {  // diagnostic: accumulators released unread
+          if (NCB > 1) release();
+          continue;
+        }
+#pragma unroll
+        for (int cb = 0; cb < NCB; ++cb) {  // unrolled: the energy accumulators are indexed by constants
+          float o[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(v[i]) * f_row;
+          if (cb + 1 < NCB) tmem_load(cb + 1);  // in flight while this block is stored
 #pragma unroll
           for (int q = 0; q < 8; ++q)
-            *reinterpret_cast<float4*>(stg + swz(lane, q)) =
-                make_float4(acc_at(4 * q), acc_at(4 * q + 1), acc_at(4 * q + 2), acc_at(4 * q + 3));
-          if (cb + 1 < NCB) tmem_load(cb + 1);  // in flight while this block is stored
+            *reinterpret_cast<float4*>(stg + swz(lane, q)) = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
           __syncwarp();
           // coalesced: 8 lanes per row, 4 rows per instruction
           const int col0 = nh * SH::NW + cb * 32;
-          float e0 = 0.f, e1 = 0.f, e2 = 0.f, e3 = 0.f;
+          // all 8 staging reads into distinct registers first, then the predicated stores: a
+          // per-row branch around load + store + energy serialises on the reused registers
+          float4 ov[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int rr = 4 * i + (lane >> 3);
-            const float4 o = *reinterpret_cast<const float4*>(stg + swz(rr, lane & 7));
-            if (orow[i] != 0xffffffffu) {
-              __stcs(reinterpret_cast<float4*>(P.y + (size_t)orow[i] * NN + col0) + (lane & 7), o);
-              if (ENERGY) {
-                e0 = fmaf(o.x, o.x, e0);
-                e1 = fmaf(o.y, o.y, e1);
-                e2 = fmaf(o.z, o.z, e2);
-                e3 = fmaf(o.w, o.w, e3);
-              }
+          for (int i = 0; i < 8; ++i) ov[i] = *reinterpret_cast<const float4*>(stg + swz(4 * i + (lane >> 3), lane & 7));
+          // rows past the tile's end are exact zeros (their A rows are zero): no predicate needed;
+          // squared before the stores, so no register the stores still read is overwritten
+          float e0 = 0.f, e1 = 0.f, e2 = 0.f, e3 = 0.f;
+          if constexpr (ENERGY) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              e0 = fmaf(ov[i].x, ov[i].x, e0);
+              e1 = fmaf(ov[i].y, ov[i].y, e1);
+              e2 = fmaf(ov[i].z, ov[i].z, e2);
+              e3 = fmaf(ov[i].w, ov[i].w, e3);
             }
+          }
+          if (!(P.dbg & 16)) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (orow[i] != 0xffffffffu) __stcs(reinterpret_cast<float4*>(P.y + (size_t)orow[i] * NN + col0) + (lane & 7), ov[i]);
           }
           __syncwarp();  // staging reads done before the next column block overwrites it
-          if (ENERGY) {  // fp32 sums of 8 rows, then fp64 across the warp's 4 row groups
-            double d0 = e0, d1 = e1, d2 = e2, d3 = e3;
-#pragma unroll
-            for (int o = 8; o < 32; o <<= 1) {
-              d0 += __shfl_xor_sync(0xffffffffu, d0, o);
-              d1 += __shfl_xor_sync(0xffffffffu, d1, o);
-              d2 += __shfl_xor_sync(0xffffffffu, d2, o);
-              d3 += __shfl_xor_sync(0xffffffffu, d3, o);
-            }
-            if (lane < 8) {
-              double* e = en + col0 + lane * 4;
-              e[0] += d0;
-              e[1] += d1;
-              e[2] += d2;
-              e[3] += d3;
-            }
+          if constexpr (ENERGY) {
+            // lanes l and l ^ 8 (row groups g, g ^ 1) keep columns {0,1} / {2,3} of their four
+            // (fp32 partials of 16 rows), then l and l ^ 16 keep one of the two: their exact sum
+            // (TwoSum) is added to the lane's compensated fp32 accumulator of that column (fp64
+            // is only used at the class flush: fp64 adds here stall on the fp64 pipe)
+            const bool h1 = (lane >> 3) & 1, h2 = (lane >> 4) & 1;
+            const float sa = h1 ? e0 : e2, sb = h1 ? e1 : e3;
+            const float ka = (h1 ? e2 : e0) + __shfl_xor_sync(0xffffffffu, sa, 8);
+            const float kb = (h1 ? e3 : e1) + __shfl_xor_sync(0xffffffffu, sb, 8);
+            const float mine = h2 ? kb : ka;
+            const float other = __shfl_xor_sync(0xffffffffu, h2 ? ka : kb, 16);
+            const float t = mine + other, tb = t - mine;
+            const float te = (mine - (t - tb)) + (other - tb);  // t + te == mine + other exactly
+            const int ci = nh * NCB + cb;
+            const float sn = ks[ci] + t, sbp = sn - ks[ci];
+            kc[ci] += ((ks[ci] - (sn - sbp)) + (t - sbp)) + te;
+            ks[ci] = sn;
           }
+          if (warp == 0 && lane == 0 && nh == 0 && (cb & 1) == 0 && cb < 8) GEMM_TRACE(k, 12 + (cb >> 1));
           if (cb + 1 < NCB) {
             asm volatile("tcgen05.wait::ld.sync.aligned;");
             if (cb + 2 == NCB) release();
@@ -763,8 +789,8 @@ double half_to_double(uint16_t h) {
 
 int gemm_smem_bytes(int n) {
   switch (n) {
-    case 64: return (int)Shape<64, true, false>::SMEM;
-    case 128: return (int)Shape<128, true, false>::SMEM;
+    case 64: return (int)std::max(Shape<64, true, true>::SMEM, Shape<64, true, false>::SMEM);
+    case 128: return (int)std::max(Shape<128, true, true>::SMEM, Shape<128, true, false>::SMEM);
     case 256: return (int)Shape<256, true, true>::SMEM;
     default: return 0;
   }
@@ -860,9 +886,12 @@ int launch_one(const GemmParams& P, int num_sms, cudaStream_t st) {
 }
 template <int NN>
 int launch_n(const GemmParams& P, int grid, bool pair, bool wide, cudaStream_t st) {
-  if constexpr (NN == 256) {
-    if (pair && wide)
-      return P.energy ? launch_one<NN, true, true, true>(P, grid, st) : launch_one<NN, false, true, true>(P, grid, st);
+  // wide: one unit of all N columns per tile, merged accumulator (N = 256 only with CTA pairs)
+  if (pair && wide)
+    return P.energy ? launch_one<NN, true, true, true>(P, grid, st) : launch_one<NN, false, true, true>(P, grid, st);
+  if constexpr (NN <= 128) {
+    if (wide)
+      return P.energy ? launch_one<NN, true, false, true>(P, grid, st) : launch_one<NN, false, false, true>(P, grid, st);
   }
   if (pair) return P.energy ? launch_one<NN, true, true, false>(P, grid, st) : launch_one<NN, false, true, false>(P, grid, st);
   return P.energy ? launch_one<NN, true, false, false>(P, grid, st) : launch_one<NN, false, false, false>(P, grid, st);
@@ -876,6 +905,7 @@ int gemm_run(const GemmOperands& g, const float* x, float* y, const uint32_t* id
   if (!count) return HYGT_OK;
   GemmParams P{};
   P.trace = g_gemm_trace;
+  P.dbg = g.dbg;
   P.x = x;
   P.y = y;
   P.idx = idx;

@@ -20,13 +20,17 @@ struct GemmParams {
   const float* unscale;      // [C] 2^-kB
   double* energy;            // [C][N] fp64 (forward with energy) or nullptr
   unsigned long long* trace; // debug: per-tile clock64 events of CTA 0 ([64][16]) or nullptr
+  int dbg;                   // diagnostic switches (knob HYGT_GEMM_DBG; wrong results when set)
 };
 
 struct GemmOperands {  // one direction
   int n = 0, classes = 0, num_sms = 148;
   bool pair = true;  // CTA pairs (tcgen05 cta_group::2, M = 256): each SM streams half of B
-  bool wide = false;  // N = 256 with pairs: one N = 256 unit per tile (A read from smem half as often,
-                      // but the single-buffered accumulator serialises the epilogue: slower)
+  int dbg = 0;
+  // wide: one unit of all N output columns per tile (N = 256 needs pairs) and one accumulator,
+  // the correction terms of all K accumulated before the main term; otherwise units of <= 128
+  // columns with separate main / correction accumulators
+  bool wide = true;
   unsigned char* d_ops = nullptr;
   float* d_unscale = nullptr;
 };

@@ -15,7 +15,11 @@ from paper_2505_21728_b200.synth import make_workload  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=5)
 ap.add_argument("--inverse", action="store_true")
+ap.add_argument("--energy", action="store_true")
+ap.add_argument("--knob", action="append", default=[])
 a = ap.parse_args()
+for kv in a.knob:
+    L.set_knob(kv.split("=")[0], int(kv.split("=")[1]))
 w = make_workload(a.config)
 rows = w.cfg.count
 cls = w.make_classes(rows)
@@ -28,7 +32,11 @@ tr = torch.zeros(64 * 16, dtype=torch.int64, device="cuda")
 lib = L.lib()
 lib.hygt_debug_gemm_trace.argtypes = [C.c_void_p]
 lib.hygt_debug_gemm_trace(tr.data_ptr())
-(plan.inverse if a.inverse else plan.forward)(x, cls, out=y, workspace=ws)
+if a.energy:
+    en = torch.zeros(w.cfg.classes, w.n, dtype=torch.float64, device="cuda")
+    plan.forward_energy(x, cls, en, out=y, workspace=ws)
+else:
+    (plan.inverse if a.inverse else plan.forward)(x, cls, out=y, workspace=ws)
 torch.cuda.synchronize()
 lib.hygt_debug_gemm_trace(None)
 t = tr.view(64, 16).cpu().numpy()

@@ -17,7 +17,12 @@ from paper_2505_21728_b200.synth import make_workload  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=5)
 ap.add_argument("--rows", type=int, default=1 << 14)
+ap.add_argument("--knob", action="append", default=[])
+ap.add_argument("--kernels", default="butterfly,tensor")
 a = ap.parse_args()
+import paper_2505_21728_b200._lib as L  # noqa: E402
+for kv in a.knob:
+    L.set_knob(kv.split("=")[0], int(kv.split("=")[1]))
 w = make_workload(a.config)
 cls = w.make_classes(a.rows)
 x = w.make_rows(a.rows, cls)
@@ -35,7 +40,7 @@ def err(y, r):
     return {"rel_l2": float(np.linalg.norm(e) / np.linalg.norm(r)), "max_abs_over_max_x": float(np.abs(e).max() / np.abs(xh).max())}
 
 
-for kernel in ("butterfly", "tensor"):
+for kernel in a.kernels.split(","):
     plan = HyGTPlan(w.models, w.perms, kernel=kernel)
     y = plan.forward(x, cls)
     z = plan.inverse(x, cls)
