@@ -90,7 +90,10 @@ struct Shape {
   // the MMA order (per unit: per atom hi, lo for the correction terms, then hi again for the
   // main term): SPT stages per tile
   static constexpr uint32_t STAGE = (uint32_t)BW * 128;
-  static constexpr int NB = STAGE <= 8192 ? 8 : 4;  // B ring stages
+  // N = 256: the epilogue stores straight from tcgen05.ld.16x256b fragments (no staging), which
+  // leaves room for a fifth B stage; N <= 128 stages through shared memory (faster there)
+  static constexpr bool DIRECT = NN == 256;
+  static constexpr int NB = STAGE <= 8192 ? 8 : (DIRECT ? 5 : 4);  // B ring stages
   static constexpr int SPT = 3 * KA * NH;
   static constexpr int TG = PAIR ? 2 * GM : GM;      // rows per tile (a CTA pair: 128 each)
   static constexpr int ABUF = KA <= 2 ? 2 : 1;       // tiles of A resident (double-buffered if small)
@@ -98,7 +101,7 @@ struct Shape {
   static constexpr uint32_t A_OFF = 0;               // A: AS atoms (hi + lo each)
   static constexpr uint32_t B_OFF = A_OFF + AS * 2 * ATOM_BYTES;
   static constexpr uint32_t STG_OFF = B_OFF + NB * STAGE;
-  static constexpr uint32_t STG_BYTES = 32 * 128;    // per epilogue warp: 32 rows x 32 floats (swizzled)
+  static constexpr uint32_t STG_BYTES = DIRECT ? 0 : 32 * 128;  // per epilogue warp: 32 rows x 32 floats (swizzled)
   static constexpr uint32_t FAC_OFF = STG_OFF + EPI_WARPS * STG_BYTES;
   static constexpr uint32_t BAR_OFF = FAC_OFF + 4 * GM * 4;
   static constexpr uint32_t SMEM = BAR_OFF + 512;  // barriers (<= 40 x 8 B) + the TMEM address
@@ -612,156 +615,312 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
       }
     }
   } else {
-    // ------------------------------------------------------------------ epilogue ------
-    // Thread = row (TMEM lane). Per 32-column block: tcgen05.ld (the next block's load in
-    // flight), unscale, swizzled staging [32 rows][32 floats], then coalesced 128-bit stores
-    // (8 lanes per row, 4 rows per instruction). Energy: each lane squares its 4 columns of
-    // 8 rows in fp32, a shuffle reduce-scatter over the 4 row groups (fp32 partials of 16
-    // rows, merged exactly) leaves every lane one column of the block summed over the warp's
-    // 32 rows, added to a per-lane compensated fp32 accumulator per block; flushed in fp64
-    // with atomics when the class changes.
-    regs_dec<REG_EPI>();
-    unsigned char* stg = sm + SH::STG_OFF + (uint32_t)warp * SH::STG_BYTES;
-    // the column of a block whose energy this lane accumulates (see the reduce-scatter below)
-    const int en_col = 4 * (lane & 7) + ((lane >> 3) & 1) * 2 + ((lane >> 4) & 1);
-    constexpr int NCT = NN / 32;  // column blocks per row
-    float ks[ENERGY ? NCT : 1], kc[ENERGY ? NCT : 1];  // per column block: compensated sum (value, error)
-#pragma unroll
-    for (int i = 0; i < (ENERGY ? NCT : 1); ++i) ks[i] = kc[i] = 0.f;
-    int en_class = -1;
-    auto flush_energy = [&]() {
-      if (ENERGY && en_class >= 0) {
-#pragma unroll
-        for (int i = 0; i < NCT; ++i) {
-          const double v = (double)ks[i] + (double)kc[i];
-          if (v != 0.0) atomicAdd(P.energy + (size_t)en_class * NN + i * 32 + en_col, v);
-          ks[i] = kc[i] = 0.f;
-        }
-      }
-    };
-    uint32_t k = 0, u = 0;
-    for (uint32_t t = t_first; t < ntiles; t += t_step, ++k) {
-      int c;
-      uint64_t p0;
-      uint32_t rows;
-      tm.of(t, c, p0, rows);
-      if (ENERGY && c != en_class) {
-        flush_energy();
-        en_class = c;
-      }
-      mbar_wait(&f_full[k & 3], (k >> 2) & 1);
-      const float f_row = fac[(k & 3) * GM + warp * 32 + lane] * __ldg(P.unscale + c);  // TMEM lane = row
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&f_empty[k & 3]);
-      // row ids of the 4-row groups this lane stores (rows warp*32 + 4 i + lane/8)
-      uint32_t orow[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int r = warp * 32 + 4 * i + (lane >> 3);
-        orow[i] = (uint32_t)r < rows ? row_at(P, p0 + r) : 0xffffffffu;
-      }
-#pragma unroll
-      for (int nh = 0; nh < SH::NH; ++nh, ++u) {
-        const int db = (int)(u & 1);
-        mbar_wait(&d_full[db], (u >> 1) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        if (nh == 0 && warp == 0 && lane == 0) GEMM_TRACE(k, 5);
-        // TMEM -> registers for column block cb of the unit's accumulator
-        uint32_t v[32];
-        auto tmem_load = [&](int cb) {
-          const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(db * SH::ACC + cb * 32);
-          asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-              "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-                "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-                "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-              : "r"(taddr));
-        };
-        constexpr int NCB = SH::NW / 32;
-        auto release = [&]() {  // unit accumulators fully read: release them to unit u + NBUF
-          asm volatile("tcgen05.fence::before_thread_sync;");
-          __syncwarp();
-          if (lane == 0) {
-            if constexpr (PAIR) mbar_arrive_remote(&d_empty[db], 0); else mbar_arrive(&d_empty[db]);
+    if constexpr (SH::DIRECT) {
+      // ------------------------------------------------------------------ epilogue ------
+      // No staging: per 32-column block two tcgen05.ld.16x256b.x4 (lanes +0 and +16 of the
+      // warp's quadrant; the next block's loads in flight) give thread t rows q0 + t/4 + {0, 8,
+      // 16, 24} and columns 8 j + 2 (t % 4) + {0, 1} (j < 4): every STG.64 writes 8 rows x 32 B,
+      // whole sectors, straight from registers. Energy: each thread sums its 8 columns over its
+      // 4 rows in fp32; a shuffle reduce-scatter over the 8 row groups (fp32 partials of 16 rows,
+      // the last merge exact) leaves every lane one column of the block summed over the warp's
+      // 32 rows, added to a per-lane compensated fp32 accumulator per block; flushed in fp64
+      // with atomics when the class changes.
+      regs_dec<REG_EPI>();
+      const int tq = lane & 3, tg = lane >> 2;  // column pair, row group
+      // the column of a block whose energy this lane accumulates (see the reduce-scatter below)
+      const int en_col = 8 * (2 * ((lane >> 2) & 1) + ((lane >> 3) & 1)) + 2 * tq + ((lane >> 4) & 1);
+      constexpr int NCT = NN / 32;  // column blocks per row
+      float ks[ENERGY ? NCT : 1], kc[ENERGY ? NCT : 1];  // per column block: compensated sum (value, error)
+  #pragma unroll
+      for (int i = 0; i < (ENERGY ? NCT : 1); ++i) ks[i] = kc[i] = 0.f;
+      int en_class = -1;
+      auto flush_energy = [&]() {
+        if (ENERGY && en_class >= 0) {
+  #pragma unroll
+          for (int i = 0; i < NCT; ++i) {
+            const double v = (double)ks[i] + (double)kc[i];
+            if (v != 0.0) atomicAdd(P.energy + (size_t)en_class * NN + i * 32 + en_col, v);
+            ks[i] = kc[i] = 0.f;
           }
-        };
-        tmem_load(0);
-        asm volatile("tcgen05.wait::ld.sync.aligned;");
-        if (NCB == 1) release();
-        if (P.dbg & 32) {  // diagnostic: accumulators released unread
-          if (NCB > 1) release();
-          continue;
         }
-#pragma unroll
-        for (int cb = 0; cb < NCB; ++cb) {  // unrolled: the energy accumulators are indexed by constants
-          float o[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(v[i]) * f_row;
-          if (cb + 1 < NCB) tmem_load(cb + 1);  // in flight while this block is stored
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            *reinterpret_cast<float4*>(stg + swz(lane, q)) = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
-          __syncwarp();
-          // coalesced: 8 lanes per row, 4 rows per instruction
-          const int col0 = nh * SH::NW + cb * 32;
-          // all 8 staging reads into distinct registers first, then the predicated stores: a
-          // per-row branch around load + store + energy serialises on the reused registers
-          float4 ov[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) ov[i] = *reinterpret_cast<const float4*>(stg + swz(4 * i + (lane >> 3), lane & 7));
-          // rows past the tile's end are exact zeros (their A rows are zero): no predicate needed;
-          // squared before the stores, so no register the stores still read is overwritten
-          float e0 = 0.f, e1 = 0.f, e2 = 0.f, e3 = 0.f;
-          if constexpr (ENERGY) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              e0 = fmaf(ov[i].x, ov[i].x, e0);
-              e1 = fmaf(ov[i].y, ov[i].y, e1);
-              e2 = fmaf(ov[i].z, ov[i].z, e2);
-              e3 = fmaf(ov[i].w, ov[i].w, e3);
+      };
+      uint32_t k = 0, u = 0;
+      for (uint32_t t = t_first; t < ntiles; t += t_step, ++k) {
+        int c;
+        uint64_t p0;
+        uint32_t rows;
+        tm.of(t, c, p0, rows);
+        if (ENERGY && c != en_class) {
+          flush_energy();
+          en_class = c;
+        }
+        // this thread's rows: warp * 32 + tg + 8 i (i < 4)
+        mbar_wait(&f_full[k & 3], (k >> 2) & 1);
+        const float ucls = __ldg(P.unscale + c);
+        float frow[4];
+        uint32_t orow[4];
+  #pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = warp * 32 + tg + 8 * i;
+          frow[i] = fac[(k & 3) * GM + r] * ucls;
+          orow[i] = (uint32_t)r < rows ? row_at(P, p0 + r) : 0xffffffffu;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&f_empty[k & 3]);
+  #pragma unroll
+        for (int nh = 0; nh < SH::NH; ++nh, ++u) {
+          const int db = (int)(u & 1);
+          mbar_wait(&d_full[db], (u >> 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          if (nh == 0 && warp == 0 && lane == 0) GEMM_TRACE(k, 5);
+          // TMEM -> registers for column block cb of the unit's accumulator: v[h][4 j + m],
+          // m = 0, 1: row tg + 16 h, columns 8 j + 2 tq + m; m = 2, 3: row tg + 8 + 16 h
+          uint32_t v[2][16];
+          auto tmem_load = [&](int cb) {
+  #pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const uint32_t taddr = tmem + ((uint32_t)(warp * 32 + 16 * h) << 16) + (uint32_t)(db * SH::ACC + cb * 32);
+              asm volatile(
+                  "tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                  : "=r"(v[h][0]), "=r"(v[h][1]), "=r"(v[h][2]), "=r"(v[h][3]), "=r"(v[h][4]), "=r"(v[h][5]),
+                    "=r"(v[h][6]), "=r"(v[h][7]), "=r"(v[h][8]), "=r"(v[h][9]), "=r"(v[h][10]), "=r"(v[h][11]),
+                    "=r"(v[h][12]), "=r"(v[h][13]), "=r"(v[h][14]), "=r"(v[h][15])
+                  : "r"(taddr));
+            }
+          };
+          constexpr int NCB = SH::NW / 32;
+          auto release = [&]() {  // unit accumulator fully read: release it to unit u + 2
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) {
+              if constexpr (PAIR) mbar_arrive_remote(&d_empty[db], 0); else mbar_arrive(&d_empty[db]);
+            }
+          };
+          tmem_load(0);
+          asm volatile("tcgen05.wait::ld.sync.aligned;");
+          if (NCB == 1) release();
+          if (P.dbg & 32) {  // diagnostic: accumulators released unread
+            if (NCB > 1) release();
+            continue;
+          }
+  #pragma unroll
+          for (int cb = 0; cb < NCB; ++cb) {  // unrolled: the energy accumulators are indexed by constants
+            // o[i][j][m]: row slot i (row tg + 8 i), column 8 j + 2 tq + m
+            float o[4][4][2];
+  #pragma unroll
+            for (int h = 0; h < 2; ++h)
+  #pragma unroll
+              for (int j = 0; j < 4; ++j)
+  #pragma unroll
+                for (int m = 0; m < 2; ++m) {
+                  o[2 * h][j][m] = __uint_as_float(v[h][4 * j + m]) * frow[2 * h];
+                  o[2 * h + 1][j][m] = __uint_as_float(v[h][4 * j + 2 + m]) * frow[2 * h + 1];
+                }
+            if (cb + 1 < NCB) tmem_load(cb + 1);  // in flight while this block is stored
+            const int col0 = nh * SH::NW + cb * 32;
+            if (!(P.dbg & 16)) {
+  #pragma unroll
+              for (int i = 0; i < 4; ++i)
+                if (orow[i] != 0xffffffffu) {
+                  float* dst = P.y + (size_t)orow[i] * NN + col0 + 2 * tq;
+  #pragma unroll
+                  for (int j = 0; j < 4; ++j) __stcs(reinterpret_cast<float2*>(dst + 8 * j), make_float2(o[i][j][0], o[i][j][1]));
+                }
+            }
+            if constexpr (ENERGY) {
+              // rows past the tile's end are exact zeros (their A rows are zero): no predicate.
+              // q[2 j + m]: column 8 j + 2 tq + m over this thread's 4 rows
+              float q[8];
+  #pragma unroll
+              for (int j = 0; j < 4; ++j)
+  #pragma unroll
+                for (int m = 0; m < 2; ++m)
+                  q[2 * j + m] = fmaf(o[0][j][m], o[0][j][m], fmaf(o[1][j][m], o[1][j][m],
+                                 fmaf(o[2][j][m], o[2][j][m], o[3][j][m] * o[3][j][m])));
+              // reduce-scatter over the row groups (lane bits 2, 3: fp32, 16 rows), then bit 4
+              // (exact merge): lane keeps index 4 b2 + 2 b3 + b4 = column en_col
+  #pragma unroll
+              for (int w = 4; w >= 2; w >>= 1) {
+                const bool up = (lane >> (w == 4 ? 2 : 3)) & 1;
+  #pragma unroll
+                for (int i = 0; i < w; ++i) {
+                  const float send = up ? q[i] : q[i + w];
+                  const float keep = up ? q[i + w] : q[i];
+                  q[i] = keep + __shfl_xor_sync(0xffffffffu, send, w == 4 ? 4 : 8);
+                }
+              }
+              const bool up = (lane >> 4) & 1;
+              const float mine = up ? q[1] : q[0];
+              const float other = __shfl_xor_sync(0xffffffffu, up ? q[0] : q[1], 16);
+              const float ts = mine + other, tb = ts - mine;
+              const float te = (mine - (ts - tb)) + (other - tb);  // ts + te == mine + other exactly
+              const int ci = nh * NCB + cb;
+              const float sn = ks[ci] + ts, sbp = sn - ks[ci];
+              kc[ci] += ((ks[ci] - (sn - sbp)) + (ts - sbp)) + te;
+              ks[ci] = sn;
+            }
+            if (warp == 0 && lane == 0 && nh == 0 && (cb & 1) == 0 && cb < 8) GEMM_TRACE(k, 12 + (cb >> 1));
+            if (cb + 1 < NCB) {
+              asm volatile("tcgen05.wait::ld.sync.aligned;");
+              if (cb + 2 == NCB) release();
             }
           }
-          if (!(P.dbg & 16)) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              if (orow[i] != 0xffffffffu) {
-                float4* dst = reinterpret_cast<float4*>(P.y + (size_t)orow[i] * NN + col0) + (lane & 7);
-                if (P.dbg & 4) *dst = ov[i];
-                else if (P.dbg & 8) __stcg(dst, ov[i]);
-                else __stcs(dst, ov[i]);
-              }
-          }
-          __syncwarp();  // staging reads done before the next column block overwrites it
-          if constexpr (ENERGY) {
-            // lanes l and l ^ 8 (row groups g, g ^ 1) keep columns {0,1} / {2,3} of their four
-            // (fp32 partials of 16 rows), then l and l ^ 16 keep one of the two: their exact sum
-            // (TwoSum) is added to the lane's compensated fp32 accumulator of that column (fp64
-            // is only used at the class flush: fp64 adds here stall on the fp64 pipe)
-            const bool h1 = (lane >> 3) & 1, h2 = (lane >> 4) & 1;
-            const float sa = h1 ? e0 : e2, sb = h1 ? e1 : e3;
-            const float ka = (h1 ? e2 : e0) + __shfl_xor_sync(0xffffffffu, sa, 8);
-            const float kb = (h1 ? e3 : e1) + __shfl_xor_sync(0xffffffffu, sb, 8);
-            const float mine = h2 ? kb : ka;
-            const float other = __shfl_xor_sync(0xffffffffu, h2 ? ka : kb, 16);
-            const float t = mine + other, tb = t - mine;
-            const float te = (mine - (t - tb)) + (other - tb);  // t + te == mine + other exactly
-            const int ci = nh * NCB + cb;
-            const float sn = ks[ci] + t, sbp = sn - ks[ci];
-            kc[ci] += ((ks[ci] - (sn - sbp)) + (t - sbp)) + te;
-            ks[ci] = sn;
-          }
-          if (warp == 0 && lane == 0 && nh == 0 && (cb & 1) == 0 && cb < 8) GEMM_TRACE(k, 12 + (cb >> 1));
-          if (cb + 1 < NCB) {
-            asm volatile("tcgen05.wait::ld.sync.aligned;");
-            if (cb + 2 == NCB) release();
+        }
+        if (warp == 0 && lane == 0) GEMM_TRACE(k, 6);
+      }
+      flush_energy();
+    } else {
+      // ------------------------------------------------------------------ epilogue ------
+      // Thread = row (TMEM lane). Per 32-column block: tcgen05.ld (the next block's load in
+      // flight), unscale, swizzled staging [32 rows][32 floats], then coalesced 128-bit stores
+      // (8 lanes per row, 4 rows per instruction). Energy: each lane squares its 4 columns of
+      // 8 rows in fp32, a shuffle reduce-scatter over the 4 row groups (fp32 partials of 16
+      // rows, merged exactly) leaves every lane one column of the block summed over the warp's
+      // 32 rows, added to a per-lane compensated fp32 accumulator per block; flushed in fp64
+      // with atomics when the class changes.
+      regs_dec<REG_EPI>();
+      unsigned char* stg = sm + SH::STG_OFF + (uint32_t)warp * SH::STG_BYTES;
+      // the column of a block whose energy this lane accumulates (see the reduce-scatter below)
+      const int en_col = 4 * (lane & 7) + ((lane >> 3) & 1) * 2 + ((lane >> 4) & 1);
+      constexpr int NCT = NN / 32;  // column blocks per row
+      float ks[ENERGY ? NCT : 1], kc[ENERGY ? NCT : 1];  // per column block: compensated sum (value, error)
+  #pragma unroll
+      for (int i = 0; i < (ENERGY ? NCT : 1); ++i) ks[i] = kc[i] = 0.f;
+      int en_class = -1;
+      auto flush_energy = [&]() {
+        if (ENERGY && en_class >= 0) {
+  #pragma unroll
+          for (int i = 0; i < NCT; ++i) {
+            const double v = (double)ks[i] + (double)kc[i];
+            if (v != 0.0) atomicAdd(P.energy + (size_t)en_class * NN + i * 32 + en_col, v);
+            ks[i] = kc[i] = 0.f;
           }
         }
+      };
+      uint32_t k = 0, u = 0;
+      for (uint32_t t = t_first; t < ntiles; t += t_step, ++k) {
+        int c;
+        uint64_t p0;
+        uint32_t rows;
+        tm.of(t, c, p0, rows);
+        if (ENERGY && c != en_class) {
+          flush_energy();
+          en_class = c;
+        }
+        mbar_wait(&f_full[k & 3], (k >> 2) & 1);
+        const float f_row = fac[(k & 3) * GM + warp * 32 + lane] * __ldg(P.unscale + c);  // TMEM lane = row
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&f_empty[k & 3]);
+        // row ids of the 4-row groups this lane stores (rows warp*32 + 4 i + lane/8)
+        uint32_t orow[8];
+  #pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = warp * 32 + 4 * i + (lane >> 3);
+          orow[i] = (uint32_t)r < rows ? row_at(P, p0 + r) : 0xffffffffu;
+        }
+  #pragma unroll
+        for (int nh = 0; nh < SH::NH; ++nh, ++u) {
+          const int db = (int)(u & 1);
+          mbar_wait(&d_full[db], (u >> 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          if (nh == 0 && warp == 0 && lane == 0) GEMM_TRACE(k, 5);
+          // TMEM -> registers for column block cb of the unit's accumulator
+          uint32_t v[32];
+          auto tmem_load = [&](int cb) {
+            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(db * SH::ACC + cb * 32);
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+                  "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+                  "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                : "r"(taddr));
+          };
+          constexpr int NCB = SH::NW / 32;
+          auto release = [&]() {  // unit accumulators fully read: release them to unit u + NBUF
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) {
+              if constexpr (PAIR) mbar_arrive_remote(&d_empty[db], 0); else mbar_arrive(&d_empty[db]);
+            }
+          };
+          tmem_load(0);
+          asm volatile("tcgen05.wait::ld.sync.aligned;");
+          if (NCB == 1) release();
+          if (P.dbg & 32) {  // diagnostic: accumulators released unread
+            if (NCB > 1) release();
+            continue;
+          }
+  #pragma unroll
+          for (int cb = 0; cb < NCB; ++cb) {  // unrolled: the energy accumulators are indexed by constants
+            float o[32];
+  #pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(v[i]) * f_row;
+            if (cb + 1 < NCB) tmem_load(cb + 1);  // in flight while this block is stored
+  #pragma unroll
+            for (int q = 0; q < 8; ++q)
+              *reinterpret_cast<float4*>(stg + swz(lane, q)) = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+            __syncwarp();
+            // coalesced: 8 lanes per row, 4 rows per instruction
+            const int col0 = nh * SH::NW + cb * 32;
+            // all 8 staging reads into distinct registers first, then the predicated stores: a
+            // per-row branch around load + store + energy serialises on the reused registers
+            float4 ov[8];
+  #pragma unroll
+            for (int i = 0; i < 8; ++i) ov[i] = *reinterpret_cast<const float4*>(stg + swz(4 * i + (lane >> 3), lane & 7));
+            // rows past the tile's end are exact zeros (their A rows are zero): no predicate needed;
+            // squared before the stores, so no register the stores still read is overwritten
+            float e0 = 0.f, e1 = 0.f, e2 = 0.f, e3 = 0.f;
+            if constexpr (ENERGY) {
+  #pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                e0 = fmaf(ov[i].x, ov[i].x, e0);
+                e1 = fmaf(ov[i].y, ov[i].y, e1);
+                e2 = fmaf(ov[i].z, ov[i].z, e2);
+                e3 = fmaf(ov[i].w, ov[i].w, e3);
+              }
+            }
+            if (!(P.dbg & 16)) {
+  #pragma unroll
+              for (int i = 0; i < 8; ++i)
+                if (orow[i] != 0xffffffffu) {
+                  float4* dst = reinterpret_cast<float4*>(P.y + (size_t)orow[i] * NN + col0) + (lane & 7);
+                  if (P.dbg & 4) *dst = ov[i];
+                  else if (P.dbg & 8) __stcg(dst, ov[i]);
+                  else __stcs(dst, ov[i]);
+                }
+            }
+            __syncwarp();  // staging reads done before the next column block overwrites it
+            if constexpr (ENERGY) {
+              // lanes l and l ^ 8 (row groups g, g ^ 1) keep columns {0,1} / {2,3} of their four
+              // (fp32 partials of 16 rows), then l and l ^ 16 keep one of the two: their exact sum
+              // (TwoSum) is added to the lane's compensated fp32 accumulator of that column (fp64
+              // is only used at the class flush: fp64 adds here stall on the fp64 pipe)
+              const bool h1 = (lane >> 3) & 1, h2 = (lane >> 4) & 1;
+              const float sa = h1 ? e0 : e2, sb = h1 ? e1 : e3;
+              const float ka = (h1 ? e2 : e0) + __shfl_xor_sync(0xffffffffu, sa, 8);
+              const float kb = (h1 ? e3 : e1) + __shfl_xor_sync(0xffffffffu, sb, 8);
+              const float mine = h2 ? kb : ka;
+              const float other = __shfl_xor_sync(0xffffffffu, h2 ? ka : kb, 16);
+              const float t = mine + other, tb = t - mine;
+              const float te = (mine - (t - tb)) + (other - tb);  // t + te == mine + other exactly
+              const int ci = nh * NCB + cb;
+              const float sn = ks[ci] + t, sbp = sn - ks[ci];
+              kc[ci] += ((ks[ci] - (sn - sbp)) + (t - sbp)) + te;
+              ks[ci] = sn;
+            }
+            if (warp == 0 && lane == 0 && nh == 0 && (cb & 1) == 0 && cb < 8) GEMM_TRACE(k, 12 + (cb >> 1));
+            if (cb + 1 < NCB) {
+              asm volatile("tcgen05.wait::ld.sync.aligned;");
+              if (cb + 2 == NCB) release();
+            }
+          }
+        }
+        if (warp == 0 && lane == 0) GEMM_TRACE(k, 6);
       }
-      if (warp == 0 && lane == 0) GEMM_TRACE(k, 6);
+      flush_energy();
     }
-    flush_energy();
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   if constexpr (PAIR) cluster_sync(); else __syncthreads();  // no peer access after this point

@@ -44,6 +44,7 @@ def main():
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--kernel", default="auto")
     ap.add_argument("--interleave", action="store_true")
+    ap.add_argument("--sorted", action="store_true", help="class ids sorted by row (bucketed order = row order)")
     a = ap.parse_args()
     for kv in a.knob:
         k, v = kv.split("=")
@@ -51,6 +52,8 @@ def main():
     w = make_workload(a.config)
     rows = w.cfg.count
     cls = w.make_classes(rows)
+    if a.sorted:
+        cls = torch.sort(cls.view(torch.int16).to(torch.int32)).values.to(torch.int16).view(torch.uint16)
     x = w.make_rows(rows, cls)
     y = torch.empty_like(x)
     xr = torch.empty_like(x)
