@@ -28,6 +28,7 @@
 
 using namespace hygt_gpu;
 #include "hygt_dispatch.h"
+#include "hygt_nvtx.h"
 
 // ============================================================================ errors =====
 namespace {
@@ -1171,6 +1172,7 @@ extern "C" int hygt_plan_create(int log2_n, int rounds, int class_count, const d
 extern "C" int hygt_plan_create_ex(int log2_n, int rounds, int class_count, const double* angles,
                                    const uint16_t* perms, uint32_t perm_mask, uint32_t flags,
                                    const hygt_plan_options* opts, hygt_plan** out) {
+  HYGT_NVTX("hygt_plan_create_ex");
   if (!out) return fail(HYGT_ERR_ARGUMENT, "hygt_plan_create: null out");
   *out = nullptr;
   hygt_plan_options opt;
@@ -1329,6 +1331,7 @@ extern "C" size_t hygt_workspace_bytes(const hygt_plan* plan, uint64_t count) {
 
 extern "C" int hygt_bucket(const hygt_plan* plan, const uint16_t* d_cls, uint64_t count,
                            void* d_ws, size_t ws_bytes, void* stream) {
+  HYGT_NVTX("hygt_bucket");
   if (!plan) return fail(HYGT_ERR_ARGUMENT, "hygt_bucket: null plan");
   if (plan->gemm)
     return plan->classes > 1 ? run_bucket(plan, plan->classes, 0, d_cls, count, d_ws, ws_bytes, as_stream(stream)) : ok();
@@ -1342,6 +1345,7 @@ extern "C" int hygt_bucket(const hygt_plan* plan, const uint16_t* d_cls, uint64_
 extern "C" int hygt_forward_f32(const hygt_plan* plan, const float* d_x, float* d_y,
                                 const uint16_t* d_cls, uint64_t count, void* d_ws,
                                 size_t ws_bytes, uint32_t flags, void* stream) {
+  HYGT_NVTX("hygt_forward_f32");
   return run_apply(plan, 0, d_x, d_y, d_cls, count, nullptr, d_ws, ws_bytes, flags,
                    as_stream(stream));
 }
@@ -1349,6 +1353,7 @@ extern "C" int hygt_forward_f32(const hygt_plan* plan, const float* d_x, float* 
 extern "C" int hygt_inverse_f32(const hygt_plan* plan, const float* d_y, float* d_x,
                                 const uint16_t* d_cls, uint64_t count, void* d_ws,
                                 size_t ws_bytes, uint32_t flags, void* stream) {
+  HYGT_NVTX("hygt_inverse_f32");
   return run_apply(plan, 1, d_y, d_x, d_cls, count, nullptr, d_ws, ws_bytes, flags,
                    as_stream(stream));
 }
@@ -1357,6 +1362,7 @@ extern "C" int hygt_forward_energy_f32(const hygt_plan* plan, const float* d_x, 
                                        const uint16_t* d_cls, uint64_t count, double* d_energy,
                                        void* d_ws, size_t ws_bytes, uint32_t flags,
                                        void* stream) {
+  HYGT_NVTX("hygt_forward_energy_f32");
   if (!d_energy) return fail(HYGT_ERR_ARGUMENT, "hygt_forward_energy_f32: null energy");
   return run_apply(plan, 0, d_x, d_y, d_cls, count, d_energy, d_ws, ws_bytes, flags,
                    as_stream(stream));
@@ -1752,6 +1758,7 @@ extern "C" int hygt_fixed_plan_create_ex(int log2_n, int rounds, int class_count
                                          int precision_bits, const uint16_t* codes,
                                          const uint16_t* perms, uint32_t perm_mask,
                                          const hygt_plan_options* opts, hygt_plan** out) {
+  HYGT_NVTX("hygt_fixed_plan_create_ex");
   if (!out) return fail(HYGT_ERR_ARGUMENT, "hygt_fixed_plan_create: null out");
   *out = nullptr;
   hygt_plan_options opt;
@@ -1919,12 +1926,14 @@ extern "C" int hygt_fixed_plan_create_ex(int log2_n, int rounds, int class_count
 extern "C" int hygt_forward_i64(const hygt_plan* plan, const int64_t* d_x, int64_t* d_y,
                                 const uint16_t* d_cls, uint64_t count, uint64_t* first_bad,
                                 void* stream) {
+  HYGT_NVTX("hygt_forward_i64");
   return run_fixed(plan, 0, d_x, d_y, d_cls, count, first_bad, as_stream(stream));
 }
 
 extern "C" int hygt_inverse_i64(const hygt_plan* plan, const int64_t* d_y, int64_t* d_x,
                                 const uint16_t* d_cls, uint64_t count, uint64_t* first_bad,
                                 void* stream) {
+  HYGT_NVTX("hygt_inverse_i64");
   return run_fixed(plan, 1, d_y, d_x, d_cls, count, first_bad, as_stream(stream));
 }
 

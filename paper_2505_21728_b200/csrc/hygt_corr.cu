@@ -18,6 +18,7 @@
 #include <string>
 
 #include "../../include/hygt_gpu.h"
+#include "hygt_nvtx.h"
 
 int hygt_set_error(int status, const char* msg);  // hygt_capi.cu
 namespace hygt_gpu {
@@ -160,6 +161,7 @@ extern "C" size_t hygt_correlation_workspace_bytes(int classes, uint64_t count) 
 extern "C" int hygt_correlation_f64(int log2_n, int classes, const float* d_x, const uint16_t* d_cls,
                                     uint64_t count, double* d_sum, unsigned long long* d_count,
                                     void* d_ws, size_t ws_bytes, void* stream) {
+  HYGT_NVTX("hygt_correlation_f64");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   CorrFn fn = select_corr(log2_n);
   if (!fn) return hygt_set_error(HYGT_ERR_ARGUMENT, "hygt_correlation_f64: log2_n must be in [2, 8]");

@@ -26,6 +26,7 @@
 
 #include "../../include/hygt_gpu.h"
 #include "hygt_gemm.h"
+#include "hygt_nvtx.h"
 
 int hygt_set_error(int status, const char* msg);  // hygt_capi.cu
 void hygt_smem_attr(const void* fn, size_t bytes);  // hygt_capi.cu: per (device, kernel), only grows
@@ -329,6 +330,7 @@ int run_klt(const hygt_klt_plan* p, bool fwd, const float* in, float* out, const
 
 extern "C" int hygt_klt_plan_create(int n, int class_count, const double* k, uint32_t flags,
                                     hygt_klt_plan** out) {
+  HYGT_NVTX("hygt_klt_plan_create");
   if (!out || !k) return kfail(HYGT_ERR_ARGUMENT, "hygt_klt_plan_create: null argument");
   *out = nullptr;
   if (n < 2 || n > KT || (n & (n - 1))) return kfail(HYGT_ERR_ARGUMENT, "hygt_klt_plan_create: n must be a power of two in [2, 256]");
@@ -411,6 +413,7 @@ extern "C" size_t hygt_klt_workspace_bytes(const hygt_klt_plan* plan, uint64_t c
 extern "C" int hygt_klt_forward_f32(const hygt_klt_plan* plan, const float* d_x, float* d_y,
                                     const uint16_t* d_cls, uint64_t count, void* d_ws,
                                     size_t ws_bytes, void* stream) {
+  HYGT_NVTX("hygt_klt_forward_f32");
   return run_klt(plan, true, d_x, d_y, d_cls, count, d_ws, ws_bytes,
                  reinterpret_cast<cudaStream_t>(stream));
 }
@@ -418,6 +421,7 @@ extern "C" int hygt_klt_forward_f32(const hygt_klt_plan* plan, const float* d_x,
 extern "C" int hygt_klt_inverse_f32(const hygt_klt_plan* plan, const float* d_y, float* d_x,
                                     const uint16_t* d_cls, uint64_t count, void* d_ws,
                                     size_t ws_bytes, void* stream) {
+  HYGT_NVTX("hygt_klt_inverse_f32");
   return run_klt(plan, false, d_y, d_x, d_cls, count, d_ws, ws_bytes,
                  reinterpret_cast<cudaStream_t>(stream));
 }

@@ -40,6 +40,7 @@
 #include <vector>
 
 #include "../../include/hygt_gpu.h"
+#include "hygt_nvtx.h"
 
 int hygt_set_error(int status, const char* msg);  // hygt_capi.cu
 
@@ -686,6 +687,7 @@ extern "C" int hygt_optimize_f64(int log2_n, int rounds, int problems, const dou
                                  double* restart_gains, int* best_restart, double* klt_gain,
                                  double* trajectories, int* trajectory_len, double* variances,
                                  void* stream) {
+  HYGT_NVTX("hygt_optimize_f64");
   if (log2_n < 1 || log2_n > 8)
     return hygt_set_error(HYGT_ERR_ARGUMENT, "hygt_optimize_f64: log2_n must be in [1, 8]");
   if (rounds < 1 || problems < 1 || !phi || !cfg || !angles || !restart_gains || !best_restart)
