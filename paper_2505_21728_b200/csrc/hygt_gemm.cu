@@ -93,18 +93,25 @@ struct Shape {
   // N = 256: the epilogue stores straight from tcgen05.ld.16x256b fragments (no staging), which
   // leaves room for a fifth B stage; N <= 128 stages through shared memory (faster there)
   static constexpr bool DIRECT = NN == 256;
-  static constexpr int NB = STAGE <= 8192 ? 8 : (DIRECT ? 5 : 4);  // B ring stages
-  static constexpr int SPT = 3 * KA * NH;
+  // BRES (one N = 256 unit per tile): the B hi halves of the class stay resident across its
+  // tiles (reloaded when the class changes) and only the lo halves stream through the ring
+  static constexpr bool BRES = WIDE && NN == 256;
+  static constexpr int NB = BRES ? 2 : (STAGE <= 8192 ? 8 : (DIRECT ? 5 : 4));  // B ring stages
+  static constexpr int SPT = BRES ? KA : 3 * KA * NH;  // ring stages per tile
   static constexpr int TG = PAIR ? 2 * GM : GM;      // rows per tile (a CTA pair: 128 each)
   static constexpr int ABUF = KA <= 2 ? 2 : 1;       // tiles of A resident (double-buffered if small)
   static constexpr int AS = KA * ABUF;               // A atom slots
   static constexpr uint32_t A_OFF = 0;               // A: AS atoms (hi + lo each)
-  static constexpr uint32_t B_OFF = A_OFF + AS * 2 * ATOM_BYTES;
+  static constexpr uint32_t BR_OFF = A_OFF + AS * 2 * ATOM_BYTES;          // BRES: KA resident B hi stages
+  static constexpr uint32_t B_OFF = BR_OFF + (BRES ? KA * STAGE : 0u);
   static constexpr uint32_t STG_OFF = B_OFF + NB * STAGE;
   static constexpr uint32_t STG_BYTES = DIRECT ? 0 : 32 * 128;  // per epilogue warp: 32 rows x 32 floats (swizzled)
   static constexpr uint32_t FAC_OFF = STG_OFF + EPI_WARPS * STG_BYTES;
-  static constexpr uint32_t BAR_OFF = FAC_OFF + 4 * GM * 4;
-  static constexpr uint32_t SMEM = BAR_OFF + 512;  // barriers (<= 40 x 8 B) + the TMEM address
+  static constexpr int FB = BRES ? 2 : 4;            // row-factor buffers (tiles in flight split -> epilogue)
+  static constexpr uint32_t BAR_OFF = FAC_OFF + FB * GM * 4;
+  static constexpr uint32_t TE_OFF = BAR_OFF + 512;  // barriers (<= 62 x 8 B) + the TMEM address
+  // + [C] u32 per-class cumulative tile counts (tile_end)
+  static constexpr uint32_t smem(int classes) { return TE_OFF + 4u * (uint32_t)classes; }
   // TMEM: one fp32 accumulator of NW columns per unit, double-buffered over units
   static constexpr int NBUF = 2;
   static constexpr int ACC = NW;
@@ -150,6 +157,9 @@ __device__ __forceinline__ void tc_commit(uint64_t* b) {
   else
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(smem_u32(b)) : "memory");
 }
+// one tcgen05.mma kind::f16 (M = 128, or 256 over the CTA pair), fp32 accumulate unless acc == 0
+template <bool PAIR, int NW>
+__device__ __forceinline__ void mma_issue(uint32_t d, uint64_t a, uint64_t b, uint32_t acc);
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -181,6 +191,19 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
 // Instruction descriptor: D f32, A/B f16, both K-major, M = m, N = n.
 __host__ __device__ constexpr uint32_t idesc_f16(int n, int m = GM) {
   return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+template <bool PAIR, int NW>
+__device__ __forceinline__ void mma_issue(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+  if constexpr (PAIR)  // M = 256: A rows and B columns from both CTAs
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n"
+        :: "r"(d), "l"(a), "l"(b), "r"(idesc_f16(NW, 2 * GM)), "r"(acc));
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n"
+        :: "r"(d), "l"(a), "l"(b), "r"(idesc_f16(NW)), "r"(acc));
 }
 // swizzled byte offset of 16 B chunk q of row r inside an SW128 atom
 __device__ __forceinline__ uint32_t swz(int r, int q) { return (uint32_t)r * 128u + (uint32_t)((q ^ (r & 7)) << 4); }
@@ -256,9 +279,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
   uint64_t* f_full = d_empty + 2;              // [4]   row scales written, count SPLIT_WARPS
   uint64_t* f_empty = f_full + 4;              // [4]   row scales read, count EPI_WARPS
   uint64_t* b_peer = f_empty + 4;              // [NB]  pair: the peer's B half landed (count 1)
-  uint32_t* tmem_sh = reinterpret_cast<uint32_t*>(b_peer + SH::NB);
-  static_assert(SH::AS * 2 + SH::NB * 3 + 12 <= 62, "barrier area");
-  __shared__ uint32_t tile_end_sh[HYGT_GEMM_MAX_CLASSES];
+  uint64_t* bh_full = b_peer + SH::NB;         // [1]   BRES: the class's resident B hi halves landed (expect_tx)
+  uint64_t* bh_empty = bh_full + 1;            // [1]   BRES: the class's last MMAs done (commit)
+  uint64_t* bh_peer = bh_empty + 1;            // [1]   BRES, pair: the peer's resident B hi landed
+  uint32_t* tmem_sh = reinterpret_cast<uint32_t*>(bh_peer + 1);
+  static_assert(SH::AS * 2 + SH::NB * 3 + 15 <= 62, "barrier area");
+  uint32_t* tile_end_sh = reinterpret_cast<uint32_t*>(sm + SH::TE_OFF);  // [C]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int C = P.classes;
@@ -306,6 +332,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
     for (int i = 0; i < SH::NB; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); mbar_init(&b_peer[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&d_full[i], 1); mbar_init(&d_empty[i], EPI_WARPS * pn); }
     for (int i = 0; i < 4; ++i) { mbar_init(&f_full[i], SPLIT_WARPS); mbar_init(&f_empty[i], EPI_WARPS); }
+    mbar_init(bh_full, 1);
+    mbar_init(bh_empty, 1);
+    mbar_init(bh_peer, 1);
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -314,7 +343,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
   const uint32_t tmem = *tmem_sh;
   const TileMap tm{tile_end_sh, &P, C, (uint32_t)SH::TG, rank * (uint32_t)GM};
   const uint32_t ntiles = C ? tile_end_sh[C - 1] : 0u;
-  float* fac = reinterpret_cast<float*>(sm + SH::FAC_OFF);  // [4][GM] per-row unscale factors
+  float* fac = reinterpret_cast<float*>(sm + SH::FAC_OFF);  // [FB][GM] per-row unscale factors
+  auto class_of = [&](uint32_t t) {
+    int lo = 0, hi = C - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (tile_end_sh[mid] <= t) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+  };
 
   if (warp == MMA_WARP) {
     // ------------------------------------------------------------------ MMA issuer ----
@@ -326,16 +363,80 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
     if (PAIR && rank == 1) {
       // the peer forwards "my B half landed" for each stage to rank 0's issuer
       if (lane == 0) {
-        uint32_t ib = 0;
-        for (uint32_t t = t_first; t < ntiles; t += t_step)
+        uint32_t ib = 0, nload = 0;
+        int cur = -1;
+        for (uint32_t t = t_first; t < ntiles; t += t_step) {
+          if constexpr (SH::BRES) {  // the class's resident B hi halves, once per class change
+            const int c = class_of(t);
+            if (c != cur) {
+              mbar_wait(bh_full, nload & 1);
+              mbar_arrive_remote(bh_peer, 0);
+              ++nload;
+              cur = c;
+            }
+          }
           for (int s = 0; s < SH::SPT; ++s, ++ib) {
             if ((P.dbg & 1) && ib >= (uint32_t)SH::NB) break;
             const int sb = (int)(ib % SH::NB);
             mbar_wait(&b_full[sb], (ib / SH::NB) & 1);
             mbar_arrive_remote(&b_peer[sb], 0);
           }
+        }
       }
-    } else if (lane == 0) {
+    } else if (SH::BRES && lane == 0) {
+      // One N = 256 unit per tile. Correction terms (per atom: lo.hi with the resident B hi,
+      // hi.lo with the streamed B lo), then the main term hi.hi (resident B hi).
+      uint32_t il = 0, k = 0, nload = 0;
+      int cur = -1;
+      for (uint32_t t = t_first; t < ntiles; t += t_step, ++k) {
+        const int c = class_of(t);
+        if (c != cur) {  // the producer loaded this class's B hi halves (one load per change)
+          mbar_wait(bh_full, nload & 1);
+          if constexpr (PAIR) mbar_wait(bh_peer, nload & 1);
+          ++nload;
+          cur = c;
+        }
+        const int db = (int)(k & 1);
+        if (k >= 2) mbar_wait(&d_empty[db], ((k >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        GEMM_TRACE(k, 3);
+        const uint32_t dacc = tmem + (uint32_t)(db * SH::ACC);
+#pragma unroll 1
+        for (int ka = 0; ka < SH::KA; ++ka, ++il) {  // correction terms
+          mbar_wait(&a_full[ka], k & 1);
+          const int sb = (int)(il % SH::NB);
+          mbar_wait(&b_full[sb], (il / SH::NB) & 1);
+          if constexpr (PAIR) mbar_wait(&b_peer[sb], (il / SH::NB) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          if (ka < 2) GEMM_TRACE(k, 8 + ka);
+          const uint64_t ahi = desc_sw128(smem_u32(sm + SH::A_OFF + (uint32_t)ka * 2 * ATOM_BYTES));
+          const uint64_t alo = ahi + (ATOM_BYTES >> 4);
+          const uint64_t bhi = desc_sw128(smem_u32(sm + SH::BR_OFF + (uint32_t)ka * SH::STAGE));
+          const uint64_t blo = desc_sw128(smem_u32(sm + SH::B_OFF + (uint32_t)sb * SH::STAGE));
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint64_t o = 2u * j;
+            mma_issue<PAIR, SH::NW>(dacc, alo + o, bhi + o, (ka | j) ? 1u : 0u);
+            mma_issue<PAIR, SH::NW>(dacc, ahi + o, blo + o, 1u);
+          }
+          tc_commit<PAIR>(&b_empty[sb]);
+        }
+#pragma unroll 1
+        for (int ka = 0; ka < SH::KA; ++ka) {  // main term
+          if (ka < 2) GEMM_TRACE(k, 10 + ka);
+          const uint64_t ahi = desc_sw128(smem_u32(sm + SH::A_OFF + (uint32_t)ka * 2 * ATOM_BYTES));
+          const uint64_t bhi = desc_sw128(smem_u32(sm + SH::BR_OFF + (uint32_t)ka * SH::STAGE));
+#pragma unroll
+          for (int j = 0; j < 4; ++j) mma_issue<PAIR, SH::NW>(dacc, ahi + 2u * j, bhi + 2u * j, 1u);
+          tc_commit<PAIR>(&a_empty[ka]);  // the atom may take the next tile's
+        }
+        tc_commit<PAIR>(&d_full[db]);
+        // the class's last tile here: its B hi halves may be replaced once these MMAs are done
+        const uint32_t tn = t + t_step;
+        if (tn >= ntiles || class_of(tn) != c) tc_commit<PAIR>(bh_empty);
+        GEMM_TRACE(k, 4);
+      }
+    } else if (!SH::BRES && lane == 0) {
       uint32_t ib = 0, u = 0, k = 0;
       auto wait_stage = [&](uint32_t i) {
         const int sb = (int)(i % SH::NB);
@@ -435,7 +536,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
     for (int a = 0; a < PF_AHEAD; ++a) prefetch_rows(t_first + (uint32_t)a * t_step);
     uint32_t k = 0;
     for (uint32_t t = t_first + PF_AHEAD * t_step; t < ntiles; t += t_step, ++k) {
-      mbar_wait(&f_full[k & 3], (k >> 2) & 1);
+      mbar_wait(&f_full[k % SH::FB], (k / SH::FB) & 1);
       prefetch_rows(t);
     }
     }
@@ -448,13 +549,27 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
       // global stages: [class][K atom][128-column half][hi | lo] (gemm_build)
       constexpr uint32_t GSTAGE = 2u * (NN < 128 ? NN : 128) * 128, PART = (uint32_t)SH::BW * 128;
       constexpr int GH = NN < 128 ? 1 : NN / 128;
-      uint32_t ib = 0;
+      uint32_t ib = 0, nload = 0;
+      int cur = -1;
       for (uint32_t t = t_first; t < ntiles; t += t_step) {
         int c;
         uint64_t p0;
         uint32_t rows;
         tm.of(t, c, p0, rows);
         const unsigned char* src = P.bops + (size_t)c * SH::KA * GH * GSTAGE;
+        if constexpr (SH::BRES) {  // class change: the resident B hi halves of this CTA's rows
+          if (c != cur) {
+            if (nload > 0) mbar_wait(bh_empty, (nload - 1) & 1);  // the previous class's MMAs are done
+            mbar_expect_tx(bh_full, SH::KA * SH::STAGE);
+            for (int ka = 0; ka < SH::KA; ++ka)
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                  :: "r"(smem_u32(sm + SH::BR_OFF + (uint32_t)ka * SH::STAGE)), "l"(src + (size_t)(ka * GH + rank) * GSTAGE),
+                     "r"(SH::STAGE), "r"(smem_u32(bh_full)) : "memory");
+            ++nload;
+            cur = c;
+          }
+        }
         for (int s = 0; s < SH::SPT; ++s, ++ib) {
             if ((P.dbg & 1) && ib >= (uint32_t)SH::NB) break;
             const int sb = (int)(ib % SH::NB);
@@ -465,9 +580,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
             // r - 2 KA hi. The unit's B rows of this CTA: with one N = 256 unit per tile and CTA
             // pairs, global half `rank` (all its 128 rows); otherwise global half nh, rows from
             // rank * BW (the layout cta_group::2 expects)
-            const int nh = s / (3 * SH::KA), r = s % (3 * SH::KA);
-            const int ka = r < 2 * SH::KA ? r >> 1 : r - 2 * SH::KA;
-            const int part = r < 2 * SH::KA ? (r & 1) : 0;
+            const int nh = SH::BRES ? 0 : s / (3 * SH::KA), r = s % (3 * SH::KA);
+            const int ka = SH::BRES ? s : (r < 2 * SH::KA ? r >> 1 : r - 2 * SH::KA);
+            const int part = SH::BRES ? 1 : (r < 2 * SH::KA ? (r & 1) : 0);  // BRES streams the lo halves
             const int gh = (WIDE && NN == 256) ? (int)rank : nh;
             const uint32_t roff = (WIDE && NN == 256) ? 0u : rank * PART;
             const unsigned char* g = src + (size_t)(ka * GH + gh) * GSTAGE + (size_t)part * (GSTAGE / 2) + roff;
@@ -552,8 +667,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
       }
       if (sw == 0 && lane == 0) GEMM_TRACE(k, 1);
       {  // row unscale factors for the epilogue: 1 / s (power of two, exact)
-        const int fb = (int)(k & 3);
-        if (k >= 4) mbar_wait(&f_empty[fb], ((k >> 2) - 1) & 1);  // tile k-4's factors were read
+        const int fb = (int)(k % SH::FB);
+        if (k >= (uint32_t)SH::FB) mbar_wait(&f_empty[fb], ((k / SH::FB) - 1) & 1);  // tile k-FB's factors were read
         if (l8 == 0) {
 #pragma unroll
           for (int g = 0; g < SH::RG; ++g) fac[fb * GM + row_of_group(g)] = 1.f / scl[g];
@@ -655,18 +770,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
           en_class = c;
         }
         // this thread's rows: warp * 32 + tg + 8 i (i < 4)
-        mbar_wait(&f_full[k & 3], (k >> 2) & 1);
+        mbar_wait(&f_full[k % SH::FB], (k / SH::FB) & 1);
         const float ucls = __ldg(P.unscale + c);
         float frow[4];
         uint32_t orow[4];
   #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int r = warp * 32 + tg + 8 * i;
-          frow[i] = fac[(k & 3) * GM + r] * ucls;
+          frow[i] = fac[(k % SH::FB) * GM + r] * ucls;
           orow[i] = (uint32_t)r < rows ? row_at(P, p0 + r) : 0xffffffffu;
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&f_empty[k & 3]);
+        if (lane == 0) mbar_arrive(&f_empty[k % SH::FB]);
   #pragma unroll
         for (int nh = 0; nh < SH::NH; ++nh, ++u) {
           const int db = (int)(u & 1);
@@ -807,10 +922,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
           flush_energy();
           en_class = c;
         }
-        mbar_wait(&f_full[k & 3], (k >> 2) & 1);
-        const float f_row = fac[(k & 3) * GM + warp * 32 + lane] * __ldg(P.unscale + c);  // TMEM lane = row
+        mbar_wait(&f_full[k % SH::FB], (k / SH::FB) & 1);
+        const float f_row = fac[(k % SH::FB) * GM + warp * 32 + lane] * __ldg(P.unscale + c);  // TMEM lane = row
         __syncwarp();
-        if (lane == 0) mbar_arrive(&f_empty[k & 3]);
+        if (lane == 0) mbar_arrive(&f_empty[k % SH::FB]);
         // row ids of the 4-row groups this lane stores (rows warp*32 + 4 i + lane/8)
         uint32_t orow[8];
   #pragma unroll
@@ -965,9 +1080,9 @@ double half_to_double(uint16_t h) {
 
 int gemm_smem_bytes(int n) {
   switch (n) {
-    case 64: return (int)std::max(Shape<64, true, true>::SMEM, Shape<64, true, false>::SMEM);
-    case 128: return (int)std::max(Shape<128, true, true>::SMEM, Shape<128, true, false>::SMEM);
-    case 256: return (int)Shape<256, true, true>::SMEM;
+    case 64: return (int)std::max(Shape<64, true, true>::smem(HYGT_GEMM_MAX_CLASSES), Shape<64, true, false>::smem(HYGT_GEMM_MAX_CLASSES));
+    case 128: return (int)std::max(Shape<128, true, true>::smem(HYGT_GEMM_MAX_CLASSES), Shape<128, true, false>::smem(HYGT_GEMM_MAX_CLASSES));
+    case 256: return (int)Shape<256, true, false>::smem(HYGT_GEMM_MAX_CLASSES);
     default: return 0;
   }
 }
@@ -1044,12 +1159,13 @@ template <int NN, bool E, bool PAIR, bool WIDE>
 int launch_one(const GemmParams& P, int num_sms, cudaStream_t st) {
   using SH = Shape<NN, PAIR, WIDE>;
   const auto fn = hygt_gemm_kernel<NN, E, PAIR, WIDE>;
-  hygt_smem_attr(reinterpret_cast<const void*>(fn), SH::SMEM);
+  const uint32_t smem = (SH::smem(P.classes) + 15u) & ~15u;
+  hygt_smem_attr(reinterpret_cast<const void*>(fn), smem);
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   cfg.gridDim = dim3(PAIR ? (unsigned)(num_sms / 2 * 2) : (unsigned)num_sms);
   cfg.blockDim = dim3(GEMM_THREADS);
-  cfg.dynamicSmemBytes = SH::SMEM;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = PAIR ? 2 : 1;
@@ -1063,7 +1179,8 @@ int launch_one(const GemmParams& P, int num_sms, cudaStream_t st) {
 template <int NN>
 int launch_n(const GemmParams& P, int grid, bool pair, bool wide, cudaStream_t st) {
   // wide: one unit of all N columns per tile, merged accumulator (N = 256 only with CTA pairs)
-  if (pair && wide)
+  // (the resident B hi halves at N = 256 leave room for at most 384 classes' tile table)
+  if (pair && wide && (NN != 256 || P.classes <= 384))
     return P.energy ? launch_one<NN, true, true, true>(P, grid, st) : launch_one<NN, false, true, true>(P, grid, st);
   if constexpr (NN <= 128) {
     if (wide)
