@@ -750,7 +750,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
       for (int i = 0; i < (ENERGY ? NCT : 1); ++i) ks[i] = kc[i] = 0.f;
       int en_class = -1;
       auto flush_energy = [&]() {
-        if (ENERGY && en_class >= 0) {
+        if (ENERGY && en_class >= 0 && P.energy) {
   #pragma unroll
           for (int i = 0; i < NCT; ++i) {
             const double v = (double)ks[i] + (double)kc[i];
@@ -903,7 +903,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
       for (int i = 0; i < (ENERGY ? NCT : 1); ++i) ks[i] = kc[i] = 0.f;
       int en_class = -1;
       auto flush_energy = [&]() {
-        if (ENERGY && en_class >= 0) {
+        if (ENERGY && en_class >= 0 && P.energy) {
   #pragma unroll
           for (int i = 0; i < NCT; ++i) {
             const double v = (double)ks[i] + (double)kc[i];
