@@ -98,9 +98,13 @@ struct Shape {
   static constexpr bool BRES = WIDE && NN == 256;
   static constexpr int NB = BRES ? 2 : (STAGE <= 8192 ? 8 : (DIRECT ? 5 : 4));  // B ring stages
   static constexpr int SPT = BRES ? KA : 3 * KA * NH;  // ring stages per tile
-  static constexpr int TG = PAIR ? 2 * GM : GM;      // rows per tile (a CTA pair: 128 each)
+  // N = 64: two 128-row sub-tiles per CTA and tile share every B stage and hand-off, which
+  // halves the per-row cost of the pipeline's synchronisation
+  static constexpr int SUB = NN == 64 ? 2 : 1;
+  static constexpr int CR = SUB * GM;                 // rows per CTA and tile
+  static constexpr int TG = PAIR ? 2 * CR : CR;      // rows per tile (a CTA pair: CR each)
   static constexpr int ABUF = KA <= 2 ? 2 : 1;       // tiles of A resident (double-buffered if small)
-  static constexpr int AS = KA * ABUF;               // A atom slots
+  static constexpr int AS = KA * SUB * ABUF;         // A atom slots (128 rows each)
   static constexpr uint32_t A_OFF = 0;               // A: AS atoms (hi + lo each)
   static constexpr uint32_t BR_OFF = A_OFF + AS * 2 * ATOM_BYTES;          // BRES: KA resident B hi stages
   static constexpr uint32_t B_OFF = BR_OFF + (BRES ? KA * STAGE : 0u);
@@ -108,15 +112,15 @@ struct Shape {
   static constexpr uint32_t STG_BYTES = DIRECT ? 0 : 32 * 128;  // per epilogue warp: 32 rows x 32 floats (swizzled)
   static constexpr uint32_t FAC_OFF = STG_OFF + EPI_WARPS * STG_BYTES;
   static constexpr int FB = BRES ? 2 : 4;            // row-factor buffers (tiles in flight split -> epilogue)
-  static constexpr uint32_t BAR_OFF = FAC_OFF + FB * GM * 4;
+  static constexpr uint32_t BAR_OFF = FAC_OFF + FB * CR * 4;
   static constexpr uint32_t TE_OFF = BAR_OFF + 512;  // barriers (<= 62 x 8 B) + the TMEM address
   // + [C] u32 per-class cumulative tile counts (tile_end)
   static constexpr uint32_t smem(int classes) { return TE_OFF + 4u * (uint32_t)classes; }
   // TMEM: one fp32 accumulator of NW columns per unit, double-buffered over units
   static constexpr int NBUF = 2;
-  static constexpr int ACC = NW;
+  static constexpr int ACC = SUB * NW;                // sub-tile s at column s NW
   static constexpr uint32_t TMEM_COLS = NBUF * ACC < 32 ? 32 : NBUF * ACC;
-  static constexpr int RG = GM / SPLIT_WARPS / 4;    // 4-row groups per split warp
+  static constexpr int RG = CR / SPLIT_WARPS / 4;    // 4-row groups per split warp
   static_assert(!WIDE || PAIR || NN <= 128, "N = 256 in one unit needs the CTA pair");
 };
 
@@ -241,7 +245,7 @@ struct TileMap {
   const uint32_t* tile_end;  // shared: [C] cumulative tile counts
   const GemmParams* P;
   int classes;
-  uint32_t tg, part;         // rows per tile, this CTA's offset in the tile (0 or 128)
+  uint32_t tg, part, cr;     // rows per tile, this CTA's offset in the tile (0 or CR), rows per CTA
   __device__ void of(uint32_t t, int& c, uint64_t& p0, uint32_t& rows) const {
     int lo = 0, hi = classes - 1;
     while (lo < hi) {
@@ -254,7 +258,7 @@ struct TileMap {
     const uint64_t s1 = seg_at(*P, c);
     p0 = s0 + (uint64_t)(t - first_tile) * tg + part;
     const uint64_t left = s1 > p0 ? s1 - p0 : 0ull;
-    rows = left < GM ? (uint32_t)left : GM;
+    rows = left < cr ? (uint32_t)left : cr;
   }
 };
 
@@ -284,6 +288,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
   uint64_t* bh_peer = bh_empty + 1;            // [1]   BRES, pair: the peer's resident B hi landed
   uint32_t* tmem_sh = reinterpret_cast<uint32_t*>(bh_peer + 1);
   static_assert(SH::AS * 2 + SH::NB * 3 + 15 <= 62, "barrier area");
+  static_assert(SH::SUB == 1 || !SH::BRES, "sub-tiles only without resident B");
   uint32_t* tile_end_sh = reinterpret_cast<uint32_t*>(sm + SH::TE_OFF);  // [C]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -341,9 +346,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
   if constexpr (PAIR) cluster_sync(); else __syncthreads();  // barriers initialised in both CTAs
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_sh;
-  const TileMap tm{tile_end_sh, &P, C, (uint32_t)SH::TG, rank * (uint32_t)GM};
+  const TileMap tm{tile_end_sh, &P, C, (uint32_t)SH::TG, rank * (uint32_t)SH::CR, (uint32_t)SH::CR};
   const uint32_t ntiles = C ? tile_end_sh[C - 1] : 0u;
-  float* fac = reinterpret_cast<float*>(sm + SH::FAC_OFF);  // [FB][GM] per-row unscale factors
+  float* fac = reinterpret_cast<float*>(sm + SH::FAC_OFF);  // [FB][CR] per-row unscale factors
   auto class_of = [&](uint32_t t) {
     int lo = 0, hi = C - 1;
     while (lo < hi) {
@@ -468,37 +473,49 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
           asm volatile("tcgen05.fence::after_thread_sync;");
           if (nh == 0) GEMM_TRACE(k, 3);
           const uint32_t dacc = tmem + (uint32_t)(db * SH::ACC);
+          // A atom slot of sub-tile sb, K atom ka; sub-tile sb accumulates at column sb NW
+          auto slot = [&](int sb, int ka) { return ((int)(k % SH::ABUF) * SH::SUB + sb) * SH::KA + ka; };
 #pragma unroll 1
           for (int ka = 0; ka < SH::KA; ++ka, ib += 2) {  // correction terms
-            const int as = (int)(k % SH::ABUF) * SH::KA + ka;
-            if (nh == 0 && !(P.dbg & 64)) mbar_wait(&a_full[as], (k / SH::ABUF) & 1);
+            if (nh == 0 && !(P.dbg & 64))
+#pragma unroll
+              for (int sb = 0; sb < SH::SUB; ++sb) mbar_wait(&a_full[slot(sb, ka)], (k / SH::ABUF) & 1);
             const uint64_t bhi = wait_stage(ib), blo = wait_stage(ib + 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
             if (nh < 2 && ka < 2) GEMM_TRACE(k, 8 + nh * 4 + ka);
-            // descriptors of the atom's / stage's first K step; the next K step (32 B further)
-            // is +2 in the 16 B-unit start-address field (no carry: addresses < 2^18)
-            const uint64_t ahi = desc_sw128(smem_u32(sm + SH::A_OFF + (uint32_t)as * 2 * ATOM_BYTES));
-            const uint64_t alo = ahi + (ATOM_BYTES >> 4);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {  // K = 16 fp16 = 32 B per instruction
-              const uint64_t o = 2u * j;
-              mma(dacc, alo + o, bhi + o, (ka | j) ? 1u : 0u);
-              mma(dacc, ahi + o, blo + o, 1u);
+            for (int sb = 0; sb < SH::SUB; ++sb) {
+              // descriptors of the atom's / stage's first K step; the next K step (32 B further)
+              // is +2 in the 16 B-unit start-address field (no carry: addresses < 2^18)
+              const uint64_t ahi = desc_sw128(smem_u32(sm + SH::A_OFF + (uint32_t)slot(sb, ka) * 2 * ATOM_BYTES));
+              const uint64_t alo = ahi + (ATOM_BYTES >> 4);
+              const uint32_t d = dacc + (uint32_t)(sb * SH::NW);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {  // K = 16 fp16 = 32 B per instruction
+                const uint64_t o = 2u * j;
+                mma(d, alo + o, bhi + o, (ka | j) ? 1u : 0u);
+                mma(d, ahi + o, blo + o, 1u);
+              }
             }
             release_stage(ib);
             release_stage(ib + 1);
           }
 #pragma unroll 1
           for (int ka = 0; ka < SH::KA; ++ka, ++ib) {  // main term
-            const int as = (int)(k % SH::ABUF) * SH::KA + ka;
             const uint64_t bhi = wait_stage(ib);
             asm volatile("tcgen05.fence::after_thread_sync;");
             if (nh < 2 && ka < 2) GEMM_TRACE(k, 10 + nh * 4 + ka);
-            const uint64_t ahi = desc_sw128(smem_u32(sm + SH::A_OFF + (uint32_t)as * 2 * ATOM_BYTES));
 #pragma unroll
-            for (int j = 0; j < 4; ++j) mma(dacc, ahi + 2u * j, bhi + 2u * j, 1u);
+            for (int sb = 0; sb < SH::SUB; ++sb) {
+              const uint64_t ahi = desc_sw128(smem_u32(sm + SH::A_OFF + (uint32_t)slot(sb, ka) * 2 * ATOM_BYTES));
+              const uint32_t d = dacc + (uint32_t)(sb * SH::NW);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) mma(d, ahi + 2u * j, bhi + 2u * j, 1u);
+            }
             release_stage(ib);
-            if (nh == SH::NH - 1) tc_commit<PAIR>(&a_empty[as]);  // the slot may take a later tile's atom
+            if (nh == SH::NH - 1)
+#pragma unroll
+              for (int sb = 0; sb < SH::SUB; ++sb) tc_commit<PAIR>(&a_empty[slot(sb, ka)]);  // may take a later tile's atom
           }
           tc_commit<PAIR>(&d_full[db]);
         }
@@ -519,14 +536,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
       uint64_t p0;
       uint32_t rows;
       tm.of(tp, c, p0, rows);
-      uint32_t id[GM / 32];
+      uint32_t id[SH::CR / 32];
 #pragma unroll
-      for (int i = 0; i < GM / 32; ++i) {
+      for (int i = 0; i < SH::CR / 32; ++i) {
         const uint32_t r = (uint32_t)(lane + 32 * i);
         id[i] = r < rows ? row_at(P, p0 + r) : 0xffffffffu;
       }
 #pragma unroll
-      for (int i = 0; i < GM / 32; ++i)
+      for (int i = 0; i < SH::CR / 32; ++i)
         if (id[i] != 0xffffffffu)
 #pragma unroll
           for (int l = 0; l < NN / 32; ++l)
@@ -604,9 +621,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
     // and is served in two 16-lane phases. Rows {0, 4} (lanes 0-15) and {1, 5} (lanes 16-31)
     // of an 8-row block fall in opposite halves of the SWIZZLE_128B pattern, so each phase
     // covers all 32 banks once: 2 wavefronts per instruction, the minimum.
+    // (with two sub-tiles, groups 4..7 are the same rows of the second 128-row sub-tile, so
+    // every split warp writes into every A atom slot)
     auto row_of_group = [&](int g) {
-      const int b16 = (sw * SH::RG + g) >> 2, gg = (sw * SH::RG + g) & 3;
-      return b16 * 16 + (gg & 1) * 2 + (gg >> 1) * 8 + (g8 >> 1) + (g8 & 1) * 4;
+      const int gb = g & 3, sub = g >> 2;
+      const int b16 = (sw * 4 + gb) >> 2, gg = (sw * 4 + gb) & 3;
+      return sub * GM + b16 * 16 + (gg & 1) * 2 + (gg >> 1) * 8 + (g8 >> 1) + (g8 & 1) * 4;
     };
     // One pass per tile: each lane holds its 4 row groups x NN / 32 float4 of the tile in
     // registers (the register rebalancing above gives the split warps room for a whole tile),
@@ -671,7 +691,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
         if (k >= (uint32_t)SH::FB) mbar_wait(&f_empty[fb], ((k / SH::FB) - 1) & 1);  // tile k-FB's factors were read
         if (l8 == 0) {
 #pragma unroll
-          for (int g = 0; g < SH::RG; ++g) fac[fb * GM + row_of_group(g)] = 1.f / scl[g];
+          for (int g = 0; g < SH::RG; ++g) fac[fb * SH::CR + row_of_group(g)] = 1.f / scl[g];
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&f_full[fb]);
@@ -680,13 +700,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
       // previous atom was read by the MMAs; one a_full arrival per atom
 #pragma unroll
       for (int ka = 0; ka < SH::KA; ++ka) {
-        const int as = (int)(k % SH::ABUF) * SH::KA + ka;
+#pragma unroll
+       for (int sb = 0; sb < SH::SUB; ++sb) {
+        const int as = ((int)(k % SH::ABUF) * SH::SUB + sb) * SH::KA + ka;
         if (k >= (uint32_t)SH::ABUF) mbar_wait(&a_empty[as], ((k / SH::ABUF) - 1) & 1);
         unsigned char* ahi = sm + SH::A_OFF + (uint32_t)as * 2 * ATOM_BYTES;
         unsigned char* alo = ahi + ATOM_BYTES;
 #pragma unroll
-        for (int g = 0; g < SH::RG; ++g) {
-          const int r = row_of_group(g);
+        for (int g = sb * 4; g < sb * 4 + 4; ++g) {
+          const int r = row_of_group(g) & (GM - 1);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const float4 v = hd[g][2 * ka + h];
@@ -706,6 +728,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
         if (lane == 0) {
           if constexpr (PAIR) mbar_arrive_remote(&a_full[as], 0); else mbar_arrive(&a_full[as]);
         }
+       }
         load_part(hd, rnext, 2 * ka);  // tile k + HB's atom ka, in flight from here
         load_part(hd, rnext, 2 * ka + 1);
       }
@@ -777,7 +800,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
   #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int r = warp * 32 + tg + 8 * i;
-          frow[i] = fac[(k % SH::FB) * GM + r] * ucls;
+          frow[i] = fac[(k % SH::FB) * SH::CR + r] * ucls;
           orow[i] = (uint32_t)r < rows ? row_at(P, p0 + r) : 0xffffffffu;
         }
         __syncwarp();
@@ -923,26 +946,32 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
           en_class = c;
         }
         mbar_wait(&f_full[k % SH::FB], (k / SH::FB) & 1);
-        const float f_row = fac[(k % SH::FB) * GM + warp * 32 + lane] * __ldg(P.unscale + c);  // TMEM lane = row
+        // per sub-tile sb: this lane's row factor (TMEM lane = row sb GM + warp 32 + lane) and
+        // the row ids of the 4-row groups it stores (rows sb GM + warp 32 + 4 i + lane / 8)
+        const float ucls = __ldg(P.unscale + c);
+        float f_rows[SH::SUB];
+  #pragma unroll
+        for (int sb = 0; sb < SH::SUB; ++sb) f_rows[sb] = fac[(k % SH::FB) * SH::CR + sb * GM + warp * 32 + lane] * ucls;
         __syncwarp();
         if (lane == 0) mbar_arrive(&f_empty[k % SH::FB]);
-        // row ids of the 4-row groups this lane stores (rows warp*32 + 4 i + lane/8)
-        uint32_t orow[8];
+        uint32_t orow[SH::SUB][8];
   #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int r = warp * 32 + 4 * i + (lane >> 3);
-          orow[i] = (uint32_t)r < rows ? row_at(P, p0 + r) : 0xffffffffu;
-        }
+        for (int sb = 0; sb < SH::SUB; ++sb)
+  #pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = sb * GM + warp * 32 + 4 * i + (lane >> 3);
+            orow[sb][i] = (uint32_t)r < rows ? row_at(P, p0 + r) : 0xffffffffu;
+          }
   #pragma unroll
         for (int nh = 0; nh < SH::NH; ++nh, ++u) {
           const int db = (int)(u & 1);
           mbar_wait(&d_full[db], (u >> 1) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
           if (nh == 0 && warp == 0 && lane == 0) GEMM_TRACE(k, 5);
-          // TMEM -> registers for column block cb of the unit's accumulator
+          // TMEM -> registers for block blk of the unit's accumulator (sub-tile blk / NCB)
           uint32_t v[32];
-          auto tmem_load = [&](int cb) {
-            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(db * SH::ACC + cb * 32);
+          auto tmem_load = [&](int blk) {
+            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(db * SH::ACC + blk * 32);
             asm volatile(
                 "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
                 "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -952,7 +981,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
                   "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
                 : "r"(taddr));
           };
-          constexpr int NCB = SH::NW / 32;
+          constexpr int NCB = SH::NW / 32;       // column blocks per sub-tile
+          constexpr int NBLK = SH::SUB * NCB;
           auto release = [&]() {  // unit accumulators fully read: release them to unit u + NBUF
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
@@ -962,17 +992,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
           };
           tmem_load(0);
           asm volatile("tcgen05.wait::ld.sync.aligned;");
-          if (NCB == 1) release();
+          if (NBLK == 1) release();
           if (P.dbg & 32) {  // diagnostic: accumulators released unread
-            if (NCB > 1) release();
+            if (NBLK > 1) release();
             continue;
           }
   #pragma unroll
-          for (int cb = 0; cb < NCB; ++cb) {  // unrolled: the energy accumulators are indexed by constants
+          for (int blk = 0; blk < NBLK; ++blk) {  // unrolled: the energy accumulators are indexed by constants
+            const int sb = blk / NCB, cb = blk % NCB;
             float o[32];
   #pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(v[i]) * f_row;
-            if (cb + 1 < NCB) tmem_load(cb + 1);  // in flight while this block is stored
+            for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(v[i]) * f_rows[sb];
+            if (blk + 1 < NBLK) tmem_load(blk + 1);  // in flight while this block is stored
   #pragma unroll
             for (int q = 0; q < 8; ++q)
               *reinterpret_cast<float4*>(stg + swz(lane, q)) = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
@@ -999,12 +1030,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
             if (!(P.dbg & 16)) {
   #pragma unroll
               for (int i = 0; i < 8; ++i)
-                if (orow[i] != 0xffffffffu) {
-                  float4* dst = reinterpret_cast<float4*>(P.y + (size_t)orow[i] * NN + col0) + (lane & 7);
-                  if (P.dbg & 4) *dst = ov[i];
-                  else if (P.dbg & 8) __stcg(dst, ov[i]);
-                  else __stcs(dst, ov[i]);
-                }
+                if (orow[sb][i] != 0xffffffffu)
+                  __stcs(reinterpret_cast<float4*>(P.y + (size_t)orow[sb][i] * NN + col0) + (lane & 7), ov[i]);
             }
             __syncwarp();  // staging reads done before the next column block overwrites it
             if constexpr (ENERGY) {
@@ -1026,9 +1053,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
               ks[ci] = sn;
             }
             if (warp == 0 && lane == 0 && nh == 0 && (cb & 1) == 0 && cb < 8) GEMM_TRACE(k, 12 + (cb >> 1));
-            if (cb + 1 < NCB) {
+            if (blk + 1 < NBLK) {
               asm volatile("tcgen05.wait::ld.sync.aligned;");
-              if (cb + 2 == NCB) release();
+              if (blk + 2 == NBLK) release();
             }
           }
         }
