@@ -1,6 +1,7 @@
 """GPU parity at the configured sizes: config 5 (2^24 rows x N = 256, 35
-classes, with the full [35][256] fp64 energy table) and config 3 (2^22 rows x N = 64, 35 classes,
-inter-round permutations, directional edges), exactly the shapes the bench times.
+classes, with the full [35][256] fp64 energy table), config 3 (2^22 rows x N = 64, 35 classes,
+inter-round permutations, directional edges), configs 1 and 2 (2^20 / 2^24 rows x N = 16, every
+row against the oracle) and config 4 (the KLT), exactly the shapes the bench times.
 
 What is checked, per config:
   * round trip inverse(forward(x)) on ALL rows (max-abs <= 1e-5 * max|x|) and per-row norm
@@ -159,3 +160,46 @@ def test_config4_klt_full_size(cuda, oracle_mod):
     check_close(y[idx].cpu().numpy(), O.klt_apply(k, xs, cs), xs, "cfg4 forward sample")
     ys = y[idx].cpu().numpy()
     check_close(back[idx].cpu().numpy(), O.klt_apply(k, ys, cs, inverse=True), ys, "cfg4 inverse sample")
+
+
+@pytest.mark.parametrize("config", [1, 2])
+def test_config1_2_full_size_every_row(cuda, oracle_mod, config):
+    """Configs 1 (2^20 rows, one class, 2 rounds, fixed inter-round permutation) and 2 (2^24
+    rows, 35 classes, 3 rounds, seeded inter-round permutations): forward of EVERY row against the
+    oracle (relative L2 and max-abs bars), inverse of the GPU's forward on all rows against the
+    oracle's inverse, round trip and norms on all rows: the staged N = 16 kernel the headline
+    bench times, at its configured size."""
+    from paper_2505_21728_b200 import HyGTPlan
+    from paper_2505_21728_b200.synth import make_workload
+    O = oracle_mod
+    w = make_workload(config)
+    count = w.cfg.count
+    assert count == (1 << 20 if config == 1 else 1 << 24) and w.n == 16
+    cls = w.make_classes(count)
+    x = w.make_rows(count, cls)
+    plan = HyGTPlan(w.models, w.perms)
+    ws = torch.zeros(plan.workspace_bytes(count), dtype=torch.uint8, device=cuda)
+    y = plan.forward(x, cls, workspace=ws)
+    back = plan.inverse(y, cls, workspace=ws, reuse_buckets=True)
+    plan.sync_status(ws)
+    torch.cuda.synchronize()
+    _roundtrip_and_norms(x, y, back)
+    C, R = w.cfg.classes, w.cfg.rounds
+    full = np.concatenate([w.perms, np.tile(np.arange(16, dtype=np.uint16), (C, 1, 1))], 1)
+    mask = (1 << (R - 1)) - 1
+    scale = x.abs().max().item()
+    acc = {"fwd": [0.0, 0.0, 0.0], "inv": [0.0, 0.0, 0.0]}
+    for r0 in range(0, count, CHUNK):
+        xs, cs = x[r0:r0 + CHUNK].cpu().numpy(), cls[r0:r0 + CHUNK].cpu().numpy()
+        ys = y[r0:r0 + CHUNK].cpu().numpy()
+        for key, got, inp, inverse in (("fwd", ys, xs, False), ("inv", back[r0:r0 + CHUNK].cpu().numpy(), ys, True)):
+            ref = O.apply_batch(4, R, w.angles, full, mask, inp, cs, inverse=inverse, hoist=True)
+            err = got.astype(np.float64) - ref
+            a = acc[key]
+            a[0] += float((err * err).sum())
+            a[1] += float((ref * ref).sum())
+            a[2] = max(a[2], float(np.abs(err).max()))
+    for key, (num, den, worst) in acc.items():
+        rel = (num / den) ** 0.5
+        assert rel <= 1e-6, f"cfg{config} {key} rel L2 {rel:.3e}"
+        assert worst <= 1e-5 * scale, f"cfg{config} {key} max-abs {worst:.3e}"
