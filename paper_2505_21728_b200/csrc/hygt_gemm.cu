@@ -98,12 +98,12 @@ struct Shape {
   static constexpr bool BRES = WIDE && NN == 256;
   static constexpr int NB = BRES ? 2 : (STAGE <= 8192 ? 8 : (DIRECT ? 5 : 4));  // B ring stages
   static constexpr int SPT = BRES ? KA : 3 * KA * NH;  // ring stages per tile
-  // N = 64: two 128-row sub-tiles per CTA and tile share every B stage and hand-off, which
+  // N <= 128: two 128-row sub-tiles per CTA and tile share every B stage and hand-off, which
   // halves the per-row cost of the pipeline's synchronisation
-  static constexpr int SUB = NN == 64 ? 2 : 1;
+  static constexpr int SUB = NN <= 128 ? 2 : 1;
   static constexpr int CR = SUB * GM;                 // rows per CTA and tile
   static constexpr int TG = PAIR ? 2 * CR : CR;      // rows per tile (a CTA pair: CR each)
-  static constexpr int ABUF = KA <= 2 ? 2 : 1;       // tiles of A resident (double-buffered if small)
+  static constexpr int ABUF = KA * SUB <= 2 ? 2 : 1;  // tiles of A resident (double-buffered if small)
   static constexpr int AS = KA * SUB * ABUF;         // A atom slots (128 rows each)
   static constexpr uint32_t A_OFF = 0;               // A: AS atoms (hi + lo each)
   static constexpr uint32_t BR_OFF = A_OFF + AS * 2 * ATOM_BYTES;          // BRES: KA resident B hi stages
