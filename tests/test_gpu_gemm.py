@@ -115,3 +115,30 @@ def test_plan_options_select_and_validate(cuda):
     y1 = HyGTPlan(ms, kernel="tensor", cta_pairs=True).forward(x, cls)
     y0 = HyGTPlan(ms, kernel="tensor", cta_pairs=False).forward(x, cls)
     assert torch.equal(y0, y1)  # same per-row arithmetic, only the operand staging differs
+
+
+@pytest.mark.parametrize("log2n,classes", [(8, 400), (6, 300)])
+def test_gemm_many_classes_and_variants(cuda, oracle_mod, log2n, classes):
+    """Many classes: at N = 256 more than 384 classes do not leave room for the per-class tile
+    table next to the resident B hi halves, so the kernel takes the variant with units of 128
+    columns and streamed B; at N = 64 the 256-row sub-tiled tiles meet a few rows per class.
+    Forward with energy and inverse against the oracle, and the single-CTA build equal to the
+    CTA-pair build bit for bit (same per-row arithmetic and accumulation order)."""
+    from paper_2505_21728_b200 import HyGTPlan
+    plan, angles, perms, mask, rng = _case(log2n, 2, classes, "none", 41 + classes)
+    n = 1 << log2n
+    rows = 20000
+    x = (rng.standard_normal((rows, n)) * 16).astype(np.float32)
+    cls = rng.integers(0, classes, rows).astype(np.uint16)
+    xd, cd = torch.from_numpy(x).to(cuda), torch.from_numpy(cls).to(cuda)
+    e = torch.zeros(classes, n, dtype=torch.float64, device=cuda)
+    y = plan.forward_energy(xd, cd, e)
+    z = plan.inverse(xd, cd)
+    plan.sync_status()
+    check_close(y.cpu().numpy(), oracle_mod.apply_batch(log2n, 2, angles, perms, mask, x, cls), x, f"fwd C={classes}")
+    check_close(z.cpu().numpy(), oracle_mod.apply_batch(log2n, 2, angles, perms, mask, x, cls, inverse=True), x, f"inv C={classes}")
+    np.testing.assert_allclose(e.cpu().numpy(), oracle_mod.class_energy(log2n, 2, angles, None, 0, x, cls), rtol=2e-6)
+    from paper_2505_21728_b200 import HyGTModel
+    models = [HyGTModel(log2n, 2, angles[c]) for c in range(classes)]
+    y1 = HyGTPlan(models, kernel="tensor", cta_pairs=False).forward(xd, cd)
+    assert torch.equal(y, y1)
