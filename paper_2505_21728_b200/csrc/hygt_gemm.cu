@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
       uint32_t ib = 0, u = 0, k = 0;
       auto wait_stage = [&](uint32_t i) {
         const int sb = (int)(i % SH::NB);
-        if ((!(P.dbg & 1) || i < (uint32_t)SH::NB) && !(P.dbg & 64)) {
+        if (!(P.dbg & 1) || i < (uint32_t)SH::NB) {
           mbar_wait(&b_full[sb], (i / SH::NB) & 1);
           if constexpr (PAIR) mbar_wait(&b_peer[sb], (i / SH::NB) & 1);
         }
@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
       for (uint32_t t = t_first; t < ntiles; t += t_step, ++k) {
         for (int nh = 0; nh < SH::NH; ++nh, ++u) {
           const int db = (int)(u & 1);
-          if (u >= 2 && !(P.dbg & 64)) mbar_wait(&d_empty[db], ((u >> 1) - 1) & 1);
+          if (u >= 2) mbar_wait(&d_empty[db], ((u >> 1) - 1) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
           if (nh == 0) GEMM_TRACE(k, 3);
           const uint32_t dacc = tmem + (uint32_t)(db * SH::ACC);
@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
           auto slot = [&](int sb, int ka) { return ((int)(k % SH::ABUF) * SH::SUB + sb) * SH::KA + ka; };
 #pragma unroll 1
           for (int ka = 0; ka < SH::KA; ++ka, ib += 2) {  // correction terms
-            if (nh == 0 && !(P.dbg & 64))
+            if (nh == 0)
 #pragma unroll
               for (int sb = 0; sb < SH::SUB; ++sb) mbar_wait(&a_full[slot(sb, ka)], (k / SH::ABUF) & 1);
             const uint64_t bhi = wait_stage(ib), blo = wait_stage(ib + 1);

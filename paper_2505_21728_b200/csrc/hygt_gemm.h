@@ -20,7 +20,9 @@ struct GemmParams {
   const float* unscale;      // [C] 2^-kB
   double* energy;            // [C][N] fp64 (forward with energy) or nullptr
   unsigned long long* trace; // debug: per-tile clock64 events of CTA 0 ([64][16]) or nullptr
-  int dbg;                   // diagnostic switches (knob HYGT_GEMM_DBG; wrong results when set)
+  int dbg;                   // diagnostic switches (test-hook knob HYGT_GEMM_DBG; wrong results when
+                             // set): 1 B stages loaded once, 2 no L2 prefetch, 16 no output stores,
+                             // 32 accumulators released unread (streamed-B variants for 1)
 };
 
 struct GemmOperands {  // one direction
