@@ -1006,9 +1006,10 @@ int run_segment(const hygt_plan* p, int dir, const float* x, float* y, uint64_t 
 }
 
 // Composed-operator path: M_c (forward) and M_c^T (inverse) per class, fp64 on the host, then
-// the fp16 hi/lo operand stages of hygt_gemm.cu. Default for N = 256, where the butterfly
-// kernels are bound by coefficient delivery through the LSU; HYGT_GEMM=1 takes
-// it at N = 64 / 128 as well, HYGT_GEMM=0 never.
+// the fp16 hi/lo operand stages of hygt_gemm.cu. Default for N = 128 / 256, where the butterfly
+// kernels are bound by coefficient delivery through the LSU (measured at N = 128,
+// 35 classes, R = 4: 27 % of HBM against 59 %); HYGT_GEMM=1 takes it at N = 64 as well (the
+// per-class NVRTC chain is faster there), HYGT_GEMM=0 never.
 int setup_gemm(hygt_plan* p, const double* angles, const uint16_t* perms) {
   const int n = 1 << p->log2n;
   if (!gemm_supported(n, p->classes)) {
@@ -1018,7 +1019,7 @@ int setup_gemm(hygt_plan* p, const double* angles, const uint16_t* perms) {
   }
   const int want = p->opt.kernel == HYGT_KERNEL_TENSOR ? 1 : p->opt.kernel == HYGT_KERNEL_BUTTERFLY ? 0
                                                                                   : env_int("HYGT_GEMM", -1);
-  if (want == 0 || (want < 0 && n != 256)) return HYGT_OK;
+  if (want == 0 || (want < 0 && n < 128)) return HYGT_OK;
   const size_t a = (size_t)p->rounds * p->log2n * n / 2;
   std::vector<double> fwd((size_t)p->classes * n * n), inv((size_t)p->classes * n * n);
   for (int c = 0; c < p->classes; ++c) {
@@ -1034,7 +1035,7 @@ int setup_gemm(hygt_plan* p, const double* angles, const uint16_t* perms) {
   for (int d = 0; d < 2; ++d) {
     p->gemm_ops[d].pair = p->opt.cta_pairs != 0 && env_int("HYGT_GEMM_PAIR", 1) != 0;
     p->gemm_ops[d].wide = env_int("HYGT_GEMM_WIDE", 1) != 0;  // merged accumulator, one unit per tile
-    p->gemm_ops[d].dbg = env_int("HYGT_GEMM_DBG", 0);  // measured slower
+    p->gemm_ops[d].dbg = env_int("HYGT_GEMM_DBG", 0);  // diagnostics only (hygt_gemm.h)
   }
   p->gemm = true;
   p->chunk_rows = 0;  // global class buckets
