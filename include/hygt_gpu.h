@@ -129,7 +129,7 @@ double hygt_plan_input_limit(const hygt_plan* plan);
  *     immediates and permutations register renames, so the class's rows touch shared memory
  *     only on their way in and out. Forward-with-energy calls run on the tile / segment
  *     kernels instead,
- * 8 = the composed-operator tensor-core path (N = 64 / 128 / 256; the default at N = 256): the
+ * 8 = the composed-operator tensor-core path (N = 64 / 128 / 256; the default at N = 128 / 256): the
  *     plan composes each class's rounds, passes and permutations into one N x N matrix (fp64)
  *     and the rows are transformed by a per-class grouped GEMM on tcgen05 (fp16 3-term split
  *     with per-row power-of-two scaling, fp32 accumulation in TMEM, CTA pairs), the per-class
