@@ -25,7 +25,7 @@ __host__ __device__ constexpr uint32_t idesc_f16(int n, int m) {
 }
 
 // A: 128 rows x 4 K atoms (64 fp16 each) = 64 KB; B: BN rows x 4 atoms
-template <bool PAIR, int NN, int NACC>
+template <bool PAIR, int NN, int NACC, int MM = PAIR ? 256 : 128>
 __global__ void __cluster_dims__(PAIR ? 2 : 1, 1, 1) rate(int iters, unsigned long long* cycles) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint32_t base_sh;
@@ -73,7 +73,7 @@ __global__ void __cluster_dims__(PAIR ? 2 : 1, 1, 1) rate(int iters, unsigned lo
           if (PAIR)
             asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                          "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n"
-                         :: "r"(d), "l"(da), "l"(db), "r"(idesc_f16(NN, 256)), "r"(acc));
+                         :: "r"(d), "l"(da), "l"(db), "r"(idesc_f16(NN, MM)), "r"(acc));
           else
             asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                          "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
@@ -98,14 +98,14 @@ __global__ void __cluster_dims__(PAIR ? 2 : 1, 1, 1) rate(int iters, unsigned lo
   }
 }
 
-template <bool PAIR, int NN, int NACC>
+template <bool PAIR, int NN, int NACC, int MM = PAIR ? 256 : 128>
 int run(int sms, unsigned long long* cyc) {
   const int iters = 2000;
   constexpr int BN = PAIR ? NN / 2 : NN;
   const int smem = 128 * 512 + BN * 512 + 1024;
-  cudaFuncSetAttribute(rate<PAIR, NN, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(rate<PAIR, NN, NACC, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaMemset(cyc, 0, sizeof(unsigned long long) * sms);
-  rate<PAIR, NN, NACC><<<sms / 2 * 2, 128, smem>>>(iters, cyc);
+  rate<PAIR, NN, NACC, MM><<<sms / 2 * 2, 128, smem>>>(iters, cyc);
   if (cudaDeviceSynchronize() != cudaSuccess) { printf("error %s\n", cudaGetErrorString(cudaGetLastError())); return 1; }
   std::vector<unsigned long long> h(sms);
   cudaMemcpy(h.data(), cyc, sizeof(unsigned long long) * sms, cudaMemcpyDeviceToHost);
@@ -114,9 +114,9 @@ int run(int sms, unsigned long long* cyc) {
   for (auto v : h) if (v) { mean += (double)v; ++n; }
   mean /= n;
   const double per = mean / (iters * 16.0);
-  const double mac_per_sm = (PAIR ? 256.0 * NN * 16 / 2 : 128.0 * NN * 16);
+  const double mac_per_sm = (double)MM * NN * 16 / (PAIR ? 2 : 1);
   printf("%s M=%d N=%3d accumulators %d: %.1f cycles/instr, %.0f MAC/clk/SM (ideal cycles %.0f at 4096)\n",
-         PAIR ? "cta_group::2" : "cta_group::1", PAIR ? 256 : 128, NN, NACC, per, mac_per_sm / per, mac_per_sm / 4096);
+         PAIR ? "cta_group::2" : "cta_group::1", MM, NN, NACC, per, mac_per_sm / per, mac_per_sm / 4096);
   return 0;
 }
 
@@ -133,5 +133,7 @@ int main() {
   e |= run<false, 128, 1>(sms, cyc);
   e |= run<true, 128, 1>(sms, cyc);
   e |= run<true, 128, 2>(sms, cyc);
+  e |= run<true, 256, 1, 128>(sms, cyc);
+  e |= run<true, 256, 2, 128>(sms, cyc);
   return e;
 }
