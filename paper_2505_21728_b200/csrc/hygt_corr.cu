@@ -18,6 +18,8 @@
 #include <string>
 
 #include "../../include/hygt_gpu.h"
+#include "hygt_corr_tc.h"
+#include "hygt_knobs.h"
 #include "hygt_nvtx.h"
 
 int hygt_set_error(int status, const char* msg);  // hygt_capi.cu
@@ -189,6 +191,18 @@ extern "C" int hygt_correlation_f64(int log2_n, int classes, const float* d_x, c
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (hygt_gpu::corr_tc_supported(log2_n) && hygt_gpu::knob("HYGT_CORR_TC", 1) != 0) {
+    // N = 64: exact integer-digit products on the tensor cores (hygt_corr_tc.cu)
+    hygt_gpu::CorrTcParams Q{};
+    Q.x = d_x;
+    Q.idx = P.idx;
+    Q.seg_end = P.seg_end;
+    Q.classes = classes;
+    Q.count = count;
+    Q.sum = d_sum;
+    Q.cnt = d_count;
+    return hygt_gpu::corr_tc_run(Q, sms, st);
+  }
   const uint64_t want = std::max<uint64_t>(1, (uint64_t)sms * 8 / tiles_ut);
   const uint64_t ctas = std::min<uint64_t>(want, (count + CORR_RT - 1) / CORR_RT);
   P.cta_span = (count + ctas - 1) / ctas;

@@ -19,7 +19,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=3)
 ap.add_argument("--rows", type=int, default=0)
 ap.add_argument("--steps", type=int, default=5)
+ap.add_argument("--knob", action="append", default=[])
 a = ap.parse_args()
+import paper_2505_21728_b200._lib as _L  # noqa: E402
+for kv in a.knob:
+    _L.set_knob(kv.split("=")[0], int(kv.split("=")[1]))
 w = make_workload(a.config)
 rows = a.rows or w.cfg.count
 cls = w.make_classes(rows)
