@@ -290,22 +290,20 @@ __global__ void __launch_bounds__(THREADS, 1) corr_tc_kernel(const CorrTcParams 
     hq[0] = beg < end && next_tile(f, pos, tq[0]);
     hq[1] = hq[0] && next_tile(f, pos, tq[1]);
     hq[2] = hq[1] && next_tile(f, pos, tq[2]);
+    // Loads are unconditional (rows past the tile's end read its last row and are masked where
+    // the samples are used): a predicated load-or-zero compiles to moves that wait on the loads.
     auto load_ids = [&](const Seg& t, bool have) -> uint32_t {
-      const uint32_t rr = (uint32_t)(w * 16 + (lane & 15));
-      if (!have || rr >= t.rows) return 0xffffffffu;
+      if (!have) return 0u;
+      const uint32_t rr = min((uint32_t)(w * 16 + (lane & 15)), t.rows - 1u);
       return P.idx ? __ldg(P.idx + t.p0 + rr) : (uint32_t)(t.p0 + rr);
     };
     auto load_x = [&](uint32_t ids, float (&v)[16][2]) {
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
         const uint32_t row = __shfl_sync(0xffffffffu, ids, r);
-        if (row != 0xffffffffu) {
-          const float* src = P.x + (uint64_t)row * CN;
-          v[r][0] = __ldcs(src + lane);
-          v[r][1] = __ldcs(src + lane + 32);
-        } else {
-          v[r][0] = v[r][1] = 0.f;
-        }
+        const float* src = P.x + (uint64_t)row * CN;
+        v[r][0] = __ldcs(src + lane);
+        v[r][1] = __ldcs(src + lane + 32);
       }
     };
     float va[16][2], vb[16][2];
@@ -322,6 +320,11 @@ __global__ void __launch_bounds__(THREADS, 1) corr_tc_kernel(const CorrTcParams 
         atomicAdd(P.cnt + t.f, (unsigned long long)(s1 - t.p0));
       }
       last_f = t.f;
+      // rows past the tile's end (warp-uniform): zero
+      const int nvalid = (int)t.rows - w * 16;
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+        if (r >= nvalid) v[r][0] = v[r][1] = 0.f;
       float m0 = 0.f, m1 = 0.f;
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
