@@ -111,18 +111,13 @@ __device__ __forceinline__ void digit_bytes(float x, int E, uint32_t& zl, uint32
   const int ex = (int)((u >> 23) & 0xFFu);
   const uint32_t mant = (u & 0x7FFFFFu) | (ex ? 0x800000u : 0u);
   const int s = (ex ? ex : 1) - 96 - E;  // |x| < 2^E: s <= 30
-  uint32_t lo, hi;
-  if (s >= 0) {
-    lo = mant << s;
-    hi = __funnelshift_l(mant, 0u, (uint32_t)s);
-  } else {
-    lo = s > -32 ? (uint32_t)(((uint64_t)mant + (1ull << (-s - 1))) >> (-s)) : 0u;
-    hi = 0u;
-  }
-  if (u >> 31) {  // two's complement of the 64-bit value
-    lo = ~lo + 1u;
-    hi = ~hi + (lo == 0u ? 1u : 0u);
-  }
+  // signed mantissa, then a 64-bit shift of the signed value (funnel shift over its sign word)
+  int32_t m = (int32_t)mant;
+  if (s < 0) m = s > -32 ? (int32_t)((mant + (1u << (-s - 1))) >> (-s)) : 0;  // rare: tiny samples
+  const int32_t ms = (u >> 31) ? -m : m;
+  const uint32_t sh = s > 0 ? (uint32_t)s : 0u;
+  const uint32_t lo = (uint32_t)ms << sh;
+  const uint32_t hi = __funnelshift_l((uint32_t)ms, (uint32_t)(ms >> 31), sh);
   const uint64_t y = (((uint64_t)hi << 32) | lo) + 0x0080808080808080ull;
   zl = (uint32_t)y ^ 0x80808080u;
   zh = (uint32_t)(y >> 32) ^ 0x00808080u;
