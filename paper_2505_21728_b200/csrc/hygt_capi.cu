@@ -1035,6 +1035,7 @@ int setup_gemm(hygt_plan* p, const double* angles, const uint16_t* perms) {
   for (int d = 0; d < 2; ++d) {
     p->gemm_ops[d].pair = p->opt.cta_pairs != 0 && env_int("HYGT_GEMM_PAIR", 1) != 0;
     p->gemm_ops[d].wide = env_int("HYGT_GEMM_WIDE", 1) != 0;  // merged accumulator, one unit per tile
+    p->gemm_ops[d].ts = env_int("HYGT_GEMM_TS", 1) != 0;      // N = 256: operator in TMEM
     p->gemm_ops[d].dbg = env_int("HYGT_GEMM_DBG", 0);  // diagnostics only (hygt_gemm.h)
   }
   p->gemm = true;

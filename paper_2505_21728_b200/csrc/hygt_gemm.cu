@@ -153,6 +153,21 @@ __device__ __forceinline__ void mbar_arrive_remote(uint64_t* b, uint32_t cta) {
       "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}\n"
       :: "r"(smem_u32(b)), "r"(cta) : "memory");
 }
+// cluster-scope release / acquire: for data a thread of the other CTA reads with generic
+// (DSMEM) loads or TMEM written with tcgen05.st that the peer's MMAs read; used where the
+// releasing thread has no global accesses in flight (a release at cluster scope waits for them)
+__device__ __forceinline__ void mbar_arrive_remote_release(uint64_t* b, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}\n"
+      :: "r"(smem_u32(b)), "r"(cta) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n\tW%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%0], %1;\n\t@!P bra W%=;\n\t}\n"
+      :: "r"(smem_u32(b)), "r"(parity) : "memory");
+}
 template <bool PAIR>
 __device__ __forceinline__ void tc_commit(uint64_t* b) {
   if constexpr (PAIR)  // the pair's MMAs done: arrive on the barrier in both CTAs
@@ -209,6 +224,52 @@ __device__ __forceinline__ void mma_issue(uint32_t d, uint64_t a, uint64_t b, ui
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n"
         :: "r"(d), "l"(a), "l"(b), "r"(idesc_f16(NW)), "r"(acc));
 }
+// One lane of a converged warp (elect.sync). The MMA issuer runs as a whole warp and issues
+// from the elected lane: the descriptors then stay in uniform registers and every
+// tcgen05.mma is one UTCHMMA, where a lone lane in a divergent branch pays R2UR moves and an
+// ELECT loop per instruction (~15 SASS instructions per MMA, which next to the split warps'
+// ALU stream limited the N = 256 MMAs to ~280 cycles each instead of 128; tools/microbench_contend.cu)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t e;
+  asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}\n" : "=r"(e));
+  return e != 0;
+}
+// The 4 K steps (16 fp16 = 32 B each: +2 in the descriptors' 16 B address field) of one 64-wide
+// K atom, M = 256 over the CTA pair, N = NW: correction terms lo.hi and hi.lo interleaved per K
+// step (the first accumulates unless acc0 == 0), or the main term hi.hi alone.
+template <int NW>
+__device__ __forceinline__ void mma_atom_corr2(uint32_t d, uint64_t alo, uint64_t bhi, uint64_t ahi, uint64_t blo, uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 a0, b0, a1, b1;\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t"
+      "mov.b64 a0, %1;\n\tmov.b64 b0, %2;\n\tmov.b64 a1, %3;\n\tmov.b64 b1, %4;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], a0, b0, %6, p;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], a1, b1, %6, 1;\n\t"
+      "add.s64 a0, a0, 2;\n\tadd.s64 b0, b0, 2;\n\tadd.s64 a1, a1, 2;\n\tadd.s64 b1, b1, 2;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], a0, b0, %6, 1;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], a1, b1, %6, 1;\n\t"
+      "add.s64 a0, a0, 2;\n\tadd.s64 b0, b0, 2;\n\tadd.s64 a1, a1, 2;\n\tadd.s64 b1, b1, 2;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], a0, b0, %6, 1;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], a1, b1, %6, 1;\n\t"
+      "add.s64 a0, a0, 2;\n\tadd.s64 b0, b0, 2;\n\tadd.s64 a1, a1, 2;\n\tadd.s64 b1, b1, 2;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], a0, b0, %6, 1;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], a1, b1, %6, 1;\n\t}\n"
+      :: "r"(d), "l"(alo), "l"(bhi), "l"(ahi), "l"(blo), "r"(acc0), "n"(idesc_f16(NW, 2 * GM)));
+}
+template <int NW>
+__device__ __forceinline__ void mma_atom_main2(uint32_t d, uint64_t ahi, uint64_t bhi) {
+  asm volatile(
+      "{\n\t.reg .b64 a0, b0;\n\t"
+      "mov.b64 a0, %1;\n\tmov.b64 b0, %2;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], a0, b0, %3, 1;\n\t"
+      "add.s64 a0, a0, 2;\n\tadd.s64 b0, b0, 2;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], a0, b0, %3, 1;\n\t"
+      "add.s64 a0, a0, 2;\n\tadd.s64 b0, b0, 2;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], a0, b0, %3, 1;\n\t"
+      "add.s64 a0, a0, 2;\n\tadd.s64 b0, b0, 2;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], a0, b0, %3, 1;\n\t}\n"
+      :: "r"(d), "l"(ahi), "l"(bhi), "n"(idesc_f16(NW, 2 * GM)));
+}
 // swizzled byte offset of 16 B chunk q of row r inside an SW128 atom
 __device__ __forceinline__ uint32_t swz(int r, int q) { return (uint32_t)r * 128u + (uint32_t)((q ^ (r & 7)) << 4); }
 
@@ -246,6 +307,7 @@ struct TileMap {
   const GemmParams* P;
   int classes;
   uint32_t tg, part, cr;     // rows per tile, this CTA's offset in the tile (0 or CR), rows per CTA
+  const uint32_t* seg_sh = nullptr;  // shared copy of the bucket ends [C] (or nullptr: global seg_end)
   __device__ void of(uint32_t t, int& c, uint64_t& p0, uint32_t& rows) const {
     int lo = 0, hi = classes - 1;
     while (lo < hi) {
@@ -254,8 +316,8 @@ struct TileMap {
     }
     c = lo;
     const uint32_t first_tile = c ? tile_end[c - 1] : 0u;
-    const uint64_t s0 = c ? seg_at(*P, c - 1) : 0ull;
-    const uint64_t s1 = seg_at(*P, c);
+    const uint64_t s0 = c ? (seg_sh ? (uint64_t)seg_sh[c - 1] : seg_at(*P, c - 1)) : 0ull;
+    const uint64_t s1 = seg_sh ? (uint64_t)seg_sh[c] : seg_at(*P, c);
     p0 = s0 + (uint64_t)(t - first_tile) * tg + part;
     const uint64_t left = s1 > p0 ? s1 - p0 : 0ull;
     rows = left < cr ? (uint32_t)left : cr;
@@ -387,6 +449,69 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
             mbar_arrive_remote(&b_peer[sb], 0);
           }
         }
+      }
+    } else if (SH::BRES && PAIR && !(P.dbg & 4)) {
+      // One N = 256 unit per tile, issued by the whole (converged) warp from one elected lane
+      // (see elect_one). Correction terms (per atom: lo.hi with the resident B hi, hi.lo with
+      // the streamed B lo), then the main term hi.hi (resident B hi).
+      const bool leader = elect_one();
+      uint32_t il = 0, k = 0, nload = 0;
+      int cur = -1;
+      for (uint32_t t = t_first; t < ntiles; t += t_step, ++k) {
+        const int c = class_of(t);
+        if (c != cur) {  // the producer loaded this class's B hi halves (one load per change)
+          mbar_wait(bh_full, nload & 1);
+          mbar_wait(bh_peer, nload & 1);
+          ++nload;
+          cur = c;
+        }
+        const int db = (int)(k & 1);
+        if (k >= 2) mbar_wait(&d_empty[db], ((k >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (leader) GEMM_TRACE(k, 3);
+        const uint32_t dacc = tmem + (uint32_t)(db * SH::ACC);
+#pragma unroll 1
+        for (int ka = 0; ka < SH::KA; ++ka, ++il) {  // correction terms
+          mbar_wait(&a_full[ka], k & 1);
+          const int sb = (int)(il % SH::NB);
+          const bool b_streamed = !(P.dbg & 1) || il < (uint32_t)SH::NB;  // diagnostic 1: loaded once
+          if (b_streamed) {
+            mbar_wait(&b_full[sb], (il / SH::NB) & 1);
+            mbar_wait(&b_peer[sb], (il / SH::NB) & 1);
+          }
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          __syncwarp();
+          if (leader) {
+            if (ka < 2) GEMM_TRACE(k, 8 + ka);
+            const uint64_t ahi = desc_sw128(smem_u32(sm + SH::A_OFF + (uint32_t)ka * 2 * ATOM_BYTES));
+            const uint64_t alo = ahi + (ATOM_BYTES >> 4);
+            const uint64_t bhi = desc_sw128(smem_u32(sm + SH::BR_OFF + (uint32_t)ka * SH::STAGE));
+            const uint64_t blo = desc_sw128(smem_u32(sm + SH::B_OFF + (uint32_t)sb * SH::STAGE));
+            mma_atom_corr2<SH::NW>(dacc, alo, bhi, ahi, blo, (uint32_t)ka);
+            if (!(P.dbg & 1)) tc_commit<PAIR>(&b_empty[sb]);
+          }
+          __syncwarp();
+        }
+#pragma unroll 1
+        for (int ka = 0; ka < SH::KA; ++ka) {  // main term
+          if (leader) {
+            if (ka < 2) GEMM_TRACE(k, 10 + ka);
+            const uint64_t ahi = desc_sw128(smem_u32(sm + SH::A_OFF + (uint32_t)ka * 2 * ATOM_BYTES));
+            const uint64_t bhi = desc_sw128(smem_u32(sm + SH::BR_OFF + (uint32_t)ka * SH::STAGE));
+            mma_atom_main2<SH::NW>(dacc, ahi, bhi);
+            tc_commit<PAIR>(&a_empty[ka]);  // the atom may take the next tile's
+          }
+          __syncwarp();
+        }
+        // the class's last tile here: its B hi halves may be replaced once these MMAs are done
+        const uint32_t tn = t + t_step;
+        const bool last_of_class = tn >= ntiles || class_of(tn) != c;
+        if (leader) {
+          tc_commit<PAIR>(&d_full[db]);
+          if (last_of_class) tc_commit<PAIR>(bh_empty);
+          GEMM_TRACE(k, 4);
+        }
+        __syncwarp();
       }
     } else if (SH::BRES && lane == 0) {
       // One N = 256 unit per tile. Correction terms (per atom: lo.hi with the resident B hi,
@@ -704,6 +829,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
        for (int sb = 0; sb < SH::SUB; ++sb) {
         const int as = ((int)(k % SH::ABUF) * SH::SUB + sb) * SH::KA + ka;
         if (k >= (uint32_t)SH::ABUF) mbar_wait(&a_empty[as], ((k / SH::ABUF) - 1) & 1);
+        if (sw == 0 && lane == 0 && sb == 0 && ka < 2) GEMM_TRACE(k, 12 + 2 * ka);  // atom slot free
         unsigned char* ahi = sm + SH::A_OFF + (uint32_t)as * 2 * ATOM_BYTES;
         unsigned char* alo = ahi + ATOM_BYTES;
 #pragma unroll
@@ -728,6 +854,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
         if (lane == 0) {
           if constexpr (PAIR) mbar_arrive_remote(&a_full[as], 0); else mbar_arrive(&a_full[as]);
         }
+        if (sw == 0 && lane == 0 && sb == 0 && ka < 2) GEMM_TRACE(k, 13 + 2 * ka);  // atom written
        }
         load_part(hd, rnext, 2 * ka);  // tile k + HB's atom ka, in flight from here
         load_part(hd, rnext, 2 * ka + 1);
@@ -897,7 +1024,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
               kc[ci] += ((ks[ci] - (sn - sbp)) + (ts - sbp)) + te;
               ks[ci] = sn;
             }
-            if (warp == 0 && lane == 0 && nh == 0 && (cb & 1) == 0 && cb < 8) GEMM_TRACE(k, 12 + (cb >> 1));
             if (cb + 1 < NCB) {
               asm volatile("tcgen05.wait::ld.sync.aligned;");
               if (cb + 2 == NCB) release();
@@ -1052,7 +1178,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
               kc[ci] += ((ks[ci] - (sn - sbp)) + (t - sbp)) + te;
               ks[ci] = sn;
             }
-            if (warp == 0 && lane == 0 && nh == 0 && (cb & 1) == 0 && cb < 8) GEMM_TRACE(k, 12 + (cb >> 1));
             if (blk + 1 < NBLK) {
               asm volatile("tcgen05.wait::ld.sync.aligned;");
               if (blk + 2 == NBLK) release();
@@ -1073,6 +1198,491 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_kernel(const GemmPa
     else
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(SH::TMEM_COLS));
   }
+}
+
+// ------------------------------------------------------------------ N = 256: operator in TMEM --
+// The N = 256 composed operator with the roles of the two MMA operands swapped ("TS" form):
+//   D[out column m][row n] = sum_k OP[m][k] X[n][k]
+// A (M = 256 output columns, 128 per CTA of the pair) is the class operator, resident in TMEM
+// (tcgen05.mma reads A from TMEM: lane = output column, column j = fp16 pair K 2j, 2j+1); it is
+// written once per class change by the epilogue warps with tcgen05.st from the operator stages
+// gemm_build lays out. B (N = 128 data rows per tile, 64 per CTA) is the split's fp16 hi / lo
+// tile in shared memory, SWIZZLE_128B K-major, with TS_DBUF tiles resident. Per tile 48 MMAs
+// (M = 256, N = 128, K = 16): the correction terms OPhi.Xlo and OPlo.Xhi over all K first,
+// then the main term OPhi.Xhi (as in the SS form, only the main term's K steps round against
+// the full-size sum).
+// Against the SS form (hygt_gemm_kernel with a resident B hi and a streamed B lo, 56% of HBM):
+//   * the epilogue thread owns one output column, so every store instruction writes 32
+//     consecutive columns of one row = one whole 128 B line (the SS form's tcgen05.ld.16x256b
+//     fragments stored 8 rows x 32 B per instruction, and those 4x more L1 wavefronts starved
+//     the split warps' shared-memory stores: tools/trace_summary.py, DBG 16);
+//   * the split runs TS_DBUF tiles ahead of the MMAs (the SS form had one A buffer and the
+//     split and MMAs advanced atom by atom), and no B operand streams through shared memory;
+//   * the per-column energy is a per-thread sum (no cross-lane reduction).
+namespace ts {
+constexpr int TR = 128;                       // rows per tile (MMA N, both CTAs)
+constexpr int CR = 64;                        // rows per CTA and tile
+constexpr int KA = 4;                         // K atoms of 64
+constexpr uint32_t HALF = CR * 128;           // one K atom, hi or lo, of this CTA's rows (8 KB)
+constexpr uint32_t TILE = KA * 2 * HALF;      // 64 KB
+constexpr int DBUF = 3;                       // data tiles resident
+constexpr int FB = 4;                         // row-factor buffers
+constexpr uint32_t FAC_OFF = DBUF * TILE;     // [FB][CR] f32
+constexpr uint32_t TAB_OFF = FAC_OFF + FB * CR * 4;  // [2][TR] {row factor, row id}: the epilogue's row table
+constexpr uint32_t BAR_OFF = TAB_OFF + 2 * TR * 8;
+constexpr uint32_t TE_OFF = BAR_OFF + 256;    // + [C] u32 tile_end, [C] u32 bucket ends
+constexpr uint32_t smem(int classes) { return TE_OFF + 8u * (uint32_t)classes; }
+constexpr uint32_t OPHI = 0, OPLO = 128, DCOL = 256;  // TMEM columns: operator hi / lo, 2 accumulators of 128
+constexpr int RG = CR / SPLIT_WARPS / 4;     // 4-row groups per split lane
+static_assert(RG == 2, "split layout");
+}  // namespace ts
+
+// 4 K steps (one 64-wide K atom) of D += A(TMEM) . B(smem)^T, M = 256 over the pair, N = 128
+__device__ __forceinline__ void mma_ts_atom(uint32_t d, uint32_t a, uint64_t b, uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 b0;\n\t.reg .b32 a0;\n\t"
+      "setp.ne.b32 p, %3, 0;\n\t"
+      "mov.b32 a0, %1;\n\tmov.b64 b0, %2;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [a0], b0, %4, p;\n\t"
+      "add.s32 a0, a0, 8;\n\tadd.s64 b0, b0, 2;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [a0], b0, %4, 1;\n\t"
+      "add.s32 a0, a0, 8;\n\tadd.s64 b0, b0, 2;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [a0], b0, %4, 1;\n\t"
+      "add.s32 a0, a0, 8;\n\tadd.s64 b0, b0, 2;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [a0], b0, %4, 1;\n\t}\n"
+      :: "r"(d), "r"(a), "l"(b), "r"(acc0), "n"(idesc_f16(ts::TR, 2 * GM)));
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+      :: "r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+         "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]),
+         "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]),
+         "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31]));
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+// read a float from the same shared-memory offset in CTA `cta` of the cluster
+__device__ __forceinline__ float ld_dsmem_f32(const float* p, uint32_t cta) {
+  float v;
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %1, %2;\n\tld.shared::cluster.f32 %0, [ra];\n\t}\n"
+      : "=f"(v) : "r"(smem_u32(p)), "r"(cta) : "memory");
+  return v;
+}
+
+template <bool ENERGY>
+__global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_ts_kernel(const GemmParams P) {  // clusters of 2
+  constexpr int NN = 256;
+  extern __shared__ __align__(1024) unsigned char sm[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + ts::BAR_OFF);
+  uint64_t* x_full = bars;                  // [DBUF] data tile written (rank 0: count 2 SPLIT_WARPS)
+  uint64_t* x_empty = x_full + ts::DBUF;    // [DBUF] data tile read by the MMAs (commit, both CTAs)
+  uint64_t* d_full = x_empty + ts::DBUF;    // [2]    accumulator done (commit, both CTAs)
+  uint64_t* d_empty = d_full + 2;           // [2]    accumulator read (rank 0: count 2 EPI_WARPS)
+  uint64_t* f_full = d_empty + 2;           // [FB]   row factors written (count 2 SPLIT_WARPS: both CTAs)
+  uint64_t* f_empty = f_full + ts::FB;      // [FB]   row factors read (count 2 EPI_WARPS: both CTAs)
+  uint64_t* op_full = f_empty + ts::FB;     // [1]    class operator in TMEM (rank 0: count 2 EPI_WARPS)
+  uint32_t* tmem_sh = reinterpret_cast<uint32_t*>(op_full + 1);
+  static_assert(3 * 2 + 4 + 2 * 4 + 1 <= 30, "barrier area");
+  uint32_t* tile_end_sh = reinterpret_cast<uint32_t*>(sm + ts::TE_OFF);
+  uint32_t* seg_sh = tile_end_sh + P.classes;  // [C] bucket ends: tile lookups without global loads
+  float* fac = reinterpret_cast<float*>(sm + ts::FAC_OFF);  // [FB][CR] this CTA's row unscale factors
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int C = P.classes;
+  const uint32_t rank = cluster_rank(), peer = rank ^ 1u;
+  const uint32_t t_first = cluster_id(), t_step = cluster_count();
+  if (warp == 0) {  // per-class cumulative tile counts (tiles of TR rows)
+    uint32_t run = 0;
+    for (int c0 = 0; c0 < C; c0 += 32) {
+      const int c = c0 + lane;
+      uint32_t nt = 0;
+      if (c < C) {
+        const uint64_t s0 = c ? seg_at(P, c - 1) : 0ull, s1 = seg_at(P, c);
+        nt = (uint32_t)((s1 - s0 + ts::TR - 1) / ts::TR);
+        seg_sh[c] = (uint32_t)s1;
+      }
+      uint32_t v = nt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+      }
+      if (c < C) tile_end_sh[c] = run + v;
+      run += __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  if (warp == MMA_WARP) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" :: "r"(smem_u32(tmem_sh)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < ts::DBUF; ++i) { mbar_init(&x_full[i], 2 * SPLIT_WARPS); mbar_init(&x_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&d_full[i], 1); mbar_init(&d_empty[i], 2 * EPI_WARPS); }
+    for (int i = 0; i < ts::FB; ++i) { mbar_init(&f_full[i], 2 * SPLIT_WARPS); mbar_init(&f_empty[i], 2 * EPI_WARPS); }
+    mbar_init(op_full, 2 * EPI_WARPS);
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  cluster_sync();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_sh;
+  const uint32_t ntiles = C ? tile_end_sh[C - 1] : 0u;
+  // this CTA's rows of a tile (split, prefetch) and the whole tile (epilogue)
+  const uint32_t* segs = (P.dbg & 8) ? nullptr : seg_sh;
+  const TileMap tm_cta{tile_end_sh, &P, C, (uint32_t)ts::TR, rank * (uint32_t)ts::CR, (uint32_t)ts::CR, segs};
+  const TileMap tm_pair{tile_end_sh, &P, C, (uint32_t)ts::TR, 0u, (uint32_t)ts::TR, segs};
+  auto class_of = [&](uint32_t t) {
+    int lo = 0, hi = C - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (tile_end_sh[mid] <= t) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+  };
+
+  if (warp == MMA_WARP) {
+    // ------------------------------------------------------------------ MMA issuer ----
+    regs_dec<REG_MISC>();
+    if (rank == 0) {  // the whole warp, one elected lane issues (see elect_one)
+      const bool leader = elect_one();
+      uint32_t k = 0, nop = 0;
+      int cur = -1;
+      for (uint32_t t = t_first; t < ntiles; t += t_step, ++k) {
+        const int c = class_of(t);
+        if (c != cur) {  // both CTAs' epilogues wrote this class's operator into TMEM
+          mbar_wait(op_full, nop & 1);
+          ++nop;
+          cur = c;
+        }
+        const int db = (int)(k & 1), xb = (int)(k % ts::DBUF);
+        if (k >= 2) mbar_wait(&d_empty[db], ((k >> 1) - 1) & 1);
+        mbar_wait(&x_full[xb], (k / ts::DBUF) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        __syncwarp();
+        if (leader) {
+          GEMM_TRACE(k, 3);
+          const uint32_t dacc = tmem + ts::DCOL + (uint32_t)db * ts::TR;
+          const uint64_t xd = desc_sw128(smem_u32(sm + (uint32_t)xb * ts::TILE));
+          constexpr uint64_t ATOM = (2 * ts::HALF) >> 4, LO = ts::HALF >> 4;  // descriptor address units
+#pragma unroll
+          for (int ka = 0; ka < ts::KA; ++ka)  // OPhi . Xlo
+            mma_ts_atom(dacc, tmem + ts::OPHI + 32u * ka, xd + ka * ATOM + LO, (uint32_t)ka);
+#pragma unroll
+          for (int ka = 0; ka < ts::KA; ++ka)  // OPlo . Xhi
+            mma_ts_atom(dacc, tmem + ts::OPLO + 32u * ka, xd + ka * ATOM, 1u);
+#pragma unroll
+          for (int ka = 0; ka < ts::KA; ++ka)  // OPhi . Xhi
+            mma_ts_atom(dacc, tmem + ts::OPHI + 32u * ka, xd + ka * ATOM, 1u);
+          tc_commit<true>(&x_empty[xb]);
+          tc_commit<true>(&d_full[db]);
+          GEMM_TRACE(k, 4);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == PF_WARP) {
+    // ------------------------------------------------------------------ row prefetch --
+    regs_dec<REG_MISC>();
+    // L2 prefetch of this CTA's rows of the tile 2 steps ahead, paced by the split (f_full)
+    auto prefetch_rows = [&](uint32_t tp) {
+      if (tp >= ntiles) return;
+      int c;
+      uint64_t p0;
+      uint32_t rows;
+      tm_cta.of(tp, c, p0, rows);
+      uint32_t id[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const uint32_t r = (uint32_t)(lane + 32 * i);
+        id[i] = r < rows ? row_at(P, p0 + r) : 0xffffffffu;
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+        if (id[i] != 0xffffffffu)
+#pragma unroll
+          for (int l = 0; l < NN / 32; ++l)
+            asm volatile("prefetch.global.L2 [%0];" :: "l"(P.x + (size_t)id[i] * NN + l * 32) : "memory");
+    };
+    if (!(P.dbg & 2)) {
+      constexpr int PF_AHEAD = 2;
+      for (int a = 0; a < PF_AHEAD; ++a) prefetch_rows(t_first + (uint32_t)a * t_step);
+      uint32_t k = 0;
+      for (uint32_t t = t_first + PF_AHEAD * t_step; t < ntiles; t += t_step, ++k) {
+        mbar_wait(&f_full[k % ts::FB], (k / ts::FB) & 1);
+        prefetch_rows(t);
+      }
+    }
+  } else if (warp >= PROD_WARP) {
+    regs_dec<REG_MISC>();  // idle (keeps the warpgroups whole for the register rebalancing)
+  } else if (warp >= EPI_WARPS) {
+    // ------------------------------------------------------------------ split warps ---
+    regs_inc<REG_SPLIT>();
+    const int sw = warp - EPI_WARPS;
+    const int g8 = lane >> 3, l8 = lane & 7;
+    // rows of 4-row group g (the conflict-free STS.64 pattern of hygt_gemm_kernel)
+    auto row_of_group = [&](int g) {
+      const int i = sw * ts::RG + g, b16 = i >> 2, gg = i & 3;
+      return b16 * 16 + (gg & 1) * 2 + (gg >> 1) * 8 + (g8 >> 1) + (g8 & 1) * 4;
+    };
+    constexpr int NV = NN / 32;
+    float4 held[ts::RG][NV];
+    auto tile_ids = [&](uint32_t t, uint32_t (&ids)[ts::RG]) {
+      if (t >= ntiles) {
+#pragma unroll
+        for (int g = 0; g < ts::RG; ++g) ids[g] = 0xffffffffu;
+        return;
+      }
+      int c;
+      uint64_t p0;
+      uint32_t rows;
+      tm_cta.of(t, c, p0, rows);
+#pragma unroll
+      for (int g = 0; g < ts::RG; ++g) {
+        const int r = row_of_group(g);
+        ids[g] = (uint32_t)r < rows ? row_at(P, p0 + r) : 0xffffffffu;
+      }
+    };
+    auto load_part = [&](const uint32_t (&ids)[ts::RG], int i) {
+#pragma unroll
+      for (int g = 0; g < ts::RG; ++g)
+        held[g][i] = ids[g] != 0xffffffffu
+                         ? __ldcs(reinterpret_cast<const float4*>(P.x + (size_t)ids[g] * NN) + i * 8 + l8)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
+    {
+      uint32_t ids[ts::RG];
+      tile_ids(t_first, ids);
+#pragma unroll
+      for (int i = 0; i < NV; ++i) load_part(ids, i);
+    }
+    uint32_t k = 0;
+    for (uint32_t t = t_first; t < ntiles; t += t_step, ++k) {
+      if (sw == 0 && lane == 0) GEMM_TRACE(k, 0);
+      float scl[ts::RG];
+#pragma unroll
+      for (int g = 0; g < ts::RG; ++g) {
+        float mx = 0.f;
+#pragma unroll
+        for (int i = 0; i < NV; ++i)
+          mx = fmaxf(mx, fmaxf(fmaxf(fabsf(held[g][i].x), fabsf(held[g][i].y)), fmaxf(fabsf(held[g][i].z), fabsf(held[g][i].w))));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+        scl[g] = row_scale(mx);
+      }
+      if (sw == 0 && lane == 0) GEMM_TRACE(k, 1);
+      {  // row unscale factors, read by the epilogues of both CTAs
+        const int fb = (int)(k % ts::FB);
+        if (k >= (uint32_t)ts::FB) mbar_wait(&f_empty[fb], ((k / ts::FB) - 1) & 1);
+        if (l8 == 0) {
+#pragma unroll
+          for (int g = 0; g < ts::RG; ++g) fac[fb * ts::CR + row_of_group(g)] = 1.f / scl[g];
+        }
+        __syncwarp();
+        if (lane == 0) {  // the peer's epilogue reads these over DSMEM: cluster-scope release (this
+                          // warp's global loads are all consumed here; the next tile's come below)
+          mbar_arrive(&f_full[fb]);
+          mbar_arrive_remote_release(&f_full[fb], peer);
+        }
+      }
+      uint32_t rnext[ts::RG];
+      tile_ids(t + t_step, rnext);
+      const int xb = (int)(k % ts::DBUF);
+      if (k >= (uint32_t)ts::DBUF) mbar_wait(&x_empty[xb], ((k / ts::DBUF) - 1) & 1);
+      if (sw == 0 && lane == 0) GEMM_TRACE(k, 12);
+      unsigned char* xt = sm + (uint32_t)xb * ts::TILE;
+#pragma unroll
+      for (int ka = 0; ka < ts::KA; ++ka) {
+        unsigned char* xhi = xt + (uint32_t)ka * 2 * ts::HALF;
+        unsigned char* xlo = xhi + ts::HALF;
+#pragma unroll
+        for (int g = 0; g < ts::RG; ++g) {
+          const int r = row_of_group(g);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const float4 v = held[g][2 * ka + h];
+            const float s = scl[g];
+            const float a0 = v.x * s, a1 = v.y * s, a2 = v.z * s, a3 = v.w * s;
+            const uint32_t h01 = pack_h2(a0, a1), h23 = pack_h2(a2, a3);
+            const float2 b01 = unpack_h2(h01), b23 = unpack_h2(h23);
+            const uint32_t l01 = pack_h2(a0 - b01.x, a1 - b01.y), l23 = pack_h2(a2 - b23.x, a3 - b23.y);
+            const uint32_t off = swz(r, h * 4 + (l8 >> 1)) + (uint32_t)(l8 & 1) * 8u;
+            *reinterpret_cast<uint2*>(xhi + off) = make_uint2(h01, h23);
+            *reinterpret_cast<uint2*>(xlo + off) = make_uint2(l01, l23);
+          }
+        }
+        load_part(rnext, 2 * ka);  // the next tile's atom ka, in flight from here
+        load_part(rnext, 2 * ka + 1);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic stores -> tensor core reads
+      __syncwarp();
+      if (lane == 0) {
+        if (rank == 0) mbar_arrive(&x_full[xb]); else mbar_arrive_remote(&x_full[xb], 0);
+      }
+      if (sw == 0 && lane == 0) GEMM_TRACE(k, 2);
+    }
+    // rows with an invalid class id (bucket C): copied through, the error is flagged by hygt_bucket
+    if (C > 0 && P.seg_end) {
+      const uint64_t s0 = seg_at(P, C - 1), s1 = seg_at(P, C);
+      for (uint64_t p = s0 + (uint64_t)blockIdx.x * SPLIT_WARPS * 4 + sw * 4 + g8; p < s1;
+           p += (uint64_t)gridDim.x * SPLIT_WARPS * 4) {
+        const uint32_t row = __ldg(P.idx + p);
+        const float4* src = reinterpret_cast<const float4*>(P.x + (size_t)row * NN);
+        float4* dst = reinterpret_cast<float4*>(P.y + (size_t)row * NN);
+        for (int i = l8; i < NN / 4; i += 8) dst[i] = src[i];
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ epilogue ------
+    // Thread = output column m = rank 128 + warp 32 + lane (TMEM lane). Per tile, per block of
+    // 32 rows one tcgen05.ld.32x32b.x32 (the next block's in flight); per row one broadcast
+    // LDS.64 of {row factor, row id} from the row table, and one STG.32 per warp = one whole
+    // 128 B line. The row table of tile k + 1 is resolved while tile k is stored: warp w looks
+    // up rows 32 w .. 32 w + 31 (tile lookup, row ids, the factors of the split that owns them:
+    // rank w / 2, over DSMEM for the peer's) with its loads issued at the top of tile k and the
+    // entries written at its end, ahead of one named barrier of the four epilogue warps per
+    // tile. Energy: the thread's column summed in fp32 per 16 rows, compensated (TwoSum)
+    // across blocks, fp64 atomics at the class flush. On a class change the class operator
+    // first: this thread's output row of the operator stages (hi and lo, de-swizzled) into
+    // TMEM lane m with tcgen05.st.
+    regs_dec<REG_EPI>();
+    const uint32_t col = rank * 128u + (uint32_t)(warp * 32 + lane);
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    float2* tab = reinterpret_cast<float2*>(sm + ts::TAB_OFF);  // [2][TR]
+    float ks = 0.f, kc = 0.f;
+    int cur = -1;
+    auto flush_energy = [&]() {
+      if (ENERGY && cur >= 0 && P.energy) {
+        const double v = (double)ks + (double)kc;
+        if (v != 0.0) atomicAdd(P.energy + (size_t)cur * NN + col, v);
+        ks = kc = 0.f;
+      }
+    };
+    // operator stages (gemm_build): [C][KA][2 halves][hi | lo][128 rows x 128 B, SW128]
+    constexpr uint32_t GSTAGE = 2u * 128 * 128;
+    const uint32_t orow = (uint32_t)(warp * 32 + lane);  // row of this CTA's half (= rank)
+    const uint32_t owner = (uint32_t)(warp >> 1);        // the CTA whose split owns rows 32 warp ..
+    // row lookup of tile t (k-th of this CTA): loads first, table entry written by finish()
+    struct Lookup { int c; uint32_t id; float f; };
+    auto lookup_issue = [&](uint32_t t, Lookup& L) {
+      uint64_t p0;
+      uint32_t rows;
+      tm_pair.of(t, L.c, p0, rows);
+      const uint32_t r = (uint32_t)(warp * 32 + lane);
+      L.id = r < rows ? row_at(P, p0 + r) : 0xffffffffu;
+      L.f = __ldg(P.unscale + L.c);
+    };
+    auto lookup_finish = [&](uint32_t k, Lookup& L) {  // after f_full: the row's factor, then the entry
+      const int fb = (int)(k % ts::FB);
+      mbar_wait_cluster(&f_full[fb], (k / ts::FB) & 1);  // pairs with the peer split's cluster release
+      const float* fp = fac + fb * ts::CR + ((warp * 32 + lane) & (ts::CR - 1));
+      const float fr = owner == rank ? *fp : ld_dsmem_f32(fp, owner);
+      tab[(k & 1) * ts::TR + warp * 32 + lane] = make_float2(fr * L.f, __uint_as_float(L.id));
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&f_empty[fb]);
+        mbar_arrive_remote(&f_empty[fb], peer);
+      }
+    };
+    auto epi_sync = [&]() { asm volatile("bar.sync 1, %0;" :: "n"(EPI_WARPS * 32) : "memory"); };
+    Lookup nxt;
+    if (t_first < ntiles) {
+      lookup_issue(t_first, nxt);
+      lookup_finish(0, nxt);
+    }
+    uint32_t k = 0;
+    for (uint32_t t = t_first; t < ntiles; t += t_step, ++k) {
+      const int c = nxt.c;
+      const bool more = t + t_step < ntiles;
+      if (more) lookup_issue(t + t_step, nxt);  // in flight while this tile is stored
+      if (c != cur) {
+        flush_energy();
+        // the previous tile's accumulator was waited for (d_full): every MMA that read the
+        // previous operator is complete, and the MMAs of this tile wait for op_full
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const unsigned char* src = P.bops + (size_t)c * ts::KA * 2 * GSTAGE + (size_t)rank * GSTAGE + (size_t)orow * 128;
+#pragma unroll 1
+        for (int part = 0; part < 2; ++part) {  // hi, lo
+#pragma unroll 1
+          for (int ka = 0; ka < ts::KA; ++ka) {
+            const uint4* s4 = reinterpret_cast<const uint4*>(src + (size_t)ka * 2 * GSTAGE + (size_t)part * (GSTAGE / 2));
+            uint32_t v[32];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {  // chunk q (K 8q .. 8q + 7) sits at 16 B slot q ^ (row & 7)
+              const uint4 u = __ldg(s4 + (q ^ (orow & 7)));
+              v[4 * q] = u.x; v[4 * q + 1] = u.y; v[4 * q + 2] = u.z; v[4 * q + 3] = u.w;
+            }
+            tmem_st32(tmem + lane_base + (part ? ts::OPLO : ts::OPHI) + 32u * ka, v);
+          }
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) {
+          if (rank == 0) mbar_arrive(op_full); else mbar_arrive_remote_release(op_full, 0);
+        }
+        cur = c;
+      }
+      epi_sync();  // the row table of tile k is complete
+      const int db = (int)(k & 1);
+      mbar_wait(&d_full[db], (k >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      if (warp == 0 && lane == 0) GEMM_TRACE(k, 5);
+      const uint32_t dbase = tmem + lane_base + ts::DCOL + (uint32_t)db * ts::TR;
+      const float2* tk = tab + (k & 1) * ts::TR;
+      uint32_t v[2][32];
+      tmem_ld32(dbase, v[0]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+        if (i + 1 < 4) tmem_ld32(dbase + 32u * (i + 1), v[(i + 1) & 1]);
+        if (i == 3) {  // accumulator read: release it to tile k + 2
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          __syncwarp();
+          if (lane == 0) {
+            if (rank == 0) mbar_arrive(&d_empty[db]); else mbar_arrive_remote(&d_empty[db], 0);
+          }
+        }
+        if (P.dbg & 32) continue;
+        float e0 = 0.f, e1 = 0.f;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float2 fe = tk[32 * i + j];  // broadcast
+          const uint32_t rid = __float_as_uint(fe.y);
+          const float val = __uint_as_float(v[i & 1][j]) * fe.x;
+          if (ENERGY) {
+            if (j & 1) e1 = fmaf(val, val, e1); else e0 = fmaf(val, val, e0);
+          }
+          if (rid != 0xffffffffu && !(P.dbg & 16)) __stcs(P.y + (size_t)rid * NN + col, val);
+        }
+        if (ENERGY) {  // rows past the tile's end are exact zeros (their B rows are zero)
+          const float ts_ = e0 + e1, tb = ts_ - e0;
+          const float te = (e0 - (ts_ - tb)) + (e1 - tb);
+          const float sn = ks + ts_, sbp = sn - ks;
+          kc += ((ks - (sn - sbp)) + (ts_ - sbp)) + te;
+          ks = sn;
+        }
+      }
+      if (more) lookup_finish(k + 1, nxt);  // the next tile's table entries
+      if (warp == 0 && lane == 0) GEMM_TRACE(k, 6);
+    }
+    flush_energy();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  cluster_sync();  // no peer access after this point
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == MMA_WARP) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" :: "r"(tmem));
 }
 
 // ---------------------------------------------------------------- host: operand builder ----
@@ -1109,7 +1719,7 @@ int gemm_smem_bytes(int n) {
   switch (n) {
     case 64: return (int)std::max(Shape<64, true, true>::smem(HYGT_GEMM_MAX_CLASSES), Shape<64, true, false>::smem(HYGT_GEMM_MAX_CLASSES));
     case 128: return (int)std::max(Shape<128, true, true>::smem(HYGT_GEMM_MAX_CLASSES), Shape<128, true, false>::smem(HYGT_GEMM_MAX_CLASSES));
-    case 256: return (int)Shape<256, true, false>::smem(HYGT_GEMM_MAX_CLASSES);
+    case 256: return (int)std::max(Shape<256, true, false>::smem(HYGT_GEMM_MAX_CLASSES), ts::smem(HYGT_GEMM_MAX_CLASSES));
     default: return 0;
   }
 }
@@ -1203,8 +1813,30 @@ int launch_one(const GemmParams& P, int num_sms, cudaStream_t st) {
   const cudaError_t e = cudaLaunchKernelEx(&cfg, fn, P);
   return e == cudaSuccess ? HYGT_OK : hygt_set_error(HYGT_ERR_CUDA, cudaGetErrorString(e));
 }
+template <bool E>
+int launch_ts(const GemmParams& P, int num_sms, cudaStream_t st) {
+  const auto fn = hygt_gemm_ts_kernel<E>;
+  const uint32_t smem = (ts::smem(P.classes) + 15u) & ~15u;
+  hygt_smem_attr(reinterpret_cast<const void*>(fn), smem);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  cfg.gridDim = dim3((unsigned)(num_sms / 2 * 2));
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, fn, P);
+  return e == cudaSuccess ? HYGT_OK : hygt_set_error(HYGT_ERR_CUDA, cudaGetErrorString(e));
+}
 template <int NN>
-int launch_n(const GemmParams& P, int grid, bool pair, bool wide, cudaStream_t st) {
+int launch_n(const GemmParams& P, int grid, bool pair, bool wide, bool tsf, cudaStream_t st) {
+  // N = 256 with CTA pairs: the operator-in-TMEM form (hygt_gemm_ts_kernel)
+  if (NN == 256 && pair && tsf) return P.energy ? launch_ts<true>(P, grid, st) : launch_ts<false>(P, grid, st);
   // wide: one unit of all N columns per tile, merged accumulator (N = 256 only with CTA pairs)
   // (the resident B hi halves at N = 256 leave room for at most 384 classes' tile table)
   if (pair && wide && (NN != 256 || P.classes <= 384))
@@ -1239,9 +1871,9 @@ int gemm_run(const GemmOperands& g, const float* x, float* y, const uint32_t* id
   const bool pair = g.pair && g.num_sms >= 2;
   const int grid = (int)std::min<uint64_t>((uint64_t)g.num_sms, pair ? 2 * ((tiles + 1) / 2) : tiles);
   switch (g.n) {
-    case 64: return launch_n<64>(P, grid, pair, g.wide, st);
-    case 128: return launch_n<128>(P, grid, pair, g.wide, st);
-    case 256: return launch_n<256>(P, grid, pair, g.wide, st);
+    case 64: return launch_n<64>(P, grid, pair, g.wide, g.ts, st);
+    case 128: return launch_n<128>(P, grid, pair, g.wide, g.ts, st);
+    case 256: return launch_n<256>(P, grid, pair, g.wide, g.ts, st);
     default: return hygt_set_error(HYGT_ERR_ARGUMENT, "gemm: unsupported N");
   }
 }

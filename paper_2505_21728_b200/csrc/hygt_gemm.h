@@ -22,7 +22,8 @@ struct GemmParams {
   unsigned long long* trace; // debug: per-tile clock64 events of CTA 0 ([64][16]) or nullptr
   int dbg;                   // diagnostic switches (test-hook knob HYGT_GEMM_DBG; wrong results when
                              // set): 1 B stages loaded once, 2 no L2 prefetch, 16 no output stores,
-                             // 32 accumulators released unread (streamed-B variants for 1)
+                             // 32 accumulators released unread (streamed-B variants for 1); 4 is
+                             // exact: N = 256 MMAs issued by a lone lane (the pre-elect.sync form)
 };
 
 struct GemmOperands {  // one direction
@@ -33,6 +34,9 @@ struct GemmOperands {  // one direction
   // the correction terms of all K accumulated before the main term; otherwise units of <= 128
   // columns with separate main / correction accumulators
   bool wide = true;
+  // N = 256 with CTA pairs: the class operator resident in TMEM as the MMA's A operand and the
+  // data rows as B (hygt_gemm_ts_kernel); otherwise the rows are A and the operator B
+  bool ts = true;
   unsigned char* d_ops = nullptr;
   float* d_unscale = nullptr;
 };

@@ -97,10 +97,12 @@ def test_gemm_invalid_class_ids(cuda):
         plan.sync_status()
 
 
-def test_plan_options_select_and_validate(cuda):
+def test_plan_options_select_and_validate(cuda, knob):
     """hygt_plan_options: "tensor" forces the composed-operator path where supported and is an
-    ArgumentError elsewhere; "butterfly" never takes it; single CTAs give the same results as
-    CTA pairs."""
+    ArgumentError elsewhere; "butterfly" never takes it. At N = 256 the CTA-pair build takes the
+    operator-in-TMEM form (same products, the MMA operand roles swapped, so the tensor cores
+    round a K step's sum in a different order): equal to the single-CTA build at the fp32 bar,
+    and its operand-in-shared-memory form (HYGT_GEMM_TS=0) equal bit for bit."""
     from paper_2505_21728_b200 import ArgumentError, HyGTModel, HyGTPlan
     rng = np.random.default_rng(5)
     ms = [HyGTModel(8, 2, rng.uniform(-np.pi, np.pi, 2 * 8 * 128)) for _ in range(3)]
@@ -114,16 +116,21 @@ def test_plan_options_select_and_validate(cuda):
     cls = torch.randint(0, 3, (4000,), device=cuda).to(torch.int16).view(torch.uint16)
     y1 = HyGTPlan(ms, kernel="tensor", cta_pairs=True).forward(x, cls)
     y0 = HyGTPlan(ms, kernel="tensor", cta_pairs=False).forward(x, cls)
-    assert torch.equal(y0, y1)  # same per-row arithmetic, only the operand staging differs
+    check_close(y1.cpu().numpy(), y0.cpu().numpy(), x.cpu().numpy(), "pair (TS) vs single")
+    knob("HYGT_GEMM_TS", "0")
+    y2 = HyGTPlan(ms, kernel="tensor", cta_pairs=True).forward(x, cls)
+    assert torch.equal(y0, y2)  # same per-row arithmetic, only the operand staging differs
 
 
 @pytest.mark.parametrize("log2n,classes", [(8, 400), (6, 300)])
-def test_gemm_many_classes_and_variants(cuda, oracle_mod, log2n, classes):
+def test_gemm_many_classes_and_variants(cuda, oracle_mod, log2n, classes, knob):
     """Many classes: at N = 256 more than 384 classes do not leave room for the per-class tile
     table next to the resident B hi halves, so the kernel takes the variant with units of 128
     columns and streamed B; at N = 64 the 256-row sub-tiled tiles meet a few rows per class.
     Forward with energy and inverse against the oracle, and the single-CTA build equal to the
-    CTA-pair build bit for bit (same per-row arithmetic and accumulation order)."""
+    CTA-pair build bit for bit (same per-row arithmetic and accumulation order; at N = 256 the
+    pair build's operand-in-shared-memory form, HYGT_GEMM_TS=0, and the default operator-in-TMEM
+    form at the fp32 bar)."""
     from paper_2505_21728_b200 import HyGTPlan
     plan, angles, perms, mask, rng = _case(log2n, 2, classes, "none", 41 + classes)
     n = 1 << log2n
@@ -141,4 +148,31 @@ def test_gemm_many_classes_and_variants(cuda, oracle_mod, log2n, classes):
     from paper_2505_21728_b200 import HyGTModel
     models = [HyGTModel(log2n, 2, angles[c]) for c in range(classes)]
     y1 = HyGTPlan(models, kernel="tensor", cta_pairs=False).forward(xd, cd)
+    if n == 256:
+        check_close(y.cpu().numpy(), y1.cpu().numpy(), x, "pair (TS) vs single")
+        knob("HYGT_GEMM_TS", "0")
+        y = HyGTPlan(models, kernel="tensor", cta_pairs=True).forward(xd, cd)
     assert torch.equal(y, y1)
+
+
+@pytest.mark.parametrize("classes", [400, 35])
+def test_gemm_n256_roundtrip_repeated(cuda, classes):
+    """N = 256 on the CTA pairs' operator-in-TMEM form, repeated: a class change on almost every
+    tile (400 classes, ~50 rows each) reloads the operator in TMEM over and over, and each
+    epilogue reads half of its row factors from the peer CTA over DSMEM (a CTA-scope release on
+    that hand-off once let stale power-of-two factors through, intermittently). Forward then
+    inverse returns the input, forward with energy equals forward bit for bit, every time."""
+    from paper_2505_21728_b200 import HyGTModel, HyGTPlan
+    rng = np.random.default_rng(70 + classes)
+    models = [HyGTModel(8, 2, rng.uniform(-np.pi, np.pi, 2 * 8 * 128)) for _ in range(classes)]
+    plan = HyGTPlan(models, kernel="tensor")
+    x = torch.from_numpy((rng.standard_normal((20000, 256)) * 16).astype(np.float32)).to(cuda)
+    cls = torch.from_numpy(rng.integers(0, classes, 20000).astype(np.uint16)).to(cuda)
+    scale = float(x.abs().max())
+    for _ in range(4):
+        y = plan.forward(x, cls)
+        e = torch.zeros(classes, 256, dtype=torch.float64, device=cuda)
+        y2 = plan.forward_energy(x, cls, e)
+        z = plan.inverse(y, cls)
+        assert torch.equal(y, y2)
+        assert float((z - x).abs().max()) <= 1e-5 * scale

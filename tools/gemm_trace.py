@@ -41,8 +41,8 @@ torch.cuda.synchronize()
 lib.hygt_debug_gemm_trace(None)
 t = tr.view(64, 16).cpu().numpy()
 t0 = t[0, 0]
-names = ["p1s", "p1e", "p2e", "mmaS", "mmaC", "epiS", "epiE", "-", "b00", "b01", "b02", "b03", "b10", "b11", "b12", "b13"]
-print("tile " + " ".join(f"{n:>8s}" for n in names) + "   (cycles since tile 0 pass-1 start)")
+names = ["p1s", "p1e", "p2e", "mmaS", "mmaC", "epiS", "epiE", "-", "b00", "b01", "b02", "b03", "a0free", "a0done", "a1free", "a1done"]
+print("tile " + " ".join(f"{n:>8s}" for n in names) + "   (cycles since tile 0 pass-1 start; b0x: MMA issue points, aN: split atom N slot free / written)")
 for k in range(64):
     if t[k, 6] == 0:
         break

@@ -26,10 +26,10 @@ __host__ __device__ constexpr uint32_t idesc_f16(int n, int m) {
 
 // A: 128 rows x 4 K atoms (64 fp16 each) = 64 KB; B: BN rows x 4 atoms
 template <bool PAIR, int NN, int NACC, int MM = PAIR ? 256 : 128>
-__global__ void __cluster_dims__(PAIR ? 2 : 1, 1, 1) rate(int iters, unsigned long long* cycles) {
+__global__ void __cluster_dims__(PAIR ? 2 : 1, 1, 1) rate(int iters, int commit_every, unsigned long long* cycles) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint32_t base_sh;
-  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t bar, cbar;
   constexpr int BN = PAIR ? NN / 2 : NN;
   const int warp = threadIdx.x >> 5;
   uint32_t rank = 0;
@@ -51,6 +51,7 @@ __global__ void __cluster_dims__(PAIR ? 2 : 1, 1, 1) rate(int iters, unsigned lo
   }
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&bar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&cbar)));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("fence.proxy.async.shared::cta;");
@@ -78,6 +79,13 @@ __global__ void __cluster_dims__(PAIR ? 2 : 1, 1, 1) rate(int iters, unsigned lo
             asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                          "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
                          :: "r"(d), "l"(da), "l"(db), "r"(idesc_f16(NN, 128)), "r"(acc));
+          if (commit_every && ((ka * 4 + j + 1) & (commit_every - 1)) == 0) {
+            if (PAIR)
+              asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                           :: "r"(smem_u32(&cbar)), "h"((uint16_t)3) : "memory");
+            else
+              asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(smem_u32(&cbar)) : "memory");
+          }
         }
     }
     if (PAIR)
@@ -99,13 +107,13 @@ __global__ void __cluster_dims__(PAIR ? 2 : 1, 1, 1) rate(int iters, unsigned lo
 }
 
 template <bool PAIR, int NN, int NACC, int MM = PAIR ? 256 : 128>
-int run(int sms, unsigned long long* cyc) {
+int run(int sms, unsigned long long* cyc, int ce = 0, int threads = 128, int extra = 0) {
   const int iters = 2000;
   constexpr int BN = PAIR ? NN / 2 : NN;
-  const int smem = 128 * 512 + BN * 512 + 1024;
+  const int smem = 128 * 512 + BN * 512 + 1024 + extra;
   cudaFuncSetAttribute(rate<PAIR, NN, NACC, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaMemset(cyc, 0, sizeof(unsigned long long) * sms);
-  rate<PAIR, NN, NACC, MM><<<sms / 2 * 2, 128, smem>>>(iters, cyc);
+  rate<PAIR, NN, NACC, MM><<<sms / 2 * 2, threads, smem>>>(iters, ce, cyc);
   if (cudaDeviceSynchronize() != cudaSuccess) { printf("error %s\n", cudaGetErrorString(cudaGetLastError())); return 1; }
   std::vector<unsigned long long> h(sms);
   cudaMemcpy(h.data(), cyc, sizeof(unsigned long long) * sms, cudaMemcpyDeviceToHost);
@@ -115,8 +123,8 @@ int run(int sms, unsigned long long* cyc) {
   mean /= n;
   const double per = mean / (iters * 16.0);
   const double mac_per_sm = (double)MM * NN * 16 / (PAIR ? 2 : 1);
-  printf("%s M=%d N=%3d accumulators %d: %.1f cycles/instr, %.0f MAC/clk/SM (ideal cycles %.0f at 4096)\n",
-         PAIR ? "cta_group::2" : "cta_group::1", MM, NN, NACC, per, mac_per_sm / per, mac_per_sm / 4096);
+  printf("%s M=%d N=%3d accumulators %d, commit every %2d, %d threads, smem %d: %.1f cycles/instr, %.0f MAC/clk/SM (ideal cycles %.0f at 4096)\n",
+         PAIR ? "cta_group::2" : "cta_group::1", MM, NN, NACC, ce, threads, smem, per, mac_per_sm / per, mac_per_sm / 4096);
   return 0;
 }
 
@@ -126,14 +134,11 @@ int main() {
   unsigned long long* cyc;
   cudaMalloc(&cyc, sizeof(unsigned long long) * sms);
   int e = 0;
-  e |= run<false, 256, 1>(sms, cyc);
-  e |= run<false, 256, 2>(sms, cyc);
-  e |= run<true, 256, 1>(sms, cyc);
-  e |= run<true, 256, 2>(sms, cyc);
-  e |= run<false, 128, 1>(sms, cyc);
-  e |= run<true, 128, 1>(sms, cyc);
-  e |= run<true, 128, 2>(sms, cyc);
-  e |= run<true, 256, 1, 128>(sms, cyc);
-  e |= run<true, 256, 2, 128>(sms, cyc);
+  for (int ce : {0, 16, 4, 1}) {
+    e |= run<true, 256, 1>(sms, cyc, ce);
+    e |= run<true, 256, 2>(sms, cyc, ce);
+    e |= run<false, 256, 1>(sms, cyc, ce);
+    e |= run<false, 128, 1>(sms, cyc, ce);
+  }
   return e;
 }
