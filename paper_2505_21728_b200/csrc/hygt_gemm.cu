@@ -1226,14 +1226,19 @@ constexpr int KA = 4;                         // K atoms of 64
 constexpr uint32_t HALF = CR * 128;           // one K atom, hi or lo, of this CTA's rows (8 KB)
 constexpr uint32_t TILE = KA * 2 * HALF;      // 64 KB
 constexpr int DBUF = 3;                       // data tiles resident
-constexpr int FB = 4;                         // row-factor buffers
-constexpr uint32_t FAC_OFF = DBUF * TILE;     // [FB][CR] f32
-constexpr uint32_t TAB_OFF = FAC_OFF + FB * CR * 4;  // [2][TR] {row factor, row id}: the epilogue's row table
-constexpr uint32_t BAR_OFF = TAB_OFF + 2 * TR * 8;
+constexpr int FB = 4;                         // row tables (tiles in flight split -> epilogue)
+constexpr uint32_t TAB_OFF = DBUF * TILE;     // [FB][TR] {row factor, row id}
+constexpr uint32_t BAR_OFF = TAB_OFF + FB * TR * 8;
 constexpr uint32_t TE_OFF = BAR_OFF + 256;    // + [C] u32 tile_end, [C] u32 bucket ends
 constexpr uint32_t smem(int classes) { return TE_OFF + 8u * (uint32_t)classes; }
 constexpr uint32_t OPHI = 0, OPLO = 128, DCOL = 256;  // TMEM columns: operator hi / lo, 2 accumulators of 128
 constexpr int RG = CR / SPLIT_WARPS / 4;     // 4-row groups per split lane
+}  // namespace ts
+// registers per thread after setmaxnreg: the split holds half the tile the SS form's does, the
+// epilogue keeps two 32-column TMEM loads and the energy in flight
+constexpr int TS_REG_EPI = 160, TS_REG_SPLIT = 144;
+static_assert(TS_REG_EPI + 2 * TS_REG_SPLIT + REG_MISC <= 512, "register pool");
+namespace ts {
 static_assert(RG == 2, "split layout");
 }  // namespace ts
 
@@ -1271,13 +1276,32 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
 }
-// read a float from the same shared-memory offset in CTA `cta` of the cluster
-__device__ __forceinline__ float ld_dsmem_f32(const float* p, uint32_t cta) {
-  float v;
+// Tiles of one CTA in increasing order: the class index only moves forward, so the lookup is
+// an incremental scan of the shared tile_end / bucket-end tables (no binary search per tile)
+struct TileCursor {
+  const uint32_t* tile_end;  // shared [C]
+  const uint32_t* seg;       // shared [C]: bucket ends
+  int classes;
+  uint32_t tg, part, cr;
+  int c = 0;
+  __device__ __forceinline__ int cls(uint32_t t) {
+    while (c < classes - 1 && tile_end[c] <= t) ++c;
+    return c;
+  }
+  __device__ __forceinline__ void of(uint32_t t, int& cc, uint64_t& p0, uint32_t& rows) {
+    cc = cls(t);
+    const uint32_t first_tile = cc ? tile_end[cc - 1] : 0u;
+    const uint64_t s0 = cc ? (uint64_t)seg[cc - 1] : 0ull, s1 = seg[cc];
+    p0 = s0 + (uint64_t)(t - first_tile) * tg + part;
+    const uint64_t left = s1 > p0 ? s1 - p0 : 0ull;
+    rows = left < cr ? (uint32_t)left : cr;
+  }
+};
+// store a float2 at the same shared-memory offset in CTA `cta` of the cluster
+__device__ __forceinline__ void st_dsmem_f2(float2* p, uint32_t cta, float2 v) {
   asm volatile(
-      "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %1, %2;\n\tld.shared::cluster.f32 %0, [ra];\n\t}\n"
-      : "=f"(v) : "r"(smem_u32(p)), "r"(cta) : "memory");
-  return v;
+      "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\tst.shared::cluster.v2.f32 [ra], {%2, %3};\n\t}\n"
+      :: "r"(smem_u32(p)), "r"(cta), "f"(v.x), "f"(v.y) : "memory");
 }
 
 template <bool ENERGY>
@@ -1289,20 +1313,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_ts_kernel(const Gem
   uint64_t* x_empty = x_full + ts::DBUF;    // [DBUF] data tile read by the MMAs (commit, both CTAs)
   uint64_t* d_full = x_empty + ts::DBUF;    // [2]    accumulator done (commit, both CTAs)
   uint64_t* d_empty = d_full + 2;           // [2]    accumulator read (rank 0: count 2 EPI_WARPS)
-  uint64_t* f_full = d_empty + 2;           // [FB]   row factors written (count 2 SPLIT_WARPS: both CTAs)
-  uint64_t* f_empty = f_full + ts::FB;      // [FB]   row factors read (count 2 EPI_WARPS: both CTAs)
+  uint64_t* f_split = d_empty + 2;          // [FB]   this CTA's half of the row table written (count SPLIT_WARPS)
+  uint64_t* f_full = f_split + ts::FB;      // [FB]   row table complete (count 2: the relays of both CTAs)
+  uint64_t* f_empty = f_full + ts::FB;      // [FB]   row table read (count 2 EPI_WARPS: both epilogues)
   uint64_t* op_full = f_empty + ts::FB;     // [1]    class operator in TMEM (rank 0: count 2 EPI_WARPS)
   uint32_t* tmem_sh = reinterpret_cast<uint32_t*>(op_full + 1);
-  static_assert(3 * 2 + 4 + 2 * 4 + 1 <= 30, "barrier area");
+  static_assert((2 * ts::DBUF + 4 + 3 * ts::FB + 1) * 8 + 4 <= 256, "barrier area");
   uint32_t* tile_end_sh = reinterpret_cast<uint32_t*>(sm + ts::TE_OFF);
-  uint32_t* seg_sh = tile_end_sh + P.classes;  // [C] bucket ends: tile lookups without global loads
-  float* fac = reinterpret_cast<float*>(sm + ts::FAC_OFF);  // [FB][CR] this CTA's row unscale factors
+  uint32_t* seg_sh = tile_end_sh + P.classes;  // [C] bucket ends
+  // [FB][TR] row table {row factor (1 / row scale x class unscale), row id (bits)}: rows
+  // rank 64 .. written by this CTA's split, the other half copied in by the peer's relay warp;
+  // read by this CTA's epilogue
+  float2* tab = reinterpret_cast<float2*>(sm + ts::TAB_OFF);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int C = P.classes;
   const uint32_t rank = cluster_rank(), peer = rank ^ 1u;
   const uint32_t t_first = cluster_id(), t_step = cluster_count();
-  if (warp == 0) {  // per-class cumulative tile counts (tiles of TR rows)
+  if (warp == 0) {  // per-class cumulative tile counts (tiles of TR rows), bucket ends
     uint32_t run = 0;
     for (int c0 = 0; c0 < C; c0 += 32) {
       const int c = c0 + lane;
@@ -1329,7 +1357,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_ts_kernel(const Gem
   if (tid == 0) {
     for (int i = 0; i < ts::DBUF; ++i) { mbar_init(&x_full[i], 2 * SPLIT_WARPS); mbar_init(&x_empty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&d_full[i], 1); mbar_init(&d_empty[i], 2 * EPI_WARPS); }
-    for (int i = 0; i < ts::FB; ++i) { mbar_init(&f_full[i], 2 * SPLIT_WARPS); mbar_init(&f_empty[i], 2 * EPI_WARPS); }
+    for (int i = 0; i < ts::FB; ++i) {
+      mbar_init(&f_split[i], SPLIT_WARPS);
+      mbar_init(&f_full[i], 2);
+      mbar_init(&f_empty[i], 2 * EPI_WARPS);
+    }
     mbar_init(op_full, 2 * EPI_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
@@ -1338,28 +1370,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_ts_kernel(const Gem
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_sh;
   const uint32_t ntiles = C ? tile_end_sh[C - 1] : 0u;
-  // this CTA's rows of a tile (split, prefetch) and the whole tile (epilogue)
-  const uint32_t* segs = (P.dbg & 8) ? nullptr : seg_sh;
-  const TileMap tm_cta{tile_end_sh, &P, C, (uint32_t)ts::TR, rank * (uint32_t)ts::CR, (uint32_t)ts::CR, segs};
-  const TileMap tm_pair{tile_end_sh, &P, C, (uint32_t)ts::TR, 0u, (uint32_t)ts::TR, segs};
-  auto class_of = [&](uint32_t t) {
-    int lo = 0, hi = C - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (tile_end_sh[mid] <= t) lo = mid + 1; else hi = mid;
-    }
-    return lo;
-  };
 
   if (warp == MMA_WARP) {
     // ------------------------------------------------------------------ MMA issuer ----
     regs_dec<REG_MISC>();
     if (rank == 0) {  // the whole warp, one elected lane issues (see elect_one)
       const bool leader = elect_one();
+      TileCursor cur_t{tile_end_sh, seg_sh, C, 0, 0, 0};
       uint32_t k = 0, nop = 0;
       int cur = -1;
       for (uint32_t t = t_first; t < ntiles; t += t_step, ++k) {
-        const int c = class_of(t);
+        const int c = cur_t.cls(t);
         if (c != cur) {  // both CTAs' epilogues wrote this class's operator into TMEM
           mbar_wait(op_full, nop & 1);
           ++nop;
@@ -1395,12 +1416,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_ts_kernel(const Gem
     // ------------------------------------------------------------------ row prefetch --
     regs_dec<REG_MISC>();
     // L2 prefetch of this CTA's rows of the tile 2 steps ahead, paced by the split (f_full)
+    TileCursor cur_t{tile_end_sh, seg_sh, C, (uint32_t)ts::TR, rank * (uint32_t)ts::CR, (uint32_t)ts::CR};
     auto prefetch_rows = [&](uint32_t tp) {
       if (tp >= ntiles) return;
       int c;
       uint64_t p0;
       uint32_t rows;
-      tm_cta.of(tp, c, p0, rows);
+      cur_t.of(tp, c, p0, rows);
       uint32_t id[2];
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
@@ -1423,11 +1445,34 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_ts_kernel(const Gem
         prefetch_rows(t);
       }
     }
-  } else if (warp >= PROD_WARP) {
+  } else if (warp == PROD_WARP) {
+    // ------------------------------------------------------------------ row-table relay
+    regs_dec<REG_MISC>();
+    // Per tile: once this CTA's split wrote its half of the row table (f_split), copy the half
+    // into the peer's table over DSMEM and signal both tables' f_full, the peer's with a
+    // cluster-scope release: the release (a memory barrier) waits only for these stores, not
+    // for the split warps' global loads in flight.
+    const float2* mine = tab + rank * ts::CR;
+    uint32_t k = 0;
+    for (uint32_t t = t_first; t < ntiles; t += t_step, ++k) {
+      const int fb = (int)(k % ts::FB);
+      mbar_wait(&f_split[fb], (k / ts::FB) & 1);
+#pragma unroll
+      for (int i = 0; i < ts::CR / 32; ++i) {
+        const float2* e = mine + fb * ts::TR + 32 * i + lane;
+        st_dsmem_f2(const_cast<float2*>(e), peer, *e);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&f_full[fb]);
+        mbar_arrive_remote_release(&f_full[fb], peer);
+      }
+    }
+  } else if (warp > PROD_WARP) {
     regs_dec<REG_MISC>();  // idle (keeps the warpgroups whole for the register rebalancing)
   } else if (warp >= EPI_WARPS) {
     // ------------------------------------------------------------------ split warps ---
-    regs_inc<REG_SPLIT>();
+    regs_inc<TS_REG_SPLIT>();
     const int sw = warp - EPI_WARPS;
     const int g8 = lane >> 3, l8 = lane & 7;
     // rows of 4-row group g (the conflict-free STS.64 pattern of hygt_gemm_kernel)
@@ -1437,21 +1482,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_ts_kernel(const Gem
     };
     constexpr int NV = NN / 32;
     float4 held[ts::RG][NV];
+    TileCursor cur_t{tile_end_sh, seg_sh, C, (uint32_t)ts::TR, rank * (uint32_t)ts::CR, (uint32_t)ts::CR};
+    // row ids of this CTA's rows of tile t (and its class)
     auto tile_ids = [&](uint32_t t, uint32_t (&ids)[ts::RG]) {
       if (t >= ntiles) {
 #pragma unroll
         for (int g = 0; g < ts::RG; ++g) ids[g] = 0xffffffffu;
-        return;
+        return 0;
       }
       int c;
       uint64_t p0;
       uint32_t rows;
-      tm_cta.of(t, c, p0, rows);
+      cur_t.of(t, c, p0, rows);
 #pragma unroll
       for (int g = 0; g < ts::RG; ++g) {
         const int r = row_of_group(g);
         ids[g] = (uint32_t)r < rows ? row_at(P, p0 + r) : 0xffffffffu;
       }
+      return c;
     };
     auto load_part = [&](const uint32_t (&ids)[ts::RG], int i) {
 #pragma unroll
@@ -1460,12 +1508,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_ts_kernel(const Gem
                          ? __ldcs(reinterpret_cast<const float4*>(P.x + (size_t)ids[g] * NN) + i * 8 + l8)
                          : make_float4(0.f, 0.f, 0.f, 0.f);
     };
-    {
-      uint32_t ids[ts::RG];
-      tile_ids(t_first, ids);
+    uint32_t ids[ts::RG];
+    int cls = tile_ids(t_first, ids);
 #pragma unroll
-      for (int i = 0; i < NV; ++i) load_part(ids, i);
-    }
+    for (int i = 0; i < NV; ++i) load_part(ids, i);
     uint32_t k = 0;
     for (uint32_t t = t_first; t < ntiles; t += t_step, ++k) {
       if (sw == 0 && lane == 0) GEMM_TRACE(k, 0);
@@ -1482,22 +1528,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_ts_kernel(const Gem
         scl[g] = row_scale(mx);
       }
       if (sw == 0 && lane == 0) GEMM_TRACE(k, 1);
-      {  // row unscale factors, read by the epilogues of both CTAs
+      {  // this CTA's rows of the row table (the relay warp copies them to the peer)
         const int fb = (int)(k % ts::FB);
-        if (k >= (uint32_t)ts::FB) mbar_wait(&f_empty[fb], ((k / ts::FB) - 1) & 1);
+        const float ucls = __ldg(P.unscale + cls);
+        if (k >= (uint32_t)ts::FB) mbar_wait(&f_empty[fb], ((k / ts::FB) - 1) & 1);  // both epilogues done with fb
         if (l8 == 0) {
 #pragma unroll
-          for (int g = 0; g < ts::RG; ++g) fac[fb * ts::CR + row_of_group(g)] = 1.f / scl[g];
+          for (int g = 0; g < ts::RG; ++g)
+            tab[fb * ts::TR + rank * ts::CR + row_of_group(g)] = make_float2(ucls / scl[g], __uint_as_float(ids[g]));
         }
         __syncwarp();
-        if (lane == 0) {  // the peer's epilogue reads these over DSMEM: cluster-scope release (this
-                          // warp's global loads are all consumed here; the next tile's come below)
-          mbar_arrive(&f_full[fb]);
-          mbar_arrive_remote_release(&f_full[fb], peer);
-        }
+        if (lane == 0) mbar_arrive(&f_split[fb]);
       }
       uint32_t rnext[ts::RG];
-      tile_ids(t + t_step, rnext);
+      const int cnext = tile_ids(t + t_step, rnext);
       const int xb = (int)(k % ts::DBUF);
       if (k >= (uint32_t)ts::DBUF) mbar_wait(&x_empty[xb], ((k / ts::DBUF) - 1) & 1);
       if (sw == 0 && lane == 0) GEMM_TRACE(k, 12);
@@ -1531,6 +1575,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_ts_kernel(const Gem
         if (rank == 0) mbar_arrive(&x_full[xb]); else mbar_arrive_remote(&x_full[xb], 0);
       }
       if (sw == 0 && lane == 0) GEMM_TRACE(k, 2);
+#pragma unroll
+      for (int g = 0; g < ts::RG; ++g) ids[g] = rnext[g];
+      cls = cnext;
     }
     // rows with an invalid class id (bucket C): copied through, the error is flagged by hygt_bucket
     if (C > 0 && P.seg_end) {
@@ -1547,19 +1594,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_ts_kernel(const Gem
     // ------------------------------------------------------------------ epilogue ------
     // Thread = output column m = rank 128 + warp 32 + lane (TMEM lane). Per tile, per block of
     // 32 rows one tcgen05.ld.32x32b.x32 (the next block's in flight); per row one broadcast
-    // LDS.64 of {row factor, row id} from the row table, and one STG.32 per warp = one whole
-    // 128 B line. The row table of tile k + 1 is resolved while tile k is stored: warp w looks
-    // up rows 32 w .. 32 w + 31 (tile lookup, row ids, the factors of the split that owns them:
-    // rank w / 2, over DSMEM for the peer's) with its loads issued at the top of tile k and the
-    // entries written at its end, ahead of one named barrier of the four epilogue warps per
-    // tile. Energy: the thread's column summed in fp32 per 16 rows, compensated (TwoSum)
-    // across blocks, fp64 atomics at the class flush. On a class change the class operator
-    // first: this thread's output row of the operator stages (hi and lo, de-swizzled) into
-    // TMEM lane m with tcgen05.st.
-    regs_dec<REG_EPI>();
+    // LDS.64 of {row factor, row id} from the row table the splits of both CTAs filled, and
+    // one STG.32 per warp = one whole 128 B line. Energy: the thread's column summed in fp32
+    // per 16 rows, compensated (TwoSum) across blocks, fp64 atomics at the class flush. On a
+    // class change first the class operator: this thread's output row of the operator stages
+    // (hi and lo, de-swizzled) into TMEM lane m with tcgen05.st.
+    regs_inc<TS_REG_EPI>();
     const uint32_t col = rank * 128u + (uint32_t)(warp * 32 + lane);
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-    float2* tab = reinterpret_cast<float2*>(sm + ts::TAB_OFF);  // [2][TR]
+    float* ycol = P.y + col;
     float ks = 0.f, kc = 0.f;
     int cur = -1;
     auto flush_energy = [&]() {
@@ -1572,40 +1615,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_ts_kernel(const Gem
     // operator stages (gemm_build): [C][KA][2 halves][hi | lo][128 rows x 128 B, SW128]
     constexpr uint32_t GSTAGE = 2u * 128 * 128;
     const uint32_t orow = (uint32_t)(warp * 32 + lane);  // row of this CTA's half (= rank)
-    const uint32_t owner = (uint32_t)(warp >> 1);        // the CTA whose split owns rows 32 warp ..
-    // row lookup of tile t (k-th of this CTA): loads first, table entry written by finish()
-    struct Lookup { int c; uint32_t id; float f; };
-    auto lookup_issue = [&](uint32_t t, Lookup& L) {
-      uint64_t p0;
-      uint32_t rows;
-      tm_pair.of(t, L.c, p0, rows);
-      const uint32_t r = (uint32_t)(warp * 32 + lane);
-      L.id = r < rows ? row_at(P, p0 + r) : 0xffffffffu;
-      L.f = __ldg(P.unscale + L.c);
-    };
-    auto lookup_finish = [&](uint32_t k, Lookup& L) {  // after f_full: the row's factor, then the entry
-      const int fb = (int)(k % ts::FB);
-      mbar_wait_cluster(&f_full[fb], (k / ts::FB) & 1);  // pairs with the peer split's cluster release
-      const float* fp = fac + fb * ts::CR + ((warp * 32 + lane) & (ts::CR - 1));
-      const float fr = owner == rank ? *fp : ld_dsmem_f32(fp, owner);
-      tab[(k & 1) * ts::TR + warp * 32 + lane] = make_float2(fr * L.f, __uint_as_float(L.id));
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&f_empty[fb]);
-        mbar_arrive_remote(&f_empty[fb], peer);
-      }
-    };
-    auto epi_sync = [&]() { asm volatile("bar.sync 1, %0;" :: "n"(EPI_WARPS * 32) : "memory"); };
-    Lookup nxt;
-    if (t_first < ntiles) {
-      lookup_issue(t_first, nxt);
-      lookup_finish(0, nxt);
-    }
+    TileCursor cur_t{tile_end_sh, seg_sh, C, 0, 0, 0};
     uint32_t k = 0;
     for (uint32_t t = t_first; t < ntiles; t += t_step, ++k) {
-      const int c = nxt.c;
-      const bool more = t + t_step < ntiles;
-      if (more) lookup_issue(t + t_step, nxt);  // in flight while this tile is stored
+      const int c = cur_t.cls(t);
       if (c != cur) {
         flush_energy();
         // the previous tile's accumulator was waited for (d_full): every MMA that read the
@@ -1634,13 +1647,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_ts_kernel(const Gem
         }
         cur = c;
       }
-      epi_sync();  // the row table of tile k is complete
-      const int db = (int)(k & 1);
+      const int fb = (int)(k % ts::FB), db = (int)(k & 1);
+      mbar_wait_cluster(&f_full[fb], (k / ts::FB) & 1);  // pairs with the relays' cluster release
       mbar_wait(&d_full[db], (k >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       if (warp == 0 && lane == 0) GEMM_TRACE(k, 5);
       const uint32_t dbase = tmem + lane_base + ts::DCOL + (uint32_t)db * ts::TR;
-      const float2* tk = tab + (k & 1) * ts::TR;
+      const float2* tk = tab + fb * ts::TR;
       uint32_t v[2][32];
       tmem_ld32(dbase, v[0]);
 #pragma unroll
@@ -1664,7 +1677,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_ts_kernel(const Gem
           if (ENERGY) {
             if (j & 1) e1 = fmaf(val, val, e1); else e0 = fmaf(val, val, e0);
           }
-          if (rid != 0xffffffffu && !(P.dbg & 16)) __stcs(P.y + (size_t)rid * NN + col, val);
+          if (rid != 0xffffffffu && !(P.dbg & 16)) __stcs(ycol + (size_t)rid * NN, val);
         }
         if (ENERGY) {  // rows past the tile's end are exact zeros (their B rows are zero)
           const float ts_ = e0 + e1, tb = ts_ - e0;
@@ -1674,7 +1687,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) hygt_gemm_ts_kernel(const Gem
           ks = sn;
         }
       }
-      if (more) lookup_finish(k + 1, nxt);  // the next tile's table entries
+      __syncwarp();
+      if (lane == 0) {  // row table fb read: both splits may refill it
+        mbar_arrive(&f_empty[fb]);
+        mbar_arrive_remote(&f_empty[fb], peer);
+      }
       if (warp == 0 && lane == 0) GEMM_TRACE(k, 6);
     }
     flush_energy();
