@@ -153,7 +153,7 @@ _KERNEL_NAMES = {
     "seg2": "hygt_seg2_kernel",
     "tile": "hygt_tile_kernel",
     "bucketed": "hygt_apply_kernel",
-    "gemm": "hygt_gemm_kernel (composed per-class operator, tcgen05.mma kind::f16 3-term split)",
+    "gemm": "hygt_gemm_kernel / hygt_gemm_ts_kernel at N = 256 (composed per-class operator, tcgen05.mma kind::f16 3-term split)",
 }
 
 
