@@ -192,9 +192,10 @@ extern "C" int hygt_correlation_f64(int log2_n, int classes, const float* d_x, c
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (hygt_gpu::corr_tc_supported(log2_n) && hygt_gpu::knob("HYGT_CORR_TC", 1) != 0) {
-    // N = 64: exact integer-digit products on the tensor cores (hygt_corr_tc.cu)
+    // N >= 64: exact integer-digit products on the tensor cores (hygt_corr_tc.cu)
     hygt_gpu::CorrTcParams Q{};
     Q.x = d_x;
+    Q.n = 1 << log2_n;
     Q.idx = P.idx;
     Q.seg_end = P.seg_end;
     Q.classes = classes;

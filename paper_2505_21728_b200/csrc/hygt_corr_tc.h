@@ -10,6 +10,7 @@ struct CorrTcParams {
   const float* x;
   const uint32_t* idx;      // bucketed position -> row (nullptr: identity, one class)
   const uint32_t* seg_end;  // [C+1] run ends
+  int n;                    // samples per row: 64, 128 or 256
   int classes;
   uint64_t count;
   double* sum;              // [C][N][N]

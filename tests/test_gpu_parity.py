@@ -826,39 +826,45 @@ def test_fast_form_input_limit(cuda, oracle_mod, config):
     check_close(y.cpu().numpy(), ref, x.cpu().numpy(), f"cfg{config} at 2^38")
 
 
+@pytest.mark.parametrize("log2n", [6, 7, 8])
 @pytest.mark.parametrize("case", ["ar1_35_classes", "magnitudes"])
-def test_correlation_tensor_cores_n64(cuda, oracle_mod, case, knob):
-    """N = 64 correlation on the tensor cores (hygt_corr_tc.cu: 7 int8 digits per sample relative
-    to a per-column power of two, exact int32 accumulation per digit level, fp64 at run flushes)
-    against the oracle's exact-product fp64 accumulator, at the fp64 bar of the SIMT path
-    (max-abs <= 1e-12 of the class's largest sum): config-3 rows (2^20, 35 classes), and rows
-    whose columns span 1e-20 .. 1e20 with outlier rows (exponent re-bases), zero columns and a
-    class without rows. Also equal, at the same bar, to the SIMT kernel (HYGT_CORR_TC=0)."""
+def test_correlation_tensor_cores(cuda, oracle_mod, case, knob, log2n):
+    """Correlation on the tensor cores (hygt_corr_tc.cu: 7 int8 digits per sample relative to a
+    per-column power of two, exact int32 accumulation per digit level, fp64 at run flushes;
+    N = 64 by digit stacks, N = 128 / 256 by 64-column block-pair roles) against the oracle's
+    exact-product fp64 accumulator, at the fp64 bar of the SIMT path (max-abs <= 1e-12 of the
+    class's largest sum): config-3 / config-5 rows (35 classes), and rows whose columns span
+    1e-20 .. 1e20 with outlier rows (exponent re-bases), zero columns and a class without rows.
+    Also equal, at the same bar, to the SIMT kernel (HYGT_CORR_TC=0)."""
     from paper_2505_21728_b200 import correlation
     from oracle import oracle as O
-    rng = np.random.default_rng(64)
+    rng = np.random.default_rng(64 + log2n)
+    n = 1 << log2n
     if case == "ar1_35_classes":
         from paper_2505_21728_b200.synth import make_workload
-        w = make_workload(3)
-        count, classes = 1 << 20, 35
+        w = make_workload(3 if log2n == 6 else 5)
+        count, classes = {6: 1 << 20, 7: 1 << 18, 8: 1 << 17}[log2n], 35
         cd = w.make_classes(count)
         xd = w.make_rows(count, cd)
+        if log2n == 7:  # config 5's rows, first 128 samples of each
+            xd = xd[:, :128].contiguous()
         x, cls = xd.cpu().numpy(), cd.cpu().numpy()
     else:
-        count, classes = 50000, 4
-        x = rng.standard_normal((count, 64)) * (10.0 ** np.linspace(-20, 20, 64))[None, :]
+        count, classes = {6: 50000, 7: 30000, 8: 20000}[log2n], 4
+        x = rng.standard_normal((count, n)) * (10.0 ** np.linspace(-20, 20, n))[None, :]
         x[rng.integers(0, count, 40)] *= 1e6  # outliers: the run's scale grows mid-run
         x[:, 5] = 0.0
         x = x.astype(np.float32)
         cls = rng.integers(0, 3, count).astype(np.uint16)  # class 3 has no rows
         xd, cd = torch.from_numpy(x).to(cuda), torch.from_numpy(cls).to(cuda)
-    ref_s, ref_k = O.correlation(6, classes, x, cls)
+    ref_s, ref_k = O.correlation(log2n, classes, x, cls)
     s, k = correlation(xd, cd, classes)
     assert np.array_equal(k.cpu().numpy().astype(np.uint64), ref_k)
     s = s.cpu().numpy()
     for c in range(classes):
         bar = 1e-12 * np.abs(ref_s[c]).max()
         assert np.abs(s[c] - ref_s[c]).max() <= bar, f"class {c}: {np.abs(s[c] - ref_s[c]).max():.3e} vs {bar:.3e}"
+        assert np.abs(s[c] - s[c].T).max() <= bar, f"class {c}: not symmetric"
     knob("HYGT_CORR_TC", "0")
     s0, _ = correlation(xd, cd, classes)
     s0 = s0.cpu().numpy()
