@@ -196,6 +196,7 @@ extern "C" int hygt_correlation_f64(int log2_n, int classes, const float* d_x, c
     hygt_gpu::CorrTcParams Q{};
     Q.x = d_x;
     Q.n = 1 << log2_n;
+    Q.dbg = hygt_gpu::knob("HYGT_CORR_DBG", 0);
     Q.idx = P.idx;
     Q.seg_end = P.seg_end;
     Q.classes = classes;

@@ -104,6 +104,7 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
   d |= (uint64_t)2 << 61;
   return d;
 }
+constexpr uint32_t DESC_HI = (uint32_t)(((uint64_t)(1024 >> 4) << 32 | (uint64_t)1 << 46 | (uint64_t)2 << 61) >> 32);
 // D s32, A and B signed 8-bit, both K-major, N = 64, M = 128
 constexpr uint32_t IDESC_I8 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(CN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 __device__ __forceinline__ uint32_t swz(int r, int q) { return (uint32_t)r * 128u + (uint32_t)((q ^ (r & 7)) << 4); }
@@ -207,9 +208,9 @@ __global__ void __launch_bounds__(Geo<PR>::THREADS, 1) corr_tc_kernel(const Corr
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_sh;
 
-  // MMA issue for tile k in buffer b (one thread, once the tile's digits are complete); pairs:
-  // issuer `is` issues the digit pairs of its levels
-  auto issue_mma = [&](uint32_t k, int is) {
+  // N = 64: MMA issue for tile k in buffer b (the MMA warp's lane 0, once the tile's digits are
+  // complete)
+  auto issue_mma = [&](uint32_t k) {
     const int b = (int)(k & 1);
     mbar_wait(&a_full[b], (k >> 1) & 1);
     asm volatile("tcgen05.fence::after_thread_sync;");
@@ -230,22 +231,53 @@ __global__ void __launch_bounds__(Geo<PR>::THREADS, 1) corr_tc_kernel(const Corr
     };
 #pragma unroll 1
     for (int q = 0; q < NDIG; ++q) {
-      if constexpr (PR) {
-        const uint64_t db = desc_sw128(base + (uint32_t)q * G::PSTRIDE + SLICE);  // digit q of block J
+      const uint64_t db = desc_sw128(base + (uint32_t)q * SLICE);
 #pragma unroll 1
-        for (int p = 0; p + q <= NDIG - 1; ++p) {
-          const int L = p + q;
-          if (L != is && L != NDIG - 1 - is) continue;
-          mma4(L, desc_sw128(base + (uint32_t)p * G::PSTRIDE), db);
-        }
-      } else {
-        const uint64_t db = desc_sw128(base + (uint32_t)q * SLICE);
-#pragma unroll 1
-        for (int p0 = 0; p0 + q <= NDIG - 1; p0 += 2) mma4(p0 + q, desc_sw128(base + (uint32_t)p0 * SLICE), db);
-      }
+      for (int p0 = 0; p0 + q <= NDIG - 1; p0 += 2) mma4(p0 + q, desc_sw128(base + (uint32_t)p0 * SLICE), db);
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                  :: "r"(su32(&a_empty[b])) : "memory");
+  };
+  // Pairs: issuer warp `is` (converged; one elected lane issues, as in hygt_gemm.cu's elect_one,
+  // so the descriptors stay in uniform registers) issues the digit pairs of levels is and 6 - is
+  // of tile k: A = stack p, B = digit q of block J.
+  auto issue_pr = [&](uint32_t k, int is) {
+    const int b = (int)(k & 1);
+    mbar_wait(&a_full[b], (k >> 1) & 1);
+    __syncwarp();  // lanes leave the wait loop independently
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    uint32_t leader;
+    asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}\n" : "=r"(leader));
+    if (leader) {
+      const uint32_t fresh = flag[2 + b] != 0 ? 1u : 0u;
+      // descriptor low words (start address >> 4 | LBO); the high word (SBO = 1024 B, version,
+      // SWIZZLE_128B) is the constant DESC_HI, joined inside the asm: ptxas 12.9 dropped the high
+      // word of 64-bit descriptor arithmetic hoisted into uniform registers here
+      const uint32_t lo0 = (uint32_t)desc_sw128(su32(sm + b * G::BUF));
+      constexpr uint32_t PST = G::PSTRIDE >> 4, SL = SLICE >> 4;  // descriptor address units
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int L = t ? NDIG - 1 - is : is;
+        if (t && L == is) break;
+        const uint32_t d = tmem + (uint32_t)(L * CN);
+#pragma unroll 1
+        for (int pp = 0; pp <= L; ++pp) {
+          const uint32_t la = lo0 + (uint32_t)pp * PST, lb = lo0 + (uint32_t)(L - pp) * PST + SL;
+          const uint32_t acc = (fresh && pp == 0) ? 0u : 1u;
+#pragma unroll
+          for (int j = 0; j < KT / 32; ++j)
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t.reg .b64 da, db;\n\t"
+                "mov.b64 da, {%1, %5};\n\tmov.b64 db, {%2, %5};\n\t"
+                "setp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], da, db, %3, p;\n\t}\n"
+                :: "r"(d), "r"(la + 2u * j), "r"(lb + 2u * j), "r"(IDESC_I8), "r"(j ? 1u : acc), "r"(DESC_HI));
+        }
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                   :: "r"(su32(&a_empty[b])) : "memory");
+    }
+    __syncwarp();
   };
   if (!PR && warp == SW) {
     // ---------------------------------------------------------------- MMA issuer ----
@@ -253,7 +285,7 @@ __global__ void __launch_bounds__(Geo<PR>::THREADS, 1) corr_tc_kernel(const Corr
       int f = f0;
       uint64_t pos = beg < seg_start(f0) ? seg_start(f0) : beg;
       Seg t;
-      for (uint32_t k = 0; next_tile(f, pos, t); ++k) issue_mma(k, 0);
+      for (uint32_t k = 0; next_tile(f, pos, t); ++k) issue_mma(k);
     }
   } else {
     // ---------------------------------------------------------------- split warps ----
@@ -337,17 +369,19 @@ __global__ void __launch_bounds__(Geo<PR>::THREADS, 1) corr_tc_kernel(const Corr
       const uint32_t rr = min((uint32_t)(g * 16 + (lane & 15)), t.rows - 1u);
       return P.idx ? __ldg(P.idx + t.p0 + rr) : (uint32_t)(t.p0 + rr);
     };
+    const char* xb = reinterpret_cast<const char*>(P.x + col0 + lane);
+    const uint32_t rowb = (uint32_t)n * 4u;
     auto load_x = [&](uint32_t ids, float (&v)[16][2]) {
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
         const uint32_t row = __shfl_sync(0xffffffffu, ids, r);
-        const float* src = P.x + (uint64_t)row * n + col0;
+        const float* src = reinterpret_cast<const float*>(xb + (uint64_t)row * rowb);  // IMAD.WIDE.U32
         if constexpr (PR) {  // the other roles' CTAs read these rows too: keep them in L2
-          v[r][0] = __ldg(src + lane);
-          v[r][1] = __ldg(src + lane + 32);
+          v[r][0] = __ldg(src);
+          v[r][1] = __ldg(src + 32);
         } else {
-          v[r][0] = __ldcs(src + lane);
-          v[r][1] = __ldcs(src + lane + 32);
+          v[r][0] = __ldcs(src);
+          v[r][1] = __ldcs(src + 32);
         }
       }
     };
@@ -367,9 +401,11 @@ __global__ void __launch_bounds__(Geo<PR>::THREADS, 1) corr_tc_kernel(const Corr
       last_f = t.f;
       // rows past the tile's end (warp-uniform): zero
       const int nvalid = (int)t.rows - g * 16;
+      if (nvalid < 16) {
 #pragma unroll
-      for (int r = 0; r < 16; ++r)
-        if (r >= nvalid) v[r][0] = v[r][1] = 0.f;
+        for (int r = 0; r < 16; ++r)
+          if (r >= nvalid) v[r][0] = v[r][1] = 0.f;
+      }
       float m0 = 0.f, m1 = 0.f;
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
@@ -451,7 +487,7 @@ __global__ void __launch_bounds__(Geo<PR>::THREADS, 1) corr_tc_kernel(const Corr
       __syncwarp();
       ++used[b];
       if (lane == 0) mbar_arrive(&a_full[b]);
-      if (PR && w < G::NISSUE && lane == 0) issue_mma(k, w);
+      if (PR && w < G::NISSUE) issue_pr(k, w);
     };
     auto advance = [&]() {
       tq[0] = tq[1];

@@ -16,6 +16,7 @@ struct CorrTcParams {
   double* sum;              // [C][N][N]
   unsigned long long* cnt;  // [C]
   uint64_t cta_span;        // set by corr_tc_run
+  int dbg;                  // development switches (HYGT_CORR_DBG through the test hook)
 };
 
 bool corr_tc_supported(int log2n);
