@@ -870,3 +870,43 @@ def test_correlation_tensor_cores(cuda, oracle_mod, case, knob, log2n):
     s0 = s0.cpu().numpy()
     for c in range(classes):
         assert np.abs(s0[c] - s[c]).max() <= 2e-12 * max(np.abs(ref_s[c]).max(), 1e-300)
+
+@pytest.mark.parametrize("log2n", [2, 4, 6, 8])
+def test_acceptance_criterion4_model_sweep(cuda, oracle_mod, log2n):
+    """The reference's acceptance criterion 4 (tests/acceptance.cpp:151-182) on the GPU path: 100
+    random models per N in {4, 16, 64, 256}, rounds 1 + trial % 3, a final permutation on odd trials;
+    T Tᵀ = I and inverse(forward(x)) = x. The reference holds both to 1e-12 in fp64; here T is read
+    off the fp32 kernels (identity rows in, one class per model), so the bars are the fp32 parity
+    ones, and T itself is also compared with the oracle's."""
+    n = 1 << log2n
+    rng = np.random.default_rng(1000 + log2n)
+    worst_o = worst_r = 0.0
+    for rounds in (1, 2, 3):
+        for with_perm in (False, True):
+            # trials with this (rounds, permutation) combination: trial % 3 == rounds - 1, trial % 2
+            k = len([t for t in range(100) if t % 3 == rounds - 1 and (t % 2 == 1) == with_perm])
+            angles = rng.uniform(-np.pi, np.pi, (k, rounds * log2n * (n // 2)))
+            perms = mask = None
+            if with_perm:
+                perms = np.tile(np.arange(n, dtype=np.uint16), (k, rounds, 1))
+                for c in range(k):
+                    perms[c, rounds - 1] = rng.permutation(n).astype(np.uint16)
+                mask = 1 << (rounds - 1)
+            plan = _plan(_models(log2n, rounds, angles, perms, mask or 0))
+            eye = np.tile(np.eye(n, dtype=np.float32), (k, 1))
+            vec = rng.standard_normal((k, n)).astype(np.float32)
+            xh = np.concatenate([eye, vec])
+            ch = np.concatenate([np.repeat(np.arange(k), n), np.arange(k)]).astype(np.uint16)
+            xd, cd = torch.from_numpy(xh).to(cuda), torch.from_numpy(ch).to(cuda)
+            y = plan.forward(xd, cd)
+            back = plan.inverse(y, cd)
+            plan.sync_status()
+            yh = y.cpu().numpy().astype(np.float64)
+            ref = oracle_mod.apply_batch(log2n, rounds, angles, perms, mask or 0, xh, ch)
+            check_close(yh, ref, xh, f"N={n} R={rounds} perm={with_perm} ({plan.algorithm})")
+            t = yh[: k * n].reshape(k, n, n)  # row i of block c = T_c e_i, so the block is T_cᵀ
+            ortho = np.abs(np.einsum("cij,ckj->cik", t, t) - np.eye(n)).max()
+            rt = np.abs(back.cpu().numpy() - xh).max()
+            worst_o, worst_r = max(worst_o, ortho), max(worst_r, rt)
+            assert ortho < 1e-5, f"N={n} R={rounds} perm={with_perm}: T Tᵀ - I = {ortho:.2e}"
+            assert rt < 1e-5 * max(1.0, np.abs(xh).max()), f"N={n} R={rounds} perm={with_perm}: round trip {rt:.2e}"
