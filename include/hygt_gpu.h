@@ -233,6 +233,18 @@ int hygt_klt_forward_f32(const hygt_klt_plan* plan, const float* d_x, float* d_y
 int hygt_klt_inverse_f32(const hygt_klt_plan* plan, const float* d_y, float* d_x,
                          const uint16_t* d_cls, uint64_t count, void* d_ws, size_t ws_bytes,
                          void* stream);
+/* The class dispatch of run_apply (hygt_main.cpp:143-149) is the same for both directions of a
+ * batch: hygt_klt_bucket groups the rows once (as hygt_bucket does for HyGT plans), and the _ex
+ * entry points take HYGT_REUSE_BUCKETS in `flags` to run on that grouping (tensor-core plans,
+ * n >= 16; the flag is ignored by the SIMT kernel, which reads d_cls directly). */
+int hygt_klt_bucket(const hygt_klt_plan* plan, const uint16_t* d_cls, uint64_t count, void* d_ws,
+                    size_t ws_bytes, void* stream);
+int hygt_klt_forward_f32_ex(const hygt_klt_plan* plan, const float* d_x, float* d_y,
+                            const uint16_t* d_cls, uint64_t count, void* d_ws, size_t ws_bytes,
+                            uint32_t flags, void* stream);
+int hygt_klt_inverse_f32_ex(const hygt_klt_plan* plan, const float* d_y, float* d_x,
+                            const uint16_t* d_cls, uint64_t count, void* d_ws, size_t ws_bytes,
+                            uint32_t flags, void* stream);
 
 /* ---- synthetic workloads, generated on the device -------------------------
  * Separable 2-D AR(1) rows (covariance sigma^2 * A (x) A, A_ij = rho^|i-j|, raster order,

@@ -45,6 +45,9 @@ SIGNATURES = {
     "hygt_klt_workspace_bytes": (_sz, [_p, _u64]),
     "hygt_klt_forward_f32": (_i, [_p, _p, _p, _p, _u64, _p, _sz, _p]),
     "hygt_klt_inverse_f32": (_i, [_p, _p, _p, _p, _u64, _p, _sz, _p]),
+    "hygt_klt_bucket": (_i, [_p, _p, _u64, _p, _sz, _p]),
+    "hygt_klt_forward_f32_ex": (_i, [_p, _p, _p, _p, _u64, _p, _sz, _u32, _p]),
+    "hygt_klt_inverse_f32_ex": (_i, [_p, _p, _p, _p, _u64, _p, _sz, _u32, _p]),
     "hygt_synth_rows_f32": (_i, [_p, _u64, _u64, _i, _p, _p, _i, _f, _f, _f, _f, _u64, _p]),
     "hygt_synth_classes": (_i, [_p, _u64, _u64, _i, _u64, _p]),
 }

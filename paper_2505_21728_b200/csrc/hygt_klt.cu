@@ -281,7 +281,7 @@ int launch_tc(const hygt_klt_plan* p, int dir, const float* in, float* out, cons
 }
 
 int run_klt(const hygt_klt_plan* p, bool fwd, const float* in, float* out, const uint16_t* cls,
-            uint64_t count, void* ws, size_t ws_bytes, cudaStream_t st) {
+            uint64_t count, void* ws, size_t ws_bytes, cudaStream_t st, bool reuse = false) {
   if (!p) return kfail(HYGT_ERR_ARGUMENT, "klt: null plan");
   if (!count) return HYGT_OK;
   if (p->gemm) {  // per-class grouped GEMM on the tensor cores (in place allowed)
@@ -294,7 +294,7 @@ int run_klt(const hygt_klt_plan* p, bool fwd, const float* in, float* out, const
     if (cls && p->classes > 1) {
       if (!ws || ws_bytes < hygt_gpu::bucket_ws_bytes(p->classes, 0, count))
         return kfail(HYGT_ERR_ARGUMENT, "klt: workspace too small");
-      if (int s = hygt_gpu::bucket_rows(p->classes, 0, cls, count, ws, ws_bytes, true, st, &idx, &seg, &nseg))
+      if (int s = hygt_gpu::bucket_rows(p->classes, 0, cls, count, ws, ws_bytes, !reuse, st, &idx, &seg, &nseg))
         return s;
     }
     return hygt_gpu::gemm_run(p->gops[fwd ? 0 : 1], in, out, idx, seg, count, nullptr, st);
@@ -307,7 +307,7 @@ int run_klt(const hygt_klt_plan* p, bool fwd, const float* in, float* out, const
     if (cls && p->classes > 1) {
       if (!ws || ws_bytes < hygt_gpu::bucket_ws_bytes(p->classes, 0, count))
         return kfail(HYGT_ERR_ARGUMENT, "klt: workspace too small");
-      if (int s = hygt_gpu::bucket_rows(p->classes, 0, cls, count, ws, ws_bytes, true, st, &idx, &seg, &nseg))
+      if (int s = hygt_gpu::bucket_rows(p->classes, 0, cls, count, ws, ws_bytes, !reuse, st, &idx, &seg, &nseg))
         return s;
     }
     const int dir = fwd ? 0 : 1;
@@ -424,4 +424,34 @@ extern "C" int hygt_klt_inverse_f32(const hygt_klt_plan* plan, const float* d_y,
   HYGT_NVTX("hygt_klt_inverse_f32");
   return run_klt(plan, false, d_y, d_x, d_cls, count, d_ws, ws_bytes,
                  reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int hygt_klt_bucket(const hygt_klt_plan* plan, const uint16_t* d_cls, uint64_t count,
+                               void* d_ws, size_t ws_bytes, void* stream) {
+  HYGT_NVTX("hygt_klt_bucket");
+  if (!plan) return kfail(HYGT_ERR_ARGUMENT, "klt: null plan");
+  if (!count || !d_cls || plan->classes <= 1 || !(plan->gemm || plan->tc)) return HYGT_OK;
+  if (!d_ws || ws_bytes < hygt_gpu::bucket_ws_bytes(plan->classes, 0, count))
+    return kfail(HYGT_ERR_ARGUMENT, "klt: workspace too small");
+  const uint32_t* idx = nullptr;
+  const uint32_t* seg = nullptr;
+  uint32_t nseg = 0;
+  return hygt_gpu::bucket_rows(plan->classes, 0, d_cls, count, d_ws, ws_bytes, true,
+                               reinterpret_cast<cudaStream_t>(stream), &idx, &seg, &nseg);
+}
+
+extern "C" int hygt_klt_forward_f32_ex(const hygt_klt_plan* plan, const float* d_x, float* d_y,
+                                       const uint16_t* d_cls, uint64_t count, void* d_ws,
+                                       size_t ws_bytes, uint32_t flags, void* stream) {
+  HYGT_NVTX("hygt_klt_forward_f32");
+  return run_klt(plan, true, d_x, d_y, d_cls, count, d_ws, ws_bytes,
+                 reinterpret_cast<cudaStream_t>(stream), (flags & HYGT_REUSE_BUCKETS) != 0);
+}
+
+extern "C" int hygt_klt_inverse_f32_ex(const hygt_klt_plan* plan, const float* d_y, float* d_x,
+                                       const uint16_t* d_cls, uint64_t count, void* d_ws,
+                                       size_t ws_bytes, uint32_t flags, void* stream) {
+  HYGT_NVTX("hygt_klt_inverse_f32");
+  return run_klt(plan, false, d_y, d_x, d_cls, count, d_ws, ws_bytes,
+                 reinterpret_cast<cudaStream_t>(stream), (flags & HYGT_REUSE_BUCKETS) != 0);
 }

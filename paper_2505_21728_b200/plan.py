@@ -408,9 +408,9 @@ class KLTPlan:
         return "klt_tc_kernel (tcgen05.mma kind::tf32, 3xTF32)" if self.n in (16, 32) else "klt_simt_kernel"
 
     def launches_per_call(self) -> int:
-        return 4 if self.classes > 1 else 1  # bucketing (3) + the GEMM kernel
+        return 4 if self.classes > 1 else 1  # bucketing (3) + the GEMM kernel (1 with reuse_buckets)
 
-    def _run(self, fn, x, cls, out, stream, workspace=None):
+    def _run(self, fn, x, cls, out, stream, workspace=None, reuse_buckets=False):
         if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dtype != torch.float32:
             raise ArgumentError("KLTPlan: x must be a CUDA float32 tensor")
         if x.shape[-1] != self.n or not x.is_contiguous():
@@ -418,6 +418,8 @@ class KLTPlan:
         count = x.numel() // self.n
         _ensure(cls, "KLTPlan cls", _CLS_DTYPES, count, x.device, optional=True)
         nbytes = max(256, self.workspace_bytes(count))
+        if reuse_buckets and workspace is None:
+            raise ArgumentError("KLTPlan: reuse_buckets needs the workspace bucket() filled")
         with _on_stream(stream):
             if out is None:
                 out = torch.empty_like(x)
@@ -429,16 +431,26 @@ class KLTPlan:
         if ws.numel() < nbytes:
             raise ArgumentError("hygt_klt: workspace too small")
         _check(fn(self._h, x.data_ptr(), out.data_ptr(), _dev_ptr(cls), count, ws.data_ptr(),
-                  ws.numel(), _stream_ptr(stream)))
+                  ws.numel(), HYGT_REUSE_BUCKETS if reuse_buckets else 0, _stream_ptr(stream)))
         return out
 
-    def forward(self, x, cls=None, out=None, stream=None, workspace=None):
-        """y = K_c x per row on the tensor cores, rows of class c = cls[row]."""
-        return self._run(_lib.lib().hygt_klt_forward_f32, x, cls, out, stream, workspace)
+    def bucket(self, cls, count, workspace, stream=None):
+        """Group the rows by class once; forward / inverse with reuse_buckets=True then run on
+        that grouping (the class dispatch of run_apply is the same for both directions)."""
+        _ensure(cls, "KLTPlan cls", _CLS_DTYPES, count, None)
+        _ensure(workspace, "KLTPlan workspace", (torch.uint8,), None, cls.device)
+        if workspace.numel() < max(256, self.workspace_bytes(count)):
+            raise ArgumentError("hygt_klt: workspace too small")
+        _check(_lib.lib().hygt_klt_bucket(self._h, _dev_ptr(cls), count, workspace.data_ptr(),
+                                          workspace.numel(), _stream_ptr(stream)))
 
-    def inverse(self, y, cls=None, out=None, stream=None, workspace=None):
+    def forward(self, x, cls=None, out=None, stream=None, workspace=None, reuse_buckets=False):
+        """y = K_c x per row on the tensor cores, rows of class c = cls[row]."""
+        return self._run(_lib.lib().hygt_klt_forward_f32_ex, x, cls, out, stream, workspace, reuse_buckets)
+
+    def inverse(self, y, cls=None, out=None, stream=None, workspace=None, reuse_buckets=False):
         """x = K_c^T y per row."""
-        return self._run(_lib.lib().hygt_klt_inverse_f32, y, cls, out, stream, workspace)
+        return self._run(_lib.lib().hygt_klt_inverse_f32_ex, y, cls, out, stream, workspace, reuse_buckets)
 
 
 # ------------------------------------------------ single-vector drop-ins (transform.hpp) ----

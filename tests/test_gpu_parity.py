@@ -910,3 +910,27 @@ def test_acceptance_criterion4_model_sweep(cuda, oracle_mod, log2n):
             worst_o, worst_r = max(worst_o, ortho), max(worst_r, rt)
             assert ortho < 1e-5, f"N={n} R={rounds} perm={with_perm}: T Tᵀ - I = {ortho:.2e}"
             assert rt < 1e-5 * max(1.0, np.abs(xh).max()), f"N={n} R={rounds} perm={with_perm}: round trip {rt:.2e}"
+
+
+@pytest.mark.parametrize("n,classes", [(16, 5), (64, 35), (256, 4)])
+def test_klt_bucket_once_reuse_both_directions(cuda, oracle_mod, n, classes):
+    """hygt_klt_bucket + HYGT_REUSE_BUCKETS: one class grouping serves forward and inverse (the
+    bench's config-4 step), bit-identical to the calls that bucket themselves."""
+    from paper_2505_21728_b200 import ArgumentError, KLTPlan
+    rng = np.random.default_rng(40 + n)
+    k = np.stack([np.linalg.qr(rng.standard_normal((n, n)))[0] for _ in range(classes)])
+    plan = KLTPlan(k)
+    rows = 5000
+    xh = (rng.standard_normal((rows, n)) * 16).astype(np.float32)
+    ch = rng.integers(0, classes, rows).astype(np.uint16)
+    x, cls = torch.from_numpy(xh).to(cuda), torch.from_numpy(ch).to(cuda)
+    y0 = plan.forward(x, cls)
+    b0 = plan.inverse(y0, cls)
+    ws = torch.zeros(max(256, plan.workspace_bytes(rows)), dtype=torch.uint8, device=cuda)
+    plan.bucket(cls, rows, ws)
+    y1 = plan.forward(x, cls, workspace=ws, reuse_buckets=True)
+    b1 = plan.inverse(y1, cls, workspace=ws, reuse_buckets=True)
+    assert torch.equal(y0, y1) and torch.equal(b0, b1)
+    check_close(y1.cpu().numpy(), oracle_mod.klt_apply(k, xh, ch), xh, f"klt reuse n={n}")
+    with pytest.raises(ArgumentError):
+        plan.forward(x, cls, reuse_buckets=True)  # no workspace to reuse

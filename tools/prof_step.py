@@ -34,8 +34,9 @@ if w.cfg.klt:  # config 4: the KLT comparison path
         if a.range and i == a.steps - 1:
             torch.cuda.synchronize()
             torch.cuda.profiler.start()
-        kplan.forward(x, cls, out=y, workspace=kws)
-        kplan.inverse(y, cls, out=xr, workspace=kws)
+        kplan.bucket(cls, rows, kws)
+        kplan.forward(x, cls, out=y, workspace=kws, reuse_buckets=True)
+        kplan.inverse(y, cls, out=xr, workspace=kws, reuse_buckets=True)
     torch.cuda.synchronize()
     if a.range:
         torch.cuda.profiler.stop()
