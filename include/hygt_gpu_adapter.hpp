@@ -8,7 +8,12 @@
 //     hygt::gpu::inverse (same signatures, fp32 device arithmetic);
 //   * forward_fixed / inverse_fixed (fixedpoint.hpp:191-224) -> hygt::gpu::FixedPlan;
 //   * the whole `hygt apply` data path on a ResidualDataset (hygt_main.cpp:130-172)
-//     -> hygt::gpu::apply(bundle, dataset, forward, fixed).
+//     -> hygt::gpu::apply(bundle, dataset, forward, fixed);
+//   * klt_forward (statistics.hpp:222-224) and its transpose -> hygt::gpu::KLTPlan (batches, one
+//     KLTResult per class) and hygt::gpu::klt_forward (one vector, same signature);
+//   * the per-class CorrelationAccumulator loop of `hygt train` (hygt_main.cpp:85-87,
+//     statistics.hpp:63-99) -> hygt::gpu::class_correlations(dataset);
+//   * hygt::optimize (optimizer.hpp:311-371) -> hygt::gpu::optimize.
 // Non-zero C-ABI statuses are rethrown as the reference's exception classes (errors.hpp:23-45).
 #pragma once
 
@@ -16,6 +21,8 @@
 
 #include <cmath>
 #include <cstdint>
+#include <optional>
+#include <span>
 #include <string>
 #include <utility>
 #include <vector>
@@ -258,6 +265,105 @@ inline ResidualDataset apply(const ModelBundle& bundle, const ResidualDataset& d
       out[r] = {cls[r], std::vector<double>(x.begin() + r * n, x.begin() + (r + 1) * n)};
   }
   return ResidualDataset(ds.log2_n(), ds.class_count(), std::move(out));
+}
+
+// Per-class dense KLT: y = K_c r (klt_forward, statistics.hpp:222-224 -> multiply,
+// matrix.hpp:70-80) and x = K_c^T y (transposed, matrix.hpp:82-88), rows of KLTResult::basis =
+// basis vectors. Device rows in/out, stream-ordered; n a power of two in [2, 256].
+class KLTPlan {
+ public:
+  explicit KLTPlan(const std::vector<KLTResult>& klts) {
+    if (klts.empty()) throw ArgumentError("gpu::KLTPlan: need at least one class");
+    n_ = klts.front().basis.n();
+    std::vector<double> k;
+    for (const auto& r : klts) {
+      if (r.basis.n() != n_) throw ArgumentError("matrix dimension mismatch");
+      k.insert(k.end(), r.basis.data().begin(), r.basis.data().end());
+    }
+    check(hygt_klt_plan_create(static_cast<int>(n_), static_cast<int>(klts.size()), k.data(), 0, &plan_));
+  }
+  ~KLTPlan() { hygt_klt_plan_destroy(plan_); }
+  KLTPlan(const KLTPlan&) = delete;
+  KLTPlan& operator=(const KLTPlan&) = delete;
+  std::size_t dimension() const { return n_; }
+
+  // Groups the rows by class once; forward / inverse with reuse = true then run on that grouping.
+  void bucket(const std::uint16_t* d_cls, std::size_t count, cudaStream_t stream = nullptr) {
+    ws_.resize(hygt_klt_workspace_bytes(plan_, count));
+    check(hygt_klt_bucket(plan_, d_cls, count, ws_.p, ws_.n, stream));
+  }
+  void forward(const float* d_x, float* d_y, const std::uint16_t* d_cls, std::size_t count,
+               cudaStream_t stream = nullptr, bool reuse = false) {
+    ws_.resize(hygt_klt_workspace_bytes(plan_, count));
+    check(hygt_klt_forward_f32_ex(plan_, d_x, d_y, d_cls, count, ws_.p, ws_.n, reuse ? HYGT_REUSE_BUCKETS : 0u, stream));
+  }
+  void inverse(const float* d_y, float* d_x, const std::uint16_t* d_cls, std::size_t count,
+               cudaStream_t stream = nullptr, bool reuse = false) {
+    ws_.resize(hygt_klt_workspace_bytes(plan_, count));
+    check(hygt_klt_inverse_f32_ex(plan_, d_y, d_x, d_cls, count, ws_.p, ws_.n, reuse ? HYGT_REUSE_BUCKETS : 0u, stream));
+  }
+
+ private:
+  hygt_klt_plan* plan_ = nullptr;
+  std::size_t n_ = 0;
+  DeviceBuffer<unsigned char> ws_;
+};
+
+// One-vector drop-in with the signature of klt_forward (statistics.hpp:222).
+inline std::vector<double> klt_forward(const KLTResult& klt, std::span<const double> r) {
+  if (r.size() != klt.basis.n()) throw ArgumentError("matrix/vector dimension mismatch");
+  KLTPlan plan({klt});
+  std::vector<float> h(r.begin(), r.end());
+  DeviceBuffer<float> d(h.size()), o(h.size());
+  cuda_check(cudaMemcpy(d.p, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+  plan.forward(d.p, o.p, nullptr, 1);
+  cuda_check(cudaMemcpy(h.data(), o.p, h.size() * 4, cudaMemcpyDeviceToHost));
+  return std::vector<double>(h.begin(), h.end());
+}
+
+// The per-class CorrelationAccumulator loop of `hygt train` (hygt_main.cpp:85-87): for every
+// class, finalize() of the accumulator over its blocks (statistics.hpp:63-99), or nullopt for a
+// class without samples (finalize would throw). Samples are taken as fp32, as RBLK stores them
+// (dataset.hpp:68-70): every product is exact in fp64, as in the reference.
+inline std::vector<std::optional<CorrelationMatrix>> class_correlations(const ResidualDataset& ds) {
+  const std::size_t n = ds.dimension(), rows = ds.blocks().size(), classes = ds.class_count();
+  if (ds.log2_n() < 2 || ds.log2_n() > 8) throw ArgumentError("gpu::class_correlations: log2_n must be in [2, 8]");
+  std::vector<float> x(rows * n);
+  std::vector<std::uint16_t> cls(rows);
+  for (std::size_t r = 0; r < rows; ++r) {
+    cls[r] = ds.blocks()[r].class_id;
+    for (std::size_t i = 0; i < n; ++i) x[r * n + i] = static_cast<float>(ds.blocks()[r].values[i]);
+  }
+  DeviceBuffer<float> dx(x.size());
+  DeviceBuffer<std::uint16_t> dc(rows);
+  DeviceBuffer<double> dsum(classes * n * n);
+  DeviceBuffer<unsigned long long> dcnt(classes);
+  DeviceBuffer<unsigned char> ws(std::max<std::size_t>(256, hygt_correlation_workspace_bytes(static_cast<int>(classes), rows)));
+  if (rows) {
+    cuda_check(cudaMemcpy(dx.p, x.data(), x.size() * 4, cudaMemcpyHostToDevice));
+    cuda_check(cudaMemcpy(dc.p, cls.data(), rows * 2, cudaMemcpyHostToDevice));
+    check(hygt_correlation_f64(ds.log2_n(), static_cast<int>(classes), dx.p, dc.p, rows, dsum.p, dcnt.p,
+                               ws.p, ws.n, nullptr));
+    check(hygt_sync_status(nullptr, ws.p, nullptr));
+  }
+  std::vector<double> sum(classes * n * n);
+  std::vector<unsigned long long> cnt(classes);
+  cuda_check(cudaMemcpy(sum.data(), dsum.p, sum.size() * 8, cudaMemcpyDeviceToHost));
+  cuda_check(cudaMemcpy(cnt.data(), dcnt.p, cnt.size() * 8, cudaMemcpyDeviceToHost));
+  std::vector<std::optional<CorrelationMatrix>> out(classes);
+  for (std::size_t c = 0; c < classes; ++c) {
+    if (!cnt[c]) continue;
+    Matrix phi(n);
+    const double inv = 1.0 / static_cast<double>(cnt[c]);  // finalize(), statistics.hpp:81-94
+    for (std::size_t i = 0; i < n; ++i)
+      for (std::size_t j = i; j < n; ++j) {
+        const double v = sum[(c * n + i) * n + j] * inv;
+        phi(i, j) = v;
+        phi(j, i) = v;
+      }
+    out[c].emplace(std::move(phi), static_cast<std::size_t>(cnt[c]));
+  }
+  return out;
 }
 
 // hygt::optimize (optimizer.hpp:311-371) with the reference's types, searched on the GPU

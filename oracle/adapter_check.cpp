@@ -119,6 +119,82 @@ int main() {
     }
     EXPECT(threw, "gpu::optimize must throw ArgumentError on an indefinite covariance");
   }
+  // --- hygt::gpu::klt_forward / KLTPlan vs klt_forward and its transpose (statistics.hpp:222-224)
+  for (int log2n : {2, 4, 6}) {
+    const std::size_t n = std::size_t{1} << log2n;
+    const int classes = 3;
+    std::vector<hygt::KLTResult> klts;
+    for (int c = 0; c < classes; ++c)
+      klts.push_back(hygt::jacobi_eigen(hygt::ar1_covariance_2d(1 << (log2n / 2), 0.6 + 0.1 * c)));
+    std::vector<double> x(n);
+    for (double& v : x) v = static_cast<float>(16 * rng.gaussian());
+    const auto yr = hygt::klt_forward(klts[1], x), yg = hygt::gpu::klt_forward(klts[1], x);
+    double e = 0, sc = 0;
+    for (std::size_t i = 0; i < n; ++i) {
+      e = std::max(e, std::abs(yr[i] - yg[i]));
+      sc = std::max(sc, std::abs(x[i]));
+    }
+    EXPECT(e <= 1e-5 * sc, "gpu::klt_forward log2n=%d err %.3g", log2n, e);
+    const std::size_t rows = 1000;
+    std::vector<float> h(rows * n), hy(rows * n), hb(rows * n);
+    std::vector<std::uint16_t> cls(rows);
+    for (std::size_t r = 0; r < rows; ++r) {
+      cls[r] = static_cast<std::uint16_t>(rng.below(classes));
+      for (std::size_t i = 0; i < n; ++i) h[r * n + i] = static_cast<float>(16 * rng.gaussian());
+    }
+    hygt::gpu::DeviceBuffer<float> dx(rows * n), dy(rows * n), db(rows * n);
+    hygt::gpu::DeviceBuffer<std::uint16_t> dc(rows);
+    cudaMemcpy(dx.p, h.data(), h.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(dc.p, cls.data(), rows * 2, cudaMemcpyHostToDevice);
+    hygt::gpu::KLTPlan plan(klts);
+    plan.bucket(dc.p, rows);
+    plan.forward(dx.p, dy.p, dc.p, rows, nullptr, true);
+    plan.inverse(dy.p, db.p, dc.p, rows, nullptr, true);
+    cudaMemcpy(hy.data(), dy.p, hy.size() * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(hb.data(), db.p, hb.size() * 4, cudaMemcpyDeviceToHost);
+    double ef = 0, eb = 0;
+    for (std::size_t r = 0; r < rows; ++r) {
+      const std::vector<double> xr(h.begin() + r * n, h.begin() + (r + 1) * n);
+      const auto ref = hygt::klt_forward(klts[cls[r]], xr);
+      for (std::size_t i = 0; i < n; ++i) {
+        ef = std::max(ef, std::abs(ref[i] - hy[r * n + i]));
+        eb = std::max(eb, std::abs(xr[i] - hb[r * n + i]));
+      }
+    }
+    EXPECT(ef <= 1e-5 * 80 && eb <= 1e-5 * 80, "gpu::KLTPlan log2n=%d fwd err %.3g roundtrip %.3g", log2n, ef, eb);
+  }
+  // --- hygt::gpu::class_correlations vs the CorrelationAccumulator loop of hygt train
+  //     (hygt_main.cpp:85-87, statistics.hpp:63-99)
+  for (int log2n : {4, 6, 7}) {
+    const std::size_t n = std::size_t{1} << log2n;
+    const int classes = 4;  // class 3 stays empty
+    std::vector<hygt::ResidualBlock> blocks(2500);
+    for (auto& b : blocks) {
+      b.class_id = static_cast<std::uint16_t>(rng.below(3));
+      b.values.resize(n);
+      for (double& v : b.values) v = static_cast<float>(16 * rng.gaussian());
+    }
+    const hygt::ResidualDataset ds(log2n, classes, blocks);
+    const auto got = hygt::gpu::class_correlations(ds);
+    for (int c = 0; c < classes; ++c) {
+      hygt::CorrelationAccumulator acc(n);
+      for (const auto& b : ds.blocks())
+        if (b.class_id == c) acc.add(b.values);
+      if (!acc.count()) {
+        EXPECT(!got[c].has_value(), "class_correlations: empty class %d must be nullopt", c);
+        continue;
+      }
+      EXPECT(got[c].has_value() && got[c]->sample_count() == acc.count(), "class_correlations: count of class %d", c);
+      if (!got[c]) continue;
+      const auto ref = acc.finalize();
+      double e = 0, m = 0;
+      for (std::size_t i = 0; i < n * n; ++i) {
+        e = std::max(e, std::abs(ref.values().data()[i] - got[c]->values().data()[i]));
+        m = std::max(m, std::abs(ref.values().data()[i]));
+      }
+      EXPECT(e <= 1e-12 * m, "class_correlations log2n=%d class %d err %.3g of %.3g", log2n, c, e, m);
+    }
+  }
   std::printf("adapter_check: %s (%d failures)\n", failures ? "FAILED" : "ok", failures);
   return failures ? 1 : 0;
 }
