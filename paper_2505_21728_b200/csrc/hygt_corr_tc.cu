@@ -392,7 +392,11 @@ __global__ void __launch_bounds__(Geo<PR>::THREADS, 1) corr_tc_kernel(const Corr
     int last_f = -1;
     bool fresh_next = true;
     auto do_tile = [&](const Seg& t, uint32_t k, float (&v)[16][2], float (&vn)[16][2]) {
-      if (hq[1]) load_x(idn, vn);                   // tile k + 1's samples, in flight from here
+      // tile k + 1's samples, in flight from here. Unconditional (without a next tile idn = 0 and
+      // row 0 is read and never used): under `if (hq[1])` ptxas loaded into temporaries and moved
+      // them into vn inside the branch, and those moves waited for the loads (12 % of the kernel's
+      // stall samples).
+      load_x(idn, vn);
       idn = load_ids(tq[2], hq[2]);                 // tile k + 2's ids
       if (tid == 0 && role_id == 0 && t.f != last_f) {  // rows of this class in the CTA's range, once
         const uint64_t s1 = umin64(seg_end(t.f), end);
