@@ -99,3 +99,21 @@ def test_gpu_apply_error_codes(cuda, tmp_path):
         rr = _run(REF_APPLY, model, d, out, arithmetic=arith)
         assert rg.returncode == rr.returncode != 0, (model, d, arith, rg.stderr, rr.stderr)
         assert rg.stderr.startswith("error: ")
+
+
+@pytest.mark.parametrize("log2n,classes", [(2, 1), (4, 3), (6, 3)])
+def test_gpu_apply_identity_model_reproduces_input_bytes(cuda, tmp_path, log2n, classes):
+    """test_cli.cpp:185-190: `apply` with HyGTModel::zeros writes the input file byte for byte
+    (every butterfly is the exact identity on the GPU too: cos = 1, sin = 0)."""
+    from paper_2505_21728_b200.formats import write_bundle
+    rng = np.random.default_rng(50 + log2n)
+    tmp = str(tmp_path)
+    data, _, _ = _dataset(tmp, rng, log2n=log2n, classes=classes, count=1500)
+    model = os.path.join(tmp, "ident.hygt")
+    write_bundle(model, log2n, angles=[np.zeros(log2n * (1 << log2n) // 2) for _ in range(classes)])
+    for direction in ("forward", "inverse"):
+        out = os.path.join(tmp, f"ident_{direction}.rblk")
+        r = _run(GPU_APPLY, model, data, out, direction, "float")
+        assert r.returncode == 0, r.stderr
+        with open(out, "rb") as fa, open(data, "rb") as fb:
+            assert fa.read() == fb.read()

@@ -186,3 +186,36 @@ def test_large_n_global_workspace(log2n):
     traj = rep.trajectories[0]
     assert len(traj) == 2 and traj[1] >= traj[0] - 1e-12
     assert traj[1] <= rep.klt_gain_db + 1e-9
+
+
+def test_acceptance_criterion8_fixed_point_fidelity():
+    """acceptance.cpp:279-317 (criterion 8) with every compute step on the GPU path: the N=16 R=2
+    and N=64 R=3 acceptance models come from the device trainer; one byte per angle costs at most
+    0.05 dB of coding gain; and the integer round trip of the quantized N=16 model at the default
+    widths (8-bit codes, TrigTable(8, 10)) over the reference's 200 vectors of Rng(501) stays
+    within the pinned bound of 4 -- run through FixedPlan and bit-exact against the oracle."""
+    import torch
+    from oracle import oracle as O
+    from paper_2505_21728_b200 import FixedPlan, TrigTable, dequantize_model, quantize_model
+    T = _train()
+    cases = {}
+    for bs, log2n, rounds in ((4, 4, 2), (8, 6, 3)):
+        phi = ar1(bs, 0.95)
+        model, _ = T.optimize(phi, log2n, rounds, T.OptimizerConfig(restarts=4, seed=1))
+        fg = O.coding_gain_db(O.propagated_variances(phi, log2n, rounds, model.angles))
+        dq = dequantize_model(quantize_model(model, 8))
+        qg = O.coding_gain_db(O.propagated_variances(phi, log2n, rounds, dq.angles))
+        assert abs(fg - qg) <= 0.05, f"N={1 << log2n}: quantization costs {abs(fg - qg):.4f} dB"
+        cases[log2n] = model
+    q16 = quantize_model(cases[4], 8)
+    rng = O.Rng(501)
+    x = np.array([[rng.below(2049) - 1024 for _ in range(16)] for _ in range(200)], np.int64)
+    plan = FixedPlan([q16], TrigTable(8, 10))
+    xd = torch.from_numpy(x).cuda()
+    y = plan.forward(xd)
+    back = plan.inverse(y).cpu().numpy()
+    st, _, ref = O.apply_batch_fixed(4, 2, 8, 10, q16.codes[None], None, 0, x, None)
+    assert st == 0 and np.array_equal(y.cpu().numpy(), ref)
+    st, _, ref_back = O.apply_batch_fixed(4, 2, 8, 10, q16.codes[None], None, 0, ref, None, inverse=True)
+    assert st == 0 and np.array_equal(back, ref_back)
+    assert np.abs(back - x).max() <= 4, f"integer round trip max {np.abs(back - x).max()} (pinned 4, acceptance.cpp:69)"
