@@ -934,3 +934,54 @@ def test_klt_bucket_once_reuse_both_directions(cuda, oracle_mod, n, classes):
     check_close(y1.cpu().numpy(), oracle_mod.klt_apply(k, xh, ch), xh, f"klt reuse n={n}")
     with pytest.raises(ArgumentError):
         plan.forward(x, cls, reuse_buckets=True)  # no workspace to reuse
+
+
+def test_reference_fixed_point_kats(cuda, oracle_mod):
+    """The reference's own fixed-point cases (tests/test_fixedpoint.cpp:90-184) through the GPU
+    drop-ins forward_fixed / inverse_fixed."""
+    from paper_2505_21728_b200 import (ArgumentError, HyGTModel, QuantizedHyGTModel, TrigTable,
+                                       dequantize_model, forward_fixed, inverse_fixed, quantize_model)
+    table = TrigTable(8, 10)
+    # :90-96 zero codes pass integers through exactly
+    ident = QuantizedHyGTModel(3, 2, 8, np.zeros(24, np.uint16))
+    x = np.array([5, -7, 1000, 0, -1, 12, 999, -1024], np.int64)
+    assert np.array_equal(forward_fixed(ident, table, x), x)
+    assert np.array_equal(inverse_fixed(ident, table, x), x)
+    # :98-105 the quarter-turn butterfly is exact in integer arithmetic
+    qt = QuantizedHyGTModel(1, 1, 8, np.array([64], np.uint16))
+    y = forward_fixed(qt, table, [100, 7])
+    assert list(y) == [7, -100] and list(inverse_fixed(qt, table, y)) == [100, 7]
+    # :107-158 the fixed transform tracks the float transform of the same codes (N=16 R=2 and the
+    # deepest smoke configuration N=64 R=5), and :160-175 the round trip stays bounded. The
+    # reference pins its seeds' maxima (4, 7, 4); here the maxima must equal the oracle's on the
+    # same inputs (bit-exact outputs) and stay under one rounding step per pass.
+    rng = np.random.default_rng(88)
+    for log2n, rounds, trials in ((4, 2, 50), (6, 5, 10)):
+        n = 1 << log2n
+        q = quantize_model(HyGTModel(log2n, rounds, rng.uniform(-np.pi, np.pi, rounds * log2n * n // 2),
+                                     rng.permutation(n).astype(np.uint16)), 8)
+        dq = dequantize_model(q)
+        perms = np.tile(np.arange(n, dtype=np.uint16), (1, rounds, 1))
+        perms[0, rounds - 1] = q.permutation
+        mask = 1 << (rounds - 1)
+        worst_f = worst_rt = 0
+        for _ in range(trials):
+            xi = rng.integers(-1024, 1025, n).astype(np.int64)
+            yi = forward_fixed(q, table, xi)
+            st, _, ref = oracle_mod.apply_batch_fixed(log2n, rounds, 8, 10, q.codes[None], perms, mask, xi[None])
+            assert st == 0 and np.array_equal(yi, ref[0])
+            yf = oracle_mod.apply_batch(log2n, rounds, dq.angles[None], perms, mask, xi[None].astype(np.float32))[0]
+            worst_f = max(worst_f, int(np.abs(yi - np.rint(yf).astype(np.int64)).max()))
+            back = inverse_fixed(q, table, yi)
+            st, _, refb = oracle_mod.apply_batch_fixed(log2n, rounds, 8, 10, q.codes[None], perms, mask, ref, None, inverse=True)
+            assert st == 0 and np.array_equal(back, refb[0])
+            worst_rt = max(worst_rt, int(np.abs(back - xi).max()))
+        assert worst_f <= rounds * log2n and worst_rt <= 2 * rounds * log2n, (worst_f, worst_rt)
+    # :177-184 the input range and the width checks
+    one = QuantizedHyGTModel(1, 1, 8, np.array([0], np.uint16))
+    with pytest.raises(ArgumentError):
+        forward_fixed(one, table, [1 << 21, 0])
+    with pytest.raises(ArgumentError):
+        forward_fixed(one, table, [0])
+    with pytest.raises(ArgumentError):
+        forward_fixed(one, TrigTable(6, 10), [1, 2])
