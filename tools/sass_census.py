@@ -11,7 +11,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KEYS = ["UTCHMMA", "UTCQMMA", "UTCBAR", "LDTM", "STTM", "UTCCP", "UBLKCP", "UBLKPF", "UTMALDG", "UTMASTG",
+KEYS = ["UTCHMMA", "UTCQMMA", "UTCIMMA", "UTCBAR", "LDTM", "STTM", "UTCCP", "UBLKCP", "UBLKPF", "UTMALDG", "UTMASTG",
         "SYNCS.ARRIVE", "SYNCS.PHASECHK", "FFMA2", "FFMA", "FMUL2", "HMMA", "LDS.128", "STS.128", "LDS.64", "STS.64",
         "LDG.E.128", "STG.E.128", "LDGSTS", "SHFL", "IMAD.WIDE", "F2FP", "DFMA", "DADD"]
 
