@@ -23,9 +23,9 @@
 //
 // Operands: digit p of column i is row i of a digit slice, K = the tile's 128 rows, SWIZZLE_128B
 // K-major. A tile is 128 bucketed rows of one class; one CTA per SM (N = 64) or per SM and role.
-//   N = 64 (one 64-column block): A = slices p, p + 1 stacked (M = 128), B = slice q (N = 64);
-//           16 stacks x 4 K steps per tile; rows 0-63 of a stack's result are level p + q,
-//           rows 64-127 level p + q + 1, both in TMEM column block p + q (slot 7 is a zero slice).
+//   N = 64 (one symmetric 64-column block): only the digit pairs p <= q are multiplied, two per
+//           MMA (A = two adjacent digit slices, M = 128; B = one slice, N = 64): 8 MMAs x 4 K
+//           steps per tile, one 64-column TMEM block each (the table at s64_pos below).
 //   N = 128 / 256 (64-column blocks I != J, one "role" per CTA): A = [digit p of block I ;
 //           digit p of block J] (M = 128), B = digit q of block J (the second half of A's stack q,
 //           no extra copy). One MMA gives output blocks (I, J) in TMEM lanes 0-63 and (J, J) in
@@ -58,6 +58,32 @@ constexpr uint32_t SLICE = CN * 128;  // 64 rows x 128 B (K = 128 int8)
 constexpr int MAX_RUN_TILES = 128;    // int32 headroom: |D_L| <= 7 * 128 * 128^2 per tile < 2^31 / 146
 constexpr int HEADROOM = 2;  // bits of a run's exponents above the first tile's column maxima
 
+// N = 64 (one symmetric 64 x 64 block): G_qp = G_pq^T, so only the 16 digit pairs p <= q, p + q <= 6
+// are multiplied, two per MMA: A = two digit slices adjacent in shared memory (M = 128), B = one
+// slice (N = 64). With the slices stored in the order 0 1 3 2 4 6 5 the 16 pairs are covered
+// exactly by 8 MMAs (x 4 K steps; found by exhaustive search over slice orders), each into its own
+// 64-column TMEM block (8 x 64 = all 512 columns), so every (block, lane half) holds one pair:
+//   block : A lower, A upper, B   -> lanes 0-63         | lanes 64-127
+//     0   :    2        4     2   -> (2,2) level 4 diag | (2,4) level 6
+//     1   :    0        1     5   -> (0,5) level 5      | (1,5) level 6
+//     2   :    0        1     0   -> (0,0) level 0 diag | (0,1) level 1
+//     3   :    1        3     1   -> (1,1) level 2 diag | (1,3) level 4
+//     4   :    3        2     0   -> (0,3) level 3      | (0,2) level 2
+//     5   :    4        6     0   -> (0,4) level 4      | (0,6) level 6
+//     6   :    3        2     3   -> (3,3) level 6 diag | (2,3) level 5
+//     7   :    2        4     1   -> (1,2) level 3      | (1,4) level 5
+// The flush forms U = sum over the off-diagonal pairs + half the diagonal pairs (weights
+// 2^(-8 level)) and adds U(i, j) to sum(i, j) and to sum(j, i): U + U^T is the full product.
+// (packed nibbles: constexpr functions are usable in device code, constexpr arrays are not)
+__host__ __device__ constexpr int s64_pos(int p) { return (0x5642310u >> (4 * p)) & 15; }  // digit -> slice position
+__host__ __device__ constexpr int s64_a(int m) { return (0x23431002u >> (4 * m)) & 15; }   // lower digit of A (the upper follows it)
+__host__ __device__ constexpr int s64_b(int m) { return (0x13001052u >> (4 * m)) & 15; }
+static_assert(s64_pos(2) == 3 && s64_pos(3) == 2 && s64_pos(5) == 6 && s64_pos(6) == 5 && s64_a(0) == 2 && s64_a(5) == 4 &&
+              s64_a(7) == 2 && s64_b(1) == 5 && s64_b(6) == 3 && s64_b(7) == 1, "N = 64 pair schedule");
+// level of the pair in (lane half, block) and whether the lower half's pair is a diagonal one (p = q)
+__constant__ int c_s64_level[2][8] = {{4, 5, 0, 2, 3, 4, 6, 3}, {6, 6, 1, 4, 2, 6, 5, 5}};
+__constant__ bool c_s64_diag[8] = {true, false, true, true, false, false, true, false};
+
 // Kernel geometry: PR = false -> N = 64 digit stacks; PR = true -> block-pair roles (N = 128 / 256)
 template <bool PR>
 struct Geo {
@@ -70,15 +96,18 @@ struct Geo {
   static constexpr int THREADS = (PR ? SW : SW + 1) * 32;
   static constexpr int NB = PR ? 2 : 1;                      // 64-column blocks per CTA
   static constexpr uint32_t PSTRIDE = PR ? 2 * SLICE : SLICE;  // bytes between digit p and p + 1
-  static constexpr uint32_t BUF = PR ? NDIG * PSTRIDE : 8 * SLICE;  // N = 64: slot 7 = zero slice
+  static constexpr uint32_t BUF = NDIG * PSTRIDE;
   static constexpr uint32_t CEX_OFF = 2 * BUF;              // [NB][64 cols][8 groups] u8 exponent fields
   static constexpr uint32_t EXP_OFF = CEX_OFF + NB * CN * 8;  // [NB * 64] int run exponents
   static constexpr uint32_t MISC_OFF = EXP_OFF + NB * CN * 4;
   static constexpr uint32_t BAR_OFF = MISC_OFF + 64;
-  static constexpr uint32_t SMEM = BAR_OFF + 64;
+  // N = 64: the raw fp32 rows of two tiles (cp.async, one tile ahead of the split)
+  static constexpr uint32_t XRAW_OFF = (BAR_OFF + 64 + 127) / 128 * 128;
+  static constexpr uint32_t XRAW_TILE = KT * CN * 4;
+  static constexpr uint32_t SMEM = PR ? BAR_OFF + 64 : XRAW_OFF + 2 * XRAW_TILE;
   static constexpr int FCOLS = CN / (SW / 4);               // flush columns per warp
 };
-static_assert(Geo<true>::SMEM <= 232448, "shared memory");
+static_assert(Geo<true>::SMEM <= 232448 && Geo<false>::SMEM <= 232448, "shared memory");
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
@@ -192,12 +221,6 @@ __global__ void __launch_bounds__(Geo<PR>::THREADS, 1) corr_tc_kernel(const Corr
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" :: "r"(su32(tmem_sh)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if constexpr (!PR) {
-    for (uint32_t i = tid; i < 2 * SLICE / 16; i += G::THREADS) {  // the zero slice 7 of both buffers
-      const uint32_t b = i / (SLICE / 16), o = i % (SLICE / 16);
-      reinterpret_cast<uint4*>(sm + b * G::BUF + 7 * SLICE)[o] = make_uint4(0u, 0u, 0u, 0u);
-    }
-  }
   if (tid == 0) {
     for (int i = 0; i < 2; ++i) { mbar_init(&a_full[i], SW); mbar_init(&a_empty[i], G::NISSUE); }
     asm volatile("fence.mbarrier_init.release.cluster;");
@@ -216,25 +239,22 @@ __global__ void __launch_bounds__(Geo<PR>::THREADS, 1) corr_tc_kernel(const Corr
     asm volatile("tcgen05.fence::after_thread_sync;");
     const bool fresh = flag[2 + b] != 0;
     const uint32_t base = su32(sm + b * G::BUF);
-    uint32_t touched = 0;
-    auto mma4 = [&](int blk, uint64_t da, uint64_t db) {
-      const uint32_t d = tmem + (uint32_t)(blk * CN);
+    if (P.dbg & 1) goto committed;  // dbg 1 (timing diagnostic): no MMAs
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const uint64_t da = desc_sw128(base + (uint32_t)s64_pos(s64_a(m)) * SLICE);
+      const uint64_t db = desc_sw128(base + (uint32_t)s64_pos(s64_b(m)) * SLICE);
+      const uint32_t d = tmem + (uint32_t)(m * CN);
 #pragma unroll
       for (int j = 0; j < KT / 32; ++j) {
-        const uint32_t acc = (fresh && !(touched >> blk & 1u) && j == 0) ? 0u : 1u;
+        const uint32_t acc = (fresh && j == 0) ? 0u : 1u;
         asm volatile(
             "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
             "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n"
             :: "r"(d), "l"(da + 2u * j), "l"(db + 2u * j), "r"(IDESC_I8), "r"(acc));
       }
-      touched |= 1u << blk;
-    };
-#pragma unroll 1
-    for (int q = 0; q < NDIG; ++q) {
-      const uint64_t db = desc_sw128(base + (uint32_t)q * SLICE);
-#pragma unroll 1
-      for (int p0 = 0; p0 + q <= NDIG - 1; p0 += 2) mma4(p0 + q, desc_sw128(base + (uint32_t)p0 * SLICE), db);
     }
+  committed:
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                  :: "r"(su32(&a_empty[b])) : "memory");
   };
@@ -326,16 +346,17 @@ __global__ void __launch_bounds__(Geo<PR>::THREADS, 1) corr_tc_kernel(const Corr
 #pragma unroll
           for (int j = 0; j < 8; ++j) s8[j] = 0.0;
 #pragma unroll 1
-          for (int blk = 0; blk < NDIG; ++blk) {
-            const int L = PR ? blk : blk + half;
-            if (L > NDIG - 1) break;
+          for (int blk = 0; blk < (PR ? NDIG : 8); ++blk) {
+            // pairs: block = level; N = 64: the (block, lane half) slot's level, diagonal pairs halved
+            const int L = PR ? blk : (half ? c_s64_level[1][blk] : c_s64_level[0][blk]);
+            const double diag = (!PR && !half && c_s64_diag[blk]) ? 0.5 : 1.0;
             uint32_t v[8];
             const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(blk * CN + cc * G::FCOLS + j0);
             asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
                          : "r"(ta));
             asm volatile("tcgen05.wait::ld.sync.aligned;");
-            const double wl = ldexp(1.0, -8 * L);
+            const double wl = ldexp(diag, -8 * L);
 #pragma unroll
             for (int j = 0; j < 8; ++j) s8[j] = fma((double)(int)v[j], wl, s8[j]);
           }
@@ -344,7 +365,8 @@ __global__ void __launch_bounds__(Geo<PR>::THREADS, 1) corr_tc_kernel(const Corr
             if (s8[j] == 0.0) continue;
             const double v = ldexp(s8[j], ei + ej[j0 + j] - 12);
             atomicAdd(out + j0 + j, v);
-            if (PR && !half) atomicAdd(P.sum + ((size_t)run_class * n + jb * CN + cc * G::FCOLS + j0 + j) * n + gi, v);
+            // mirror: pairs, the off-diagonal block's transpose; N = 64, U^T
+            if (!PR || !half) atomicAdd(P.sum + ((size_t)run_class * n + jb * CN + cc * G::FCOLS + j0 + j) * n + gi, v);
           }
         }
       }
@@ -385,9 +407,27 @@ __global__ void __launch_bounds__(Geo<PR>::THREADS, 1) corr_tc_kernel(const Corr
         }
       }
     };
+    // N = 64: the rows go through shared memory instead. Samples held in registers a tile ahead
+    // were moved by ptxas right behind their loads (loop-carried register homes), so every tile
+    // waited out the DRAM latency there (24 % of the stall samples). The warp copies its 16 rows
+    // of tile k + 1 with cp.async (lanes 0-15 one row, lanes 16-31 the next, 16 B each) while it
+    // converts tile k, and reads tile k back with conflict-free LDS (lane = column).
+    auto stage_rows = [&](uint32_t ids, uint32_t b) {
+      const uint32_t dst0 = su32(sm + G::XRAW_OFF) + b * G::XRAW_TILE + (uint32_t)(g * 16 + (lane >> 4)) * (CN * 4u) +
+                            (uint32_t)(lane & 15) * 16u;
+      const char* src0 = reinterpret_cast<const char*>(P.x) + (lane & 15) * 16;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t row = __shfl_sync(0xffffffffu, ids, 2 * i + (lane >> 4));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
+                     :: "r"(dst0 + (uint32_t)i * (2u * CN * 4u)), "l"(src0 + (uint64_t)row * (CN * 4u)) : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
     float va[16][2], vb[16][2];
     uint32_t ida = load_ids(tq[0], hq[0]);
-    load_x(ida, va);
+    if constexpr (PR) load_x(ida, va);
+    else stage_rows(ida, 0u);
     uint32_t idn = load_ids(tq[1], hq[1]);  // ids of the next tile
     int last_f = -1;
     bool fresh_next = true;
@@ -396,13 +436,28 @@ __global__ void __launch_bounds__(Geo<PR>::THREADS, 1) corr_tc_kernel(const Corr
       // row 0 is read and never used): under `if (hq[1])` ptxas loaded into temporaries and moved
       // them into vn inside the branch, and those moves waited for the loads (12 % of the kernel's
       // stall samples).
-      load_x(idn, vn);
+      if constexpr (PR) {
+        load_x(idn, vn);
+      } else {
+        __syncwarp();  // the warp's reads of tile k - 1 (same buffer) are done
+        stage_rows(idn, (k + 1u) & 1u);
+      }
       idn = load_ids(tq[2], hq[2]);                 // tile k + 2's ids
       if (tid == 0 && role_id == 0 && t.f != last_f) {  // rows of this class in the CTA's range, once
         const uint64_t s1 = umin64(seg_end(t.f), end);
         atomicAdd(P.cnt + t.f, (unsigned long long)(s1 - t.p0));
       }
       last_f = t.f;
+      if constexpr (!PR) {  // tile k's rows have landed (all groups but the one just committed)
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncwarp();
+        const float* xr = reinterpret_cast<const float*>(sm + G::XRAW_OFF + (k & 1u) * G::XRAW_TILE) + g * 16 * CN + lane;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          v[r][0] = xr[r * CN];
+          v[r][1] = xr[r * CN + 32];
+        }
+      }
       // rows past the tile's end (warp-uniform): zero
       const int nvalid = (int)t.rows - g * 16;
       if (nvalid < 16) {
@@ -456,7 +511,7 @@ __global__ void __launch_bounds__(Geo<PR>::THREADS, 1) corr_tc_kernel(const Corr
       fresh_next = false;
       unsigned char* buf = sm + b * G::BUF + (PR ? h * SLICE : 0);
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
+      for (int hh = 0; hh < ((P.dbg & 2) ? 0 : 2); ++hh) {  // dbg 2 (timing diagnostic): no digits
         const int col = lane + 32 * hh;
         // 2^(54 - E) as two exact factors (E in [-125, 131])
         const int a = 54 - erun[h * CN + col], a1 = a >> 1;
@@ -481,7 +536,7 @@ __global__ void __launch_bounds__(Geo<PR>::THREADS, 1) corr_tc_kernel(const Corr
               const uint32_t a2 = bsel < 4 ? zl[4 * gg + 2] : zh[4 * gg + 2], a3 = bsel < 4 ? zl[4 * gg + 3] : zh[4 * gg + 3];
               q[gg] = __byte_perm(__byte_perm(a0, a1w, s01), __byte_perm(a2, a3, s01), 0x5410);
             }
-            unsigned char* dst = buf + (uint32_t)p * G::PSTRIDE + swz(col, g) + (uint32_t)r0;
+            unsigned char* dst = buf + (uint32_t)(PR ? p : s64_pos(p)) * G::PSTRIDE + swz(col, g) + (uint32_t)r0;
             if constexpr (RC == 16) *reinterpret_cast<uint4*>(dst) = make_uint4(q[0], q[1], q[2], q[3]);
             else *reinterpret_cast<uint2*>(dst) = make_uint2(q[0], q[1]);
           }
@@ -509,6 +564,7 @@ __global__ void __launch_bounds__(Geo<PR>::THREADS, 1) corr_tc_kernel(const Corr
       advance();
     }
     if (run_class >= 0) flush();
+    if constexpr (!PR) asm volatile("cp.async.wait_all;" ::: "memory");  // the look-ahead copy past the last tile
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
