@@ -1,5 +1,7 @@
+"""Staged N = 16 kernel with and without the consumers' arithmetic (debug build, hook
+hygt_debug_stage_trace + knob HYGT_STAGE_DEBUG_SKIP): the TMA copy pipeline's own rate (development tool)."""
 import ctypes, sys, torch
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
 from paper_2505_21728_b200 import _lib
 from paper_2505_21728_b200.synth import make_workload
 from paper_2505_21728_b200.plan import HyGTPlan
