@@ -191,9 +191,7 @@ extern "C" int hygt_correlation_f64(int log2_n, int classes, const float* d_x, c
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // (the N = 64 kernel copies rows with 16-byte cp.async: an unaligned d_x takes the SIMT kernel)
-  if (hygt_gpu::corr_tc_supported(log2_n) && hygt_gpu::knob("HYGT_CORR_TC", 1) != 0 &&
-      (reinterpret_cast<uintptr_t>(d_x) & 15) == 0) {
+  if (hygt_gpu::corr_tc_supported(log2_n) && hygt_gpu::knob("HYGT_CORR_TC", 1) != 0) {  // (d_x is 16-byte aligned, checked above)
     // N >= 64: exact integer-digit products on the tensor cores (hygt_corr_tc.cu)
     hygt_gpu::CorrTcParams Q{};
     Q.x = d_x;

@@ -697,7 +697,7 @@ def test_seg2_path_edges(cuda, oracle_mod, standard, cls_env, jit_env, path, R, 
     assert torch.equal(y[123], x[123])
 
 
-@pytest.mark.parametrize("log2n,classes,count", [(2, 1, 1000), (4, 3, 20000), (6, 5, 30001), (8, 2, 3000)])
+@pytest.mark.parametrize("log2n,classes,count", [(2, 1, 1000), (4, 3, 20000), (6, 5, 30001), (6, 1, 7001), (7, 1, 3000), (8, 2, 3000)])
 def test_correlation_vs_oracle(cuda, oracle_mod, log2n, classes, count):
     """Per-class r r^T sums and counts against the oracle restatement of
     CorrelationAccumulator (pinned bit for bit to the reference in test_oracle.py). Products of
@@ -723,6 +723,13 @@ def test_correlation_vs_oracle(cuda, oracle_mod, log2n, classes, count):
     for c in range(classes):
         ref_phi = O.correlation_finalize(log2n, ref_s[c], ref_k[c])
         assert np.abs(phi[c] - ref_phi).max() <= 1e-12 * np.abs(ref_phi).max()
+    # rows that start 4 bytes off a 16-byte boundary are refused (the kernels read 16-byte vectors)
+    from paper_2505_21728_b200 import ArgumentError
+    flat = torch.empty(count * n + 1, dtype=torch.float32, device=cuda)
+    xo = flat[1:].view(count, n)
+    xo.copy_(xd)
+    with pytest.raises(ArgumentError):
+        correlation(xo, cd, classes)
 
 
 def test_correlation_invalid_ids(cuda):
