@@ -13,7 +13,8 @@
 //     KLTResult per class) and hygt::gpu::klt_forward (one vector, same signature);
 //   * the per-class CorrelationAccumulator loop of `hygt train` (hygt_main.cpp:85-87,
 //     statistics.hpp:63-99) -> hygt::gpu::class_correlations(dataset);
-//   * hygt::optimize (optimizer.hpp:311-371) -> hygt::gpu::optimize.
+//   * hygt::optimize (optimizer.hpp:311-371) -> hygt::gpu::optimize;
+//   * the training loop of `hygt train` (run_train, hygt_main.cpp:74-120) -> hygt::gpu::train(dataset, rounds, ...).
 // Non-zero C-ABI statuses are rethrown as the reference's exception classes (errors.hpp:23-45).
 #pragma once
 
@@ -391,6 +392,41 @@ inline std::pair<HyGTModel, TrainingReport> optimize(const CorrelationMatrix& ph
   rep.klt_gain_db = klt;
   rep.gain_ratio = klt > 1e-15 ? gains[best] / klt : 1.0;
   return {HyGTModel(log2_n, rounds, std::move(angles)), std::move(rep)};
+}
+
+// The training loop of `hygt train` (run_train, tools/hygt_main.cpp:74-120) on an in-memory
+// dataset: per-class correlation on the GPU (class_correlations), the identity model for classes
+// with fewer than N samples (:89-96), hygt::gpu::optimize with seed derive_seed(seed, c) (:96),
+// variance_permutation (:100), and the optional angle quantisation (:110-115). `reports`, if
+// given, receives one TrainingReport per class (default-constructed for identity classes).
+inline ModelBundle train(const ResidualDataset& ds, int rounds, int restarts = 4, std::uint64_t seed = 0,
+                         int angle_bits = 0, std::vector<TrainingReport>* reports = nullptr) {
+  if (rounds < 1 || rounds > 255) throw ArgumentError("train: rounds out of range [1, 255]");
+  if (angle_bits != 0 && (angle_bits < 1 || angle_bits > 8))
+    throw ArgumentError("train: angle-bits must be 0 (float) or in [1, 8]");
+  const std::size_t n = ds.dimension();
+  const auto phis = class_correlations(ds);
+  std::vector<HyGTModel> models;
+  if (reports) reports->assign(ds.class_count(), TrainingReport{});
+  for (std::uint16_t c = 0; c < ds.class_count(); ++c) {
+    if (!phis[c] || phis[c]->sample_count() < n) {
+      models.push_back(HyGTModel::zeros(ds.log2_n(), rounds));
+      continue;
+    }
+    OptimizerConfig config;
+    config.restarts = restarts;
+    config.seed = derive_seed(seed, c);
+    auto [model, report] = gpu::optimize(*phis[c], ds.log2_n(), rounds, config);
+    models.push_back(variance_permutation(model, *phis[c]));
+    if (reports) (*reports)[c] = std::move(report);
+  }
+  if (angle_bits > 0) {
+    std::vector<QuantizedHyGTModel> quantized;
+    quantized.reserve(models.size());
+    for (const auto& m : models) quantized.push_back(quantize_model(m, angle_bits));
+    return ModelBundle(std::move(quantized));
+  }
+  return ModelBundle(std::move(models));
 }
 
 }  // namespace hygt::gpu

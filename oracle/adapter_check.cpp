@@ -195,6 +195,55 @@ int main() {
       EXPECT(e <= 1e-12 * m, "class_correlations log2n=%d class %d err %.3g of %.3g", log2n, c, e, m);
     }
   }
+  // --- hygt::gpu::train vs the loop of run_train (hygt_main.cpp:74-120): same per-class gains
+  {
+    const int log2n = 4, rounds = 2, classes = 3;  // class 2 gets too few samples -> identity
+    const std::size_t n = 16;
+    std::vector<hygt::ResidualBlock> blocks;
+    const auto cov = hygt::ar1_covariance_2d(4, 0.9);
+    hygt::Rng srng(77);
+    for (int c = 0; c < classes; ++c) {
+      const std::size_t m = c == 2 ? 5 : 600;
+      for (std::size_t k = 0; k < m; ++k) {
+        hygt::ResidualBlock b;
+        b.class_id = static_cast<std::uint16_t>(c);
+        b.values.resize(n);
+        double prev = 0.0;
+        for (std::size_t i = 0; i < n; ++i) {  // an AR(1) line with a class-dependent rho
+          const double rho = 0.5 + 0.2 * c;
+          prev = i ? rho * prev + std::sqrt(1 - rho * rho) * srng.gaussian() : srng.gaussian();
+          b.values[i] = static_cast<float>(16 * prev);
+        }
+        blocks.push_back(std::move(b));
+      }
+    }
+    const hygt::ResidualDataset ds(log2n, classes, blocks);
+    std::vector<hygt::TrainingReport> reps;
+    const hygt::ModelBundle bundle = hygt::gpu::train(ds, rounds, 2, 9, 0, &reps);
+    EXPECT(bundle.class_count() == static_cast<std::size_t>(classes), "gpu::train class count");
+    for (std::uint16_t c = 0; c < classes; ++c) {
+      hygt::CorrelationAccumulator acc(n);
+      for (const auto& b : ds.blocks())
+        if (b.class_id == c) acc.add(b.values);
+      const hygt::HyGTModel got = bundle.dequantized(c);
+      if (acc.count() < n) {
+        bool zero = !got.permutation();
+        for (double a : got.angles()) zero = zero && a == 0.0;
+        EXPECT(zero, "gpu::train: class %d must keep the identity model", c);
+        continue;
+      }
+      const auto phi = acc.finalize();
+      hygt::OptimizerConfig cfg;
+      cfg.restarts = 2;
+      cfg.seed = hygt::derive_seed(9, c);
+      auto [mr, rr] = hygt::optimize(phi, log2n, rounds, cfg);
+      EXPECT(std::abs(rr.restart_gains_db[rr.best_restart] - reps[c].restart_gains_db[reps[c].best_restart]) < 1e-5,
+             "gpu::train class %d gain %.9f vs %.9f", c, reps[c].restart_gains_db[reps[c].best_restart],
+             rr.restart_gains_db[rr.best_restart]);
+      EXPECT(got.permutation().has_value(), "gpu::train: class %d has no variance permutation", c);
+    }
+    (void)cov;
+  }
   std::printf("adapter_check: %s (%d failures)\n", failures ? "FAILED" : "ok", failures);
   return failures ? 1 : 0;
 }
