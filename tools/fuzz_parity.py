@@ -24,16 +24,18 @@ rng = np.random.default_rng(a.seed)
 t0 = time.time()
 n_float = n_fixed = n_klt = n_corr = 0
 worst = 0.0
+worst_what = ""
 
 
 def close(y, ref, x, what):
-    global worst
+    global worst, worst_what
     err = np.asarray(y, np.float64) - ref
     if err.size == 0:
         return
     rel = np.linalg.norm(err) / max(np.linalg.norm(ref), 1e-300)
     mab = np.abs(err).max() if err.size else 0.0
-    worst = max(worst, rel)
+    if rel > worst:
+        worst, worst_what = rel, what
     assert rel <= 1e-6 and mab <= 1e-5 * max(np.abs(x).max(), 1e-30), f"{what}: rel {rel:.3e} max-abs {mab:.3e}"
 
 
@@ -121,4 +123,4 @@ while time.time() - t0 < a.seconds:
         print("FAIL", what)
         raise
 print(f"fuzz ok: {n_float} float, {n_fixed} fixed, {n_klt} klt, {n_corr} correlation cases in {time.time() - t0:.0f} s; "
-      f"worst float rel L2 {worst:.2e}")
+      f"worst float rel L2 {worst:.2e} ({worst_what})")
