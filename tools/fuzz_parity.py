@@ -19,6 +19,7 @@ from paper_2505_21728_b200.plan import HYGT_PLAN_FORCE_STANDARD  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--seconds", type=float, default=240)
 ap.add_argument("--seed", type=int, default=1)
+ap.add_argument("--big", action="store_true", help="also batches of 3e5 and 2^20 rows (N <= 64): multi-tile steady state")
 a = ap.parse_args()
 rng = np.random.default_rng(a.seed)
 t0 = time.time()
@@ -45,6 +46,8 @@ while time.time() - t0 < a.seconds:
     rounds = int(rng.integers(1, 5))
     classes = int(rng.choice([1, 1, 2, 3, 5, 8, 35, 40, 70]))
     rows = int(rng.choice([0, 1, 7, 31, 33, 127, 129, 1000, 4097, 20000, 66000]))
+    if a.big and n <= 64 and rng.random() < 0.5:
+        rows = int(rng.choice([300001, 1 << 20]))
     if n >= 128:
         rows = min(rows, 20000)
     mask = int(rng.integers(0, 1 << rounds)) if rng.random() < 0.7 else 0
