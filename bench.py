@@ -551,7 +551,7 @@ def impl_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        srows = cpu_sample_rows(w.n, threads, seconds=5.0)
+        srows = min(rows, cpu_sample_rows(w.n, threads, seconds=5.0))  # never more rows than the batch holds
         t = run_reference_sample(w, srows, threads, (x[:srows].cpu().numpy(), cls[:srows].cpu().numpy()))
         cpu = {"value": srows / t, "unit": "vectors/s", "cores": threads, "kind": "reference",
                "cpu_model": cpu_model(),
